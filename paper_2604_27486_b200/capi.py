@@ -1,0 +1,196 @@
+"""ctypes binding of the C ABI in ``include/culifter.h``.
+
+``Engine()`` loads the product library (``csrc/libculifter.so``: sm_100a CUDA
+kernels).  There is no CPU fallback: if the library is missing or no CUDA
+device answers, construction raises.  Tests and ``bench.py``'s CPU-baseline
+leg may point ``Engine`` at the oracle library explicitly (``Engine(path)``);
+nothing in the package does.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from . import layout as L
+from .patterns import BLOB, PATTERN, SLOT, TEMPLATE, compile_patterns
+from .soa import Corpus
+
+PKG = Path(__file__).resolve().parent
+PRODUCT_LIB = PKG / "csrc" / "libculifter.so"
+
+SR_ENTRY = np.dtype([("arch", "<u4"), ("offset", "<u4"), ("sreg", "<u4")])
+STATS = np.dtype([("matches", "<u8", (16,)), ("selected", "<u8", (16,)),
+                  ("rewrites", "<u8", (16,)), ("refused", "<u8", (16,)),
+                  ("n_inst_in", "<u8"), ("n_inst_out", "<u8"), ("n_events", "<u8"),
+                  ("reserved", "<u8")])
+
+
+class CorpusStruct(C.Structure):
+    _fields_ = [("n_funcs", C.c_uint32), ("n_blocks", C.c_uint32),
+                ("n_modsets", C.c_uint32), ("reserved", C.c_uint32)] + \
+        [(name, C.c_void_p) for name in (
+            "func", "func_blk_off", "ext_off", "mem_off", "imm_off", "val_off", "blk",
+            "blk_off", "hdr", "tag", "pay", "ext_tag", "ext_pay", "mem", "imm",
+            "val_alive", "val_def_iid", "val_origin", "modsets")]
+
+
+class RunOpts(C.Structure):
+    _fields_ = [("passes", C.c_uint32), ("max_rounds", C.c_uint32),
+                ("emit_matches", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+_ABI_SIZES = (L.HDR.itemsize, L.IMM.itemsize, L.MEMREF.itemsize, L.BLK.itemsize,
+              L.FUNC.itemsize, L.MODSET.itemsize, SLOT.itemsize, TEMPLATE.itemsize,
+              PATTERN.itemsize, BLOB.itemsize, L.EVENT.itemsize, C.sizeof(CorpusStruct),
+              C.sizeof(RunOpts), STATS.itemsize, SR_ENTRY.itemsize)
+
+EXPORTS = ("cl_last_error", "cl_backend", "cl_abi_sizeof", "cl_create", "cl_destroy",
+           "cl_set_patterns", "cl_set_threads", "cl_upload", "cl_run_postssa", "cl_run_raw",
+           "cl_out_sizes", "cl_download", "cl_get_stats", "cl_last_run_ms",
+           "cl_device_counts_ptr", "cl_stream")
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+def load_library(path=None):
+    path = Path(path) if path is not None else PRODUCT_LIB
+    if not path.exists():
+        raise EngineError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            f"g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
+    lib = C.CDLL(str(path))
+    for name in EXPORTS:
+        if not hasattr(lib, name):
+            raise EngineError(f"{path}: symbol {name} is not exported")
+    lib.cl_last_error.restype = C.c_char_p
+    lib.cl_backend.restype = C.c_char_p
+    lib.cl_abi_sizeof.restype = C.c_long
+    lib.cl_device_counts_ptr.restype = C.c_void_p
+    lib.cl_stream.restype = C.c_void_p
+    lib.cl_device_counts_ptr.argtypes = lib.cl_stream.argtypes = [C.c_void_p]
+    lib.cl_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    lib.cl_destroy.argtypes = [C.c_void_p]
+    lib.cl_destroy.restype = None
+    lib.cl_set_patterns.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    lib.cl_set_threads.argtypes = [C.c_void_p, C.c_int]
+    lib.cl_upload.argtypes = [C.c_void_p, C.POINTER(CorpusStruct)]
+    lib.cl_run_postssa.argtypes = [C.c_void_p, C.POINTER(RunOpts)]
+    lib.cl_run_raw.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32]
+    lib.cl_out_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+    lib.cl_download.argtypes = [C.c_void_p, C.POINTER(CorpusStruct), C.c_void_p]
+    lib.cl_get_stats.argtypes = [C.c_void_p, C.c_void_p]
+    lib.cl_last_run_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+    for i, want in enumerate(_ABI_SIZES):
+        got = lib.cl_abi_sizeof(i)
+        if got != want:
+            raise EngineError(f"{path}: ABI struct {i} is {got} bytes, binding expects {want}")
+    return lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _struct_of(c: Corpus, modsets: np.ndarray) -> CorpusStruct:
+    st = CorpusStruct()
+    st.n_funcs, st.n_blocks, st.n_modsets = c.n_funcs, c.n_blocks, len(modsets)
+    for name in Corpus.ARRAYS:
+        a = getattr(c, name)
+        if not a.flags["C_CONTIGUOUS"]:
+            raise EngineError(f"corpus array {name} is not contiguous")
+        setattr(st, name, _ptr(a))
+    st.modsets = _ptr(modsets)
+    return st
+
+
+class Engine:
+    """One ``cl_ctx``: a device (or, for the oracle library, host threads)."""
+
+    def __init__(self, lib_path=None, device: int = 0, patterns=None):
+        self.lib = load_library(lib_path)
+        self.backend = self.lib.cl_backend().decode()
+        self._ctx = C.c_void_p()
+        self._check(self.lib.cl_create(device, C.byref(self._ctx)))
+        self._blob = None
+        self._n_blocks = 0
+        self._keep = None
+        self.set_patterns(*(patterns or (None, None)))
+
+    def _check(self, rc):
+        if rc != 0:
+            raise EngineError(f"{self.backend}: {self.lib.cl_last_error().decode()}")
+
+    def close(self):
+        if self._ctx:
+            self.lib.cl_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+    def set_patterns(self, aggregation=None, xmad=None, budget=50_000):
+        self._blob = compile_patterns(aggregation, xmad, budget)
+        self._check(self.lib.cl_set_patterns(self._ctx, _ptr(self._blob), self._blob.nbytes))
+
+    def set_threads(self, n: int):
+        self._check(self.lib.cl_set_threads(self._ctx, n))
+
+    def upload(self, corpus: Corpus):
+        modsets = np.ascontiguousarray(L.TABLES.modset_info())
+        st = _struct_of(corpus, modsets)
+        self._keep = (corpus, modsets)
+        self._check(self.lib.cl_upload(self._ctx, C.byref(st)))
+        self._src = corpus
+
+    def run_postssa(self, passes=L.PASS_ALL, max_rounds=4, emit_matches=False):
+        opts = RunOpts(passes, max_rounds, int(emit_matches), 0)
+        self._check(self.lib.cl_run_postssa(self._ctx, C.byref(opts)))
+
+    def run_raw(self, passes, sr_map=()):
+        m = np.array([tuple(e) for e in sr_map], SR_ENTRY) if len(sr_map) else np.zeros(0, SR_ENTRY)
+        self._check(self.lib.cl_run_raw(self._ctx, passes, _ptr(m), len(m)))
+
+    def download(self) -> Corpus:
+        sizes = (C.c_uint64 * 6)()
+        self._check(self.lib.cl_out_sizes(self._ctx, sizes))
+        n_inst, n_ext, n_mem, n_imm, n_val, n_ev = (int(x) for x in sizes)
+        src = self._src
+        F, B = src.n_funcs, src.n_blocks
+        out = Corpus(
+            func=np.zeros(F, L.FUNC), func_blk_off=np.zeros(F + 1, np.uint32),
+            ext_off=np.zeros(F + 1, np.uint32), mem_off=np.zeros(F + 1, np.uint32),
+            imm_off=np.zeros(F + 1, np.uint32), val_off=np.zeros(F + 1, np.uint32),
+            blk=np.zeros(B, L.BLK), blk_off=np.zeros(B + 1, np.uint32),
+            hdr=np.zeros(n_inst, L.HDR), tag=np.zeros((n_inst, 8), np.uint16),
+            pay=np.zeros((n_inst, 8), np.uint32), ext_tag=np.zeros(n_ext, np.uint16),
+            ext_pay=np.zeros(n_ext, np.uint32), mem=np.zeros(n_mem, L.MEMREF),
+            imm=np.zeros(n_imm, L.IMM), val_alive=np.zeros(n_val, np.uint8),
+            val_def_iid=np.zeros(n_val, np.int32), val_origin=np.zeros(n_val, np.uint32),
+            events=np.zeros(n_ev, L.EVENT), functions=src.functions, raw=src.raw)
+        st = _struct_of(out, self._keep[1])
+        self._check(self.lib.cl_download(self._ctx, C.byref(st), _ptr(out.events)))
+        return out
+
+    def stats(self):
+        s = np.zeros(1, STATS)
+        self._check(self.lib.cl_get_stats(self._ctx, _ptr(s)))
+        return s[0]
+
+    def last_run_ms(self) -> float:
+        ms = C.c_float()
+        self._check(self.lib.cl_last_run_ms(self._ctx, C.byref(ms)))
+        return float(ms.value)
+
+    def device_counts_ptr(self):
+        return self.lib.cl_device_counts_ptr(self._ctx)
+
+    def stream(self):
+        return self.lib.cl_stream(self._ctx)
