@@ -264,8 +264,9 @@ enum cl_event_kind {
                             b = add iid, idx = append order inside the function      */
     CL_EV_MATCH = 3      /* Match record (:100-106): a = pattern | selected << 16,
                             b, c, d = block positions of the matched instructions
-                            (0xFFFFFFFF when the pattern is shorter); idx = index in
-                            match_patterns' list (:187-203 product order), or
+                            (0xFFFFFFFF when the pattern is shorter); idx = pattern
+                            << 20 | rank of the tuple in itertools.product order
+                            (:195), which sorts like match_patterns' list, or
                             0x80000000 | rank in select_matches' list (:241)         */
 };
 /* seq = phase << 28 | index of the block inside its function; phase 0 = xmad

@@ -1,0 +1,1553 @@
+/* core.cuh -- the device algorithm of the normalisation + pattern-aggregation
+ * path: one cooperative thread *group* (a warp for small functions, a whole
+ * CTA for large ones) keeps one function resident in a gap buffer (shared
+ * memory when it fits, L2-resident scratch otherwise) and takes it through
+ *
+ *   seed scan -> tuple unification -> overlap selection -> rewrite planning
+ *   (count / exclusive scan / emit) -> pack simplification -> dead-pseudo
+ *   elimination -> reciprocal normalisation -> CUDA-object tagging
+ *
+ * so that HBM sees one read of the input stream and one write of the result.
+ * Semantics are those of the reference (cited per function, paths relative to
+ * /root/reference/pkg/src/sasslift/); results are bit-exact with oracle/.
+ *
+ * The code is written against a small `Grp` interface (rank/size/sync/scan)
+ * and plain generic pointers, so the same source also compiles as ordinary
+ * C++ with a one-lane group (CL_SIM) -- used only by tests/sim to debug the
+ * logic on machines without a GPU; the package never loads that build.
+ */
+#pragma once
+#include "../../include/culifter.h"
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__CUDACC__) && !defined(CL_SIM)
+#define CL_DEV 1
+#define CLD __device__ __forceinline__
+#define CLF __device__ __noinline__
+#define CLHD __host__ __device__ inline
+#define CLM static __device__ __forceinline__
+#else
+#define CL_DEV 0
+#define CLD static inline
+#define CLF static
+#define CLHD static inline
+#define CLM static inline
+struct alignas(16) uint4 { uint32_t x, y, z, w; };
+#endif
+
+namespace clk {
+
+static constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+static constexpr unsigned long long NONE64 = ~0ull;
+
+/* ----------------------------------------------------------------- atomics */
+CLD uint32_t a_add(uint32_t *p, uint32_t v) {
+#if CL_DEV
+    return atomicAdd(p, v);
+#else
+    uint32_t o = *p; *p += v; return o;
+#endif
+}
+CLD void a_cas0(uint32_t *p, uint32_t v) {      /* set if still zero */
+#if CL_DEV
+    atomicCAS(p, 0u, v);
+#else
+    if (*p == 0) *p = v;
+#endif
+}
+CLD uint32_t a_sub(uint32_t *p, uint32_t v) {
+#if CL_DEV
+    return atomicSub(p, v);
+#else
+    uint32_t o = *p; *p -= v; return o;
+#endif
+}
+CLD void a_min64(unsigned long long *p, unsigned long long v) {
+#if CL_DEV
+    atomicMin(p, v);
+#else
+    if (v < *p) *p = v;
+#endif
+}
+CLD unsigned long long a_add64(unsigned long long *p, unsigned long long v) {
+#if CL_DEV
+    return atomicAdd(p, v);
+#else
+    unsigned long long o = *p; *p += v; return o;
+#endif
+}
+
+/* ------------------------------------------------------------------ groups */
+/* NW = warps per group.  NW == 1: the group is a warp (several independent
+ * groups per CTA).  NW > 1: the group is the whole CTA.  NW == 0: host.     */
+template <int NW> struct Grp {
+    uint32_t rank, size;
+    uint32_t *red;             /* NW > 1: shared scratch, NW + 2 words         */
+#if CL_DEV
+    CLD void sync() const { if (NW == 1) __syncwarp(); else __syncthreads(); }
+    CLD uint32_t exscan(uint32_t x, uint32_t &total) const {
+        const uint32_t lane = rank & 31u;
+        uint32_t v = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, d);
+            if (lane >= (uint32_t)d) v += t;
+        }
+        if (NW == 1) { total = __shfl_sync(0xFFFFFFFFu, v, 31); return v - x; }
+        const uint32_t w = rank >> 5;
+        if (lane == 31) red[w] = v;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+        for (int i = 0; i < NW; i++) { uint32_t t = red[i]; if ((uint32_t)i < w) pre += t; tot += t; }
+        __syncthreads();
+        total = tot;
+        return pre + v - x;
+    }
+    /* ballot + popc compaction offsets */
+    CLD uint32_t flag_exscan(bool f, uint32_t &total) const {
+        const uint32_t lane = rank & 31u;
+        const uint32_t b = __ballot_sync(0xFFFFFFFFu, f);
+        const uint32_t mine = __popc(b & ((1u << lane) - 1u));
+        if (NW == 1) { total = __popc(b); return mine; }
+        const uint32_t w = rank >> 5;
+        if (lane == 0) red[w] = __popc(b);
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+        for (int i = 0; i < NW; i++) { uint32_t t = red[i]; if ((uint32_t)i < w) pre += t; tot += t; }
+        __syncthreads();
+        total = tot;
+        return pre + mine;
+    }
+    CLD bool any(bool f) const {
+        if (NW == 1) return __any_sync(0xFFFFFFFFu, f);
+        return __syncthreads_or(f) != 0;
+    }
+    CLD uint32_t sum(uint32_t x) const { uint32_t t; exscan(x, t); return t; }
+    CLD uint32_t bcast0(uint32_t x) const {
+        if (NW == 1) return __shfl_sync(0xFFFFFFFFu, x, 0);
+        if (rank == 0) red[NW] = x;
+        __syncthreads();
+        uint32_t r = red[NW];
+        __syncthreads();
+        return r;
+    }
+#else
+    void sync() const {}
+    uint32_t exscan(uint32_t x, uint32_t &total) const { total = x; return 0; }
+    uint32_t flag_exscan(bool f, uint32_t &total) const { total = f; return 0; }
+    bool any(bool f) const { return f; }
+    uint32_t sum(uint32_t x) const { return x; }
+    uint32_t bcast0(uint32_t x) const { return x; }
+#endif
+};
+
+/* uniform strided loop: every lane runs every iteration (collectives inside
+ * are legal); `i < n` guards the work.                                       */
+#define GFOR(g, i, n) for (uint32_t _b##i = 0, i = (g).rank; _b##i < (n); _b##i += (g).size, i += (g).size)
+
+/* ------------------------------------------------------------ data model */
+struct opnd { uint16_t tag; uint32_t pay; };
+struct Rec { cl_hdr h; uint16_t tag[8]; uint32_t pay[8]; };
+struct Planes { cl_hdr *hdr; uint16_t *tag; uint32_t *pay; };
+
+struct okey { uint32_t cls; unsigned long long v; };
+enum { KC_NONE = 0, KC_V, KC_IMM, KC_RZ, KC_PT, KC_P, KC_CM, KC_R, KC_UR, KC_SR, KC_OTHER, KC_MOD };
+static constexpr int NBIND = CL_MAX_VARS + CL_MAX_GROUPS;
+struct Bind { okey var[NBIND]; };
+
+struct MatchRec {              /* Match (patterns.py:100-106) on block positions */
+    uint8_t pat, n, state, pad;
+    uint32_t pos[3];
+    uint32_t seq;              /* pattern << 20 | tuple rank: list order          */
+};
+enum { MS_UNDECIDED = 0, MS_SELECTED = 1, MS_REJECTED = 2 };
+
+struct SelRec {                /* selected match, function wide                  */
+    uint8_t pat, n, pad0, pad1;
+    uint32_t blk;              /* block index                                    */
+    uint32_t pos[3];           /* block-relative positions                       */
+};
+struct Plan {
+    uint8_t ok, rm, nins, retag;
+    uint32_t esc;              /* escape query log (replayed by the emit pass)   */
+    uint32_t nv, ni, nm;       /* allocations incl. leaked ones (G4)             */
+    uint32_t vbase, ibase, mbase;
+};
+struct XRec {                  /* bitcast inserted by the reciprocal pass        */
+    Rec r;
+    uint32_t anchor;           /* stream position of the add                     */
+    uint32_t order;            /* index in its anchor's before / after list      */
+    uint32_t after;
+    uint32_t next;             /* next extra user of the same value              */
+};
+
+/* opcode classes of the seed scan: distinct head opcodes of one table        */
+static constexpr int MAX_CLS = 12;
+
+struct Caps {                  /* capacities of one group's work memory          */
+    uint32_t I;                /* records in the gap buffer                      */
+    uint32_t V;                /* values                                         */
+    uint32_t B;                /* blocks                                         */
+    uint32_t M;                /* raw matches of one block                       */
+    uint32_t S;                /* selected matches of one function               */
+    uint32_t Q;                /* immediates                                     */
+    uint32_t E;                /* events                                         */
+    uint32_t U;                /* use sites (reciprocal CSR)                     */
+    uint32_t X;                /* inserted bitcasts                              */
+};
+
+struct FS {                    /* one function resident in a group's work memory */
+    const cl_pattern_blob *pb;
+    const cl_modset *ms;
+    const uint8_t *opflags;    /* CL_OPF_* by opcode id (< CL_OP__COUNT)         */
+    Caps cap;
+    uint32_t f;                /* function index                                 */
+    uint32_t arch;
+    uint32_t *st;              /* group-shared status word (enum cl_status)      */
+    uint32_t passes, max_rounds, emit_matches;
+    /* stream: records [0, n) of S, blocks bo[0..nb]                           */
+    Planes S;
+    uint32_t n, nb;
+    uint32_t *bo, *bo2;        /* [B + 1] block offsets / next round's           */
+    cl_blk *blk;               /* [B] mutable copy (terminator operands)         */
+    /* values */
+    uint32_t *usecnt, *defpos; /* [V]                                            */
+    uint8_t *alive;            /* [V]                                            */
+    int32_t *def_iid;          /* [V]                                            */
+    uint32_t *origin;          /* [V]                                            */
+    uint32_t *redirect;        /* [V]  (also CSR offsets of the reciprocal pass) */
+    uint32_t next_vid, next_iid;
+    /* side tables */
+    cl_imm *imm; uint32_t n_imm;
+    cl_memref *mem; uint32_t n_mem;
+    uint16_t *ext_tag; uint32_t *ext_pay; uint32_t n_ext;
+    cl_event *ev; uint32_t *n_ev;       /* n_ev: one word of group-shared memory  */
+    /* per position scratch [I] */
+    uint8_t *keep, *inscnt, *clsid;
+    uint32_t *outpos, *cand, *sel_at;
+    unsigned long long *owner;
+    /* per match scratch */
+    MatchRec *mt;              /* [M]                                            */
+    SelRec *sel;               /* [S]                                            */
+    Plan *plan;                /* [S]                                            */
+    uint32_t *blk_sel;         /* [B + 1] selected-match range of each block     */
+    /* reciprocal */
+    uint32_t *site;            /* [U]                                            */
+    XRec *xr;                  /* [X]                                            */
+    uint32_t *xhead;           /* [V]                                            */
+    uint32_t *root;            /* [V]                                            */
+    /* statistics (group-private, flushed by the kernel)                       */
+    uint32_t *st_matches, *st_selected, *st_rewrites, *st_refused;   /* [16] each */
+    /* seed classes of the current table */
+    uint32_t n_cls;
+    uint16_t cls_op[MAX_CLS];
+    uint32_t cls_off[MAX_CLS + 1];
+};
+
+/* ---------------------------------------------------------- operand access */
+CLD unsigned kind_of(uint16_t t) { return CL_T_KIND(t); }
+CLD bool has_guard(const cl_hdr &h) { return (h.flags & CL_IF_GUARD) != 0; }
+CLD unsigned def0(const cl_hdr &h) { return has_guard(h); }
+CLD unsigned aux0(const cl_hdr &h) { return has_guard(h) + h.n_defs; }
+CLD unsigned use0(const cl_hdr &h) { return has_guard(h) + h.n_defs + h.n_aux; }
+CLD opnd get_slot(const FS &s, const cl_hdr &h, uint32_t i, unsigned k) {
+    opnd o;
+    if (h.flags & CL_IF_EXT) { o.tag = s.ext_tag[h.ext + k]; o.pay = s.ext_pay[h.ext + k]; }
+    else { o.tag = s.S.tag[(size_t)i * 8 + k]; o.pay = s.S.pay[(size_t)i * 8 + k]; }
+    return o;
+}
+CLD void set_slot(FS &s, const cl_hdr &h, uint32_t i, unsigned k, opnd o) {
+    if (h.flags & CL_IF_EXT) { s.ext_tag[h.ext + k] = o.tag; s.ext_pay[h.ext + k] = o.pay; }
+    else { s.S.tag[(size_t)i * 8 + k] = o.tag; s.S.pay[(size_t)i * 8 + k] = o.pay; }
+}
+CLD opnd get_use(const FS &s, const cl_hdr &h, uint32_t i, unsigned k) { return get_slot(s, h, i, use0(h) + k); }
+CLD opnd get_def(const FS &s, const cl_hdr &h, uint32_t i, unsigned k) { return get_slot(s, h, i, def0(h) + k); }
+CLD opnd get_aux(const FS &s, const cl_hdr &h, uint32_t i, unsigned k) { return get_slot(s, h, i, aux0(h) + k); }
+CLD bool is_value(opnd o) { return kind_of(o.tag) == CL_K_VALUE; }
+CLD bool is_zero(opnd o) { return kind_of(o.tag) == CL_K_RZ || kind_of(o.tag) == CL_K_URZ; }
+CLD bool is_imm(opnd o) { return kind_of(o.tag) == CL_K_IMM; }
+CLD bool is_none(opnd o) { return kind_of(o.tag) == CL_K_NONE; }
+/* getattr(op, "negated"/"bitnot"/"half", default) of patterns.py:142-144     */
+CLD bool o_neg(opnd o) { return (o.tag & CL_T_NEG) != 0; }
+CLD bool o_not(opnd o) { return !is_imm(o) && (o.tag & CL_T_NOT) != 0; }
+CLD unsigned o_half(opnd o) { return is_imm(o) ? 0u : CL_T_HALF(o.tag); }
+CLD uint64_t modmask(const FS &s, const cl_hdr &h) { return s.ms[h.modset].mask; }
+CLD bool has_mod(const FS &s, const cl_hdr &h, unsigned bit) { return (modmask(s, h) >> bit) & 1u; }
+CLD opnd value_ref(uint32_t vid) { opnd o; o.tag = CL_K_VALUE; o.pay = vid; return o; }
+CLD opnd strip(opnd o) { if (is_value(o)) o.tag &= (uint16_t)~(CL_T_NEG | CL_T_NOT); return o; }
+
+/* value_operands (ssa.py:599-610): guard, uses, MemRef base/ureg             */
+template <class F> CLD void for_value_operands(const FS &s, const cl_hdr &h, uint32_t i, F fn) {
+    if (has_guard(h)) { opnd g = get_slot(s, h, i, 0); if (is_value(g)) fn(g.pay); }
+    const unsigned u0 = use0(h);
+    for (unsigned k = 0; k < h.n_uses; k++) {
+        opnd u = get_slot(s, h, i, u0 + k);
+        if (is_value(u)) fn(u.pay);
+        else if (kind_of(u.tag) == CL_K_MEMREF) {
+            const cl_memref &m = s.mem[u.pay];
+            if (kind_of(m.base_tag) == CL_K_VALUE) fn(m.base_pay);
+            if (kind_of(m.ureg_tag) == CL_K_VALUE) fn(m.ureg_pay);
+        }
+    }
+}
+template <class F> CLD void for_value_defs(const FS &s, const cl_hdr &h, uint32_t i, F fn) {
+    const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
+    for (unsigned k = 0; k < nd; k++) { opnd d = get_slot(s, h, i, d0 + k); if (is_value(d)) fn(d.pay); }
+}
+
+CLD void ld_rec(const FS &s, uint32_t i, Rec &r) {
+    r.h = s.S.hdr[i];
+    const uint4 *t = (const uint4 *)(s.S.tag + (size_t)i * 8);
+    const uint4 *p = (const uint4 *)(s.S.pay + (size_t)i * 8);
+    *(uint4 *)r.tag = t[0];
+    ((uint4 *)r.pay)[0] = p[0];
+    ((uint4 *)r.pay)[1] = p[1];
+}
+CLD void st_rec(FS &s, uint32_t i, const Rec &r) {
+    s.S.hdr[i] = r.h;
+    *(uint4 *)(s.S.tag + (size_t)i * 8) = *(const uint4 *)r.tag;
+    ((uint4 *)(s.S.pay + (size_t)i * 8))[0] = ((const uint4 *)r.pay)[0];
+    ((uint4 *)(s.S.pay + (size_t)i * 8))[1] = ((const uint4 *)r.pay)[1];
+}
+
+/* move n records from src to dst inside the gap buffer (any overlap)          */
+template <class G> CLF void move_recs(const G &g, FS &s, uint32_t dst, uint32_t src, uint32_t n) {
+    if (dst == src || n == 0) return;
+    const uint32_t chunks = (n + g.size - 1) / g.size;
+    for (uint32_t c = 0; c < chunks; c++) {
+        const uint32_t cc = dst < src ? c : chunks - 1 - c;
+        const uint32_t i = cc * g.size + g.rank;
+        Rec r;
+        if (i < n) ld_rec(s, src + i, r);
+        g.sync();
+        if (i < n) st_rec(s, dst + i, r);
+        g.sync();
+    }
+}
+
+/* first error wins; read it back only after a group sync                     */
+CLD void fail(FS &s, uint32_t code) { a_cas0(s.st, code); }
+CLD uint32_t status(const FS &s) { return *(volatile uint32_t *)s.st; }
+
+CLD void push_event(FS &s, uint32_t seq, uint32_t kind, uint32_t idx, uint32_t a, uint32_t b,
+                    uint32_t c, uint32_t d) {
+    uint32_t k = a_add(s.n_ev, 1u);
+    if (k < s.cap.E) {
+        cl_event e; e.func = s.f; e.seq = seq; e.kind = kind; e.idx = idx; e.a = a; e.b = b; e.c = c; e.d = d;
+        s.ev[k] = e;
+    }
+}
+
+/* ------------------------------------------------------------------ def-use */
+/* Use counts (= len(du.users(vid)), terminator sites included) and the stream
+ * position of each value's defining instruction (du.def_inst), ssa.py:613-636 */
+template <class G> CLF void build_usecount(const G &g, FS &s) {
+    GFOR(g, v, s.next_vid) if (v < s.next_vid) { s.usecnt[v] = 0; s.defpos[v] = NONE32; }
+    g.sync();
+    GFOR(g, i, s.n) if (i < s.n) {
+        const cl_hdr h = s.S.hdr[i];
+        for_value_defs(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.defpos[v] = i; });
+        for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_add(&s.usecnt[v], 1u); });
+    }
+    GFOR(g, b, s.nb) if (b < s.nb)
+        for (int k = 0; k < 2; k++)
+            if (kind_of(s.blk[b].term_tag[k]) == CL_K_VALUE && s.blk[b].term_pay[k] < s.cap.V)
+                a_add(&s.usecnt[s.blk[b].term_pay[k]], 1u);
+    g.sync();
+}
+
+/* ----------------------------------------------------------------- matching */
+/* operand_key (patterns.py:109-127)                                           */
+CLD okey operand_key(const FS &s, opnd o) {
+    okey k; k.cls = KC_OTHER; k.v = o.pay;
+    switch (kind_of(o.tag)) {
+    case CL_K_VALUE: k.cls = KC_V; break;
+    case CL_K_IMM: k.cls = KC_IMM; k.v = s.imm[o.pay].bits; break;
+    case CL_K_RZ: case CL_K_URZ: k.cls = KC_RZ; k.v = 0; break;
+    case CL_K_PRED: if (o.pay == CL_PT_INDEX) { k.cls = KC_PT; k.v = 0; } else k.cls = KC_P; break;
+    case CL_K_CONSTMEM: k.cls = KC_CM; break;
+    case CL_K_REG: k.cls = KC_R; break;
+    case CL_K_UREG: k.cls = KC_UR; break;
+    case CL_K_SREG: k.cls = KC_SR; break;
+    default: break;
+    }
+    return k;
+}
+CLD bool memref_equal(const FS &s, uint32_t a, uint32_t b) {
+    const cl_memref &x = s.mem[a], &y = s.mem[b];
+    if (x.base_tag != y.base_tag || x.ureg_tag != y.ureg_tag) return false;
+    if (kind_of(x.base_tag) != CL_K_NONE && x.base_pay != y.base_pay) return false;
+    if (kind_of(x.ureg_tag) != CL_K_NONE && x.ureg_pay != y.ureg_pay) return false;
+    return x.off_hi == y.off_hi && x.off_lo == y.off_lo;
+}
+CLD bool key_equal(const FS &s, okey a, okey b) {
+    if (a.cls != b.cls) return false;
+    if (a.cls == KC_OTHER) return memref_equal(s, (uint32_t)a.v, (uint32_t)b.v);
+    return a.v == b.v;
+}
+/* Bindings.bind (patterns.py:93-97)                                           */
+CLD bool bind(const FS &s, Bind &b, unsigned name, okey k) {
+    if (b.var[name].cls != KC_NONE && !key_equal(s, b.var[name], k)) return false;
+    b.var[name] = k;
+    return true;
+}
+/* _match_slot (patterns.py:130-152)                                           */
+CLD bool match_slot(const FS &s, const cl_slot &sl, opnd o, Bind &b) {
+    switch (sl.kind) {
+    case CL_S_ANY: return true;
+    case CL_S_RZ: return is_zero(o);
+    case CL_S_PT:
+        if (!(kind_of(o.tag) == CL_K_PRED && o.pay == CL_PT_INDEX)) return false;
+        return sl.neg == 0 || o_neg(o) == (sl.neg == 2);
+    case CL_S_IMM: return is_imm(o) && s.imm[o.pay].bits == sl.imm;
+    case CL_S_VAR:
+        if (sl.neg && o_neg(o) != (sl.neg == 2)) return false;
+        if (sl.bitnot && o_not(o) != (sl.bitnot == 2)) return false;
+        if (sl.half && o_half(o) != sl.half) return false;
+        return bind(s, b, sl.var, operand_key(s, o));
+    }
+    return false;
+}
+/* _match_opcode + _unify (patterns.py:155-178)                                */
+CLD bool match_inst(const FS &s, const cl_template &t, const cl_hdr &h, uint32_t i, Bind &b) {
+    if (h.op != t.op) return false;
+    const cl_modset &ms = s.ms[h.modset];
+    if ((ms.mask & t.mods_all) != t.mods_all) return false;
+    if (ms.mask & t.mods_none) return false;
+    for (unsigned k = 0; k < t.n_modvars; k++) {
+        const uint8_t got = ms.first[t.modvar_group[k]];
+        okey key; key.cls = KC_MOD; key.v = got;
+        if (got == 0xFF || !bind(s, b, CL_MAX_VARS + t.modvar_var[k], key)) return false;
+    }
+    if (t.n_defs != h.n_defs || t.n_aux != h.n_aux || t.n_uses != h.n_uses) return false;
+    const unsigned n = (unsigned)t.n_defs + t.n_aux + t.n_uses, g0 = has_guard(h);
+    if (h.flags & CL_IF_EXT) return false;          /* > 8 slots never equals a template's arity */
+    for (unsigned k = 0; k < n; k++)
+        if (!match_slot(s, t.slot[k], get_slot(s, h, i, g0 + k), b)) return false;
+    return true;
+}
+/* _connected (patterns.py:219-238)                                            */
+CLF bool connected(const FS &s, const uint32_t *idx, unsigned n) {
+    if (n == 1) return true;
+    uint32_t vals[CL_MAX_TEMPLATES][24];
+    unsigned cnt[CL_MAX_TEMPLATES];
+    for (unsigned t = 0; t < n; t++) {
+        unsigned c = 0;
+        const cl_hdr h = s.S.hdr[idx[t]];
+        for_value_defs(s, h, idx[t], [&](uint32_t v) { if (c < 24) vals[t][c++] = v; });
+        for_value_operands(s, h, idx[t], [&](uint32_t v) { if (c < 24) vals[t][c++] = v; });
+        cnt[t] = c;
+    }
+    unsigned linked = 1;
+    for (bool changed = true; changed;) {
+        changed = false;
+        for (unsigned i = 0; i < n; i++) {
+            if (linked >> i & 1) continue;
+            bool hit = false;
+            for (unsigned j = 0; j < n && !hit; j++) {
+                if (!(linked >> j & 1)) continue;
+                for (unsigned a = 0; a < cnt[i] && !hit; a++)
+                    for (unsigned c = 0; c < cnt[j]; c++) if (vals[i][a] == vals[j][c]) { hit = true; break; }
+            }
+            if (hit) { linked |= 1u << i; changed = true; }
+        }
+    }
+    return linked == (1u << n) - 1u;
+}
+/* one candidate tuple of match_patterns (patterns.py:199-215); idx = stream
+ * positions, strictly increasing order already checked by the caller         */
+CLF bool check_tuple(const FS &s, const cl_pattern &p, const uint32_t *idx, Bind &b) {
+    for (int k = 0; k < NBIND; k++) b.var[k].cls = KC_NONE;
+    for (unsigned t = 0; t < p.n_templates; t++) {
+        const cl_hdr h = s.S.hdr[idx[t]];
+        if (!match_inst(s, p.t[t], h, idx[t], b)) return false;
+    }
+    return connected(s, idx, p.n_templates);
+}
+
+/* head opcodes of one pattern table -> seed classes                          */
+CLF void setup_classes(FS &s, unsigned table) {
+    s.n_cls = 0;
+    const cl_pattern_blob *pb = s.pb;
+    for (unsigned pi = 0; pi < pb->n_patterns; pi++) {
+        const cl_pattern &p = pb->p[pi];
+        if (p.table != table) continue;
+        for (unsigned t = 0; t < p.n_templates; t++) {
+            bool seen = false;
+            for (unsigned c = 0; c < s.n_cls; c++) seen |= s.cls_op[c] == p.t[t].op;
+            if (!seen && s.n_cls < (unsigned)MAX_CLS) s.cls_op[s.n_cls++] = p.t[t].op;
+        }
+    }
+}
+CLD int class_of(const FS &s, uint16_t op) {
+    for (unsigned c = 0; c < s.n_cls; c++) if (s.cls_op[c] == op) return (int)c;
+    return -1;
+}
+
+/* FindSeeds (patterns.py:189-191): per head opcode, the block positions whose
+ * base opcode fits, in order -- ballot/popc compaction per class.            */
+template <class G> CLF uint32_t seed_scan(const G &g, FS &s, uint32_t lo, uint32_t n) {
+    GFOR(g, i, n) if (i < n) {
+        const uint16_t op = s.S.hdr[lo + i].op;
+        s.clsid[i] = (uint8_t)class_of(s, op);
+    }
+    g.sync();
+    uint32_t total = 0;
+    for (unsigned c = 0; c < s.n_cls; c++) {
+        s.cls_off[c] = total;
+        GFOR(g, i, n) {
+            const bool f = i < n && s.clsid[i] == c;
+            uint32_t cnt;
+            const uint32_t off = g.flag_exscan(f, cnt);
+            if (f) s.cand[total + off] = i;
+            total += cnt;
+        }
+    }
+    s.cls_off[s.n_cls] = total;
+    g.sync();
+    return total;
+}
+
+/* match_patterns (patterns.py:181-216) of one block: every tuple of rank
+ * < budget in product order; matches appended in list order.                */
+template <class G> CLF uint32_t match_block(const G &g, FS &s, uint32_t lo, uint32_t n, unsigned table) {
+    if (seed_scan(g, s, lo, n) == 0) return 0;
+    const cl_pattern_blob *pb = s.pb;
+    uint32_t nm = 0;
+    for (unsigned pi = 0; pi < pb->n_patterns; pi++) {
+        const cl_pattern &p = pb->p[pi];
+        if (p.table != table) continue;
+        const unsigned nt = p.n_templates;
+        uint32_t cn[3] = { 1, 1, 1 }, cb[3] = { 0, 0, 0 };
+        bool empty = false;
+        for (unsigned t = 0; t < nt; t++) {
+            const int c = class_of(s, p.t[t].op);
+            cn[t] = s.cls_off[c + 1] - s.cls_off[c];
+            cb[t] = s.cls_off[c];
+            empty |= cn[t] == 0;
+        }
+        if (empty) continue;
+        unsigned long long T = (unsigned long long)cn[0] * cn[1] * cn[2];
+        if (T > pb->budget) T = pb->budget;                     /* :194-198 */
+        const uint32_t Tl = (uint32_t)T;
+        GFOR(g, r, Tl) {
+            bool ok = false;
+            uint32_t idx[3] = { NONE32, NONE32, NONE32 };
+            if (r < Tl) {
+                uint32_t q = r;
+                uint32_t i2 = 0, i1 = 0;
+                if (nt > 2) { i2 = q % cn[2]; q /= cn[2]; }
+                if (nt > 1) { i1 = q % cn[1]; q /= cn[1]; }
+                idx[0] = s.cand[cb[0] + q];
+                ok = true;
+                if (nt > 1) { idx[1] = s.cand[cb[1] + i1]; ok = idx[0] < idx[1]; }
+                if (nt > 2) { idx[2] = s.cand[cb[2] + i2]; ok = ok && idx[1] < idx[2]; }
+                if (ok) {
+                    uint32_t abs_idx[3] = { lo + idx[0], lo + idx[1], lo + idx[2] };
+                    Bind b;
+                    ok = check_tuple(s, p, abs_idx, b);
+                }
+            }
+            uint32_t cnt;
+            const uint32_t off = g.flag_exscan(ok, cnt);
+            if (ok && nm + off < s.cap.M) {
+                MatchRec m;
+                m.pat = (uint8_t)pi; m.n = (uint8_t)nt; m.state = MS_UNDECIDED; m.pad = 0;
+                m.pos[0] = idx[0]; m.pos[1] = idx[1]; m.pos[2] = idx[2];
+                m.seq = (uint32_t)pi << 20 | r;
+                s.mt[nm + off] = m;
+            }
+            nm += cnt;
+        }
+    }
+    g.sync();
+    if (nm > s.cap.M) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }
+    return nm;
+}
+
+/* select_matches (patterns.py:241-252).  The stable sort key is
+ * (start_pos, -len, list order); the greedy scan keeps a match iff no kept
+ * match of smaller key overlaps it.  Parallel form: every round each
+ * undecided match bids for its positions with its key (atomicMin); a match
+ * that owns all of them has no smaller undecided rival and no kept rival, so
+ * the sequential scan would keep it too; a match touching a kept position is
+ * dropped.  Kept matches have distinct start positions, so ordered compaction
+ * over positions yields them in sorted order.                               */
+CLD unsigned long long match_key(const MatchRec &m) {
+    return (unsigned long long)m.pos[0] << 32 | (unsigned long long)(3u - m.n) << 30 | (m.seq & 0x3FFFFFFFu);
+}
+template <class G> CLF uint32_t select_block(const G &g, FS &s, uint32_t n, uint32_t nm, uint32_t bi,
+                                             uint32_t nsel) {
+    GFOR(g, p, n) if (p < n) { s.keep[p] = 0; s.sel_at[p] = NONE32; }
+    g.sync();
+    for (;;) {
+        GFOR(g, p, n) if (p < n && !s.keep[p]) s.owner[p] = NONE64;
+        g.sync();
+        GFOR(g, m, nm) if (m < nm && s.mt[m].state == MS_UNDECIDED) {
+            MatchRec &r = s.mt[m];
+            bool clash = false;
+            for (unsigned t = 0; t < r.n; t++) clash |= s.keep[r.pos[t]] != 0;
+            if (clash) r.state = MS_REJECTED;
+            else for (unsigned t = 0; t < r.n; t++) a_min64(&s.owner[r.pos[t]], match_key(r));
+        }
+        g.sync();
+        bool left = false;
+        GFOR(g, m, nm) if (m < nm && s.mt[m].state == MS_UNDECIDED) {
+            MatchRec &r = s.mt[m];
+            const unsigned long long key = match_key(r);
+            bool mine = true;
+            for (unsigned t = 0; t < r.n; t++) mine &= s.owner[r.pos[t]] == key;
+            if (mine) {
+                r.state = MS_SELECTED;
+                for (unsigned t = 0; t < r.n; t++) s.keep[r.pos[t]] = 1;
+                s.sel_at[r.pos[0]] = m;
+            } else
+                left = true;
+        }
+        const bool again = g.any(left);
+        g.sync();
+        if (!again) break;
+    }
+    uint32_t count = 0;
+    GFOR(g, p, n) {
+        const bool f = p < n && s.sel_at[p] != NONE32;
+        uint32_t cnt;
+        const uint32_t off = g.flag_exscan(f, cnt);
+        if (f && nsel + count + off < s.cap.S) {
+            const MatchRec &m = s.mt[s.sel_at[p]];
+            SelRec r;
+            r.pat = m.pat; r.n = m.n; r.pad0 = r.pad1 = 0; r.blk = bi;
+            r.pos[0] = m.pos[0]; r.pos[1] = m.pos[1]; r.pos[2] = m.pos[2];
+            s.sel[nsel + count + off] = r;
+        }
+        count += cnt;
+    }
+    g.sync();
+    if (nsel + count > s.cap.S) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }
+    return count;
+}
+
+/* CL_EV_MATCH events of one block (match-only runs, emit_matches)            */
+template <class G> CLF void emit_match_events(const G &g, FS &s, uint32_t seq, uint32_t nm, uint32_t sel0,
+                                              uint32_t nsel) {
+    GFOR(g, m, nm) if (m < nm) {
+        const MatchRec &r = s.mt[m];
+        push_event(s, seq, CL_EV_MATCH, r.seq, r.pat, r.pos[0], r.pos[1], r.pos[2]);
+    }
+    GFOR(g, j, nsel) if (j < nsel) {
+        const SelRec &r = s.sel[sel0 + j];
+        push_event(s, seq, CL_EV_MATCH, 0x80000000u | j, r.pat | 1u << 16, r.pos[0], r.pos[1], r.pos[2]);
+    }
+}
+
+/* ------------------------------------------------------------------ rewrites */
+/* One lane plans one selected match.  The same code runs twice: a COUNT pass
+ * (allocation counts, escape decisions, refusal) and, after an exclusive scan
+ * over the block's matches in select order (G3), a WRITE pass that replays
+ * the logged escape decisions and emits with the scanned bases.             */
+struct RW {
+    FS *s;
+    bool write, store;
+    uint32_t vid, iid, imm;        /* allocation cursors                        */
+    uint32_t nins, out;            /* records emitted / first output position   */
+    uint32_t esc, esc_n;           /* escape query log                          */
+    uint32_t idx[3];               /* stream positions of the matched records   */
+    cl_hdr h[3];
+    unsigned n, pat;
+    unsigned rm;                   /* removal mask (bit t = instruction t)      */
+    bool retag;
+    Bind b;
+};
+
+CLD uint32_t rw_value(RW &c, uint32_t origin) {
+    const uint32_t v = c.vid++;
+    if (c.write && v < c.s->cap.V) { c.s->alive[v] = 1; c.s->def_iid[v] = -1; c.s->origin[v] = origin; c.s->usecnt[v] = 0; c.s->defpos[v] = NONE32; }
+    return v;
+}
+CLD opnd rw_imm(RW &c, unsigned long long bits, unsigned long long text, bool hextext) {
+    const uint32_t q = c.imm++;
+    if (c.write && q < c.s->cap.Q) { cl_imm im; im.bits = bits; im.text = text; c.s->imm[q] = im; }
+    opnd o; o.tag = (uint16_t)(CL_K_IMM | (hextext ? CL_T_IMM_HEXTEXT : 0)); o.pay = q;
+    return o;
+}
+/* LiftedFunction.make_inst (ssir.py:237-241)                                  */
+CLD Rec rw_make(RW &c, uint16_t op, uint16_t modset, const opnd *defs, unsigned nd, const opnd *uses,
+                unsigned nu) {
+    Rec r;
+    r.h.iid = c.iid++;
+    r.h.op = op; r.h.modset = modset;
+    r.h.n_defs = (uint8_t)nd; r.h.n_aux = 0; r.h.n_uses = (uint8_t)nu; r.h.flags = 0; r.h.ext = 0;
+    unsigned k = 0;
+    for (unsigned i = 0; i < nd; i++, k++) { r.tag[k] = defs[i].tag; r.pay[k] = defs[i].pay; }
+    for (unsigned i = 0; i < nu; i++, k++) { r.tag[k] = uses[i].tag; r.pay[k] = uses[i].pay; }
+    for (; k < 8; k++) { r.tag[k] = 0; r.pay[k] = 0; }
+    return r;
+}
+CLD void rw_push(RW &c, const Rec &r) {
+    if (c.write && c.store) {
+        FS &s = *c.s;
+        st_rec(s, c.out + c.nins, r);
+        const unsigned u0 = (unsigned)r.h.n_defs;
+        for (unsigned k = 0; k < r.h.n_uses; k++) {          /* new records hold no guard / MemRef of their own */
+            const unsigned kk = u0 + k;
+            if (kind_of(r.tag[kk]) == CL_K_VALUE) { if (r.pay[kk] < s.cap.V) a_add(&s.usecnt[r.pay[kk]], 1u); }
+            else if (kind_of(r.tag[kk]) == CL_K_MEMREF) {
+                const cl_memref &m = s.mem[r.pay[kk]];
+                if (kind_of(m.base_tag) == CL_K_VALUE) a_add(&s.usecnt[m.base_pay], 1u);
+                if (kind_of(m.ureg_tag) == CL_K_VALUE) a_add(&s.usecnt[m.ureg_pay], 1u);
+            }
+        }
+    }
+    c.nins++;
+}
+CLD void rw_set_def_iid(RW &c, uint32_t vid, uint32_t iid) {
+    if (c.write && vid < c.s->cap.V) c.s->def_iid[vid] = (int32_t)iid;
+}
+CLD void rw_drop(RW &c, opnd o) {                       /* _drop_values :314-317 */
+    if (c.write && c.store && is_value(o) && o.pay < c.s->cap.V) c.s->alive[o.pay] = 0;
+}
+CLD void rw_fail(RW &c, uint32_t code) { if (!c.write) fail(*c.s, code); }
+
+/* _escapes (patterns.py:259-263) against the def-use snapshot of the block:
+ * a value escapes iff it has more use sites than the group itself holds.    */
+CLF bool rw_escapes(RW &c, uint32_t vid) {
+    bool r;
+    if (c.write) r = (c.esc >> c.esc_n) & 1u;
+    else {
+        FS &s = *c.s;
+        uint32_t inside = 0;
+        for (unsigned t = 0; t < c.n; t++)
+            for_value_operands(s, c.h[t], c.idx[t], [&](uint32_t v) { inside += v == vid; });
+        r = vid < s.cap.V && s.usecnt[vid] != inside;
+        if (r) c.esc |= 1u << c.esc_n;
+    }
+    c.esc_n++;
+    return r;
+}
+/* _safe (patterns.py:266-275)                                                 */
+CLF bool rw_safe(RW &c, const opnd *redef, unsigned nredef) {
+    FS &s = *c.s;
+    bool ok = true;
+    for (unsigned t = 0; t < c.n && ok; t++) {
+        const unsigned d0 = def0(c.h[t]), nd = (unsigned)c.h[t].n_defs + c.h[t].n_aux;
+        for (unsigned k = 0; k < nd && ok; k++) {
+            opnd d = get_slot(s, c.h[t], c.idx[t], d0 + k);
+            if (!is_value(d)) continue;
+            bool re = false;
+            for (unsigned j = 0; j < nredef; j++) re |= is_value(redef[j]) && redef[j].pay == d.pay;
+            if (!re && rw_escapes(c, d.pay)) ok = false;
+        }
+    }
+    return ok;
+}
+/* _pack_pair (patterns.py:278-300); CL_K_NONE stands for None                 */
+CLF opnd rw_pack_pair(RW &c, opnd lo, opnd hi) {
+    FS &s = *c.s;
+    const bool lo_zero = is_zero(lo), hi_zero = is_zero(hi);
+    opnd none; none.tag = CL_K_NONE; none.pay = 0;
+    if (lo_zero && hi_zero) return none;
+    if (is_imm(lo) && hi_zero) {
+        const cl_imm im = s.imm[lo.pay];
+        return rw_imm(c, im.bits & 0xFFFFFFFFull, im.text, (lo.tag & CL_T_IMM_HEXTEXT) != 0);
+    }
+    if (is_imm(lo) && is_imm(hi)) {
+        const unsigned long long bits = (s.imm[lo.pay].bits & 0xFFFFFFFFull) | (s.imm[hi.pay].bits & 0xFFFFFFFFull) << 32;
+        return rw_imm(c, bits, bits, true);
+    }
+    if (lo_zero && is_imm(hi)) {
+        const unsigned long long bits = (s.imm[hi.pay].bits & 0xFFFFFFFFull) << 32;
+        return rw_imm(c, bits, bits, true);
+    }
+    const uint32_t v = rw_value(c, CL_ORG_PAIR);
+    opnd u[2];
+    u[0] = lo_zero ? rw_imm(c, 0, 0, true) : strip(lo);
+    u[1] = hi_zero ? rw_imm(c, 0, 0, true) : strip(hi);
+    opnd d = value_ref(v);
+    Rec pk = rw_make(c, CL_OP_PACK64, CL_MS_NONE, &d, 1, u, 2);
+    rw_set_def_iid(c, v, pk.h.iid);
+    rw_push(c, pk);
+    return d;
+}
+/* _unpack_into (patterns.py:303-311)                                          */
+CLF void rw_unpack_into(RW &c, uint32_t src, opnd lo_ref, opnd hi_ref) {
+    opnd refs[2] = { lo_ref, hi_ref };
+    for (int k = 0; k < 2; k++) {
+        if (!is_value(refs[k])) continue;
+        opnd d = value_ref(refs[k].pay), u = value_ref(src);
+        Rec up = rw_make(c, CL_OP_UNPACK64, k ? CL_MS_HI : CL_MS_LO, &d, 1, &u, 1);
+        if (!c.write && !(d.pay < c.s->cap.V && c.s->alive[d.pay])) { rw_fail(c, CL_ST_KEY_ERROR); return; }
+        rw_set_def_iid(c, d.pay, up.h.iid);
+        rw_push(c, up);
+    }
+}
+CLD bool rw_redefine(RW &c, opnd res, uint32_t iid) {
+    if (!c.write) {
+        if (!is_value(res)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+        if (!(res.pay < c.s->cap.V && c.s->alive[res.pay])) { rw_fail(c, CL_ST_KEY_ERROR); return false; }
+    }
+    rw_set_def_iid(c, res.pay, iid);
+    return true;
+}
+
+/* _rw_iadd364 (patterns.py:324-362)                                           */
+CLF bool rw_iadd364(RW &c) {
+    FS &s = *c.s;
+    const cl_hdr &lo = c.h[0], &hi = c.h[1];
+    opnd carry = get_aux(s, lo, c.idx[0], 0);
+    opnd redef[2] = { get_def(s, lo, c.idx[0], 0), get_def(s, hi, c.idx[1], 0) };
+    if (!rw_safe(c, redef, 2)) return false;
+    opnd ops[3];
+    unsigned nops = 0;
+    for (unsigned k = 0; k < 3; k++) {
+        opnd lo_op = get_use(s, lo, c.idx[0], k), hi_op = get_use(s, hi, c.idx[1], k);
+        const bool neg_lo = o_neg(lo_op), not_hi = o_not(hi_op);
+        const bool plain = !neg_lo && !not_hi && !o_not(lo_op) && !o_neg(hi_op);
+        if (plain) {
+            opnd p = rw_pack_pair(c, lo_op, hi_op);
+            if (!is_none(p)) ops[nops++] = p;
+        } else if (neg_lo && not_hi) {
+            opnd p = rw_pack_pair(c, strip(lo_op), strip(hi_op));
+            if (is_none(p)) return false;
+            if (is_imm(p)) {
+                /* Imm(-p.int_value(64) & M64, p.text): in the COUNT pass the table entry of p
+                 * does not exist yet, so recompute it the way rw_pack_pair did.              */
+                unsigned long long bits, text; bool hx;
+                const bool lz = is_zero(lo_op), hz = is_zero(hi_op);
+                if (is_imm(lo_op) && hz) { const cl_imm im = s.imm[lo_op.pay]; bits = im.bits & 0xFFFFFFFFull; text = im.text; hx = (lo_op.tag & CL_T_IMM_HEXTEXT) != 0; }
+                else if (is_imm(lo_op) && is_imm(hi_op)) { bits = (s.imm[lo_op.pay].bits & 0xFFFFFFFFull) | (s.imm[hi_op.pay].bits & 0xFFFFFFFFull) << 32; text = bits; hx = true; }
+                else { (void)lz; bits = (s.imm[hi_op.pay].bits & 0xFFFFFFFFull) << 32; text = bits; hx = true; }
+                ops[nops++] = rw_imm(c, 0ull - bits, text, hx);
+            } else {
+                p.tag |= CL_T_NEG;
+                ops[nops++] = p;
+            }
+        } else
+            return false;
+    }
+    if (!nops) return false;
+    const uint32_t res = rw_value(c, CL_ORG_PAIR);
+    opnd d = value_ref(res);
+    Rec agg = rw_make(c, CL_OP_IADD364, CL_MS_NONE, &d, 1, ops, nops);
+    rw_set_def_iid(c, res, agg.h.iid);
+    rw_push(c, agg);
+    rw_unpack_into(c, res, redef[0], redef[1]);
+    rw_drop(c, carry);
+    c.rm = 3;
+    return true;
+}
+/* _rw_isetp64 (patterns.py:371-390)                                           */
+CLF bool rw_isetp64(RW &c) {
+    FS &s = *c.s;
+    const cl_pattern &p = s.pb->p[c.pat];
+    const cl_hdr &lo = c.h[0], &hi = c.h[1];
+    opnd res = get_def(s, hi, c.idx[1], 0);
+    if (!rw_safe(c, &res, 1)) return false;
+    const unsigned cond = s.pb->group_pos[c.b.var[CL_MAX_VARS + p.modvar_cond].v & 63];
+    const unsigned bop = s.pb->group_pos[c.b.var[CL_MAX_VARS + p.modvar_bop].v & 63];
+    const unsigned unsigned_hi = has_mod(s, hi, CL_MB_U32);
+    opnd u[3];
+    u[0] = rw_pack_pair(c, get_use(s, lo, c.idx[0], 0), get_use(s, hi, c.idx[1], 0));
+    u[1] = rw_pack_pair(c, get_use(s, lo, c.idx[0], 1), get_use(s, hi, c.idx[1], 1));
+    if (is_none(u[0])) u[0] = rw_imm(c, 0, 0, true);
+    if (is_none(u[1])) u[1] = rw_imm(c, 0, 0, true);
+    u[2] = get_use(s, hi, c.idx[1], 2);
+    if (!is_value(res)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+    opnd d = value_ref(res.pay);
+    Rec agg = rw_make(c, CL_OP_ISETP64, s.pb->isetp64_ms[cond & 7][unsigned_hi][bop & 7], &d, 1, u, 3);
+    if (!rw_redefine(c, res, agg.h.iid)) return false;
+    rw_push(c, agg);
+    rw_drop(c, get_def(s, lo, c.idx[0], 0));
+    c.rm = 3;
+    return true;
+}
+/* _rw_lea64 (patterns.py:393-411)                                             */
+CLF bool rw_lea64(RW &c) {
+    FS &s = *c.s;
+    const cl_hdr &lo = c.h[0], &hi = c.h[1];
+    opnd carry = get_aux(s, lo, c.idx[0], 0);
+    opnd redef[2] = { get_def(s, lo, c.idx[0], 0), get_def(s, hi, c.idx[1], 0) };
+    if (!rw_safe(c, redef, 2)) return false;
+    opnd a64 = rw_pack_pair(c, get_use(s, lo, c.idx[0], 0), get_use(s, hi, c.idx[1], 2));
+    opnd b64 = rw_pack_pair(c, get_use(s, lo, c.idx[0], 1), get_use(s, hi, c.idx[1], 1));
+    if (is_none(a64) || is_none(b64)) return false;
+    const uint32_t res = rw_value(c, CL_ORG_PAIR);
+    opnd d = value_ref(res), u[3] = { b64, a64, get_use(s, lo, c.idx[0], 2) };
+    Rec agg = rw_make(c, CL_OP_LEA64, CL_MS_NONE, &d, 1, u, 3);
+    rw_set_def_iid(c, res, agg.h.iid);
+    rw_push(c, agg);
+    rw_unpack_into(c, res, redef[0], redef[1]);
+    rw_drop(c, carry);
+    c.rm = 3;
+    return true;
+}
+/* _rw_imad_wide (patterns.py:414-418): in-place retag                         */
+CLF bool rw_imad_wide(RW &c) {
+    if (c.write) {
+        cl_hdr &h = c.s->S.hdr[c.idx[0]];
+        h.modset = c.s->ms[h.modset].minus_wide;
+        h.op = CL_OP_IMAD64;
+    }
+    c.retag = true;
+    return true;
+}
+/* tail of mov64 / cast64 / shl64 / shr64 (patterns.py:433-439 and alike)      */
+CLF bool rw_finish_pack(RW &c, const Rec &agg, unsigned n_feed) {
+    FS &s = *c.s;
+    rw_push(c, agg);
+    c.rm = 1u << n_feed;
+    for (unsigned t = 0; t < n_feed; t++) {
+        opnd d = get_def(s, c.h[t], c.idx[t], 0);
+        if (!is_value(d)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+        if (!rw_escapes(c, d.pay)) { rw_drop(c, d); c.rm |= 1u << t; }
+    }
+    return true;
+}
+/* _rw_mov64 (patterns.py:421-439)                                             */
+CLF bool rw_mov64(RW &c) {
+    FS &s = *c.s;
+    opnd clo = get_use(s, c.h[0], c.idx[0], 0), chi = get_use(s, c.h[1], c.idx[1], 0);
+    if (kind_of(clo.tag) != CL_K_CONSTMEM || kind_of(chi.tag) != CL_K_CONSTMEM) return false;
+    const uint32_t mask = (1u << CL_CM_OFFSET_BITS) - 1u;
+    if ((clo.pay >> CL_CM_OFFSET_BITS) != (chi.pay >> CL_CM_OFFSET_BITS) ||
+        (chi.pay & mask) != (clo.pay & mask) + 4u) return false;
+    opnd res = get_def(s, c.h[2], c.idx[2], 0);
+    if (!is_value(res)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+    opnd d = value_ref(res.pay), u;
+    u.tag = (uint16_t)(CL_K_CONSTMEM | 2u << CL_T_WIDTH_SHIFT); u.pay = clo.pay;
+    Rec agg = rw_make(c, CL_OP_MOV64, CL_MS_NONE, &d, 1, &u, 1);
+    if (!rw_redefine(c, res, agg.h.iid)) return false;
+    return rw_finish_pack(c, agg, 2);
+}
+/* _rw_cast64 (patterns.py:442-453)                                            */
+CLF bool rw_cast64(RW &c) {
+    FS &s = *c.s;
+    opnd res = get_def(s, c.h[1], c.idx[1], 0);
+    if (!is_value(res)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+    opnd d = value_ref(res.pay), u = strip(get_use(s, c.h[1], c.idx[1], 0));
+    Rec agg = rw_make(c, CL_OP_CAST64, CL_MS_NONE, &d, 1, &u, 1);
+    if (!rw_redefine(c, res, agg.h.iid)) return false;
+    return rw_finish_pack(c, agg, 1);
+}
+/* _rw_shl64 / _rw_shr64 (patterns.py:456-495)                                 */
+CLF bool rw_shift64(RW &c, bool right) {
+    FS &s = *c.s;
+    const bool is_signed = has_mod(s, c.h[0], CL_MB_S32);
+    opnd src = right ? rw_pack_pair(c, get_use(s, c.h[1], c.idx[1], 0), get_use(s, c.h[0], c.idx[0], 2))
+                     : rw_pack_pair(c, get_use(s, c.h[0], c.idx[0], 0), get_use(s, c.h[0], c.idx[0], 2));
+    if (is_none(src)) return false;
+    opnd res = get_def(s, c.h[2], c.idx[2], 0);
+    if (!is_value(res)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+    opnd d = value_ref(res.pay), u[2] = { src, get_use(s, c.h[0], c.idx[0], 1) };
+    Rec agg = rw_make(c, right ? CL_OP_SHR64 : CL_OP_SHL64,
+                      right ? (is_signed ? CL_MS_S64 : CL_MS_U64) : CL_MS_NONE, &d, 1, u, 2);
+    if (!rw_redefine(c, res, agg.h.iid)) return false;
+    return rw_finish_pack(c, agg, 2);
+}
+/* _var_operand (patterns.py:514-524)                                          */
+CLD bool rw_var_operand(RW &c, okey k, opnd *out) {
+    switch (k.cls) {
+    case KC_V: *out = value_ref((uint32_t)k.v); return true;
+    case KC_IMM: *out = rw_imm(c, k.v, k.v, true); return true;
+    case KC_CM: out->tag = (uint16_t)(CL_K_CONSTMEM | 1u << CL_T_WIDTH_SHIFT); out->pay = (uint32_t)k.v; return true;
+    case KC_RZ: out->tag = CL_K_RZ; out->pay = 0; return true;
+    default: rw_fail(c, k.cls == KC_NONE ? CL_ST_KEY_ERROR : CL_ST_ASSERTION_ERROR); return false;
+    }
+}
+/* _rw_xmad (patterns.py:498-511)                                              */
+CLF bool rw_xmad(RW &c) {
+    FS &s = *c.s;
+    const cl_pattern &p = s.pb->p[c.pat];
+    opnd dres = get_def(s, c.h[2], c.idx[2], 0);
+    if (!rw_safe(c, &dres, 1)) return false;
+    opnd u[3];
+    if (!rw_var_operand(c, c.b.var[p.var_a & 15], &u[0])) return false;
+    if (!rw_var_operand(c, c.b.var[p.var_b & 15], &u[1])) return false;
+    if (!rw_var_operand(c, c.b.var[p.var_c & 15], &u[2])) return false;
+    if (!is_value(dres)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+    opnd d = value_ref(dres.pay);
+    Rec agg = rw_make(c, CL_OP_IMAD, CL_MS_NONE, &d, 1, u, 3);
+    if (!rw_redefine(c, dres, agg.h.iid)) return false;
+    rw_push(c, agg);
+    for (unsigned t = 0; t < 2; t++)
+        for (unsigned k = 0; k < c.h[t].n_defs; k++) rw_drop(c, get_def(s, c.h[t], c.idx[t], k));
+    c.rm = 7;
+    return true;
+}
+CLF bool run_rewrite(RW &c) {
+    switch (c.s->pb->p[c.pat].rewrite) {
+    case CL_RW_IADD364: return rw_iadd364(c);
+    case CL_RW_ISETP64: return rw_isetp64(c);
+    case CL_RW_LEA64: return rw_lea64(c);
+    case CL_RW_IMAD_WIDE: return rw_imad_wide(c);
+    case CL_RW_MOV64: return rw_mov64(c);
+    case CL_RW_CAST64: return rw_cast64(c);
+    case CL_RW_SHL64: return rw_shift64(c, false);
+    case CL_RW_SHR64: return rw_shift64(c, true);
+    case CL_RW_XMAD: return rw_xmad(c);
+    }
+    rw_fail(c, CL_ST_UNSUPPORTED);
+    return false;
+}
+CLF void rw_setup(RW &c, FS &s, const SelRec &m, uint32_t lo) {
+    c.s = &s; c.n = m.n; c.pat = m.pat;
+    c.nins = 0; c.esc_n = 0; c.rm = 0; c.retag = false;
+    for (unsigned t = 0; t < m.n; t++) { c.idx[t] = lo + m.pos[t]; c.h[t] = s.S.hdr[c.idx[t]]; }
+    for (unsigned t = m.n; t < 3; t++) c.idx[t] = NONE32;
+    check_tuple(s, s.pb->p[m.pat], c.idx, c.b);          /* rebuild the bindings */
+}
+
+/* _apply_patterns (patterns.py:671-707): one round over all blocks.
+ * Phase 1 matches and selects every block (matching never looks outside its
+ * block); if nothing was selected the round is over.  Phase 2 walks the
+ * blocks in order -- the escape test of block b must see the use counts left
+ * by the rewrites of blocks < b (G5) -- compacting the stream from the right
+ * end of the gap buffer to the left.                                        */
+template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table, uint32_t phase) {
+    setup_classes(s, table);
+    uint32_t nsel = 0;
+    for (uint32_t bi = 0; bi < s.nb; bi++) {
+        const uint32_t lo = s.bo[bi], n = s.bo[bi + 1] - lo;
+        if (g.rank == 0) s.blk_sel[bi] = nsel;
+        if (n == 0) continue;
+        const uint32_t nm = match_block(g, s, lo, n, table);
+        if (status(s)) return 0;
+        if (nm == 0) continue;
+        const uint32_t ns = select_block(g, s, n, nm, bi, nsel);
+        if (status(s)) return 0;
+        if (g.rank == 0) {
+            for (uint32_t m = 0; m < nm; m++) s.st_matches[s.mt[m].pat]++;
+            for (uint32_t j = 0; j < ns; j++) s.st_selected[s.sel[nsel + j].pat]++;
+        }
+        if (s.emit_matches) emit_match_events(g, s, phase << 28 | bi, nm, nsel, ns);
+        nsel += ns;
+        g.sync();
+    }
+    if (g.rank == 0) s.blk_sel[s.nb] = nsel;
+    g.sync();
+    if (nsel == 0) return 0;
+
+    build_usecount(g, s);
+    const uint32_t shift = s.cap.I - s.n;                    /* right-align the stream */
+    move_recs(g, s, shift, 0, s.n);
+    uint32_t wr = 0, total_ok = 0;
+    for (uint32_t bi = 0; bi < s.nb; bi++) {
+        const uint32_t lo = s.bo[bi] + shift, n = s.bo[bi + 1] - s.bo[bi];
+        const uint32_t j0 = s.blk_sel[bi], ns = s.blk_sel[bi + 1] - j0;
+        if (g.rank == 0) s.bo2[bi] = wr;
+        if (ns == 0) {
+            move_recs(g, s, wr, lo, n);
+            wr += n;
+            continue;
+        }
+        /* COUNT pass */
+        GFOR(g, p, n) if (p < n) { s.keep[p] = 1; s.inscnt[p] = 0; }
+        g.sync();
+        GFOR(g, j, ns) if (j < ns) {
+            RW c;
+            c.write = false; c.store = false; c.vid = c.iid = c.imm = 0; c.out = 0; c.esc = 0;
+            rw_setup(c, s, s.sel[j0 + j], lo);
+            const bool ok = run_rewrite(c);
+            Plan pl;
+            pl.ok = ok; pl.rm = (uint8_t)c.rm; pl.nins = (uint8_t)c.nins; pl.retag = c.retag;
+            pl.esc = c.esc; pl.nv = c.vid; pl.ni = c.iid; pl.nm = c.imm;
+            pl.vbase = pl.ibase = pl.mbase = 0;
+            s.plan[j0 + j] = pl;
+        }
+        g.sync();
+        if (status(s)) return 0;
+        /* exclusive scans in select order: id bases (G3) */
+        uint32_t vb = s.next_vid, ib = s.next_iid, mb = s.n_imm, okc = 0;
+        GFOR(g, j, ns) {
+            uint32_t nv = 0, ni = 0, nq = 0, ok = 0;
+            if (j < ns) { const Plan &pl = s.plan[j0 + j]; nv = pl.nv; ni = pl.ni; nq = pl.nm; ok = pl.ok; }
+            uint32_t tv, ti, tq, to;
+            const uint32_t ov = g.exscan(nv, tv), oi = g.exscan(ni, ti), oq = g.exscan(nq, tq);
+            g.exscan(ok, to);
+            if (j < ns) {
+                Plan &pl = s.plan[j0 + j];
+                pl.vbase = vb + ov; pl.ibase = ib + oi; pl.mbase = mb + oq;
+                const SelRec &m = s.sel[j0 + j];
+                if (pl.ok) {
+                    s.inscnt[m.pos[m.n - 1]] = pl.nins;                  /* anchor :689 */
+                    for (unsigned t = 0; t < m.n; t++) if (pl.rm >> t & 1) s.keep[m.pos[t]] = 0;
+                }
+            }
+            vb += tv; ib += ti; mb += tq; okc += to;
+        }
+        if (vb > s.cap.V || mb > s.cap.Q) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }
+        g.sync();
+        /* output offsets of the block */
+        uint32_t tot = 0;
+        GFOR(g, p, n) {
+            const uint32_t x = p < n ? (uint32_t)s.keep[p] + s.inscnt[p] : 0u;
+            uint32_t t;
+            const uint32_t o = g.exscan(x, t);
+            if (p < n) s.outpos[p] = tot + o;
+            tot += t;
+        }
+        if (wr + tot > lo) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }     /* gap exhausted */
+        g.sync();
+        /* WRITE pass */
+        GFOR(g, j, ns) if (j < ns) {
+            const Plan pl = s.plan[j0 + j];
+            const SelRec m = s.sel[j0 + j];
+            RW c;
+            c.write = true; c.store = pl.ok != 0;
+            c.vid = pl.vbase; c.iid = pl.ibase; c.imm = pl.mbase; c.esc = pl.esc;
+            c.out = wr + s.outpos[m.pos[m.n - 1]];
+            rw_setup(c, s, m, lo);
+            run_rewrite(c);
+            if (!pl.ok) push_event(s, phase << 28 | bi, CL_EV_REFUSED, j, m.pat, s.blk[bi].bid, 0, 0);
+        }
+        if (g.rank == 0)
+            for (uint32_t j = 0; j < ns; j++) {
+                const unsigned pat = s.sel[j0 + j].pat;
+                if (s.plan[j0 + j].ok) s.st_rewrites[pat]++; else s.st_refused[pat]++;
+            }
+        g.sync();
+        /* kept records move left; removed ones give their uses back */
+        GFOR(g, p, n) if (p < n) {
+            if (s.keep[p]) {
+                Rec r;
+                ld_rec(s, lo + p, r);
+                st_rec(s, wr + s.outpos[p] + s.inscnt[p], r);
+            } else {
+                const cl_hdr h = s.S.hdr[lo + p];
+                for_value_operands(s, h, lo + p, [&](uint32_t v) { if (v < s.cap.V) a_sub(&s.usecnt[v], 1u); });
+            }
+        }
+        g.sync();
+        wr += tot;
+        s.next_vid = vb; s.next_iid = ib; s.n_imm = mb;
+        total_ok += okc;
+    }
+    if (g.rank == 0) s.bo2[s.nb] = wr;
+    { uint32_t *t = s.bo; s.bo = s.bo2; s.bo2 = t; }
+    s.n = wr;
+    g.sync();
+    return total_ok;
+}
+
+/* ordered in-place compaction of the stream by keep[] (block offsets follow) */
+template <class G> CLF void compact_stream(const G &g, FS &s) {
+    /* new offset of every block = kept records before its old start */
+    uint32_t run = 0;
+    uint32_t bi = 0;
+    /* outpos[i] = kept before i */
+    GFOR(g, i, s.n) {
+        const uint32_t x = i < s.n ? (uint32_t)s.keep[i] : 0u;
+        uint32_t t;
+        const uint32_t o = g.exscan(x, t);
+        if (i < s.n) s.outpos[i] = run + o;
+        run += t;
+    }
+    (void)bi;
+    g.sync();
+    GFOR(g, b, s.nb + 1) if (b <= s.nb) {
+        const uint32_t old = s.bo[b];
+        s.bo2[b] = old < s.n ? s.outpos[old] : run;
+    }
+    g.sync();
+    const uint32_t chunks = (s.n + g.size - 1) / g.size;
+    for (uint32_t c = 0; c < chunks; c++) {
+        const uint32_t i = c * g.size + g.rank;
+        Rec r;
+        const bool k = i < s.n && s.keep[i];
+        uint32_t dst = 0;
+        if (k) { ld_rec(s, i, r); dst = s.outpos[i]; }
+        g.sync();
+        if (k) st_rec(s, dst, r);
+        g.sync();
+    }
+    { uint32_t *t = s.bo; s.bo = s.bo2; s.bo2 = t; }
+    s.n = run;
+}
+
+/* remove_dead_pseudo (patterns.py:771-791).  The reference removes, round by
+ * round, every pure instruction whose values have no users; the union of the
+ * rounds is the least fixpoint of "dead", which chaotic iteration reaches in
+ * any order, so dead marks and use-count decrements are applied on the fly. */
+template <class G> CLF uint32_t remove_dead_pseudo(const G &g, FS &s) {
+    build_usecount(g, s);
+    GFOR(g, i, s.n) if (i < s.n) s.keep[i] = 1;
+    g.sync();
+    uint32_t removed = 0;
+    for (;;) {
+        uint32_t mine = 0;
+        GFOR(g, i, s.n) if (i < s.n && s.keep[i]) {
+            const cl_hdr h = s.S.hdr[i];
+            if (h.op >= CL_OP__COUNT || !(s.opflags[h.op] & CL_OPF_PURE)) continue;
+            unsigned nd = 0; bool used = false;
+            for_value_defs(s, h, i, [&](uint32_t v) { nd++; used |= v < s.cap.V && *(volatile uint32_t *)&s.usecnt[v] != 0; });
+            if (!nd || used) continue;
+            s.keep[i] = 0;
+            mine++;
+            for_value_defs(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.alive[v] = 0; });
+            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_sub(&s.usecnt[v], 1u); });
+        }
+        const uint32_t dead = g.sum(mine);
+        g.sync();
+        if (!dead) break;
+        removed += dead;
+    }
+    if (removed) compact_stream(g, s);
+    return removed;
+}
+
+/* simplify_packs + _redirect_values (patterns.py:710-764)                     */
+CLD uint32_t final_of(const FS &s, uint32_t v) {
+    while (v < s.cap.V && s.redirect[v] != NONE32) v = s.redirect[v];
+    return v;
+}
+template <class G> CLF uint32_t simplify_packs(const G &g, FS &s) {
+    build_usecount(g, s);
+    GFOR(g, v, s.next_vid) if (v < s.next_vid) s.redirect[v] = NONE32;
+    g.sync();
+    uint32_t mine = 0;
+    GFOR(g, i, s.n) if (i < s.n) {
+        const cl_hdr h = s.S.hdr[i];
+        if (h.op != CL_OP_PACK64 || h.n_uses != 2) continue;
+        opnd lo = get_use(s, h, i, 0), hi = get_use(s, h, i, 1);
+        if (!is_value(lo) || !is_value(hi)) continue;
+        if ((lo.tag | hi.tag) & (CL_T_NEG | CL_T_NOT)) continue;
+        if (lo.pay >= s.cap.V || hi.pay >= s.cap.V) continue;
+        const uint32_t plo = s.defpos[lo.pay], phi = s.defpos[hi.pay];
+        if (plo == NONE32 || phi == NONE32) continue;
+        const cl_hdr dlo = s.S.hdr[plo], dhi = s.S.hdr[phi];
+        if (!(dlo.op == CL_OP_UNPACK64 && has_mod(s, dlo, CL_MB_LO) && dhi.op == CL_OP_UNPACK64 && has_mod(s, dhi, CL_MB_HI))) continue;
+        if (!dlo.n_uses || !dhi.n_uses) { fail(s, CL_ST_INDEX_ERROR); continue; }
+        opnd slo = get_use(s, dlo, plo, 0), shi = get_use(s, dhi, phi, 0);
+        if (!(is_value(slo) && is_value(shi) && slo.pay == shi.pay)) continue;
+        if (!h.n_defs) { fail(s, CL_ST_INDEX_ERROR); continue; }
+        opnd d = get_def(s, h, i, 0);
+        if (!is_value(d)) { fail(s, CL_ST_ATTRIBUTE_ERROR); continue; }
+        if (d.pay < s.cap.V) s.redirect[d.pay] = slo.pay;
+        mine++;
+    }
+    const uint32_t changed = g.sum(mine);
+    g.sync();
+    if (status(s) || !changed) return changed;
+    GFOR(g, i, s.n) if (i < s.n) {
+        const cl_hdr h = s.S.hdr[i];
+        const unsigned u0 = use0(h);
+        for (unsigned k = 0; k < h.n_uses; k++) {
+            opnd u = get_slot(s, h, i, u0 + k);
+            if (is_value(u)) { const uint32_t f = final_of(s, u.pay); if (f != u.pay) { u.pay = f; set_slot(s, h, i, u0 + k, u); } }
+            else if (kind_of(u.tag) == CL_K_MEMREF) {
+                cl_memref &m = s.mem[u.pay];
+                if (kind_of(m.base_tag) == CL_K_VALUE) m.base_pay = final_of(s, m.base_pay);
+                if (kind_of(m.ureg_tag) == CL_K_VALUE) m.ureg_pay = final_of(s, m.ureg_pay);
+            }
+        }
+        if (has_guard(h)) { opnd gd = get_slot(s, h, i, 0); if (is_value(gd)) { gd.pay = final_of(s, gd.pay); set_slot(s, h, i, 0, gd); } }
+    }
+    GFOR(g, b, s.nb) if (b < s.nb)
+        for (int k = 0; k < 2; k++)
+            if (kind_of(s.blk[b].term_tag[k]) == CL_K_VALUE) s.blk[b].term_pay[k] = final_of(s, s.blk[b].term_pay[k]);
+    g.sync();
+    remove_dead_pseudo(g, s);
+    return changed;
+}
+
+/* apply_aggregations (patterns.py:794-802)                                    */
+template <class G> CLF void apply_aggregations(const G &g, FS &s) {
+    for (uint32_t round = 0; round < s.max_rounds; round++) {
+        uint32_t n = apply_patterns(g, s, 0, 2 + round);
+        if (status(s)) return;
+        n += simplify_packs(g, s);
+        if (status(s)) return;
+        if (!n) break;
+    }
+    remove_dead_pseudo(g, s);
+}
+/* normalize_xmad (patterns.py:805-810)                                        */
+template <class G> CLF void normalize_xmad(const G &g, FS &s) {
+    if (s.arch != CL_ARCH_SM52) return;
+    apply_patterns(g, s, 1, 0);
+    if (status(s)) return;
+    remove_dead_pseudo(g, s);
+}
+
+/* tag_cuda_objects (patterns.py:895-916)                                      */
+template <class G> CLF void tag_cuda_objects(const G &g, FS &s) {
+    GFOR(g, i, s.n) if (i < s.n) {
+        cl_hdr h = s.S.hdr[i];
+        unsigned kind = 0, use = 7;
+        if (h.op == CL_OP_BAR && has_mod(s, h, CL_MB_SYNC)) {
+            kind = 1;
+            for (unsigned k = 0; k < h.n_uses && k < 7; k++) if (is_imm(get_use(s, h, i, k))) use = k;
+        } else if (h.op == CL_OP_WARPSYNC) {
+            for (unsigned k = 0; k < h.n_uses && k < 7; k++) {
+                opnd u = get_use(s, h, i, k);
+                if (is_imm(u)) { if (s.imm[u.pay].bits == 0xFFFFFFFFull) { kind = 2; use = k; } break; }
+            }
+        } else if (h.op == CL_OP_SHFL)
+            kind = 3;
+        if (kind) {
+            h.flags &= (uint8_t)~(CL_IF_OBJ_MASK | CL_IF_OBJUSE_MASK);
+            h.flags |= (uint8_t)(kind << CL_IF_OBJ_SHIFT | use << CL_IF_OBJUSE_SHIFT);
+            s.S.hdr[i].flags = h.flags;
+        }
+    }
+    g.sync();
+}
+
+/* ------------------------------------------------------- reciprocal chains */
+/* normalize_reciprocal (patterns.py:817-888).  The reference is sequential
+ * over chains and rebuilds def-use after each one, so chains see each other's
+ * bitcasts.  Here: the group builds use lists once (CSR by value, unordered),
+ * then lane 0 walks the chains in stream order on a *mutable* view --
+ *   users(v) = entries of CSR(root(v)) whose record currently references v
+ *              + the inserted bitcasts chained from xhead[v]
+ * where root(v) is the original value a renamed value (.bits / .f) took its
+ * sites from -- and the group materialises the inserted records at the end. */
+CLD bool rec_references(const FS &s, uint32_t i, uint32_t vid) {
+    const cl_hdr h = s.S.hdr[i];
+    bool r = false;
+    for_value_operands(s, h, i, [&](uint32_t v) { r |= v == vid; });
+    return r;
+}
+CLD uint32_t count_sites(const FS &s, uint32_t i, uint32_t vid) {
+    const cl_hdr h = s.S.hdr[i];
+    uint32_t r = 0;
+    for_value_operands(s, h, i, [&](uint32_t v) { r += v == vid; });
+    return r;
+}
+/* iterate users(v): fn(is_extra, index) returns true to stop; a record that
+ * references v through several slots may be visited more than once           */
+template <class F> CLD bool for_users(const FS &s, uint32_t v, F fn) {
+    const uint32_t r = s.root[v];
+    for (uint32_t e = s.redirect[r]; e < s.redirect[r + 1]; e++) {
+        const uint32_t p = s.site[e];
+        if (rec_references(s, p, v) && fn(false, p)) return true;
+    }
+    for (uint32_t x = s.xhead[v]; x != NONE32; x = s.xr[x].next)
+        if (fn(true, x)) return true;
+    return false;
+}
+/* _reaches_f2i (patterns.py:850-860), depth unrolled at compile time         */
+template <int D> struct Reach {
+    CLM bool run(const FS &s, bool extra, uint32_t idx) {
+        const uint16_t op = extra ? s.xr[idx].r.h.op : s.S.hdr[idx].op;
+        if (op == CL_OP_F2I) return true;
+        uint32_t defs[8]; unsigned nd = 0;
+        if (extra) defs[nd++] = s.xr[idx].r.pay[0];
+        else {
+            const cl_hdr h = s.S.hdr[idx];
+            for_value_defs(s, h, idx, [&](uint32_t v) { if (nd < 8) defs[nd++] = v; });
+        }
+        for (unsigned k = 0; k < nd; k++) {
+            const uint32_t v = defs[k];
+            if (v >= s.cap.V) continue;
+            if (for_users(s, v, [&](bool ex, uint32_t u) { return Reach<D - 1>::run(s, ex, u); })) return true;
+        }
+        return false;
+    }
+};
+template <> struct Reach<0> {
+    CLM bool run(const FS &s, bool extra, uint32_t idx) {
+        return (extra ? s.xr[idx].r.h.op : s.S.hdr[idx].op) == CL_OP_F2I;
+    }
+};
+CLD uint32_t block_of(const FS &s, uint32_t pos) {
+    uint32_t lo = 0, hi = s.nb;                 /* last b with bo[b] <= pos and non-empty range */
+    while (lo + 1 < hi) { const uint32_t mid = (lo + hi) / 2; if (s.bo[mid] <= pos) lo = mid; else hi = mid; }
+    return lo;
+}
+
+template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
+    /* cheap exit: no MUFU.RCP at all */
+    bool mine = false;
+    GFOR(g, i, s.n) if (i < s.n) { const cl_hdr h = s.S.hdr[i]; mine |= h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP); }
+    if (!g.any(mine)) return;
+    build_usecount(g, s);
+    /* CSR offsets in redirect[0 .. next_vid] */
+    const uint32_t nv = s.next_vid;
+    uint32_t run = 0;
+    GFOR(g, v, nv + 1) {
+        const uint32_t x = v < nv ? s.usecnt[v] : 0u;
+        uint32_t t;
+        const uint32_t o = g.exscan(x, t);
+        if (v <= nv) s.redirect[v] = run + o;
+        run += t;
+    }
+    if (run > s.cap.U || nv + 1 > s.cap.V) { fail(s, CL_ST_CAPACITY); g.sync(); return; }
+    g.sync();
+    GFOR(g, v, s.cap.V) if (v < s.cap.V) { s.xhead[v] = NONE32; s.root[v] = v; if (v < nv) s.usecnt[v] = s.redirect[v]; }
+    GFOR(g, i, s.n) if (i < s.n) { s.keep[i] = 0; s.inscnt[i] = 0; }       /* before / after counts */
+    g.sync();
+    GFOR(g, i, s.n) if (i < s.n) {
+        const cl_hdr h = s.S.hdr[i];
+        for_value_operands(s, h, i, [&](uint32_t v) { if (v < nv) s.site[a_add(&s.usecnt[v], 1u)] = i; });
+    }
+    g.sync();
+    uint32_t nx = 0, n_events = 0, vid = s.next_vid, iid = s.next_iid;
+    if (g.rank == 0) {
+        for (uint32_t bi = 0; bi < s.nb && !status(s); bi++) {
+            for (uint32_t i = s.bo[bi]; i < s.bo[bi + 1] && !status(s); i++) {
+                const cl_hdr h = s.S.hdr[i];
+                if (h.op != CL_OP_MUFU || !has_mod(s, h, CL_MB_RCP) || !h.n_uses) continue;
+                opnd src = get_use(s, h, i, 0);
+                if (!is_value(src) || src.pay >= s.cap.V) continue;
+                /* du.def_inst of the source: original values only (bitcast results never feed a MUFU's I2F test) */
+                {
+                    uint32_t dp = src.pay < nv ? s.defpos[src.pay] : NONE32;
+                    bool is_i2f = dp != NONE32 && s.S.hdr[dp].op == CL_OP_I2F;
+                    if (!is_i2f) continue;
+                }
+                if (!h.n_defs) { fail(s, CL_ST_INDEX_ERROR); break; }
+                opnd rcp = get_def(s, h, i, 0);
+                if (!is_value(rcp)) { fail(s, CL_ST_ATTRIBUTE_ERROR); break; }
+                /* adds = user sites of rcp that are IADD/IADD3 with an Imm use, stream order :835-837.
+                 * The list is fixed before the first chain of this MUFU is rewritten.          */
+                uint32_t *adds = s.cand, *uniq = s.sel_at;          /* scratch: [I] each */
+                uint32_t n_adds = 0, n_uniq = 0;
+                for_users(s, rcp.pay, [&](bool ex, uint32_t u) {
+                    if (ex) return false;
+                    const cl_hdr ah = s.S.hdr[u];
+                    if (ah.op != CL_OP_IADD && ah.op != CL_OP_IADD3) return false;
+                    bool any_imm = false;
+                    for (unsigned k = 0; k < ah.n_uses; k++) any_imm |= is_imm(get_use(s, ah, u, k));
+                    if (!any_imm) return false;
+                    /* the CSR lists are unordered: insertion-sort the (few) distinct adds */
+                    uint32_t j = n_uniq;
+                    for (uint32_t q = 0; q < n_uniq; q++) if (uniq[q] == u) return false;
+                    if (n_uniq >= s.cap.I) return false;
+                    while (j > 0 && uniq[j - 1] > u) { uniq[j] = uniq[j - 1]; j--; }
+                    uniq[j] = u;
+                    n_uniq++;
+                    return false;
+                });
+                for (uint32_t q = 0; q < n_uniq; q++) {              /* one entry per use site */
+                    const uint32_t mult = count_sites(s, uniq[q], rcp.pay);
+                    for (uint32_t m = 0; m < mult && n_adds < s.cap.I; m++) adds[n_adds++] = uniq[q];
+                }
+                for (uint32_t ai = 0; ai < n_adds && !status(s); ai++) {
+                    const uint32_t a = adds[ai];
+                    if (!Reach<3>::run(s, false, a)) continue;
+                    if (nx + 2 > s.cap.X || vid + 2 > s.cap.V) { fail(s, CL_ST_CAPACITY); break; }
+                    const cl_hdr ah = s.S.hdr[a];
+                    /* _insert_reciprocal_bitcasts :863-888 */
+                    const uint32_t vi = vid++;
+                    s.alive[vi] = 1; s.origin[vi] = CL_ORG_BITS | rcp.pay; s.root[vi] = s.root[rcp.pay]; s.xhead[vi] = NONE32;
+                    XRec &ci = s.xr[nx];
+                    memset(&ci.r, 0, sizeof ci.r);
+                    ci.r.h.iid = iid++; ci.r.h.op = CL_OP_BITCAST; ci.r.h.modset = CL_MS_F2I; ci.r.h.n_defs = 1; ci.r.h.n_uses = 1;
+                    ci.r.tag[0] = CL_K_VALUE; ci.r.pay[0] = vi; ci.r.tag[1] = CL_K_VALUE; ci.r.pay[1] = rcp.pay;
+                    s.def_iid[vi] = (int32_t)ci.r.h.iid;
+                    ci.anchor = a; ci.after = 0; ci.order = s.keep[a]++;
+                    ci.next = s.xhead[rcp.pay]; s.xhead[rcp.pay] = nx;
+                    nx++;
+                    for (unsigned k = 0; k < ah.n_uses; k++) {
+                        opnd x = get_use(s, ah, a, k);
+                        if (is_value(x) && x.pay == rcp.pay) { x.pay = vi; set_slot(s, ah, a, use0(ah) + k, x); }
+                    }
+                    if (!ah.n_defs) { fail(s, CL_ST_INDEX_ERROR); break; }
+                    opnd add_ref = get_def(s, ah, a, 0);
+                    if (!is_value(add_ref)) { fail(s, CL_ST_ATTRIBUTE_ERROR); break; }
+                    const uint32_t vf = vid++;
+                    s.alive[vf] = 1; s.origin[vf] = CL_ORG_F | add_ref.pay; s.root[vf] = s.root[add_ref.pay]; s.xhead[vf] = NONE32;
+                    const uint32_t co_i = nx;
+                    XRec &co = s.xr[nx];
+                    memset(&co.r, 0, sizeof co.r);
+                    co.r.h.iid = iid++; co.r.h.op = CL_OP_BITCAST; co.r.h.modset = CL_MS_I2F; co.r.h.n_defs = 1; co.r.h.n_uses = 1;
+                    co.r.tag[0] = CL_K_VALUE; co.r.pay[0] = vf; co.r.tag[1] = CL_K_VALUE; co.r.pay[1] = add_ref.pay;
+                    s.def_iid[vf] = (int32_t)co.r.h.iid;
+                    co.anchor = a; co.after = 1; co.order = s.inscnt[a]++;
+                    nx++;
+                    /* every current user of add_def (top-level uses only) now reads vf :878-883 */
+                    const uint32_t r0 = s.root[add_ref.pay];
+                    for (uint32_t e = s.redirect[r0]; e < s.redirect[r0 + 1]; e++) {
+                        const uint32_t p = s.site[e];
+                        const cl_hdr uh = s.S.hdr[p];
+                        for (unsigned k = 0; k < uh.n_uses; k++) {
+                            opnd x = get_use(s, uh, p, k);
+                            if (is_value(x) && x.pay == add_ref.pay) { x.pay = vf; set_slot(s, uh, p, use0(uh) + k, x); }
+                        }
+                    }
+                    /* earlier bitcasts reading add_def move over too (the add was rewritten twice) */
+                    for (uint32_t x = s.xhead[add_ref.pay]; x != NONE32;) {
+                        const uint32_t nxt = s.xr[x].next;
+                        s.xr[x].r.pay[1] = vf;
+                        s.xr[x].next = s.xhead[vf]; s.xhead[vf] = x;
+                        x = nxt;
+                    }
+                    s.xhead[add_ref.pay] = co_i;
+                    s.xr[co_i].next = NONE32;
+                    if (block_of(s, a) != bi) { fail(s, CL_ST_KEY_ERROR); break; }            /* pos[add.iid] :886 */
+                    push_event(s, 1u << 28, CL_EV_BOUNDARY, n_events++, rcp.pay, ah.iid, 0, 0);
+                }
+            }
+        }
+    }
+    g.sync();
+    nx = g.bcast0(nx); vid = g.bcast0(vid); iid = g.bcast0(iid);
+    if (status(s)) return;
+    s.next_vid = vid; s.next_iid = iid;
+    if (nx == 0) return;
+    if (s.n + nx > s.cap.I) { fail(s, CL_ST_CAPACITY); g.sync(); return; }
+    /* materialise: right-align, then expand leftwards in order */
+    const uint32_t n = s.n, shift = s.cap.I - n;
+    uint32_t run2 = 0;
+    GFOR(g, i, n) {
+        const uint32_t x = i < n ? 1u + s.keep[i] + s.inscnt[i] : 0u;
+        uint32_t t;
+        const uint32_t o = g.exscan(x, t);
+        if (i < n) s.outpos[i] = run2 + o;
+        run2 += t;
+    }
+    g.sync();
+    GFOR(g, b, s.nb + 1) if (b <= s.nb) { const uint32_t old = s.bo[b]; s.bo2[b] = old < n ? s.outpos[old] : run2; }
+    move_recs(g, s, shift, 0, n);
+    /* outpos is increasing and outpos[i] <= i + inserted-before, so a chunked forward move is safe:
+     * destination of record i never passes the source of record i (shift >= nx).            */
+    const uint32_t chunks = (n + g.size - 1) / g.size;
+    for (uint32_t c = 0; c < chunks; c++) {
+        const uint32_t i = c * g.size + g.rank;
+        Rec r;
+        if (i < n) ld_rec(s, shift + i, r);
+        g.sync();
+        if (i < n) st_rec(s, s.outpos[i] + s.keep[i], r);
+        g.sync();
+    }
+    GFOR(g, x, nx) if (x < nx) {
+        const XRec &e = s.xr[x];
+        const uint32_t base = s.outpos[e.anchor];
+        const uint32_t at = e.after ? base + s.keep[e.anchor] + 1u + (s.inscnt[e.anchor] - 1u - e.order) : base + e.order;
+        st_rec(s, at, e.r);
+    }
+    { uint32_t *t = s.bo; s.bo = s.bo2; s.bo2 = t; }
+    s.n = run2;
+    g.sync();
+}
+
+/* the four calls of pipeline.py:165-169 on one resident function             */
+template <class G> CLF void run_postssa(const G &g, FS &s) {
+    if ((s.passes & CL_PASS_XMAD) && !status(s)) normalize_xmad(g, s);
+    if ((s.passes & CL_PASS_RECIPROCAL) && !status(s)) normalize_reciprocal(g, s);
+    if ((s.passes & CL_PASS_AGGREGATE) && !status(s)) apply_aggregations(g, s);
+    if ((s.passes & CL_PASS_TAG) && !status(s)) tag_cuda_objects(g, s);
+}
+/* match_patterns + select_matches only                                       */
+template <class G> CLF void run_match_only(const G &g, FS &s) {
+    const unsigned table = (s.passes & CL_PASS_MATCH_XMAD) ? 1 : 0;
+    setup_classes(s, table);
+    for (uint32_t bi = 0; bi < s.nb; bi++) {
+        const uint32_t lo = s.bo[bi], n = s.bo[bi + 1] - lo;
+        if (n == 0) continue;
+        const uint32_t nm = match_block(g, s, lo, n, table);
+        if (status(s)) return;
+        if (nm == 0) continue;
+        const uint32_t ns = select_block(g, s, n, nm, bi, 0);
+        if (status(s)) return;
+        if (g.rank == 0) {
+            for (uint32_t m = 0; m < nm; m++) s.st_matches[s.mt[m].pat]++;
+            for (uint32_t j = 0; j < ns; j++) s.st_selected[s.sel[j].pat]++;
+        }
+        emit_match_events(g, s, bi, nm, 0, ns);
+        g.sync();
+    }
+}
+
+} /* namespace clk */

@@ -1,0 +1,110 @@
+"""Shared test plumbing: fixture loading, engines, state comparison.
+
+Only tests (and bench.py's cpu_baseline leg / __graft_entry__.smoke) touch
+oracle/; the package itself never does.
+"""
+from __future__ import annotations
+
+import copy
+import gzip
+import pickle
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from paper_2604_27486_b200 import ir, soa
+from paper_2604_27486_b200.capi import Engine
+from paper_2604_27486_b200.patterns import pattern_list
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLDEN = ROOT / "tests" / "golden"
+ORACLE_LIB = ROOT / "oracle" / "liboracle.so"
+SIM_LIB = ROOT / "tests" / "sim" / "libculifter_sim.so"
+CSRC = ROOT / "paper_2604_27486_b200" / "csrc"
+
+FIXTURES = sorted(p.name[:-len(".pkl.gz")] for p in GOLDEN.glob("*.pkl.gz"))
+STATUS_ERROR = {2: "AttributeError", 3: "AssertionError", 4: "KeyError", 6: "IndexError"}
+
+
+def load_fixture(name):
+    with gzip.open(GOLDEN / f"{name}.pkl.gz", "rb") as fh:
+        return pickle.load(fh)
+
+
+def build_oracle():
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+    return ORACLE_LIB
+
+
+def build_sim():
+    """One-lane CPU build of the device code (tests/sim): logic checks without a GPU."""
+    srcs = [CSRC / "culifter.cu", CSRC / "core.cuh", ROOT / "include" / "culifter.h"]
+    if not SIM_LIB.exists() or any(s.stat().st_mtime > SIM_LIB.stat().st_mtime for s in srcs):
+        SIM_LIB.parent.mkdir(parents=True, exist_ok=True)
+        subprocess.run(["g++", "-x", "c++", "-std=c++17", "-O1", "-g", "-DCL_SIM", "-fPIC", "-shared",
+                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu")], check=True)
+    return SIM_LIB
+
+
+def oracle_engine():
+    return Engine(build_oracle())
+
+
+def sim_engine():
+    return Engine(build_sim())
+
+
+def cuda_engine():
+    return Engine()          # the product library; raises without GPU / without the .so
+
+
+def state_of(fn):
+    return {
+        "dump": ir.dump(fn),
+        "diagnostics": list(fn.diagnostics),
+        "boundaries": list(fn.meta.get("pattern_boundaries", [])),
+        "cuda_objects": [tuple(t) for t in fn.meta.get("cuda_objects", [])],
+        "next": (fn._next_vid, fn._next_iid),
+        "values": {vid: (v.origin, v.def_iid) for vid, v in sorted(fn.values.items())},
+    }
+
+
+def run_postssa(engine, functions, passes=15, **kw):
+    """encode -> device -> decode in place; returns the output corpus."""
+    corpus = soa.encode(functions)
+    engine.upload(corpus)
+    engine.run_postssa(passes, **kw)
+    out = engine.download()
+    soa.apply(out, functions, patterns=pattern_list(), tagged=bool(passes & 8))
+    return corpus, out
+
+
+def check_fixture(engine, name):
+    fix = load_fixture(name)
+    fns = copy.deepcopy(fix["functions"])
+    _, out = run_postssa(engine, fns, fix["passes"])
+    problems = []
+    for f, (fn, want) in enumerate(zip(fns, fix["expect"])):
+        st = int(out.func["status"][f])
+        if "error" in want:
+            if STATUS_ERROR.get(st) != want["error"]:
+                problems.append(f"{name}/{fn.name}: status {st}, reference raises {want['error']}")
+            continue
+        if st != 0:
+            problems.append(f"{name}/{fn.name}: status {st}, reference succeeds")
+            continue
+        got = state_of(fn)
+        for key in want:
+            if got[key] != want[key]:
+                problems.append(f"{name}/{fn.name}: {key} differs\n--- reference\n{want[key]}\n--- got\n{got[key]}")
+                break
+    return problems
+
+
+def corpora_equal(a: soa.Corpus, b: soa.Corpus):
+    """Bit-exact equality of two result corpora, events included."""
+    diffs = a.equal(b)
+    if a.events.shape != b.events.shape or not np.array_equal(a.events, b.events):
+        diffs.append(f"events differ ({len(a.events)} vs {len(b.events)})")
+    return diffs

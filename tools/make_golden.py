@@ -1,0 +1,97 @@
+"""Generate the travelling parity fixtures under tests/golden/ (in-container
+only: needs the reference at /root/reference).
+
+Each fixture is a gzip pickle of
+    {"name", "passes", "functions": [paper_2604_27486_b200.ir.LiftedFunction ...],
+     "expect": [state dict | {"error": "KeyError"} ...]}
+where `functions` are SSA-phase inputs produced by the reference's own front
+half and `expect` is what the reference's own passes
+(normalize_xmad / normalize_reciprocal / apply_aggregations / tag_cuda_objects,
+pipeline.py:165-169) make of them: dump() text, diagnostics, pattern
+boundaries, CUDA-object tags, id counters and the value table.
+"""
+import gzip, pickle, sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import refharness as R
+import gen_sass
+from paper_2604_27486_b200 import ir
+
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+
+SNIPPETS = {  # the shapes of the reference's own unit tests (tests/test_patterns.py)
+    "interleaved_pairs": ("sm90", """.text.k:
+IADD3 R4, P0, R0, R2, RZ
+IADD3 R8, P1, R10, R12, RZ
+IADD3.X R5, R1, R3, RZ, P0, !PT
+IADD3.X R9, R11, R13, RZ, P1, !PT
+EXIT
+"""),
+    "inconsistent_carry": ("sm90", """.text.k:
+IADD3 R4, P0, R0, R2, RZ
+IADD3.X R5, R1, R3, RZ, P1, !PT
+EXIT
+"""),
+    "carry_escape": ("sm90", """.text.k:
+IADD3 R4, P0, R0, R2, RZ
+IADD3.X R5, R1, R3, RZ, P0, !PT
+SEL R6, 0x1, RZ, P0
+STG.E.64 [R10], R4
+STG.E [R12], R6
+EXIT
+"""),
+    "fadd_only": ("sm75", """.text.k:
+FADD R0, R1, R2
+FADD R3, R0, R2
+EXIT
+"""),
+    "xmad_on_sm90": ("sm90", """.text.k:
+XMAD.MRG R2, R0, R0.H1, RZ
+XMAD R3, R0, R2, RZ
+XMAD.PSL.CBCC R4, R0.H1, R3, R1
+EXIT
+"""),
+}
+
+
+def expected(fns, passes):
+    out = []
+    for fn in fns:
+        ref = R.clone(fn)
+        err = R.run_postssa(ref, xmad=bool(passes & 1), recip=bool(passes & 2),
+                            aggregate=bool(passes & 4), tag=bool(passes & 8))
+        out.append({"error": type(err).__name__} if err is not None else R.state_of(ref))
+    return out
+
+
+def write(name, fns, passes=15):
+    fix = {"name": name, "passes": passes, "functions": [ir.convert(f) for f in fns],
+           "expect": expected(fns, passes)}
+    path = OUT / f"{name}.pkl.gz"
+    with gzip.open(path, "wb", compresslevel=9) as fh:
+        pickle.dump(fix, fh, protocol=4)
+    n = sum(len(b.instructions) for f in fns for b in f.blocks.values())
+    print(f"{path.name}: {len(fns)} functions, {n} records, {path.stat().st_size} bytes")
+
+
+def main():
+    OUT.mkdir(parents=True, exist_ok=True)
+    fns = []
+    for f in R.corpus_files():
+        fns += R.ssa_from_path(f)
+    write("bundled", fns)
+    write("bundled_noagg", [f for p in R.corpus_files() for f in R.ssa_from_path(p)], passes=11)
+    sn = []
+    for name, (arch, text) in SNIPPETS.items():
+        for f in R.ssa_functions(text, arch):
+            f.name = name
+            sn.append(f)
+    write("snippets", sn)
+    for kind, seed, n in (("sm90", 11, 40), ("sm52", 12, 40), ("sm75", 13, 30), ("long", 14, 3)):
+        arch, text = gen_sass.gen_corpus(seed, kind, n, near_miss=0.15)
+        write(f"synth_{kind}", R.ssa_functions(text, arch))
+
+
+if __name__ == "__main__":
+    main()
