@@ -148,7 +148,7 @@ template <int NW> struct Grp {
 
 /* ------------------------------------------------------------ data model */
 struct opnd { uint16_t tag; uint32_t pay; };
-struct Rec { cl_hdr h; uint16_t tag[8]; uint32_t pay[8]; };
+struct alignas(16) Rec { cl_hdr h; uint16_t tag[8]; uint32_t pay[8]; };
 struct Planes { cl_hdr *hdr; uint16_t *tag; uint32_t *pay; };
 
 struct okey { uint32_t cls; unsigned long long v; };
