@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- lifted SASS instructions / second of the normalisation +
+pattern-aggregation path (BASELINE.json metric) on N B200s.
+
+A "step" is one pass of the whole post-SSA stage (normalize_xmad,
+normalize_reciprocal, apply_aggregations, tag_cuda_objects) over this rank's
+shard of the synthetic mixed-architecture corpus (BASELINE.json configs[4]:
+40 % sm90 / 40 % sm75 / 20 % sm52 kernels plus long-block kernels).  The
+corpus is fixed (strong scaling): kernels are partitioned across ranks by
+basic-block count, no data crosses ranks, and each step ends with an NCCL
+allgather of the per-pattern match counters.
+
+  value        device-resident: input already in HBM, CUDA-event time of the
+               stage (max over ranks); inputs are far larger than L2.
+  e2e          through the C ABI with pinned HOST buffers: cl_upload (H2D) +
+               cl_run_postssa + cl_download (device densify + D2H) per step.
+  roofline     algorithmic bytes / kernel time vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline the oracle (C port of the reference) on this box's host cores,
+               bounded sample of the same corpus.
+
+`--impl reference` times that CPU port alone (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2604_27486_b200 import synth  # noqa: E402
+from paper_2604_27486_b200.soa import Corpus  # noqa: E402
+
+METRIC = "lifted SASS instructions/sec"
+UNIT = "inst/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="mixed", choices=["mixed", "sm90", "sm52", "sm75", "long"])
+    ap.add_argument("--insts", type=float, default=float(os.environ.get("CL_BENCH_INSTS", 100e6)),
+                    help="SASS instructions in the whole corpus (all ranks)")
+    ap.add_argument("--seed", type=int, default=100)
+    ap.add_argument("--cpu-sample", type=float, default=1.5e6, help="SASS instructions of the CPU-baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- corpus
+def plan_shards(kind, n_sass, seed, n_shards):
+    """Kernel picks of the whole corpus (cheap: indices only) and their
+    partition by basic-block count (synth.shard_by_blocks rule)."""
+    rng = np.random.default_rng(seed)
+    shares = synth.MIXED if kind == "mixed" else ((kind, 1.0),)
+    pools = {k: synth.pool(k) for k, _ in shares}
+    mean = sum(sh * float(pools[k].n_sass.mean()) for k, sh in shares)
+    n_kernels = max(n_shards, int(round(n_sass / mean)))
+    kinds = [k for k, _ in shares]
+    kid = rng.choice(len(kinds), n_kernels, p=np.array([sh for _, sh in shares]) / sum(sh for _, sh in shares))
+    pick = np.zeros(n_kernels, np.int64)
+    nb = np.zeros(n_kernels, np.int64)
+    ns = np.zeros(n_kernels, np.int64)
+    for i, k in enumerate(kinds):
+        m = kid == i
+        p = pools[k]
+        pick[m] = rng.integers(0, p.corpus.n_funcs, int(m.sum()))
+        nb[m] = np.diff(p.corpus.func_blk_off.astype(np.int64))[pick[m]]
+        ns[m] = p.n_sass[pick[m]]
+    order = np.argsort(-nb, kind="stable")
+    pos = np.arange(n_kernels)
+    cyc = pos % (2 * n_shards)
+    shard = np.empty(n_kernels, np.int64)
+    shard[order] = np.where(cyc < n_shards, cyc, 2 * n_shards - 1 - cyc)
+    return kinds, pools, kid, pick, ns, nb, shard
+
+
+def materialize(kinds, pools, kid, pick, sel):
+    """SoA corpus of kernels `sel` (indices into the plan), in plan order."""
+    parts, where = [], []
+    for i, k in enumerate(kinds):
+        idx = sel[kid[sel] == i]
+        if len(idx) == 0:
+            continue
+        parts.append(synth.take_functions(pools[k].corpus, pick[idx]))
+        where.append(idx)
+    if len(parts) == 1:
+        return parts[0]
+    corpus = synth.concat(parts)
+    order = np.argsort(np.concatenate(where), kind="stable")       # back to plan order: archs interleaved
+    return synth.take_functions(corpus, order)
+
+
+def pinned_like(corpus: Corpus):
+    """Copy of the corpus whose arrays live in pinned host memory."""
+    import torch
+    out = {}
+    for name in Corpus.ARRAYS:
+        a = np.ascontiguousarray(getattr(corpus, name))
+        t = torch.empty(max(a.nbytes, 16), dtype=torch.uint8, pin_memory=True)
+        v = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+        v[...] = a
+        out[name] = v
+        out.setdefault("_keep", []).append(t)
+    keep = out.pop("_keep")
+    c = Corpus(**out)
+    c._pinned = keep
+    return c
+
+
+# ------------------------------------------------------------- measurement
+class ClockSampler:
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.rows, self.proc, self.index = [], None, index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(c_in: Corpus, n_out, n_selected):
+    """one read of the stage input, one write of the stage output."""
+    return 64 * (c_in.n_insts + n_out) + 4 * (2 * c_in.n_blocks + 2 * c_in.n_funcs) + 16 * n_selected
+
+
+def cpu_leg(corpus: Corpus, n_sass, threads, steps=1, warmup=0):
+    """The oracle (C port of the reference path) on the host cores."""
+    from paper_2604_27486_b200.capi import Engine
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+    eng = Engine(ROOT / "oracle" / "liboracle.so")
+    eng.set_threads(threads)
+    eng.upload(corpus)
+    times = []
+    for i in range(warmup + steps):
+        eng.run_postssa()
+        if i >= warmup:
+            times.append(eng.last_run_ms() / 1e3)
+    return n_sass * len(times) / sum(times), float(np.mean(times))
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    n_total = int(args.insts)
+    threads = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        sample_n = int(min(n_total, args.cpu_sample))
+        kinds, pools, kid, pick, ns, nb, shard = plan_shards(args.workload, sample_n, args.seed, 1)
+        corpus = materialize(kinds, pools, kid, pick, np.arange(len(kid)))
+        n_sass = int(ns.sum())
+        value, sec = cpu_leg(corpus, n_sass, threads, args.steps, args.warmup)
+        sample = f"{n_sass} SASS instructions ({corpus.n_insts} SSA records, {corpus.n_funcs} kernels) of the {args.workload} corpus per step"
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}-{n_total / 1e6:g}M (BASELINE.json configs[4]), CPU sample", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0,
+        }))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2604_27486_b200.capi import Engine
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t0 = time.time()
+    kinds, pools, kid, pick, ns, nb, shard = plan_shards(args.workload, n_total, args.seed, world)
+    mine = np.nonzero(shard == rank)[0]
+    corpus = materialize(kinds, pools, kid, pick, mine)
+    n_sass_rank = int(ns[mine].sum())
+    n_sass_all = int(ns.sum())
+    t_gen = time.time() - t0
+
+    eng = Engine(device=local)
+    eng.upload(corpus)
+    counts = torch.zeros(68, dtype=torch.int64, device="cuda")
+    gathered = [torch.zeros_like(counts) for _ in range(world)] if world > 1 else None
+
+    class _Raw:           # device counters of the library as a CUDA array (no host copy)
+        def __init__(self, ptr):
+            self.__cuda_array_interface__ = {"shape": (68,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+    lib_counts = torch.as_tensor(_Raw(eng.device_counts_ptr()), device="cuda")
+
+    def step():
+        eng.run_postssa()
+        if world > 1:                      # the only inter-GPU traffic: match counters
+            counts.copy_(lib_counts)
+            dist.all_gather(gathered, counts)
+        return eng.last_run_ms()
+
+    def fence():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    fence()
+    dev_ms = []
+    with ClockSampler(local) as clocks:
+        t1 = time.perf_counter()
+        for _ in range(args.steps):
+            dev_ms.append(step())
+        fence()
+        wall = time.perf_counter() - t1
+    st = eng.stats()
+    n_out = int(st["n_inst_out"])
+    n_sel = int(st["selected"].sum())
+    # max over ranks of the device time of the K steps
+    t_dev = torch.tensor([sum(dev_ms) / 1e3, wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    t_dev_s, t_wall_s = (float(x) for x in t_dev.cpu())
+    value = n_sass_all * args.steps / t_dev_s
+
+    bytes_per_step = algorithmic_bytes(corpus, n_out, n_sel)
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_per_step / (np.mean(dev_ms) / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                "kernel": "k_postssa_warp + k_postssa_cta (the whole stage, rank 0)",
+                "algorithmic_bytes_per_launch": bytes_per_step,
+                "bytes_per_sass_inst": bytes_per_step / max(n_sass_rank, 1)}
+
+    # end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = pinned_like(corpus)
+        h2d = host_in.nbytes()
+        eng.upload(host_in); eng.run_postssa(); out = eng.download()       # sizes the pinned result buffers
+        d2h = out.nbytes() + out.events.nbytes
+        host_out = pinned_like(out)
+        ev_out = np.zeros(len(out.events) + 1024, out.events.dtype)
+        del out
+        import ctypes as C
+        from paper_2604_27486_b200 import capi
+
+        def e2e_step():
+            eng.upload(host_in)
+            eng.run_postssa()
+            sizes = (C.c_uint64 * 6)()
+            eng._check(eng.lib.cl_out_sizes(eng._ctx, sizes))
+            stc = capi._struct_of(host_out, eng._keep[1])
+            eng._check(eng.lib.cl_download(eng._ctx, C.byref(stc), capi._ptr(ev_out)))
+
+        for _ in range(max(1, args.warmup - 1)):
+            e2e_step()
+        fence()
+        t2 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        fence()
+        te = torch.tensor([time.perf_counter() - t2], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_sass_all * args.steps / float(te.cpu()[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te.cpu()[0]) / args.steps * 1e3,
+               "path": "cl_upload (pinned H2D) + cl_run_postssa + cl_download (device densify + pinned D2H)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu and world == 1:
+        sample_n = int(min(n_total, args.cpu_sample))
+        k2, p2, kid2, pick2, ns2, _, _ = plan_shards(args.workload, sample_n, args.seed, 1)
+        sample_c = materialize(k2, p2, kid2, pick2, np.arange(len(kid2)))
+        v, sec = cpu_leg(sample_c, int(ns2.sum()), threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{int(ns2.sum())} SASS instructions ({sample_c.n_insts} records) of the same corpus, {sec:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_dev_s / args.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}-{n_sass_all / 1e6:.1f}M SASS instructions (BASELINE.json configs[4]: "
+                                   f"40% sm90 / 40% sm75 / 20% sm52 kernels + long-block kernels), full post-SSA stage",
+                       "kernels": int(len(kid)), "ssa_records_rank0": int(corpus.n_insts), "sass_rank0": n_sass_rank,
+                       "sharding": f"{world} shard(s) by basic-block count, no data-path collective, allgather of match counts",
+                       "l2": "inputs larger than L2 (no flush needed)", "seed": args.seed,
+                       "corpus": "kernels drawn with replacement from reference-front-half pools (tests/golden/pool_*.npz)",
+                       "gen_seconds": round(t_gen, 1), "wall_ms_per_step": t_wall_s / args.steps * 1e3},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+            "gpu_launches": 2 * args.steps,
+            "match_counts": {"selected": int(n_sel), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

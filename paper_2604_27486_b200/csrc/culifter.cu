@@ -335,6 +335,111 @@ template <int WARPS> __global__ void __launch_bounds__(WARPS * 32) k_postssa_cta
 }
 #endif
 
+
+/* ------------------------------------------------------- densification */
+/* The run leaves every function's result at an atomically reserved place
+ * (completion order).  cl_download turns that into the dense CSR of the ABI
+ * on the device: 4-way exclusive scan of the per-function sizes in function
+ * order, then one warp per function copies its pieces to their final place. */
+struct DenseArgs {
+    const FuncOut *fo; uint32_t n_funcs;
+    uint4 *off;                /* [n_funcs + 1] x {inst, imm, val, ev} exclusive  */
+    uint4 *block_sums; uint32_t n_scan_blocks;
+    const uint32_t *func_blk_off; const uint32_t *blk_start, *blk_cnt;
+    const cl_hdr *s_hdr; const uint16_t *s_tag; const uint32_t *s_pay; const cl_imm *s_imm;
+    const uint8_t *s_alive; const int32_t *s_def_iid; const uint32_t *s_origin; const cl_event *s_ev;
+    cl_hdr *d_hdr; uint16_t *d_tag; uint32_t *d_pay; cl_imm *d_imm;
+    uint8_t *d_alive; int32_t *d_def_iid; uint32_t *d_origin; cl_event *d_ev;
+    uint32_t *d_blk_off;       /* [n_blocks + 1]                                   */
+    uint32_t *d_imm_off, *d_val_off;   /* [n_funcs + 1]                            */
+    cl_func *d_func;
+    uint32_t n_blocks;
+};
+#if CL_CUDA
+static constexpr int SCAN_T = 256, SCAN_ITEMS = 8, SCAN_TILE = SCAN_T * SCAN_ITEMS;
+__device__ __forceinline__ uint4 add4(uint4 a, uint4 b) { return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ uint4 sizes_of(const DenseArgs &a, uint32_t f) {
+    if (f >= a.n_funcs) return make_uint4(0, 0, 0, 0);
+    const FuncOut o = a.fo[f];
+    return make_uint4(o.n_inst, o.n_imm, o.f.next_vid, o.n_ev);
+}
+__device__ uint4 block_exscan4(uint4 v, uint4 &total) {
+    __shared__ uint4 ws[SCAN_T / 32];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint4 inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint4 t = make_uint4(__shfl_up_sync(~0u, inc.x, d), __shfl_up_sync(~0u, inc.y, d), __shfl_up_sync(~0u, inc.z, d), __shfl_up_sync(~0u, inc.w, d));
+        if (lane >= (uint32_t)d) inc = add4(inc, t);
+    }
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    uint4 pre = make_uint4(0, 0, 0, 0), tot = pre;
+    for (int i = 0; i < SCAN_T / 32; i++) { if ((uint32_t)i < w) pre = add4(pre, ws[i]); tot = add4(tot, ws[i]); }
+    __syncthreads();
+    total = tot;
+    return make_uint4(pre.x + inc.x - v.x, pre.y + inc.y - v.y, pre.z + inc.z - v.z, pre.w + inc.w - v.w);
+}
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(DenseArgs a) {       /* pass 1: tile sums */
+    uint4 sum = make_uint4(0, 0, 0, 0);
+    const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+    for (int i = 0; i < SCAN_ITEMS; i++) sum = add4(sum, sizes_of(a, base + i));
+    uint4 tot;
+    block_exscan4(sum, tot);
+    if (threadIdx.x == 0) a.block_sums[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(SCAN_T) k_scan_sums(DenseArgs a) {        /* pass 2: one CTA */
+    uint4 run = make_uint4(0, 0, 0, 0);
+    for (uint32_t b0 = 0; b0 < a.n_scan_blocks; b0 += SCAN_T) {
+        const uint32_t i = b0 + threadIdx.x;
+        uint4 v = i < a.n_scan_blocks ? a.block_sums[i] : make_uint4(0, 0, 0, 0), tot;
+        uint4 ex = block_exscan4(v, tot);
+        if (i < a.n_scan_blocks) a.block_sums[i] = add4(run, ex);
+        run = add4(run, tot);
+    }
+    if (threadIdx.x == 0) a.off[a.n_funcs] = run;
+}
+__global__ void __launch_bounds__(SCAN_T) k_scan_apply(DenseArgs a) {       /* pass 3 */
+    const uint32_t base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+    uint4 v[SCAN_ITEMS], sum = make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < SCAN_ITEMS; i++) { v[i] = sizes_of(a, base + i); sum = add4(sum, v[i]); }
+    uint4 tot;
+    uint4 run = add4(block_exscan4(sum, tot), a.block_sums[blockIdx.x]);
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+        if (base + i < a.n_funcs) a.off[base + i] = run;
+        run = add4(run, v[i]);
+    }
+}
+/* one warp per function */
+__global__ void __launch_bounds__(256) k_densify(DenseArgs a) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t f = blockIdx.x * 8 + (threadIdx.x >> 5); f < a.n_funcs; f += gridDim.x * 8) {
+        const FuncOut o = a.fo[f];
+        const uint4 off = a.off[f];
+        if (lane == 0) { a.d_func[f] = o.f; a.d_imm_off[f] = off.y; a.d_val_off[f] = off.z; }
+        const uint32_t b0 = a.func_blk_off[f], b1 = a.func_blk_off[f + 1];
+        for (uint32_t b = b0 + lane; b < b1; b += 32)
+            a.d_blk_off[b] = off.x + (o.n_inst ? a.blk_start[b] - o.inst_start : 0u);
+        const uint4 *sh = (const uint4 *)(a.s_hdr + o.inst_start); uint4 *dh = (uint4 *)(a.d_hdr + off.x);
+        const uint4 *st = (const uint4 *)(a.s_tag + (size_t)o.inst_start * 8); uint4 *dt = (uint4 *)(a.d_tag + (size_t)off.x * 8);
+        const uint4 *sp = (const uint4 *)(a.s_pay + (size_t)o.inst_start * 8); uint4 *dp = (uint4 *)(a.d_pay + (size_t)off.x * 8);
+        for (uint32_t i = lane; i < o.n_inst; i += 32) { dh[i] = sh[i]; dt[i] = st[i]; }
+        for (uint32_t i = lane; i < 2 * o.n_inst; i += 32) dp[i] = sp[i];
+        for (uint32_t i = lane; i < o.n_imm; i += 32) a.d_imm[off.y + i] = a.s_imm[o.imm_start + i];
+        for (uint32_t i = lane; i < o.f.next_vid; i += 32) {
+            a.d_alive[off.z + i] = a.s_alive[o.val_start + i];
+            a.d_def_iid[off.z + i] = a.s_def_iid[o.val_start + i];
+            a.d_origin[off.z + i] = a.s_origin[o.val_start + i];
+        }
+        for (uint32_t i = lane; i < o.n_ev; i += 32) a.d_ev[off.w + i] = a.s_ev[o.ev_start + i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint4 tot = a.off[a.n_funcs];
+        a.d_blk_off[a.n_blocks] = tot.x; a.d_imm_off[a.n_funcs] = tot.y; a.d_val_off[a.n_funcs] = tot.z;
+    }
+}
+#endif
+
 /* ------------------------------------------------------------------ context */
 struct Part {                  /* one kernel's share of the functions            */
     std::vector<uint32_t> list;
@@ -344,6 +449,19 @@ struct Part {                  /* one kernel's share of the functions           
     Caps cap{};
     uint32_t n_groups = 0, hot_bytes = 0, grid = 0;
 };
+
+/* device buffers are grow-only slots: repeated uploads of same-sized corpora
+ * (the end-to-end loop) do not pay cudaMalloc/cudaFree again                */
+enum {
+    B_FUNC = 0, B_FBO, B_EXT_OFF, B_MEM_OFF, B_IMM_OFF, B_VAL_OFF, B_BLK, B_BLK_OFF, B_HDR, B_TAG, B_PAY,
+    B_EXT_TAG, B_EXT_PAY, B_MEM, B_IMM, B_ALIVE, B_DEF_IID, B_MODSETS,
+    B_O_HDR, B_O_TAG, B_O_PAY, B_O_IMM, B_O_ALIVE, B_O_DEF_IID, B_O_ORIGIN, B_O_EXT_TAG, B_O_EXT_PAY, B_O_MEM,
+    B_O_BLK, B_O_BLK_START, B_O_BLK_CNT, B_O_EV, B_O_FUNC,
+    B_LIST0, B_LIST1, B_COUNTER0, B_COUNTER1, B_SCRATCH0, B_SCRATCH1,
+    B_D_OFF, B_D_SUMS, B_D_HDR, B_D_TAG, B_D_PAY, B_D_IMM, B_D_ALIVE, B_D_DEF_IID, B_D_ORIGIN, B_D_EV,
+    B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B__N
+};
+struct DBuf { void *p = nullptr; size_t cap = 0; };
 
 struct cl_ctx {
     int device = 0;
@@ -356,16 +474,11 @@ struct cl_ctx {
     bool have_pb = false, have_in = false, have_out = false;
     cl_pattern_blob *d_pb = nullptr;
     uint8_t *d_opflags = nullptr;
-    /* host copy of the small arrays + device corpus */
-    std::vector<cl_func> h_func;
-    std::vector<uint32_t> h_fbo, h_ext_off, h_mem_off, h_imm_off, h_val_off, h_blk_off;
-    std::vector<cl_blk> h_blk;
+    DBuf buf[B__N];
+    uint32_t F = 0, B = 0, n_modsets = 0;
     cl_corpus d_in{};
-    std::vector<void *> d_in_allocs;
     uint64_t n_inst = 0, n_ext = 0, n_mem = 0, n_imm = 0, n_val = 0;
-    /* results */
     KArgs k{};
-    std::vector<void *> d_out_allocs;
     unsigned long long *d_cursor = nullptr, *d_stats = nullptr;
     unsigned long long h_cursor[CUR__N] = { 0, 0, 0, 0 };
     Part part[2];              /* 0 = warp groups, 1 = CTA groups                */
@@ -374,17 +487,21 @@ struct cl_ctx {
     uint32_t small_max = 128;  /* records: warp-group kernel up to here          */
 };
 
-static void free_list(std::vector<void *> &v) { for (void *p : v) dfree(p); v.clear(); }
-template <class T> static int dalloc(cl_ctx *c, std::vector<void *> &pool, T **p, size_t n) {
-    (void)c;
-    void *q = nullptr;
-    if (dmalloc(&q, n * sizeof(T))) return -1;
-    pool.push_back(q);
-    *p = (T *)q;
+template <class T> static int dget(cl_ctx *c, int id, T **p, size_t n) {
+    DBuf &b = c->buf[id];
+    const size_t need = n * sizeof(T);
+    if (b.cap < need || !b.p) {
+        dfree(b.p);
+        b.p = nullptr; b.cap = 0;
+        const size_t want = need + need / 16 + 256;
+        if (dmalloc(&b.p, want)) return -1;
+        b.cap = want;
+    }
+    *p = (T *)b.p;
     return 0;
 }
-template <class T> static int dupload(cl_ctx *c, std::vector<void *> &pool, T **p, const T *h, size_t n) {
-    if (dalloc(c, pool, p, n)) return -1;
+template <class T> static int dput(cl_ctx *c, int id, T **p, const T *h, size_t n) {
+    if (dget(c, id, p, n)) return -1;
     return h2d(*p, h, n * sizeof(T), c->stream);
 }
 
@@ -418,19 +535,13 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     return 0;
 }
 
-static void free_parts(cl_ctx *c) {
-    for (Part &p : c->part) {
-        dfree(p.d_list); dfree(p.d_counter); dfree(p.d_scratch);
-        p = Part();
-    }
-}
 extern "C" void cl_destroy(cl_ctx *c) {
     if (!c) return;
 #if CL_CUDA
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
 #endif
-    free_list(c->d_in_allocs); free_list(c->d_out_allocs); free_parts(c);
+    for (DBuf &b : c->buf) dfree(b.p);
     dfree(c->d_opflags); dfree(c->d_pb); dfree(c->d_cursor); dfree(c->d_stats);
 #if CL_CUDA
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -477,82 +588,65 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     CUDA_OK(cudaSetDevice(c->device));
     CUDA_OK(cudaStreamSynchronize(c->stream));
 #endif
-    free_list(c->d_in_allocs); free_list(c->d_out_allocs); free_parts(c);
     c->have_in = c->have_out = false;
     const uint32_t F = in->n_funcs, B = in->n_blocks;
     if (in->func_blk_off[F] != B) FAIL("func_blk_off[n_funcs] != n_blocks");
+    c->F = F; c->B = B; c->n_modsets = in->n_modsets;
     c->n_inst = in->blk_off[B]; c->n_ext = in->ext_off[F]; c->n_mem = in->mem_off[F];
     c->n_imm = in->imm_off[F]; c->n_val = in->val_off[F];
-    c->h_func.assign(in->func, in->func + F);
-    c->h_fbo.assign(in->func_blk_off, in->func_blk_off + F + 1);
-    c->h_ext_off.assign(in->ext_off, in->ext_off + F + 1);
-    c->h_mem_off.assign(in->mem_off, in->mem_off + F + 1);
-    c->h_imm_off.assign(in->imm_off, in->imm_off + F + 1);
-    c->h_val_off.assign(in->val_off, in->val_off + F + 1);
-    c->h_blk_off.assign(in->blk_off, in->blk_off + B + 1);
-    c->h_blk.assign(in->blk, in->blk + B);
-    for (uint32_t f = 0; f < F; f++)
-        if (in->val_off[f + 1] - in->val_off[f] != in->func[f].next_vid)
-            FAIL("function %u: value region holds %u entries, next_vid is %u", f, in->val_off[f + 1] - in->val_off[f], in->func[f].next_vid);
+    if (3 * c->n_inst + 1024 >= (1ull << 32)) FAIL("corpus too large for 32-bit stream offsets: shard it");
     cl_corpus &d = c->d_in;
     d = *in;
-    auto &pool = c->d_in_allocs;
-    if (dupload(c, pool, &d.func, in->func, F) || dupload(c, pool, &d.func_blk_off, in->func_blk_off, F + 1) ||
-        dupload(c, pool, &d.ext_off, in->ext_off, F + 1) || dupload(c, pool, &d.mem_off, in->mem_off, F + 1) ||
-        dupload(c, pool, &d.imm_off, in->imm_off, F + 1) || dupload(c, pool, &d.val_off, in->val_off, F + 1) ||
-        dupload(c, pool, &d.blk, in->blk, B) || dupload(c, pool, &d.blk_off, in->blk_off, B + 1) ||
-        dupload(c, pool, &d.hdr, in->hdr, c->n_inst) || dupload(c, pool, &d.tag, in->tag, c->n_inst * 8) ||
-        dupload(c, pool, &d.pay, in->pay, c->n_inst * 8) || dupload(c, pool, &d.ext_tag, in->ext_tag, c->n_ext) ||
-        dupload(c, pool, &d.ext_pay, in->ext_pay, c->n_ext) || dupload(c, pool, &d.mem, in->mem, c->n_mem) ||
-        dupload(c, pool, &d.imm, in->imm, c->n_imm) || dupload(c, pool, &d.val_alive, in->val_alive, c->n_val) ||
-        dupload(c, pool, &d.val_def_iid, in->val_def_iid, c->n_val))
-        return -1;
     cl_modset *dms = nullptr;
-    if (dupload(c, pool, &dms, in->modsets, in->n_modsets)) return -1;
+    if (dput(c, B_FUNC, &d.func, in->func, F) || dput(c, B_FBO, &d.func_blk_off, in->func_blk_off, F + 1) ||
+        dput(c, B_EXT_OFF, &d.ext_off, in->ext_off, F + 1) || dput(c, B_MEM_OFF, &d.mem_off, in->mem_off, F + 1) ||
+        dput(c, B_IMM_OFF, &d.imm_off, in->imm_off, F + 1) || dput(c, B_VAL_OFF, &d.val_off, in->val_off, F + 1) ||
+        dput(c, B_BLK, &d.blk, in->blk, B) || dput(c, B_BLK_OFF, &d.blk_off, in->blk_off, B + 1) ||
+        dput(c, B_HDR, &d.hdr, in->hdr, c->n_inst) || dput(c, B_TAG, &d.tag, in->tag, c->n_inst * 8) ||
+        dput(c, B_PAY, &d.pay, in->pay, c->n_inst * 8) || dput(c, B_EXT_TAG, &d.ext_tag, in->ext_tag, c->n_ext) ||
+        dput(c, B_EXT_PAY, &d.ext_pay, in->ext_pay, c->n_ext) || dput(c, B_MEM, &d.mem, in->mem, c->n_mem) ||
+        dput(c, B_IMM, &d.imm, in->imm, c->n_imm) || dput(c, B_ALIVE, &d.val_alive, in->val_alive, c->n_val) ||
+        dput(c, B_DEF_IID, &d.val_def_iid, in->val_def_iid, c->n_val) ||
+        dput(c, B_MODSETS, &dms, in->modsets, in->n_modsets))
+        return -1;
     d.modsets = dms;
     d.val_origin = nullptr;
 
-    /* work partition: warp groups take the small functions */
+    /* work partition (while the copies are in flight): warp groups take the small functions */
     uint32_t n_max[2] = { 0, 0 }, nv_max[2] = { 0, 0 }, nb_max[2] = { 0, 0 }, imm_max[2] = { 0, 0 }, blk_max[2] = { 0, 0 }, ext_max[2] = { 0, 0 };
+    for (Part &p : c->part) p.list.clear();
+    std::vector<std::pair<uint32_t, uint32_t>> big;
     for (uint32_t f = 0; f < F; f++) {
         const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
         const uint32_t n = in->blk_off[b1] - in->blk_off[b0];
+        if (in->val_off[f + 1] - in->val_off[f] != in->func[f].next_vid)
+            FAIL("function %u: value region holds %u entries, next_vid is %u", f, in->val_off[f + 1] - in->val_off[f], in->func[f].next_vid);
         const int k = n <= c->small_max ? 0 : 1;
-        c->part[k].list.push_back(f);
+        if (k) big.emplace_back(~n, f); else c->part[0].list.push_back(f);
         n_max[k] = std::max(n_max[k], n);
         nv_max[k] = std::max(nv_max[k], in->func[f].next_vid);
         nb_max[k] = std::max(nb_max[k], b1 - b0);
         imm_max[k] = std::max(imm_max[k], in->imm_off[f + 1] - in->imm_off[f]);
         ext_max[k] = std::max(ext_max[k], in->ext_off[f + 1] - in->ext_off[f]);
-        for (uint32_t b = b0; b < b1; b++) blk_max[k] = std::max(blk_max[k], in->blk_off[b + 1] - in->blk_off[b]);
+        if (b1 - b0 == 1) blk_max[k] = std::max(blk_max[k], n);
+        else for (uint32_t b = b0; b < b1; b++) blk_max[k] = std::max(blk_max[k], in->blk_off[b + 1] - in->blk_off[b]);
     }
-    /* big functions first: the tail of the work list is cheap */
+    std::sort(big.begin(), big.end());            /* long poles first */
+    for (auto &pr : big) c->part[1].list.push_back(pr.second);
     for (int k = 0; k < 2; k++) {
         Part &p = c->part[k];
-        std::stable_sort(p.list.begin(), p.list.end(), [&](uint32_t x, uint32_t y) {
-            const uint32_t nx = in->blk_off[in->func_blk_off[x + 1]] - in->blk_off[in->func_blk_off[x]];
-            const uint32_t ny = in->blk_off[in->func_blk_off[y + 1]] - in->blk_off[in->func_blk_off[y]];
-            return nx > ny;
-        });
         if (p.list.empty()) continue;
         p.cap = caps_for(n_max[k], nv_max[k], nb_max[k], imm_max[k], blk_max[k], ext_max[k]);
         p.scratch_per_group = (scratch_bytes(p.cap) + 255) & ~(size_t)255;
 #if CL_CUDA
-        if (k == 0) { p.hot_bytes = 12 * 1024; p.grid = c->n_sm * 4; p.n_groups = p.grid * 4; }
-        else { p.hot_bytes = 100 * 1024; p.grid = c->n_sm * 2; p.n_groups = p.grid; }
-        p.grid = (uint32_t)std::min<size_t>(p.grid, k == 0 ? (p.list.size() + 3) / 4 : p.list.size());
-        p.n_groups = k == 0 ? p.grid * 4 : p.grid;
+        if (k == 0) { p.hot_bytes = 12 * 1024; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * 4, (p.list.size() + 3) / 4); p.n_groups = p.grid * 4; }
+        else { p.hot_bytes = 100 * 1024; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * 2, p.list.size()); p.n_groups = p.grid; }
 #else
         p.hot_bytes = 0; p.grid = 1; p.n_groups = 1;
 #endif
-        void *q = nullptr;
-        if (dmalloc(&q, p.list.size() * sizeof(uint32_t))) return -1;
-        p.d_list = (uint32_t *)q;
-        if (h2d(p.d_list, p.list.data(), p.list.size() * sizeof(uint32_t), c->stream)) return -1;
-        if (dmalloc(&q, sizeof(uint32_t))) return -1;
-        p.d_counter = (uint32_t *)q;
-        if (dmalloc(&q, p.scratch_per_group * p.n_groups)) return -1;
-        p.d_scratch = (uint8_t *)q;
+        if (dput(c, k ? B_LIST1 : B_LIST0, &p.d_list, p.list.data(), p.list.size())) return -1;
+        if (dget(c, k ? B_COUNTER1 : B_COUNTER0, &p.d_counter, 1)) return -1;
+        if (dget(c, k ? B_SCRATCH1 : B_SCRATCH0, &p.d_scratch, p.scratch_per_group * p.n_groups)) return -1;
     }
 
     /* result buffers (worst-case growth, G3/G4) */
@@ -563,18 +657,17 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     k.cap[CUR_IMM] = c->n_imm + 2 * c->n_inst + 1024;
     k.cap[CUR_VAL] = c->n_val + 2 * c->n_inst + 1024;
     k.cap[CUR_EV] = 2 * c->n_inst + 4096;
-    auto &op = c->d_out_allocs;
-    if (dalloc(c, op, &k.o_hdr, k.cap[CUR_INST]) || dalloc(c, op, &k.o_tag, k.cap[CUR_INST] * 8) ||
-        dalloc(c, op, &k.o_pay, k.cap[CUR_INST] * 8) || dalloc(c, op, &k.o_imm, k.cap[CUR_IMM]) ||
-        dalloc(c, op, &k.o_alive, k.cap[CUR_VAL]) || dalloc(c, op, &k.o_def_iid, k.cap[CUR_VAL]) ||
-        dalloc(c, op, &k.o_origin, k.cap[CUR_VAL]) || dalloc(c, op, &k.o_ext_tag, c->n_ext) ||
-        dalloc(c, op, &k.o_ext_pay, c->n_ext) || dalloc(c, op, &k.o_mem, c->n_mem) ||
-        dalloc(c, op, &k.o_blk, B) || dalloc(c, op, &k.o_blk_start, B) || dalloc(c, op, &k.o_blk_cnt, B) ||
-        dalloc(c, op, &k.o_ev, k.cap[CUR_EV]) || dalloc(c, op, &k.o_func, F))
+    if (dget(c, B_O_HDR, &k.o_hdr, k.cap[CUR_INST]) || dget(c, B_O_TAG, &k.o_tag, k.cap[CUR_INST] * 8) ||
+        dget(c, B_O_PAY, &k.o_pay, k.cap[CUR_INST] * 8) || dget(c, B_O_IMM, &k.o_imm, k.cap[CUR_IMM]) ||
+        dget(c, B_O_ALIVE, &k.o_alive, k.cap[CUR_VAL]) || dget(c, B_O_DEF_IID, &k.o_def_iid, k.cap[CUR_VAL]) ||
+        dget(c, B_O_ORIGIN, &k.o_origin, k.cap[CUR_VAL]) || dget(c, B_O_EXT_TAG, &k.o_ext_tag, c->n_ext) ||
+        dget(c, B_O_EXT_PAY, &k.o_ext_pay, c->n_ext) || dget(c, B_O_MEM, &k.o_mem, c->n_mem) ||
+        dget(c, B_O_BLK, &k.o_blk, B) || dget(c, B_O_BLK_START, &k.o_blk_start, B) || dget(c, B_O_BLK_CNT, &k.o_blk_cnt, B) ||
+        dget(c, B_O_EV, &k.o_ev, k.cap[CUR_EV]) || dget(c, B_O_FUNC, &k.o_func, F))
         return -1;
     k.cursor = c->d_cursor; k.stats = c->d_stats;
 #if CL_CUDA
-    CUDA_OK(cudaStreamSynchronize(c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));     /* the caller may reuse its buffers */
 #endif
     c->have_in = true;
     return 0;
@@ -651,70 +744,98 @@ extern "C" int cl_out_sizes(cl_ctx *c, uint64_t sizes[6]) {
     return 0;
 }
 
-/* D2H, then densify: the device wrote functions in completion order; the ABI
- * returns them in function order (dense CSR).                               */
+#if !CL_CUDA
+/* host rendition of the densify kernels for the sim build */
+static void densify_host(const DenseArgs &a) {
+    uint32_t oi = 0, oq = 0, ov = 0, oe = 0;
+    for (uint32_t f = 0; f < a.n_funcs; f++) {
+        const FuncOut o = a.fo[f];
+        a.d_func[f] = o.f; a.d_imm_off[f] = oq; a.d_val_off[f] = ov;
+        for (uint32_t b = a.func_blk_off[f]; b < a.func_blk_off[f + 1]; b++)
+            a.d_blk_off[b] = oi + (o.n_inst ? a.blk_start[b] - o.inst_start : 0u);
+        memcpy(a.d_hdr + oi, a.s_hdr + o.inst_start, sizeof(cl_hdr) * o.n_inst);
+        memcpy(a.d_tag + (size_t)oi * 8, a.s_tag + (size_t)o.inst_start * 8, 16ull * o.n_inst);
+        memcpy(a.d_pay + (size_t)oi * 8, a.s_pay + (size_t)o.inst_start * 8, 32ull * o.n_inst);
+        memcpy(a.d_imm + oq, a.s_imm + o.imm_start, sizeof(cl_imm) * o.n_imm);
+        memcpy(a.d_alive + ov, a.s_alive + o.val_start, o.f.next_vid);
+        memcpy(a.d_def_iid + ov, a.s_def_iid + o.val_start, 4ull * o.f.next_vid);
+        memcpy(a.d_origin + ov, a.s_origin + o.val_start, 4ull * o.f.next_vid);
+        memcpy(a.d_ev + oe, a.s_ev + o.ev_start, sizeof(cl_event) * o.n_ev);
+        oi += o.n_inst; oq += o.n_imm; ov += o.f.next_vid; oe += o.n_ev;
+    }
+    a.d_blk_off[a.n_blocks] = oi; a.d_imm_off[a.n_funcs] = oq; a.d_val_off[a.n_funcs] = ov;
+}
+#endif
+
+/* densify on the device, then D2H straight into the caller's arrays          */
 extern "C" int cl_download(cl_ctx *c, cl_corpus *o, cl_event *events) {
     uint64_t sz[6];
     if (cl_out_sizes(c, sz)) return -1;
-    const uint32_t F = (uint32_t)c->h_func.size(), B = (uint32_t)c->h_blk.size();
+    const uint32_t F = c->F, B = c->B;
     const KArgs &k = c->k;
-    std::vector<FuncOut> fo(F);
-    std::vector<cl_hdr> hdr(sz[0]); std::vector<uint16_t> tag(sz[0] * 8); std::vector<uint32_t> pay(sz[0] * 8);
-    std::vector<cl_imm> imm(sz[3]);
-    std::vector<uint8_t> alive(sz[4]); std::vector<int32_t> def_iid(sz[4]); std::vector<uint32_t> origin(sz[4]);
-    std::vector<cl_event> ev(sz[5]);
-    std::vector<uint32_t> bstart(B), bcnt(B);
 #if CL_CUDA
     CUDA_OK(cudaSetDevice(c->device));
 #endif
-    if (d2h(fo.data(), k.o_func, F * sizeof(FuncOut), c->stream) || d2h(hdr.data(), k.o_hdr, sz[0] * sizeof(cl_hdr), c->stream) ||
-        d2h(tag.data(), k.o_tag, sz[0] * 16, c->stream) || d2h(pay.data(), k.o_pay, sz[0] * 32, c->stream) ||
-        d2h(imm.data(), k.o_imm, sz[3] * sizeof(cl_imm), c->stream) || d2h(alive.data(), k.o_alive, sz[4], c->stream) ||
-        d2h(def_iid.data(), k.o_def_iid, sz[4] * 4, c->stream) || d2h(origin.data(), k.o_origin, sz[4] * 4, c->stream) ||
-        d2h(ev.data(), k.o_ev, sz[5] * sizeof(cl_event), c->stream) || d2h(bstart.data(), k.o_blk_start, B * 4ull, c->stream) ||
-        d2h(bcnt.data(), k.o_blk_cnt, B * 4ull, c->stream) || d2h(o->blk, k.o_blk, B * sizeof(cl_blk), c->stream) ||
-        d2h(o->ext_tag, k.o_ext_tag, c->n_ext * 2, c->stream) || d2h(o->ext_pay, k.o_ext_pay, c->n_ext * 4, c->stream) ||
-        d2h(o->mem, k.o_mem, c->n_mem * sizeof(cl_memref), c->stream))
+    DenseArgs a;
+    memset(&a, 0, sizeof a);
+    a.fo = k.o_func; a.n_funcs = F; a.n_blocks = B;
+    a.func_blk_off = c->d_in.func_blk_off; a.blk_start = k.o_blk_start; a.blk_cnt = k.o_blk_cnt;
+    a.s_hdr = k.o_hdr; a.s_tag = k.o_tag; a.s_pay = k.o_pay; a.s_imm = k.o_imm;
+    a.s_alive = k.o_alive; a.s_def_iid = k.o_def_iid; a.s_origin = k.o_origin; a.s_ev = k.o_ev;
+#if CL_CUDA
+    a.n_scan_blocks = (F + SCAN_TILE - 1) / SCAN_TILE;
+#else
+    a.n_scan_blocks = 1;
+#endif
+    if (dget(c, B_D_OFF, &a.off, (size_t)F + 1) || dget(c, B_D_SUMS, &a.block_sums, (size_t)a.n_scan_blocks + 1) ||
+        dget(c, B_D_HDR, &a.d_hdr, sz[0]) || dget(c, B_D_TAG, &a.d_tag, sz[0] * 8) || dget(c, B_D_PAY, &a.d_pay, sz[0] * 8) ||
+        dget(c, B_D_IMM, &a.d_imm, sz[3]) || dget(c, B_D_ALIVE, &a.d_alive, sz[4]) || dget(c, B_D_DEF_IID, &a.d_def_iid, sz[4]) ||
+        dget(c, B_D_ORIGIN, &a.d_origin, sz[4]) || dget(c, B_D_EV, &a.d_ev, sz[5]) || dget(c, B_D_BLK_OFF, &a.d_blk_off, (size_t)B + 1) ||
+        dget(c, B_D_IMM_OFF, &a.d_imm_off, (size_t)F + 1) || dget(c, B_D_VAL_OFF, &a.d_val_off, (size_t)F + 1) ||
+        dget(c, B_D_FUNC, &a.d_func, F))
         return -1;
+#if CL_CUDA
+    if (F) {
+        k_scan_tiles<<<a.n_scan_blocks, SCAN_T, 0, c->stream>>>(a);
+        k_scan_sums<<<1, SCAN_T, 0, c->stream>>>(a);
+        k_scan_apply<<<a.n_scan_blocks, SCAN_T, 0, c->stream>>>(a);
+        k_densify<<<std::min<uint32_t>((F + 7) / 8, (uint32_t)c->n_sm * 16), 256, 0, c->stream>>>(a);
+        CUDA_OK(cudaGetLastError());
+    }
+#else
+    densify_host(a);
+#endif
+    o->n_funcs = F; o->n_blocks = B; o->n_modsets = c->n_modsets;
+    if (d2h(o->func, a.d_func, F * sizeof(cl_func), c->stream) || d2h(o->func_blk_off, c->d_in.func_blk_off, 4ull * (F + 1), c->stream) ||
+        d2h(o->ext_off, c->d_in.ext_off, 4ull * (F + 1), c->stream) || d2h(o->mem_off, c->d_in.mem_off, 4ull * (F + 1), c->stream) ||
+        d2h(o->imm_off, a.d_imm_off, 4ull * (F + 1), c->stream) || d2h(o->val_off, a.d_val_off, 4ull * (F + 1), c->stream) ||
+        d2h(o->blk, k.o_blk, B * sizeof(cl_blk), c->stream) || d2h(o->blk_off, a.d_blk_off, 4ull * (B + 1), c->stream) ||
+        d2h(o->hdr, a.d_hdr, sz[0] * sizeof(cl_hdr), c->stream) || d2h(o->tag, a.d_tag, sz[0] * 16, c->stream) ||
+        d2h(o->pay, a.d_pay, sz[0] * 32, c->stream) || d2h(o->ext_tag, k.o_ext_tag, c->n_ext * 2, c->stream) ||
+        d2h(o->ext_pay, k.o_ext_pay, c->n_ext * 4, c->stream) || d2h(o->mem, k.o_mem, c->n_mem * sizeof(cl_memref), c->stream) ||
+        d2h(o->imm, a.d_imm, sz[3] * sizeof(cl_imm), c->stream) || d2h(o->val_alive, a.d_alive, sz[4], c->stream) ||
+        d2h(o->val_def_iid, a.d_def_iid, sz[4] * 4, c->stream) || d2h(o->val_origin, a.d_origin, sz[4] * 4, c->stream))
+        return -1;
+    if (events && d2h(events, a.d_ev, sz[5] * sizeof(cl_event), c->stream)) return -1;
 #if CL_CUDA
     CUDA_OK(cudaStreamSynchronize(c->stream));
 #endif
-    o->n_funcs = F; o->n_blocks = B; o->n_modsets = c->d_in.n_modsets;
-    uint64_t ni = 0, nq = 0, nv = 0, ne = 0;
-    for (uint32_t f = 0; f < F; f++) {
-        const FuncOut &r = fo[f];
-        o->func[f] = r.f;
-        o->func_blk_off[f] = c->h_fbo[f]; o->ext_off[f] = c->h_ext_off[f]; o->mem_off[f] = c->h_mem_off[f];
-        o->imm_off[f] = (uint32_t)nq; o->val_off[f] = (uint32_t)nv;
-        for (uint32_t b = c->h_fbo[f]; b < c->h_fbo[f + 1]; b++) {
-            o->blk_off[b] = (uint32_t)ni;
-            if (bcnt[b]) {
-                memcpy(o->hdr + ni, hdr.data() + bstart[b], sizeof(cl_hdr) * bcnt[b]);
-                memcpy(o->tag + ni * 8, tag.data() + (size_t)bstart[b] * 8, 16ull * bcnt[b]);
-                memcpy(o->pay + ni * 8, pay.data() + (size_t)bstart[b] * 8, 32ull * bcnt[b]);
-            }
-            ni += bcnt[b];
-        }
-        if (r.n_imm) memcpy(o->imm + nq, imm.data() + r.imm_start, sizeof(cl_imm) * r.n_imm);
-        nq += r.n_imm;
-        const uint32_t nvf = r.f.next_vid;
-        if (nvf) {
-            memcpy(o->val_alive + nv, alive.data() + r.val_start, nvf);
-            memcpy(o->val_def_iid + nv, def_iid.data() + r.val_start, 4ull * nvf);
-            memcpy(o->val_origin + nv, origin.data() + r.val_start, 4ull * nvf);
-        }
-        nv += r.f.next_vid;
-        if (events && r.n_ev) memcpy(events + ne, ev.data() + r.ev_start, sizeof(cl_event) * r.n_ev);
-        ne += r.n_ev;
-    }
-    o->func_blk_off[F] = B; o->ext_off[F] = c->h_ext_off[F]; o->mem_off[F] = c->h_mem_off[F];
-    o->imm_off[F] = (uint32_t)nq; o->val_off[F] = (uint32_t)nv; o->blk_off[B] = (uint32_t)ni;
-    if (events)
-        std::sort(events, events + ne, [](const cl_event &x, const cl_event &y) {
-            const uint32_t *a = (const uint32_t *)&x, *b = (const uint32_t *)&y;
-            for (int i = 0; i < 8; i++) if (a[i] != b[i]) return a[i] < b[i];
+    if (events) {
+        /* events of one function are contiguous now; order each run the way the
+         * reference appends (seq, kind, idx, ...)                              */
+        auto less = [](const cl_event &x, const cl_event &y) {
+            const uint32_t *p = (const uint32_t *)&x, *q = (const uint32_t *)&y;
+            for (int i = 0; i < 8; i++) if (p[i] != q[i]) return p[i] < q[i];
             return false;
-        });
+        };
+        uint64_t i = 0;
+        while (i < sz[5]) {
+            uint64_t j = i + 1;
+            while (j < sz[5] && events[j].func == events[i].func) j++;
+            if (j - i > 1) std::sort(events + i, events + j, less);
+            i = j;
+        }
+    }
     return 0;
 }
 

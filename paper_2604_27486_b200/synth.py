@@ -1,0 +1,183 @@
+"""Synthetic corpora at benchmark scale, directly in struct-of-arrays form.
+
+The reference has no large-corpus generator and its front
+half (parser, CFG, SSA) does not exist on the GPU box, so the big corpora are
+built in two steps:
+
+1. ``tools/make_pools.py`` (in-container) writes seeded SASS *text* with
+   ``tools/gen_sass.py``, pushes it through the reference's own front half and
+   stores the resulting SSA-phase functions as an encoded *pool*
+   (``tests/golden/pool_<kind>.npz``: a few thousand distinct kernels per
+   kind, with their SASS source-line counts).
+2. ``build_corpus`` (anywhere) draws kernels from the pools with replacement
+   (seeded) until the requested number of SASS instructions is reached and
+   concatenates them.  Every index inside a function is function-local, so
+   concatenation only has to rebuild the CSR offset arrays.
+
+Kinds follow BASELINE.json's configs: ``sm52`` (XMAD heavy, config 2),
+``sm90`` (all aggregation idioms + near misses, config 3), ``long`` (4096+
+instruction blocks with reciprocal chains, config 4) and ``mixed`` (40 % sm90,
+40 % sm75, 20 % sm52 kernels plus a sprinkle of long ones, config 5).
+"""
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import layout as L
+from .soa import Corpus
+
+POOL_DIR = Path(__file__).resolve().parent.parent / "tests" / "golden"
+KINDS = ("sm52", "sm75", "sm90", "long")
+MIXED = (("sm90", 0.3995), ("sm75", 0.40), ("sm52", 0.20), ("long", 0.0005))
+
+
+@dataclass
+class Pool:
+    corpus: Corpus
+    n_sass: np.ndarray          # SASS source instructions per function
+    kind: str
+
+
+def save_pool(path, corpus: Corpus, n_sass, kind: str):
+    tables = {"op_name": L.TABLES.op_name, "modset_tuple": [list(t) for t in L.TABLES.modset_tuple],
+              "strings": L.TABLES.strings}
+    np.savez_compressed(path, n_sass=np.asarray(n_sass, np.uint32), kind=np.array(kind),
+                        tables=np.array(json.dumps(tables)),
+                        **{a: getattr(corpus, a) for a in Corpus.ARRAYS})
+
+
+def load_pool(kind: str, path=None) -> Pool:
+    """Load a pool and translate its interned ids (opcodes, modifier tuples,
+    strings) into this process's tables."""
+    z = np.load(path or POOL_DIR / f"pool_{kind}.npz")
+    tables = json.loads(str(z["tables"]))
+    c = Corpus(**{a: z[a].copy() for a in Corpus.ARRAYS})
+    op_map = np.array([L.TABLES.opcode(n) for n in tables["op_name"]], np.uint16)
+    ms_map = np.array([L.TABLES.modset(tuple(t)) for t in tables["modset_tuple"]], np.uint16)
+    st_map = np.array([L.TABLES.string(s) for s in tables["strings"]] or [0], np.uint32)
+    c.hdr["op"] = op_map[c.hdr["op"]]
+    c.hdr["modset"] = ms_map[c.hdr["modset"]]
+    for tag, pay in ((c.tag, c.pay), (c.ext_tag, c.ext_pay)):
+        is_sreg = (tag & 15) == L.K_SREG
+        pay[is_sreg] = st_map[pay[is_sreg]]
+    # pools are encoder output: every immediate spelling is a string id (hex-text
+    # immediates only come out of the device rewrites)
+    if ((c.tag[(c.tag & 15) == L.K_IMM] & L.T_IMM_HEXTEXT) != 0).any():
+        raise ValueError("pool holds device-created immediates")
+    c.imm["text"] = st_map[c.imm["text"].astype(np.int64)]
+    return Pool(c, z["n_sass"].astype(np.int64), str(z["kind"]))
+
+
+def _ranges(starts, counts):
+    """Concatenated aranges: [s0, s0+1, .., s0+c0-1, s1, ..] as int64."""
+    counts = counts.astype(np.int64)
+    total = int(counts.sum())
+    if total == 0:
+        return np.zeros(0, np.int64)
+    ends = np.cumsum(counts)
+    base = np.repeat(starts.astype(np.int64) - (ends - counts), counts)
+    return base + np.arange(total, dtype=np.int64)
+
+
+def take_functions(c: Corpus, picks: np.ndarray) -> Corpus:
+    """New corpus made of functions ``picks`` (with repetition) of ``c``."""
+    picks = np.asarray(picks, np.int64)
+    fbo = c.func_blk_off.astype(np.int64)
+    nb = fbo[picks + 1] - fbo[picks]
+    blk_idx = _ranges(fbo[picks], nb)
+    bo = c.blk_off.astype(np.int64)
+    ni_blk = bo[blk_idx + 1] - bo[blk_idx]
+    inst_idx = _ranges(bo[blk_idx], ni_blk)
+
+    def region(off, data_arrays):
+        off = off.astype(np.int64)
+        cnt = off[picks + 1] - off[picks]
+        idx = _ranges(off[picks], cnt)
+        new_off = np.zeros(len(picks) + 1, np.uint32)
+        np.cumsum(cnt, out=new_off[1:])
+        return new_off, [a[idx] for a in data_arrays]
+
+    ext_off, (ext_tag, ext_pay) = region(c.ext_off, (c.ext_tag, c.ext_pay))
+    mem_off, (mem,) = region(c.mem_off, (c.mem,))
+    imm_off, (imm,) = region(c.imm_off, (c.imm,))
+    val_off, (alive, def_iid, origin) = region(c.val_off, (c.val_alive, c.val_def_iid, c.val_origin))
+    func_blk_off = np.zeros(len(picks) + 1, np.uint32)
+    np.cumsum(nb, out=func_blk_off[1:])
+    blk_off = np.zeros(len(blk_idx) + 1, np.uint32)
+    np.cumsum(ni_blk, out=blk_off[1:])
+    return Corpus(func=c.func[picks], func_blk_off=func_blk_off, ext_off=ext_off, mem_off=mem_off,
+                  imm_off=imm_off, val_off=val_off, blk=c.blk[blk_idx], blk_off=blk_off,
+                  hdr=c.hdr[inst_idx], tag=c.tag[inst_idx], pay=c.pay[inst_idx], ext_tag=ext_tag,
+                  ext_pay=ext_pay, mem=mem, imm=imm, val_alive=alive, val_def_iid=def_iid,
+                  val_origin=origin)
+
+
+def concat(parts) -> Corpus:
+    """Concatenate corpora (function-local indices need no fix-up)."""
+    def cat_off(name):
+        out, base = [np.zeros(1, np.uint32)], 0
+        for p in parts:
+            o = getattr(p, name).astype(np.int64)
+            out.append((o[1:] + base).astype(np.uint32))
+            base += int(o[-1])
+        return np.concatenate(out)
+    kw = {n: cat_off(n) for n in ("func_blk_off", "ext_off", "mem_off", "imm_off", "val_off", "blk_off")}
+    for n in Corpus.ARRAYS:
+        if n not in kw:
+            kw[n] = np.concatenate([getattr(p, n) for p in parts])
+    return Corpus(**kw)
+
+
+_POOLS = {}
+
+
+def pool(kind: str) -> Pool:
+    if kind not in _POOLS:
+        _POOLS[kind] = load_pool(kind)
+    return _POOLS[kind]
+
+
+def build_corpus(kind: str, n_sass: int, seed: int = 0):
+    """-> (Corpus, n_sass_actual, info).  ``kind`` in KINDS or 'mixed'."""
+    rng = np.random.default_rng(seed)
+    shares = MIXED if kind == "mixed" else ((kind, 1.0),)
+    parts, total, info = [], 0, {}
+    pools = {k: pool(k) for k, _ in shares}
+    mean = sum(sh * float(pools[k].n_sass.mean()) for k, sh in shares)     # SASS per kernel draw
+    n_kernels = max(1, int(round(n_sass / mean)))
+    for k, sh in shares:
+        p = pools[k]
+        nk = int(round(n_kernels * sh)) if kind == "mixed" else n_kernels
+        if nk == 0:
+            continue
+        picks = rng.integers(0, p.corpus.n_funcs, nk)
+        parts.append(take_functions(p.corpus, picks))
+        got = int(p.n_sass[picks].sum())
+        total += got
+        info[k] = {"kernels": nk, "sass": got, "pool_kernels": int(p.corpus.n_funcs)}
+    corpus = parts[0] if len(parts) == 1 else concat(parts)
+    if kind == "mixed":                      # interleave the architectures kernel by kernel
+        order = rng.permutation(corpus.n_funcs)
+        corpus = take_functions(corpus, order)
+    return corpus, total, info
+
+
+def shard_by_blocks(corpus: Corpus, n_shards: int):
+    """Corpus sharder (north star subsystem 5): greedy longest-first bin packing
+    of kernels by basic-block count; returns the function indices of each shard.
+    No data crosses shards afterwards (functions are independent)."""
+    nb = np.diff(corpus.func_blk_off.astype(np.int64))
+    order = np.argsort(-nb, kind="stable")
+    if n_shards == 1:
+        return [np.arange(corpus.n_funcs)]
+    # longest-first round robin with a snake order is LPT-equivalent for near-uniform kernels
+    # and O(F); the handful of heavy kernels go first, one per shard.
+    shard = np.empty(corpus.n_funcs, np.int64)
+    pos = np.arange(corpus.n_funcs)
+    cyc = pos % (2 * n_shards)
+    shard[order] = np.where(cyc < n_shards, cyc, 2 * n_shards - 1 - cyc)
+    return [np.sort(np.nonzero(shard == s)[0]) for s in range(n_shards)]
