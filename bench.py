@@ -260,6 +260,10 @@ def main():
         fence()
         wall = time.perf_counter() - t1
     st = eng.stats()
+    if os.environ.get("CL_PROF") and rank == 0:
+        prof = eng.debug_profile()
+        tot = max(prof.get("total", 1), 1)
+        print("phase cycles (share of group time):", {k: round(v / tot, 3) for k, v in prof.items() if v}, file=sys.stderr)
     n_out = int(st["n_inst_out"])
     n_sel = int(st["selected"].sum())
     # max over ranks of the device time of the K steps

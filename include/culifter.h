@@ -243,7 +243,15 @@ typedef struct cl_pattern {     /* Pattern (patterns.py:78-86)                  
     uint8_t n_templates, rewrite, n_vars, table; /* table: 0 aggregation, 1 xmad */
     uint8_t var_a, var_b, var_c; /* CL_RW_XMAD: indices of $a $b $c             */
     uint8_t modvar_cond, modvar_bop; /* CL_RW_ISETP64: "mod:cond", "mod:bop"     */
-    uint8_t pad[7];
+    /* Join plan (host-derived from the slots, an optimisation only): every
+     * template but the anchor defines a variable that an already resolved
+     * template uses, so its instruction is the SSA definition of that operand
+     * instead of a member of the candidate product (patterns.py:195).        */
+    uint8_t join_ok;            /* 0: enumerate the product                       */
+    uint8_t join_order[3];      /* templates in resolution order, [0] = anchor    */
+    uint8_t join_from[3];       /* [k>=1]: resolved template holding the use      */
+    uint8_t join_slot[3];       /* [k>=1]: its slot index (defs, aux, uses order) */
+    uint8_t pad[13];
     cl_template t[CL_MAX_TEMPLATES];
 } cl_pattern;
 

@@ -189,6 +189,17 @@ class Engine:
         self._check(self.lib.cl_last_run_ms(self._ctx, C.byref(ms)))
         return float(ms.value)
 
+    PROFILE_SLOTS = ("total", "load", "store", "usecount", "seed", "match", "select", "plan+emit", "emit",
+                     "move", "simplify", "dce", "recip", "tag", "setup", "-")
+
+    def debug_profile(self):
+        """Per-phase cycle sums (lane 0 of every group) of the last run; CUDA library only."""
+        if not hasattr(self.lib, "cl_debug_profile"):
+            return {}
+        buf = (C.c_ulonglong * 16)()
+        self.lib.cl_debug_profile(self._ctx, buf, 16)
+        return dict(zip(self.PROFILE_SLOTS, (int(x) for x in buf)))
+
     def device_counts_ptr(self):
         return self.lib.cl_device_counts_ptr(self._ctx)
 

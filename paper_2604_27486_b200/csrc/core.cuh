@@ -27,12 +27,14 @@
 #define CLF __device__ __noinline__
 #define CLHD __host__ __device__ inline
 #define CLM static __device__ __forceinline__
+#define CLMEM __device__ __forceinline__
 #else
 #define CL_DEV 0
 #define CLD static inline
 #define CLF static
 #define CLHD static inline
 #define CLM static inline
+#define CLMEM inline
 struct alignas(16) uint4 { uint32_t x, y, z, w; };
 #endif
 
@@ -77,6 +79,25 @@ CLD unsigned long long a_add64(unsigned long long *p, unsigned long long v) {
     unsigned long long o = *p; *p += v; return o;
 #endif
 }
+
+/* ---------------------------------------------------------------- profiling */
+/* cycle counters per phase, accumulated by lane 0 of every group (cheap, always on);
+ * cl_debug_profile() returns their sum over all groups                         */
+enum { PF_TOTAL = 0, PF_LOAD, PF_STORE, PF_USECOUNT, PF_SEED, PF_MATCH, PF_SELECT, PF_PLAN, PF_EMIT, PF_MOVE,
+       PF_SIMPLIFY, PF_DCE, PF_RECIP, PF_TAG, PF_SETUP, PF__N = 16 };
+CLD unsigned long long now() {
+#if CL_DEV
+    return clock64();
+#else
+    return 0;
+#endif
+}
+struct Prof {
+    unsigned long long *acc, t0; bool on;
+    CLMEM Prof(unsigned long long *a, int slot, bool lane0) : acc(a + slot), t0(0), on(lane0) { if (on) t0 = now(); }
+    CLMEM ~Prof() { if (on) *acc += now() - t0; }
+};
+#define PROF(g, s, slot) Prof _prof_##slot((s).prof, slot, (g).rank == 0)
 
 /* ------------------------------------------------------------------ groups */
 /* NW = warps per group.  NW == 1: the group is a warp (several independent
@@ -168,12 +189,6 @@ struct SelRec {                /* selected match, function wide                 
     uint32_t blk;              /* block index                                    */
     uint32_t pos[3];           /* block-relative positions                       */
 };
-struct Plan {
-    uint8_t ok, rm, nins, retag;
-    uint32_t esc;              /* escape query log (replayed by the emit pass)   */
-    uint32_t nv, ni, nm;       /* allocations incl. leaked ones (G4)             */
-    uint32_t vbase, ibase, mbase;
-};
 struct XRec {                  /* bitcast inserted by the reciprocal pass        */
     Rec r;
     uint32_t anchor;           /* stream position of the add                     */
@@ -226,11 +241,12 @@ struct FS {                    /* one function resident in a group's work memory
     /* per position scratch [I] */
     uint8_t *keep, *inscnt, *clsid;
     uint32_t *outpos, *cand, *sel_at;
+    uint32_t *cidx;            /* index of a position inside its seed class (aliases outpos) */
     unsigned long long *owner;
     /* per match scratch */
     MatchRec *mt;              /* [M]                                            */
     SelRec *sel;               /* [S]                                            */
-    Plan *plan;                /* [S]                                            */
+    struct Stage *stage;       /* [S] staged rewrite of each selected match       */
     uint32_t *blk_sel;         /* [B + 1] selected-match range of each block     */
     /* reciprocal */
     uint32_t *site;            /* [U]                                            */
@@ -239,6 +255,7 @@ struct FS {                    /* one function resident in a group's work memory
     uint32_t *root;            /* [V]                                            */
     /* statistics (group-private, flushed by the kernel)                       */
     uint32_t *st_matches, *st_selected, *st_rewrites, *st_refused;   /* [16] each */
+    unsigned long long *prof;  /* [PF__N] group-private cycle counters              */
     /* seed classes of the current table */
     uint32_t n_cls;
     uint16_t cls_op[MAX_CLS];
@@ -313,6 +330,7 @@ CLD void st_rec(FS &s, uint32_t i, const Rec &r) {
 
 /* move n records from src to dst inside the gap buffer (any overlap)          */
 template <class G> CLF void move_recs(const G &g, FS &s, uint32_t dst, uint32_t src, uint32_t n) {
+    PROF(g, s, PF_MOVE);
     if (dst == src || n == 0) return;
     const uint32_t chunks = (n + g.size - 1) / g.size;
     for (uint32_t c = 0; c < chunks; c++) {
@@ -343,6 +361,7 @@ CLD void push_event(FS &s, uint32_t seq, uint32_t kind, uint32_t idx, uint32_t a
 /* Use counts (= len(du.users(vid)), terminator sites included) and the stream
  * position of each value's defining instruction (du.def_inst), ssa.py:613-636 */
 template <class G> CLF void build_usecount(const G &g, FS &s) {
+    PROF(g, s, PF_USECOUNT);
     GFOR(g, v, s.next_vid) if (v < s.next_vid) { s.usecnt[v] = 0; s.defpos[v] = NONE32; }
     g.sync();
     GFOR(g, i, s.n) if (i < s.n) {
@@ -458,7 +477,8 @@ CLF bool connected(const FS &s, const uint32_t *idx, unsigned n) {
 /* one candidate tuple of match_patterns (patterns.py:199-215); idx = stream
  * positions, strictly increasing order already checked by the caller         */
 CLF bool check_tuple(const FS &s, const cl_pattern &p, const uint32_t *idx, Bind &b) {
-    for (int k = 0; k < NBIND; k++) b.var[k].cls = KC_NONE;
+    for (unsigned k = 0; k < p.n_vars; k++) b.var[k].cls = KC_NONE;
+    for (int k = CL_MAX_VARS; k < NBIND; k++) b.var[k].cls = KC_NONE;
     for (unsigned t = 0; t < p.n_templates; t++) {
         const cl_hdr h = s.S.hdr[idx[t]];
         if (!match_inst(s, p.t[t], h, idx[t], b)) return false;
@@ -488,6 +508,7 @@ CLD int class_of(const FS &s, uint16_t op) {
 /* FindSeeds (patterns.py:189-191): per head opcode, the block positions whose
  * base opcode fits, in order -- ballot/popc compaction per class.            */
 template <class G> CLF uint32_t seed_scan(const G &g, FS &s, uint32_t lo, uint32_t n) {
+    PROF(g, s, PF_SEED);
     GFOR(g, i, n) if (i < n) {
         const uint16_t op = s.S.hdr[lo + i].op;
         s.clsid[i] = (uint8_t)class_of(s, op);
@@ -500,7 +521,7 @@ template <class G> CLF uint32_t seed_scan(const G &g, FS &s, uint32_t lo, uint32
             const bool f = i < n && s.clsid[i] == c;
             uint32_t cnt;
             const uint32_t off = g.flag_exscan(f, cnt);
-            if (f) s.cand[total + off] = i;
+            if (f) { s.cand[total + off] = i; s.cidx[i] = total + off - s.cls_off[c]; }
             total += cnt;
         }
     }
@@ -509,58 +530,140 @@ template <class G> CLF uint32_t seed_scan(const G &g, FS &s, uint32_t lo, uint32
     return total;
 }
 
-/* match_patterns (patterns.py:181-216) of one block: every tuple of rank
- * < budget in product order; matches appended in list order.                */
+/* append helper: ordered (ballot/popc) compaction of this iteration's hits   */
+template <class G> CLD void append_match(const G &g, FS &s, uint32_t &nm, bool ok, unsigned pi, unsigned nt,
+                                         const uint32_t *pos, unsigned long long r) {
+    uint32_t cnt;
+    const uint32_t off = g.flag_exscan(ok, cnt);
+    if (ok && nm + off < s.cap.M) {
+        MatchRec m;
+        m.pat = (uint8_t)pi; m.n = (uint8_t)nt; m.state = MS_UNDECIDED; m.pad = 0;
+        m.pos[0] = pos[0]; m.pos[1] = nt > 1 ? pos[1] : NONE32; m.pos[2] = nt > 2 ? pos[2] : NONE32;
+        m.seq = (uint32_t)pi << 20 | (uint32_t)r;
+        s.mt[nm + off] = m;
+    }
+    nm += cnt;
+}
+
+/* the candidate product of one pattern, literally (patterns.py:189-215): every
+ * tuple of rank < budget in itertools.product order                          */
+template <class G> CLF void match_product(const G &g, FS &s, uint32_t lo, unsigned pi, uint32_t &nm) {
+    const cl_pattern &p = s.pb->p[pi];
+    const unsigned nt = p.n_templates;
+    uint32_t cn[3] = { 1, 1, 1 }, cb[3] = { 0, 0, 0 };
+    for (unsigned t = 0; t < nt; t++) {
+        const int c = class_of(s, p.t[t].op);
+        cn[t] = s.cls_off[c + 1] - s.cls_off[c];
+        cb[t] = s.cls_off[c];
+        if (cn[t] == 0) return;
+    }
+    unsigned long long T = (unsigned long long)cn[0] * cn[1] * cn[2];
+    if (T > s.pb->budget) T = s.pb->budget;                     /* :194-198 */
+    const uint32_t Tl = (uint32_t)T;
+    GFOR(g, r, Tl) {
+        bool ok = false;
+        uint32_t idx[3] = { NONE32, NONE32, NONE32 };
+        if (r < Tl) {
+            uint32_t q = r, i2 = 0, i1 = 0;
+            if (nt > 2) { i2 = q % cn[2]; q /= cn[2]; }
+            if (nt > 1) { i1 = q % cn[1]; q /= cn[1]; }
+            idx[0] = s.cand[cb[0] + q];
+            ok = true;
+            if (nt > 1) { idx[1] = s.cand[cb[1] + i1]; ok = idx[0] < idx[1]; }
+            if (nt > 2) { idx[2] = s.cand[cb[2] + i2]; ok = ok && idx[1] < idx[2]; }
+            if (ok) {
+                uint32_t abs_idx[3] = { lo + idx[0], lo + idx[1], lo + idx[2] };
+                Bind b;
+                ok = check_tuple(s, p, abs_idx, b);
+            }
+        }
+        append_match(g, s, nm, ok, pi, nt, idx, r);
+    }
+}
+
+/* match_patterns (patterns.py:181-216) of one block.
+ * Join form: the work items are the (pattern, anchor seed) pairs of all
+ * patterns, flattened so that lanes stay busy; every other instruction of a
+ * tuple is the SSA definition of the operand that links it to an already
+ * resolved one (unique), so the candidate product collapses to one tuple per
+ * anchor.  The tuple's rank in itertools.product order still decides the
+ * budget cut (G1) and the list order.  A link that is not an SSA value (RZ,
+ * PT, an immediate...) sends its pattern to the literal product.            */
 template <class G> CLF uint32_t match_block(const G &g, FS &s, uint32_t lo, uint32_t n, unsigned table) {
+    PROF(g, s, PF_MATCH);
     if (seed_scan(g, s, lo, n) == 0) return 0;
     const cl_pattern_blob *pb = s.pb;
-    uint32_t nm = 0;
+    uint32_t pref[CL_MAX_PATTERNS + 1];
+    uint32_t product_mask = 0, items = 0;
     for (unsigned pi = 0; pi < pb->n_patterns; pi++) {
         const cl_pattern &p = pb->p[pi];
+        pref[pi] = items;
         if (p.table != table) continue;
-        const unsigned nt = p.n_templates;
-        uint32_t cn[3] = { 1, 1, 1 }, cb[3] = { 0, 0, 0 };
         bool empty = false;
-        for (unsigned t = 0; t < nt; t++) {
+        for (unsigned t = 0; t < p.n_templates; t++) {
             const int c = class_of(s, p.t[t].op);
-            cn[t] = s.cls_off[c + 1] - s.cls_off[c];
-            cb[t] = s.cls_off[c];
-            empty |= cn[t] == 0;
+            empty |= s.cls_off[c + 1] == s.cls_off[c];
         }
         if (empty) continue;
-        unsigned long long T = (unsigned long long)cn[0] * cn[1] * cn[2];
-        if (T > pb->budget) T = pb->budget;                     /* :194-198 */
-        const uint32_t Tl = (uint32_t)T;
-        GFOR(g, r, Tl) {
-            bool ok = false;
-            uint32_t idx[3] = { NONE32, NONE32, NONE32 };
-            if (r < Tl) {
-                uint32_t q = r;
-                uint32_t i2 = 0, i1 = 0;
-                if (nt > 2) { i2 = q % cn[2]; q /= cn[2]; }
-                if (nt > 1) { i1 = q % cn[1]; q /= cn[1]; }
-                idx[0] = s.cand[cb[0] + q];
-                ok = true;
-                if (nt > 1) { idx[1] = s.cand[cb[1] + i1]; ok = idx[0] < idx[1]; }
-                if (nt > 2) { idx[2] = s.cand[cb[2] + i2]; ok = ok && idx[1] < idx[2]; }
-                if (ok) {
-                    uint32_t abs_idx[3] = { lo + idx[0], lo + idx[1], lo + idx[2] };
-                    Bind b;
-                    ok = check_tuple(s, p, abs_idx, b);
-                }
-            }
-            uint32_t cnt;
-            const uint32_t off = g.flag_exscan(ok, cnt);
-            if (ok && nm + off < s.cap.M) {
-                MatchRec m;
-                m.pat = (uint8_t)pi; m.n = (uint8_t)nt; m.state = MS_UNDECIDED; m.pad = 0;
-                m.pos[0] = idx[0]; m.pos[1] = idx[1]; m.pos[2] = idx[2];
-                m.seq = (uint32_t)pi << 20 | r;
-                s.mt[nm + off] = m;
-            }
-            nm += cnt;
-        }
+        if (!p.join_ok) { product_mask |= 1u << pi; continue; }
+        const int ca = class_of(s, p.t[p.join_order[0]].op);
+        items += s.cls_off[ca + 1] - s.cls_off[ca];
     }
+    pref[pb->n_patterns] = items;
+    uint32_t nm = 0, fb_mask = 0;
+    GFOR(g, it, items) {
+        bool ok = it < items;
+        unsigned pi = 0, nt = 1;
+        uint32_t idx[3] = { NONE32, NONE32, NONE32 }, pos[3] = { NONE32, NONE32, NONE32 };
+        unsigned long long r = 0;
+        if (ok) {
+            while (pref[pi + 1] <= it) pi++;
+            const cl_pattern &p = pb->p[pi];
+            nt = p.n_templates;
+            uint32_t cn[3] = { 1, 1, 1 };
+            const unsigned ta = p.join_order[0];
+            for (unsigned t = 0; t < nt; t++) { const int c = class_of(s, p.t[t].op); cn[t] = s.cls_off[c + 1] - s.cls_off[c]; }
+            idx[ta] = lo + s.cand[s.cls_off[class_of(s, p.t[ta].op)] + (it - pref[pi])];
+            for (unsigned k = 1; k < nt && ok; k++) {
+                const unsigned t = p.join_order[k], from = p.join_from[k];
+                const cl_hdr hf = s.S.hdr[idx[from]];
+                const cl_template &tf = p.t[from];
+                if (hf.n_defs != tf.n_defs || hf.n_aux != tf.n_aux || hf.n_uses != tf.n_uses || (hf.flags & CL_IF_EXT)) { ok = false; break; }
+                const opnd o = get_slot(s, hf, idx[from], has_guard(hf) + p.join_slot[k]);
+                if (!is_value(o)) { fb_mask |= 1u << pi; ok = false; break; }           /* not an SSA link */
+                const uint32_t dp = o.pay < s.cap.V ? s.defpos[o.pay] : NONE32;
+                if (dp == NONE32 || dp < lo || dp >= lo + n || s.S.hdr[dp].op != p.t[t].op) { ok = false; break; }
+                idx[t] = dp;
+            }
+            if (ok && nt > 1) ok = idx[0] < idx[1] && (nt < 3 || idx[1] < idx[2]);
+            if (ok) {
+                r = s.cidx[idx[0] - lo];
+                if (nt > 1) r = r * cn[1] + s.cidx[idx[1] - lo];
+                if (nt > 2) r = r * cn[2] + s.cidx[idx[2] - lo];
+                ok = r < pb->budget;
+            }
+            if (ok) { Bind b; ok = check_tuple(s, p, idx, b); }
+            for (unsigned t = 0; t < nt; t++) pos[t] = idx[t] - lo;
+        }
+        append_match(g, s, nm, ok, pi, nt, pos, r);
+    }
+    if (nm > s.cap.M) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }
+    if (g.any(fb_mask != 0)) {
+        /* rare: drop what the join found for those patterns and enumerate their product */
+        uint32_t all = 0;
+        for (unsigned pi = 0; pi < pb->n_patterns; pi++) if (g.any((fb_mask >> pi) & 1u)) all |= 1u << pi;
+        g.sync();
+        uint32_t kept = 0;
+        const uint32_t have = nm < s.cap.M ? nm : s.cap.M;
+        if (g.rank == 0) {
+            for (uint32_t m = 0; m < have; m++) if (!((all >> s.mt[m].pat) & 1u)) s.mt[kept++] = s.mt[m];
+        }
+        nm = g.bcast0(kept);
+        product_mask |= all;
+        g.sync();
+    }
+    for (unsigned pi = 0; pi < pb->n_patterns; pi++)
+        if ((product_mask >> pi) & 1u) match_product(g, s, lo, pi, nm);
     g.sync();
     if (nm > s.cap.M) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }
     return nm;
@@ -579,6 +682,7 @@ CLD unsigned long long match_key(const MatchRec &m) {
 }
 template <class G> CLF uint32_t select_block(const G &g, FS &s, uint32_t n, uint32_t nm, uint32_t bi,
                                              uint32_t nsel) {
+    PROF(g, s, PF_SELECT);
     GFOR(g, p, n) if (p < n) { s.keep[p] = 0; s.sel_at[p] = NONE32; }
     g.sync();
     for (;;) {
@@ -642,40 +746,58 @@ template <class G> CLF void emit_match_events(const G &g, FS &s, uint32_t seq, u
 }
 
 /* ------------------------------------------------------------------ rewrites */
-/* One lane plans one selected match.  The same code runs twice: a COUNT pass
- * (allocation counts, escape decisions, refusal) and, after an exclusive scan
- * over the block's matches in select order (G3), a WRITE pass that replays
- * the logged escape decisions and emits with the scanned bases.             */
-struct RW {
-    FS *s;
-    bool write, store;
-    uint32_t vid, iid, imm;        /* allocation cursors                        */
-    uint32_t nins, out;            /* records emitted / first output position   */
-    uint32_t esc, esc_n;           /* escape query log                          */
-    uint32_t idx[3];               /* stream positions of the matched records   */
-    cl_hdr h[3];
-    unsigned n, pat;
-    unsigned rm;                   /* removal mask (bit t = instruction t)      */
-    bool retag;
-    Bind b;
+/* One lane plans one selected match, once, into a staging record: new
+ * instructions, values and immediates carry ids *relative* to the match
+ * (CL_T_REL in the slot tag).  An exclusive scan over the block's matches in
+ * select order then yields the id bases (vid, iid and immediate index are
+ * allocated in exactly the reference's order, G3; refused rewrites keep what
+ * they allocated before giving up, G4) and a fix-up pass writes the records
+ * to their final place.                                                     */
+static constexpr uint16_t CL_T_REL = 1u << 15;      /* payload is relative to the match's base */
+static constexpr int ST_RECS = 6, ST_VALS = 4, ST_IMMS = 8, ST_UPD = 3, ST_DROP = 4;
+
+struct Stage {
+    Rec rec[ST_RECS];
+    cl_imm imm[ST_IMMS];
+    uint32_t val_origin[ST_VALS];
+    int32_t val_def[ST_VALS];      /* relative iid of the defining record, -1 none */
+    uint32_t upd_vid[ST_UPD], upd_iid[ST_UPD];   /* existing values redefined (relative iid) */
+    uint32_t drop_vid[ST_DROP];
+    uint8_t ok, rm, nins, retag, nv, nq, nupd, ndrop;
+    uint32_t ni;                   /* iids taken, orphans included                 */
+    uint32_t vbase, ibase, mbase;  /* after the scan                               */
 };
 
-CLD uint32_t rw_value(RW &c, uint32_t origin) {
-    const uint32_t v = c.vid++;
-    if (c.write && v < c.s->cap.V) { c.s->alive[v] = 1; c.s->def_iid[v] = -1; c.s->origin[v] = origin; c.s->usecnt[v] = 0; c.s->defpos[v] = NONE32; }
-    return v;
-}
-CLD opnd rw_imm(RW &c, unsigned long long bits, unsigned long long text, bool hextext) {
-    const uint32_t q = c.imm++;
-    if (c.write && q < c.s->cap.Q) { cl_imm im; im.bits = bits; im.text = text; c.s->imm[q] = im; }
-    opnd o; o.tag = (uint16_t)(CL_K_IMM | (hextext ? CL_T_IMM_HEXTEXT : 0)); o.pay = q;
+struct RW {
+    FS *s;
+    Stage *st;
+    uint32_t idx[3];               /* stream positions of the matched records      */
+    cl_hdr h[3];
+    unsigned n, pat;
+    bool overflow;
+};
+
+CLD opnd rw_value(RW &c, uint32_t origin) {               /* LiftedFunction.new_value */
+    Stage &st = *c.st;
+    opnd o; o.tag = (uint16_t)(CL_K_VALUE | CL_T_REL); o.pay = st.nv;
+    if (st.nv < ST_VALS) { st.val_origin[st.nv] = origin; st.val_def[st.nv] = -1; st.nv++; } else c.overflow = true;
     return o;
 }
-/* LiftedFunction.make_inst (ssir.py:237-241)                                  */
+CLD opnd rw_imm(RW &c, unsigned long long bits, unsigned long long text, bool hextext) {
+    Stage &st = *c.st;
+    opnd o; o.tag = (uint16_t)(CL_K_IMM | CL_T_REL | (hextext ? CL_T_IMM_HEXTEXT : 0)); o.pay = st.nq;
+    if (st.nq < ST_IMMS) { st.imm[st.nq].bits = bits; st.imm[st.nq].text = text; st.nq++; } else c.overflow = true;
+    return o;
+}
+/* bits/text of an immediate operand, staged or already in the function's table */
+CLD cl_imm rw_imm_of(const RW &c, opnd o) {
+    return (o.tag & CL_T_REL) ? c.st->imm[o.pay & (ST_IMMS - 1)] : c.s->imm[o.pay];
+}
+/* LiftedFunction.make_inst (ssir.py:237-241); iid relative                    */
 CLD Rec rw_make(RW &c, uint16_t op, uint16_t modset, const opnd *defs, unsigned nd, const opnd *uses,
                 unsigned nu) {
     Rec r;
-    r.h.iid = c.iid++;
+    r.h.iid = c.st->ni++;
     r.h.op = op; r.h.modset = modset;
     r.h.n_defs = (uint8_t)nd; r.h.n_aux = 0; r.h.n_uses = (uint8_t)nu; r.h.flags = 0; r.h.ext = 0;
     unsigned k = 0;
@@ -685,108 +807,89 @@ CLD Rec rw_make(RW &c, uint16_t op, uint16_t modset, const opnd *defs, unsigned 
     return r;
 }
 CLD void rw_push(RW &c, const Rec &r) {
-    if (c.write && c.store) {
-        FS &s = *c.s;
-        st_rec(s, c.out + c.nins, r);
-        const unsigned u0 = (unsigned)r.h.n_defs;
-        for (unsigned k = 0; k < r.h.n_uses; k++) {          /* new records hold no guard / MemRef of their own */
-            const unsigned kk = u0 + k;
-            if (kind_of(r.tag[kk]) == CL_K_VALUE) { if (r.pay[kk] < s.cap.V) a_add(&s.usecnt[r.pay[kk]], 1u); }
-            else if (kind_of(r.tag[kk]) == CL_K_MEMREF) {
-                const cl_memref &m = s.mem[r.pay[kk]];
-                if (kind_of(m.base_tag) == CL_K_VALUE) a_add(&s.usecnt[m.base_pay], 1u);
-                if (kind_of(m.ureg_tag) == CL_K_VALUE) a_add(&s.usecnt[m.ureg_pay], 1u);
-            }
-        }
-    }
-    c.nins++;
+    Stage &st = *c.st;
+    if (st.nins < ST_RECS) st.rec[st.nins++] = r; else c.overflow = true;
 }
-CLD void rw_set_def_iid(RW &c, uint32_t vid, uint32_t iid) {
-    if (c.write && vid < c.s->cap.V) c.s->def_iid[vid] = (int32_t)iid;
+/* info.def_iid = inst.iid for a staged (relative) or an existing value        */
+CLD void rw_set_def_iid(RW &c, opnd v, uint32_t iid_rel) {
+    Stage &st = *c.st;
+    if (v.tag & CL_T_REL) { if (v.pay < (uint32_t)ST_VALS) st.val_def[v.pay] = (int32_t)iid_rel; }
+    else if (st.nupd < ST_UPD) { st.upd_vid[st.nupd] = v.pay; st.upd_iid[st.nupd] = iid_rel; st.nupd++; }
+    else c.overflow = true;
 }
 CLD void rw_drop(RW &c, opnd o) {                       /* _drop_values :314-317 */
-    if (c.write && c.store && is_value(o) && o.pay < c.s->cap.V) c.s->alive[o.pay] = 0;
+    Stage &st = *c.st;
+    if (!is_value(o)) return;
+    if (st.ndrop < ST_DROP) st.drop_vid[st.ndrop++] = o.pay; else c.overflow = true;
 }
-CLD void rw_fail(RW &c, uint32_t code) { if (!c.write) fail(*c.s, code); }
+CLD void rw_fail(RW &c, uint32_t code) { fail(*c.s, code); }
 
 /* _escapes (patterns.py:259-263) against the def-use snapshot of the block:
  * a value escapes iff it has more use sites than the group itself holds.    */
 CLF bool rw_escapes(RW &c, uint32_t vid) {
-    bool r;
-    if (c.write) r = (c.esc >> c.esc_n) & 1u;
-    else {
-        FS &s = *c.s;
-        uint32_t inside = 0;
-        for (unsigned t = 0; t < c.n; t++)
-            for_value_operands(s, c.h[t], c.idx[t], [&](uint32_t v) { inside += v == vid; });
-        r = vid < s.cap.V && s.usecnt[vid] != inside;
-        if (r) c.esc |= 1u << c.esc_n;
-    }
-    c.esc_n++;
-    return r;
+    FS &s = *c.s;
+    uint32_t inside = 0;
+    for (unsigned t = 0; t < c.n; t++)
+        for_value_operands(s, c.h[t], c.idx[t], [&](uint32_t v) { inside += v == vid; });
+    return vid < s.cap.V && s.usecnt[vid] != inside;
 }
 /* _safe (patterns.py:266-275)                                                 */
 CLF bool rw_safe(RW &c, const opnd *redef, unsigned nredef) {
     FS &s = *c.s;
-    bool ok = true;
-    for (unsigned t = 0; t < c.n && ok; t++) {
+    for (unsigned t = 0; t < c.n; t++) {
         const unsigned d0 = def0(c.h[t]), nd = (unsigned)c.h[t].n_defs + c.h[t].n_aux;
-        for (unsigned k = 0; k < nd && ok; k++) {
+        for (unsigned k = 0; k < nd; k++) {
             opnd d = get_slot(s, c.h[t], c.idx[t], d0 + k);
             if (!is_value(d)) continue;
             bool re = false;
             for (unsigned j = 0; j < nredef; j++) re |= is_value(redef[j]) && redef[j].pay == d.pay;
-            if (!re && rw_escapes(c, d.pay)) ok = false;
+            if (!re && rw_escapes(c, d.pay)) return false;
         }
     }
-    return ok;
+    return true;
 }
 /* _pack_pair (patterns.py:278-300); CL_K_NONE stands for None                 */
 CLF opnd rw_pack_pair(RW &c, opnd lo, opnd hi) {
-    FS &s = *c.s;
     const bool lo_zero = is_zero(lo), hi_zero = is_zero(hi);
     opnd none; none.tag = CL_K_NONE; none.pay = 0;
     if (lo_zero && hi_zero) return none;
     if (is_imm(lo) && hi_zero) {
-        const cl_imm im = s.imm[lo.pay];
+        const cl_imm im = rw_imm_of(c, lo);
         return rw_imm(c, im.bits & 0xFFFFFFFFull, im.text, (lo.tag & CL_T_IMM_HEXTEXT) != 0);
     }
     if (is_imm(lo) && is_imm(hi)) {
-        const unsigned long long bits = (s.imm[lo.pay].bits & 0xFFFFFFFFull) | (s.imm[hi.pay].bits & 0xFFFFFFFFull) << 32;
+        const unsigned long long bits = (rw_imm_of(c, lo).bits & 0xFFFFFFFFull) | (rw_imm_of(c, hi).bits & 0xFFFFFFFFull) << 32;
         return rw_imm(c, bits, bits, true);
     }
     if (lo_zero && is_imm(hi)) {
-        const unsigned long long bits = (s.imm[hi.pay].bits & 0xFFFFFFFFull) << 32;
+        const unsigned long long bits = (rw_imm_of(c, hi).bits & 0xFFFFFFFFull) << 32;
         return rw_imm(c, bits, bits, true);
     }
-    const uint32_t v = rw_value(c, CL_ORG_PAIR);
+    opnd d = rw_value(c, CL_ORG_PAIR);
     opnd u[2];
     u[0] = lo_zero ? rw_imm(c, 0, 0, true) : strip(lo);
     u[1] = hi_zero ? rw_imm(c, 0, 0, true) : strip(hi);
-    opnd d = value_ref(v);
     Rec pk = rw_make(c, CL_OP_PACK64, CL_MS_NONE, &d, 1, u, 2);
-    rw_set_def_iid(c, v, pk.h.iid);
+    rw_set_def_iid(c, d, pk.h.iid);
     rw_push(c, pk);
     return d;
 }
 /* _unpack_into (patterns.py:303-311)                                          */
-CLF void rw_unpack_into(RW &c, uint32_t src, opnd lo_ref, opnd hi_ref) {
+CLF void rw_unpack_into(RW &c, opnd src, opnd lo_ref, opnd hi_ref) {
     opnd refs[2] = { lo_ref, hi_ref };
     for (int k = 0; k < 2; k++) {
         if (!is_value(refs[k])) continue;
-        opnd d = value_ref(refs[k].pay), u = value_ref(src);
-        Rec up = rw_make(c, CL_OP_UNPACK64, k ? CL_MS_HI : CL_MS_LO, &d, 1, &u, 1);
-        if (!c.write && !(d.pay < c.s->cap.V && c.s->alive[d.pay])) { rw_fail(c, CL_ST_KEY_ERROR); return; }
-        rw_set_def_iid(c, d.pay, up.h.iid);
+        opnd d = value_ref(refs[k].pay);
+        Rec up = rw_make(c, CL_OP_UNPACK64, k ? CL_MS_HI : CL_MS_LO, &d, 1, &src, 1);
+        if (!(d.pay < c.s->cap.V && c.s->alive[d.pay])) { rw_fail(c, CL_ST_KEY_ERROR); return; }
+        rw_set_def_iid(c, d, up.h.iid);
         rw_push(c, up);
     }
 }
 CLD bool rw_redefine(RW &c, opnd res, uint32_t iid) {
-    if (!c.write) {
-        if (!is_value(res)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
-        if (!(res.pay < c.s->cap.V && c.s->alive[res.pay])) { rw_fail(c, CL_ST_KEY_ERROR); return false; }
-    }
-    rw_set_def_iid(c, res.pay, iid);
+    if (!is_value(res)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
+    if (!(res.pay < c.s->cap.V && c.s->alive[res.pay])) { rw_fail(c, CL_ST_KEY_ERROR); return false; }
+    rw_set_def_iid(c, value_ref(res.pay), iid);
     return true;
 }
 
@@ -809,32 +912,33 @@ CLF bool rw_iadd364(RW &c) {
         } else if (neg_lo && not_hi) {
             opnd p = rw_pack_pair(c, strip(lo_op), strip(hi_op));
             if (is_none(p)) return false;
-            if (is_imm(p)) {
-                /* Imm(-p.int_value(64) & M64, p.text): in the COUNT pass the table entry of p
-                 * does not exist yet, so recompute it the way rw_pack_pair did.              */
-                unsigned long long bits, text; bool hx;
-                const bool lz = is_zero(lo_op), hz = is_zero(hi_op);
-                if (is_imm(lo_op) && hz) { const cl_imm im = s.imm[lo_op.pay]; bits = im.bits & 0xFFFFFFFFull; text = im.text; hx = (lo_op.tag & CL_T_IMM_HEXTEXT) != 0; }
-                else if (is_imm(lo_op) && is_imm(hi_op)) { bits = (s.imm[lo_op.pay].bits & 0xFFFFFFFFull) | (s.imm[hi_op.pay].bits & 0xFFFFFFFFull) << 32; text = bits; hx = true; }
-                else { (void)lz; bits = (s.imm[hi_op.pay].bits & 0xFFFFFFFFull) << 32; text = bits; hx = true; }
-                ops[nops++] = rw_imm(c, 0ull - bits, text, hx);
+            if (is_imm(p)) {                       /* Imm(-p.int_value(64) & M64, p.text) :348 */
+                const cl_imm im = rw_imm_of(c, p);
+                ops[nops++] = rw_imm(c, 0ull - im.bits, im.text, (p.tag & CL_T_IMM_HEXTEXT) != 0);
             } else {
                 p.tag |= CL_T_NEG;
                 ops[nops++] = p;
             }
         } else
-            return false;
+            return false;                          /* mixed negation :353 */
     }
     if (!nops) return false;
-    const uint32_t res = rw_value(c, CL_ORG_PAIR);
-    opnd d = value_ref(res);
+    opnd d = rw_value(c, CL_ORG_PAIR);
     Rec agg = rw_make(c, CL_OP_IADD364, CL_MS_NONE, &d, 1, ops, nops);
-    rw_set_def_iid(c, res, agg.h.iid);
+    rw_set_def_iid(c, d, agg.h.iid);
     rw_push(c, agg);
-    rw_unpack_into(c, res, redef[0], redef[1]);
+    rw_unpack_into(c, d, redef[0], redef[1]);
     rw_drop(c, carry);
-    c.rm = 3;
+    c.st->rm = 3;
     return true;
+}
+/* "mod:<var>" binding of _match_opcode (patterns.py:163-166) for the matched
+ * instruction t: first modifier of its tuple that belongs to the choice group */
+CLD unsigned rw_modvar(const RW &c, unsigned t, unsigned modvar) {
+    const cl_template &tm = c.s->pb->p[c.pat].t[t];
+    for (unsigned k = 0; k < tm.n_modvars; k++)
+        if (tm.modvar_var[k] == modvar) return c.s->ms[c.h[t].modset].first[tm.modvar_group[k]];
+    return 0;
 }
 /* _rw_isetp64 (patterns.py:371-390)                                           */
 CLF bool rw_isetp64(RW &c) {
@@ -843,8 +947,8 @@ CLF bool rw_isetp64(RW &c) {
     const cl_hdr &lo = c.h[0], &hi = c.h[1];
     opnd res = get_def(s, hi, c.idx[1], 0);
     if (!rw_safe(c, &res, 1)) return false;
-    const unsigned cond = s.pb->group_pos[c.b.var[CL_MAX_VARS + p.modvar_cond].v & 63];
-    const unsigned bop = s.pb->group_pos[c.b.var[CL_MAX_VARS + p.modvar_bop].v & 63];
+    const unsigned cond = s.pb->group_pos[rw_modvar(c, 0, p.modvar_cond) & 63];
+    const unsigned bop = s.pb->group_pos[rw_modvar(c, 0, p.modvar_bop) & 63];
     const unsigned unsigned_hi = has_mod(s, hi, CL_MB_U32);
     opnd u[3];
     u[0] = rw_pack_pair(c, get_use(s, lo, c.idx[0], 0), get_use(s, hi, c.idx[1], 0));
@@ -858,7 +962,7 @@ CLF bool rw_isetp64(RW &c) {
     if (!rw_redefine(c, res, agg.h.iid)) return false;
     rw_push(c, agg);
     rw_drop(c, get_def(s, lo, c.idx[0], 0));
-    c.rm = 3;
+    c.st->rm = 3;
     return true;
 }
 /* _rw_lea64 (patterns.py:393-411)                                             */
@@ -871,35 +975,29 @@ CLF bool rw_lea64(RW &c) {
     opnd a64 = rw_pack_pair(c, get_use(s, lo, c.idx[0], 0), get_use(s, hi, c.idx[1], 2));
     opnd b64 = rw_pack_pair(c, get_use(s, lo, c.idx[0], 1), get_use(s, hi, c.idx[1], 1));
     if (is_none(a64) || is_none(b64)) return false;
-    const uint32_t res = rw_value(c, CL_ORG_PAIR);
-    opnd d = value_ref(res), u[3] = { b64, a64, get_use(s, lo, c.idx[0], 2) };
+    opnd d = rw_value(c, CL_ORG_PAIR), u[3] = { b64, a64, get_use(s, lo, c.idx[0], 2) };
     Rec agg = rw_make(c, CL_OP_LEA64, CL_MS_NONE, &d, 1, u, 3);
-    rw_set_def_iid(c, res, agg.h.iid);
+    rw_set_def_iid(c, d, agg.h.iid);
     rw_push(c, agg);
-    rw_unpack_into(c, res, redef[0], redef[1]);
+    rw_unpack_into(c, d, redef[0], redef[1]);
     rw_drop(c, carry);
-    c.rm = 3;
+    c.st->rm = 3;
     return true;
 }
-/* _rw_imad_wide (patterns.py:414-418): in-place retag                         */
+/* _rw_imad_wide (patterns.py:414-418): in-place retag, applied by the fix-up  */
 CLF bool rw_imad_wide(RW &c) {
-    if (c.write) {
-        cl_hdr &h = c.s->S.hdr[c.idx[0]];
-        h.modset = c.s->ms[h.modset].minus_wide;
-        h.op = CL_OP_IMAD64;
-    }
-    c.retag = true;
+    c.st->retag = 1;
     return true;
 }
 /* tail of mov64 / cast64 / shl64 / shr64 (patterns.py:433-439 and alike)      */
 CLF bool rw_finish_pack(RW &c, const Rec &agg, unsigned n_feed) {
     FS &s = *c.s;
     rw_push(c, agg);
-    c.rm = 1u << n_feed;
+    c.st->rm = (uint8_t)(1u << n_feed);
     for (unsigned t = 0; t < n_feed; t++) {
         opnd d = get_def(s, c.h[t], c.idx[t], 0);
         if (!is_value(d)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
-        if (!rw_escapes(c, d.pay)) { rw_drop(c, d); c.rm |= 1u << t; }
+        if (!rw_escapes(c, d.pay)) { rw_drop(c, d); c.st->rm |= (uint8_t)(1u << t); }
     }
     return true;
 }
@@ -944,15 +1042,29 @@ CLF bool rw_shift64(RW &c, bool right) {
     if (!rw_redefine(c, res, agg.h.iid)) return false;
     return rw_finish_pack(c, agg, 2);
 }
-/* _var_operand (patterns.py:514-524)                                          */
-CLD bool rw_var_operand(RW &c, okey k, opnd *out) {
-    switch (k.cls) {
-    case KC_V: *out = value_ref((uint32_t)k.v); return true;
-    case KC_IMM: *out = rw_imm(c, k.v, k.v, true); return true;
-    case KC_CM: out->tag = (uint16_t)(CL_K_CONSTMEM | 1u << CL_T_WIDTH_SHIFT); out->pay = (uint32_t)k.v; return true;
-    case KC_RZ: out->tag = CL_K_RZ; out->pay = 0; return true;
-    default: rw_fail(c, k.cls == KC_NONE ? CL_ST_KEY_ERROR : CL_ST_ASSERTION_ERROR); return false;
+/* Binding of a pattern variable = key of the first slot (template order, then
+ * defs/aux/uses) that mentions it -- what Bindings.vars holds after a
+ * successful unification.  Then _var_operand (patterns.py:514-524).           */
+CLF bool rw_var_operand(RW &c, unsigned var, opnd *out) {
+    FS &s = *c.s;
+    const cl_pattern &p = s.pb->p[c.pat];
+    for (unsigned t = 0; t < c.n; t++) {
+        const cl_template &tm = p.t[t];
+        const unsigned ns = (unsigned)tm.n_defs + tm.n_aux + tm.n_uses;
+        for (unsigned k = 0; k < ns; k++) {
+            if (tm.slot[k].kind != CL_S_VAR || tm.slot[k].var != var) continue;
+            const okey key = operand_key(s, get_slot(s, c.h[t], c.idx[t], has_guard(c.h[t]) + k));
+            switch (key.cls) {
+            case KC_V: *out = value_ref((uint32_t)key.v); return true;
+            case KC_IMM: *out = rw_imm(c, key.v, key.v, true); return true;
+            case KC_CM: out->tag = (uint16_t)(CL_K_CONSTMEM | 1u << CL_T_WIDTH_SHIFT); out->pay = (uint32_t)key.v; return true;
+            case KC_RZ: out->tag = CL_K_RZ; out->pay = 0; return true;
+            default: rw_fail(c, CL_ST_ASSERTION_ERROR); return false;
+            }
+        }
     }
+    rw_fail(c, CL_ST_KEY_ERROR);
+    return false;
 }
 /* _rw_xmad (patterns.py:498-511)                                              */
 CLF bool rw_xmad(RW &c) {
@@ -961,9 +1073,9 @@ CLF bool rw_xmad(RW &c) {
     opnd dres = get_def(s, c.h[2], c.idx[2], 0);
     if (!rw_safe(c, &dres, 1)) return false;
     opnd u[3];
-    if (!rw_var_operand(c, c.b.var[p.var_a & 15], &u[0])) return false;
-    if (!rw_var_operand(c, c.b.var[p.var_b & 15], &u[1])) return false;
-    if (!rw_var_operand(c, c.b.var[p.var_c & 15], &u[2])) return false;
+    if (!rw_var_operand(c, p.var_a, &u[0])) return false;
+    if (!rw_var_operand(c, p.var_b, &u[1])) return false;
+    if (!rw_var_operand(c, p.var_c, &u[2])) return false;
     if (!is_value(dres)) { rw_fail(c, CL_ST_ATTRIBUTE_ERROR); return false; }
     opnd d = value_ref(dres.pay);
     Rec agg = rw_make(c, CL_OP_IMAD, CL_MS_NONE, &d, 1, u, 3);
@@ -971,7 +1083,7 @@ CLF bool rw_xmad(RW &c) {
     rw_push(c, agg);
     for (unsigned t = 0; t < 2; t++)
         for (unsigned k = 0; k < c.h[t].n_defs; k++) rw_drop(c, get_def(s, c.h[t], c.idx[t], k));
-    c.rm = 7;
+    c.st->rm = 7;
     return true;
 }
 CLF bool run_rewrite(RW &c) {
@@ -989,12 +1101,44 @@ CLF bool run_rewrite(RW &c) {
     rw_fail(c, CL_ST_UNSUPPORTED);
     return false;
 }
-CLF void rw_setup(RW &c, FS &s, const SelRec &m, uint32_t lo) {
-    c.s = &s; c.n = m.n; c.pat = m.pat;
-    c.nins = 0; c.esc_n = 0; c.rm = 0; c.retag = false;
-    for (unsigned t = 0; t < m.n; t++) { c.idx[t] = lo + m.pos[t]; c.h[t] = s.S.hdr[c.idx[t]]; }
-    for (unsigned t = m.n; t < 3; t++) c.idx[t] = NONE32;
-    check_tuple(s, s.pb->p[m.pat], c.idx, c.b);          /* rebuild the bindings */
+
+/* fix-up of one staged match once the bases are known                        */
+CLF void apply_stage(FS &s, const SelRec &m, Stage &st, uint32_t lo, uint32_t out) {
+    for (unsigned k = 0; k < st.nv; k++) {
+        const uint32_t v = st.vbase + k;
+        if (v >= s.cap.V) continue;
+        s.alive[v] = 1; s.origin[v] = st.val_origin[k];
+        s.def_iid[v] = st.val_def[k] < 0 ? -1 : (int32_t)(st.ibase + (uint32_t)st.val_def[k]);
+        s.usecnt[v] = 0; s.defpos[v] = NONE32;
+    }
+    for (unsigned k = 0; k < st.nq; k++) if (st.mbase + k < s.cap.Q) s.imm[st.mbase + k] = st.imm[k];
+    if (!st.ok) return;                      /* refused: the allocations above leak (G4) */
+    for (unsigned r = 0; r < st.nins; r++) {
+        Rec rec = st.rec[r];
+        rec.h.iid += st.ibase;
+        const unsigned ns = (unsigned)rec.h.n_defs + rec.h.n_uses;
+        for (unsigned k = 0; k < ns; k++) {
+            if (rec.tag[k] & CL_T_REL) {
+                rec.pay[k] += kind_of(rec.tag[k]) == CL_K_VALUE ? st.vbase : st.mbase;
+                rec.tag[k] &= (uint16_t)~CL_T_REL;
+            }
+            if (k < rec.h.n_defs) continue;
+            if (kind_of(rec.tag[k]) == CL_K_VALUE) { if (rec.pay[k] < s.cap.V) a_add(&s.usecnt[rec.pay[k]], 1u); }
+            else if (kind_of(rec.tag[k]) == CL_K_MEMREF) {
+                const cl_memref &mr = s.mem[rec.pay[k]];
+                if (kind_of(mr.base_tag) == CL_K_VALUE) a_add(&s.usecnt[mr.base_pay], 1u);
+                if (kind_of(mr.ureg_tag) == CL_K_VALUE) a_add(&s.usecnt[mr.ureg_pay], 1u);
+            }
+        }
+        st_rec(s, out + r, rec);
+    }
+    for (unsigned k = 0; k < st.nupd; k++) if (st.upd_vid[k] < s.cap.V) s.def_iid[st.upd_vid[k]] = (int32_t)(st.ibase + st.upd_iid[k]);
+    for (unsigned k = 0; k < st.ndrop; k++) if (st.drop_vid[k] < s.cap.V) s.alive[st.drop_vid[k]] = 0;
+    if (st.retag) {                          /* _rw_imad_wide :414-418 */
+        cl_hdr &h = s.S.hdr[lo + m.pos[0]];
+        h.modset = s.ms[h.modset].minus_wide;
+        h.op = CL_OP_IMAD64;
+    }
 }
 
 /* _apply_patterns (patterns.py:671-707): one round over all blocks.
@@ -1005,6 +1149,7 @@ CLF void rw_setup(RW &c, FS &s, const SelRec &m, uint32_t lo) {
  * end of the gap buffer to the left.                                        */
 template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table, uint32_t phase) {
     setup_classes(s, table);
+    build_usecount(g, s);                 /* def positions for the join, use counts for the escapes */
     uint32_t nsel = 0;
     for (uint32_t bi = 0; bi < s.nb; bi++) {
         const uint32_t lo = s.bo[bi], n = s.bo[bi + 1] - lo;
@@ -1027,7 +1172,6 @@ template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table
     g.sync();
     if (nsel == 0) return 0;
 
-    build_usecount(g, s);
     const uint32_t shift = s.cap.I - s.n;                    /* right-align the stream */
     move_recs(g, s, shift, 0, s.n);
     uint32_t wr = 0, total_ok = 0;
@@ -1040,37 +1184,41 @@ template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table
             wr += n;
             continue;
         }
-        /* COUNT pass */
+        PROF(g, s, PF_PLAN);
         GFOR(g, p, n) if (p < n) { s.keep[p] = 1; s.inscnt[p] = 0; }
         g.sync();
+        /* plan: one lane per match, once */
+        bool over = false;
         GFOR(g, j, ns) if (j < ns) {
+            const SelRec m = s.sel[j0 + j];
+            Stage &st = s.stage[j0 + j];
+            st.ok = st.rm = st.nins = st.retag = st.nv = st.nq = st.nupd = st.ndrop = 0;
+            st.ni = 0;
             RW c;
-            c.write = false; c.store = false; c.vid = c.iid = c.imm = 0; c.out = 0; c.esc = 0;
-            rw_setup(c, s, s.sel[j0 + j], lo);
-            const bool ok = run_rewrite(c);
-            Plan pl;
-            pl.ok = ok; pl.rm = (uint8_t)c.rm; pl.nins = (uint8_t)c.nins; pl.retag = c.retag;
-            pl.esc = c.esc; pl.nv = c.vid; pl.ni = c.iid; pl.nm = c.imm;
-            pl.vbase = pl.ibase = pl.mbase = 0;
-            s.plan[j0 + j] = pl;
+            c.s = &s; c.st = &st; c.n = m.n; c.pat = m.pat; c.overflow = false;
+            for (unsigned t = 0; t < m.n; t++) { c.idx[t] = lo + m.pos[t]; c.h[t] = s.S.hdr[c.idx[t]]; }
+            for (unsigned t = m.n; t < 3; t++) c.idx[t] = NONE32;
+            st.ok = run_rewrite(c);
+            over |= c.overflow;
         }
+        if (g.any(over)) fail(s, CL_ST_UNSUPPORTED);
         g.sync();
         if (status(s)) return 0;
         /* exclusive scans in select order: id bases (G3) */
         uint32_t vb = s.next_vid, ib = s.next_iid, mb = s.n_imm, okc = 0;
         GFOR(g, j, ns) {
             uint32_t nv = 0, ni = 0, nq = 0, ok = 0;
-            if (j < ns) { const Plan &pl = s.plan[j0 + j]; nv = pl.nv; ni = pl.ni; nq = pl.nm; ok = pl.ok; }
+            if (j < ns) { const Stage &st = s.stage[j0 + j]; nv = st.nv; ni = st.ni; nq = st.nq; ok = st.ok; }
             uint32_t tv, ti, tq, to;
             const uint32_t ov = g.exscan(nv, tv), oi = g.exscan(ni, ti), oq = g.exscan(nq, tq);
             g.exscan(ok, to);
             if (j < ns) {
-                Plan &pl = s.plan[j0 + j];
-                pl.vbase = vb + ov; pl.ibase = ib + oi; pl.mbase = mb + oq;
+                Stage &st = s.stage[j0 + j];
+                st.vbase = vb + ov; st.ibase = ib + oi; st.mbase = mb + oq;
                 const SelRec &m = s.sel[j0 + j];
-                if (pl.ok) {
-                    s.inscnt[m.pos[m.n - 1]] = pl.nins;                  /* anchor :689 */
-                    for (unsigned t = 0; t < m.n; t++) if (pl.rm >> t & 1) s.keep[m.pos[t]] = 0;
+                if (st.ok) {
+                    s.inscnt[m.pos[m.n - 1]] = st.nins;                  /* anchor :689 */
+                    for (unsigned t = 0; t < m.n; t++) if (st.rm >> t & 1) s.keep[m.pos[t]] = 0;
                 }
             }
             vb += tv; ib += ti; mb += tq; okc += to;
@@ -1088,22 +1236,17 @@ template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table
         }
         if (wr + tot > lo) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }     /* gap exhausted */
         g.sync();
-        /* WRITE pass */
+        /* fix-up: staged records to their place, value table, immediates */
         GFOR(g, j, ns) if (j < ns) {
-            const Plan pl = s.plan[j0 + j];
             const SelRec m = s.sel[j0 + j];
-            RW c;
-            c.write = true; c.store = pl.ok != 0;
-            c.vid = pl.vbase; c.iid = pl.ibase; c.imm = pl.mbase; c.esc = pl.esc;
-            c.out = wr + s.outpos[m.pos[m.n - 1]];
-            rw_setup(c, s, m, lo);
-            run_rewrite(c);
-            if (!pl.ok) push_event(s, phase << 28 | bi, CL_EV_REFUSED, j, m.pat, s.blk[bi].bid, 0, 0);
+            Stage &st = s.stage[j0 + j];
+            apply_stage(s, m, st, lo, wr + s.outpos[m.pos[m.n - 1]]);
+            if (!st.ok) push_event(s, phase << 28 | bi, CL_EV_REFUSED, j, m.pat, s.blk[bi].bid, 0, 0);
         }
         if (g.rank == 0)
             for (uint32_t j = 0; j < ns; j++) {
                 const unsigned pat = s.sel[j0 + j].pat;
-                if (s.plan[j0 + j].ok) s.st_rewrites[pat]++; else s.st_refused[pat]++;
+                if (s.stage[j0 + j].ok) s.st_rewrites[pat]++; else s.st_refused[pat]++;
             }
         g.sync();
         /* kept records move left; removed ones give their uses back */
@@ -1169,6 +1312,7 @@ template <class G> CLF void compact_stream(const G &g, FS &s) {
  * rounds is the least fixpoint of "dead", which chaotic iteration reaches in
  * any order, so dead marks and use-count decrements are applied on the fly. */
 template <class G> CLF uint32_t remove_dead_pseudo(const G &g, FS &s) {
+    PROF(g, s, PF_DCE);
     build_usecount(g, s);
     GFOR(g, i, s.n) if (i < s.n) s.keep[i] = 1;
     g.sync();
@@ -1201,6 +1345,7 @@ CLD uint32_t final_of(const FS &s, uint32_t v) {
     return v;
 }
 template <class G> CLF uint32_t simplify_packs(const G &g, FS &s) {
+    PROF(g, s, PF_SIMPLIFY);
     build_usecount(g, s);
     GFOR(g, v, s.next_vid) if (v < s.next_vid) s.redirect[v] = NONE32;
     g.sync();
@@ -1271,6 +1416,7 @@ template <class G> CLF void normalize_xmad(const G &g, FS &s) {
 
 /* tag_cuda_objects (patterns.py:895-916)                                      */
 template <class G> CLF void tag_cuda_objects(const G &g, FS &s) {
+    PROF(g, s, PF_TAG);
     GFOR(g, i, s.n) if (i < s.n) {
         cl_hdr h = s.S.hdr[i];
         unsigned kind = 0, use = 7;
@@ -1357,6 +1503,7 @@ CLD uint32_t block_of(const FS &s, uint32_t pos) {
 }
 
 template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
+    PROF(g, s, PF_RECIP);
     /* cheap exit: no MUFU.RCP at all */
     bool mine = false;
     GFOR(g, i, s.n) if (i < s.n) { const cl_hdr h = s.S.hdr[i]; mine |= h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP); }
@@ -1533,6 +1680,7 @@ template <class G> CLF void run_postssa(const G &g, FS &s) {
 template <class G> CLF void run_match_only(const G &g, FS &s) {
     const unsigned table = (s.passes & CL_PASS_MATCH_XMAD) ? 1 : 0;
     setup_classes(s, table);
+    build_usecount(g, s);
     for (uint32_t bi = 0; bi < s.nb; bi++) {
         const uint32_t lo = s.bo[bi], n = s.bo[bi + 1] - lo;
         if (n == 0) continue;

@@ -86,6 +86,7 @@ struct KArgs {
     unsigned long long cap[CUR__N];
     unsigned long long *cursor;          /* [CUR__N]                            */
     unsigned long long *stats;           /* cl_stats as u64[]                   */
+    unsigned long long *prof;            /* [PF__N] cycle counters               */
     /* work */
     const uint32_t *list; uint32_t n_list; uint32_t *work_counter;
     uint8_t *scratch; unsigned long long scratch_per_group;
@@ -130,12 +131,13 @@ CLHD size_t carve_cold(FS &s, uint8_t *base, const Caps &c, bool with_hot) {
     s.inscnt = carve<uint8_t>(p, c.I);
     s.clsid = carve<uint8_t>(p, c.I);
     s.outpos = carve<uint32_t>(p, c.I);
+    s.cidx = s.outpos;
     s.cand = carve<uint32_t>(p, c.I);
     s.sel_at = carve<uint32_t>(p, c.I);
     s.owner = carve<unsigned long long>(p, c.I);
     s.mt = carve<MatchRec>(p, c.M);
     s.sel = carve<SelRec>(p, c.S);
-    s.plan = carve<Plan>(p, c.S);
+    s.stage = carve<Stage>(p, c.S);
     s.imm = carve<cl_imm>(p, c.Q);
     s.ev = carve<cl_event>(p, c.E);
     s.site = carve<uint32_t>(p, c.U);
@@ -152,6 +154,7 @@ enum { GW_STATUS = 0, GW_NEV, GW_WORK, GW_STATS, GW__N = GW_STATS + 64 };
 
 /* ------------------------------------------------------------ load / store */
 template <class G> CLF void load_function(const G &g, FS &s, const KArgs &a, uint32_t f) {
+    PROF(g, s, PF_LOAD);
     const cl_corpus &in = a.in;
     const uint32_t b0 = in.func_blk_off[f], b1 = in.func_blk_off[f + 1];
     const uint32_t i0 = in.blk_off[b0], i1 = in.blk_off[b1];
@@ -195,6 +198,7 @@ template <class G> CLF void load_function(const G &g, FS &s, const KArgs &a, uin
 }
 
 template <class G> CLF void store_function(const G &g, FS &s, const KArgs &a, uint32_t f, uint32_t next_temp) {
+    PROF(g, s, PF_STORE);
     const uint32_t st = status(s);
     const uint32_t n_ev = *s.n_ev <= s.cap.E ? *s.n_ev : s.cap.E;
     uint32_t r_inst = 0, r_imm = 0, r_val = 0, r_ev = 0;
@@ -287,6 +291,10 @@ template <class G> CLF void process_function(const G &g, FS &s, const KArgs &a, 
 /* persistent group loop                                                      */
 template <class G> CLF void group_loop(const G &g, const KArgs &a, uint32_t *gw, uint8_t *hot, uint8_t *cold) {
     FS s;
+    unsigned long long prof[PF__N];
+    for (int k = 0; k < PF__N; k++) prof[k] = 0;
+    s.prof = prof;
+    const unsigned long long t_begin = now();
     s.pb = a.pb; s.ms = a.in.modsets; s.opflags = a.opflags;
     s.passes = a.passes; s.max_rounds = a.max_rounds; s.emit_matches = a.emit_matches;
     s.st = gw + GW_STATUS; s.n_ev = gw + GW_NEV;
@@ -308,6 +316,8 @@ template <class G> CLF void group_loop(const G &g, const KArgs &a, uint32_t *gw,
         g.sync();
     }
     if (g.rank == 0) {
+        prof[PF_TOTAL] = now() - t_begin;
+        for (int k = 0; k < PF__N; k++) a_add64(&a.prof[k], prof[k]);
         for (int k = 0; k < 64; k++) if (gw[GW_STATS + k]) a_add64(&a.stats[k], gw[GW_STATS + k]);
         a_add64(&a.stats[64], n_in); a_add64(&a.stats[65], n_out); a_add64(&a.stats[66], n_ev);
     }
@@ -479,7 +489,8 @@ struct cl_ctx {
     cl_corpus d_in{};
     uint64_t n_inst = 0, n_ext = 0, n_mem = 0, n_imm = 0, n_val = 0;
     KArgs k{};
-    unsigned long long *d_cursor = nullptr, *d_stats = nullptr;
+    unsigned long long *d_cursor = nullptr, *d_stats = nullptr, *d_prof = nullptr;
+    unsigned long long h_prof[PF__N] = { 0 };
     unsigned long long h_cursor[CUR__N] = { 0, 0, 0, 0 };
     Part part[2];              /* 0 = warp groups, 1 = CTA groups                */
     cl_stats stats{};
@@ -531,6 +542,8 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     c->d_cursor = (unsigned long long *)p;
     if (dmalloc(&p, sizeof(cl_stats))) { delete c; return -1; }
     c->d_stats = (unsigned long long *)p;
+    if (dmalloc(&p, sizeof(unsigned long long) * PF__N)) { delete c; return -1; }
+    c->d_prof = (unsigned long long *)p;
     *out = c;
     return 0;
 }
@@ -665,7 +678,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         dget(c, B_O_BLK, &k.o_blk, B) || dget(c, B_O_BLK_START, &k.o_blk_start, B) || dget(c, B_O_BLK_CNT, &k.o_blk_cnt, B) ||
         dget(c, B_O_EV, &k.o_ev, k.cap[CUR_EV]) || dget(c, B_O_FUNC, &k.o_func, F))
         return -1;
-    k.cursor = c->d_cursor; k.stats = c->d_stats;
+    k.cursor = c->d_cursor; k.stats = c->d_stats; k.prof = c->d_prof;
 #if CL_CUDA
     CUDA_OK(cudaStreamSynchronize(c->stream));     /* the caller may reuse its buffers */
 #endif
@@ -705,6 +718,7 @@ static int run(cl_ctx *c, KArgs k) {
 #endif
     if (dzero(c->d_cursor, sizeof(unsigned long long) * CUR__N, c->stream)) return -1;
     if (dzero(c->d_stats, sizeof(cl_stats), c->stream)) return -1;
+    if (dzero(c->d_prof, sizeof(unsigned long long) * PF__N, c->stream)) return -1;
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev0, c->stream));
 #endif
@@ -715,6 +729,7 @@ static int run(cl_ctx *c, KArgs k) {
 #endif
     if (d2h(c->h_cursor, c->d_cursor, sizeof c->h_cursor, c->stream)) return -1;
     if (d2h(&c->stats, c->d_stats, sizeof(cl_stats), c->stream)) return -1;
+    if (d2h(c->h_prof, c->d_prof, sizeof c->h_prof, c->stream)) return -1;
 #if CL_CUDA
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
@@ -839,6 +854,11 @@ extern "C" int cl_download(cl_ctx *c, cl_corpus *o, cl_event *events) {
     return 0;
 }
 
+/* debugging aid (not part of include/culifter.h): per-phase cycle sums of the last run */
+extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
+    for (int i = 0; i < n && i < PF__N; i++) out[i] = c->h_prof[i];
+    return PF__N;
+}
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }
 extern "C" int cl_last_run_ms(cl_ctx *c, float *ms) { *ms = c->last_ms; return 0; }
 extern "C" void *cl_device_counts_ptr(cl_ctx *c) { return c->d_stats; }

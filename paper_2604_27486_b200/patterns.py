@@ -220,14 +220,16 @@ TEMPLATE = np.dtype([("op", "<u2"), ("n_defs", "u1"), ("n_aux", "u1"), ("n_uses"
                      ("mods_all", "<u8"), ("mods_none", "<u8"), ("slot", SLOT, (8,))])
 PATTERN = np.dtype([("n_templates", "u1"), ("rewrite", "u1"), ("n_vars", "u1"),
                     ("table", "u1"), ("var_a", "u1"), ("var_b", "u1"), ("var_c", "u1"),
-                    ("modvar_cond", "u1"), ("modvar_bop", "u1"), ("pad", "u1", (7,)),
+                    ("modvar_cond", "u1"), ("modvar_bop", "u1"), ("join_ok", "u1"),
+                    ("join_order", "u1", (3,)), ("join_from", "u1", (3,)), ("join_slot", "u1", (3,)),
+                    ("pad", "u1", (13,)),
                     ("t", TEMPLATE, (MAX_TEMPLATES,))])
 BLOB = np.dtype([("magic", "<u4"), ("n_patterns", "<u4"), ("n_groups", "<u4"),
                  ("budget", "<u4"), ("group_mask", "<u8", (MAX_GROUPS,)),
                  ("group_pos", "u1", (64,)), ("isetp64_ms", "<u2", (8, 2, 8)),
                  ("p", PATTERN, (MAX_PATTERNS,))])
 assert (SLOT.itemsize, TEMPLATE.itemsize, PATTERN.itemsize, BLOB.itemsize) == \
-    (16, 160, 496, 8304)
+    (16, 160, 512, 8560)
 
 _TRI = {None: 0, False: 1, True: 2}
 _HALF = {None: 0, "H0": 1, "H1": 2}
@@ -266,6 +268,40 @@ def _slot(slot, var_ids, pat):
         return (S_VAR, var_ids[slot.name], _TRI[slot.negated], _TRI[slot.bitnot],
                 _HALF[slot.half], (0, 0, 0), 0)
     raise PatternError(f"pattern {pat.name!r}: unknown slot {slot!r}")
+
+
+def _join_plan(pat):
+    """Resolution order that replaces the candidate product by def-use lookups:
+    -> [(template, from_template, from_slot)] with the anchor first, or None."""
+    tm = pat.templates
+    n = len(tm)
+    slots = [tuple(t.defs) + tuple(t.aux) + tuple(t.uses) for t in tm]
+    ndef = [len(t.defs) + len(t.aux) for t in tm]
+    isvar = lambda s: type(s).__name__ == "Var"
+    for anchor in reversed(range(n)):
+        plan, done = [(anchor, 0, 0)], {anchor}
+        while len(done) < n:
+            found = None
+            for t in range(n):
+                if t in done:
+                    continue
+                names = {s.name for s in slots[t][:ndef[t]] if isvar(s)}
+                for r in plan:
+                    for k, s in enumerate(slots[r[0]]):
+                        if k >= ndef[r[0]] and isvar(s) and s.name in names:
+                            found = (t, r[0], k)
+                            break
+                    if found:
+                        break
+                if found:
+                    break
+            if not found:
+                break
+            plan.append(found)
+            done.add(found[0])
+        if len(done) == n:
+            return plan
+    return None
 
 
 def compile_patterns(aggregation=None, xmad=None, budget: int = 50_000) -> np.ndarray:
@@ -313,6 +349,11 @@ def compile_patterns(aggregation=None, xmad=None, budget: int = 50_000) -> np.nd
             for k, slot in enumerate(slots):
                 tr["slot"][k] = _slot(slot, var_ids, pat)
         rec["n_vars"] = len(var_ids)
+        plan = _join_plan(pat)
+        if plan is not None:
+            rec["join_ok"] = 1
+            for k, (t, frm, slot) in enumerate(plan):
+                rec["join_order"][k], rec["join_from"][k], rec["join_slot"][k] = t, frm, slot
         rec["var_a"] = rec["var_b"] = rec["var_c"] = 0xFF
         rec["modvar_cond"] = rec["modvar_bop"] = 0xFF
         kind = REWRITE_KINDS[int(rec["rewrite"])]

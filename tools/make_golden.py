@@ -41,6 +41,22 @@ STG.E.64 [R10], R4
 STG.E [R12], R6
 EXIT
 """),
+    "carry_in_pt": ("sm90", """.text.k:
+IADD3 R4, P0, R0, R2, RZ
+IADD3.X R5, R1, R3, RZ, PT, !PT
+IADD3 R8, P1, R4, R2, RZ
+IADD3.X R9, R5, R3, RZ, P1, !PT
+STG.E.64 [R10], R8
+EXIT
+"""),
+    "mov_rz_pair": ("sm75", """.text.k:
+MOV R4, c[0x0][0x160]
+MOV R5, c[0x0][0x164]
+MOV R6, RZ
+LDG.E R8, [R4]
+STG.E.64 [R4], R6
+EXIT
+"""),
     "fadd_only": ("sm75", """.text.k:
 FADD R0, R1, R2
 FADD R3, R0, R2
