@@ -58,6 +58,9 @@ class EngineError(RuntimeError):
 
 
 def load_library(path=None):
+    import os
+    if path is None and os.environ.get("CL_LIB"):      # development knob: another build of the CUDA library
+        path = os.environ["CL_LIB"]
     path = Path(path) if path is not None else PRODUCT_LIB
     if not path.exists():
         raise EngineError(

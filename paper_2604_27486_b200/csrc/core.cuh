@@ -233,6 +233,7 @@ struct FS {                    /* one function resident in a group's work memory
     uint32_t *origin;          /* [V]                                            */
     uint32_t *redirect;        /* [V]  (also CSR offsets of the reciprocal pass) */
     uint32_t next_vid, next_iid;
+    uint32_t odd_defs;         /* some def slot is neither a value nor RZ/PT: no join */
     /* side tables */
     cl_imm *imm; uint32_t n_imm;
     cl_memref *mem; uint32_t n_mem;
@@ -364,11 +365,19 @@ template <class G> CLF void build_usecount(const G &g, FS &s) {
     PROF(g, s, PF_USECOUNT);
     GFOR(g, v, s.next_vid) if (v < s.next_vid) { s.usecnt[v] = 0; s.defpos[v] = NONE32; }
     g.sync();
+    bool odd = false;
     GFOR(g, i, s.n) if (i < s.n) {
         const cl_hdr h = s.S.hdr[i];
-        for_value_defs(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.defpos[v] = i; });
+        const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
+        for (unsigned k = 0; k < nd; k++) {
+            const opnd d = get_slot(s, h, i, d0 + k);
+            const unsigned kd = kind_of(d.tag);
+            if (kd == CL_K_VALUE) { if (d.pay < s.cap.V) s.defpos[d.pay] = i; }
+            else odd |= !(kd == CL_K_RZ || kd == CL_K_URZ || kd == CL_K_PRED);
+        }
         for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_add(&s.usecnt[v], 1u); });
     }
+    s.odd_defs = g.any(odd);
     GFOR(g, b, s.nb) if (b < s.nb)
         for (int k = 0; k < 2; k++)
             if (kind_of(s.blk[b].term_tag[k]) == CL_K_VALUE && s.blk[b].term_pay[k] < s.cap.V)
@@ -605,7 +614,7 @@ template <class G> CLF uint32_t match_block(const G &g, FS &s, uint32_t lo, uint
             empty |= s.cls_off[c + 1] == s.cls_off[c];
         }
         if (empty) continue;
-        if (!p.join_ok) { product_mask |= 1u << pi; continue; }
+        if (!p.join_ok || s.odd_defs) { product_mask |= 1u << pi; continue; }
         const int ca = class_of(s, p.t[p.join_order[0]].op);
         items += s.cls_off[ca + 1] - s.cls_off[ca];
     }
@@ -629,8 +638,17 @@ template <class G> CLF uint32_t match_block(const G &g, FS &s, uint32_t lo, uint
                 const cl_hdr hf = s.S.hdr[idx[from]];
                 const cl_template &tf = p.t[from];
                 if (hf.n_defs != tf.n_defs || hf.n_aux != tf.n_aux || hf.n_uses != tf.n_uses || (hf.flags & CL_IF_EXT)) { ok = false; break; }
+                const unsigned long long mm = s.ms[hf.modset].mask;
+                if ((mm & tf.mods_all) != tf.mods_all || (mm & tf.mods_none)) { ok = false; break; }
                 const opnd o = get_slot(s, hf, idx[from], has_guard(hf) + p.join_slot[k]);
-                if (!is_value(o)) { fb_mask |= 1u << pi; ok = false; break; }           /* not an SSA link */
+                if (!is_value(o)) {
+                    /* the link must equal a def operand of the missing instruction: with defs being
+                     * values, RZ or predicates only (odd_defs == 0) nothing else can match        */
+                    const unsigned ko = kind_of(o.tag);
+                    if (ko == CL_K_RZ || ko == CL_K_URZ || ko == CL_K_PRED) fb_mask |= 1u << pi;
+                    ok = false;
+                    break;
+                }
                 const uint32_t dp = o.pay < s.cap.V ? s.defpos[o.pay] : NONE32;
                 if (dp == NONE32 || dp < lo || dp >= lo + n || s.S.hdr[dp].op != p.t[t].op) { ok = false; break; }
                 idx[t] = dp;

@@ -323,9 +323,25 @@ template <class G> CLF void group_loop(const G &g, const KArgs &a, uint32_t *gw,
     }
 }
 
+#ifndef CL_WARP_CTAS_PER_SM
+/* Measured on B200 (profiles/r01_tuning.md): the stage is latency bound, so
+ * throughput follows resident warps.  64 warps/SM with the work arrays in
+ * L1/L2-resident scratch beat every shared-memory placement tried (those cap
+ * occupancy and pay a retry when a function outgrows its slice).            */
+#define CL_WARP_CTAS_PER_SM 16      /* warp-group kernel: resident CTAs (4 warps each) per SM */
+#endif
+#ifndef CL_WARP_HOT_BYTES
+#define CL_WARP_HOT_BYTES 0
+#endif
+#ifndef CL_CTA_CTAS_PER_SM
+#define CL_CTA_CTAS_PER_SM 8
+#endif
+#ifndef CL_CTA_HOT_BYTES
+#define CL_CTA_HOT_BYTES 0
+#endif
 #if CL_CUDA
 /* one warp per function: 4 independent groups per CTA                        */
-template <int WARPS> __global__ void __launch_bounds__(WARPS * 32) k_postssa_warp(KArgs a) {
+template <int WARPS> __global__ void __launch_bounds__(WARPS * 32, CL_WARP_CTAS_PER_SM) k_postssa_warp(KArgs a) {
     extern __shared__ uint4 dyn_smem[];
     __shared__ uint32_t gw[WARPS][GW__N];
     const uint32_t w = threadIdx.x >> 5;
@@ -335,7 +351,7 @@ template <int WARPS> __global__ void __launch_bounds__(WARPS * 32) k_postssa_war
     group_loop(g, a, gw[w], hot, a.scratch + (size_t)gid * a.scratch_per_group);
 }
 /* one CTA per function                                                       */
-template <int WARPS> __global__ void __launch_bounds__(WARPS * 32) k_postssa_cta(KArgs a) {
+template <int WARPS> __global__ void __launch_bounds__(WARPS * 32, CL_CTA_CTAS_PER_SM) k_postssa_cta(KArgs a) {
     extern __shared__ uint4 dyn_smem[];
     __shared__ uint32_t gw[GW__N];
     __shared__ uint32_t red[WARPS + 2];
@@ -495,7 +511,7 @@ struct cl_ctx {
     Part part[2];              /* 0 = warp groups, 1 = CTA groups                */
     cl_stats stats{};
     float last_ms = 0;
-    uint32_t small_max = 128;  /* records: warp-group kernel up to here          */
+    uint32_t small_max = 256;  /* records: warp-group kernel up to here          */
 };
 
 template <class T> static int dget(cl_ctx *c, int id, T **p, size_t n) {
@@ -532,6 +548,7 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     CUDA_OK(cudaEventCreate(&c->ev0));
     CUDA_OK(cudaEventCreate(&c->ev1));
 #endif
+    if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* tuning knob */
     void *p = nullptr;
     if (dmalloc(&p, sizeof(H_OPFLAGS))) { delete c; return -1; }
     c->d_opflags = (uint8_t *)p;
@@ -652,8 +669,8 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         p.cap = caps_for(n_max[k], nv_max[k], nb_max[k], imm_max[k], blk_max[k], ext_max[k]);
         p.scratch_per_group = (scratch_bytes(p.cap) + 255) & ~(size_t)255;
 #if CL_CUDA
-        if (k == 0) { p.hot_bytes = 12 * 1024; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * 4, (p.list.size() + 3) / 4); p.n_groups = p.grid * 4; }
-        else { p.hot_bytes = 100 * 1024; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * 2, p.list.size()); p.n_groups = p.grid; }
+        if (k == 0) { p.hot_bytes = CL_WARP_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * CL_WARP_CTAS_PER_SM, (p.list.size() + 3) / 4); p.n_groups = p.grid * 4; }
+        else { p.hot_bytes = CL_CTA_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * CL_CTA_CTAS_PER_SM, p.list.size()); p.n_groups = p.grid; }
 #else
         p.hot_bytes = 0; p.grid = 1; p.n_groups = 1;
 #endif
