@@ -59,48 +59,7 @@ def parse_args():
     return ap.parse_args()
 
 
-# ----------------------------------------------------------------- corpus
-def plan_shards(kind, n_sass, seed, n_shards):
-    """Kernel picks of the whole corpus (cheap: indices only) and their
-    partition by basic-block count (synth.shard_by_blocks rule)."""
-    rng = np.random.default_rng(seed)
-    shares = synth.MIXED if kind == "mixed" else ((kind, 1.0),)
-    pools = {k: synth.pool(k) for k, _ in shares}
-    mean = sum(sh * float(pools[k].n_sass.mean()) for k, sh in shares)
-    n_kernels = max(n_shards, int(round(n_sass / mean)))
-    kinds = [k for k, _ in shares]
-    kid = rng.choice(len(kinds), n_kernels, p=np.array([sh for _, sh in shares]) / sum(sh for _, sh in shares))
-    pick = np.zeros(n_kernels, np.int64)
-    nb = np.zeros(n_kernels, np.int64)
-    ns = np.zeros(n_kernels, np.int64)
-    for i, k in enumerate(kinds):
-        m = kid == i
-        p = pools[k]
-        pick[m] = rng.integers(0, p.corpus.n_funcs, int(m.sum()))
-        nb[m] = np.diff(p.corpus.func_blk_off.astype(np.int64))[pick[m]]
-        ns[m] = p.n_sass[pick[m]]
-    order = np.argsort(-nb, kind="stable")
-    pos = np.arange(n_kernels)
-    cyc = pos % (2 * n_shards)
-    shard = np.empty(n_kernels, np.int64)
-    shard[order] = np.where(cyc < n_shards, cyc, 2 * n_shards - 1 - cyc)
-    return kinds, pools, kid, pick, ns, nb, shard
-
-
-def materialize(kinds, pools, kid, pick, sel):
-    """SoA corpus of kernels `sel` (indices into the plan), in plan order."""
-    parts, where = [], []
-    for i, k in enumerate(kinds):
-        idx = sel[kid[sel] == i]
-        if len(idx) == 0:
-            continue
-        parts.append(synth.take_functions(pools[k].corpus, pick[idx]))
-        where.append(idx)
-    if len(parts) == 1:
-        return parts[0]
-    corpus = synth.concat(parts)
-    order = np.argsort(np.concatenate(where), kind="stable")       # back to plan order: archs interleaved
-    return synth.take_functions(corpus, order)
+from paper_2604_27486_b200.sharding import allgather_counts, materialize, plan_shards  # noqa: E402
 
 
 def pinned_like(corpus: Corpus):
@@ -230,7 +189,6 @@ def main():
     eng = Engine(device=local)
     eng.upload(corpus)
     counts = torch.zeros(68, dtype=torch.int64, device="cuda")
-    gathered = [torch.zeros_like(counts) for _ in range(world)] if world > 1 else None
 
     class _Raw:           # device counters of the library as a CUDA array (no host copy)
         def __init__(self, ptr):
@@ -241,7 +199,7 @@ def main():
         eng.run_postssa()
         if world > 1:                      # the only inter-GPU traffic: match counters
             counts.copy_(lib_counts)
-            dist.all_gather(gathered, counts)
+            allgather_counts(counts, world)
         return eng.last_run_ms()
 
     def fence():

@@ -31,8 +31,9 @@
  * fix-up.
  *
  * At the ABI boundary every stream is a dense CSR (offset arrays of length
- * n+1).  On the device the result of a pass lives in capacity-sized regions
- * (cl_out_capacity()) and is compacted to dense CSR by cl_download().
+ * n+1).  On the device every function's result is written once, at an
+ * atomically reserved place (completion order); cl_download() densifies it
+ * to function order on the device before the D2H copy.
  */
 #ifndef CULIFTER_H
 #define CULIFTER_H

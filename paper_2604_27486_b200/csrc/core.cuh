@@ -72,6 +72,13 @@ CLD void a_min64(unsigned long long *p, unsigned long long v) {
     if (v < *p) *p = v;
 #endif
 }
+CLD void a_min32(uint32_t *p, uint32_t v) {
+#if CL_DEV
+    atomicMin(p, v);
+#else
+    if (v < *p) *p = v;
+#endif
+}
 CLD unsigned long long a_add64(unsigned long long *p, unsigned long long v) {
 #if CL_DEV
     return atomicAdd(p, v);
@@ -232,7 +239,7 @@ struct FS {                    /* one function resident in a group's work memory
     int32_t *def_iid;          /* [V]                                            */
     uint32_t *origin;          /* [V]                                            */
     uint32_t *redirect;        /* [V]  (also CSR offsets of the reciprocal pass) */
-    uint32_t next_vid, next_iid;
+    uint32_t next_vid, next_iid, next_temp;
     uint32_t odd_defs;         /* some def slot is neither a value nor RZ/PT: no join */
     /* side tables */
     cl_imm *imm; uint32_t n_imm;
@@ -1714,6 +1721,204 @@ template <class G> CLF void run_match_only(const G &g, FS &s) {
         emit_match_events(g, s, bi, nm, 0, ns);
         g.sync();
     }
+}
+
+/* ------------------------------------------------------------- raw stage */
+/* The function is one block holding fn.raw_instructions (register operands,
+ * guards in slot 0).  Both passes expand the stream in place: count, scan,
+ * right-align, move.                                                        */
+
+/* expand the stream: record i moves to outpos[i] + inscnt[i]; the inscnt[i]
+ * slots before it are left for the caller to fill                           */
+template <class G> CLF uint32_t expand_stream(const G &g, FS &s) {
+    const uint32_t n = s.n;
+    uint32_t run = 0;
+    GFOR(g, i, n) {
+        const uint32_t x = i < n ? 1u + s.inscnt[i] : 0u;
+        uint32_t t;
+        const uint32_t o = g.exscan(x, t);
+        if (i < n) s.outpos[i] = run + o;
+        run += t;
+    }
+    if (run > s.cap.I) { fail(s, CL_ST_CAPACITY); g.sync(); return 0; }
+    g.sync();
+    if (run == n) return n;
+    const uint32_t shift = s.cap.I - n;
+    move_recs(g, s, shift, 0, n);
+    const uint32_t chunks = (n + g.size - 1) / g.size;
+    for (uint32_t c = 0; c < chunks; c++) {
+        const uint32_t i = c * g.size + g.rank;
+        Rec r;
+        if (i < n) ld_rec(s, shift + i, r);
+        g.sync();
+        if (i < n) st_rec(s, s.outpos[i] + s.inscnt[i], r);
+        g.sync();
+    }
+    GFOR(g, b, s.nb + 1) if (b <= s.nb) s.bo[b] = b == 0 ? 0u : run;     /* raw corpora: one block */
+    s.n = run;
+    g.sync();
+    return run;
+}
+
+/* normalize_instruction (frontend.py:523-548): PT aux defs dropped; `.X4`
+ * loads/stores get an explicit SHL of the address base into a fresh R1000+
+ * temporary (temps, iids and immediates numbered in stream order by scan).  */
+template <class G> CLF void raw_x4(const G &g, FS &s) {
+    const uint32_t n = s.n;
+    GFOR(g, i, n) if (i < n) {
+        cl_hdr h = s.S.hdr[i];
+        if (h.n_aux) {                                        /* :527-528 */
+            const unsigned a0 = aux0(h), total = a0 + h.n_aux + h.n_uses;
+            unsigned w = a0, na = 0;
+            for (unsigned k = a0; k < total; k++) {
+                const opnd o = get_slot(s, h, i, k);
+                const bool is_aux = k < a0 + h.n_aux;
+                if (is_aux && kind_of(o.tag) == CL_K_PRED && o.pay == CL_PT_INDEX) continue;
+                if (w != k) set_slot(s, h, i, w, o);
+                w++;
+                na += is_aux;
+            }
+            opnd none; none.tag = 0; none.pay = 0;
+            if (!(h.flags & CL_IF_EXT)) for (unsigned k = w; k < 8; k++) set_slot(s, h, i, k, none);
+            if (na != h.n_aux) { h.n_aux = (uint8_t)na; s.S.hdr[i].n_aux = (uint8_t)na; }
+        }
+        unsigned want = 0;
+        if (has_mod(s, h, CL_MB_X4) && h.op < CL_OP__COUNT && (s.opflags[h.op] & CL_OPF_LDST))
+            for (unsigned k = 0; k < h.n_uses; k++) {
+                const opnd u = get_use(s, h, i, k);
+                if (kind_of(u.tag) != CL_K_MEMREF) continue;
+                want = kind_of(s.mem[u.pay].base_tag) == CL_K_REG;      /* first MemRef only :534 */
+                break;
+            }
+        s.inscnt[i] = (uint8_t)want;
+    }
+    g.sync();
+    /* rank of every scaled access = its temp / iid / immediate number */
+    uint32_t run = 0;
+    GFOR(g, i, n) {
+        const uint32_t x = i < n ? s.inscnt[i] : 0u;
+        uint32_t t;
+        const uint32_t o = g.exscan(x, t);
+        if (i < n) s.cand[i] = run + o;
+        run += t;
+    }
+    if (s.n_imm + run > s.cap.Q) { fail(s, CL_ST_CAPACITY); g.sync(); return; }
+    g.sync();
+    if (run == 0) return;
+    if (expand_stream(g, s) == 0 && status(s)) return;
+    GFOR(g, i, n) if (i < n && s.inscnt[i]) {
+        const uint32_t at = s.outpos[i] + 1u;                 /* the access itself; the SHL goes right before */
+        cl_hdr h = s.S.hdr[at];
+        const uint32_t k = s.cand[i];
+        const uint32_t tmp = s.next_temp + k;
+        uint32_t mi = 0;
+        for (unsigned u = 0; u < h.n_uses; u++) {
+            const opnd o = get_use(s, h, at, u);
+            if (kind_of(o.tag) == CL_K_MEMREF) { mi = o.pay; break; }
+        }
+        cl_memref &m = s.mem[mi];
+        cl_imm two; two.bits = 2; two.text = 2;
+        s.imm[s.n_imm + k] = two;
+        Rec shl;
+        shl.h.iid = s.next_iid + k; shl.h.op = CL_OP_SHL; shl.h.modset = CL_MS_NONE;
+        shl.h.n_defs = 1; shl.h.n_aux = 0; shl.h.n_uses = 2; shl.h.flags = CL_IF_SYNTH;
+        shl.h.ext = (h.flags & CL_IF_SYNTH) && !(h.flags & CL_IF_EXT) ? h.ext : h.iid;   /* shares inst.raw */
+        for (unsigned q = 0; q < 8; q++) { shl.tag[q] = 0; shl.pay[q] = 0; }
+        unsigned q = 0;
+        if (has_guard(h)) { const opnd gd = get_slot(s, h, at, 0); shl.h.flags |= CL_IF_GUARD; shl.tag[0] = gd.tag; shl.pay[0] = gd.pay; q = 1; }
+        shl.tag[q] = CL_K_REG; shl.pay[q] = tmp | 1u << 16; q++;
+        shl.tag[q] = m.base_tag; shl.pay[q] = m.base_pay; q++;
+        shl.tag[q] = (uint16_t)(CL_K_IMM | CL_T_IMM_HEXTEXT); shl.pay[q] = s.n_imm + k;
+        st_rec(s, at - 1u, shl);
+        m.base_tag = CL_K_REG;                                /* Reg(tmp, old width): flags cleared */
+        m.base_pay = tmp | (m.base_pay & 0xFFFF0000u);
+        s.S.hdr[at].modset = s.ms[h.modset].minus_x4;
+    }
+    s.next_temp += run; s.next_iid += run; s.n_imm += run;
+    g.sync();
+}
+
+/* substitute_special_registers (frontend.py:697-722): constant-bank aliases of
+ * special registers become reads of one S2R per (function, offset), inserted
+ * before the first instruction that uses it; temporaries are numbered in
+ * order of first encounter (instruction, then use index).                   */
+static constexpr int MAX_SR = 16;
+template <class G> CLF void raw_sr(const G &g, FS &s, const cl_sr_entry *map, uint32_t n_map) {
+    uint32_t mine[MAX_SR];
+    unsigned nmine = 0;
+    for (uint32_t k = 0; k < n_map && nmine < (unsigned)MAX_SR; k++) if (map[k].arch == s.arch) mine[nmine++] = k;
+    if (!nmine) return;
+    const uint32_t n = s.n;
+    uint32_t *first = s.redirect;                            /* [MAX_SR] first encounter: pos << 8 | use */
+    GFOR(g, k, nmine) if (k < nmine) first[k] = NONE32;
+    GFOR(g, i, n) if (i < n) s.inscnt[i] = 0;
+    g.sync();
+    const uint32_t off_mask = (1u << CL_CM_OFFSET_BITS) - 1u;
+    GFOR(g, i, n) if (i < n) {
+        const cl_hdr h = s.S.hdr[i];
+        for (unsigned u = 0; u < h.n_uses; u++) {
+            const opnd o = get_use(s, h, i, u);
+            if (kind_of(o.tag) != CL_K_CONSTMEM || (o.pay >> CL_CM_OFFSET_BITS)) continue;     /* bank 0 only */
+            for (unsigned k = 0; k < nmine; k++)
+                if (map[mine[k]].offset == (o.pay & off_mask)) { a_min32(&first[k], i << 8 | (u < 255 ? u : 255)); break; }
+        }
+    }
+    g.sync();
+    /* order of first encounter -> temp / iid numbers (tiny: every lane computes it) */
+    uint32_t ord[MAX_SR], nfound = 0;
+    for (unsigned k = 0; k < nmine; k++) {
+        if (first[k] == NONE32) { ord[k] = NONE32; continue; }
+        uint32_t r = 0;
+        for (unsigned j = 0; j < nmine; j++) r += first[j] < first[k];
+        ord[k] = r;
+        nfound++;
+    }
+    if (!nfound) return;
+    if (g.rank == 0) for (unsigned k = 0; k < nmine; k++) if (ord[k] != NONE32) s.inscnt[first[k] >> 8]++;
+    g.sync();
+    if (expand_stream(g, s) == 0 && status(s)) return;
+    /* S2R records: before their instruction, in encounter order */
+    GFOR(g, k, nmine) if (k < nmine && ord[k] != NONE32) {
+        const uint32_t p = first[k] >> 8;
+        uint32_t before = 0;                                  /* earlier encounters at the same instruction */
+        for (unsigned j = 0; j < nmine; j++) before += ord[j] != NONE32 && (first[j] >> 8) == p && first[j] < first[k];
+        const uint32_t at = s.outpos[p] + before;
+        const cl_hdr h = s.S.hdr[s.outpos[p] + s.inscnt[p]];
+        Rec r;
+        r.h.iid = s.next_iid + ord[k]; r.h.op = CL_OP_S2R; r.h.modset = CL_MS_NONE;
+        r.h.n_defs = 1; r.h.n_aux = 0; r.h.n_uses = 1; r.h.flags = CL_IF_SYNTH;
+        r.h.ext = (h.flags & CL_IF_SYNTH) && !(h.flags & CL_IF_EXT) ? h.ext : h.iid;
+        for (unsigned q = 0; q < 8; q++) { r.tag[q] = 0; r.pay[q] = 0; }
+        r.tag[0] = CL_K_REG; r.pay[0] = (s.next_temp + ord[k]) | 1u << 16;
+        r.tag[1] = CL_K_SREG; r.pay[1] = map[mine[k]].sreg;
+        st_rec(s, at, r);
+    }
+    g.sync();
+    /* every aliasing use becomes the temporary (flags of the ConstMem kept) */
+    GFOR(g, i, s.n) if (i < s.n) {
+        const cl_hdr h = s.S.hdr[i];
+        if (h.op == CL_OP_S2R && (h.flags & CL_IF_SYNTH)) continue;
+        for (unsigned u = 0; u < h.n_uses; u++) {
+            const opnd o = get_use(s, h, i, u);
+            if (kind_of(o.tag) != CL_K_CONSTMEM || (o.pay >> CL_CM_OFFSET_BITS)) continue;
+            for (unsigned k = 0; k < nmine; k++)
+                if (map[mine[k]].offset == (o.pay & off_mask)) {
+                    opnd r;
+                    r.tag = (uint16_t)(CL_K_REG | (o.tag & (CL_T_NEG | CL_T_ABS)) | (o.tag & (3u << CL_T_HALF_SHIFT)));
+                    r.pay = (s.next_temp + ord[k]) | 1u << 16;
+                    set_slot(s, h, i, use0(h) + u, r);
+                    break;
+                }
+        }
+    }
+    s.next_temp += nfound; s.next_iid += nfound;
+    g.sync();
+}
+
+template <class G> CLF void run_raw(const G &g, FS &s, uint32_t passes, const cl_sr_entry *map, uint32_t n_map) {
+    if (s.nb != 1) { fail(s, CL_ST_UNSUPPORTED); g.sync(); return; }
+    if ((passes & CL_RAW_X4) && !status(s)) raw_x4(g, s);
+    if ((passes & CL_RAW_SR) && !status(s)) raw_sr(g, s, map, n_map);
 }
 
 } /* namespace clk */

@@ -161,7 +161,7 @@ template <class G> CLF void load_function(const G &g, FS &s, const KArgs &a, uin
     const cl_func fn = in.func[f];
     s.f = f; s.arch = fn.arch;
     s.nb = b1 - b0; s.n = i1 - i0;
-    s.next_vid = fn.next_vid; s.next_iid = fn.next_iid;
+    s.next_vid = fn.next_vid; s.next_iid = fn.next_iid; s.next_temp = fn.next_temp_reg;
     if (g.rank == 0) { *s.st = 0; *s.n_ev = 0; }
     GFOR(g, b, s.nb + 1) if (b <= s.nb) s.bo[b] = in.blk_off[b0 + b] - i0;
     GFOR(g, b, s.nb) if (b < s.nb) s.blk[b] = in.blk[b0 + b];
@@ -197,7 +197,7 @@ template <class G> CLF void load_function(const G &g, FS &s, const KArgs &a, uin
     g.sync();
 }
 
-template <class G> CLF void store_function(const G &g, FS &s, const KArgs &a, uint32_t f, uint32_t next_temp) {
+template <class G> CLF void store_function(const G &g, FS &s, const KArgs &a, uint32_t f) {
     PROF(g, s, PF_STORE);
     const uint32_t st = status(s);
     const uint32_t n_ev = *s.n_ev <= s.cap.E ? *s.n_ev : s.cap.E;
@@ -214,7 +214,7 @@ template <class G> CLF void store_function(const G &g, FS &s, const KArgs &a, ui
     const uint32_t b0 = a.in.func_blk_off[f];
     if (g.rank == 0) {
         FuncOut o;
-        o.f.next_vid = s.next_vid; o.f.next_iid = s.next_iid; o.f.next_temp_reg = next_temp;
+        o.f.next_vid = s.next_vid; o.f.next_iid = s.next_iid; o.f.next_temp_reg = s.next_temp;
         o.f.arch = (uint8_t)s.arch; o.f.status = (uint8_t)(fits ? st : (uint32_t)CL_ST_CAPACITY); o.f.reserved = 0;
         o.inst_start = r_inst; o.n_inst = fits ? s.n : 0; o.imm_start = r_imm; o.n_imm = fits ? s.n_imm : 0;
         o.val_start = r_val; o.ev_start = r_ev; o.n_ev = fits ? n_ev : 0; o.pad = 0;
@@ -254,7 +254,6 @@ template <class G> CLF void process_function(const G &g, FS &s, const KArgs &a, 
     const uint32_t b0 = in.func_blk_off[f], b1 = in.func_blk_off[f + 1];
     const uint32_t n_in = in.blk_off[b1] - in.blk_off[b0];
     const uint32_t nv_in = in.func[f].next_vid;
-    uint32_t next_temp = in.func[f].next_temp_reg;
     /* placement: hot arrays in shared memory when a 1.5x stream fits */
     Caps tight = a.gcap;
     tight.I = n_in + n_in / 2 + 16;
@@ -267,9 +266,8 @@ template <class G> CLF void process_function(const G &g, FS &s, const KArgs &a, 
         s.cap = a.gcap;
         if (use_hot) { carve_hot(s, hot, tight.I, tight.V); s.cap.I = tight.I; s.cap.V = tight.V; }
         load_function(g, s, a, f);
-        if (a.raw_passes) {
-            /* raw stage kernels live in raw.cuh */
-        } else if (a.passes & CL_PASS_MATCH_ONLY) run_match_only(g, s);
+        if (a.raw_passes) run_raw(g, s, a.raw_passes, a.sr, a.n_sr);
+        else if (a.passes & CL_PASS_MATCH_ONLY) run_match_only(g, s);
         else run_postssa(g, s);
         g.sync();
         if (status(s) == CL_ST_CAPACITY && use_hot) { use_hot = false; g.sync(); continue; }
@@ -284,7 +282,7 @@ template <class G> CLF void process_function(const G &g, FS &s, const KArgs &a, 
         if (g.rank == 0) *s.st = code;
         g.sync();
     }
-    store_function(g, s, a, f, next_temp);
+    store_function(g, s, a, f);
     g.sync();
 }
 
@@ -485,7 +483,7 @@ enum {
     B_O_BLK, B_O_BLK_START, B_O_BLK_CNT, B_O_EV, B_O_FUNC,
     B_LIST0, B_LIST1, B_COUNTER0, B_COUNTER1, B_SCRATCH0, B_SCRATCH1,
     B_D_OFF, B_D_SUMS, B_D_HDR, B_D_TAG, B_D_PAY, B_D_IMM, B_D_ALIVE, B_D_DEF_IID, B_D_ORIGIN, B_D_EV,
-    B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B__N
+    B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B_SR_MAP, B__N
 };
 struct DBuf { void *p = nullptr; size_t cap = 0; };
 
@@ -763,8 +761,14 @@ extern "C" int cl_run_postssa(cl_ctx *c, const cl_run_opts *opts) {
     return run(c, k);
 }
 extern "C" int cl_run_raw(cl_ctx *c, uint32_t passes, const cl_sr_entry *map, uint32_t n_map) {
-    (void)c; (void)passes; (void)map; (void)n_map;
-    FAIL("cl_run_raw: the raw stage is not built yet");
+    if (!(passes & (CL_RAW_X4 | CL_RAW_SR))) FAIL("cl_run_raw: no pass selected");
+    if (n_map > 64) FAIL("cl_run_raw: more than 64 special-register aliases");
+    KArgs k = c->k;
+    cl_sr_entry *dmap = nullptr;
+    if (dput(c, B_SR_MAP, &dmap, map, (size_t)n_map)) return -1;
+    k.passes = 0; k.max_rounds = 0; k.emit_matches = 0;
+    k.raw_passes = passes; k.sr = dmap; k.n_sr = n_map;
+    return run(c, k);
 }
 
 extern "C" int cl_out_sizes(cl_ctx *c, uint64_t sizes[6]) {

@@ -50,6 +50,7 @@ ARCHS = ("sm52", "sm75", "sm90", "sm100", "sm120")
 
 ST_OK, ST_CAPACITY, ST_ATTRIBUTE_ERROR, ST_ASSERTION_ERROR, ST_KEY_ERROR, \
     ST_UNSUPPORTED = range(6)
+ST_INDEX_ERROR = 6
 
 EV_REFUSED, EV_BOUNDARY, EV_MATCH = 1, 2, 3
 
@@ -59,6 +60,7 @@ ORG_BITS, ORG_F = 2 << 28, 3 << 28
 PASS_XMAD, PASS_RECIPROCAL, PASS_AGGREGATE, PASS_TAG = 1, 2, 4, 8
 PASS_ALL = 15
 PASS_MATCH_ONLY, PASS_MATCH_XMAD = 16, 32
+RAW_X4, RAW_SR = 1, 2
 
 # ---------------------------------------------------------------- opcode table
 OPF = {"CL_OPF_PURE": 1, "CL_OPF_LDST": 2, "CL_OPF_GLOBAL": 4, "CL_OPF_ATOMIC": 8,

@@ -23,7 +23,9 @@ ORACLE_LIB = ROOT / "oracle" / "liboracle.so"
 SIM_LIB = ROOT / "tests" / "sim" / "libculifter_sim.so"
 CSRC = ROOT / "paper_2604_27486_b200" / "csrc"
 
-FIXTURES = sorted(p.name[:-len(".pkl.gz")] for p in GOLDEN.glob("*.pkl.gz"))
+_ALL = sorted(p.name[:-len(".pkl.gz")] for p in GOLDEN.glob("*.pkl.gz"))
+RAW_FIXTURES = [n for n in _ALL if n.startswith("raw_")]
+FIXTURES = [n for n in _ALL if n not in RAW_FIXTURES]
 STATUS_ERROR = {2: "AttributeError", 3: "AssertionError", 4: "KeyError", 6: "IndexError"}
 
 
@@ -108,3 +110,36 @@ def corpora_equal(a: soa.Corpus, b: soa.Corpus):
     if a.events.shape != b.events.shape or not np.array_equal(a.events, b.events):
         diffs.append(f"events differ ({len(a.events)} vs {len(b.events)})")
     return diffs
+
+
+def raw_state(fn):
+    return {"dump": ir.dump(fn), "next_iid": fn._next_iid, "next_temp_reg": fn.meta.get("next_temp_reg", 1000),
+            "synthetic": [(i.iid, i.meta.get("synthetic")) for i in fn.raw_instructions if i.meta.get("synthetic")],
+            "diagnostics": list(fn.diagnostics)}
+
+
+def run_raw(engine, functions, passes):
+    from paper_2604_27486_b200 import passes as P
+    corpus = soa.encode(functions, raw=True)
+    engine.upload(corpus)
+    engine.run_raw(passes, P._sr_map())
+    out = engine.download()
+    soa.apply(out, functions, tagged=False)
+    return corpus, out
+
+
+def check_raw_fixture(engine, name):
+    fix = load_fixture(name)
+    fns = copy.deepcopy(fix["functions"])
+    _, out = run_raw(engine, fns, 1 if fix["kind"] == "raw_x4" else 2)
+    problems = []
+    for f, (fn, want) in enumerate(zip(fns, fix["expect"])):
+        if int(out.func["status"][f]) != 0:
+            problems.append(f"{name}/{fn.name}: status {int(out.func['status'][f])}")
+            continue
+        got = raw_state(fn)
+        for key in want:
+            if got[key] != want[key]:
+                problems.append(f"{name}/{fn.name}: {key} differs\n--- reference\n{want[key]}\n--- got\n{got[key]}")
+                break
+    return problems

@@ -91,8 +91,53 @@ def write(name, fns, passes=15):
     print(f"{path.name}: {len(fns)} functions, {n} records, {path.stat().st_size} bytes")
 
 
+def raw_state(fn):
+    from sasslift.ssir import dump
+    return {"dump": dump(fn), "next_iid": fn._next_iid, "next_temp_reg": fn.meta.get("next_temp_reg", 1000),
+            "synthetic": [(i.iid, i.meta.get("synthetic")) for i in fn.raw_instructions if i.meta.get("synthetic")],
+            "diagnostics": list(fn.diagnostics)}
+
+
+def write_raw(name, texts):
+    """Raw-stage fixtures: `<name>_x4` (parsed -> normalize_instruction on every
+    instruction, frontend.py:523) and `<name>_sr` (parsed + normalized + expanded ->
+    substitute_special_registers, frontend.py:697)."""
+    R.load()
+    from sasslift import frontend
+    x4_in, x4_exp, sr_in, sr_exp = [], [], [], []
+    for arch, text in texts:
+        for fn in R.raw_functions(text, arch, normalize=False):
+            x4_in.append(ir.convert(fn))
+            out = []
+            for inst in fn.raw_instructions:
+                out.extend(frontend.normalize_instruction(fn, inst))
+            fn.raw_instructions = out
+            x4_exp.append(raw_state(fn))
+            for inst in fn.raw_instructions:
+                frontend.expand_implicit_registers(inst, arch)
+            sr_in.append(ir.convert(fn))
+            frontend.substitute_special_registers(fn)
+            sr_exp.append(raw_state(fn))
+    for suffix, fns, exp in (("x4", x4_in, x4_exp), ("sr", sr_in, sr_exp)):
+        path = OUT / f"{name}_{suffix}.pkl.gz"
+        with gzip.open(path, "wb", compresslevel=9) as fh:
+            pickle.dump({"name": f"{name}_{suffix}", "kind": "raw_" + suffix, "functions": fns, "expect": exp}, fh, protocol=4)
+        print(f"{path.name}: {len(fns)} functions, {sum(len(f.raw_instructions) for f in fns)} instructions, {path.stat().st_size} bytes")
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    raw_texts = [("sm52", gen_sass.gen_corpus(21, "sm52", 30, near_miss=0.2)[1]),
+                 ("sm75", gen_sass.gen_corpus(22, "sm75", 10)[1])]
+    for f in R.corpus_files():
+        man = f.with_suffix(".manifest")
+        arch = "sm75"
+        if man.exists():
+            for ln in man.read_text().splitlines():
+                if ln.startswith("arch:"):
+                    arch = ln.split(":")[1].strip()
+        raw_texts.append((arch, f.read_text()))
+    write_raw("raw", raw_texts)
     fns = []
     for f in R.corpus_files():
         fns += R.ssa_from_path(f)
