@@ -509,7 +509,8 @@ struct cl_ctx {
     Part part[2];              /* 0 = warp groups, 1 = CTA groups                */
     cl_stats stats{};
     float last_ms = 0;
-    uint32_t small_max = 256;  /* records: warp-group kernel up to here          */
+    uint32_t small_max = 256;
+    int warp_ctas = CL_WARP_CTAS_PER_SM, cta_ctas = CL_CTA_CTAS_PER_SM;   /* resident CTAs per SM actually launched */  /* records: warp-group kernel up to here          */
 };
 
 template <class T> static int dget(cl_ctx *c, int id, T **p, size_t n) {
@@ -546,7 +547,9 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     CUDA_OK(cudaEventCreate(&c->ev0));
     CUDA_OK(cudaEventCreate(&c->ev1));
 #endif
-    if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* tuning knob */
+    if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* tuning knobs */
+    if (const char *e = getenv("CL_WARP_CTAS")) c->warp_ctas = std::min(CL_WARP_CTAS_PER_SM, std::max(1, atoi(e)));
+    if (const char *e = getenv("CL_CTA_CTAS")) c->cta_ctas = std::min(CL_CTA_CTAS_PER_SM, std::max(1, atoi(e)));
     void *p = nullptr;
     if (dmalloc(&p, sizeof(H_OPFLAGS))) { delete c; return -1; }
     c->d_opflags = (uint8_t *)p;
@@ -667,8 +670,8 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         p.cap = caps_for(n_max[k], nv_max[k], nb_max[k], imm_max[k], blk_max[k], ext_max[k]);
         p.scratch_per_group = (scratch_bytes(p.cap) + 255) & ~(size_t)255;
 #if CL_CUDA
-        if (k == 0) { p.hot_bytes = CL_WARP_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * CL_WARP_CTAS_PER_SM, (p.list.size() + 3) / 4); p.n_groups = p.grid * 4; }
-        else { p.hot_bytes = CL_CTA_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * CL_CTA_CTAS_PER_SM, p.list.size()); p.n_groups = p.grid; }
+        if (k == 0) { p.hot_bytes = CL_WARP_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->warp_ctas, (p.list.size() + 3) / 4); p.n_groups = p.grid * 4; }
+        else { p.hot_bytes = CL_CTA_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->cta_ctas, p.list.size()); p.n_groups = p.grid; }
 #else
         p.hot_bytes = 0; p.grid = 1; p.n_groups = 1;
 #endif

@@ -78,6 +78,7 @@ def run_postssa(engine, functions, passes=15, **kw):
     engine.upload(corpus)
     engine.run_postssa(passes, **kw)
     out = engine.download()
+    out.stats = engine.stats().copy()
     soa.apply(out, functions, patterns=pattern_list(), tagged=bool(passes & 8))
     return corpus, out
 
@@ -109,6 +110,9 @@ def corpora_equal(a: soa.Corpus, b: soa.Corpus):
     diffs = a.equal(b)
     if a.events.shape != b.events.shape or not np.array_equal(a.events, b.events):
         diffs.append(f"events differ ({len(a.events)} vs {len(b.events)})")
+    sa, sb = getattr(a, "stats", None), getattr(b, "stats", None)
+    if sa is not None and sb is not None and sa.tobytes() != sb.tobytes():
+        diffs.append(f"match counters differ: {sa} vs {sb}")
     return diffs
 
 
