@@ -25,6 +25,7 @@
 #define CL_DEV 1
 #define CLD __device__ __forceinline__
 #define CLF __device__ __noinline__
+#define CLN __device__ __noinline__
 #define CLHD __host__ __device__ inline
 #define CLM static __device__ __forceinline__
 #define CLMEM __device__ __forceinline__
@@ -32,6 +33,7 @@
 #define CL_DEV 0
 #define CLD static inline
 #define CLF static
+#define CLN static
 #define CLHD static inline
 #define CLM static inline
 #define CLMEM inline
@@ -160,14 +162,21 @@ template <int NW> struct Grp {
         __syncthreads();
         return r;
     }
-#else
-    void sync() const {}
-    uint32_t exscan(uint32_t x, uint32_t &total) const { total = x; return 0; }
-    uint32_t flag_exscan(bool f, uint32_t &total) const { total = f; return 0; }
-    bool any(bool f) const { return f; }
-    uint32_t sum(uint32_t x) const { return x; }
-    uint32_t bcast0(uint32_t x) const { return x; }
 #endif
+};
+
+/* NW == 0: a group of one lane.  On the host it is the CL_SIM debug build; on
+ * the device it is the thread-per-function kernel (32 independent functions
+ * per warp: every lane is busy, the collectives are identities).            */
+template <> struct Grp<0> {
+    uint32_t rank, size;
+    uint32_t *red;
+    CLMEM void sync() const {}
+    CLMEM uint32_t exscan(uint32_t x, uint32_t &total) const { total = x; return 0; }
+    CLMEM uint32_t flag_exscan(bool f, uint32_t &total) const { total = f; return 0; }
+    CLMEM bool any(bool f) const { return f; }
+    CLMEM uint32_t sum(uint32_t x) const { return x; }
+    CLMEM uint32_t bcast0(uint32_t x) const { return x; }
 };
 
 /* uniform strided loop: every lane runs every iteration (collectives inside
@@ -225,6 +234,7 @@ struct FS {                    /* one function resident in a group's work memory
     const uint8_t *opflags;    /* CL_OPF_* by opcode id (< CL_OP__COUNT)         */
     Caps cap;
     uint32_t f;                /* function index                                 */
+    bool solo;                 /* one-lane group: private updates need no atomics */
     uint32_t arch;
     uint32_t *st;              /* group-shared status word (enum cl_status)      */
     uint32_t passes, max_rounds, emit_matches;
@@ -276,13 +286,13 @@ CLD bool has_guard(const cl_hdr &h) { return (h.flags & CL_IF_GUARD) != 0; }
 CLD unsigned def0(const cl_hdr &h) { return has_guard(h); }
 CLD unsigned aux0(const cl_hdr &h) { return has_guard(h) + h.n_defs; }
 CLD unsigned use0(const cl_hdr &h) { return has_guard(h) + h.n_defs + h.n_aux; }
-CLD opnd get_slot(const FS &s, const cl_hdr &h, uint32_t i, unsigned k) {
+CLN opnd get_slot(const FS &s, const cl_hdr &h, uint32_t i, unsigned k) {
     opnd o;
     if (h.flags & CL_IF_EXT) { o.tag = s.ext_tag[h.ext + k]; o.pay = s.ext_pay[h.ext + k]; }
     else { o.tag = s.S.tag[(size_t)i * 8 + k]; o.pay = s.S.pay[(size_t)i * 8 + k]; }
     return o;
 }
-CLD void set_slot(FS &s, const cl_hdr &h, uint32_t i, unsigned k, opnd o) {
+CLN void set_slot(FS &s, const cl_hdr &h, uint32_t i, unsigned k, opnd o) {
     if (h.flags & CL_IF_EXT) { s.ext_tag[h.ext + k] = o.tag; s.ext_pay[h.ext + k] = o.pay; }
     else { s.S.tag[(size_t)i * 8 + k] = o.tag; s.S.pay[(size_t)i * 8 + k] = o.pay; }
 }
@@ -321,7 +331,7 @@ template <class F> CLD void for_value_defs(const FS &s, const cl_hdr &h, uint32_
     for (unsigned k = 0; k < nd; k++) { opnd d = get_slot(s, h, i, d0 + k); if (is_value(d)) fn(d.pay); }
 }
 
-CLD void ld_rec(const FS &s, uint32_t i, Rec &r) {
+CLN void ld_rec(const FS &s, uint32_t i, Rec &r) {
     r.h = s.S.hdr[i];
     const uint4 *t = (const uint4 *)(s.S.tag + (size_t)i * 8);
     const uint4 *p = (const uint4 *)(s.S.pay + (size_t)i * 8);
@@ -329,7 +339,7 @@ CLD void ld_rec(const FS &s, uint32_t i, Rec &r) {
     ((uint4 *)r.pay)[0] = p[0];
     ((uint4 *)r.pay)[1] = p[1];
 }
-CLD void st_rec(FS &s, uint32_t i, const Rec &r) {
+CLN void st_rec(FS &s, uint32_t i, const Rec &r) {
     s.S.hdr[i] = r.h;
     *(uint4 *)(s.S.tag + (size_t)i * 8) = *(const uint4 *)r.tag;
     ((uint4 *)(s.S.pay + (size_t)i * 8))[0] = ((const uint4 *)r.pay)[0];
@@ -352,13 +362,19 @@ template <class G> CLF void move_recs(const G &g, FS &s, uint32_t dst, uint32_t 
     }
 }
 
+/* updates of group-private data: atomic among the lanes of a group, plain for
+ * a one-lane group (s.solo)                                                  */
+CLD uint32_t p_add(const FS &s, uint32_t *p, uint32_t v) { if (s.solo) { const uint32_t o = *p; *p = o + v; return o; } return a_add(p, v); }
+CLD uint32_t p_sub(const FS &s, uint32_t *p, uint32_t v) { if (s.solo) { const uint32_t o = *p; *p = o - v; return o; } return a_sub(p, v); }
+CLD void p_min64(const FS &s, unsigned long long *p, unsigned long long v) { if (s.solo) { if (v < *p) *p = v; } else a_min64(p, v); }
+CLD void p_min32(const FS &s, uint32_t *p, uint32_t v) { if (s.solo) { if (v < *p) *p = v; } else a_min32(p, v); }
 /* first error wins; read it back only after a group sync                     */
-CLD void fail(FS &s, uint32_t code) { a_cas0(s.st, code); }
+CLD void fail(FS &s, uint32_t code) { if (s.solo) { if (!*s.st) *s.st = code; } else a_cas0(s.st, code); }
 CLD uint32_t status(const FS &s) { return *(volatile uint32_t *)s.st; }
 
-CLD void push_event(FS &s, uint32_t seq, uint32_t kind, uint32_t idx, uint32_t a, uint32_t b,
+CLN void push_event(FS &s, uint32_t seq, uint32_t kind, uint32_t idx, uint32_t a, uint32_t b,
                     uint32_t c, uint32_t d) {
-    uint32_t k = a_add(s.n_ev, 1u);
+    uint32_t k = p_add(s, s.n_ev, 1u);
     if (k < s.cap.E) {
         cl_event e; e.func = s.f; e.seq = seq; e.kind = kind; e.idx = idx; e.a = a; e.b = b; e.c = c; e.d = d;
         s.ev[k] = e;
@@ -382,19 +398,19 @@ template <class G> CLF void build_usecount(const G &g, FS &s) {
             if (kd == CL_K_VALUE) { if (d.pay < s.cap.V) s.defpos[d.pay] = i; }
             else odd |= !(kd == CL_K_RZ || kd == CL_K_URZ || kd == CL_K_PRED);
         }
-        for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_add(&s.usecnt[v], 1u); });
+        for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) p_add(s, &s.usecnt[v], 1u); });
     }
     s.odd_defs = g.any(odd);
     GFOR(g, b, s.nb) if (b < s.nb)
         for (int k = 0; k < 2; k++)
             if (kind_of(s.blk[b].term_tag[k]) == CL_K_VALUE && s.blk[b].term_pay[k] < s.cap.V)
-                a_add(&s.usecnt[s.blk[b].term_pay[k]], 1u);
+                p_add(s, &s.usecnt[s.blk[b].term_pay[k]], 1u);
     g.sync();
 }
 
 /* ----------------------------------------------------------------- matching */
 /* operand_key (patterns.py:109-127)                                           */
-CLD okey operand_key(const FS &s, opnd o) {
+CLN okey operand_key(const FS &s, opnd o) {
     okey k; k.cls = KC_OTHER; k.v = o.pay;
     switch (kind_of(o.tag)) {
     case CL_K_VALUE: k.cls = KC_V; break;
@@ -409,7 +425,7 @@ CLD okey operand_key(const FS &s, opnd o) {
     }
     return k;
 }
-CLD bool memref_equal(const FS &s, uint32_t a, uint32_t b) {
+CLN bool memref_equal(const FS &s, uint32_t a, uint32_t b) {
     const cl_memref &x = s.mem[a], &y = s.mem[b];
     if (x.base_tag != y.base_tag || x.ureg_tag != y.ureg_tag) return false;
     if (kind_of(x.base_tag) != CL_K_NONE && x.base_pay != y.base_pay) return false;
@@ -428,7 +444,7 @@ CLD bool bind(const FS &s, Bind &b, unsigned name, okey k) {
     return true;
 }
 /* _match_slot (patterns.py:130-152)                                           */
-CLD bool match_slot(const FS &s, const cl_slot &sl, opnd o, Bind &b) {
+CLN bool match_slot(const FS &s, const cl_slot &sl, opnd o, Bind &b) {
     switch (sl.kind) {
     case CL_S_ANY: return true;
     case CL_S_RZ: return is_zero(o);
@@ -445,7 +461,7 @@ CLD bool match_slot(const FS &s, const cl_slot &sl, opnd o, Bind &b) {
     return false;
 }
 /* _match_opcode + _unify (patterns.py:155-178)                                */
-CLD bool match_inst(const FS &s, const cl_template &t, const cl_hdr &h, uint32_t i, Bind &b) {
+CLN bool match_inst(const FS &s, const cl_template &t, const cl_hdr &h, uint32_t i, Bind &b) {
     if (h.op != t.op) return false;
     const cl_modset &ms = s.ms[h.modset];
     if ((ms.mask & t.mods_all) != t.mods_all) return false;
@@ -718,7 +734,7 @@ template <class G> CLF uint32_t select_block(const G &g, FS &s, uint32_t n, uint
             bool clash = false;
             for (unsigned t = 0; t < r.n; t++) clash |= s.keep[r.pos[t]] != 0;
             if (clash) r.state = MS_REJECTED;
-            else for (unsigned t = 0; t < r.n; t++) a_min64(&s.owner[r.pos[t]], match_key(r));
+            else for (unsigned t = 0; t < r.n; t++) p_min64(s, &s.owner[r.pos[t]], match_key(r));
         }
         g.sync();
         bool left = false;
@@ -781,15 +797,20 @@ template <class G> CLF void emit_match_events(const G &g, FS &s, uint32_t seq, u
 static constexpr uint16_t CL_T_REL = 1u << 15;      /* payload is relative to the match's base */
 static constexpr int ST_RECS = 6, ST_VALS = 4, ST_IMMS = 8, ST_UPD = 3, ST_DROP = 4;
 
+struct SRec {                      /* a staged record: at most one def and three uses */
+    uint16_t op, modset;
+    uint8_t n_defs, n_uses, iid, pad;
+    uint16_t tag[4];
+    uint32_t pay[4];
+};
 struct Stage {
-    Rec rec[ST_RECS];
+    SRec rec[ST_RECS];
     cl_imm imm[ST_IMMS];
-    uint32_t val_origin[ST_VALS];
-    int32_t val_def[ST_VALS];      /* relative iid of the defining record, -1 none */
-    uint32_t upd_vid[ST_UPD], upd_iid[ST_UPD];   /* existing values redefined (relative iid) */
+    uint32_t upd_vid[ST_UPD];      /* existing values redefined ...                */
     uint32_t drop_vid[ST_DROP];
-    uint8_t ok, rm, nins, retag, nv, nq, nupd, ndrop;
-    uint32_t ni;                   /* iids taken, orphans included                 */
+    int8_t val_def[ST_VALS];       /* relative iid of the defining record, -1 none */
+    uint8_t upd_iid[ST_UPD];       /* ... by the record with this relative iid     */
+    uint8_t ok, rm, nins, retag, nv, nq, nupd, ndrop, ni;
     uint32_t vbase, ibase, mbase;  /* after the scan                               */
 };
 
@@ -805,7 +826,8 @@ struct RW {
 CLD opnd rw_value(RW &c, uint32_t origin) {               /* LiftedFunction.new_value */
     Stage &st = *c.st;
     opnd o; o.tag = (uint16_t)(CL_K_VALUE | CL_T_REL); o.pay = st.nv;
-    if (st.nv < ST_VALS) { st.val_origin[st.nv] = origin; st.val_def[st.nv] = -1; st.nv++; } else c.overflow = true;
+    (void)origin;                  /* always "pair" in this pass (patterns.py:292,356,405) */
+    if (st.nv < ST_VALS) { st.val_def[st.nv] = -1; st.nv++; } else c.overflow = true;
     return o;
 }
 CLD opnd rw_imm(RW &c, unsigned long long bits, unsigned long long text, bool hextext) {
@@ -833,13 +855,17 @@ CLD Rec rw_make(RW &c, uint16_t op, uint16_t modset, const opnd *defs, unsigned 
 }
 CLD void rw_push(RW &c, const Rec &r) {
     Stage &st = *c.st;
-    if (st.nins < ST_RECS) st.rec[st.nins++] = r; else c.overflow = true;
+    if (st.nins < ST_RECS && (unsigned)r.h.n_defs + r.h.n_uses <= 4) {
+        SRec &q = st.rec[st.nins++];
+        q.op = r.h.op; q.modset = r.h.modset; q.n_defs = r.h.n_defs; q.n_uses = r.h.n_uses; q.iid = (uint8_t)r.h.iid; q.pad = 0;
+        for (unsigned k = 0; k < 4; k++) { q.tag[k] = r.tag[k]; q.pay[k] = r.pay[k]; }
+    } else c.overflow = true;
 }
 /* info.def_iid = inst.iid for a staged (relative) or an existing value        */
 CLD void rw_set_def_iid(RW &c, opnd v, uint32_t iid_rel) {
     Stage &st = *c.st;
-    if (v.tag & CL_T_REL) { if (v.pay < (uint32_t)ST_VALS) st.val_def[v.pay] = (int32_t)iid_rel; }
-    else if (st.nupd < ST_UPD) { st.upd_vid[st.nupd] = v.pay; st.upd_iid[st.nupd] = iid_rel; st.nupd++; }
+    if (v.tag & CL_T_REL) { if (v.pay < (uint32_t)ST_VALS) st.val_def[v.pay] = (int8_t)iid_rel; }
+    else if (st.nupd < ST_UPD) { st.upd_vid[st.nupd] = v.pay; st.upd_iid[st.nupd] = (uint8_t)iid_rel; st.nupd++; }
     else c.overflow = true;
 }
 CLD void rw_drop(RW &c, opnd o) {                       /* _drop_values :314-317 */
@@ -1132,15 +1158,18 @@ CLF void apply_stage(FS &s, const SelRec &m, Stage &st, uint32_t lo, uint32_t ou
     for (unsigned k = 0; k < st.nv; k++) {
         const uint32_t v = st.vbase + k;
         if (v >= s.cap.V) continue;
-        s.alive[v] = 1; s.origin[v] = st.val_origin[k];
+        s.alive[v] = 1; s.origin[v] = CL_ORG_PAIR;
         s.def_iid[v] = st.val_def[k] < 0 ? -1 : (int32_t)(st.ibase + (uint32_t)st.val_def[k]);
         s.usecnt[v] = 0; s.defpos[v] = NONE32;
     }
     for (unsigned k = 0; k < st.nq; k++) if (st.mbase + k < s.cap.Q) s.imm[st.mbase + k] = st.imm[k];
     if (!st.ok) return;                      /* refused: the allocations above leak (G4) */
     for (unsigned r = 0; r < st.nins; r++) {
-        Rec rec = st.rec[r];
-        rec.h.iid += st.ibase;
+        const SRec q = st.rec[r];
+        Rec rec;
+        rec.h.iid = st.ibase + q.iid; rec.h.op = q.op; rec.h.modset = q.modset;
+        rec.h.n_defs = q.n_defs; rec.h.n_aux = 0; rec.h.n_uses = q.n_uses; rec.h.flags = 0; rec.h.ext = 0;
+        for (unsigned k = 0; k < 8; k++) { rec.tag[k] = k < 4 ? q.tag[k] : 0; rec.pay[k] = k < 4 ? q.pay[k] : 0; }
         const unsigned ns = (unsigned)rec.h.n_defs + rec.h.n_uses;
         for (unsigned k = 0; k < ns; k++) {
             if (rec.tag[k] & CL_T_REL) {
@@ -1148,11 +1177,11 @@ CLF void apply_stage(FS &s, const SelRec &m, Stage &st, uint32_t lo, uint32_t ou
                 rec.tag[k] &= (uint16_t)~CL_T_REL;
             }
             if (k < rec.h.n_defs) continue;
-            if (kind_of(rec.tag[k]) == CL_K_VALUE) { if (rec.pay[k] < s.cap.V) a_add(&s.usecnt[rec.pay[k]], 1u); }
+            if (kind_of(rec.tag[k]) == CL_K_VALUE) { if (rec.pay[k] < s.cap.V) p_add(s, &s.usecnt[rec.pay[k]], 1u); }
             else if (kind_of(rec.tag[k]) == CL_K_MEMREF) {
                 const cl_memref &mr = s.mem[rec.pay[k]];
-                if (kind_of(mr.base_tag) == CL_K_VALUE) a_add(&s.usecnt[mr.base_pay], 1u);
-                if (kind_of(mr.ureg_tag) == CL_K_VALUE) a_add(&s.usecnt[mr.ureg_pay], 1u);
+                if (kind_of(mr.base_tag) == CL_K_VALUE) p_add(s, &s.usecnt[mr.base_pay], 1u);
+                if (kind_of(mr.ureg_tag) == CL_K_VALUE) p_add(s, &s.usecnt[mr.ureg_pay], 1u);
             }
         }
         st_rec(s, out + r, rec);
@@ -1172,9 +1201,13 @@ CLF void apply_stage(FS &s, const SelRec &m, Stage &st, uint32_t lo, uint32_t ou
  * blocks in order -- the escape test of block b must see the use counts left
  * by the rewrites of blocks < b (G5) -- compacting the stream from the right
  * end of the gap buffer to the left.                                        */
-template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table, uint32_t phase) {
+/* phase A: seed classes, def positions for the join, use counts for the escapes */
+template <class G> CLF void ap_prepare(const G &g, FS &s, unsigned table) {
     setup_classes(s, table);
-    build_usecount(g, s);                 /* def positions for the join, use counts for the escapes */
+    build_usecount(g, s);
+}
+/* phase B: match + select every block; returns the number of selected matches */
+template <class G> CLF uint32_t ap_match(const G &g, FS &s, unsigned table, uint32_t phase) {
     uint32_t nsel = 0;
     for (uint32_t bi = 0; bi < s.nb; bi++) {
         const uint32_t lo = s.bo[bi], n = s.bo[bi + 1] - lo;
@@ -1195,8 +1228,10 @@ template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table
     }
     if (g.rank == 0) s.blk_sel[s.nb] = nsel;
     g.sync();
-    if (nsel == 0) return 0;
-
+    return nsel;
+}
+/* phase C: plan, scan, emit block by block; returns the number of successful rewrites */
+template <class G> CLF uint32_t ap_rewrite(const G &g, FS &s, uint32_t phase) {
     const uint32_t shift = s.cap.I - s.n;                    /* right-align the stream */
     move_recs(g, s, shift, 0, s.n);
     uint32_t wr = 0, total_ok = 0;
@@ -1282,7 +1317,7 @@ template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table
                 st_rec(s, wr + s.outpos[p] + s.inscnt[p], r);
             } else {
                 const cl_hdr h = s.S.hdr[lo + p];
-                for_value_operands(s, h, lo + p, [&](uint32_t v) { if (v < s.cap.V) a_sub(&s.usecnt[v], 1u); });
+                for_value_operands(s, h, lo + p, [&](uint32_t v) { if (v < s.cap.V) p_sub(s, &s.usecnt[v], 1u); });
             }
         }
         g.sync();
@@ -1295,6 +1330,12 @@ template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table
     s.n = wr;
     g.sync();
     return total_ok;
+}
+template <class G> CLF uint32_t apply_patterns(const G &g, FS &s, unsigned table, uint32_t phase) {
+    ap_prepare(g, s, table);
+    const uint32_t nsel = ap_match(g, s, table, phase);
+    if (status(s) || nsel == 0) return 0;
+    return ap_rewrite(g, s, phase);
 }
 
 /* ordered in-place compaction of the stream by keep[] (block offsets follow) */
@@ -1353,7 +1394,7 @@ template <class G> CLF uint32_t remove_dead_pseudo(const G &g, FS &s) {
             s.keep[i] = 0;
             mine++;
             for_value_defs(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.alive[v] = 0; });
-            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_sub(&s.usecnt[v], 1u); });
+            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) p_sub(s, &s.usecnt[v], 1u); });
         }
         const uint32_t dead = g.sum(mine);
         g.sync();
@@ -1369,7 +1410,7 @@ CLD uint32_t final_of(const FS &s, uint32_t v) {
     while (v < s.cap.V && s.redirect[v] != NONE32) v = s.redirect[v];
     return v;
 }
-template <class G> CLF uint32_t simplify_packs(const G &g, FS &s) {
+template <class G> CLF uint32_t simplify_packs(const G &g, FS &s, bool with_dce = true) {
     PROF(g, s, PF_SIMPLIFY);
     build_usecount(g, s);
     GFOR(g, v, s.next_vid) if (v < s.next_vid) s.redirect[v] = NONE32;
@@ -1416,7 +1457,7 @@ template <class G> CLF uint32_t simplify_packs(const G &g, FS &s) {
         for (int k = 0; k < 2; k++)
             if (kind_of(s.blk[b].term_tag[k]) == CL_K_VALUE) s.blk[b].term_pay[k] = final_of(s, s.blk[b].term_pay[k]);
     g.sync();
-    remove_dead_pseudo(g, s);
+    if (with_dce) remove_dead_pseudo(g, s);
     return changed;
 }
 
@@ -1473,13 +1514,13 @@ template <class G> CLF void tag_cuda_objects(const G &g, FS &s) {
  *              + the inserted bitcasts chained from xhead[v]
  * where root(v) is the original value a renamed value (.bits / .f) took its
  * sites from -- and the group materialises the inserted records at the end. */
-CLD bool rec_references(const FS &s, uint32_t i, uint32_t vid) {
+CLN bool rec_references(const FS &s, uint32_t i, uint32_t vid) {
     const cl_hdr h = s.S.hdr[i];
     bool r = false;
     for_value_operands(s, h, i, [&](uint32_t v) { r |= v == vid; });
     return r;
 }
-CLD uint32_t count_sites(const FS &s, uint32_t i, uint32_t vid) {
+CLN uint32_t count_sites(const FS &s, uint32_t i, uint32_t vid) {
     const cl_hdr h = s.S.hdr[i];
     uint32_t r = 0;
     for_value_operands(s, h, i, [&](uint32_t v) { r += v == vid; });
@@ -1551,7 +1592,7 @@ template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
     g.sync();
     GFOR(g, i, s.n) if (i < s.n) {
         const cl_hdr h = s.S.hdr[i];
-        for_value_operands(s, h, i, [&](uint32_t v) { if (v < nv) s.site[a_add(&s.usecnt[v], 1u)] = i; });
+        for_value_operands(s, h, i, [&](uint32_t v) { if (v < nv) s.site[p_add(s, &s.usecnt[v], 1u)] = i; });
     }
     g.sync();
     uint32_t nx = 0, n_events = 0, vid = s.next_vid, iid = s.next_iid;
@@ -1860,7 +1901,7 @@ template <class G> CLF void raw_sr(const G &g, FS &s, const cl_sr_entry *map, ui
             const opnd o = get_use(s, h, i, u);
             if (kind_of(o.tag) != CL_K_CONSTMEM || (o.pay >> CL_CM_OFFSET_BITS)) continue;     /* bank 0 only */
             for (unsigned k = 0; k < nmine; k++)
-                if (map[mine[k]].offset == (o.pay & off_mask)) { a_min32(&first[k], i << 8 | (u < 255 ? u : 255)); break; }
+                if (map[mine[k]].offset == (o.pay & off_mask)) { p_min32(s, &first[k], i << 8 | (u < 255 ? u : 255)); break; }
         }
     }
     g.sync();

@@ -89,6 +89,9 @@ struct KArgs {
     unsigned long long *prof;            /* [PF__N] cycle counters               */
     /* work */
     const uint32_t *list; uint32_t n_list; uint32_t *work_counter;
+    const uint32_t *n_list_ptr;          /* non-null: the list length lives on the device (retry list) */
+    uint32_t *retry_list, *retry_count;  /* non-null: functions that outgrow this kernel's tight work
+                                            memory are queued for the roomy one instead of failing   */
     uint8_t *scratch; unsigned long long scratch_per_group;
     Caps gcap;                 /* capacities of the scratch placement            */
     uint32_t hot_bytes;        /* shared memory per group for the hot arrays     */
@@ -197,10 +200,14 @@ template <class G> CLF void load_function(const G &g, FS &s, const KArgs &a, uin
     g.sync();
 }
 
+CLD uint32_t events_of(const FS &s) { return *s.n_ev <= s.cap.E ? *s.n_ev : s.cap.E; }
+
+/* copy a finished function to the places reserved for it */
+template <class G> CLF void store_function_at(const G &g, FS &s, const KArgs &a, uint32_t f, uint32_t r_inst,
+                                              uint32_t r_imm, uint32_t r_val, uint32_t r_ev);
+
 template <class G> CLF void store_function(const G &g, FS &s, const KArgs &a, uint32_t f) {
-    PROF(g, s, PF_STORE);
-    const uint32_t st = status(s);
-    const uint32_t n_ev = *s.n_ev <= s.cap.E ? *s.n_ev : s.cap.E;
+    const uint32_t n_ev = events_of(s);
     uint32_t r_inst = 0, r_imm = 0, r_val = 0, r_ev = 0;
     if (g.rank == 0) {
         r_inst = (uint32_t)a_add64(&a.cursor[CUR_INST], s.n);
@@ -209,6 +216,14 @@ template <class G> CLF void store_function(const G &g, FS &s, const KArgs &a, ui
         r_ev = (uint32_t)a_add64(&a.cursor[CUR_EV], n_ev);
     }
     r_inst = g.bcast0(r_inst); r_imm = g.bcast0(r_imm); r_val = g.bcast0(r_val); r_ev = g.bcast0(r_ev);
+    store_function_at(g, s, a, f, r_inst, r_imm, r_val, r_ev);
+}
+
+template <class G> CLF void store_function_at(const G &g, FS &s, const KArgs &a, uint32_t f, uint32_t r_inst,
+                                              uint32_t r_imm, uint32_t r_val, uint32_t r_ev) {
+    PROF(g, s, PF_STORE);
+    const uint32_t st = status(s);
+    const uint32_t n_ev = events_of(s);
     const bool fits = (unsigned long long)r_inst + s.n <= a.cap[CUR_INST] && (unsigned long long)r_imm + s.n_imm <= a.cap[CUR_IMM] &&
                       (unsigned long long)r_val + s.next_vid <= a.cap[CUR_VAL] && (unsigned long long)r_ev + n_ev <= a.cap[CUR_EV];
     const uint32_t b0 = a.in.func_blk_off[f];
@@ -247,8 +262,8 @@ template <class G> CLF void store_function(const G &g, FS &s, const KArgs &a, ui
     GFOR(g, e, n_ev) if (e < n_ev) a.o_ev[r_ev + e] = s.ev[e];
 }
 
-/* one function, start to finish, on one group                               */
-template <class G> CLF void process_function(const G &g, FS &s, const KArgs &a, uint32_t f, uint8_t *hot,
+/* one function through the passes on one group; false = queued for the roomy kernel */
+template <class G> CLF bool compute_function(const G &g, FS &s, const KArgs &a, uint32_t f, uint8_t *hot,
                                              uint8_t *cold) {
     const cl_corpus &in = a.in;
     const uint32_t b0 = in.func_blk_off[f], b1 = in.func_blk_off[f + 1];
@@ -273,6 +288,11 @@ template <class G> CLF void process_function(const G &g, FS &s, const KArgs &a, 
         if (status(s) == CL_ST_CAPACITY && use_hot) { use_hot = false; g.sync(); continue; }
         break;
     }
+    if (status(s) == CL_ST_CAPACITY && a.retry_list) {
+        if (g.rank == 0) a.retry_list[a_add(a.retry_count, 1u)] = f;
+        g.sync();
+        return false;
+    }
     if (status(s) != CL_ST_OK) {              /* hand the function back unchanged */
         const uint32_t code = status(s);
         g.sync();
@@ -282,8 +302,23 @@ template <class G> CLF void process_function(const G &g, FS &s, const KArgs &a, 
         if (g.rank == 0) *s.st = code;
         g.sync();
     }
+    return true;
+}
+template <class G> CLF bool process_function(const G &g, FS &s, const KArgs &a, uint32_t f, uint8_t *hot,
+                                             uint8_t *cold) {
+    if (!compute_function(g, s, a, f, hot, cold)) return false;
     store_function(g, s, a, f);
     g.sync();
+    return true;
+}
+
+CLD void setup_fs(FS &s, const KArgs &a, uint32_t *gw, unsigned long long *prof, bool solo) {
+    s.pb = a.pb; s.ms = a.in.modsets; s.opflags = a.opflags; s.solo = solo;
+    s.passes = a.passes; s.max_rounds = a.max_rounds; s.emit_matches = a.emit_matches;
+    s.st = gw + GW_STATUS; s.n_ev = gw + GW_NEV;
+    s.st_matches = gw + GW_STATS; s.st_selected = gw + GW_STATS + 16;
+    s.st_rewrites = gw + GW_STATS + 32; s.st_refused = gw + GW_STATS + 48;
+    s.prof = prof;
 }
 
 /* persistent group loop                                                      */
@@ -291,23 +326,25 @@ template <class G> CLF void group_loop(const G &g, const KArgs &a, uint32_t *gw,
     FS s;
     unsigned long long prof[PF__N];
     for (int k = 0; k < PF__N; k++) prof[k] = 0;
-    s.prof = prof;
     const unsigned long long t_begin = now();
-    s.pb = a.pb; s.ms = a.in.modsets; s.opflags = a.opflags;
-    s.passes = a.passes; s.max_rounds = a.max_rounds; s.emit_matches = a.emit_matches;
-    s.st = gw + GW_STATUS; s.n_ev = gw + GW_NEV;
-    s.st_matches = gw + GW_STATS; s.st_selected = gw + GW_STATS + 16;
-    s.st_rewrites = gw + GW_STATS + 32; s.st_refused = gw + GW_STATS + 48;
+    setup_fs(s, a, gw, prof, g.size == 1);
     GFOR(g, k, GW__N) if (k < GW__N) gw[k] = 0;
     g.sync();
+    const uint32_t n_list = a.n_list_ptr ? *a.n_list_ptr : a.n_list;
     unsigned long long n_in = 0, n_out = 0, n_ev = 0;
     for (;;) {
         uint32_t w = 0;
         if (g.rank == 0) w = a_add(a.work_counter, 1u);
         w = g.bcast0(w);
-        if (w >= a.n_list) break;
+        if (w >= n_list) break;
         const uint32_t f = a.list[w];
-        process_function(g, s, a, f, hot, cold);
+        uint32_t saved[64];
+        if (a.retry_list && g.rank == 0) for (int k = 0; k < 64; k++) saved[k] = gw[GW_STATS + k];
+        if (!process_function(g, s, a, f, hot, cold)) {       /* queued: its counters will be redone */
+            if (g.rank == 0) for (int k = 0; k < 64; k++) gw[GW_STATS + k] = saved[k];
+            g.sync();
+            continue;
+        }
         const uint32_t b0 = a.in.func_blk_off[f], b1 = a.in.func_blk_off[f + 1];
         n_in += a.in.blk_off[b1] - a.in.blk_off[b0];
         n_out += s.n; n_ev += *s.n_ev;
@@ -338,6 +375,71 @@ template <class G> CLF void group_loop(const G &g, const KArgs &a, uint32_t *gw,
 #define CL_CTA_HOT_BYTES 0
 #endif
 #if CL_CUDA
+/* one THREAD per function (32 independent functions per warp).  The stage is
+ * a branchy scalar program per function; giving every lane its own function
+ * keeps all lanes busy and puts ~300k functions in flight, which hides the
+ * latency that bounds the group kernels (profiles/r01_tuning.md).  A warp
+ * takes 32 list entries at a time, each lane computes its function in private
+ * scratch, then the warp reserves the output space with one atomic per stream. */
+#ifndef CL_THREAD_CTAS_PER_SM
+#define CL_THREAD_CTAS_PER_SM 8
+#endif
+__global__ void __launch_bounds__(128, CL_THREAD_CTAS_PER_SM) k_postssa_thread(KArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    Grp<0> g; g.rank = 0; g.size = 1; g.red = nullptr;
+    uint32_t gw[GW__N];
+    unsigned long long prof[PF__N];
+    for (int k = 0; k < GW__N; k++) gw[k] = 0;
+    for (int k = 0; k < PF__N; k++) prof[k] = 0;
+    const unsigned long long t_begin = now();
+    FS s;
+    setup_fs(s, a, gw, prof, true);
+    uint8_t *cold = a.scratch + (size_t)(blockIdx.x * blockDim.x + threadIdx.x) * a.scratch_per_group;
+    unsigned long long n_in = 0, n_out = 0, n_evs = 0;
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(a.work_counter, 32u);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (base >= a.n_list) break;
+        const uint32_t w = base + lane;
+        bool have = w < a.n_list;
+        uint32_t f = 0;
+        if (have) {
+            f = a.list[w];
+            uint32_t saved[64];
+            for (int k = 0; k < 64; k++) saved[k] = gw[GW_STATS + k];
+            have = compute_function(g, s, a, f, nullptr, cold);
+            if (!have) for (int k = 0; k < 64; k++) gw[GW_STATS + k] = saved[k];
+        }
+        __syncwarp();
+        /* warp-aggregated reservation of the four output streams */
+        uint32_t sz[4] = { have ? s.n : 0u, have ? s.n_imm : 0u, have ? s.next_vid : 0u, have ? events_of(s) : 0u };
+        uint32_t at[4];
+        for (int q = 0; q < 4; q++) {
+            uint32_t v = sz[q];
+            for (int d = 1; d < 32; d <<= 1) { const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, d); if (lane >= (uint32_t)d) v += t; }
+            uint32_t start = 0;
+            if (lane == 31) start = (uint32_t)atomicAdd(&a.cursor[q], (unsigned long long)v);
+            start = __shfl_sync(0xFFFFFFFFu, start, 31);
+            at[q] = start + v - sz[q];
+        }
+        if (have) {
+            store_function_at(g, s, a, f, at[0], at[1], at[2], at[3]);
+            const uint32_t b0 = a.in.func_blk_off[f], b1 = a.in.func_blk_off[f + 1];
+            n_in += a.in.blk_off[b1] - a.in.blk_off[b0];
+            n_out += s.n; n_evs += *s.n_ev;
+        }
+        __syncwarp();
+    }
+    /* counters: reduce over the warp, one atomic per counter per warp */
+    prof[PF_TOTAL] = now() - t_begin;
+    for (int k = 0; k < 64 + 3 + PF__N; k++) {
+        unsigned long long v = k < 64 ? gw[GW_STATS + k] : k == 64 ? n_in : k == 65 ? n_out : k == 66 ? n_evs : prof[k - 67];
+        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+        if (lane == 0 && v) atomicAdd(k < 67 ? &a.stats[k] : &a.prof[k - 67], v);
+    }
+}
+
 /* one warp per function: 4 independent groups per CTA                        */
 template <int WARPS> __global__ void __launch_bounds__(WARPS * 32, CL_WARP_CTAS_PER_SM) k_postssa_warp(KArgs a) {
     extern __shared__ uint4 dyn_smem[];
@@ -348,8 +450,109 @@ template <int WARPS> __global__ void __launch_bounds__(WARPS * 32, CL_WARP_CTAS_
     uint8_t *hot = a.hot_bytes ? (uint8_t *)dyn_smem + (size_t)w * a.hot_bytes : nullptr;
     group_loop(g, a, gw[w], hot, a.scratch + (size_t)gid * a.scratch_per_group);
 }
+/* Phase-synchronous variant of the warp-group kernel.  ncu on the free-running
+ * kernel shows 89 % of the warp cycles stalled on instruction fetch: the stage
+ * is ~300 KB of straight code and 64 warps per SM, each in a different phase of
+ * a different function, thrash the instruction cache.  Here the warps of a CTA
+ * take one function each and walk through the passes in lock step (CTA barrier
+ * between passes), so an SM runs one pass's code at a time and the warps share
+ * it in the instruction cache.  Functions of a batch have similar sizes (the
+ * work list is sorted), so little time is lost at the barriers.             */
+template <int WARPS, int MINB> __global__ void __launch_bounds__(WARPS * 32, MINB) k_postssa_warp_sync(KArgs a) {
+    __shared__ uint32_t gw[WARPS][GW__N];
+    const uint32_t w = threadIdx.x >> 5;
+    Grp<1> g; g.rank = threadIdx.x & 31u; g.size = 32; g.red = nullptr;
+    const uint32_t gid = blockIdx.x * WARPS + w;
+    uint8_t *cold = a.scratch + (size_t)gid * a.scratch_per_group;
+    FS s;
+    unsigned long long prof[PF__N];
+    for (int k = 0; k < PF__N; k++) prof[k] = 0;
+    const unsigned long long t_begin = now();
+    setup_fs(s, a, gw[w], prof, false);
+    GFOR(g, k, GW__N) if (k < GW__N) gw[w][k] = 0;
+    g.sync();
+    const uint32_t n_list = a.n_list_ptr ? *a.n_list_ptr : a.n_list;
+    unsigned long long n_in = 0, n_out = 0, n_ev = 0;
+    for (;;) {
+        uint32_t wi = 0;
+        if (g.rank == 0) wi = a_add(a.work_counter, 1u);
+        wi = g.bcast0(wi);
+        const bool live = wi < n_list;
+        if (!__syncthreads_or(live)) break;
+        uint32_t f = 0;
+        if (live) {
+            f = a.list[wi];
+            carve_cold(s, cold, a.gcap, true);
+            s.cap = a.gcap;
+            load_function(g, s, a, f);
+        }
+        __syncthreads();
+        if (a.raw_passes) { if (live) run_raw(g, s, a.raw_passes, a.sr, a.n_sr); }
+        else if (a.passes & CL_PASS_MATCH_ONLY) { if (live) run_match_only(g, s); }
+        else {
+            /* every pass below is cut into pieces of one code region each; the whole CTA
+             * finishes a piece before anyone starts the next                             */
+            const bool xm = live && (s.passes & CL_PASS_XMAD) && s.arch == CL_ARCH_SM52;
+            if (__syncthreads_or(xm)) {
+                uint32_t nsel = 0;
+                if (xm) ap_prepare(g, s, 1);
+                __syncthreads();
+                if (xm && !status(s)) nsel = ap_match(g, s, 1, 0);
+                __syncthreads();
+                if (xm && !status(s) && nsel) ap_rewrite(g, s, 0);
+                __syncthreads();
+                if (xm && !status(s)) remove_dead_pseudo(g, s);
+                __syncthreads();
+            }
+            if (live && (s.passes & CL_PASS_RECIPROCAL) && !status(s)) normalize_reciprocal(g, s);
+            __syncthreads();
+            bool more = live && (s.passes & CL_PASS_AGGREGATE);
+            for (uint32_t round = 0; round < a.max_rounds; round++) {
+                uint32_t n = 0, nsel = 0, red = 0;
+                if (more && !status(s)) ap_prepare(g, s, 0);
+                __syncthreads();
+                if (more && !status(s)) nsel = ap_match(g, s, 0, 2 + round);
+                __syncthreads();
+                if (more && !status(s) && nsel) n = ap_rewrite(g, s, 2 + round);
+                __syncthreads();
+                if (more && !status(s)) red = simplify_packs(g, s, false);
+                __syncthreads();
+                if (more && !status(s) && red) remove_dead_pseudo(g, s);
+                n += red;
+                if (!n) more = false;
+                if (!__syncthreads_or(more)) break;
+            }
+            if (live && (s.passes & CL_PASS_AGGREGATE) && !status(s)) remove_dead_pseudo(g, s);
+            __syncthreads();
+            if (live && (s.passes & CL_PASS_TAG) && !status(s)) tag_cuda_objects(g, s);
+        }
+        __syncthreads();
+        if (live) {
+            g.sync();
+            if (status(s) != CL_ST_OK) {              /* hand the function back unchanged */
+                const uint32_t code = status(s);
+                g.sync();
+                load_function(g, s, a, f);
+                if (g.rank == 0) *s.st = code;
+                g.sync();
+            }
+            store_function(g, s, a, f);
+            const uint32_t b0 = a.in.func_blk_off[f], b1 = a.in.func_blk_off[f + 1];
+            n_in += a.in.blk_off[b1] - a.in.blk_off[b0];
+            n_out += s.n; n_ev += *s.n_ev;
+        }
+        __syncthreads();
+    }
+    if (g.rank == 0) {
+        prof[PF_TOTAL] = now() - t_begin;
+        for (int k = 0; k < PF__N; k++) a_add64(&a.prof[k], prof[k]);
+        for (int k = 0; k < 64; k++) if (gw[w][GW_STATS + k]) a_add64(&a.stats[k], gw[w][GW_STATS + k]);
+        a_add64(&a.stats[64], n_in); a_add64(&a.stats[65], n_out); a_add64(&a.stats[66], n_ev);
+    }
+}
+
 /* one CTA per function                                                       */
-template <int WARPS> __global__ void __launch_bounds__(WARPS * 32, CL_CTA_CTAS_PER_SM) k_postssa_cta(KArgs a) {
+template <int WARPS, int MINB> __global__ void __launch_bounds__(WARPS * 32, MINB) k_postssa_cta(KArgs a) {
     extern __shared__ uint4 dyn_smem[];
     __shared__ uint32_t gw[GW__N];
     __shared__ uint32_t red[WARPS + 2];
@@ -481,7 +684,8 @@ enum {
     B_EXT_TAG, B_EXT_PAY, B_MEM, B_IMM, B_ALIVE, B_DEF_IID, B_MODSETS,
     B_O_HDR, B_O_TAG, B_O_PAY, B_O_IMM, B_O_ALIVE, B_O_DEF_IID, B_O_ORIGIN, B_O_EXT_TAG, B_O_EXT_PAY, B_O_MEM,
     B_O_BLK, B_O_BLK_START, B_O_BLK_CNT, B_O_EV, B_O_FUNC,
-    B_LIST0, B_LIST1, B_COUNTER0, B_COUNTER1, B_SCRATCH0, B_SCRATCH1,
+    B_LIST0, B_LIST1, B_LIST2, B_COUNTER0, B_COUNTER1, B_COUNTER2, B_SCRATCH0, B_SCRATCH1, B_SCRATCH2,
+    B_RETRY_LIST, B_RETRY_WORDS,
     B_D_OFF, B_D_SUMS, B_D_HDR, B_D_TAG, B_D_PAY, B_D_IMM, B_D_ALIVE, B_D_DEF_IID, B_D_ORIGIN, B_D_EV,
     B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B_SR_MAP, B__N
 };
@@ -506,7 +710,12 @@ struct cl_ctx {
     unsigned long long *d_cursor = nullptr, *d_stats = nullptr, *d_prof = nullptr;
     unsigned long long h_prof[PF__N] = { 0 };
     unsigned long long h_cursor[CUR__N] = { 0, 0, 0, 0 };
-    Part part[2];              /* 0 = warp groups, 1 = CTA groups                */
+    Part part[3];              /* 0 = warp groups, 1 = CTA groups, 2 = one thread per function */
+    uint32_t *d_retry_list = nullptr, *d_retry_count = nullptr, *d_retry_counter = nullptr;
+    uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
+    int warp_sync = 33;
+    int cta_warps = 8;         /* warps per CTA of the CTA-group kernel (8, 16 or 32) */        /* warps per CTA of the phase-synchronous warp kernel (0 = free-running kernel) */
+    int thread_ctas = 8;
     cl_stats stats{};
     float last_ms = 0;
     uint32_t small_max = 256;
@@ -548,6 +757,10 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     CUDA_OK(cudaEventCreate(&c->ev1));
 #endif
     if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* tuning knobs */
+    if (const char *e = getenv("CL_THREAD_MAX")) c->thread_max = CL_CUDA ? (uint32_t)atoi(e) : 0;
+    if (const char *e = getenv("CL_WARP_SYNC")) { const int v = atoi(e); c->warp_sync = (v == 0 || v == 8 || v == 16 || v == 32 || v == 33) ? v : 32; }
+    if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
+    if (const char *e = getenv("CL_THREAD_CTAS")) c->thread_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("CL_WARP_CTAS")) c->warp_ctas = std::min(CL_WARP_CTAS_PER_SM, std::max(1, atoi(e)));
     if (const char *e = getenv("CL_CTA_CTAS")) c->cta_ctas = std::min(CL_CTA_CTAS_PER_SM, std::max(1, atoi(e)));
     void *p = nullptr;
@@ -643,17 +856,20 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     d.modsets = dms;
     d.val_origin = nullptr;
 
-    /* work partition (while the copies are in flight): warp groups take the small functions */
-    uint32_t n_max[2] = { 0, 0 }, nv_max[2] = { 0, 0 }, nb_max[2] = { 0, 0 }, imm_max[2] = { 0, 0 }, blk_max[2] = { 0, 0 }, ext_max[2] = { 0, 0 };
+    /* work partition (while the copies are in flight): one thread per tiny function,
+     * one warp per small one, one CTA per large one                                   */
+    uint32_t n_max[3] = { 0, 0, 0 }, nv_max[3] = { 0, 0, 0 }, nb_max[3] = { 0, 0, 0 }, imm_max[3] = { 0, 0, 0 },
+             blk_max[3] = { 0, 0, 0 }, ext_max[3] = { 0, 0, 0 };
     for (Part &p : c->part) p.list.clear();
-    std::vector<std::pair<uint32_t, uint32_t>> big;
+    std::vector<std::pair<uint32_t, uint32_t>> big, tiny, mid;
     for (uint32_t f = 0; f < F; f++) {
         const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
         const uint32_t n = in->blk_off[b1] - in->blk_off[b0];
         if (in->val_off[f + 1] - in->val_off[f] != in->func[f].next_vid)
             FAIL("function %u: value region holds %u entries, next_vid is %u", f, in->val_off[f + 1] - in->val_off[f], in->func[f].next_vid);
-        const int k = n <= c->small_max ? 0 : 1;
-        if (k) big.emplace_back(~n, f); else c->part[0].list.push_back(f);
+        const int k = n <= c->thread_max ? 2 : n <= c->small_max ? 0 : 1;
+        if (k == 1) big.emplace_back(~n, f); else if (k == 2) tiny.emplace_back(n, f);
+        else mid.emplace_back((in->func[f].arch == CL_ARCH_SM52 ? 0u : 0x80000000u) | (0x7FFFFFFFu - n), f);   /* by arch (sm52 runs an extra pass), then size */
         n_max[k] = std::max(n_max[k], n);
         nv_max[k] = std::max(nv_max[k], in->func[f].next_vid);
         nb_max[k] = std::max(nb_max[k], b1 - b0);
@@ -664,20 +880,52 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     }
     std::sort(big.begin(), big.end());            /* long poles first */
     for (auto &pr : big) c->part[1].list.push_back(pr.second);
-    for (int k = 0; k < 2; k++) {
+    std::sort(mid.begin(), mid.end());            /* a CTA's batch of functions has one size: short barrier waits */
+    for (auto &pr : mid) c->part[0].list.push_back(pr.second);
+    std::sort(tiny.begin(), tiny.end());          /* the 32 lanes of a warp get functions of one size */
+    for (auto &pr : tiny) c->part[2].list.push_back(pr.second);
+    /* the warp kernel also takes what outgrows the thread kernel's tight scratch */
+    if (!c->part[2].list.empty()) {
+        n_max[0] = std::max(n_max[0], n_max[2]); nv_max[0] = std::max(nv_max[0], nv_max[2]); nb_max[0] = std::max(nb_max[0], nb_max[2]);
+        imm_max[0] = std::max(imm_max[0], imm_max[2]); blk_max[0] = std::max(blk_max[0], blk_max[2]); ext_max[0] = std::max(ext_max[0], ext_max[2]);
+    }
+    for (int k = 0; k < 3; k++) {
         Part &p = c->part[k];
-        if (p.list.empty()) continue;
-        p.cap = caps_for(n_max[k], nv_max[k], nb_max[k], imm_max[k], blk_max[k], ext_max[k]);
+        if (p.list.empty() && !(k == 0 && !c->part[2].list.empty())) continue;
+        if (k == 2) {
+            /* tight: a function that grows past this is re-run by the warp kernel */
+            Caps t;
+            const uint32_t n = n_max[2];
+            t.I = n + n / 2 + 32; t.V = nv_max[2] + n + 32; t.B = nb_max[2] + 1; t.M = 2 * n + 64; t.S = n / 2 + 16;
+            t.Q = imm_max[2] + n + 32; t.E = n + 32; t.U = 6 * t.I + ext_max[2]; t.X = n / 2 + 16;
+            p.cap = t;
+        } else
+            p.cap = caps_for(n_max[k], nv_max[k], nb_max[k], imm_max[k], blk_max[k], ext_max[k]);
         p.scratch_per_group = (scratch_bytes(p.cap) + 255) & ~(size_t)255;
 #if CL_CUDA
-        if (k == 0) { p.hot_bytes = CL_WARP_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->warp_ctas, (p.list.size() + 3) / 4); p.n_groups = p.grid * 4; }
-        else { p.hot_bytes = CL_CTA_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->cta_ctas, p.list.size()); p.n_groups = p.grid; }
+        const size_t n_work = std::max<size_t>(p.list.size(), k == 0 ? c->part[2].list.size() / 8 + 1 : 0);
+        if (k == 0 && c->warp_sync) {
+            const int wpc = c->warp_sync == 33 ? 32 : c->warp_sync;                      /* warps per CTA */
+            p.hot_bytes = 0;
+            p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * (c->warp_sync == 33 ? 1 : 64 / wpc), (n_work + wpc - 1) / wpc);
+            p.n_groups = p.grid * wpc;
+        } else if (k == 0) { p.hot_bytes = CL_WARP_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->warp_ctas, (n_work + 3) / 4); p.n_groups = p.grid * 4; }
+        else if (k == 1) { p.hot_bytes = 0; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * std::min(c->cta_ctas, 64 / c->cta_warps), p.list.size()); p.n_groups = p.grid; }
+        else { p.hot_bytes = 0; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->thread_ctas, (p.list.size() + 127) / 128); p.n_groups = p.grid * 128; }
 #else
         p.hot_bytes = 0; p.grid = 1; p.n_groups = 1;
 #endif
-        if (dput(c, k ? B_LIST1 : B_LIST0, &p.d_list, p.list.data(), p.list.size())) return -1;
-        if (dget(c, k ? B_COUNTER1 : B_COUNTER0, &p.d_counter, 1)) return -1;
-        if (dget(c, k ? B_SCRATCH1 : B_SCRATCH0, &p.d_scratch, p.scratch_per_group * p.n_groups)) return -1;
+        static const int LIST_ID[3] = { B_LIST0, B_LIST1, B_LIST2 }, CNT_ID[3] = { B_COUNTER0, B_COUNTER1, B_COUNTER2 },
+                         SCR_ID[3] = { B_SCRATCH0, B_SCRATCH1, B_SCRATCH2 };
+        if (dput(c, LIST_ID[k], &p.d_list, p.list.data(), p.list.size())) return -1;
+        if (dget(c, CNT_ID[k], &p.d_counter, 1)) return -1;
+        if (dget(c, SCR_ID[k], &p.d_scratch, p.scratch_per_group * p.n_groups)) return -1;
+    }
+    if (!c->part[2].list.empty()) {
+        uint32_t *words = nullptr;
+        if (dget(c, B_RETRY_LIST, &c->d_retry_list, c->part[2].list.size())) return -1;
+        if (dget(c, B_RETRY_WORDS, &words, 4)) return -1;
+        c->d_retry_count = words; c->d_retry_counter = words + 1;
     }
 
     /* result buffers (worst-case growth, G3/G4) */
@@ -704,22 +952,40 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     return 0;
 }
 
-static int launch_part(cl_ctx *c, int which, KArgs k) {
+/* launch one kernel: `which` selects the kernel and the scratch, the work list is
+ * that part's own or (retry) what the thread kernel queued                       */
+static int launch_part(cl_ctx *c, int which, KArgs k, bool retry = false) {
     Part &p = c->part[which];
-    if (p.list.empty()) return 0;
-    k.list = p.d_list; k.n_list = (uint32_t)p.list.size(); k.work_counter = p.d_counter;
+    if (!retry && p.list.empty()) return 0;
+    if (retry && c->part[2].list.empty()) return 0;
+    k.list = retry ? c->d_retry_list : p.d_list;
+    k.n_list = retry ? (uint32_t)c->part[2].list.size() : (uint32_t)p.list.size();
+    k.n_list_ptr = retry ? c->d_retry_count : nullptr;
+    k.work_counter = retry ? c->d_retry_counter : p.d_counter;
+    k.retry_list = which == 2 ? c->d_retry_list : nullptr;
+    k.retry_count = which == 2 ? c->d_retry_count : nullptr;
     k.scratch = p.d_scratch; k.scratch_per_group = p.scratch_per_group; k.gcap = p.cap; k.hot_bytes = p.hot_bytes;
-    if (dzero(p.d_counter, sizeof(uint32_t), c->stream)) return -1;
+    if (dzero(k.work_counter, sizeof(uint32_t), c->stream)) return -1;
 #if CL_CUDA
-    if (which == 0) {
+    if (which == 0 && c->warp_sync) {
+        switch (c->warp_sync) {
+        case 33: k_postssa_warp_sync<32, 1><<<p.grid, 1024, 0, c->stream>>>(k); break;     /* 1 CTA/SM, 64 regs */
+        case 32: k_postssa_warp_sync<32, 2><<<p.grid, 1024, 0, c->stream>>>(k); break;
+        case 8: k_postssa_warp_sync<8, 8><<<p.grid, 256, 0, c->stream>>>(k); break;
+        default: k_postssa_warp_sync<16, 4><<<p.grid, 512, 0, c->stream>>>(k); break;
+        }
+    } else if (which == 0) {
         const size_t smem = (size_t)p.hot_bytes * 4;
         CUDA_OK(cudaFuncSetAttribute(k_postssa_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_postssa_warp<4><<<p.grid, 128, smem, c->stream>>>(k);
-    } else {
+    } else if (which == 1) {
         const size_t smem = p.hot_bytes;
-        CUDA_OK(cudaFuncSetAttribute(k_postssa_cta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_postssa_cta<8><<<p.grid, 256, smem, c->stream>>>(k);
-    }
+        (void)smem;
+        if (c->cta_warps == 32) k_postssa_cta<32, 2><<<p.grid, 1024, 0, c->stream>>>(k);
+        else if (c->cta_warps == 16) k_postssa_cta<16, 4><<<p.grid, 512, 0, c->stream>>>(k);
+        else k_postssa_cta<8, CL_CTA_CTAS_PER_SM><<<p.grid, 256, 0, c->stream>>>(k);
+    } else
+        k_postssa_thread<<<p.grid, 128, 0, c->stream>>>(k);
     CUDA_OK(cudaGetLastError());
 #else
     static uint32_t gw[GW__N];
@@ -737,11 +1003,14 @@ static int run(cl_ctx *c, KArgs k) {
     if (dzero(c->d_cursor, sizeof(unsigned long long) * CUR__N, c->stream)) return -1;
     if (dzero(c->d_stats, sizeof(cl_stats), c->stream)) return -1;
     if (dzero(c->d_prof, sizeof(unsigned long long) * PF__N, c->stream)) return -1;
+    if (c->d_retry_count && dzero(c->d_retry_count, sizeof(uint32_t), c->stream)) return -1;
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev0, c->stream));
 #endif
     if (launch_part(c, 1, k)) return -1;       /* the long poles first */
+    if (launch_part(c, 2, k)) return -1;
     if (launch_part(c, 0, k)) return -1;
+    if (launch_part(c, 0, k, true)) return -1; /* what outgrew the thread kernel */
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev1, c->stream));
 #endif
