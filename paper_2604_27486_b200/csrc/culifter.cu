@@ -695,7 +695,8 @@ struct cl_ctx {
     int device = 0;
     cudaStream_t stream = 0;
 #if CL_CUDA
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t stream2 = nullptr;     /* the CTA-group kernel runs beside the warp kernel */
     int n_sm = 148;
 #endif
     cl_pattern_blob h_pb{};
@@ -718,7 +719,7 @@ struct cl_ctx {
     int thread_ctas = 8;
     cl_stats stats{};
     float last_ms = 0;
-    uint32_t small_max = 256;
+    uint32_t small_max = 512;
     int warp_ctas = CL_WARP_CTAS_PER_SM, cta_ctas = CL_CTA_CTAS_PER_SM;   /* resident CTAs per SM actually launched */  /* records: warp-group kernel up to here          */
 };
 
@@ -755,6 +756,9 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreate(&c->ev0));
     CUDA_OK(cudaEventCreate(&c->ev1));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
 #endif
     if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* tuning knobs */
     if (const char *e = getenv("CL_THREAD_MAX")) c->thread_max = CL_CUDA ? (uint32_t)atoi(e) : 0;
@@ -790,6 +794,9 @@ extern "C" void cl_destroy(cl_ctx *c) {
 #if CL_CUDA
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->stream2) cudaStreamDestroy(c->stream2);
     if (c->stream) cudaStreamDestroy(c->stream);
 #endif
     delete c;
@@ -954,7 +961,12 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
 
 /* launch one kernel: `which` selects the kernel and the scratch, the work list is
  * that part's own or (retry) what the thread kernel queued                       */
-static int launch_part(cl_ctx *c, int which, KArgs k, bool retry = false) {
+static int launch_part(cl_ctx *c, int which, KArgs k, bool retry = false, bool side = false) {
+#if CL_CUDA
+    cudaStream_t st = side ? c->stream2 : c->stream;
+#else
+    cudaStream_t st = c->stream; (void)side;
+#endif
     Part &p = c->part[which];
     if (!retry && p.list.empty()) return 0;
     if (retry && c->part[2].list.empty()) return 0;
@@ -965,27 +977,27 @@ static int launch_part(cl_ctx *c, int which, KArgs k, bool retry = false) {
     k.retry_list = which == 2 ? c->d_retry_list : nullptr;
     k.retry_count = which == 2 ? c->d_retry_count : nullptr;
     k.scratch = p.d_scratch; k.scratch_per_group = p.scratch_per_group; k.gcap = p.cap; k.hot_bytes = p.hot_bytes;
-    if (dzero(k.work_counter, sizeof(uint32_t), c->stream)) return -1;
+    if (dzero(k.work_counter, sizeof(uint32_t), st)) return -1;
 #if CL_CUDA
     if (which == 0 && c->warp_sync) {
         switch (c->warp_sync) {
-        case 33: k_postssa_warp_sync<32, 1><<<p.grid, 1024, 0, c->stream>>>(k); break;     /* 1 CTA/SM, 64 regs */
-        case 32: k_postssa_warp_sync<32, 2><<<p.grid, 1024, 0, c->stream>>>(k); break;
-        case 8: k_postssa_warp_sync<8, 8><<<p.grid, 256, 0, c->stream>>>(k); break;
-        default: k_postssa_warp_sync<16, 4><<<p.grid, 512, 0, c->stream>>>(k); break;
+        case 33: k_postssa_warp_sync<32, 1><<<p.grid, 1024, 0, st>>>(k); break;     /* 1 CTA/SM, 64 regs */
+        case 32: k_postssa_warp_sync<32, 2><<<p.grid, 1024, 0, st>>>(k); break;
+        case 8: k_postssa_warp_sync<8, 8><<<p.grid, 256, 0, st>>>(k); break;
+        default: k_postssa_warp_sync<16, 4><<<p.grid, 512, 0, st>>>(k); break;
         }
     } else if (which == 0) {
         const size_t smem = (size_t)p.hot_bytes * 4;
         CUDA_OK(cudaFuncSetAttribute(k_postssa_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_postssa_warp<4><<<p.grid, 128, smem, c->stream>>>(k);
+        k_postssa_warp<4><<<p.grid, 128, smem, st>>>(k);
     } else if (which == 1) {
         const size_t smem = p.hot_bytes;
         (void)smem;
-        if (c->cta_warps == 32) k_postssa_cta<32, 2><<<p.grid, 1024, 0, c->stream>>>(k);
-        else if (c->cta_warps == 16) k_postssa_cta<16, 4><<<p.grid, 512, 0, c->stream>>>(k);
-        else k_postssa_cta<8, CL_CTA_CTAS_PER_SM><<<p.grid, 256, 0, c->stream>>>(k);
+        if (c->cta_warps == 32) k_postssa_cta<32, 2><<<p.grid, 1024, 0, st>>>(k);
+        else if (c->cta_warps == 16) k_postssa_cta<16, 4><<<p.grid, 512, 0, st>>>(k);
+        else k_postssa_cta<8, CL_CTA_CTAS_PER_SM><<<p.grid, 256, 0, st>>>(k);
     } else
-        k_postssa_thread<<<p.grid, 128, 0, c->stream>>>(k);
+        k_postssa_thread<<<p.grid, 128, 0, st>>>(k);
     CUDA_OK(cudaGetLastError());
 #else
     static uint32_t gw[GW__N];
@@ -1007,11 +1019,18 @@ static int run(cl_ctx *c, KArgs k) {
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev0, c->stream));
 #endif
-    if (launch_part(c, 1, k)) return -1;       /* the long poles first */
+#if CL_CUDA
+    /* large functions (CTA groups) on a side stream, concurrently with the rest */
+    CUDA_OK(cudaEventRecord(c->ev_fork, c->stream));
+    CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+#endif
+    if (launch_part(c, 1, k, false, true)) return -1;
     if (launch_part(c, 2, k)) return -1;
     if (launch_part(c, 0, k)) return -1;
     if (launch_part(c, 0, k, true)) return -1; /* what outgrew the thread kernel */
 #if CL_CUDA
+    CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
+    CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     CUDA_OK(cudaEventRecord(c->ev1, c->stream));
 #endif
     if (d2h(c->h_cursor, c->d_cursor, sizeof c->h_cursor, c->stream)) return -1;
