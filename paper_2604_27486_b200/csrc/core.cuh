@@ -112,6 +112,7 @@ struct Prof {
 /* NW = warps per group.  NW == 1: the group is a warp (several independent
  * groups per CTA).  NW > 1: the group is the whole CTA.  NW == 0: host.     */
 template <int NW> struct Grp {
+    static constexpr uint32_t THREADS = NW * 32;
     uint32_t rank, size;
     uint32_t *red;             /* NW > 1: shared scratch, NW + 2 words         */
 #if CL_DEV
@@ -169,6 +170,7 @@ template <int NW> struct Grp {
  * the device it is the thread-per-function kernel (32 independent functions
  * per warp: every lane is busy, the collectives are identities).            */
 template <> struct Grp<0> {
+    static constexpr uint32_t THREADS = 1;
     uint32_t rank, size;
     uint32_t *red;
     CLMEM void sync() const {}

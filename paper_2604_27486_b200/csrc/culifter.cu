@@ -12,6 +12,7 @@
  * loads it and there is no CPU fallback in the product path.
  */
 #include "core.cuh"
+#include "tile.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -97,6 +98,9 @@ struct KArgs {
     uint32_t hot_bytes;        /* shared memory per group for the hot arrays     */
     uint32_t passes, max_rounds, emit_matches, raw_passes;
     const cl_sr_entry *sr; uint32_t n_sr;
+    /* tile kernel (tile.cuh) */
+    const TileDesc *tiles; uint32_t n_tiles; uint32_t *tile_counter;
+    uint8_t *tile_scratch; unsigned long long tile_scratch_per_cta;
 };
 
 /* ------------------------------------------------------ work memory layout */
@@ -563,6 +567,67 @@ template <int WARPS, int MINB> __global__ void __launch_bounds__(WARPS * 32, MIN
 #endif
 
 
+/* ------------------------------------------------------------- tile kernel */
+/* one CTA = one tile of consecutive small functions resident in shared memory
+ * (tile.cuh); persistent CTAs pull tiles off a counter                       */
+static_assert(sizeof(TFuncOut) == sizeof(FuncOut), "TFuncOut mirrors FuncOut");
+template <class C> CLHD size_t tile_scratch_bytes() {
+    return ((sizeof(Stage) * C::S + 255) & ~(size_t)255) + ((sizeof(cl_event) * C::E + 255) & ~(size_t)255);
+}
+CLHD TileIO tile_io(const KArgs &a) {
+    TileIO io;
+    io.in = a.in;
+    io.o_hdr = a.o_hdr; io.o_tag = a.o_tag; io.o_pay = a.o_pay; io.o_imm = a.o_imm;
+    io.o_alive = a.o_alive; io.o_def_iid = a.o_def_iid; io.o_origin = a.o_origin;
+    io.o_blk = a.o_blk; io.o_blk_start = a.o_blk_start; io.o_blk_cnt = a.o_blk_cnt;
+    io.o_ev = a.o_ev; io.o_func = a.o_func;
+    for (int k = 0; k < 4; k++) io.cap[k] = a.cap[k];
+    io.cursor = a.cursor; io.stats = a.stats;
+    io.retry_list = a.retry_list; io.retry_count = a.retry_count;
+    return io;
+}
+template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const KArgs &a, uint32_t cta) {
+    FS s;
+    unsigned long long prof[PF__N];
+    for (int k = 0; k < PF__N; k++) prof[k] = 0;
+    const unsigned long long t_begin = now();
+    memset(&s, 0, sizeof s);
+    s.pb = a.pb; s.ms = a.in.modsets; s.opflags = a.opflags; s.solo = g.size == 1;
+    s.passes = a.passes; s.max_rounds = a.max_rounds; s.emit_matches = 0;
+    s.S.hdr = T.hdr; s.S.tag = T.tag; s.S.pay = T.pay;
+    s.st = &T.f_stat[0]; s.n_ev = &T.n_ev;
+    s.prof = prof;
+    TileG<C> tg;
+    tg.T = &T;
+    uint8_t *scr = a.tile_scratch + (size_t)cta * a.tile_scratch_per_cta;
+    tg.stage = (Stage *)scr;
+    tg.ev = (cl_event *)(scr + ((sizeof(Stage) * C::S + 255) & ~(size_t)255));
+    tg.mem = a.o_mem;
+    const TileIO io = tile_io(a);
+    t_setup(g, T, s);
+    for (;;) {
+        uint32_t w = 0;
+        if (g.rank == 0) w = a_add(a.tile_counter, 1u);
+        w = g.bcast0(w);
+        if (w >= a.n_tiles) break;
+        t_run_tile(g, T, tg, s, io, a.tiles[w]);
+        g.sync();
+    }
+    if (g.rank == 0) {
+        prof[PF_TOTAL] = now() - t_begin;
+        for (int k = 0; k < PF__N; k++) a_add64(&a.prof[k], prof[k]);
+    }
+}
+#if CL_CUDA
+template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, MINB) k_postssa_tile(KArgs a) {
+    extern __shared__ uint4 dyn_smem[];
+    TileS<C> &T = *(TileS<C> *)dyn_smem;
+    Grp<NW> g; g.rank = threadIdx.x; g.size = NW * 32; g.red = T.red;
+    tile_loop(g, T, a, blockIdx.x);
+}
+#endif
+
+
 /* ------------------------------------------------------- densification */
 /* The run leaves every function's result at an atomically reserved place
  * (completion order).  cl_download turns that into the dense CSR of the ABI
@@ -685,7 +750,7 @@ enum {
     B_O_HDR, B_O_TAG, B_O_PAY, B_O_IMM, B_O_ALIVE, B_O_DEF_IID, B_O_ORIGIN, B_O_EXT_TAG, B_O_EXT_PAY, B_O_MEM,
     B_O_BLK, B_O_BLK_START, B_O_BLK_CNT, B_O_EV, B_O_FUNC,
     B_LIST0, B_LIST1, B_LIST2, B_COUNTER0, B_COUNTER1, B_COUNTER2, B_SCRATCH0, B_SCRATCH1, B_SCRATCH2,
-    B_RETRY_LIST, B_RETRY_WORDS,
+    B_RETRY_LIST, B_RETRY_WORDS, B_TILES, B_TILE_COUNTER, B_TILE_SCRATCH, B_REST_LIST,
     B_D_OFF, B_D_SUMS, B_D_HDR, B_D_TAG, B_D_PAY, B_D_IMM, B_D_ALIVE, B_D_DEF_IID, B_D_ORIGIN, B_D_EV,
     B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B_SR_MAP, B__N
 };
@@ -713,6 +778,13 @@ struct cl_ctx {
     unsigned long long h_cursor[CUR__N] = { 0, 0, 0, 0 };
     Part part[3];              /* 0 = warp groups, 1 = CTA groups, 2 = one thread per function */
     uint32_t *d_retry_list = nullptr, *d_retry_count = nullptr, *d_retry_counter = nullptr;
+    /* tile kernel (tile.cuh): runs of consecutive small functions, one CTA per tile */
+    int tile_mode = 2;         /* 0 off, 1 small tiles (2 CTAs/SM), 2 large tiles (1 CTA/SM) */
+    int tile_warps = 16;
+    std::vector<TileDesc> tiles;
+    std::vector<uint32_t> rest;          /* small functions that are not in a tile */
+    TileDesc *d_tiles = nullptr; uint32_t *d_tile_counter = nullptr, *d_rest = nullptr; uint8_t *d_tile_scratch = nullptr;
+    size_t tile_scratch_per_cta = 0; uint32_t tile_grid = 0, n_tile_funcs = 0, h_retry = 0; bool used_tiles = false;
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
     int cta_warps = 8;         /* warps per CTA of the CTA-group kernel (8, 16 or 32) */        /* warps per CTA of the phase-synchronous warp kernel (0 = free-running kernel) */
@@ -764,6 +836,8 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_THREAD_MAX")) c->thread_max = CL_CUDA ? (uint32_t)atoi(e) : 0;
     if (const char *e = getenv("CL_WARP_SYNC")) { const int v = atoi(e); c->warp_sync = (v == 0 || v == 8 || v == 16 || v == 32 || v == 33) ? v : 32; }
     if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
+    if (const char *e = getenv("CL_TILE")) c->tile_mode = std::min(2, std::max(0, atoi(e)));
+    if (const char *e = getenv("CL_TILE_WARPS")) { const int v = atoi(e); c->tile_warps = (v == 8 || v == 32) ? v : 16; }
     if (const char *e = getenv("CL_THREAD_CTAS")) c->thread_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("CL_WARP_CTAS")) c->warp_ctas = std::min(CL_WARP_CTAS_PER_SM, std::max(1, atoi(e)));
     if (const char *e = getenv("CL_CTA_CTAS")) c->cta_ctas = std::min(CL_CTA_CTAS_PER_SM, std::max(1, atoi(e)));
@@ -928,11 +1002,49 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         if (dget(c, CNT_ID[k], &p.d_counter, 1)) return -1;
         if (dget(c, SCR_ID[k], &p.d_scratch, p.scratch_per_group * p.n_groups)) return -1;
     }
-    if (!c->part[2].list.empty()) {
+    /* tiles: maximal runs of consecutive small functions whose capacities fit one tile */
+    c->tiles.clear(); c->rest.clear(); c->n_tile_funcs = 0;
+    if (c->tile_mode) {
+        const bool large = c->tile_mode == 2;
+        const uint32_t cI = large ? TileCfgL::I : TileCfgS::I, cV = large ? TileCfgL::V : TileCfgS::V,
+                       cQ = large ? TileCfgL::Q : TileCfgS::Q, cF = large ? TileCfgL::F : TileCfgS::F,
+                       cB = large ? TileCfgL::B : TileCfgS::B;
+        TileDesc cur = { 0, 0 };
+        uint32_t sI = 0, sV = 0, sQ = 0, sB = 0;
+        auto flush = [&]() { if (cur.nf) { c->tiles.push_back(cur); c->n_tile_funcs += cur.nf; } cur.nf = 0; sI = sV = sQ = sB = 0; };
+        for (uint32_t f = 0; f < F; f++) {
+            const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
+            const uint32_t n = in->blk_off[b1] - in->blk_off[b0], nb = b1 - b0;
+            const uint32_t nimm = in->imm_off[f + 1] - in->imm_off[f];
+            const uint32_t iI = tile_icap(n), iV = tile_vcap(in->func[f].next_vid, n), iQ = tile_qcap(nimm, n);
+            const bool small = n <= c->small_max && n > c->thread_max;
+            const bool fits = small && in->ext_off[f + 1] == in->ext_off[f] && 2 * iI <= cI + 16 && iV <= cV && iQ <= cQ && nb <= cB && nb > 0;
+            if (!fits) { flush(); if (small) c->rest.push_back(f); continue; }
+            if (cur.nf && (sI + iI > cI || sV + iV > cV || sQ + iQ > cQ || sB + nb > cB || cur.nf >= cF)) flush();
+            if (!cur.nf) cur.f0 = f;
+            cur.nf++; sI += iI; sV += iV; sQ += iQ; sB += nb;
+        }
+        flush();
+    }
+    {
         uint32_t *words = nullptr;
-        if (dget(c, B_RETRY_LIST, &c->d_retry_list, c->part[2].list.size())) return -1;
+        if (dget(c, B_RETRY_LIST, &c->d_retry_list, std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs))) return -1;
         if (dget(c, B_RETRY_WORDS, &words, 4)) return -1;
         c->d_retry_count = words; c->d_retry_counter = words + 1;
+    }
+    if (!c->tiles.empty()) {
+#if CL_CUDA
+        const bool large = c->tile_mode == 2;
+        c->tile_scratch_per_cta = large ? tile_scratch_bytes<TileCfgL>() : tile_scratch_bytes<TileCfgS>();
+        c->tile_grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * (large ? 1 : 2), c->tiles.size());
+#else
+        c->tile_scratch_per_cta = tile_scratch_bytes<TileCfgL>();
+        c->tile_grid = 1;
+#endif
+        if (dput(c, B_TILES, &c->d_tiles, c->tiles.data(), c->tiles.size())) return -1;
+        if (dget(c, B_TILE_COUNTER, &c->d_tile_counter, 1)) return -1;
+        if (dget(c, B_TILE_SCRATCH, &c->d_tile_scratch, c->tile_scratch_per_cta * c->tile_grid)) return -1;
+        if (dput(c, B_REST_LIST, &c->d_rest, c->rest.data(), c->rest.size())) return -1;
     }
 
     /* result buffers (worst-case growth, G3/G4) */
@@ -960,18 +1072,20 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
 }
 
 /* launch one kernel: `which` selects the kernel and the scratch, the work list is
- * that part's own or (retry) what the thread kernel queued                       */
-static int launch_part(cl_ctx *c, int which, KArgs k, bool retry = false, bool side = false) {
+ * that part's own, or (mode 1) what an earlier kernel queued on the device, or
+ * (mode 2) the small functions outside the tiles                                */
+static int launch_part(cl_ctx *c, int which, KArgs k, int mode = 0, bool side = false) {
 #if CL_CUDA
     cudaStream_t st = side ? c->stream2 : c->stream;
 #else
     cudaStream_t st = c->stream; (void)side;
 #endif
     Part &p = c->part[which];
-    if (!retry && p.list.empty()) return 0;
-    if (retry && c->part[2].list.empty()) return 0;
-    k.list = retry ? c->d_retry_list : p.d_list;
-    k.n_list = retry ? (uint32_t)c->part[2].list.size() : (uint32_t)p.list.size();
+    const bool retry = mode == 1;
+    if (mode == 0 && p.list.empty()) return 0;
+    if (mode == 2 && c->rest.empty()) return 0;
+    k.list = retry ? c->d_retry_list : mode == 2 ? c->d_rest : p.d_list;
+    k.n_list = retry ? (uint32_t)std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs) : mode == 2 ? (uint32_t)c->rest.size() : (uint32_t)p.list.size();
     k.n_list_ptr = retry ? c->d_retry_count : nullptr;
     k.work_counter = retry ? c->d_retry_counter : p.d_counter;
     k.retry_list = which == 2 ? c->d_retry_list : nullptr;
@@ -1007,6 +1121,36 @@ static int launch_part(cl_ctx *c, int which, KArgs k, bool retry = false, bool s
     return 0;
 }
 
+#if CL_CUDA
+template <class C, int NW, int MINB> static int launch_tile_kernel(cl_ctx *c, const KArgs &k) {
+    const size_t smem = sizeof(TileS<C>);
+    CUDA_OK(cudaFuncSetAttribute(k_postssa_tile<C, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_postssa_tile<C, NW, MINB><<<c->tile_grid, NW * 32, smem, c->stream>>>(k);
+    CUDA_OK(cudaGetLastError());
+    return 0;
+}
+#endif
+static int launch_tiles(cl_ctx *c, KArgs k) {
+    k.tiles = c->d_tiles; k.n_tiles = (uint32_t)c->tiles.size(); k.tile_counter = c->d_tile_counter;
+    k.tile_scratch = c->d_tile_scratch; k.tile_scratch_per_cta = c->tile_scratch_per_cta;
+    k.retry_list = c->d_retry_list; k.retry_count = c->d_retry_count;
+    if (dzero(k.tile_counter, sizeof(uint32_t), c->stream)) return -1;
+#if CL_CUDA
+    if (c->tile_mode == 2) {
+        if (c->tile_warps == 32) return launch_tile_kernel<TileCfgL, 32, 1>(c, k);
+        if (c->tile_warps == 8) return launch_tile_kernel<TileCfgL, 8, 1>(c, k);
+        return launch_tile_kernel<TileCfgL, 16, 1>(c, k);
+    }
+    if (c->tile_warps == 8) return launch_tile_kernel<TileCfgS, 8, 2>(c, k);
+    return launch_tile_kernel<TileCfgS, 16, 2>(c, k);
+#else
+    static TileS<TileCfgL> T;
+    Grp<0> g; g.rank = 0; g.size = 1; g.red = T.red;
+    tile_loop(g, T, k, 0);
+    return 0;
+#endif
+}
+
 static int run(cl_ctx *c, KArgs k) {
     if (!c->have_in) FAIL("no corpus uploaded");
 #if CL_CUDA
@@ -1016,18 +1160,27 @@ static int run(cl_ctx *c, KArgs k) {
     if (dzero(c->d_stats, sizeof(cl_stats), c->stream)) return -1;
     if (dzero(c->d_prof, sizeof(unsigned long long) * PF__N, c->stream)) return -1;
     if (c->d_retry_count && dzero(c->d_retry_count, sizeof(uint32_t), c->stream)) return -1;
+    /* the tile kernel takes the production run of the post-SSA stage; match lists
+     * (emit_matches / MATCH_ONLY), the raw stage and tables with a pattern that has
+     * no join plan go through the general kernels                                  */
+    bool use_tiles = !c->tiles.empty() && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
+    for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_tiles = use_tiles && c->h_pb.p[pi].join_ok;
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev0, c->stream));
-#endif
-#if CL_CUDA
     /* large functions (CTA groups) on a side stream, concurrently with the rest */
     CUDA_OK(cudaEventRecord(c->ev_fork, c->stream));
     CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
 #endif
-    if (launch_part(c, 1, k, false, true)) return -1;
-    if (launch_part(c, 2, k)) return -1;
-    if (launch_part(c, 0, k)) return -1;
-    if (launch_part(c, 0, k, true)) return -1; /* what outgrew the thread kernel */
+    if (launch_part(c, 1, k, 0, true)) return -1;
+    if (use_tiles) {
+        if (launch_tiles(c, k)) return -1;
+        if (launch_part(c, 0, k, 2)) return -1;  /* small functions outside the tiles */
+        if (launch_part(c, 0, k, 1)) return -1;  /* what the tile kernel handed back */
+    } else {
+        if (launch_part(c, 2, k)) return -1;
+        if (launch_part(c, 0, k)) return -1;
+        if (!c->part[2].list.empty() && launch_part(c, 0, k, 1)) return -1; /* what outgrew the thread kernel */
+    }
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
     CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
@@ -1036,6 +1189,8 @@ static int run(cl_ctx *c, KArgs k) {
     if (d2h(c->h_cursor, c->d_cursor, sizeof c->h_cursor, c->stream)) return -1;
     if (d2h(&c->stats, c->d_stats, sizeof(cl_stats), c->stream)) return -1;
     if (d2h(c->h_prof, c->d_prof, sizeof c->h_prof, c->stream)) return -1;
+    c->h_retry = 0; c->used_tiles = use_tiles;
+    if (c->d_retry_count && d2h(&c->h_retry, c->d_retry_count, sizeof(uint32_t), c->stream)) return -1;
 #if CL_CUDA
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
@@ -1170,6 +1325,12 @@ extern "C" int cl_download(cl_ctx *c, cl_corpus *o, cl_event *events) {
 extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
     for (int i = 0; i < n && i < PF__N; i++) out[i] = c->h_prof[i];
     return PF__N;
+}
+/* debugging aid: how the last run was partitioned: {tiles, functions in tiles, functions the tile kernel
+ * handed back to the general kernel, small functions outside tiles, tile kernel used}            */
+extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
+    out[0] = c->tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles;
+    return 0;
 }
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }
 extern "C" int cl_last_run_ms(cl_ctx *c, float *ms) { *ms = c->last_ms; return 0; }

@@ -1,0 +1,1106 @@
+/* tile.cuh -- the data-parallel form of the post-SSA stage: one CTA keeps a
+ * *tile* (a run of consecutive small functions, ~1000 records) resident in
+ * shared memory and takes all of them through the passes together, one
+ * thread per instruction record / candidate / selected match:
+ *
+ *   use counts + def positions (smem atomics)
+ *   seed classes (per-block class counts)  -> FindSeeds  patterns.py:189-191
+ *   join unification per (pattern, anchor) -> Unify      patterns.py:130-216
+ *   overlap selection (atomicMin bidding)  -> select_matches :241-252
+ *   rewrite planning, id allocation by segmented scans, in-place
+ *   permutation of the stream              -> _apply_patterns :671-707
+ *   pack simplification, dead-pseudo fixpoint, reciprocal chains, tagging
+ *
+ * HBM sees one coalesced read of the tile and one write of the result; every
+ * intermediate round lives in shared memory.  The per-match leaf code
+ * (match_inst, check_tuple, the nine rewrite planners) is core.cuh's: a thread
+ * points its FS at the function that owns the item it works on ("view").
+ *
+ * Exactness: the reference is sequential over blocks and chains.  Everything
+ * here is evaluated on the snapshot taken at the start of a pass, which equals
+ * the sequential result unless a later item observes an earlier item's edit.
+ * Those cases (G5 cross-block escapes, interfering reciprocal chains, RZ/PT
+ * join links, capacity, reference exceptions) are *detected* and the function
+ * is handed, untouched, to the general per-function kernel of core.cuh.
+ */
+#pragma once
+#include "core.cuh"
+
+namespace clk {
+
+static constexpr uint32_t CL_ST_REDO = 100;     /* internal: redo this function on the general kernel */
+
+struct TileDesc { uint32_t f0, nf; };
+
+struct TMatch { uint16_t pos[3]; uint8_t pat, n; };
+struct TChain { uint16_t add, mufu; uint32_t rcp, addv; uint8_t f, ok; uint16_t rank; };
+
+/* capacities of one tile (compile time: the tile lives in shared memory) */
+struct TileCfgL { static constexpr uint32_t I = 1024, V = 1792, Q = 320, F = 32, B = 96, M = 1024, S = 512, X = 256, E = 512; };
+struct TileCfgS { static constexpr uint32_t I = 640, V = 1152, Q = 208, F = 24, B = 64, M = 640, S = 320, X = 160, E = 320; };
+
+template <class C> struct TileS {
+    alignas(16) cl_hdr hdr[C::I];
+    alignas(16) uint16_t tag[C::I * 8];
+    alignas(16) uint32_t pay[C::I * 8];
+    unsigned long long owner[C::I];
+    uint32_t usecnt[C::V], defpos[C::V], redirect[C::V], origin[C::V];
+    int32_t def_iid[C::V];
+    cl_imm imm[C::Q];
+    SelRec sel[C::S];
+    TMatch mt[C::M];
+    TChain chain[C::X];
+    uint16_t outpos[C::I], sel_at[C::I];
+    uint8_t keep[C::I], inscnt[C::I], clsid[C::I], fidx[C::I], bidx[C::I], flag[C::I];
+    uint8_t alive[C::V];
+    uint8_t mstate[C::M];
+    /* blocks */
+    uint32_t bo[C::B + 1], bo2[C::B + 1], b_first[C::B];
+    cl_blk blk[C::B];
+    uint32_t ccnt[C::B][MAX_CLS];
+    uint8_t bfun[C::B];
+    /* functions */
+    uint32_t f_vbase[C::F + 1], f_qbase[C::F + 1], f_vcap[C::F], f_qcap[C::F], f_mem0[C::F];
+    uint32_t f_nvid[C::F], f_niid[C::F], f_nimm[C::F], f_ntemp[C::F], f_stat[C::F], f_nev[C::F];
+    uint32_t f_b0[C::F + 1], f_chg[C::F], f_red[C::F], f_first[C::F], f_aux[C::F], f_nin[C::F];
+    uint32_t f_oi[C::F], f_oq[C::F], f_ov[C::F], f_oe[C::F];
+    uint32_t f_stats[C::F][64];
+    uint8_t f_arch[C::F], f_active[C::F], f_odd[C::F], f_gate[C::F];
+    /* class tables of the two pattern tables */
+    uint16_t cls_op[2][MAX_CLS];
+    uint32_t n_cls[2], anchor_mask[2][MAX_CLS];
+    /* tile scalars */
+    uint32_t n, nb, nf, f0, I0, B0, n_mt, n_sel, n_ev, fail, vtot, qtot, n_chain, work;
+    uint32_t red[40];
+};
+
+template <class C> struct TileG {      /* what lives outside shared memory */
+    TileS<C> *T;
+    Stage *stage;             /* [C::S] staged rewrites (L2-resident scratch)   */
+    cl_event *ev;             /* [C::E]                                          */
+    cl_memref *mem;           /* o_mem: memrefs of the corpus, mutable copy      */
+};
+
+/* ------------------------------------------------------------------ views */
+template <class C> CLD void tv_view(FS &s, TileS<C> &T, const TileG<C> &tg, uint32_t f) {
+    const uint32_t vb = T.f_vbase[f], qb = T.f_qbase[f];
+    s.usecnt = T.usecnt + vb; s.defpos = T.defpos + vb; s.redirect = T.redirect + vb; s.origin = T.origin + vb;
+    s.def_iid = T.def_iid + vb; s.alive = T.alive + vb;
+    s.imm = T.imm + qb;
+    s.cap.V = T.f_vcap[f]; s.cap.Q = T.f_qcap[f];
+    s.mem = tg.mem + T.f_mem0[f];
+    s.st = &T.f_stat[f];
+    s.f = T.f0 + f; s.arch = T.f_arch[f];
+}
+template <class C> CLD bool tf_ok(const TileS<C> &T, uint32_t f) { return *(volatile const uint32_t *)&T.f_stat[f] == 0; }
+template <class C> CLD void tf_fail(TileS<C> &T, uint32_t f, uint32_t code) { a_cas0(&T.f_stat[f], code); }
+
+template <class C> CLD void t_event(FS &s, TileS<C> &T, const TileG<C> &tg, uint32_t f, uint32_t seq, uint32_t kind,
+                                    uint32_t idx, uint32_t a, uint32_t b) {
+    const uint32_t k = a_add(&T.n_ev, 1u);
+    if (k < C::E) {
+        cl_event e; e.func = T.f0 + f; e.seq = seq; e.kind = kind; e.idx = idx; e.a = a; e.b = b; e.c = 0; e.d = 0;
+        tg.ev[k] = e;
+        a_add(&T.f_nev[f], 1u);
+    } else
+        T.fail = 1;
+    (void)s;
+}
+
+template <class C> CLD int t_class_of(const TileS<C> &T, unsigned table, uint16_t op) {
+    const uint32_t n = T.n_cls[table];
+    for (uint32_t c = 0; c < n; c++) if (T.cls_op[table][c] == op) return (int)c;
+    return -1;
+}
+
+/* block / function index of every record from the block offsets */
+template <class G, class C> CLF void t_index(const G &g, TileS<C> &T) {
+    GFOR(g, i, T.n) if (i < T.n) {
+        uint32_t lo = 0, hi = T.nb;                  /* last b with bo[b] <= i */
+        while (lo + 1 < hi) { const uint32_t mid = (lo + hi) >> 1; if (T.bo[mid] <= i) lo = mid; else hi = mid; }
+        T.bidx[i] = (uint8_t)lo; T.fidx[i] = T.bfun[lo];
+    }
+    g.sync();
+}
+
+/* in-place permutation of the stream: record i moves to dst(i) (NONE32 = dropped).
+ * Everything is read before anything is written.                              */
+template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T, uint32_t n, F dst) {
+#if CL_DEV
+    constexpr int K = (int)((C::I + G::THREADS - 1) / G::THREADS);
+    uint4 r[K][4];
+    uint32_t d[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const uint32_t i = (uint32_t)k * g.size + g.rank;
+        d[k] = i < n ? dst(i) : NONE32;
+        if (d[k] != NONE32) {
+            r[k][0] = *(const uint4 *)&T.hdr[i];
+            r[k][1] = *(const uint4 *)&T.tag[(size_t)i * 8];
+            r[k][2] = ((const uint4 *)&T.pay[(size_t)i * 8])[0];
+            r[k][3] = ((const uint4 *)&T.pay[(size_t)i * 8])[1];
+        }
+    }
+    g.sync();
+#pragma unroll
+    for (int k = 0; k < K; k++)
+        if (d[k] != NONE32) {
+            const uint32_t o = d[k];
+            *(uint4 *)&T.hdr[o] = r[k][0];
+            *(uint4 *)&T.tag[(size_t)o * 8] = r[k][1];
+            ((uint4 *)&T.pay[(size_t)o * 8])[0] = r[k][2];
+            ((uint4 *)&T.pay[(size_t)o * 8])[1] = r[k][3];
+        }
+    g.sync();
+#else
+    static Rec tmp[C::I];
+    static uint32_t d[C::I];
+    for (uint32_t i = 0; i < n; i++) {
+        d[i] = dst(i);
+        if (d[i] != NONE32) { tmp[i].h = T.hdr[i]; memcpy(tmp[i].tag, &T.tag[(size_t)i * 8], 16); memcpy(tmp[i].pay, &T.pay[(size_t)i * 8], 32); }
+    }
+    for (uint32_t i = 0; i < n; i++)
+        if (d[i] != NONE32) { T.hdr[d[i]] = tmp[i].h; memcpy(&T.tag[(size_t)d[i] * 8], tmp[i].tag, 16); memcpy(&T.pay[(size_t)d[i] * 8], tmp[i].pay, 32); }
+    (void)g;
+#endif
+}
+
+/* ------------------------------------------------------------------ def-use */
+/* ssa.py:613-636 for every live function of the tile at once                  */
+template <class G, class C> CLF void t_usecount(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
+    PROF(g, s, PF_USECOUNT);
+    GFOR(g, v, T.vtot) if (v < T.vtot) { T.usecnt[v] = 0; T.defpos[v] = NONE32; }
+    g.sync();
+    GFOR(g, i, T.n) if (i < T.n) {
+        const uint32_t f = T.fidx[i];
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        const cl_hdr h = T.hdr[i];
+        const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
+        bool odd = false;
+        for (unsigned k = 0; k < nd; k++) {
+            const opnd d = get_slot(s, h, i, d0 + k);
+            const unsigned kd = kind_of(d.tag);
+            if (kd == CL_K_VALUE) { if (d.pay < s.cap.V) s.defpos[d.pay] = i; }
+            else odd |= !(kd == CL_K_RZ || kd == CL_K_URZ || kd == CL_K_PRED);
+        }
+        if (odd) T.f_odd[f] = 1;
+        for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_add(&s.usecnt[v], 1u); });
+    }
+    GFOR(g, b, T.nb) if (b < T.nb) {
+        const uint32_t f = T.bfun[b];
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        for (int k = 0; k < 2; k++)
+            if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE && T.blk[b].term_pay[k] < s.cap.V)
+                a_add(&s.usecnt[T.blk[b].term_pay[k]], 1u);
+    }
+    g.sync();
+}
+
+/* ----------------------------------------------------------------- matching */
+/* one (pattern, anchor) item of match_patterns (patterns.py:181-216), join form
+ * (see match_block in core.cuh); positions are tile positions                  */
+template <class C> CLF void t_try_anchor(TileS<C> &T, FS &s, unsigned table, uint32_t i, unsigned pi, uint32_t f) {
+    const cl_pattern_blob *pb = s.pb;
+    const cl_pattern &p = pb->p[pi];
+    const unsigned nt = p.n_templates;
+    const uint32_t b = T.bidx[i], lo = T.bo[b], hi = T.bo[b + 1];
+    uint32_t idx[3] = { NONE32, NONE32, NONE32 };
+    idx[p.join_order[0]] = i;
+    for (unsigned k = 1; k < nt; k++) {
+        const unsigned t = p.join_order[k], from = p.join_from[k];
+        const cl_hdr hf = T.hdr[idx[from]];
+        const cl_template &tf = p.t[from];
+        if (hf.n_defs != tf.n_defs || hf.n_aux != tf.n_aux || hf.n_uses != tf.n_uses || (hf.flags & CL_IF_EXT)) return;
+        const unsigned long long mm = s.ms[hf.modset].mask;
+        if ((mm & tf.mods_all) != tf.mods_all || (mm & tf.mods_none)) return;
+        const opnd o = get_slot(s, hf, idx[from], has_guard(hf) + p.join_slot[k]);
+        if (!is_value(o)) {
+            const unsigned ko = kind_of(o.tag);       /* a non-SSA link: the literal product decides */
+            if (ko == CL_K_RZ || ko == CL_K_URZ || ko == CL_K_PRED) tf_fail(T, f, CL_ST_REDO);
+            return;
+        }
+        const uint32_t dp = o.pay < s.cap.V ? s.defpos[o.pay] : NONE32;
+        if (dp == NONE32 || dp < lo || dp >= hi || T.hdr[dp].op != p.t[t].op) return;
+        idx[t] = dp;
+    }
+    if (nt > 1 && !(idx[0] < idx[1] && (nt < 3 || idx[1] < idx[2]))) return;
+    /* budget (G1): rank of the tuple in itertools.product order, needed only when the
+     * product of the candidate-list sizes can exceed it                             */
+    {
+        uint32_t cn[3] = { 1, 1, 1 };
+        int cl[3] = { 0, 0, 0 };
+        for (unsigned t = 0; t < nt; t++) { cl[t] = t_class_of(T, table, p.t[t].op); cn[t] = T.ccnt[b][cl[t]]; }
+        const unsigned long long prod = (unsigned long long)cn[0] * cn[1] * cn[2];
+        if (prod > pb->budget) {
+            unsigned long long r = 0;
+            for (unsigned t = 0; t < nt; t++) {
+                uint32_t ci = 0;
+                for (uint32_t j = lo; j < idx[t]; j++) ci += T.clsid[j] == (uint8_t)cl[t];
+                r = t == 0 ? ci : r * cn[t] + ci;
+            }
+            if (r >= pb->budget) return;
+        }
+    }
+    Bind bd;
+    if (!check_tuple(s, p, idx, bd)) return;
+    const uint32_t m = a_add(&T.n_mt, 1u);
+    if (m < C::M) {
+        TMatch r;
+        r.pat = (uint8_t)pi; r.n = (uint8_t)nt;
+        r.pos[0] = (uint16_t)idx[0]; r.pos[1] = (uint16_t)(nt > 1 ? idx[1] : 0xFFFFu); r.pos[2] = (uint16_t)(nt > 2 ? idx[2] : 0xFFFFu);
+        T.mt[m] = r;
+        T.mstate[m] = MS_UNDECIDED;
+    } else
+        T.fail = 1;
+    a_add(&T.f_stats[f][pi], 1u);
+}
+
+template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, unsigned table) {
+    PROF(g, s, PF_MATCH);
+    GFOR(g, k, T.nb * MAX_CLS) if (k < T.nb * MAX_CLS) (&T.ccnt[0][0])[k] = 0;
+    if (g.rank == 0) T.n_mt = 0;
+    g.sync();
+    GFOR(g, i, T.n) if (i < T.n) {
+        int c = -1;
+        if (T.f_gate[T.fidx[i]]) {
+            c = t_class_of(T, table, T.hdr[i].op);
+            if (c >= 0) a_add(&T.ccnt[T.bidx[i]][c], 1u);
+        }
+        T.clsid[i] = (uint8_t)c;
+    }
+    g.sync();
+    GFOR(g, i, T.n) if (i < T.n) {
+        const unsigned c = T.clsid[i];
+        if (c == 0xFFu) continue;
+        uint32_t pm = T.anchor_mask[table][c];
+        if (!pm) continue;
+        const uint32_t f = T.fidx[i];
+        if (!tf_ok(T, f)) continue;
+        if (T.f_odd[f]) { tf_fail(T, f, CL_ST_REDO); continue; }
+        tv_view(s, T, tg, f);
+        for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) t_try_anchor(T, s, table, i, pi, f);
+    }
+    g.sync();
+}
+
+/* select_matches (patterns.py:241-252) for all blocks of the tile at once; the
+ * key orders like the reference's stable sort: (start, -len, pattern, product
+ * order) where product order within one pattern and start is position order.  */
+CLD unsigned long long t_key(const TMatch &m) {
+    return (unsigned long long)m.pos[0] << 40 | (unsigned long long)(3u - m.n) << 38 | (unsigned long long)m.pat << 32 |
+           (unsigned long long)m.pos[1] << 16 | m.pos[2];
+}
+template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T, FS &s) {
+    PROF(g, s, PF_SELECT);
+    const uint32_t n = T.n, nm = T.n_mt;
+    GFOR(g, p, n) if (p < n) { T.keep[p] = 0; T.sel_at[p] = 0xFFFFu; }
+    g.sync();
+    for (;;) {
+        GFOR(g, p, n) if (p < n && !T.keep[p]) T.owner[p] = NONE64;
+        g.sync();
+        GFOR(g, m, nm) if (m < nm && T.mstate[m] == MS_UNDECIDED) {
+            const TMatch r = T.mt[m];
+            bool clash = false;
+            for (unsigned t = 0; t < r.n; t++) clash |= T.keep[r.pos[t]] != 0;
+            if (clash) T.mstate[m] = MS_REJECTED;
+            else { const unsigned long long key = t_key(r); for (unsigned t = 0; t < r.n; t++) a_min64(&T.owner[r.pos[t]], key); }
+        }
+        g.sync();
+        bool left = false;
+        GFOR(g, m, nm) if (m < nm && T.mstate[m] == MS_UNDECIDED) {
+            const TMatch r = T.mt[m];
+            const unsigned long long key = t_key(r);
+            bool mine = true;
+            for (unsigned t = 0; t < r.n; t++) mine &= T.owner[r.pos[t]] == key;
+            if (mine) T.mstate[m] = MS_SELECTED; else left = true;
+        }
+        g.sync();
+        /* marks are written after every bid was compared (a winner never blocks a rival's compare) */
+        GFOR(g, m, nm) if (m < nm && T.mstate[m] == MS_SELECTED && T.sel_at[T.mt[m].pos[0]] == 0xFFFFu) {
+            const TMatch r = T.mt[m];
+            for (unsigned t = 0; t < r.n; t++) T.keep[r.pos[t]] = 1;
+            T.sel_at[r.pos[0]] = (uint16_t)m;
+        }
+        const bool again = g.any(left);
+        g.sync();
+        if (!again) break;
+    }
+    uint32_t count = 0;
+    GFOR(g, p, n) {
+        const bool fl = p < n && T.sel_at[p] != 0xFFFFu;
+        uint32_t cnt;
+        const uint32_t off = g.flag_exscan(fl, cnt);
+        if (fl && count + off < C::S) {
+            const TMatch m = T.mt[T.sel_at[p]];
+            SelRec r;
+            r.pat = m.pat; r.n = m.n; r.pad0 = r.pad1 = 0; r.blk = T.bidx[p];
+            r.pos[0] = m.pos[0]; r.pos[1] = m.n > 1 ? m.pos[1] : NONE32; r.pos[2] = m.n > 2 ? m.pos[2] : NONE32;
+            T.sel[count + off] = r;
+            a_add(&T.f_stats[T.fidx[p]][16 + m.pat], 1u);
+        }
+        count += cnt;
+    }
+    if (count > C::S) { if (g.rank == 0) T.fail = 1; count = 0; }
+    g.sync();
+    return count;
+}
+
+/* fix-up of one staged match once the bases are known (apply_stage of core.cuh
+ * without the in-place retag, which the caller does before the stream moves)   */
+template <class C> CLF void t_apply_stage(FS &s, Stage &st, uint32_t out) {
+    for (unsigned k = 0; k < st.nv; k++) {
+        const uint32_t v = st.vbase + k;
+        if (v >= s.cap.V) continue;
+        s.alive[v] = 1; s.origin[v] = CL_ORG_PAIR;
+        s.def_iid[v] = st.val_def[k] < 0 ? -1 : (int32_t)(st.ibase + (uint32_t)st.val_def[k]);
+    }
+    for (unsigned k = 0; k < st.nq; k++) if (st.mbase + k < s.cap.Q) s.imm[st.mbase + k] = st.imm[k];
+    if (!st.ok) return;                      /* refused: the allocations above leak (G4) */
+    for (unsigned r = 0; r < st.nins; r++) {
+        const SRec q = st.rec[r];
+        Rec rec;
+        rec.h.iid = st.ibase + q.iid; rec.h.op = q.op; rec.h.modset = q.modset;
+        rec.h.n_defs = q.n_defs; rec.h.n_aux = 0; rec.h.n_uses = q.n_uses; rec.h.flags = 0; rec.h.ext = 0;
+        for (unsigned k = 0; k < 8; k++) { rec.tag[k] = k < 4 ? q.tag[k] : 0; rec.pay[k] = k < 4 ? q.pay[k] : 0; }
+        const unsigned ns = (unsigned)rec.h.n_defs + rec.h.n_uses;
+        for (unsigned k = 0; k < ns; k++)
+            if (rec.tag[k] & CL_T_REL) {
+                rec.pay[k] += kind_of(rec.tag[k]) == CL_K_VALUE ? st.vbase : st.mbase;
+                rec.tag[k] &= (uint16_t)~CL_T_REL;
+            }
+        st_rec(s, out + r, rec);
+    }
+    for (unsigned k = 0; k < st.nupd; k++) if (st.upd_vid[k] < s.cap.V) s.def_iid[st.upd_vid[k]] = (int32_t)(st.ibase + st.upd_iid[k]);
+    for (unsigned k = 0; k < st.ndrop; k++) if (st.drop_vid[k] < s.cap.V) s.alive[st.drop_vid[k]] = 0;
+}
+
+
+/* running exclusive scan over items [0, n) in order                           */
+template <class G, class FIN, class FOUT> CLD uint32_t t_scan(const G &g, uint32_t n, FIN in, FOUT out) {
+    uint32_t run = 0;
+    GFOR(g, j, n) {
+        const uint32_t x = j < n ? in(j) : 0u;
+        uint32_t t;
+        const uint32_t o = g.exscan(x, t);
+        if (j < n) out(j, run + o);
+        run += t;
+    }
+    return run;
+}
+
+/* new block offsets after a permutation described by outpos[] (position of the
+ * first output slot of every old record) and the new length                   */
+template <class G, class C> CLD void t_rebase_blocks(const G &g, TileS<C> &T, uint32_t n_old, uint32_t n_new) {
+    GFOR(g, b, T.nb + 1) if (b <= T.nb) { const uint32_t old = T.bo[b]; T.bo2[b] = old < n_old ? (uint32_t)T.outpos[old] : n_new; }
+    g.sync();
+    GFOR(g, b, T.nb + 1) if (b <= T.nb) T.bo[b] = T.bo2[b];
+    if (g.rank == 0) T.n = n_new;
+    g.sync();
+}
+
+/* _apply_patterns (patterns.py:671-707): one round over every gated function.
+ * All blocks are rewritten against the def-use snapshot of the round's start;
+ * a rewrite that removes a use of a value defined in a *later* block of its
+ * function would be seen by that block's escape test in the reference (G5):
+ * such functions are redone sequentially.                                   */
+template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, unsigned table,
+                                                      uint32_t phase) {
+    t_usecount(g, T, tg, s);
+    t_match(g, T, tg, s, table);
+    if (T.fail || T.n_mt == 0) return;
+    const uint32_t ns = t_select(g, T, s);
+    if (T.fail || ns == 0) return;
+    const uint32_t n = T.n;
+    PROF(g, s, PF_PLAN);
+    GFOR(g, p, n) if (p < n) { T.keep[p] = 1; T.inscnt[p] = 0; }
+    GFOR(g, f, T.nf) if (f < T.nf) T.f_first[f] = NONE32;
+    GFOR(g, b, T.nb) if (b < T.nb) T.b_first[b] = NONE32;
+    g.sync();
+    /* plan: one lane per selected match, once */
+    GFOR(g, j, ns) if (j < ns) {
+        const SelRec m = T.sel[j];
+        Stage &st = tg.stage[j];
+        st.ok = st.rm = st.nins = st.retag = st.nv = st.nq = st.nupd = st.ndrop = 0;
+        st.ni = 0;
+        const uint32_t f = T.fidx[m.pos[0]];
+        if (j == 0 || T.fidx[T.sel[j - 1].pos[0]] != f) T.f_first[f] = j;
+        if (j == 0 || T.sel[j - 1].blk != m.blk) T.b_first[m.blk] = j;
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        RW c;
+        c.s = &s; c.st = &st; c.n = m.n; c.pat = m.pat; c.overflow = false;
+        for (unsigned t = 0; t < m.n; t++) { c.idx[t] = m.pos[t]; c.h[t] = T.hdr[c.idx[t]]; }
+        for (unsigned t = m.n; t < 3; t++) c.idx[t] = NONE32;
+        st.ok = run_rewrite(c);
+        if (c.overflow) tf_fail(T, f, CL_ST_REDO);
+        if (st.ok && st.rm) {
+            /* G5: does a removed record use a value defined in a later block of its function? */
+            bool hazard = false;
+            for (unsigned t = 0; t < m.n; t++) {
+                if (!(st.rm >> t & 1)) continue;
+                for_value_operands(s, c.h[t], c.idx[t], [&](uint32_t v) {
+                    const uint32_t dp = v < s.cap.V ? s.defpos[v] : NONE32;
+                    hazard |= dp != NONE32 && T.bidx[dp] > m.blk;
+                });
+            }
+            if (hazard) tf_fail(T, f, CL_ST_REDO);
+        }
+    }
+    g.sync();
+    /* exclusive scans in select order (tile wide; rebased per function below): id bases (G3) */
+    t_scan(g, ns, [&](uint32_t j) { const Stage &st = tg.stage[j]; return (uint32_t)st.nv | (uint32_t)st.ni << 16; },
+           [&](uint32_t j, uint32_t x) { T.owner[j] = x; });
+    t_scan(g, ns, [&](uint32_t j) { return (uint32_t)tg.stage[j].nq; },
+           [&](uint32_t j, uint32_t x) { T.owner[j] |= (unsigned long long)x << 32; });
+    g.sync();
+    GFOR(g, j, ns) if (j < ns) {
+        const SelRec m = T.sel[j];
+        const uint32_t f = T.fidx[m.pos[0]];
+        Stage &st = tg.stage[j];
+        const unsigned long long me = T.owner[j], first = T.owner[T.f_first[f]];
+        const uint32_t rv = (uint32_t)(me & 0xFFFFu) - (uint32_t)(first & 0xFFFFu);
+        const uint32_t ri = (uint32_t)(me >> 16 & 0xFFFFu) - (uint32_t)(first >> 16 & 0xFFFFu);
+        const uint32_t rq = (uint32_t)(me >> 32) - (uint32_t)(first >> 32);
+        st.vbase = T.f_nvid[f] + rv; st.ibase = T.f_niid[f] + ri; st.mbase = T.f_nimm[f] + rq;
+        if (j + 1 == ns || T.fidx[T.sel[j + 1].pos[0]] != f) {
+            /* last match of its function: the function's new counters; over capacity -> general kernel */
+            if (st.vbase + st.nv > T.f_vcap[f] || st.mbase + st.nq > T.f_qcap[f]) tf_fail(T, f, CL_ST_REDO);
+            T.f_aux[f] = j;
+        }
+    }
+    g.sync();
+    GFOR(g, f, T.nf) if (f < T.nf && T.f_first[f] != NONE32 && tf_ok(T, f)) {
+        const Stage &st = tg.stage[T.f_aux[f]];
+        T.f_nvid[f] = st.vbase + st.nv; T.f_niid[f] = st.ibase + st.ni; T.f_nimm[f] = st.mbase + st.nq;
+    }
+    /* marks, in-place retags (_rw_imad_wide :414-418), diagnostics, counters */
+    GFOR(g, j, ns) if (j < ns) {
+        const SelRec m = T.sel[j];
+        const uint32_t f = T.fidx[m.pos[0]];
+        if (!tf_ok(T, f)) continue;
+        Stage &st = tg.stage[j];
+        if (st.ok) {
+            T.inscnt[m.pos[m.n - 1]] = st.nins;                      /* anchor :689 */
+            for (unsigned t = 0; t < m.n; t++) if (st.rm >> t & 1) T.keep[m.pos[t]] = 0;
+            if (st.retag) {
+                cl_hdr &h = T.hdr[m.pos[0]];
+                h.modset = s.ms[h.modset].minus_wide;
+                h.op = CL_OP_IMAD64;
+            }
+            a_add(&T.f_stats[f][32 + m.pat], 1u);
+            a_add(&T.f_chg[f], 1u);
+        } else {
+            a_add(&T.f_stats[f][48 + m.pat], 1u);
+            t_event(s, T, tg, f, phase << 28 | (m.blk - T.f_b0[f]), CL_EV_REFUSED, j - T.b_first[m.blk], m.pat, T.blk[m.blk].bid);
+        }
+    }
+    g.sync();
+    /* output position of every record (dead functions keep their records as they are) */
+    const uint32_t tot = t_scan(g, n, [&](uint32_t p) { return (uint32_t)T.keep[p] + T.inscnt[p]; },
+                                [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
+    if (tot > C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
+    g.sync();
+    PROF(g, s, PF_EMIT);
+    t_permute(g, T, n, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] + T.inscnt[p] : NONE32; });
+    /* staged records to their place, value table, immediates */
+    GFOR(g, j, ns) if (j < ns) {
+        const SelRec m = T.sel[j];
+        const uint32_t f = T.fidx[m.pos[0]];
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        t_apply_stage<C>(s, tg.stage[j], T.outpos[m.pos[m.n - 1]]);
+    }
+    g.sync();
+    t_rebase_blocks(g, T, n, tot);
+    t_index(g, T);
+}
+
+/* ordered in-place compaction of the stream by keep[]                         */
+template <class G, class C> CLF void t_compact(const G &g, TileS<C> &T) {
+    const uint32_t n = T.n;
+    const uint32_t tot = t_scan(g, n, [&](uint32_t p) { return (uint32_t)T.keep[p]; },
+                                [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
+    g.sync();
+    t_permute(g, T, n, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] : NONE32; });
+    t_rebase_blocks(g, T, n, tot);
+    t_index(g, T);
+}
+
+/* remove_dead_pseudo (patterns.py:771-791) for the functions with f_gate set   */
+template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
+    PROF(g, s, PF_DCE);
+    t_usecount(g, T, tg, s);
+    GFOR(g, i, T.n) if (i < T.n) T.keep[i] = 1;
+    g.sync();
+    uint32_t removed = 0;
+    for (;;) {
+        uint32_t mine = 0;
+        GFOR(g, i, T.n) if (i < T.n && T.keep[i]) {
+            const uint32_t f = T.fidx[i];
+            if (!T.f_gate[f] || !tf_ok(T, f)) continue;
+            const cl_hdr h = T.hdr[i];
+            if (h.op >= CL_OP__COUNT || !(s.opflags[h.op] & CL_OPF_PURE)) continue;
+            tv_view(s, T, tg, f);
+            unsigned nd = 0; bool used = false;
+            for_value_defs(s, h, i, [&](uint32_t v) { nd++; used |= v < s.cap.V && *(volatile uint32_t *)&s.usecnt[v] != 0; });
+            if (!nd || used) continue;
+            T.keep[i] = 0;
+            mine++;
+            for_value_defs(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.alive[v] = 0; });
+            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_sub(&s.usecnt[v], 1u); });
+        }
+        const uint32_t dead = g.sum(mine);
+        g.sync();
+        if (!dead) break;
+        removed += dead;
+    }
+    if (removed) t_compact(g, T);
+}
+
+/* simplify_packs + _redirect_values (patterns.py:710-764) for the gated functions;
+ * f_red[f] = redirects of function f                                          */
+template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
+    PROF(g, s, PF_SIMPLIFY);
+    t_usecount(g, T, tg, s);
+    GFOR(g, v, T.vtot) if (v < T.vtot) T.redirect[v] = NONE32;
+    GFOR(g, f, T.nf) if (f < T.nf) T.f_red[f] = 0;
+    g.sync();
+    uint32_t mine = 0;
+    GFOR(g, i, T.n) if (i < T.n) {
+        const cl_hdr h = T.hdr[i];
+        if (h.op != CL_OP_PACK64 || h.n_uses != 2) continue;
+        const uint32_t f = T.fidx[i];
+        if (!T.f_gate[f] || !tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        opnd lo = get_use(s, h, i, 0), hi = get_use(s, h, i, 1);
+        if (!is_value(lo) || !is_value(hi)) continue;
+        if ((lo.tag | hi.tag) & (CL_T_NEG | CL_T_NOT)) continue;
+        if (lo.pay >= s.cap.V || hi.pay >= s.cap.V) continue;
+        const uint32_t plo = s.defpos[lo.pay], phi = s.defpos[hi.pay];
+        if (plo == NONE32 || phi == NONE32) continue;
+        const cl_hdr dlo = T.hdr[plo], dhi = T.hdr[phi];
+        if (!(dlo.op == CL_OP_UNPACK64 && has_mod(s, dlo, CL_MB_LO) && dhi.op == CL_OP_UNPACK64 && has_mod(s, dhi, CL_MB_HI))) continue;
+        if (!dlo.n_uses || !dhi.n_uses) { fail(s, CL_ST_INDEX_ERROR); continue; }
+        opnd slo = get_use(s, dlo, plo, 0), shi = get_use(s, dhi, phi, 0);
+        if (!(is_value(slo) && is_value(shi) && slo.pay == shi.pay)) continue;
+        if (!h.n_defs) { fail(s, CL_ST_INDEX_ERROR); continue; }
+        opnd d = get_def(s, h, i, 0);
+        if (!is_value(d)) { fail(s, CL_ST_ATTRIBUTE_ERROR); continue; }
+        if (d.pay < s.cap.V) s.redirect[d.pay] = slo.pay;
+        a_add(&T.f_red[f], 1u);
+        mine++;
+    }
+    const uint32_t changed = g.sum(mine);
+    g.sync();
+    if (!changed) return;
+    GFOR(g, i, T.n) if (i < T.n) {
+        const uint32_t f = T.fidx[i];
+        if (!T.f_red[f] || !tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        const cl_hdr h = T.hdr[i];
+        const unsigned u0 = use0(h);
+        for (unsigned k = 0; k < h.n_uses; k++) {
+            opnd u = get_slot(s, h, i, u0 + k);
+            if (is_value(u)) { const uint32_t fo = final_of(s, u.pay); if (fo != u.pay) { u.pay = fo; set_slot(s, h, i, u0 + k, u); } }
+            else if (kind_of(u.tag) == CL_K_MEMREF) {
+                cl_memref &m = s.mem[u.pay];
+                if (kind_of(m.base_tag) == CL_K_VALUE) m.base_pay = final_of(s, m.base_pay);
+                if (kind_of(m.ureg_tag) == CL_K_VALUE) m.ureg_pay = final_of(s, m.ureg_pay);
+            }
+        }
+        if (has_guard(h)) { opnd gd = get_slot(s, h, i, 0); if (is_value(gd)) { gd.pay = final_of(s, gd.pay); set_slot(s, h, i, 0, gd); } }
+    }
+    GFOR(g, b, T.nb) if (b < T.nb) {
+        const uint32_t f = T.bfun[b];
+        if (!T.f_red[f] || !tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        for (int k = 0; k < 2; k++)
+            if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE) T.blk[b].term_pay[k] = final_of(s, T.blk[b].term_pay[k]);
+    }
+    g.sync();
+}
+
+/* tag_cuda_objects (patterns.py:895-916)                                      */
+template <class G, class C> CLF void t_tag(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
+    PROF(g, s, PF_TAG);
+    GFOR(g, i, T.n) if (i < T.n) {
+        cl_hdr h = T.hdr[i];
+        if (h.op != CL_OP_BAR && h.op != CL_OP_WARPSYNC && h.op != CL_OP_SHFL) continue;
+        const uint32_t f = T.fidx[i];
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        unsigned kind = 0, use = 7;
+        if (h.op == CL_OP_BAR) {
+            if (has_mod(s, h, CL_MB_SYNC)) {
+                kind = 1;
+                for (unsigned k = 0; k < h.n_uses && k < 7; k++) if (is_imm(get_use(s, h, i, k))) use = k;
+            }
+        } else if (h.op == CL_OP_WARPSYNC) {
+            for (unsigned k = 0; k < h.n_uses && k < 7; k++) {
+                opnd u = get_use(s, h, i, k);
+                if (is_imm(u)) { if (s.imm[u.pay].bits == 0xFFFFFFFFull) { kind = 2; use = k; } break; }
+            }
+        } else
+            kind = 3;
+        if (kind) {
+            h.flags &= (uint8_t)~(CL_IF_OBJ_MASK | CL_IF_OBJUSE_MASK);
+            h.flags |= (uint8_t)(kind << CL_IF_OBJ_SHIFT | use << CL_IF_OBJUSE_SHIFT);
+            T.hdr[i].flags = h.flags;
+        }
+    }
+    g.sync();
+}
+
+/* ------------------------------------------------------- reciprocal chains */
+/* normalize_reciprocal (patterns.py:817-888), chains in parallel.
+ *   R_k(r): an F2I is reachable from record r in <= k def-use hops (_reaches_f2i :850)
+ *           -- backward propagation from the F2I records, three sweeps;
+ *   a chain (MUFU.RCP of an I2F, IADD/IADD3 with an immediate using it) is
+ *   accepted iff R_3(add);
+ *   its number (vids, iids, boundary index) is its rank by (mufu, add) position.
+ * The reference rewrites chain after chain on a rebuilt def-use graph; a later
+ * chain sees an earlier one only if its search walks over that chain's add or
+ * MUFU.  Functions where an accepted add reaches another accepted chain within
+ * three hops, adds with two reciprocal operands and every exception path of the
+ * reference are redone by the sequential kernel.                            */
+enum { RF_R0 = 1, RF_R1 = 2, RF_R2 = 4, RF_R3 = 8, RF_SEED = 16, RF_Q = 32, RF_MUFU = 128 };
+template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
+    PROF(g, s, PF_RECIP);
+    bool mine = false;
+    GFOR(g, i, T.n) if (i < T.n) { const cl_hdr h = T.hdr[i]; mine |= h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP); }
+    if (!g.any(mine)) return;
+    t_usecount(g, T, tg, s);
+    const uint32_t n = T.n;
+    uint32_t *valbits = T.redirect;
+    GFOR(g, v, T.vtot) if (v < T.vtot) valbits[v] = 0;
+    GFOR(g, f, T.nf) if (f < T.nf) T.f_aux[f] = 0;
+    if (g.rank == 0) T.n_chain = 0;
+    /* R_0 and the MUFU.RCP records fed by an I2F */
+    GFOR(g, i, n) if (i < n) {
+        const cl_hdr h = T.hdr[i];
+        uint8_t fl = h.op == CL_OP_F2I ? (uint8_t)(RF_R0 | RF_R1 | RF_R2 | RF_R3) : (uint8_t)0;
+        const uint32_t f = T.fidx[i];
+        if (h.op == CL_OP_MUFU && tf_ok(T, f) && has_mod(s, h, CL_MB_RCP) && h.n_uses) {
+            tv_view(s, T, tg, f);
+            const opnd src = get_use(s, h, i, 0);
+            if (is_value(src) && src.pay < s.cap.V) {
+                const uint32_t dp = s.defpos[src.pay];
+                if (dp != NONE32 && T.hdr[dp].op == CL_OP_I2F) {
+                    if (!h.n_defs || !is_value(get_def(s, h, i, 0))) tf_fail(T, f, CL_ST_REDO);   /* IndexError / AttributeError */
+                    else fl |= RF_MUFU;
+                }
+            }
+        }
+        T.flag[i] = fl;
+        T.keep[i] = 0; T.inscnt[i] = 0;
+    }
+    g.sync();
+    for (unsigned k = 1; k <= 3; k++) {
+        const uint8_t prev = (uint8_t)(1u << (k - 1)), cur = (uint8_t)(1u << k);
+        GFOR(g, i, n) if (i < n && (T.flag[i] & prev)) {
+            const uint32_t f = T.fidx[i];
+            if (!tf_ok(T, f)) continue;
+            tv_view(s, T, tg, f);
+            const cl_hdr h = T.hdr[i];
+            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.redirect[v] |= cur; });
+        }
+        g.sync();
+        GFOR(g, i, n) if (i < n && !(T.flag[i] & cur)) {
+            const uint32_t f = T.fidx[i];
+            if (!tf_ok(T, f)) continue;
+            tv_view(s, T, tg, f);
+            const cl_hdr h = T.hdr[i];
+            bool r = false;
+            for_value_defs(s, h, i, [&](uint32_t v) { r |= v < s.cap.V && (s.redirect[v] & cur); });
+            if (r) T.flag[i] |= (uint8_t)((0xFu << k) & 0xFu);        /* R_k implies R_k+1.. */
+        }
+        g.sync();
+    }
+    /* accepted chains */
+    GFOR(g, i, n) if (i < n) {
+        const cl_hdr h = T.hdr[i];
+        if (h.op != CL_OP_IADD && h.op != CL_OP_IADD3) continue;
+        const uint32_t f = T.fidx[i];
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        bool any_imm = false;
+        for (unsigned k = 0; k < h.n_uses; k++) any_imm |= is_imm(get_use(s, h, i, k));
+        if (!any_imm) continue;
+        unsigned hits = 0;
+        uint32_t mp = NONE32, rcp = 0;
+        for_value_operands(s, h, i, [&](uint32_t v) {
+            const uint32_t dp = v < s.cap.V ? s.defpos[v] : NONE32;
+            if (dp == NONE32 || !(T.flag[dp] & RF_MUFU)) return;
+            const cl_hdr hm = T.hdr[dp];
+            const opnd d0 = get_def(s, hm, dp, 0);
+            if (!is_value(d0) || d0.pay != v) return;
+            hits++; mp = dp; rcp = v;
+        });
+        if (!hits) continue;
+        if (hits > 1 || has_guard(h) || (h.flags & CL_IF_EXT)) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (!(T.flag[i] & RF_R3)) continue;
+        if (T.bidx[mp] != T.bidx[i] || !h.n_defs || !is_value(get_def(s, h, i, 0))) { tf_fail(T, f, CL_ST_REDO); continue; }
+        const uint32_t c = a_add(&T.n_chain, 1u);
+        if (c < C::X) {
+            TChain ch;
+            ch.add = (uint16_t)i; ch.mufu = (uint16_t)mp; ch.rcp = rcp; ch.addv = get_def(s, h, i, 0).pay; ch.f = (uint8_t)f; ch.ok = 1; ch.rank = 0;
+            T.chain[c] = ch;
+        } else
+            T.fail = 1;
+        T.flag[i] |= RF_SEED;
+        T.flag[mp] |= RF_SEED;
+    }
+    g.sync();
+    const uint32_t nc = T.n_chain;
+    if (nc == 0 || T.fail) return;
+    /* interference: does an accepted add reach another chain's add or MUFU within three hops? */
+    for (unsigned k = 1; k <= 3; k++) {
+        const uint32_t cur = 0x100u << k;
+        GFOR(g, i, n) if (i < n && (T.flag[i] & (RF_SEED | RF_Q))) {
+            const uint32_t f = T.fidx[i];
+            if (!tf_ok(T, f)) continue;
+            tv_view(s, T, tg, f);
+            const cl_hdr h = T.hdr[i];
+            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.redirect[v] |= cur; });
+        }
+        g.sync();
+        GFOR(g, i, n) if (i < n && !(T.flag[i] & RF_Q)) {
+            const uint32_t f = T.fidx[i];
+            if (!tf_ok(T, f)) continue;
+            tv_view(s, T, tg, f);
+            const cl_hdr h = T.hdr[i];
+            bool r = false;
+            for_value_defs(s, h, i, [&](uint32_t v) { r |= v < s.cap.V && (s.redirect[v] & cur); });
+            if (r) T.flag[i] |= RF_Q;
+        }
+        g.sync();
+    }
+    /* rank, ids, value table; vmap (usecnt[]) = add result -> its float view */
+    GFOR(g, v, T.vtot) if (v < T.vtot) T.usecnt[v] = NONE32;
+    g.sync();
+    GFOR(g, c, nc) if (c < nc) {
+        TChain &ch = T.chain[c];
+        const uint32_t f = ch.f;
+        if ((T.flag[ch.add] & RF_Q) != 0) { tf_fail(T, f, CL_ST_REDO); continue; }
+        uint32_t rank = 0;
+        const uint32_t key = (uint32_t)ch.mufu << 16 | ch.add;
+        for (uint32_t o = 0; o < nc; o++) {
+            const TChain &x = T.chain[o];
+            rank += x.f == f && ((uint32_t)x.mufu << 16 | x.add) < key;
+        }
+        ch.rank = (uint16_t)rank;
+        a_add(&T.f_aux[f], 1u);
+    }
+    g.sync();
+    GFOR(g, c, nc) if (c < nc) {
+        const TChain ch = T.chain[c];
+        const uint32_t f = ch.f;
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        const uint32_t vi = T.f_nvid[f] + 2u * ch.rank, vf = vi + 1u, iid = T.f_niid[f] + 2u * ch.rank;
+        if (vf >= s.cap.V) { tf_fail(T, f, CL_ST_REDO); continue; }
+        /* _insert_reciprocal_bitcasts :863-888 */
+        s.alive[vi] = 1; s.origin[vi] = CL_ORG_BITS | ch.rcp; s.def_iid[vi] = (int32_t)iid;
+        s.alive[vf] = 1; s.origin[vf] = CL_ORG_F | ch.addv; s.def_iid[vf] = (int32_t)(iid + 1u);
+        const cl_hdr ah = T.hdr[ch.add];
+        for (unsigned k = 0; k < ah.n_uses; k++) {
+            opnd x = get_use(s, ah, ch.add, k);
+            if (is_value(x) && x.pay == ch.rcp) { x.pay = vi; set_slot(s, ah, ch.add, use0(ah) + k, x); }
+        }
+        s.usecnt[ch.addv] = vf;
+        T.keep[ch.add] = 1; T.inscnt[ch.add] = 1;
+        t_event(s, T, tg, f, 1u << 28, CL_EV_BOUNDARY, ch.rank, ch.rcp, ah.iid);
+    }
+    g.sync();
+    /* every user of an add result (top-level uses only :878-883) reads the float view */
+    GFOR(g, i, n) if (i < n) {
+        const uint32_t f = T.fidx[i];
+        if (!T.f_aux[f] || !tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        const cl_hdr h = T.hdr[i];
+        for (unsigned k = 0; k < h.n_uses; k++) {
+            opnd x = get_use(s, h, i, k);
+            if (is_value(x) && x.pay < s.cap.V && s.usecnt[x.pay] != NONE32) { x.pay = s.usecnt[x.pay]; set_slot(s, h, i, use0(h) + k, x); }
+        }
+    }
+    g.sync();
+    /* materialise the bitcasts */
+    const uint32_t tot = t_scan(g, n, [&](uint32_t p) { return 1u + T.keep[p] + T.inscnt[p]; },
+                                [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
+    if (tot > C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
+    g.sync();
+    t_permute(g, T, n, [&](uint32_t p) { return (uint32_t)T.outpos[p] + T.keep[p]; });
+    GFOR(g, c, nc) if (c < nc) {
+        const TChain ch = T.chain[c];
+        const uint32_t f = ch.f;
+        if (!tf_ok(T, f)) continue;
+        tv_view(s, T, tg, f);
+        const uint32_t vi = T.f_nvid[f] + 2u * ch.rank, iid = T.f_niid[f] + 2u * ch.rank;
+        Rec r;
+        memset(&r, 0, sizeof r);
+        r.h.iid = iid; r.h.op = CL_OP_BITCAST; r.h.modset = CL_MS_F2I; r.h.n_defs = 1; r.h.n_uses = 1;
+        r.tag[0] = CL_K_VALUE; r.pay[0] = vi; r.tag[1] = CL_K_VALUE; r.pay[1] = ch.rcp;
+        st_rec(s, T.outpos[ch.add], r);
+        r.h.iid = iid + 1u; r.h.modset = CL_MS_I2F; r.pay[0] = vi + 1u; r.pay[1] = ch.addv;
+        st_rec(s, (uint32_t)T.outpos[ch.add] + 2u, r);
+    }
+    g.sync();
+    GFOR(g, f, T.nf) if (f < T.nf && T.f_aux[f] && tf_ok(T, f)) { T.f_nvid[f] += 2u * T.f_aux[f]; T.f_niid[f] += 2u * T.f_aux[f]; }
+    t_rebase_blocks(g, T, n, tot);
+    t_index(g, T);
+}
+
+/* ------------------------------------------------------------ load / store */
+/* capacities a function gets inside a tile (host planner and device agree)    */
+CLHD uint32_t tile_icap(uint32_t nrec) { return nrec + nrec / 2 + 8; }
+CLHD uint32_t tile_vcap(uint32_t nvid, uint32_t nrec) { return nvid + nrec + 8; }
+CLHD uint32_t tile_qcap(uint32_t nimm, uint32_t nrec) { return nimm + nrec / 2 + 8; }
+
+struct TileIO {                /* the part of KArgs the tile kernel needs (see culifter.cu) */
+    cl_corpus in;
+    cl_hdr *o_hdr; uint16_t *o_tag; uint32_t *o_pay; cl_imm *o_imm;
+    uint8_t *o_alive; int32_t *o_def_iid; uint32_t *o_origin;
+    cl_blk *o_blk; uint32_t *o_blk_start, *o_blk_cnt;
+    cl_event *o_ev;
+    void *o_func;              /* FuncOut[]                                       */
+    unsigned long long cap[4];
+    unsigned long long *cursor, *stats;
+    uint32_t *retry_list, *retry_count;
+};
+struct TFuncOut { cl_func f; uint32_t inst_start, n_inst, imm_start, n_imm, val_start, ev_start, n_ev, pad; };
+
+template <class C> CLD uint32_t t_func_of_value(const TileS<C> &T, uint32_t k) {
+    uint32_t f = 0;
+    while (f + 1 < T.nf && T.f_vbase[f + 1] <= k) f++;
+    return f;
+}
+template <class C> CLD uint32_t t_func_of_imm(const TileS<C> &T, uint32_t k) {
+    uint32_t f = 0;
+    while (f + 1 < T.nf && T.f_qbase[f + 1] <= k) f++;
+    return f;
+}
+
+template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, const TileIO &a, const TileDesc td) {
+    PROF(g, s, PF_LOAD);
+    const cl_corpus &in = a.in;
+    const uint32_t f0 = td.f0, nf = td.nf;
+    const uint32_t B0 = in.func_blk_off[f0], B1 = in.func_blk_off[f0 + nf];
+    const uint32_t I0 = in.blk_off[B0], I1 = in.blk_off[B1];
+    const uint32_t nb = B1 - B0, n = I1 - I0;
+    if (g.rank == 0) {
+        T.f0 = f0; T.nf = nf; T.nb = nb; T.n = n; T.I0 = I0; T.B0 = B0;
+        T.n_ev = 0; T.fail = 0; T.n_chain = 0; T.n_mt = 0; T.n_sel = 0;
+        T.f_b0[nf] = nb;
+    }
+    GFOR(g, f, nf) if (f < nf) {
+        const cl_func fn = in.func[f0 + f];
+        const uint32_t b0 = in.func_blk_off[f0 + f], b1 = in.func_blk_off[f0 + f + 1];
+        const uint32_t nrec = in.blk_off[b1] - in.blk_off[b0];
+        const uint32_t nimm = in.imm_off[f0 + f + 1] - in.imm_off[f0 + f];
+        T.f_arch[f] = fn.arch; T.f_nvid[f] = fn.next_vid; T.f_niid[f] = fn.next_iid; T.f_ntemp[f] = fn.next_temp_reg;
+        T.f_nimm[f] = nimm; T.f_stat[f] = 0; T.f_nev[f] = 0; T.f_odd[f] = 0; T.f_b0[f] = b0 - B0;
+        T.f_mem0[f] = in.mem_off[f0 + f]; T.f_nin[f] = nrec;
+        T.f_vcap[f] = tile_vcap(fn.next_vid, nrec); T.f_qcap[f] = tile_qcap(nimm, nrec);
+        T.f_active[f] = 0; T.f_gate[f] = 0; T.f_chg[f] = 0; T.f_red[f] = 0; T.f_aux[f] = 0;
+        for (uint32_t b = b0; b < b1; b++) T.bfun[b - B0] = (uint8_t)f;
+    }
+    GFOR(g, k, nf * 64) if (k < nf * 64) (&T.f_stats[0][0])[k] = 0;
+    GFOR(g, b, nb + 1) if (b <= nb) T.bo[b] = in.blk_off[B0 + b] - I0;
+    GFOR(g, b, nb) if (b < nb) T.blk[b] = in.blk[B0 + b];
+    {
+        const uint4 *src = (const uint4 *)(in.hdr + I0);
+        uint4 *dst = (uint4 *)T.hdr;
+        GFOR(g, i, n) if (i < n) dst[i] = src[i];
+        const uint4 *st = (const uint4 *)(in.tag + (size_t)I0 * 8);
+        uint4 *dt = (uint4 *)T.tag;
+        GFOR(g, i, n) if (i < n) dt[i] = st[i];
+        const uint4 *sp = (const uint4 *)(in.pay + (size_t)I0 * 8);
+        uint4 *dp = (uint4 *)T.pay;
+        GFOR(g, i, 2 * n) if (i < 2 * n) dp[i] = sp[i];
+    }
+    {
+        const uint32_t m0 = in.mem_off[f0], m1 = in.mem_off[f0 + nf];
+        GFOR(g, m, m1 - m0) if (m < m1 - m0) tg.mem[m0 + m] = in.mem[m0 + m];
+    }
+    g.sync();
+    if (g.rank == 0) {
+        uint32_t vb = 0, qb = 0;
+        for (uint32_t f = 0; f < nf; f++) { T.f_vbase[f] = vb; T.f_qbase[f] = qb; vb += T.f_vcap[f]; qb += T.f_qcap[f]; }
+        T.f_vbase[nf] = vb; T.f_qbase[nf] = qb; T.vtot = vb; T.qtot = qb;
+        if (vb > C::V || qb > C::Q || n > C::I || nb > C::B || nf > C::F) T.fail = 1;      /* planner bug: loud */
+    }
+    g.sync();
+    if (T.fail) return;
+    GFOR(g, k, T.vtot) if (k < T.vtot) {
+        const uint32_t f = t_func_of_value(T, k), v = k - T.f_vbase[f];
+        const uint32_t v0 = in.val_off[f0 + f];
+        const bool have = v < T.f_nvid[f];
+        T.alive[k] = have ? in.val_alive[v0 + v] : (uint8_t)0;
+        T.def_iid[k] = have ? in.val_def_iid[v0 + v] : -1;
+        T.origin[k] = CL_ORG_HOST;
+    }
+    GFOR(g, k, T.qtot) if (k < T.qtot) {
+        const uint32_t f = t_func_of_imm(T, k), q = k - T.f_qbase[f];
+        if (q < T.f_nimm[f]) T.imm[k] = in.imm[in.imm_off[f0 + f] + q];
+    }
+    g.sync();
+    t_index(g, T);
+}
+
+/* results of the live functions go to one atomically reserved place per tile (function
+ * order inside it); dead ones are queued for the general kernel                 */
+template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, const TileIO &a) {
+    PROF(g, s, PF_STORE);
+    const uint32_t nf = T.nf, f0 = T.f0;
+    if (g.rank == 0) {
+        uint32_t oi = 0, oq = 0, ov = 0, oe = 0;
+        const bool tile_ok = !T.fail;
+        for (uint32_t f = 0; f < nf; f++) {
+            const bool ok = tile_ok && T.f_stat[f] == 0;
+            if (!ok && T.f_stat[f] == 0) T.f_stat[f] = CL_ST_REDO;
+            T.f_oi[f] = oi; T.f_oq[f] = oq; T.f_ov[f] = ov; T.f_oe[f] = oe;
+            if (ok) { oi += T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]]; oq += T.f_nimm[f]; ov += T.f_nvid[f]; oe += T.f_nev[f]; }
+        }
+        const uint32_t ri = (uint32_t)a_add64(&a.cursor[0], oi), rq = (uint32_t)a_add64(&a.cursor[1], oq),
+                       rv = (uint32_t)a_add64(&a.cursor[2], ov), re = (uint32_t)a_add64(&a.cursor[3], oe);
+        const bool fits = (unsigned long long)ri + oi <= a.cap[0] && (unsigned long long)rq + oq <= a.cap[1] &&
+                          (unsigned long long)rv + ov <= a.cap[2] && (unsigned long long)re + oe <= a.cap[3];
+        unsigned long long n_in = 0;
+        for (uint32_t f = 0; f < nf; f++) {
+            T.f_oi[f] += ri; T.f_oq[f] += rq; T.f_ov[f] += rv; T.f_oe[f] += re;
+            T.f_aux[f] = 0;
+            if (T.f_stat[f] == 0) n_in += T.f_nin[f];
+        }
+        T.work = fits ? 1u : 0u;
+        a_add64(&a.stats[64], n_in); a_add64(&a.stats[65], oi); a_add64(&a.stats[66], oe);
+    }
+    g.sync();
+    const bool fits = T.work != 0;
+    TFuncOut *o_func = (TFuncOut *)a.o_func;
+    GFOR(g, f, nf) if (f < nf) {
+        if (T.f_stat[f] != 0) { a.retry_list[a_add(a.retry_count, 1u)] = f0 + f; continue; }
+        const uint32_t cnt = T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]];
+        TFuncOut o;
+        o.f.next_vid = T.f_nvid[f]; o.f.next_iid = T.f_niid[f]; o.f.next_temp_reg = T.f_ntemp[f];
+        o.f.arch = T.f_arch[f]; o.f.status = (uint8_t)(fits ? CL_ST_OK : CL_ST_CAPACITY); o.f.reserved = 0;
+        o.inst_start = T.f_oi[f]; o.n_inst = fits ? cnt : 0; o.imm_start = T.f_oq[f]; o.n_imm = fits ? T.f_nimm[f] : 0;
+        o.val_start = T.f_ov[f]; o.ev_start = T.f_oe[f]; o.n_ev = fits ? T.f_nev[f] : 0; o.pad = 0;
+        o_func[f0 + f] = o;
+    }
+    GFOR(g, b, T.nb) if (b < T.nb) {
+        const uint32_t f = T.bfun[b];
+        if (T.f_stat[f] != 0) continue;
+        a.o_blk[T.B0 + b] = T.blk[b];
+        a.o_blk_start[T.B0 + b] = fits ? T.f_oi[f] + (T.bo[b] - T.bo[T.f_b0[f]]) : 0u;
+        a.o_blk_cnt[T.B0 + b] = fits ? T.bo[b + 1] - T.bo[b] : 0u;
+    }
+    if (fits) {
+        GFOR(g, i, T.n) if (i < T.n) {
+            const uint32_t f = T.fidx[i];
+            if (T.f_stat[f] != 0) continue;
+            const size_t d = (size_t)T.f_oi[f] + (i - T.bo[T.f_b0[f]]);
+            *(uint4 *)(a.o_hdr + d) = *(const uint4 *)&T.hdr[i];
+            *(uint4 *)(a.o_tag + d * 8) = *(const uint4 *)&T.tag[(size_t)i * 8];
+            ((uint4 *)(a.o_pay + d * 8))[0] = ((const uint4 *)&T.pay[(size_t)i * 8])[0];
+            ((uint4 *)(a.o_pay + d * 8))[1] = ((const uint4 *)&T.pay[(size_t)i * 8])[1];
+        }
+        GFOR(g, k, T.qtot) if (k < T.qtot) {
+            const uint32_t f = t_func_of_imm(T, k), q = k - T.f_qbase[f];
+            if (T.f_stat[f] == 0 && q < T.f_nimm[f]) a.o_imm[T.f_oq[f] + q] = T.imm[k];
+        }
+        GFOR(g, k, T.vtot) if (k < T.vtot) {
+            const uint32_t f = t_func_of_value(T, k), v = k - T.f_vbase[f];
+            if (T.f_stat[f] == 0 && v < T.f_nvid[f]) {
+                const size_t d = (size_t)T.f_ov[f] + v;
+                a.o_alive[d] = T.alive[k]; a.o_def_iid[d] = T.def_iid[k]; a.o_origin[d] = T.origin[k];
+            }
+        }
+        const uint32_t nev = T.n_ev < C::E ? T.n_ev : C::E;
+        GFOR(g, e, nev) if (e < nev) {
+            const cl_event ev = tg.ev[e];
+            const uint32_t f = ev.func - f0;
+            if (T.f_stat[f] == 0) a.o_ev[T.f_oe[f] + a_add(&T.f_aux[f], 1u)] = ev;
+        }
+    }
+    GFOR(g, k, 64) if (k < 64) {
+        unsigned long long sum = 0;
+        for (uint32_t f = 0; f < nf; f++) if (T.f_stat[f] == 0) sum += T.f_stats[f][k];
+        if (sum) a_add64(&a.stats[k], sum);
+    }
+    g.sync();
+}
+
+/* the four calls of pipeline.py:165-169 on every function of one tile         */
+template <class G, class C> CLF void t_set_gate(const G &g, TileS<C> &T, int mode) {
+    /* 0: live sm52 functions, 1: live active functions, 2: live functions with redirects, 3: all live */
+    GFOR(g, f, T.nf) if (f < T.nf) {
+        bool on = tf_ok(T, f);
+        if (mode == 0) on = on && T.f_arch[f] == CL_ARCH_SM52;
+        else if (mode == 1) on = on && T.f_active[f];
+        else if (mode == 2) on = on && T.f_red[f] != 0;
+        T.f_gate[f] = on;
+    }
+    g.sync();
+}
+template <class G, class C> CLD bool t_any_gate(const G &g, TileS<C> &T) {
+    bool m = false;
+    GFOR(g, f, T.nf) if (f < T.nf) m |= T.f_gate[f] != 0;
+    return g.any(m);
+}
+
+template <class G, class C> CLF void t_run_tile(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, const TileIO &a,
+                                                const TileDesc td) {
+    t_load(g, T, tg, s, a, td);
+    if (!T.fail && (s.passes & CL_PASS_XMAD)) {
+        t_set_gate(g, T, 0);
+        if (t_any_gate(g, T)) {
+            t_apply_patterns(g, T, tg, s, 1, 0);
+            if (!T.fail) { t_set_gate(g, T, 0); t_dce(g, T, tg, s); }
+        }
+    }
+    if (!T.fail && (s.passes & CL_PASS_RECIPROCAL)) t_reciprocal(g, T, tg, s);
+    if (!T.fail && (s.passes & CL_PASS_AGGREGATE)) {
+        GFOR(g, f, T.nf) if (f < T.nf) T.f_active[f] = 1;
+        g.sync();
+        for (uint32_t round = 0; round < s.max_rounds && !T.fail; round++) {
+            t_set_gate(g, T, 1);
+            if (!t_any_gate(g, T)) break;
+            GFOR(g, f, T.nf) if (f < T.nf) T.f_chg[f] = 0;
+            g.sync();
+            t_apply_patterns(g, T, tg, s, 0, 2 + round);
+            if (T.fail) break;
+            t_set_gate(g, T, 1);
+            t_simplify(g, T, tg, s);
+            t_set_gate(g, T, 2);
+            if (t_any_gate(g, T)) t_dce(g, T, tg, s);
+            GFOR(g, f, T.nf) if (f < T.nf) T.f_active[f] = T.f_active[f] && (T.f_chg[f] + T.f_red[f]) != 0;
+            g.sync();
+        }
+        if (!T.fail) { t_set_gate(g, T, 3); t_dce(g, T, tg, s); }
+    }
+    if (!T.fail && (s.passes & CL_PASS_TAG)) t_tag(g, T, tg, s);
+    g.sync();
+    t_store(g, T, tg, s, a);
+}
+
+/* class tables of both pattern tables, once per CTA                           */
+template <class G, class C> CLF void t_setup(const G &g, TileS<C> &T, FS &s) {
+    if (g.rank == 0) {
+        for (unsigned table = 0; table < 2; table++) {
+            setup_classes(s, table);
+            T.n_cls[table] = s.n_cls;
+            for (unsigned c = 0; c < (unsigned)MAX_CLS; c++) { T.cls_op[table][c] = c < s.n_cls ? s.cls_op[c] : (uint16_t)0xFFFF; T.anchor_mask[table][c] = 0; }
+            for (unsigned pi = 0; pi < s.pb->n_patterns; pi++) {
+                const cl_pattern &p = s.pb->p[pi];
+                if (p.table != table) continue;
+                const int c = class_of(s, p.t[p.join_order[0]].op);
+                if (c >= 0) T.anchor_mask[table][c] |= 1u << pi;
+            }
+        }
+    }
+    g.sync();
+}
+
+} /* namespace clk */
