@@ -823,6 +823,7 @@ struct RW {
     cl_hdr h[3];
     unsigned n, pat;
     bool overflow;
+    uint32_t *stw;                 /* status word of the function that owns the match */
 };
 
 CLD opnd rw_value(RW &c, uint32_t origin) {               /* LiftedFunction.new_value */
@@ -875,7 +876,7 @@ CLD void rw_drop(RW &c, opnd o) {                       /* _drop_values :314-317
     if (!is_value(o)) return;
     if (st.ndrop < ST_DROP) st.drop_vid[st.ndrop++] = o.pay; else c.overflow = true;
 }
-CLD void rw_fail(RW &c, uint32_t code) { fail(*c.s, code); }
+CLD void rw_fail(RW &c, uint32_t code) { if (c.s->solo) { if (!*c.stw) *c.stw = code; } else a_cas0(c.stw, code); }
 
 /* _escapes (patterns.py:259-263) against the def-use snapshot of the block:
  * a value escapes iff it has more use sites than the group itself holds.    */
@@ -1257,7 +1258,7 @@ template <class G> CLF uint32_t ap_rewrite(const G &g, FS &s, uint32_t phase) {
             st.ok = st.rm = st.nins = st.retag = st.nv = st.nq = st.nupd = st.ndrop = 0;
             st.ni = 0;
             RW c;
-            c.s = &s; c.st = &st; c.n = m.n; c.pat = m.pat; c.overflow = false;
+            c.s = &s; c.st = &st; c.n = m.n; c.pat = m.pat; c.overflow = false; c.stw = s.st;
             for (unsigned t = 0; t < m.n; t++) { c.idx[t] = lo + m.pos[t]; c.h[t] = s.S.hdr[c.idx[t]]; }
             for (unsigned t = m.n; t < 3; t++) c.idx[t] = NONE32;
             st.ok = run_rewrite(c);

@@ -100,7 +100,8 @@ struct KArgs {
     const cl_sr_entry *sr; uint32_t n_sr;
     /* tile kernel (tile.cuh) */
     const TileDesc *tiles; uint32_t n_tiles; uint32_t *tile_counter;
-    uint8_t *tile_scratch; unsigned long long tile_scratch_per_cta;
+    const uint32_t *tile_flist;
+    uint8_t *tile_scratch; unsigned long long tile_scratch_per_cta;   /* per group */
 };
 
 /* ------------------------------------------------------ work memory layout */
@@ -578,52 +579,91 @@ CLHD TileIO tile_io(const KArgs &a) {
     TileIO io;
     io.in = a.in;
     io.o_hdr = a.o_hdr; io.o_tag = a.o_tag; io.o_pay = a.o_pay; io.o_imm = a.o_imm;
-    io.o_alive = a.o_alive; io.o_def_iid = a.o_def_iid; io.o_origin = a.o_origin;
+    io.o_alive = a.o_alive; io.o_def_iid = a.o_def_iid; io.o_origin = a.o_origin; io.o_mem = a.o_mem;
     io.o_blk = a.o_blk; io.o_blk_start = a.o_blk_start; io.o_blk_cnt = a.o_blk_cnt;
     io.o_ev = a.o_ev; io.o_func = a.o_func;
     for (int k = 0; k < 4; k++) io.cap[k] = a.cap[k];
     io.cursor = a.cursor; io.stats = a.stats;
     io.retry_list = a.retry_list; io.retry_count = a.retry_count;
+    io.flist = a.tile_flist;
     return io;
 }
-template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const KArgs &a, uint32_t cta) {
-    FS s;
-    unsigned long long prof[PF__N];
-    for (int k = 0; k < PF__N; k++) prof[k] = 0;
+/* persistent loop of one group (a warp or a CTA) over the tiles of its size class */
+template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const TileP &P, const KArgs &a, uint32_t group) {
     const unsigned long long t_begin = now();
-    memset(&s, 0, sizeof s);
-    s.pb = a.pb; s.ms = a.in.modsets; s.opflags = a.opflags; s.solo = g.size == 1;
-    s.passes = a.passes; s.max_rounds = a.max_rounds; s.emit_matches = 0;
-    s.S.hdr = T.hdr; s.S.tag = T.tag; s.S.pay = T.pay;
-    s.st = &T.f_stat[0]; s.n_ev = &T.n_ev;
-    s.prof = prof;
+    if (g.rank == 0) {
+        FS &s = T.fs;
+        memset(&s, 0, sizeof s);
+        T.P = &P;
+        s.pb = &P.pb; s.ms = a.in.modsets; s.opflags = a.opflags; s.solo = g.size == 1;
+        s.passes = a.passes; s.max_rounds = a.max_rounds; s.emit_matches = 0;
+        s.S.hdr = T.hdr; s.S.tag = T.tag; s.S.pay = T.pay;
+        s.usecnt = T.usecnt; s.defpos = T.defpos; s.redirect = T.redirect; s.origin = T.origin;
+        s.def_iid = T.def_iid; s.alive = T.alive; s.imm = T.imm;
+        s.cap.I = C::I; s.cap.V = C::V; s.cap.Q = C::Q; s.cap.B = C::B; s.cap.M = C::M; s.cap.S = C::S; s.cap.E = C::E;
+        s.st = &T.fail; s.n_ev = &T.n_ev;
+        s.prof = T.prof;
+        for (int k = 0; k < PF__N; k++) T.prof[k] = 0;
+    }
+    g.sync();
     TileG<C> tg;
-    tg.T = &T;
-    uint8_t *scr = a.tile_scratch + (size_t)cta * a.tile_scratch_per_cta;
+    uint8_t *scr = a.tile_scratch + (size_t)group * a.tile_scratch_per_cta;
     tg.stage = (Stage *)scr;
     tg.ev = (cl_event *)(scr + ((sizeof(Stage) * C::S + 255) & ~(size_t)255));
     tg.mem = a.o_mem;
     const TileIO io = tile_io(a);
-    t_setup(g, T, s);
     for (;;) {
         uint32_t w = 0;
         if (g.rank == 0) w = a_add(a.tile_counter, 1u);
         w = g.bcast0(w);
         if (w >= a.n_tiles) break;
-        t_run_tile(g, T, tg, s, io, a.tiles[w]);
+        t_run_tile(g, T, tg, io, a.tiles[w]);
         g.sync();
     }
     if (g.rank == 0) {
-        prof[PF_TOTAL] = now() - t_begin;
-        for (int k = 0; k < PF__N; k++) a_add64(&a.prof[k], prof[k]);
+        T.prof[PF_TOTAL] = now() - t_begin;
+        for (int k = 0; k < PF__N; k++) a_add64(&a.prof[k], T.prof[k]);
     }
 }
+CLHD size_t tile_p_bytes() { return (sizeof(TileP) + 255) & ~(size_t)255; }
 #if CL_CUDA
+/* a CTA is one group */
 template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, MINB) k_postssa_tile(KArgs a) {
     extern __shared__ uint4 dyn_smem[];
-    TileS<C> &T = *(TileS<C> *)dyn_smem;
+    TileP &P = *(TileP *)dyn_smem;
+    TileS<C> &T = *(TileS<C> *)((uint8_t *)dyn_smem + tile_p_bytes());
     Grp<NW> g; g.rank = threadIdx.x; g.size = NW * 32; g.red = T.red;
-    tile_loop(g, T, a, blockIdx.x);
+    t_setup(g, P, a.pb);
+    tile_loop(g, T, P, a, blockIdx.x);
+}
+/* every warp of the CTA is a group with its own tile */
+template <class C, int WARPS, int MINB> __global__ void __launch_bounds__(WARPS * 32, MINB) k_postssa_wtile(KArgs a) {
+    extern __shared__ uint4 dyn_smem[];
+    TileP &P = *(TileP *)dyn_smem;
+    const uint32_t w = threadIdx.x >> 5;
+    TileS<C> &T = *(TileS<C> *)((uint8_t *)dyn_smem + tile_p_bytes() + (size_t)w * ((sizeof(TileS<C>) + 15) & ~(size_t)15));
+    {
+        Grp<WARPS> gc; gc.rank = threadIdx.x; gc.size = WARPS * 32; gc.red = T.red;     /* warp 0's words: only rank 0 .. */
+        gc.red = ((TileS<C> *)((uint8_t *)dyn_smem + tile_p_bytes()))->red;
+        t_setup(gc, P, a.pb);
+    }
+    Grp<1> g; g.rank = threadIdx.x & 31u; g.size = 32; g.red = nullptr;
+    tile_loop(g, T, P, a, blockIdx.x * WARPS + w);
+}
+/* experiment: the same warp tiles with the tile state in L2-resident scratch instead of shared
+ * memory (more warps in flight, longer access latency)                                       */
+template <class C, int WARPS, int MINB> __global__ void __launch_bounds__(WARPS * 32, MINB) k_postssa_wtile_g(KArgs a) {
+    __shared__ TileP P;
+    __shared__ uint32_t red[40];
+    const uint32_t w = threadIdx.x >> 5, group = blockIdx.x * WARPS + w;
+    uint8_t *base = a.tile_scratch + (size_t)group * a.tile_scratch_per_cta;
+    TileS<C> &T = *(TileS<C> *)(base + tile_scratch_bytes<C>());
+    {
+        Grp<WARPS> gc; gc.rank = threadIdx.x; gc.size = WARPS * 32; gc.red = red;
+        t_setup(gc, P, a.pb);
+    }
+    Grp<1> g; g.rank = threadIdx.x & 31u; g.size = 32; g.red = nullptr;
+    tile_loop(g, T, P, a, group);
 }
 #endif
 
@@ -750,7 +790,7 @@ enum {
     B_O_HDR, B_O_TAG, B_O_PAY, B_O_IMM, B_O_ALIVE, B_O_DEF_IID, B_O_ORIGIN, B_O_EXT_TAG, B_O_EXT_PAY, B_O_MEM,
     B_O_BLK, B_O_BLK_START, B_O_BLK_CNT, B_O_EV, B_O_FUNC,
     B_LIST0, B_LIST1, B_LIST2, B_COUNTER0, B_COUNTER1, B_COUNTER2, B_SCRATCH0, B_SCRATCH1, B_SCRATCH2,
-    B_RETRY_LIST, B_RETRY_WORDS, B_TILES, B_TILE_COUNTER, B_TILE_SCRATCH, B_REST_LIST,
+    B_RETRY_LIST, B_RETRY_WORDS, B_TILES0, B_TILES1, B_TILE_COUNTER0, B_TILE_COUNTER1, B_TILE_SCRATCH0, B_TILE_SCRATCH1, B_TILE_FLIST, B_REST_LIST,
     B_D_OFF, B_D_SUMS, B_D_HDR, B_D_TAG, B_D_PAY, B_D_IMM, B_D_ALIVE, B_D_DEF_IID, B_D_ORIGIN, B_D_EV,
     B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B_SR_MAP, B__N
 };
@@ -778,13 +818,21 @@ struct cl_ctx {
     unsigned long long h_cursor[CUR__N] = { 0, 0, 0, 0 };
     Part part[3];              /* 0 = warp groups, 1 = CTA groups, 2 = one thread per function */
     uint32_t *d_retry_list = nullptr, *d_retry_count = nullptr, *d_retry_counter = nullptr;
-    /* tile kernel (tile.cuh): runs of consecutive small functions, one CTA per tile */
-    int tile_mode = 2;         /* 0 off, 1 small tiles (2 CTAs/SM), 2 large tiles (1 CTA/SM) */
-    int tile_warps = 16;
-    std::vector<TileDesc> tiles;
+    /* tile kernels (tile.cuh): small functions packed into shared-memory tiles, in two size classes:
+     * [0] warp tiles (one warp per tile), [1] CTA tiles                                        */
+    int tile_mode = 3;         /* bit 0: warp tiles, bit 1: CTA tiles; 0 = general kernels only */
+    int tile_warps = 16;       /* warps of a CTA-tile group */
+    int wtile_warps = 6;       /* warp tiles (= warps) per CTA */
+    int wtile_global = 0;      /* experiment: > 0 = warp tiles resident in global scratch, this many CTAs of 8 warps per SM */
+    struct TileClass {
+        std::vector<TileDesc> tiles;
+        TileDesc *d_tiles = nullptr; uint32_t *d_counter = nullptr; uint8_t *d_scratch = nullptr;
+        size_t scratch_per_group = 0; uint32_t grid = 0, groups = 0;
+    } tc[2];
+    std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest;          /* small functions that are not in a tile */
-    TileDesc *d_tiles = nullptr; uint32_t *d_tile_counter = nullptr, *d_rest = nullptr; uint8_t *d_tile_scratch = nullptr;
-    size_t tile_scratch_per_cta = 0; uint32_t tile_grid = 0, n_tile_funcs = 0, h_retry = 0; bool used_tiles = false;
+    uint32_t *d_tile_flist = nullptr, *d_rest = nullptr;
+    uint32_t n_tile_funcs = 0, h_retry = 0; bool used_tiles = false;
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
     int cta_warps = 8;         /* warps per CTA of the CTA-group kernel (8, 16 or 32) */        /* warps per CTA of the phase-synchronous warp kernel (0 = free-running kernel) */
@@ -836,8 +884,10 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_THREAD_MAX")) c->thread_max = CL_CUDA ? (uint32_t)atoi(e) : 0;
     if (const char *e = getenv("CL_WARP_SYNC")) { const int v = atoi(e); c->warp_sync = (v == 0 || v == 8 || v == 16 || v == 32 || v == 33) ? v : 32; }
     if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
-    if (const char *e = getenv("CL_TILE")) c->tile_mode = std::min(2, std::max(0, atoi(e)));
+    if (const char *e = getenv("CL_TILE")) c->tile_mode = atoi(e) & 3;
     if (const char *e = getenv("CL_TILE_WARPS")) { const int v = atoi(e); c->tile_warps = (v == 8 || v == 32) ? v : 16; }
+    if (const char *e = getenv("CL_WTILE_GLOBAL")) c->wtile_global = std::min(8, std::max(0, atoi(e)));
+    if (const char *e = getenv("CL_WTILE_WARPS")) c->wtile_warps = std::min(6, std::max(1, atoi(e)));
     if (const char *e = getenv("CL_THREAD_CTAS")) c->thread_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("CL_WARP_CTAS")) c->warp_ctas = std::min(CL_WARP_CTAS_PER_SM, std::max(1, atoi(e)));
     if (const char *e = getenv("CL_CTA_CTAS")) c->cta_ctas = std::min(CL_CTA_CTAS_PER_SM, std::max(1, atoi(e)));
@@ -1002,29 +1052,38 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         if (dget(c, CNT_ID[k], &p.d_counter, 1)) return -1;
         if (dget(c, SCR_ID[k], &p.d_scratch, p.scratch_per_group * p.n_groups)) return -1;
     }
-    /* tiles: maximal runs of consecutive small functions whose capacities fit one tile */
-    c->tiles.clear(); c->rest.clear(); c->n_tile_funcs = 0;
-    if (c->tile_mode) {
-        const bool large = c->tile_mode == 2;
-        const uint32_t cI = large ? TileCfgL::I : TileCfgS::I, cV = large ? TileCfgL::V : TileCfgS::V,
-                       cQ = large ? TileCfgL::Q : TileCfgS::Q, cF = large ? TileCfgL::F : TileCfgS::F,
-                       cB = large ? TileCfgL::B : TileCfgS::B;
-        TileDesc cur = { 0, 0 };
-        uint32_t sI = 0, sV = 0, sQ = 0, sB = 0;
-        auto flush = [&]() { if (cur.nf) { c->tiles.push_back(cur); c->n_tile_funcs += cur.nf; } cur.nf = 0; sI = sV = sQ = sB = 0; };
+    /* tiles: small functions without overflow slots, by size class, packed in size order */
+    for (auto &t : c->tc) t.tiles.clear();
+    c->tile_flist.clear(); c->rest.clear(); c->n_tile_funcs = 0;
+    {
+        struct Need { uint32_t I, V, Q, B, f; };
+        std::vector<Need> cls[2];
         for (uint32_t f = 0; f < F; f++) {
             const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
             const uint32_t n = in->blk_off[b1] - in->blk_off[b0], nb = b1 - b0;
+            if (!(n <= c->small_max && n > c->thread_max)) continue;
             const uint32_t nimm = in->imm_off[f + 1] - in->imm_off[f];
-            const uint32_t iI = tile_icap(n), iV = tile_vcap(in->func[f].next_vid, n), iQ = tile_qcap(nimm, n);
-            const bool small = n <= c->small_max && n > c->thread_max;
-            const bool fits = small && in->ext_off[f + 1] == in->ext_off[f] && 2 * iI <= cI + 16 && iV <= cV && iQ <= cQ && nb <= cB && nb > 0;
-            if (!fits) { flush(); if (small) c->rest.push_back(f); continue; }
-            if (cur.nf && (sI + iI > cI || sV + iV > cV || sQ + iQ > cQ || sB + nb > cB || cur.nf >= cF)) flush();
-            if (!cur.nf) cur.f0 = f;
-            cur.nf++; sI += iI; sV += iV; sQ += iQ; sB += nb;
+            const Need nd = { tile_icap(n), tile_vcap(in->func[f].next_vid, n), tile_qcap(nimm, n), nb, f };
+            const bool plain = in->ext_off[f + 1] == in->ext_off[f] && nb > 0;
+            if (plain && (c->tile_mode & 1) && nd.I <= TileCfgW::I && nd.V <= TileCfgW::V && nd.Q <= TileCfgW::Q && nd.B <= TileCfgW::B) cls[0].push_back(nd);
+            else if (plain && (c->tile_mode & 2) && nd.I <= TileCfgL::I && nd.V <= TileCfgL::V && nd.Q <= TileCfgL::Q && nd.B <= TileCfgL::B) cls[1].push_back(nd);
+            else c->rest.push_back(f);
         }
-        flush();
+        const uint32_t capI[2] = { TileCfgW::I, TileCfgL::I }, capV[2] = { TileCfgW::V, TileCfgL::V }, capQ[2] = { TileCfgW::Q, TileCfgL::Q },
+                       capB[2] = { TileCfgW::B, TileCfgL::B }, capF[2] = { TileCfgW::F, TileCfgL::F };
+        for (int k = 0; k < 2; k++) {
+            std::stable_sort(cls[k].begin(), cls[k].end(), [](const Need &x, const Need &y) { return x.I > y.I; });    /* long poles first */
+            TileDesc cur = { (uint32_t)c->tile_flist.size(), 0 };
+            uint32_t sI = 0, sV = 0, sQ = 0, sB = 0;
+            auto flush = [&]() { if (cur.nf) c->tc[k].tiles.push_back(cur); cur.first = (uint32_t)c->tile_flist.size(); cur.nf = 0; sI = sV = sQ = sB = 0; };
+            for (const Need &nd : cls[k]) {
+                if (cur.nf && (sI + nd.I > capI[k] || sV + nd.V > capV[k] || sQ + nd.Q > capQ[k] || sB + nd.B > capB[k] || cur.nf >= capF[k])) flush();
+                c->tile_flist.push_back(nd.f);
+                cur.nf++; sI += nd.I; sV += nd.V; sQ += nd.Q; sB += nd.B;
+            }
+            flush();
+        }
+        c->n_tile_funcs = (uint32_t)c->tile_flist.size();
     }
     {
         uint32_t *words = nullptr;
@@ -1032,20 +1091,36 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         if (dget(c, B_RETRY_WORDS, &words, 4)) return -1;
         c->d_retry_count = words; c->d_retry_counter = words + 1;
     }
-    if (!c->tiles.empty()) {
+    if (c->n_tile_funcs) {
+        static const int T_ID[2] = { B_TILES0, B_TILES1 }, C_ID[2] = { B_TILE_COUNTER0, B_TILE_COUNTER1 }, S_ID[2] = { B_TILE_SCRATCH0, B_TILE_SCRATCH1 };
+        for (int k = 0; k < 2; k++) {
+            cl_ctx::TileClass &t = c->tc[k];
+            if (t.tiles.empty()) continue;
 #if CL_CUDA
-        const bool large = c->tile_mode == 2;
-        c->tile_scratch_per_cta = large ? tile_scratch_bytes<TileCfgL>() : tile_scratch_bytes<TileCfgS>();
-        c->tile_grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * (large ? 1 : 2), c->tiles.size());
+            if (k == 0 && c->wtile_global) {
+                t.scratch_per_group = tile_scratch_bytes<TileCfgW>() + ((sizeof(TileS<TileCfgW>) + 255) & ~(size_t)255);
+                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->wtile_global, (t.tiles.size() + 7) / 8);
+                t.groups = t.grid * 8;
+            } else if (k == 0) {
+                t.scratch_per_group = tile_scratch_bytes<TileCfgW>();
+                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, (t.tiles.size() + c->wtile_warps - 1) / c->wtile_warps);
+                t.groups = t.grid * c->wtile_warps;
+            } else {
+                t.scratch_per_group = tile_scratch_bytes<TileCfgL>();
+                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, t.tiles.size());
+                t.groups = t.grid;
+            }
 #else
-        c->tile_scratch_per_cta = tile_scratch_bytes<TileCfgL>();
-        c->tile_grid = 1;
+            t.scratch_per_group = k == 0 ? tile_scratch_bytes<TileCfgW>() : tile_scratch_bytes<TileCfgL>();
+            t.grid = t.groups = 1;
 #endif
-        if (dput(c, B_TILES, &c->d_tiles, c->tiles.data(), c->tiles.size())) return -1;
-        if (dget(c, B_TILE_COUNTER, &c->d_tile_counter, 1)) return -1;
-        if (dget(c, B_TILE_SCRATCH, &c->d_tile_scratch, c->tile_scratch_per_cta * c->tile_grid)) return -1;
-        if (dput(c, B_REST_LIST, &c->d_rest, c->rest.data(), c->rest.size())) return -1;
+            if (dput(c, T_ID[k], &t.d_tiles, t.tiles.data(), t.tiles.size())) return -1;
+            if (dget(c, C_ID[k], &t.d_counter, 1)) return -1;
+            if (dget(c, S_ID[k], &t.d_scratch, t.scratch_per_group * t.groups)) return -1;
+        }
+        if (dput(c, B_TILE_FLIST, &c->d_tile_flist, c->tile_flist.data(), c->tile_flist.size())) return -1;
     }
+    if (dput(c, B_REST_LIST, &c->d_rest, c->rest.data(), c->rest.size())) return -1;
 
     /* result buffers (worst-case growth, G3/G4) */
     KArgs &k = c->k;
@@ -1122,31 +1197,67 @@ static int launch_part(cl_ctx *c, int which, KArgs k, int mode = 0, bool side = 
 }
 
 #if CL_CUDA
-template <class C, int NW, int MINB> static int launch_tile_kernel(cl_ctx *c, const KArgs &k) {
-    const size_t smem = sizeof(TileS<C>);
+template <class C, int NW, int MINB> static int launch_tile_kernel(cl_ctx *c, const KArgs &k, uint32_t grid, cudaStream_t st) {
+    const size_t smem = tile_p_bytes() + sizeof(TileS<C>);
     CUDA_OK(cudaFuncSetAttribute(k_postssa_tile<C, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_postssa_tile<C, NW, MINB><<<c->tile_grid, NW * 32, smem, c->stream>>>(k);
+    k_postssa_tile<C, NW, MINB><<<grid, NW * 32, smem, st>>>(k);
     CUDA_OK(cudaGetLastError());
+    (void)c;
+    return 0;
+}
+template <class C, int WARPS> static int launch_wtile_kernel(cl_ctx *c, const KArgs &k, uint32_t grid, cudaStream_t st) {
+    const size_t smem = tile_p_bytes() + WARPS * ((sizeof(TileS<C>) + 15) & ~(size_t)15);
+    CUDA_OK(cudaFuncSetAttribute(k_postssa_wtile<C, WARPS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_postssa_wtile<C, WARPS, 1><<<grid, WARPS * 32, smem, st>>>(k);
+    CUDA_OK(cudaGetLastError());
+    (void)c;
     return 0;
 }
 #endif
-static int launch_tiles(cl_ctx *c, KArgs k) {
-    k.tiles = c->d_tiles; k.n_tiles = (uint32_t)c->tiles.size(); k.tile_counter = c->d_tile_counter;
-    k.tile_scratch = c->d_tile_scratch; k.tile_scratch_per_cta = c->tile_scratch_per_cta;
+/* class 0 (warp tiles) on the main stream, class 1 (CTA tiles) on the side stream */
+static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
+    cl_ctx::TileClass &t = c->tc[cls];
+    if (t.tiles.empty()) return 0;
+    k.tiles = t.d_tiles; k.n_tiles = (uint32_t)t.tiles.size(); k.tile_counter = t.d_counter;
+    k.tile_scratch = t.d_scratch; k.tile_scratch_per_cta = t.scratch_per_group; k.tile_flist = c->d_tile_flist;
     k.retry_list = c->d_retry_list; k.retry_count = c->d_retry_count;
-    if (dzero(k.tile_counter, sizeof(uint32_t), c->stream)) return -1;
 #if CL_CUDA
-    if (c->tile_mode == 2) {
-        if (c->tile_warps == 32) return launch_tile_kernel<TileCfgL, 32, 1>(c, k);
-        if (c->tile_warps == 8) return launch_tile_kernel<TileCfgL, 8, 1>(c, k);
-        return launch_tile_kernel<TileCfgL, 16, 1>(c, k);
+    cudaStream_t st = cls == 0 ? c->stream : c->stream2;
+    if (dzero(k.tile_counter, sizeof(uint32_t), st)) return -1;
+    if (cls == 0 && c->wtile_global) {
+        switch (c->wtile_global) {
+        case 1: k_postssa_wtile_g<TileCfgW, 8, 1><<<t.grid, 256, 0, st>>>(k); break;
+        case 2: k_postssa_wtile_g<TileCfgW, 8, 2><<<t.grid, 256, 0, st>>>(k); break;
+        case 3: k_postssa_wtile_g<TileCfgW, 8, 3><<<t.grid, 256, 0, st>>>(k); break;
+        case 4: k_postssa_wtile_g<TileCfgW, 8, 4><<<t.grid, 256, 0, st>>>(k); break;
+        case 6: k_postssa_wtile_g<TileCfgW, 8, 6><<<t.grid, 256, 0, st>>>(k); break;
+        default: k_postssa_wtile_g<TileCfgW, 8, 8><<<t.grid, 256, 0, st>>>(k); break;
+        }
+        CUDA_OK(cudaGetLastError());
+        return 0;
     }
-    if (c->tile_warps == 8) return launch_tile_kernel<TileCfgS, 8, 2>(c, k);
-    return launch_tile_kernel<TileCfgS, 16, 2>(c, k);
+    if (cls == 0) {
+        switch (c->wtile_warps) {
+        case 1: return launch_wtile_kernel<TileCfgW, 1>(c, k, t.grid, st);
+        case 2: return launch_wtile_kernel<TileCfgW, 2>(c, k, t.grid, st);
+        case 3: return launch_wtile_kernel<TileCfgW, 3>(c, k, t.grid, st);
+        case 4: return launch_wtile_kernel<TileCfgW, 4>(c, k, t.grid, st);
+        case 5: return launch_wtile_kernel<TileCfgW, 5>(c, k, t.grid, st);
+        case 6: return launch_wtile_kernel<TileCfgW, 6>(c, k, t.grid, st);
+        case 7: return launch_wtile_kernel<TileCfgW, 7>(c, k, t.grid, st);
+        default: return launch_wtile_kernel<TileCfgW, 8>(c, k, t.grid, st);
+        }
+    }
+    if (c->tile_warps == 32) return launch_tile_kernel<TileCfgL, 32, 1>(c, k, t.grid, st);
+    if (c->tile_warps == 8) return launch_tile_kernel<TileCfgL, 8, 1>(c, k, t.grid, st);
+    return launch_tile_kernel<TileCfgL, 16, 1>(c, k, t.grid, st);
 #else
-    static TileS<TileCfgL> T;
-    Grp<0> g; g.rank = 0; g.size = 1; g.red = T.red;
-    tile_loop(g, T, k, 0);
+    if (dzero(k.tile_counter, sizeof(uint32_t), c->stream)) return -1;
+    static TileP P;
+    Grp<0> g; g.rank = 0; g.size = 1; g.red = nullptr;
+    t_setup(g, P, k.pb);
+    if (cls == 0) { static TileS<TileCfgW> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    else { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
     return 0;
 #endif
 }
@@ -1163,7 +1274,7 @@ static int run(cl_ctx *c, KArgs k) {
     /* the tile kernel takes the production run of the post-SSA stage; match lists
      * (emit_matches / MATCH_ONLY), the raw stage and tables with a pattern that has
      * no join plan go through the general kernels                                  */
-    bool use_tiles = !c->tiles.empty() && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
+    bool use_tiles = c->n_tile_funcs && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
     for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_tiles = use_tiles && c->h_pb.p[pi].join_ok;
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev0, c->stream));
@@ -1173,9 +1284,14 @@ static int run(cl_ctx *c, KArgs k) {
 #endif
     if (launch_part(c, 1, k, 0, true)) return -1;
     if (use_tiles) {
-        if (launch_tiles(c, k)) return -1;
+        if (launch_tiles(c, k, 1)) return -1;    /* CTA tiles: side stream, after the large functions */
+        if (launch_tiles(c, k, 0)) return -1;    /* warp tiles */
         if (launch_part(c, 0, k, 2)) return -1;  /* small functions outside the tiles */
-        if (launch_part(c, 0, k, 1)) return -1;  /* what the tile kernel handed back */
+#if CL_CUDA
+        CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
+        CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+#endif
+        if (launch_part(c, 0, k, 1)) return -1;  /* what the tile kernels handed back */
     } else {
         if (launch_part(c, 2, k)) return -1;
         if (launch_part(c, 0, k)) return -1;
@@ -1329,7 +1445,7 @@ extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
 /* debugging aid: how the last run was partitioned: {tiles, functions in tiles, functions the tile kernel
  * handed back to the general kernel, small functions outside tiles, tile kernel used}            */
 extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
-    out[0] = c->tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles;
+    out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles;
     return 0;
 }
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }

@@ -12,9 +12,13 @@
  *   pack simplification, dead-pseudo fixpoint, reciprocal chains, tagging
  *
  * HBM sees one coalesced read of the tile and one write of the result; every
- * intermediate round lives in shared memory.  The per-match leaf code
- * (match_inst, check_tuple, the nine rewrite planners) is core.cuh's: a thread
- * points its FS at the function that owns the item it works on ("view").
+ * intermediate round lives in shared memory.
+ *
+ * Ids: value, immediate and memref indices are function-local in the corpus.
+ * On load they are rebased into tile-wide index spaces (each function gets a
+ * slice with room to grow), so ONE function state (`FS`, in shared memory)
+ * describes the whole tile and the per-match leaf code of core.cuh (the nine
+ * rewrite planners) runs on it unchanged; the store rebases them back.
  *
  * Exactness: the reference is sequential over blocks and chains.  Everything
  * here is evaluated on the snapshot taken at the start of a pass, which equals
@@ -30,14 +34,32 @@ namespace clk {
 
 static constexpr uint32_t CL_ST_REDO = 100;     /* internal: redo this function on the general kernel */
 
-struct TileDesc { uint32_t f0, nf; };
+struct TileDesc { uint32_t first, nf; };      /* functions flist[first .. first + nf) */
 
 struct TMatch { uint16_t pos[3]; uint8_t pat, n; };
 struct TChain { uint16_t add, mufu; uint32_t rcp, addv; uint8_t f, ok; uint16_t rank; };
+/* unification of one pattern as equality constraints between operand slots:
+ * every later occurrence of a variable must carry the key of its first one
+ * (Bindings.bind, patterns.py:93-97), same for the "mod:<var>" bindings (:163-166) */
+struct TPat {
+    uint8_t n_pairs, n_mpairs, pad[2];
+    uint8_t pair[28][4];       /* tA, kA, tB, kB: slots in defs, aux, uses order    */
+    uint8_t mpair[4][4];       /* tA, groupA, tB, groupB                            */
+};
 
 /* capacities of one tile (compile time: the tile lives in shared memory) */
 struct TileCfgL { static constexpr uint32_t I = 1024, V = 1792, Q = 320, F = 32, B = 96, M = 1024, S = 512, X = 256, E = 512; };
-struct TileCfgS { static constexpr uint32_t I = 640, V = 1152, Q = 208, F = 24, B = 64, M = 640, S = 320, X = 160, E = 320; };
+struct TileCfgS { static constexpr uint32_t I = 576, V = 1024, Q = 192, F = 24, B = 64, M = 512, S = 288, X = 128, E = 256; };
+struct TileCfgW { static constexpr uint32_t I = 192, V = 352, Q = 64, F = 3, B = 16, M = 192, S = 96, X = 32, E = 64; };   /* one warp */
+
+/* the pattern table and what t_setup derives from it: shared by the tiles of a CTA */
+struct TileP {
+    cl_pattern_blob pb;
+    TPat pat[CL_MAX_PATTERNS];
+    uint16_t cls_op[2][MAX_CLS];
+    uint32_t n_cls[2], anchor_mask[2][MAX_CLS];
+    uint8_t op_cls[2][CL_OP__COUNT];      /* opcode id -> seed class of the table, 0xFF none */
+};
 
 template <class C> struct TileS {
     alignas(16) cl_hdr hdr[C::I];
@@ -59,58 +81,69 @@ template <class C> struct TileS {
     cl_blk blk[C::B];
     uint32_t ccnt[C::B][MAX_CLS];
     uint8_t bfun[C::B];
-    /* functions */
-    uint32_t f_vbase[C::F + 1], f_qbase[C::F + 1], f_vcap[C::F], f_qcap[C::F], f_mem0[C::F];
+    /* functions: slices of the tile-wide value / immediate / memref index spaces */
+    uint32_t f_vbase[C::F + 1], f_qbase[C::F + 1], f_mbase[C::F + 1];
     uint32_t f_nvid[C::F], f_niid[C::F], f_nimm[C::F], f_ntemp[C::F], f_stat[C::F], f_nev[C::F];
-    uint32_t f_b0[C::F + 1], f_chg[C::F], f_red[C::F], f_first[C::F], f_aux[C::F], f_nin[C::F];
+    uint32_t f_b0[C::F + 1], f_i0[C::F + 1], f_gf[C::F], f_gb0[C::F], f_gi0[C::F];   /* tile block / record ranges; global function, block, record */
+    uint32_t f_chg[C::F], f_red[C::F], f_first[C::F], f_aux[C::F], f_nin[C::F];
     uint32_t f_oi[C::F], f_oq[C::F], f_ov[C::F], f_oe[C::F];
     uint32_t f_stats[C::F][64];
     uint8_t f_arch[C::F], f_active[C::F], f_odd[C::F], f_gate[C::F];
-    /* class tables of the two pattern tables */
-    uint16_t cls_op[2][MAX_CLS];
-    uint32_t n_cls[2], anchor_mask[2][MAX_CLS];
-    /* tile scalars */
-    uint32_t n, nb, nf, f0, I0, B0, n_mt, n_sel, n_ev, fail, vtot, qtot, n_chain, work;
+    /* the one function state of the tile + tile scalars */
+    const struct TileP *P;
+    FS fs;
+    unsigned long long prof[PF__N];
+    uint32_t n, nb, nf, n_mt, n_sel, n_ev, fail, vtot, qtot, n_chain, work;
     uint32_t red[40];
 };
 
 template <class C> struct TileG {      /* what lives outside shared memory */
-    TileS<C> *T;
     Stage *stage;             /* [C::S] staged rewrites (L2-resident scratch)   */
     cl_event *ev;             /* [C::E]                                          */
-    cl_memref *mem;           /* o_mem: memrefs of the corpus, mutable copy      */
+    cl_memref *mem;           /* memrefs of the tile: mutable copy in the output  */
 };
 
-/* ------------------------------------------------------------------ views */
-template <class C> CLD void tv_view(FS &s, TileS<C> &T, const TileG<C> &tg, uint32_t f) {
-    const uint32_t vb = T.f_vbase[f], qb = T.f_qbase[f];
-    s.usecnt = T.usecnt + vb; s.defpos = T.defpos + vb; s.redirect = T.redirect + vb; s.origin = T.origin + vb;
-    s.def_iid = T.def_iid + vb; s.alive = T.alive + vb;
-    s.imm = T.imm + qb;
-    s.cap.V = T.f_vcap[f]; s.cap.Q = T.f_qcap[f];
-    s.mem = tg.mem + T.f_mem0[f];
-    s.st = &T.f_stat[f];
-    s.f = T.f0 + f; s.arch = T.f_arch[f];
-}
 template <class C> CLD bool tf_ok(const TileS<C> &T, uint32_t f) { return *(volatile const uint32_t *)&T.f_stat[f] == 0; }
 template <class C> CLD void tf_fail(TileS<C> &T, uint32_t f, uint32_t code) { a_cas0(&T.f_stat[f], code); }
 
-template <class C> CLD void t_event(FS &s, TileS<C> &T, const TileG<C> &tg, uint32_t f, uint32_t seq, uint32_t kind,
+template <class C> CLD void t_event(TileS<C> &T, const TileG<C> &tg, uint32_t f, uint32_t seq, uint32_t kind,
                                     uint32_t idx, uint32_t a, uint32_t b) {
     const uint32_t k = a_add(&T.n_ev, 1u);
     if (k < C::E) {
-        cl_event e; e.func = T.f0 + f; e.seq = seq; e.kind = kind; e.idx = idx; e.a = a; e.b = b; e.c = 0; e.d = 0;
+        cl_event e; e.func = f;      /* tile-local: t_store writes the global id */ e.seq = seq; e.kind = kind; e.idx = idx; e.a = a; e.b = b; e.c = 0; e.d = 0;
         tg.ev[k] = e;
         a_add(&T.f_nev[f], 1u);
     } else
         T.fail = 1;
-    (void)s;
 }
 
 template <class C> CLD int t_class_of(const TileS<C> &T, unsigned table, uint16_t op) {
-    const uint32_t n = T.n_cls[table];
-    for (uint32_t c = 0; c < n; c++) if (T.cls_op[table][c] == op) return (int)c;
-    return -1;
+    if (op >= CL_OP__COUNT) return -1;            /* dynamic opcodes never head a template */
+    const uint8_t c = T.P->op_cls[table][op];
+    return c == 0xFF ? -1 : (int)c;
+}
+/* operand slot k (guard included) of a record without overflow slots           */
+template <class C> CLD opnd t_slot(const TileS<C> &T, uint32_t i, unsigned k) {
+    opnd o; o.tag = T.tag[(size_t)i * 8 + k]; o.pay = T.pay[(size_t)i * 8 + k];
+    return o;
+}
+/* value_operands (ssa.py:599-610) / all_defs of a record without overflow slots */
+template <class C, class F> CLD void t_value_operands(const TileS<C> &T, const TileG<C> &tg, const cl_hdr &h, uint32_t i, F fn) {
+    if (has_guard(h)) { const opnd g = t_slot(T, i, 0); if (is_value(g)) fn(g.pay); }
+    const unsigned u0 = use0(h);
+    for (unsigned k = 0; k < h.n_uses; k++) {
+        const opnd u = t_slot(T, i, u0 + k);
+        if (is_value(u)) fn(u.pay);
+        else if (kind_of(u.tag) == CL_K_MEMREF) {
+            const cl_memref &m = tg.mem[u.pay];
+            if (kind_of(m.base_tag) == CL_K_VALUE) fn(m.base_pay);
+            if (kind_of(m.ureg_tag) == CL_K_VALUE) fn(m.ureg_pay);
+        }
+    }
+}
+template <class C, class F> CLD void t_value_defs(const TileS<C> &T, const cl_hdr &h, uint32_t i, F fn) {
+    const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
+    for (unsigned k = 0; k < nd; k++) { const opnd d = t_slot(T, i, d0 + k); if (is_value(d)) fn(d.pay); }
 }
 
 /* block / function index of every record from the block offsets */
@@ -165,45 +198,150 @@ template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T,
 #endif
 }
 
+/* running exclusive scan over items [0, n) in order; returns the total        */
+template <class G, class FIN, class FOUT> CLD uint32_t t_scan(const G &g, uint32_t n, FIN in, FOUT out) {
+    uint32_t run = 0;
+    GFOR(g, j, n) {
+        const uint32_t x = j < n ? in(j) : 0u;
+        uint32_t t;
+        const uint32_t o = g.exscan(x, t);
+        if (j < n) out(j, run + o);
+        run += t;
+    }
+    return run;
+}
+
+/* new block offsets after a permutation described by outpos[] (position of the
+ * first output slot of every old record) and the new length                   */
+template <class G, class C> CLD void t_rebase_blocks(const G &g, TileS<C> &T, uint32_t n_old, uint32_t n_new) {
+    GFOR(g, b, T.nb + 1) if (b <= T.nb) { const uint32_t old = T.bo[b]; T.bo2[b] = old < n_old ? (uint32_t)T.outpos[old] : n_new; }
+    g.sync();
+    GFOR(g, b, T.nb + 1) if (b <= T.nb) T.bo[b] = T.bo2[b];
+    if (g.rank == 0) T.n = n_new;
+    g.sync();
+}
+
 /* ------------------------------------------------------------------ def-use */
 /* ssa.py:613-636 for every live function of the tile at once                  */
-template <class G, class C> CLF void t_usecount(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
-    PROF(g, s, PF_USECOUNT);
+template <class G, class C> CLF void t_usecount(const G &g, TileS<C> &T, const TileG<C> &tg) {
+    PROF(g, T.fs, PF_USECOUNT);
     GFOR(g, v, T.vtot) if (v < T.vtot) { T.usecnt[v] = 0; T.defpos[v] = NONE32; }
     g.sync();
     GFOR(g, i, T.n) if (i < T.n) {
         const uint32_t f = T.fidx[i];
         if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
         const cl_hdr h = T.hdr[i];
         const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
         bool odd = false;
         for (unsigned k = 0; k < nd; k++) {
-            const opnd d = get_slot(s, h, i, d0 + k);
+            const opnd d = t_slot(T, i, d0 + k);
             const unsigned kd = kind_of(d.tag);
-            if (kd == CL_K_VALUE) { if (d.pay < s.cap.V) s.defpos[d.pay] = i; }
+            if (kd == CL_K_VALUE) { if (d.pay < C::V) T.defpos[d.pay] = i; }
             else odd |= !(kd == CL_K_RZ || kd == CL_K_URZ || kd == CL_K_PRED);
         }
         if (odd) T.f_odd[f] = 1;
-        for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_add(&s.usecnt[v], 1u); });
+        t_value_operands(T, tg, h, i, [&](uint32_t v) { if (v < C::V) a_add(&T.usecnt[v], 1u); });
     }
     GFOR(g, b, T.nb) if (b < T.nb) {
-        const uint32_t f = T.bfun[b];
-        if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
+        if (!tf_ok(T, T.bfun[b])) continue;
         for (int k = 0; k < 2; k++)
-            if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE && T.blk[b].term_pay[k] < s.cap.V)
-                a_add(&s.usecnt[T.blk[b].term_pay[k]], 1u);
+            if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE && T.blk[b].term_pay[k] < C::V)
+                a_add(&T.usecnt[T.blk[b].term_pay[k]], 1u);
     }
     g.sync();
 }
 
 /* ----------------------------------------------------------------- matching */
+/* operand_key equality (patterns.py:109-127) of two operands                   */
+template <class C> CLD bool t_key_equal(const TileS<C> &T, const TileG<C> &tg, opnd a, opnd b) {
+    unsigned ka = kind_of(a.tag), kb = kind_of(b.tag);
+    if (ka == CL_K_URZ) ka = CL_K_RZ;
+    if (kb == CL_K_URZ) kb = CL_K_RZ;
+    const bool oa = ka == CL_K_NONE || ka >= CL_K_MEMREF, ob = kb == CL_K_NONE || kb >= CL_K_MEMREF;
+    if (oa || ob) {
+        if (!(oa && ob)) return false;
+        const cl_memref &x = tg.mem[a.pay], &y = tg.mem[b.pay];       /* ("other", str(op)) */
+        if (x.base_tag != y.base_tag || x.ureg_tag != y.ureg_tag) return false;
+        if (kind_of(x.base_tag) != CL_K_NONE && x.base_pay != y.base_pay) return false;
+        if (kind_of(x.ureg_tag) != CL_K_NONE && x.ureg_pay != y.ureg_pay) return false;
+        return x.off_hi == y.off_hi && x.off_lo == y.off_lo;
+    }
+    if (ka != kb) return false;
+    if (ka == CL_K_RZ) return true;
+    if (ka == CL_K_IMM) return T.imm[a.pay].bits == T.imm[b.pay].bits;
+    return a.pay == b.pay;
+}
+/* _match_opcode + the slot-local part of _unify (patterns.py:155-178, :130-152) */
+template <class C> CLD bool t_match_local(const TileS<C> &T, const cl_template &t, const cl_hdr &h, uint32_t i) {
+    if (h.op != t.op) return false;
+    const cl_modset &ms = T.fs.ms[h.modset];
+    if ((ms.mask & t.mods_all) != t.mods_all) return false;
+    if (ms.mask & t.mods_none) return false;
+    for (unsigned k = 0; k < t.n_modvars; k++) if (ms.first[t.modvar_group[k]] == 0xFF) return false;
+    if (t.n_defs != h.n_defs || t.n_aux != h.n_aux || t.n_uses != h.n_uses) return false;
+    if (h.flags & CL_IF_EXT) return false;
+    const unsigned n = (unsigned)t.n_defs + t.n_aux + t.n_uses, g0 = has_guard(h);
+    for (unsigned k = 0; k < n; k++) {
+        const cl_slot &sl = t.slot[k];
+        if (sl.kind == CL_S_ANY) continue;
+        const opnd o = t_slot(T, i, g0 + k);
+        switch (sl.kind) {
+        case CL_S_RZ: if (!is_zero(o)) return false; break;
+        case CL_S_PT:
+            if (!(kind_of(o.tag) == CL_K_PRED && o.pay == CL_PT_INDEX)) return false;
+            if (sl.neg != 0 && o_neg(o) != (sl.neg == 2)) return false;
+            break;
+        case CL_S_IMM: if (!(is_imm(o) && T.imm[o.pay].bits == sl.imm)) return false; break;
+        case CL_S_VAR:
+            if (sl.neg && o_neg(o) != (sl.neg == 2)) return false;
+            if (sl.bitnot && o_not(o) != (sl.bitnot == 2)) return false;
+            if (sl.half && o_half(o) != sl.half) return false;
+            break;
+        default: return false;
+        }
+    }
+    return true;
+}
+/* do two records share a value (defs and value operands of both)?  One edge of
+ * _connected (patterns.py:219-238)                                            */
+template <class C> CLD bool t_linked(const TileS<C> &T, const TileG<C> &tg, uint32_t i, uint32_t j) {
+    const cl_hdr hi = T.hdr[i], hj = T.hdr[j];
+    bool hit = false;
+    auto probe = [&](uint32_t v) {
+        t_value_defs(T, hj, j, [&](uint32_t w) { hit |= v == w; });
+        t_value_operands(T, tg, hj, j, [&](uint32_t w) { hit |= v == w; });
+    };
+    t_value_defs(T, hi, i, probe);
+    if (!hit) t_value_operands(T, tg, hi, i, probe);
+    return hit;
+}
+/* one candidate tuple of match_patterns (patterns.py:199-215)                  */
+template <class C> CLD bool t_check_tuple(const TileS<C> &T, const TileG<C> &tg, unsigned pi, const uint32_t *idx) {
+    const cl_pattern &p = T.P->pb.p[pi];
+    const unsigned nt = p.n_templates;
+    for (unsigned t = 0; t < nt; t++) if (!t_match_local(T, p.t[t], T.hdr[idx[t]], idx[t])) return false;
+    const TPat &tp = T.P->pat[pi];
+    for (unsigned q = 0; q < tp.n_mpairs; q++) {
+        const uint8_t *m = tp.mpair[q];
+        if (T.fs.ms[T.hdr[idx[m[0]]].modset].first[m[1]] != T.fs.ms[T.hdr[idx[m[2]]].modset].first[m[3]]) return false;
+    }
+    for (unsigned q = 0; q < tp.n_pairs; q++) {
+        const uint8_t *m = tp.pair[q];
+        const uint32_t ia = idx[m[0]], ib = idx[m[2]];
+        if (!t_key_equal(T, tg, t_slot(T, ia, has_guard(T.hdr[ia]) + m[1]), t_slot(T, ib, has_guard(T.hdr[ib]) + m[3]))) return false;
+    }
+    if (nt == 1) return true;
+    if (nt == 2) return t_linked(T, tg, idx[0], idx[1]);
+    const unsigned e = (unsigned)t_linked(T, tg, idx[0], idx[1]) + (unsigned)t_linked(T, tg, idx[0], idx[2]);
+    if (e == 2) return true;
+    if (e == 0) return false;
+    return t_linked(T, tg, idx[1], idx[2]);
+}
+
 /* one (pattern, anchor) item of match_patterns (patterns.py:181-216), join form
  * (see match_block in core.cuh); positions are tile positions                  */
-template <class C> CLF void t_try_anchor(TileS<C> &T, FS &s, unsigned table, uint32_t i, unsigned pi, uint32_t f) {
-    const cl_pattern_blob *pb = s.pb;
-    const cl_pattern &p = pb->p[pi];
+template <class C> CLF void t_try_anchor(TileS<C> &T, const TileG<C> &tg, unsigned table, uint32_t i, unsigned pi, uint32_t f) {
+    const cl_pattern &p = T.P->pb.p[pi];
     const unsigned nt = p.n_templates;
     const uint32_t b = T.bidx[i], lo = T.bo[b], hi = T.bo[b + 1];
     uint32_t idx[3] = { NONE32, NONE32, NONE32 };
@@ -213,15 +351,15 @@ template <class C> CLF void t_try_anchor(TileS<C> &T, FS &s, unsigned table, uin
         const cl_hdr hf = T.hdr[idx[from]];
         const cl_template &tf = p.t[from];
         if (hf.n_defs != tf.n_defs || hf.n_aux != tf.n_aux || hf.n_uses != tf.n_uses || (hf.flags & CL_IF_EXT)) return;
-        const unsigned long long mm = s.ms[hf.modset].mask;
+        const unsigned long long mm = T.fs.ms[hf.modset].mask;
         if ((mm & tf.mods_all) != tf.mods_all || (mm & tf.mods_none)) return;
-        const opnd o = get_slot(s, hf, idx[from], has_guard(hf) + p.join_slot[k]);
+        const opnd o = t_slot(T, idx[from], has_guard(hf) + p.join_slot[k]);
         if (!is_value(o)) {
             const unsigned ko = kind_of(o.tag);       /* a non-SSA link: the literal product decides */
             if (ko == CL_K_RZ || ko == CL_K_URZ || ko == CL_K_PRED) tf_fail(T, f, CL_ST_REDO);
             return;
         }
-        const uint32_t dp = o.pay < s.cap.V ? s.defpos[o.pay] : NONE32;
+        const uint32_t dp = o.pay < C::V ? T.defpos[o.pay] : NONE32;
         if (dp == NONE32 || dp < lo || dp >= hi || T.hdr[dp].op != p.t[t].op) return;
         idx[t] = dp;
     }
@@ -233,18 +371,17 @@ template <class C> CLF void t_try_anchor(TileS<C> &T, FS &s, unsigned table, uin
         int cl[3] = { 0, 0, 0 };
         for (unsigned t = 0; t < nt; t++) { cl[t] = t_class_of(T, table, p.t[t].op); cn[t] = T.ccnt[b][cl[t]]; }
         const unsigned long long prod = (unsigned long long)cn[0] * cn[1] * cn[2];
-        if (prod > pb->budget) {
+        if (prod > T.P->pb.budget) {
             unsigned long long r = 0;
             for (unsigned t = 0; t < nt; t++) {
                 uint32_t ci = 0;
                 for (uint32_t j = lo; j < idx[t]; j++) ci += T.clsid[j] == (uint8_t)cl[t];
                 r = t == 0 ? ci : r * cn[t] + ci;
             }
-            if (r >= pb->budget) return;
+            if (r >= T.P->pb.budget) return;
         }
     }
-    Bind bd;
-    if (!check_tuple(s, p, idx, bd)) return;
+    if (!t_check_tuple(T, tg, pi, idx)) return;
     const uint32_t m = a_add(&T.n_mt, 1u);
     if (m < C::M) {
         TMatch r;
@@ -257,8 +394,8 @@ template <class C> CLF void t_try_anchor(TileS<C> &T, FS &s, unsigned table, uin
     a_add(&T.f_stats[f][pi], 1u);
 }
 
-template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, unsigned table) {
-    PROF(g, s, PF_MATCH);
+template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const TileG<C> &tg, unsigned table) {
+    PROF(g, T.fs, PF_MATCH);
     GFOR(g, k, T.nb * MAX_CLS) if (k < T.nb * MAX_CLS) (&T.ccnt[0][0])[k] = 0;
     if (g.rank == 0) T.n_mt = 0;
     g.sync();
@@ -274,13 +411,12 @@ template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const Tile
     GFOR(g, i, T.n) if (i < T.n) {
         const unsigned c = T.clsid[i];
         if (c == 0xFFu) continue;
-        uint32_t pm = T.anchor_mask[table][c];
+        uint32_t pm = T.P->anchor_mask[table][c];
         if (!pm) continue;
         const uint32_t f = T.fidx[i];
         if (!tf_ok(T, f)) continue;
         if (T.f_odd[f]) { tf_fail(T, f, CL_ST_REDO); continue; }
-        tv_view(s, T, tg, f);
-        for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) t_try_anchor(T, s, table, i, pi, f);
+        for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) t_try_anchor(T, tg, table, i, pi, f);
     }
     g.sync();
 }
@@ -292,8 +428,8 @@ CLD unsigned long long t_key(const TMatch &m) {
     return (unsigned long long)m.pos[0] << 40 | (unsigned long long)(3u - m.n) << 38 | (unsigned long long)m.pat << 32 |
            (unsigned long long)m.pos[1] << 16 | m.pos[2];
 }
-template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T, FS &s) {
-    PROF(g, s, PF_SELECT);
+template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T) {
+    PROF(g, T.fs, PF_SELECT);
     const uint32_t n = T.n, nm = T.n_mt;
     GFOR(g, p, n) if (p < n) { T.keep[p] = 0; T.sel_at[p] = 0xFFFFu; }
     g.sync();
@@ -314,14 +450,12 @@ template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T, FS &s
             const unsigned long long key = t_key(r);
             bool mine = true;
             for (unsigned t = 0; t < r.n; t++) mine &= T.owner[r.pos[t]] == key;
-            if (mine) T.mstate[m] = MS_SELECTED; else left = true;
-        }
-        g.sync();
-        /* marks are written after every bid was compared (a winner never blocks a rival's compare) */
-        GFOR(g, m, nm) if (m < nm && T.mstate[m] == MS_SELECTED && T.sel_at[T.mt[m].pos[0]] == 0xFFFFu) {
-            const TMatch r = T.mt[m];
-            for (unsigned t = 0; t < r.n; t++) T.keep[r.pos[t]] = 1;
-            T.sel_at[r.pos[0]] = (uint16_t)m;
+            if (mine) {
+                T.mstate[m] = MS_SELECTED;
+                for (unsigned t = 0; t < r.n; t++) T.keep[r.pos[t]] = 1;      /* keep[] is read again only after the sync */
+                T.sel_at[r.pos[0]] = (uint16_t)m;
+            } else
+                left = true;
         }
         const bool again = g.any(left);
         g.sync();
@@ -349,55 +483,36 @@ template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T, FS &s
 
 /* fix-up of one staged match once the bases are known (apply_stage of core.cuh
  * without the in-place retag, which the caller does before the stream moves)   */
-template <class C> CLF void t_apply_stage(FS &s, Stage &st, uint32_t out) {
+template <class C> CLF void t_apply_stage(TileS<C> &T, Stage &st, uint32_t out) {
     for (unsigned k = 0; k < st.nv; k++) {
         const uint32_t v = st.vbase + k;
-        if (v >= s.cap.V) continue;
-        s.alive[v] = 1; s.origin[v] = CL_ORG_PAIR;
-        s.def_iid[v] = st.val_def[k] < 0 ? -1 : (int32_t)(st.ibase + (uint32_t)st.val_def[k]);
+        if (v >= C::V) continue;
+        T.alive[v] = 1; T.origin[v] = CL_ORG_PAIR;
+        T.def_iid[v] = st.val_def[k] < 0 ? -1 : (int32_t)(st.ibase + (uint32_t)st.val_def[k]);
     }
-    for (unsigned k = 0; k < st.nq; k++) if (st.mbase + k < s.cap.Q) s.imm[st.mbase + k] = st.imm[k];
+    for (unsigned k = 0; k < st.nq; k++) if (st.mbase + k < C::Q) T.imm[st.mbase + k] = st.imm[k];
     if (!st.ok) return;                      /* refused: the allocations above leak (G4) */
     for (unsigned r = 0; r < st.nins; r++) {
         const SRec q = st.rec[r];
-        Rec rec;
-        rec.h.iid = st.ibase + q.iid; rec.h.op = q.op; rec.h.modset = q.modset;
-        rec.h.n_defs = q.n_defs; rec.h.n_aux = 0; rec.h.n_uses = q.n_uses; rec.h.flags = 0; rec.h.ext = 0;
-        for (unsigned k = 0; k < 8; k++) { rec.tag[k] = k < 4 ? q.tag[k] : 0; rec.pay[k] = k < 4 ? q.pay[k] : 0; }
-        const unsigned ns = (unsigned)rec.h.n_defs + rec.h.n_uses;
-        for (unsigned k = 0; k < ns; k++)
-            if (rec.tag[k] & CL_T_REL) {
-                rec.pay[k] += kind_of(rec.tag[k]) == CL_K_VALUE ? st.vbase : st.mbase;
-                rec.tag[k] &= (uint16_t)~CL_T_REL;
+        const uint32_t o = out + r;
+        cl_hdr h;
+        h.iid = st.ibase + q.iid; h.op = q.op; h.modset = q.modset;
+        h.n_defs = q.n_defs; h.n_aux = 0; h.n_uses = q.n_uses; h.flags = 0; h.ext = 0;
+        T.hdr[o] = h;
+        const unsigned ns = (unsigned)q.n_defs + q.n_uses;
+#pragma unroll
+        for (unsigned k = 0; k < 8; k++) {
+            uint16_t tg_ = k < 4 ? q.tag[k] : (uint16_t)0;
+            uint32_t py = k < 4 ? q.pay[k] : 0u;
+            if (k < ns && (tg_ & CL_T_REL)) {
+                py += kind_of(tg_) == CL_K_VALUE ? st.vbase : st.mbase;
+                tg_ &= (uint16_t)~CL_T_REL;
             }
-        st_rec(s, out + r, rec);
+            T.tag[(size_t)o * 8 + k] = tg_; T.pay[(size_t)o * 8 + k] = py;
+        }
     }
-    for (unsigned k = 0; k < st.nupd; k++) if (st.upd_vid[k] < s.cap.V) s.def_iid[st.upd_vid[k]] = (int32_t)(st.ibase + st.upd_iid[k]);
-    for (unsigned k = 0; k < st.ndrop; k++) if (st.drop_vid[k] < s.cap.V) s.alive[st.drop_vid[k]] = 0;
-}
-
-
-/* running exclusive scan over items [0, n) in order                           */
-template <class G, class FIN, class FOUT> CLD uint32_t t_scan(const G &g, uint32_t n, FIN in, FOUT out) {
-    uint32_t run = 0;
-    GFOR(g, j, n) {
-        const uint32_t x = j < n ? in(j) : 0u;
-        uint32_t t;
-        const uint32_t o = g.exscan(x, t);
-        if (j < n) out(j, run + o);
-        run += t;
-    }
-    return run;
-}
-
-/* new block offsets after a permutation described by outpos[] (position of the
- * first output slot of every old record) and the new length                   */
-template <class G, class C> CLD void t_rebase_blocks(const G &g, TileS<C> &T, uint32_t n_old, uint32_t n_new) {
-    GFOR(g, b, T.nb + 1) if (b <= T.nb) { const uint32_t old = T.bo[b]; T.bo2[b] = old < n_old ? (uint32_t)T.outpos[old] : n_new; }
-    g.sync();
-    GFOR(g, b, T.nb + 1) if (b <= T.nb) T.bo[b] = T.bo2[b];
-    if (g.rank == 0) T.n = n_new;
-    g.sync();
+    for (unsigned k = 0; k < st.nupd; k++) if (st.upd_vid[k] < C::V) T.def_iid[st.upd_vid[k]] = (int32_t)(st.ibase + st.upd_iid[k]);
+    for (unsigned k = 0; k < st.ndrop; k++) if (st.drop_vid[k] < C::V) T.alive[st.drop_vid[k]] = 0;
 }
 
 /* _apply_patterns (patterns.py:671-707): one round over every gated function.
@@ -405,15 +520,15 @@ template <class G, class C> CLD void t_rebase_blocks(const G &g, TileS<C> &T, ui
  * a rewrite that removes a use of a value defined in a *later* block of its
  * function would be seen by that block's escape test in the reference (G5):
  * such functions are redone sequentially.                                   */
-template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, unsigned table,
+template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, const TileG<C> &tg, unsigned table,
                                                       uint32_t phase) {
-    t_usecount(g, T, tg, s);
-    t_match(g, T, tg, s, table);
+    t_usecount(g, T, tg);
+    t_match(g, T, tg, table);
     if (T.fail || T.n_mt == 0) return;
-    const uint32_t ns = t_select(g, T, s);
+    const uint32_t ns = t_select(g, T);
     if (T.fail || ns == 0) return;
     const uint32_t n = T.n;
-    PROF(g, s, PF_PLAN);
+    PROF(g, T.fs, PF_PLAN);
     GFOR(g, p, n) if (p < n) { T.keep[p] = 1; T.inscnt[p] = 0; }
     GFOR(g, f, T.nf) if (f < T.nf) T.f_first[f] = NONE32;
     GFOR(g, b, T.nb) if (b < T.nb) T.b_first[b] = NONE32;
@@ -428,9 +543,8 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
         if (j == 0 || T.fidx[T.sel[j - 1].pos[0]] != f) T.f_first[f] = j;
         if (j == 0 || T.sel[j - 1].blk != m.blk) T.b_first[m.blk] = j;
         if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
         RW c;
-        c.s = &s; c.st = &st; c.n = m.n; c.pat = m.pat; c.overflow = false;
+        c.s = &T.fs; c.st = &st; c.n = m.n; c.pat = m.pat; c.overflow = false; c.stw = &T.f_stat[f];
         for (unsigned t = 0; t < m.n; t++) { c.idx[t] = m.pos[t]; c.h[t] = T.hdr[c.idx[t]]; }
         for (unsigned t = m.n; t < 3; t++) c.idx[t] = NONE32;
         st.ok = run_rewrite(c);
@@ -440,8 +554,8 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
             bool hazard = false;
             for (unsigned t = 0; t < m.n; t++) {
                 if (!(st.rm >> t & 1)) continue;
-                for_value_operands(s, c.h[t], c.idx[t], [&](uint32_t v) {
-                    const uint32_t dp = v < s.cap.V ? s.defpos[v] : NONE32;
+                t_value_operands(T, tg, c.h[t], c.idx[t], [&](uint32_t v) {
+                    const uint32_t dp = v < C::V ? T.defpos[v] : NONE32;
                     hazard |= dp != NONE32 && T.bidx[dp] > m.blk;
                 });
             }
@@ -463,17 +577,17 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
         const uint32_t rv = (uint32_t)(me & 0xFFFFu) - (uint32_t)(first & 0xFFFFu);
         const uint32_t ri = (uint32_t)(me >> 16 & 0xFFFFu) - (uint32_t)(first >> 16 & 0xFFFFu);
         const uint32_t rq = (uint32_t)(me >> 32) - (uint32_t)(first >> 32);
-        st.vbase = T.f_nvid[f] + rv; st.ibase = T.f_niid[f] + ri; st.mbase = T.f_nimm[f] + rq;
+        st.vbase = T.f_vbase[f] + T.f_nvid[f] + rv; st.ibase = T.f_niid[f] + ri; st.mbase = T.f_qbase[f] + T.f_nimm[f] + rq;
         if (j + 1 == ns || T.fidx[T.sel[j + 1].pos[0]] != f) {
-            /* last match of its function: the function's new counters; over capacity -> general kernel */
-            if (st.vbase + st.nv > T.f_vcap[f] || st.mbase + st.nq > T.f_qcap[f]) tf_fail(T, f, CL_ST_REDO);
+            /* last match of its function: the function's new counters; over its slices -> general kernel */
+            if (st.vbase + st.nv > T.f_vbase[f + 1] || st.mbase + st.nq > T.f_qbase[f + 1]) tf_fail(T, f, CL_ST_REDO);
             T.f_aux[f] = j;
         }
     }
     g.sync();
     GFOR(g, f, T.nf) if (f < T.nf && T.f_first[f] != NONE32 && tf_ok(T, f)) {
         const Stage &st = tg.stage[T.f_aux[f]];
-        T.f_nvid[f] = st.vbase + st.nv; T.f_niid[f] = st.ibase + st.ni; T.f_nimm[f] = st.mbase + st.nq;
+        T.f_nvid[f] = st.vbase + st.nv - T.f_vbase[f]; T.f_niid[f] = st.ibase + st.ni; T.f_nimm[f] = st.mbase + st.nq - T.f_qbase[f];
     }
     /* marks, in-place retags (_rw_imad_wide :414-418), diagnostics, counters */
     GFOR(g, j, ns) if (j < ns) {
@@ -486,14 +600,14 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
             for (unsigned t = 0; t < m.n; t++) if (st.rm >> t & 1) T.keep[m.pos[t]] = 0;
             if (st.retag) {
                 cl_hdr &h = T.hdr[m.pos[0]];
-                h.modset = s.ms[h.modset].minus_wide;
+                h.modset = T.fs.ms[h.modset].minus_wide;
                 h.op = CL_OP_IMAD64;
             }
             a_add(&T.f_stats[f][32 + m.pat], 1u);
             a_add(&T.f_chg[f], 1u);
         } else {
             a_add(&T.f_stats[f][48 + m.pat], 1u);
-            t_event(s, T, tg, f, phase << 28 | (m.blk - T.f_b0[f]), CL_EV_REFUSED, j - T.b_first[m.blk], m.pat, T.blk[m.blk].bid);
+            t_event(T, tg, f, phase << 28 | (m.blk - T.f_b0[f]), CL_EV_REFUSED, j - T.b_first[m.blk], m.pat, T.blk[m.blk].bid);
         }
     }
     g.sync();
@@ -502,15 +616,13 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
                                 [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
     if (tot > C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
     g.sync();
-    PROF(g, s, PF_EMIT);
+    PROF(g, T.fs, PF_EMIT);
     t_permute(g, T, n, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] + T.inscnt[p] : NONE32; });
     /* staged records to their place, value table, immediates */
     GFOR(g, j, ns) if (j < ns) {
         const SelRec m = T.sel[j];
-        const uint32_t f = T.fidx[m.pos[0]];
-        if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
-        t_apply_stage<C>(s, tg.stage[j], T.outpos[m.pos[m.n - 1]]);
+        if (!tf_ok(T, T.fidx[m.pos[0]])) continue;
+        t_apply_stage(T, tg.stage[j], T.outpos[m.pos[m.n - 1]]);
     }
     g.sync();
     t_rebase_blocks(g, T, n, tot);
@@ -529,9 +641,9 @@ template <class G, class C> CLF void t_compact(const G &g, TileS<C> &T) {
 }
 
 /* remove_dead_pseudo (patterns.py:771-791) for the functions with f_gate set   */
-template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
-    PROF(g, s, PF_DCE);
-    t_usecount(g, T, tg, s);
+template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<C> &tg) {
+    PROF(g, T.fs, PF_DCE);
+    t_usecount(g, T, tg);
     GFOR(g, i, T.n) if (i < T.n) T.keep[i] = 1;
     g.sync();
     uint32_t removed = 0;
@@ -541,15 +653,14 @@ template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<
             const uint32_t f = T.fidx[i];
             if (!T.f_gate[f] || !tf_ok(T, f)) continue;
             const cl_hdr h = T.hdr[i];
-            if (h.op >= CL_OP__COUNT || !(s.opflags[h.op] & CL_OPF_PURE)) continue;
-            tv_view(s, T, tg, f);
+            if (h.op >= CL_OP__COUNT || !(T.fs.opflags[h.op] & CL_OPF_PURE)) continue;
             unsigned nd = 0; bool used = false;
-            for_value_defs(s, h, i, [&](uint32_t v) { nd++; used |= v < s.cap.V && *(volatile uint32_t *)&s.usecnt[v] != 0; });
+            t_value_defs(T, h, i, [&](uint32_t v) { nd++; used |= v < C::V && *(volatile uint32_t *)&T.usecnt[v] != 0; });
             if (!nd || used) continue;
             T.keep[i] = 0;
             mine++;
-            for_value_defs(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.alive[v] = 0; });
-            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) a_sub(&s.usecnt[v], 1u); });
+            t_value_defs(T, h, i, [&](uint32_t v) { if (v < C::V) T.alive[v] = 0; });
+            t_value_operands(T, tg, h, i, [&](uint32_t v) { if (v < C::V) a_sub(&T.usecnt[v], 1u); });
         }
         const uint32_t dead = g.sum(mine);
         g.sync();
@@ -561,9 +672,14 @@ template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<
 
 /* simplify_packs + _redirect_values (patterns.py:710-764) for the gated functions;
  * f_red[f] = redirects of function f                                          */
-template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
-    PROF(g, s, PF_SIMPLIFY);
-    t_usecount(g, T, tg, s);
+template <class C> CLD uint32_t t_final_of(const TileS<C> &T, uint32_t v) {
+    while (v < C::V && T.redirect[v] != NONE32) v = T.redirect[v];
+    return v;
+}
+template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const TileG<C> &tg) {
+    PROF(g, T.fs, PF_SIMPLIFY);
+    const FS &s = T.fs;
+    t_usecount(g, T, tg);
     GFOR(g, v, T.vtot) if (v < T.vtot) T.redirect[v] = NONE32;
     GFOR(g, f, T.nf) if (f < T.nf) T.f_red[f] = 0;
     g.sync();
@@ -573,22 +689,22 @@ template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const T
         if (h.op != CL_OP_PACK64 || h.n_uses != 2) continue;
         const uint32_t f = T.fidx[i];
         if (!T.f_gate[f] || !tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
-        opnd lo = get_use(s, h, i, 0), hi = get_use(s, h, i, 1);
+        const unsigned u0 = use0(h);
+        const opnd lo = t_slot(T, i, u0), hi = t_slot(T, i, u0 + 1);
         if (!is_value(lo) || !is_value(hi)) continue;
         if ((lo.tag | hi.tag) & (CL_T_NEG | CL_T_NOT)) continue;
-        if (lo.pay >= s.cap.V || hi.pay >= s.cap.V) continue;
-        const uint32_t plo = s.defpos[lo.pay], phi = s.defpos[hi.pay];
+        if (lo.pay >= C::V || hi.pay >= C::V) continue;
+        const uint32_t plo = T.defpos[lo.pay], phi = T.defpos[hi.pay];
         if (plo == NONE32 || phi == NONE32) continue;
         const cl_hdr dlo = T.hdr[plo], dhi = T.hdr[phi];
         if (!(dlo.op == CL_OP_UNPACK64 && has_mod(s, dlo, CL_MB_LO) && dhi.op == CL_OP_UNPACK64 && has_mod(s, dhi, CL_MB_HI))) continue;
-        if (!dlo.n_uses || !dhi.n_uses) { fail(s, CL_ST_INDEX_ERROR); continue; }
-        opnd slo = get_use(s, dlo, plo, 0), shi = get_use(s, dhi, phi, 0);
+        if (!dlo.n_uses || !dhi.n_uses) { tf_fail(T, f, CL_ST_REDO); continue; }
+        const opnd slo = t_slot(T, plo, use0(dlo)), shi = t_slot(T, phi, use0(dhi));
         if (!(is_value(slo) && is_value(shi) && slo.pay == shi.pay)) continue;
-        if (!h.n_defs) { fail(s, CL_ST_INDEX_ERROR); continue; }
-        opnd d = get_def(s, h, i, 0);
-        if (!is_value(d)) { fail(s, CL_ST_ATTRIBUTE_ERROR); continue; }
-        if (d.pay < s.cap.V) s.redirect[d.pay] = slo.pay;
+        if (!h.n_defs) { tf_fail(T, f, CL_ST_REDO); continue; }
+        const opnd d = t_slot(T, i, def0(h));
+        if (!is_value(d)) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (d.pay < C::V) T.redirect[d.pay] = slo.pay;
         a_add(&T.f_red[f], 1u);
         mine++;
     }
@@ -598,49 +714,47 @@ template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const T
     GFOR(g, i, T.n) if (i < T.n) {
         const uint32_t f = T.fidx[i];
         if (!T.f_red[f] || !tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
         const cl_hdr h = T.hdr[i];
         const unsigned u0 = use0(h);
         for (unsigned k = 0; k < h.n_uses; k++) {
-            opnd u = get_slot(s, h, i, u0 + k);
-            if (is_value(u)) { const uint32_t fo = final_of(s, u.pay); if (fo != u.pay) { u.pay = fo; set_slot(s, h, i, u0 + k, u); } }
+            const opnd u = t_slot(T, i, u0 + k);
+            if (is_value(u)) { const uint32_t fo = t_final_of(T, u.pay); if (fo != u.pay) T.pay[(size_t)i * 8 + u0 + k] = fo; }
             else if (kind_of(u.tag) == CL_K_MEMREF) {
-                cl_memref &m = s.mem[u.pay];
-                if (kind_of(m.base_tag) == CL_K_VALUE) m.base_pay = final_of(s, m.base_pay);
-                if (kind_of(m.ureg_tag) == CL_K_VALUE) m.ureg_pay = final_of(s, m.ureg_pay);
+                cl_memref &m = tg.mem[u.pay];
+                if (kind_of(m.base_tag) == CL_K_VALUE) m.base_pay = t_final_of(T, m.base_pay);
+                if (kind_of(m.ureg_tag) == CL_K_VALUE) m.ureg_pay = t_final_of(T, m.ureg_pay);
             }
         }
-        if (has_guard(h)) { opnd gd = get_slot(s, h, i, 0); if (is_value(gd)) { gd.pay = final_of(s, gd.pay); set_slot(s, h, i, 0, gd); } }
+        if (has_guard(h)) { const opnd gd = t_slot(T, i, 0); if (is_value(gd)) T.pay[(size_t)i * 8] = t_final_of(T, gd.pay); }
     }
     GFOR(g, b, T.nb) if (b < T.nb) {
         const uint32_t f = T.bfun[b];
         if (!T.f_red[f] || !tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
         for (int k = 0; k < 2; k++)
-            if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE) T.blk[b].term_pay[k] = final_of(s, T.blk[b].term_pay[k]);
+            if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE) T.blk[b].term_pay[k] = t_final_of(T, T.blk[b].term_pay[k]);
     }
     g.sync();
 }
 
 /* tag_cuda_objects (patterns.py:895-916)                                      */
-template <class G, class C> CLF void t_tag(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
-    PROF(g, s, PF_TAG);
+template <class G, class C> CLF void t_tag(const G &g, TileS<C> &T) {
+    PROF(g, T.fs, PF_TAG);
+    const FS &s = T.fs;
     GFOR(g, i, T.n) if (i < T.n) {
         cl_hdr h = T.hdr[i];
         if (h.op != CL_OP_BAR && h.op != CL_OP_WARPSYNC && h.op != CL_OP_SHFL) continue;
-        const uint32_t f = T.fidx[i];
-        if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
+        if (!tf_ok(T, T.fidx[i])) continue;
         unsigned kind = 0, use = 7;
+        const unsigned u0 = use0(h);
         if (h.op == CL_OP_BAR) {
             if (has_mod(s, h, CL_MB_SYNC)) {
                 kind = 1;
-                for (unsigned k = 0; k < h.n_uses && k < 7; k++) if (is_imm(get_use(s, h, i, k))) use = k;
+                for (unsigned k = 0; k < h.n_uses && k < 7; k++) if (is_imm(t_slot(T, i, u0 + k))) use = k;
             }
         } else if (h.op == CL_OP_WARPSYNC) {
             for (unsigned k = 0; k < h.n_uses && k < 7; k++) {
-                opnd u = get_use(s, h, i, k);
-                if (is_imm(u)) { if (s.imm[u.pay].bits == 0xFFFFFFFFull) { kind = 2; use = k; } break; }
+                const opnd u = t_slot(T, i, u0 + k);
+                if (is_imm(u)) { if (T.imm[u.pay].bits == 0xFFFFFFFFull) { kind = 2; use = k; } break; }
             }
         } else
             kind = 3;
@@ -666,12 +780,13 @@ template <class G, class C> CLF void t_tag(const G &g, TileS<C> &T, const TileG<
  * three hops, adds with two reciprocal operands and every exception path of the
  * reference are redone by the sequential kernel.                            */
 enum { RF_R0 = 1, RF_R1 = 2, RF_R2 = 4, RF_R3 = 8, RF_SEED = 16, RF_Q = 32, RF_MUFU = 128 };
-template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s) {
-    PROF(g, s, PF_RECIP);
+template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const TileG<C> &tg) {
+    PROF(g, T.fs, PF_RECIP);
+    const FS &s = T.fs;
     bool mine = false;
     GFOR(g, i, T.n) if (i < T.n) { const cl_hdr h = T.hdr[i]; mine |= h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP); }
     if (!g.any(mine)) return;
-    t_usecount(g, T, tg, s);
+    t_usecount(g, T, tg);
     const uint32_t n = T.n;
     uint32_t *valbits = T.redirect;
     GFOR(g, v, T.vtot) if (v < T.vtot) valbits[v] = 0;
@@ -683,12 +798,11 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         uint8_t fl = h.op == CL_OP_F2I ? (uint8_t)(RF_R0 | RF_R1 | RF_R2 | RF_R3) : (uint8_t)0;
         const uint32_t f = T.fidx[i];
         if (h.op == CL_OP_MUFU && tf_ok(T, f) && has_mod(s, h, CL_MB_RCP) && h.n_uses) {
-            tv_view(s, T, tg, f);
-            const opnd src = get_use(s, h, i, 0);
-            if (is_value(src) && src.pay < s.cap.V) {
-                const uint32_t dp = s.defpos[src.pay];
+            const opnd src = t_slot(T, i, use0(h));
+            if (is_value(src) && src.pay < C::V) {
+                const uint32_t dp = T.defpos[src.pay];
                 if (dp != NONE32 && T.hdr[dp].op == CL_OP_I2F) {
-                    if (!h.n_defs || !is_value(get_def(s, h, i, 0))) tf_fail(T, f, CL_ST_REDO);   /* IndexError / AttributeError */
+                    if (!h.n_defs || !is_value(t_slot(T, i, def0(h)))) tf_fail(T, f, CL_ST_REDO);   /* IndexError / AttributeError */
                     else fl |= RF_MUFU;
                 }
             }
@@ -700,20 +814,14 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     for (unsigned k = 1; k <= 3; k++) {
         const uint8_t prev = (uint8_t)(1u << (k - 1)), cur = (uint8_t)(1u << k);
         GFOR(g, i, n) if (i < n && (T.flag[i] & prev)) {
-            const uint32_t f = T.fidx[i];
-            if (!tf_ok(T, f)) continue;
-            tv_view(s, T, tg, f);
-            const cl_hdr h = T.hdr[i];
-            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.redirect[v] |= cur; });
+            if (!tf_ok(T, T.fidx[i])) continue;
+            t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) valbits[v] |= cur; });
         }
         g.sync();
         GFOR(g, i, n) if (i < n && !(T.flag[i] & cur)) {
-            const uint32_t f = T.fidx[i];
-            if (!tf_ok(T, f)) continue;
-            tv_view(s, T, tg, f);
-            const cl_hdr h = T.hdr[i];
+            if (!tf_ok(T, T.fidx[i])) continue;
             bool r = false;
-            for_value_defs(s, h, i, [&](uint32_t v) { r |= v < s.cap.V && (s.redirect[v] & cur); });
+            t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { r |= v < C::V && (valbits[v] & cur); });
             if (r) T.flag[i] |= (uint8_t)((0xFu << k) & 0xFu);        /* R_k implies R_k+1.. */
         }
         g.sync();
@@ -724,28 +832,27 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         if (h.op != CL_OP_IADD && h.op != CL_OP_IADD3) continue;
         const uint32_t f = T.fidx[i];
         if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
         bool any_imm = false;
-        for (unsigned k = 0; k < h.n_uses; k++) any_imm |= is_imm(get_use(s, h, i, k));
+        const unsigned u0 = use0(h);
+        for (unsigned k = 0; k < h.n_uses; k++) any_imm |= is_imm(t_slot(T, i, u0 + k));
         if (!any_imm) continue;
         unsigned hits = 0;
         uint32_t mp = NONE32, rcp = 0;
-        for_value_operands(s, h, i, [&](uint32_t v) {
-            const uint32_t dp = v < s.cap.V ? s.defpos[v] : NONE32;
+        t_value_operands(T, tg, h, i, [&](uint32_t v) {
+            const uint32_t dp = v < C::V ? T.defpos[v] : NONE32;
             if (dp == NONE32 || !(T.flag[dp] & RF_MUFU)) return;
-            const cl_hdr hm = T.hdr[dp];
-            const opnd d0 = get_def(s, hm, dp, 0);
+            const opnd d0 = t_slot(T, dp, def0(T.hdr[dp]));
             if (!is_value(d0) || d0.pay != v) return;
             hits++; mp = dp; rcp = v;
         });
         if (!hits) continue;
         if (hits > 1 || has_guard(h) || (h.flags & CL_IF_EXT)) { tf_fail(T, f, CL_ST_REDO); continue; }
         if (!(T.flag[i] & RF_R3)) continue;
-        if (T.bidx[mp] != T.bidx[i] || !h.n_defs || !is_value(get_def(s, h, i, 0))) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (T.bidx[mp] != T.bidx[i] || !h.n_defs || !is_value(t_slot(T, i, def0(h)))) { tf_fail(T, f, CL_ST_REDO); continue; }
         const uint32_t c = a_add(&T.n_chain, 1u);
         if (c < C::X) {
             TChain ch;
-            ch.add = (uint16_t)i; ch.mufu = (uint16_t)mp; ch.rcp = rcp; ch.addv = get_def(s, h, i, 0).pay; ch.f = (uint8_t)f; ch.ok = 1; ch.rank = 0;
+            ch.add = (uint16_t)i; ch.mufu = (uint16_t)mp; ch.rcp = rcp; ch.addv = t_slot(T, i, def0(h)).pay; ch.f = (uint8_t)f; ch.ok = 1; ch.rank = 0;
             T.chain[c] = ch;
         } else
             T.fail = 1;
@@ -759,20 +866,14 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     for (unsigned k = 1; k <= 3; k++) {
         const uint32_t cur = 0x100u << k;
         GFOR(g, i, n) if (i < n && (T.flag[i] & (RF_SEED | RF_Q))) {
-            const uint32_t f = T.fidx[i];
-            if (!tf_ok(T, f)) continue;
-            tv_view(s, T, tg, f);
-            const cl_hdr h = T.hdr[i];
-            for_value_operands(s, h, i, [&](uint32_t v) { if (v < s.cap.V) s.redirect[v] |= cur; });
+            if (!tf_ok(T, T.fidx[i])) continue;
+            t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) valbits[v] |= cur; });
         }
         g.sync();
         GFOR(g, i, n) if (i < n && !(T.flag[i] & RF_Q)) {
-            const uint32_t f = T.fidx[i];
-            if (!tf_ok(T, f)) continue;
-            tv_view(s, T, tg, f);
-            const cl_hdr h = T.hdr[i];
+            if (!tf_ok(T, T.fidx[i])) continue;
             bool r = false;
-            for_value_defs(s, h, i, [&](uint32_t v) { r |= v < s.cap.V && (s.redirect[v] & cur); });
+            t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { r |= v < C::V && (valbits[v] & cur); });
             if (r) T.flag[i] |= RF_Q;
         }
         g.sync();
@@ -798,31 +899,32 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         const TChain ch = T.chain[c];
         const uint32_t f = ch.f;
         if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
-        const uint32_t vi = T.f_nvid[f] + 2u * ch.rank, vf = vi + 1u, iid = T.f_niid[f] + 2u * ch.rank;
-        if (vf >= s.cap.V) { tf_fail(T, f, CL_ST_REDO); continue; }
-        /* _insert_reciprocal_bitcasts :863-888 */
-        s.alive[vi] = 1; s.origin[vi] = CL_ORG_BITS | ch.rcp; s.def_iid[vi] = (int32_t)iid;
-        s.alive[vf] = 1; s.origin[vf] = CL_ORG_F | ch.addv; s.def_iid[vf] = (int32_t)(iid + 1u);
+        const uint32_t vb = T.f_vbase[f];
+        const uint32_t vi = vb + T.f_nvid[f] + 2u * ch.rank, vf = vi + 1u, iid = T.f_niid[f] + 2u * ch.rank;
+        if (vf >= T.f_vbase[f + 1]) { tf_fail(T, f, CL_ST_REDO); continue; }
+        /* _insert_reciprocal_bitcasts :863-888 (origin codes carry function-local vids) */
+        T.alive[vi] = 1; T.origin[vi] = CL_ORG_BITS | (ch.rcp - vb); T.def_iid[vi] = (int32_t)iid;
+        T.alive[vf] = 1; T.origin[vf] = CL_ORG_F | (ch.addv - vb); T.def_iid[vf] = (int32_t)(iid + 1u);
         const cl_hdr ah = T.hdr[ch.add];
+        const unsigned u0 = use0(ah);
         for (unsigned k = 0; k < ah.n_uses; k++) {
-            opnd x = get_use(s, ah, ch.add, k);
-            if (is_value(x) && x.pay == ch.rcp) { x.pay = vi; set_slot(s, ah, ch.add, use0(ah) + k, x); }
+            const opnd x = t_slot(T, ch.add, u0 + k);
+            if (is_value(x) && x.pay == ch.rcp) T.pay[(size_t)ch.add * 8 + u0 + k] = vi;
         }
-        s.usecnt[ch.addv] = vf;
+        T.usecnt[ch.addv] = vf;
         T.keep[ch.add] = 1; T.inscnt[ch.add] = 1;
-        t_event(s, T, tg, f, 1u << 28, CL_EV_BOUNDARY, ch.rank, ch.rcp, ah.iid);
+        t_event(T, tg, f, 1u << 28, CL_EV_BOUNDARY, ch.rank, ch.rcp - vb, ah.iid);
     }
     g.sync();
     /* every user of an add result (top-level uses only :878-883) reads the float view */
     GFOR(g, i, n) if (i < n) {
         const uint32_t f = T.fidx[i];
         if (!T.f_aux[f] || !tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
         const cl_hdr h = T.hdr[i];
+        const unsigned u0 = use0(h);
         for (unsigned k = 0; k < h.n_uses; k++) {
-            opnd x = get_use(s, h, i, k);
-            if (is_value(x) && x.pay < s.cap.V && s.usecnt[x.pay] != NONE32) { x.pay = s.usecnt[x.pay]; set_slot(s, h, i, use0(h) + k, x); }
+            const opnd x = t_slot(T, i, u0 + k);
+            if (is_value(x) && x.pay < C::V && T.usecnt[x.pay] != NONE32) T.pay[(size_t)i * 8 + u0 + k] = T.usecnt[x.pay];
         }
     }
     g.sync();
@@ -836,15 +938,16 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         const TChain ch = T.chain[c];
         const uint32_t f = ch.f;
         if (!tf_ok(T, f)) continue;
-        tv_view(s, T, tg, f);
-        const uint32_t vi = T.f_nvid[f] + 2u * ch.rank, iid = T.f_niid[f] + 2u * ch.rank;
-        Rec r;
-        memset(&r, 0, sizeof r);
-        r.h.iid = iid; r.h.op = CL_OP_BITCAST; r.h.modset = CL_MS_F2I; r.h.n_defs = 1; r.h.n_uses = 1;
-        r.tag[0] = CL_K_VALUE; r.pay[0] = vi; r.tag[1] = CL_K_VALUE; r.pay[1] = ch.rcp;
-        st_rec(s, T.outpos[ch.add], r);
-        r.h.iid = iid + 1u; r.h.modset = CL_MS_I2F; r.pay[0] = vi + 1u; r.pay[1] = ch.addv;
-        st_rec(s, (uint32_t)T.outpos[ch.add] + 2u, r);
+        const uint32_t vi = T.f_vbase[f] + T.f_nvid[f] + 2u * ch.rank, iid = T.f_niid[f] + 2u * ch.rank;
+        for (unsigned q = 0; q < 2; q++) {
+            const uint32_t o = (uint32_t)T.outpos[ch.add] + 2u * q;
+            cl_hdr h;
+            h.iid = iid + q; h.op = CL_OP_BITCAST; h.modset = q ? CL_MS_I2F : CL_MS_F2I;
+            h.n_defs = 1; h.n_aux = 0; h.n_uses = 1; h.flags = 0; h.ext = 0;
+            T.hdr[o] = h;
+            for (unsigned k = 0; k < 8; k++) { T.tag[(size_t)o * 8 + k] = k < 2 ? (uint16_t)CL_K_VALUE : (uint16_t)0; T.pay[(size_t)o * 8 + k] = 0; }
+            T.pay[(size_t)o * 8] = vi + q; T.pay[(size_t)o * 8 + 1] = q ? ch.addv : ch.rcp;
+        }
     }
     g.sync();
     GFOR(g, f, T.nf) if (f < T.nf && T.f_aux[f] && tf_ok(T, f)) { T.f_nvid[f] += 2u * T.f_aux[f]; T.f_niid[f] += 2u * T.f_aux[f]; }
@@ -862,88 +965,119 @@ struct TileIO {                /* the part of KArgs the tile kernel needs (see c
     cl_corpus in;
     cl_hdr *o_hdr; uint16_t *o_tag; uint32_t *o_pay; cl_imm *o_imm;
     uint8_t *o_alive; int32_t *o_def_iid; uint32_t *o_origin;
+    cl_memref *o_mem;
     cl_blk *o_blk; uint32_t *o_blk_start, *o_blk_cnt;
     cl_event *o_ev;
     void *o_func;              /* FuncOut[]                                       */
     unsigned long long cap[4];
     unsigned long long *cursor, *stats;
     uint32_t *retry_list, *retry_count;
+    const uint32_t *flist;     /* function ids of all tiles                          */
 };
 struct TFuncOut { cl_func f; uint32_t inst_start, n_inst, imm_start, n_imm, val_start, ev_start, n_ev, pad; };
 
-template <class C> CLD uint32_t t_func_of_value(const TileS<C> &T, uint32_t k) {
-    uint32_t f = 0;
-    while (f + 1 < T.nf && T.f_vbase[f + 1] <= k) f++;
-    return f;
+/* slice that holds tile index k: last f with base[f] <= k                      */
+CLD uint32_t t_slice_of(const uint32_t *base, uint32_t nf, uint32_t k) {
+    uint32_t lo = 0, hi = nf;
+    while (lo + 1 < hi) { const uint32_t mid = (lo + hi) >> 1; if (base[mid] <= k) lo = mid; else hi = mid; }
+    return lo;
 }
-template <class C> CLD uint32_t t_func_of_imm(const TileS<C> &T, uint32_t k) {
-    uint32_t f = 0;
-    while (f + 1 < T.nf && T.f_qbase[f + 1] <= k) f++;
-    return f;
+/* rebase the ids of one operand into (in) or out of the tile's index spaces    */
+template <class C> CLD uint32_t t_rebase(const TileS<C> &T, uint32_t f, uint16_t tag, uint32_t pay, bool in) {
+    uint32_t d;
+    switch (kind_of(tag)) {
+    case CL_K_VALUE: d = T.f_vbase[f]; break;
+    case CL_K_IMM: d = T.f_qbase[f]; break;
+    case CL_K_MEMREF: d = T.f_mbase[f]; break;
+    default: return pay;
+    }
+    return in ? pay + d : pay - d;
 }
 
-template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, const TileIO &a, const TileDesc td) {
-    PROF(g, s, PF_LOAD);
+template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, TileG<C> &tg, const TileIO &a, const TileDesc td) {
+    PROF(g, T.fs, PF_LOAD);
     const cl_corpus &in = a.in;
-    const uint32_t f0 = td.f0, nf = td.nf;
-    const uint32_t B0 = in.func_blk_off[f0], B1 = in.func_blk_off[f0 + nf];
-    const uint32_t I0 = in.blk_off[B0], I1 = in.blk_off[B1];
-    const uint32_t nb = B1 - B0, n = I1 - I0;
+    const uint32_t nf = td.nf;
+    tg.mem = a.o_mem;
     if (g.rank == 0) {
-        T.f0 = f0; T.nf = nf; T.nb = nb; T.n = n; T.I0 = I0; T.B0 = B0;
+        T.fs.mem = tg.mem;
+        T.nf = nf;
         T.n_ev = 0; T.fail = 0; T.n_chain = 0; T.n_mt = 0; T.n_sel = 0;
-        T.f_b0[nf] = nb;
     }
     GFOR(g, f, nf) if (f < nf) {
-        const cl_func fn = in.func[f0 + f];
-        const uint32_t b0 = in.func_blk_off[f0 + f], b1 = in.func_blk_off[f0 + f + 1];
-        const uint32_t nrec = in.blk_off[b1] - in.blk_off[b0];
-        const uint32_t nimm = in.imm_off[f0 + f + 1] - in.imm_off[f0 + f];
+        const uint32_t gf = a.flist[td.first + f];
+        const cl_func fn = in.func[gf];
+        const uint32_t b0 = in.func_blk_off[gf], b1 = in.func_blk_off[gf + 1];
+        const uint32_t i0 = in.blk_off[b0], nrec = in.blk_off[b1] - i0;
+        const uint32_t nimm = in.imm_off[gf + 1] - in.imm_off[gf];
+        T.f_gf[f] = gf; T.f_gb0[f] = b0; T.f_gi0[f] = i0;
         T.f_arch[f] = fn.arch; T.f_nvid[f] = fn.next_vid; T.f_niid[f] = fn.next_iid; T.f_ntemp[f] = fn.next_temp_reg;
-        T.f_nimm[f] = nimm; T.f_stat[f] = 0; T.f_nev[f] = 0; T.f_odd[f] = 0; T.f_b0[f] = b0 - B0;
-        T.f_mem0[f] = in.mem_off[f0 + f]; T.f_nin[f] = nrec;
-        T.f_vcap[f] = tile_vcap(fn.next_vid, nrec); T.f_qcap[f] = tile_qcap(nimm, nrec);
+        T.f_nimm[f] = nimm; T.f_stat[f] = 0; T.f_nev[f] = 0; T.f_odd[f] = 0;
+        T.f_mbase[f] = in.mem_off[gf]; T.f_nin[f] = nrec;
+        T.f_oi[f] = tile_vcap(fn.next_vid, nrec); T.f_oq[f] = tile_qcap(nimm, nrec);     /* slice sizes, scanned below */
+        T.f_ov[f] = b1 - b0;
         T.f_active[f] = 0; T.f_gate[f] = 0; T.f_chg[f] = 0; T.f_red[f] = 0; T.f_aux[f] = 0;
-        for (uint32_t b = b0; b < b1; b++) T.bfun[b - B0] = (uint8_t)f;
     }
     GFOR(g, k, nf * 64) if (k < nf * 64) (&T.f_stats[0][0])[k] = 0;
-    GFOR(g, b, nb + 1) if (b <= nb) T.bo[b] = in.blk_off[B0 + b] - I0;
-    GFOR(g, b, nb) if (b < nb) T.blk[b] = in.blk[B0 + b];
-    {
-        const uint4 *src = (const uint4 *)(in.hdr + I0);
-        uint4 *dst = (uint4 *)T.hdr;
-        GFOR(g, i, n) if (i < n) dst[i] = src[i];
-        const uint4 *st = (const uint4 *)(in.tag + (size_t)I0 * 8);
-        uint4 *dt = (uint4 *)T.tag;
-        GFOR(g, i, n) if (i < n) dt[i] = st[i];
-        const uint4 *sp = (const uint4 *)(in.pay + (size_t)I0 * 8);
-        uint4 *dp = (uint4 *)T.pay;
-        GFOR(g, i, 2 * n) if (i < 2 * n) dp[i] = sp[i];
-    }
-    {
-        const uint32_t m0 = in.mem_off[f0], m1 = in.mem_off[f0 + nf];
-        GFOR(g, m, m1 - m0) if (m < m1 - m0) tg.mem[m0 + m] = in.mem[m0 + m];
-    }
     g.sync();
     if (g.rank == 0) {
-        uint32_t vb = 0, qb = 0;
-        for (uint32_t f = 0; f < nf; f++) { T.f_vbase[f] = vb; T.f_qbase[f] = qb; vb += T.f_vcap[f]; qb += T.f_qcap[f]; }
-        T.f_vbase[nf] = vb; T.f_qbase[nf] = qb; T.vtot = vb; T.qtot = qb;
-        if (vb > C::V || qb > C::Q || n > C::I || nb > C::B || nf > C::F) T.fail = 1;      /* planner bug: loud */
+        uint32_t vb = 0, qb = 0, bb = 0, ib = 0;
+        for (uint32_t f = 0; f < nf; f++) {
+            T.f_vbase[f] = vb; T.f_qbase[f] = qb; T.f_b0[f] = bb; T.f_i0[f] = ib;
+            vb += T.f_oi[f]; qb += T.f_oq[f]; bb += T.f_ov[f]; ib += T.f_nin[f];
+        }
+        T.f_vbase[nf] = vb; T.f_qbase[nf] = qb; T.f_b0[nf] = bb; T.f_i0[nf] = ib;
+        T.vtot = vb; T.qtot = qb; T.nb = bb; T.n = ib;
+        if (vb > C::V || qb > C::Q || ib > C::I || bb > C::B || nf > C::F) T.fail = 1;      /* planner bug: loud */
     }
     g.sync();
     if (T.fail) return;
+    const uint32_t nb = T.nb, n = T.n;
+    GFOR(g, b, nb) if (b < nb) {
+        const uint32_t f = t_slice_of(T.f_b0, nf, b), gb = T.f_gb0[f] + (b - T.f_b0[f]);
+        T.bfun[b] = (uint8_t)f;
+        T.bo[b] = T.f_i0[f] + (in.blk_off[gb] - T.f_gi0[f]);
+        cl_blk bk = in.blk[gb];
+        for (int k = 0; k < 2; k++) if (kind_of(bk.term_tag[k]) == CL_K_VALUE) bk.term_pay[k] += T.f_vbase[f];
+        T.blk[b] = bk;
+    }
+    if (g.rank == 0) T.bo[nb] = n;
+    /* records: coalesced per function; value / immediate / memref ids rebased into the tile's index spaces */
+    GFOR(g, i, n) if (i < n) {
+        const uint32_t f = t_slice_of(T.f_i0, nf, i);
+        const size_t src = (size_t)T.f_gi0[f] + (i - T.f_i0[f]);
+        T.fidx[i] = (uint8_t)f;
+        *(uint4 *)&T.hdr[i] = *(const uint4 *)(in.hdr + src);
+        const uint4 tg4 = *(const uint4 *)(in.tag + src * 8);
+        uint4 p0 = ((const uint4 *)(in.pay + src * 8))[0], p1 = ((const uint4 *)(in.pay + src * 8))[1];
+        const uint16_t *tags = (const uint16_t *)&tg4;
+        uint32_t *pp0 = (uint32_t *)&p0, *pp1 = (uint32_t *)&p1;
+#pragma unroll
+        for (unsigned k = 0; k < 4; k++) { pp0[k] = t_rebase(T, f, tags[k], pp0[k], true); pp1[k] = t_rebase(T, f, tags[4 + k], pp1[k], true); }
+        *(uint4 *)&T.tag[(size_t)i * 8] = tg4;
+        ((uint4 *)&T.pay[(size_t)i * 8])[0] = p0;
+        ((uint4 *)&T.pay[(size_t)i * 8])[1] = p1;
+    }
+    for (uint32_t f = 0; f < nf; f++) {           /* memrefs: mutable copy in the output, value ids rebased */
+        const uint32_t m0 = T.f_mbase[f], nm = in.mem_off[T.f_gf[f] + 1] - m0, vb = T.f_vbase[f];
+        GFOR(g, m, nm) if (m < nm) {
+            cl_memref r = in.mem[m0 + m];
+            if (kind_of(r.base_tag) == CL_K_VALUE) r.base_pay += vb;
+            if (kind_of(r.ureg_tag) == CL_K_VALUE) r.ureg_pay += vb;
+            tg.mem[m0 + m] = r;
+        }
+    }
     GFOR(g, k, T.vtot) if (k < T.vtot) {
-        const uint32_t f = t_func_of_value(T, k), v = k - T.f_vbase[f];
-        const uint32_t v0 = in.val_off[f0 + f];
+        const uint32_t f = t_slice_of(T.f_vbase, nf, k), v = k - T.f_vbase[f];
+        const uint32_t v0 = in.val_off[T.f_gf[f]];
         const bool have = v < T.f_nvid[f];
         T.alive[k] = have ? in.val_alive[v0 + v] : (uint8_t)0;
         T.def_iid[k] = have ? in.val_def_iid[v0 + v] : -1;
         T.origin[k] = CL_ORG_HOST;
     }
     GFOR(g, k, T.qtot) if (k < T.qtot) {
-        const uint32_t f = t_func_of_imm(T, k), q = k - T.f_qbase[f];
-        if (q < T.f_nimm[f]) T.imm[k] = in.imm[in.imm_off[f0 + f] + q];
+        const uint32_t f = t_slice_of(T.f_qbase, nf, k), q = k - T.f_qbase[f];
+        if (q < T.f_nimm[f]) T.imm[k] = in.imm[in.imm_off[T.f_gf[f]] + q];
     }
     g.sync();
     t_index(g, T);
@@ -951,9 +1085,9 @@ template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, const TileG
 
 /* results of the live functions go to one atomically reserved place per tile (function
  * order inside it); dead ones are queued for the general kernel                 */
-template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, const TileIO &a) {
-    PROF(g, s, PF_STORE);
-    const uint32_t nf = T.nf, f0 = T.f0;
+template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const TileG<C> &tg, const TileIO &a) {
+    PROF(g, T.fs, PF_STORE);
+    const uint32_t nf = T.nf;
     if (g.rank == 0) {
         uint32_t oi = 0, oq = 0, ov = 0, oe = 0;
         const bool tile_ok = !T.fail;
@@ -980,38 +1114,57 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
     const bool fits = T.work != 0;
     TFuncOut *o_func = (TFuncOut *)a.o_func;
     GFOR(g, f, nf) if (f < nf) {
-        if (T.f_stat[f] != 0) { a.retry_list[a_add(a.retry_count, 1u)] = f0 + f; continue; }
+        if (T.f_stat[f] != 0) { a.retry_list[a_add(a.retry_count, 1u)] = T.f_gf[f]; continue; }
         const uint32_t cnt = T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]];
         TFuncOut o;
         o.f.next_vid = T.f_nvid[f]; o.f.next_iid = T.f_niid[f]; o.f.next_temp_reg = T.f_ntemp[f];
         o.f.arch = T.f_arch[f]; o.f.status = (uint8_t)(fits ? CL_ST_OK : CL_ST_CAPACITY); o.f.reserved = 0;
         o.inst_start = T.f_oi[f]; o.n_inst = fits ? cnt : 0; o.imm_start = T.f_oq[f]; o.n_imm = fits ? T.f_nimm[f] : 0;
         o.val_start = T.f_ov[f]; o.ev_start = T.f_oe[f]; o.n_ev = fits ? T.f_nev[f] : 0; o.pad = 0;
-        o_func[f0 + f] = o;
+        o_func[T.f_gf[f]] = o;
     }
     GFOR(g, b, T.nb) if (b < T.nb) {
         const uint32_t f = T.bfun[b];
         if (T.f_stat[f] != 0) continue;
-        a.o_blk[T.B0 + b] = T.blk[b];
-        a.o_blk_start[T.B0 + b] = fits ? T.f_oi[f] + (T.bo[b] - T.bo[T.f_b0[f]]) : 0u;
-        a.o_blk_cnt[T.B0 + b] = fits ? T.bo[b + 1] - T.bo[b] : 0u;
+        cl_blk bk = T.blk[b];
+        for (int k = 0; k < 2; k++) bk.term_pay[k] = t_rebase(T, f, bk.term_tag[k], bk.term_pay[k], false);
+        const uint32_t gb = T.f_gb0[f] + (b - T.f_b0[f]);
+        a.o_blk[gb] = bk;
+        a.o_blk_start[gb] = fits ? T.f_oi[f] + (T.bo[b] - T.bo[T.f_b0[f]]) : 0u;
+        a.o_blk_cnt[gb] = fits ? T.bo[b + 1] - T.bo[b] : 0u;
+    }
+    /* memrefs of the live functions back to function-local value ids (dead ones are reloaded by the general kernel) */
+    for (uint32_t f = 0; f < nf; f++) {
+        if (T.f_stat[f] != 0) continue;
+        const uint32_t m0 = T.f_mbase[f], nm = a.in.mem_off[T.f_gf[f] + 1] - m0, vb = T.f_vbase[f];
+        GFOR(g, m, nm) if (m < nm) {
+            cl_memref &r = tg.mem[m0 + m];
+            if (kind_of(r.base_tag) == CL_K_VALUE) r.base_pay -= vb;
+            if (kind_of(r.ureg_tag) == CL_K_VALUE) r.ureg_pay -= vb;
+        }
     }
     if (fits) {
         GFOR(g, i, T.n) if (i < T.n) {
             const uint32_t f = T.fidx[i];
             if (T.f_stat[f] != 0) continue;
             const size_t d = (size_t)T.f_oi[f] + (i - T.bo[T.f_b0[f]]);
+            uint4 tg4 = *(const uint4 *)&T.tag[(size_t)i * 8];
+            uint4 p0 = ((const uint4 *)&T.pay[(size_t)i * 8])[0], p1 = ((const uint4 *)&T.pay[(size_t)i * 8])[1];
+            const uint16_t *tags = (const uint16_t *)&tg4;
+            uint32_t *pp0 = (uint32_t *)&p0, *pp1 = (uint32_t *)&p1;
+#pragma unroll
+            for (unsigned k = 0; k < 4; k++) { pp0[k] = t_rebase(T, f, tags[k], pp0[k], false); pp1[k] = t_rebase(T, f, tags[4 + k], pp1[k], false); }
             *(uint4 *)(a.o_hdr + d) = *(const uint4 *)&T.hdr[i];
-            *(uint4 *)(a.o_tag + d * 8) = *(const uint4 *)&T.tag[(size_t)i * 8];
-            ((uint4 *)(a.o_pay + d * 8))[0] = ((const uint4 *)&T.pay[(size_t)i * 8])[0];
-            ((uint4 *)(a.o_pay + d * 8))[1] = ((const uint4 *)&T.pay[(size_t)i * 8])[1];
+            *(uint4 *)(a.o_tag + d * 8) = tg4;
+            ((uint4 *)(a.o_pay + d * 8))[0] = p0;
+            ((uint4 *)(a.o_pay + d * 8))[1] = p1;
         }
         GFOR(g, k, T.qtot) if (k < T.qtot) {
-            const uint32_t f = t_func_of_imm(T, k), q = k - T.f_qbase[f];
+            const uint32_t f = t_slice_of(T.f_qbase, nf, k), q = k - T.f_qbase[f];
             if (T.f_stat[f] == 0 && q < T.f_nimm[f]) a.o_imm[T.f_oq[f] + q] = T.imm[k];
         }
         GFOR(g, k, T.vtot) if (k < T.vtot) {
-            const uint32_t f = t_func_of_value(T, k), v = k - T.f_vbase[f];
+            const uint32_t f = t_slice_of(T.f_vbase, nf, k), v = k - T.f_vbase[f];
             if (T.f_stat[f] == 0 && v < T.f_nvid[f]) {
                 const size_t d = (size_t)T.f_ov[f] + v;
                 a.o_alive[d] = T.alive[k]; a.o_def_iid[d] = T.def_iid[k]; a.o_origin[d] = T.origin[k];
@@ -1019,8 +1172,9 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
         }
         const uint32_t nev = T.n_ev < C::E ? T.n_ev : C::E;
         GFOR(g, e, nev) if (e < nev) {
-            const cl_event ev = tg.ev[e];
-            const uint32_t f = ev.func - f0;
+            cl_event ev = tg.ev[e];
+            const uint32_t f = ev.func;
+            ev.func = T.f_gf[f];
             if (T.f_stat[f] == 0) a.o_ev[T.f_oe[f] + a_add(&T.f_aux[f], 1u)] = ev;
         }
     }
@@ -1050,53 +1204,94 @@ template <class G, class C> CLD bool t_any_gate(const G &g, TileS<C> &T) {
     return g.any(m);
 }
 
-template <class G, class C> CLF void t_run_tile(const G &g, TileS<C> &T, const TileG<C> &tg, FS &s, const TileIO &a,
-                                                const TileDesc td) {
-    t_load(g, T, tg, s, a, td);
-    if (!T.fail && (s.passes & CL_PASS_XMAD)) {
+template <class G, class C> CLF void t_run_tile(const G &g, TileS<C> &T, TileG<C> &tg, const TileIO &a, const TileDesc td) {
+    const uint32_t passes = T.fs.passes, max_rounds = T.fs.max_rounds;
+    t_load(g, T, tg, a, td);
+    if (!T.fail && (passes & CL_PASS_XMAD)) {
         t_set_gate(g, T, 0);
         if (t_any_gate(g, T)) {
-            t_apply_patterns(g, T, tg, s, 1, 0);
-            if (!T.fail) { t_set_gate(g, T, 0); t_dce(g, T, tg, s); }
+            t_apply_patterns(g, T, tg, 1, 0);
+            if (!T.fail) { t_set_gate(g, T, 0); t_dce(g, T, tg); }
         }
     }
-    if (!T.fail && (s.passes & CL_PASS_RECIPROCAL)) t_reciprocal(g, T, tg, s);
-    if (!T.fail && (s.passes & CL_PASS_AGGREGATE)) {
+    if (!T.fail && (passes & CL_PASS_RECIPROCAL)) t_reciprocal(g, T, tg);
+    if (!T.fail && (passes & CL_PASS_AGGREGATE)) {
         GFOR(g, f, T.nf) if (f < T.nf) T.f_active[f] = 1;
         g.sync();
-        for (uint32_t round = 0; round < s.max_rounds && !T.fail; round++) {
+        for (uint32_t round = 0; round < max_rounds && !T.fail; round++) {
             t_set_gate(g, T, 1);
             if (!t_any_gate(g, T)) break;
             GFOR(g, f, T.nf) if (f < T.nf) T.f_chg[f] = 0;
             g.sync();
-            t_apply_patterns(g, T, tg, s, 0, 2 + round);
+            t_apply_patterns(g, T, tg, 0, 2 + round);
             if (T.fail) break;
             t_set_gate(g, T, 1);
-            t_simplify(g, T, tg, s);
+            t_simplify(g, T, tg);
             t_set_gate(g, T, 2);
-            if (t_any_gate(g, T)) t_dce(g, T, tg, s);
+            if (t_any_gate(g, T)) t_dce(g, T, tg);
             GFOR(g, f, T.nf) if (f < T.nf) T.f_active[f] = T.f_active[f] && (T.f_chg[f] + T.f_red[f]) != 0;
             g.sync();
         }
-        if (!T.fail) { t_set_gate(g, T, 3); t_dce(g, T, tg, s); }
+        if (!T.fail) { t_set_gate(g, T, 3); t_dce(g, T, tg); }
     }
-    if (!T.fail && (s.passes & CL_PASS_TAG)) t_tag(g, T, tg, s);
+    if (!T.fail && (passes & CL_PASS_TAG)) t_tag(g, T);
     g.sync();
-    t_store(g, T, tg, s, a);
+    t_store(g, T, tg, a);
 }
 
-/* class tables of both pattern tables, once per CTA                           */
-template <class G, class C> CLF void t_setup(const G &g, TileS<C> &T, FS &s) {
+/* once per CTA: the pattern table in shared memory, seed classes of both tables,
+ * anchors, unification constraints.  `fs` is any FS whose pb can be pointed at P. */
+template <class G> CLF void t_setup(const G &g, TileP &P, const cl_pattern_blob *pb) {
+    {
+        const uint32_t *src = (const uint32_t *)pb;
+        uint32_t *dst = (uint32_t *)&P.pb;
+        GFOR(g, k, sizeof(cl_pattern_blob) / 4) if (k < sizeof(cl_pattern_blob) / 4) dst[k] = src[k];
+        GFOR(g, k, 2 * CL_OP__COUNT) if (k < 2 * CL_OP__COUNT) (&P.op_cls[0][0])[k] = 0xFF;
+    }
+    g.sync();
     if (g.rank == 0) {
         for (unsigned table = 0; table < 2; table++) {
-            setup_classes(s, table);
-            T.n_cls[table] = s.n_cls;
-            for (unsigned c = 0; c < (unsigned)MAX_CLS; c++) { T.cls_op[table][c] = c < s.n_cls ? s.cls_op[c] : (uint16_t)0xFFFF; T.anchor_mask[table][c] = 0; }
-            for (unsigned pi = 0; pi < s.pb->n_patterns; pi++) {
-                const cl_pattern &p = s.pb->p[pi];
+            unsigned n_cls = 0;
+            for (unsigned c = 0; c < (unsigned)MAX_CLS; c++) { P.cls_op[table][c] = 0xFFFF; P.anchor_mask[table][c] = 0; }
+            for (unsigned pi = 0; pi < P.pb.n_patterns; pi++) {
+                const cl_pattern &p = P.pb.p[pi];
                 if (p.table != table) continue;
-                const int c = class_of(s, p.t[p.join_order[0]].op);
-                if (c >= 0) T.anchor_mask[table][c] |= 1u << pi;
+                for (unsigned t = 0; t < p.n_templates; t++) {
+                    bool seen = false;
+                    for (unsigned c = 0; c < n_cls; c++) seen |= P.cls_op[table][c] == p.t[t].op;
+                    if (!seen && n_cls < (unsigned)MAX_CLS) P.cls_op[table][n_cls++] = p.t[t].op;
+                }
+            }
+            P.n_cls[table] = n_cls;
+            for (unsigned c = 0; c < n_cls; c++) if (P.cls_op[table][c] < CL_OP__COUNT) P.op_cls[table][P.cls_op[table][c]] = (uint8_t)c;
+            for (unsigned pi = 0; pi < P.pb.n_patterns; pi++) {
+                const cl_pattern &p = P.pb.p[pi];
+                if (p.table != table) continue;
+                const uint16_t aop = p.t[p.join_order[0]].op;
+                for (unsigned c = 0; c < n_cls; c++) if (P.cls_op[table][c] == aop) P.anchor_mask[table][c] |= 1u << pi;
+            }
+        }
+    }
+    GFOR(g, pi, P.pb.n_patterns) if (pi < P.pb.n_patterns) {
+        const cl_pattern &p = P.pb.p[pi];
+        TPat &tp = P.pat[pi];
+        tp.n_pairs = tp.n_mpairs = 0;
+        uint8_t ft[CL_MAX_VARS], fk[CL_MAX_VARS], mt[CL_MAX_GROUPS], mg[CL_MAX_GROUPS];
+        for (int v = 0; v < CL_MAX_VARS; v++) ft[v] = 0xFF;
+        for (int v = 0; v < CL_MAX_GROUPS; v++) mt[v] = 0xFF;
+        for (unsigned t = 0; t < p.n_templates; t++) {
+            const cl_template &tm = p.t[t];
+            for (unsigned k = 0; k < tm.n_modvars; k++) {
+                const unsigned mv = tm.modvar_var[k] & (CL_MAX_GROUPS - 1);
+                if (mt[mv] == 0xFF) { mt[mv] = (uint8_t)t; mg[mv] = tm.modvar_group[k]; }
+                else if (tp.n_mpairs < 4) { uint8_t *m = tp.mpair[tp.n_mpairs++]; m[0] = mt[mv]; m[1] = mg[mv]; m[2] = (uint8_t)t; m[3] = tm.modvar_group[k]; }
+            }
+            const unsigned ns = (unsigned)tm.n_defs + tm.n_aux + tm.n_uses;
+            for (unsigned k = 0; k < ns && k < 8; k++) {
+                if (tm.slot[k].kind != CL_S_VAR) continue;
+                const unsigned v = tm.slot[k].var & (CL_MAX_VARS - 1);
+                if (ft[v] == 0xFF) { ft[v] = (uint8_t)t; fk[v] = (uint8_t)k; }
+                else if (tp.n_pairs < 28) { uint8_t *m = tp.pair[tp.n_pairs++]; m[0] = ft[v]; m[1] = fk[v]; m[2] = (uint8_t)t; m[3] = (uint8_t)k; }
             }
         }
     }
