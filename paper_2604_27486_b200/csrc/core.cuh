@@ -106,7 +106,11 @@ struct Prof {
     CLMEM Prof(unsigned long long *a, int slot, bool lane0) : acc(a + slot), t0(0), on(lane0) { if (on) t0 = now(); }
     CLMEM ~Prof() { if (on) *acc += now() - t0; }
 };
+#ifdef CL_PROFILE
 #define PROF(g, s, slot) Prof _prof_##slot((s).prof, slot, (g).rank == 0)
+#else
+#define PROF(g, s, slot) do { } while (0)      /* build with -DCL_PROFILE for the per-phase cycle counters */
+#endif
 
 /* ------------------------------------------------------------------ groups */
 /* NW = warps per group.  NW == 1: the group is a warp (several independent
@@ -117,6 +121,22 @@ template <int NW> struct Grp {
     uint32_t *red;             /* NW > 1: shared scratch, NW + 2 words         */
 #if CL_DEV
     CLD void sync() const { if (NW == 1) __syncwarp(); else __syncthreads(); }
+    /* second level of the CTA scans: warp 0 turns the per-warp totals in red[0 .. NW) into exclusive
+     * prefixes (in place) and the grand total in red[NW]; callers sync before and after            */
+    CLD void scan_warp_totals() const {
+        if ((rank >> 5) == 0) {
+            const uint32_t lane = rank & 31u;
+            const uint32_t t = lane < (uint32_t)NW ? red[lane] : 0u;
+            uint32_t v = t;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, v, d);
+                if (lane >= (uint32_t)d) v += u;
+            }
+            if (lane < (uint32_t)NW) red[lane] = v - t;
+            if (lane == 31) red[NW] = v;
+        }
+    }
     CLD uint32_t exscan(uint32_t x, uint32_t &total) const {
         const uint32_t lane = rank & 31u;
         uint32_t v = x;
@@ -129,11 +149,12 @@ template <int NW> struct Grp {
         const uint32_t w = rank >> 5;
         if (lane == 31) red[w] = v;
         __syncthreads();
-        uint32_t pre = 0, tot = 0;
-        for (int i = 0; i < NW; i++) { uint32_t t = red[i]; if ((uint32_t)i < w) pre += t; tot += t; }
+        scan_warp_totals();
         __syncthreads();
-        total = tot;
-        return pre + v - x;
+        /* red[w] is rewritten only by warp w itself (next call) and red[NW] only after the next call's
+         * first barrier: no trailing barrier needed                                               */
+        total = red[NW];
+        return red[w] + v - x;
     }
     /* ballot + popc compaction offsets */
     CLD uint32_t flag_exscan(bool f, uint32_t &total) const {
@@ -144,11 +165,10 @@ template <int NW> struct Grp {
         const uint32_t w = rank >> 5;
         if (lane == 0) red[w] = __popc(b);
         __syncthreads();
-        uint32_t pre = 0, tot = 0;
-        for (int i = 0; i < NW; i++) { uint32_t t = red[i]; if ((uint32_t)i < w) pre += t; tot += t; }
+        scan_warp_totals();
         __syncthreads();
-        total = tot;
-        return pre + mine;
+        total = red[NW];
+        return red[w] + mine;
     }
     CLD bool any(bool f) const {
         if (NW == 1) return __any_sync(0xFFFFFFFFu, f);
@@ -157,9 +177,9 @@ template <int NW> struct Grp {
     CLD uint32_t sum(uint32_t x) const { uint32_t t; exscan(x, t); return t; }
     CLD uint32_t bcast0(uint32_t x) const {
         if (NW == 1) return __shfl_sync(0xFFFFFFFFu, x, 0);
-        if (rank == 0) red[NW] = x;
+        if (rank == 0) red[NW + 1] = x;
         __syncthreads();
-        uint32_t r = red[NW];
+        uint32_t r = red[NW + 1];
         __syncthreads();
         return r;
     }

@@ -589,7 +589,7 @@ CLHD TileIO tile_io(const KArgs &a) {
     return io;
 }
 /* persistent loop of one group (a warp or a CTA) over the tiles of its size class */
-template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const TileP &P, const KArgs &a, uint32_t group) {
+template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const TileP &P, const KArgs &a, uint32_t group, Rec *tmp = nullptr) {
     const unsigned long long t_begin = now();
     if (g.rank == 0) {
         FS &s = T.fs;
@@ -611,6 +611,7 @@ template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const Ti
     tg.stage = (Stage *)scr;
     tg.ev = (cl_event *)(scr + ((sizeof(Stage) * C::S + 255) & ~(size_t)255));
     tg.mem = a.o_mem;
+    tg.tmp = tmp;
     const TileIO io = tile_io(a);
     for (;;) {
         uint32_t w = 0;
@@ -649,6 +650,20 @@ template <class C, int WARPS, int MINB> __global__ void __launch_bounds__(WARPS 
     }
     Grp<1> g; g.rank = threadIdx.x & 31u; g.size = 32; g.red = nullptr;
     tile_loop(g, T, P, a, blockIdx.x * WARPS + w);
+}
+/* big tiles resident in L2 (global scratch): a CTA is one group; scratch = stages, events, the tile, a second stream buffer */
+template <class C> CLHD size_t gtile_scratch_bytes() {
+    return tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255) + ((sizeof(Rec) * C::I + 255) & ~(size_t)255);
+}
+template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, MINB) k_postssa_gtile(KArgs a) {
+    __shared__ TileP P;
+    uint8_t *base = a.tile_scratch + (size_t)blockIdx.x * a.tile_scratch_per_cta;
+    TileS<C> &T = *(TileS<C> *)(base + tile_scratch_bytes<C>());
+    Grp<NW> g; g.rank = threadIdx.x; g.size = NW * 32; g.red = T.red;
+    __shared__ uint32_t red[40];
+    g.red = red;
+    t_setup(g, P, a.pb);
+    tile_loop(g, T, P, a, blockIdx.x, (Rec *)(base + tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255)));
 }
 /* experiment: the same warp tiles with the tile state in L2-resident scratch instead of shared
  * memory (more warps in flight, longer access latency)                                       */
@@ -790,7 +805,7 @@ enum {
     B_O_HDR, B_O_TAG, B_O_PAY, B_O_IMM, B_O_ALIVE, B_O_DEF_IID, B_O_ORIGIN, B_O_EXT_TAG, B_O_EXT_PAY, B_O_MEM,
     B_O_BLK, B_O_BLK_START, B_O_BLK_CNT, B_O_EV, B_O_FUNC,
     B_LIST0, B_LIST1, B_LIST2, B_COUNTER0, B_COUNTER1, B_COUNTER2, B_SCRATCH0, B_SCRATCH1, B_SCRATCH2,
-    B_RETRY_LIST, B_RETRY_WORDS, B_TILES0, B_TILES1, B_TILE_COUNTER0, B_TILE_COUNTER1, B_TILE_SCRATCH0, B_TILE_SCRATCH1, B_TILE_FLIST, B_REST_LIST,
+    B_RETRY_LIST, B_RETRY_WORDS, B_TILES0, B_TILES1, B_TILES2, B_TILE_COUNTER0, B_TILE_COUNTER1, B_TILE_COUNTER2, B_TILE_SCRATCH0, B_TILE_SCRATCH1, B_TILE_SCRATCH2, B_TILE_FLIST, B_REST_LIST,
     B_D_OFF, B_D_SUMS, B_D_HDR, B_D_TAG, B_D_PAY, B_D_IMM, B_D_ALIVE, B_D_DEF_IID, B_D_ORIGIN, B_D_EV,
     B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B_SR_MAP, B__N
 };
@@ -820,7 +835,8 @@ struct cl_ctx {
     uint32_t *d_retry_list = nullptr, *d_retry_count = nullptr, *d_retry_counter = nullptr;
     /* tile kernels (tile.cuh): small functions packed into shared-memory tiles, in two size classes:
      * [0] warp tiles (one warp per tile), [1] CTA tiles                                        */
-    int tile_mode = 3;         /* bit 0: warp tiles, bit 1: CTA tiles; 0 = general kernels only */
+    int tile_mode = -1;        /* bit 0: warp tiles (smem), bit 1: CTA tiles (smem), bit 2: big CTA tiles (L2); 0 = general kernels only;
+                                  -1 = by corpus size: big tiles when they keep every SM busy, else shared-memory CTA tiles */
     int tile_warps = 16;       /* warps of a CTA-tile group */
     int wtile_warps = 6;       /* warp tiles (= warps) per CTA */
     int wtile_global = 0;      /* experiment: > 0 = warp tiles resident in global scratch, this many CTAs of 8 warps per SM */
@@ -828,7 +844,9 @@ struct cl_ctx {
         std::vector<TileDesc> tiles;
         TileDesc *d_tiles = nullptr; uint32_t *d_counter = nullptr; uint8_t *d_scratch = nullptr;
         size_t scratch_per_group = 0; uint32_t grid = 0, groups = 0;
-    } tc[2];
+    } tc[3];                   /* [2]: big CTA tiles resident in L2 (global scratch) */
+    int gtile_warps = 32, gtile_ctas = 1, gtile_cfg = -1;    /* cfg 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
+    int tile_mode_env = -1, gtile_cfg_env = -1;
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest;          /* small functions that are not in a tile */
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr;
@@ -884,7 +902,10 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_THREAD_MAX")) c->thread_max = CL_CUDA ? (uint32_t)atoi(e) : 0;
     if (const char *e = getenv("CL_WARP_SYNC")) { const int v = atoi(e); c->warp_sync = (v == 0 || v == 8 || v == 16 || v == 32 || v == 33) ? v : 32; }
     if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
-    if (const char *e = getenv("CL_TILE")) c->tile_mode = atoi(e) & 3;
+    if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 7;
+    if (const char *e = getenv("CL_GTILE_WARPS")) { const int v = atoi(e); c->gtile_warps = (v == 8 || v == 32) ? v : 16; }
+    if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(2, std::max(0, atoi(e)));
+    if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(4, std::max(1, atoi(e)));
     if (const char *e = getenv("CL_TILE_WARPS")) { const int v = atoi(e); c->tile_warps = (v == 8 || v == 32) ? v : 16; }
     if (const char *e = getenv("CL_WTILE_GLOBAL")) c->wtile_global = std::min(8, std::max(0, atoi(e)));
     if (const char *e = getenv("CL_WTILE_WARPS")) c->wtile_warps = std::min(6, std::max(1, atoi(e)));
@@ -1057,7 +1078,29 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     c->tile_flist.clear(); c->rest.clear(); c->n_tile_funcs = 0;
     {
         struct Need { uint32_t I, V, Q, B, f; };
-        std::vector<Need> cls[2];
+        /* tile size by corpus size: the bigger the tile the better the passes amortise (profiles/r01_tuning.md),
+         * as long as there are a few tiles per SM                                                              */
+        {
+            uint64_t n_small = 0;
+            for (uint32_t f = 0; f < F; f++) {
+                const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
+                if (n <= c->small_max && n > c->thread_max) n_small += n;
+            }
+            int n_sm = 148;
+#if CL_CUDA
+            n_sm = c->n_sm;
+#endif
+            const uint64_t per_sm = n_small / (uint64_t)n_sm;
+            c->gtile_cfg = per_sm >= 3 * 9800 ? 2 : per_sm >= 3 * 4900 ? 1 : 0;
+            c->tile_mode = per_sm >= 3 * 2450 ? 4 : 2;
+            if (c->gtile_cfg_env >= 0) c->gtile_cfg = c->gtile_cfg_env;
+            if (c->tile_mode_env >= 0) c->tile_mode = c->tile_mode_env;
+        }
+        const int gc = c->gtile_cfg;
+        const uint32_t gI = gc == 2 ? TileCfgG3::I : gc == 1 ? TileCfgG2::I : TileCfgG::I, gV = gc == 2 ? TileCfgG3::V : gc == 1 ? TileCfgG2::V : TileCfgG::V,
+                       gQ = gc == 2 ? TileCfgG3::Q : gc == 1 ? TileCfgG2::Q : TileCfgG::Q, gB = gc == 2 ? TileCfgG3::B : gc == 1 ? TileCfgG2::B : TileCfgG::B,
+                       gF = gc == 2 ? TileCfgG3::F : gc == 1 ? TileCfgG2::F : TileCfgG::F;
+        std::vector<Need> cls[3];
         for (uint32_t f = 0; f < F; f++) {
             const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
             const uint32_t n = in->blk_off[b1] - in->blk_off[b0], nb = b1 - b0;
@@ -1067,11 +1110,13 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             const bool plain = in->ext_off[f + 1] == in->ext_off[f] && nb > 0;
             if (plain && (c->tile_mode & 1) && nd.I <= TileCfgW::I && nd.V <= TileCfgW::V && nd.Q <= TileCfgW::Q && nd.B <= TileCfgW::B) cls[0].push_back(nd);
             else if (plain && (c->tile_mode & 2) && nd.I <= TileCfgL::I && nd.V <= TileCfgL::V && nd.Q <= TileCfgL::Q && nd.B <= TileCfgL::B) cls[1].push_back(nd);
+            else if (plain && (c->tile_mode & 4) && nd.I <= gI && nd.V <= gV && nd.Q <= gQ && nd.B <= gB) cls[2].push_back(nd);
             else c->rest.push_back(f);
         }
-        const uint32_t capI[2] = { TileCfgW::I, TileCfgL::I }, capV[2] = { TileCfgW::V, TileCfgL::V }, capQ[2] = { TileCfgW::Q, TileCfgL::Q },
-                       capB[2] = { TileCfgW::B, TileCfgL::B }, capF[2] = { TileCfgW::F, TileCfgL::F };
-        for (int k = 0; k < 2; k++) {
+        const uint32_t capI[3] = { TileCfgW::I, TileCfgL::I, gI }, capV[3] = { TileCfgW::V, TileCfgL::V, gV },
+                       capQ[3] = { TileCfgW::Q, TileCfgL::Q, gQ }, capB[3] = { TileCfgW::B, TileCfgL::B, gB },
+                       capF[3] = { TileCfgW::F, TileCfgL::F, gF };
+        for (int k = 0; k < 3; k++) {
             std::stable_sort(cls[k].begin(), cls[k].end(), [](const Need &x, const Need &y) { return x.I > y.I; });    /* long poles first */
             TileDesc cur = { (uint32_t)c->tile_flist.size(), 0 };
             uint32_t sI = 0, sV = 0, sQ = 0, sB = 0;
@@ -1092,8 +1137,9 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         c->d_retry_count = words; c->d_retry_counter = words + 1;
     }
     if (c->n_tile_funcs) {
-        static const int T_ID[2] = { B_TILES0, B_TILES1 }, C_ID[2] = { B_TILE_COUNTER0, B_TILE_COUNTER1 }, S_ID[2] = { B_TILE_SCRATCH0, B_TILE_SCRATCH1 };
-        for (int k = 0; k < 2; k++) {
+        static const int T_ID[3] = { B_TILES0, B_TILES1, B_TILES2 }, C_ID[3] = { B_TILE_COUNTER0, B_TILE_COUNTER1, B_TILE_COUNTER2 },
+                         S_ID[3] = { B_TILE_SCRATCH0, B_TILE_SCRATCH1, B_TILE_SCRATCH2 };
+        for (int k = 0; k < 3; k++) {
             cl_ctx::TileClass &t = c->tc[k];
             if (t.tiles.empty()) continue;
 #if CL_CUDA
@@ -1105,13 +1151,17 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
                 t.scratch_per_group = tile_scratch_bytes<TileCfgW>();
                 t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, (t.tiles.size() + c->wtile_warps - 1) / c->wtile_warps);
                 t.groups = t.grid * c->wtile_warps;
-            } else {
+            } else if (k == 1) {
                 t.scratch_per_group = tile_scratch_bytes<TileCfgL>();
                 t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, t.tiles.size());
                 t.groups = t.grid;
+            } else {
+                t.scratch_per_group = c->gtile_cfg == 2 ? gtile_scratch_bytes<TileCfgG3>() : c->gtile_cfg == 1 ? gtile_scratch_bytes<TileCfgG2>() : gtile_scratch_bytes<TileCfgG>();
+                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->gtile_ctas, t.tiles.size());
+                t.groups = t.grid;
             }
 #else
-            t.scratch_per_group = k == 0 ? tile_scratch_bytes<TileCfgW>() : tile_scratch_bytes<TileCfgL>();
+            t.scratch_per_group = k == 0 ? tile_scratch_bytes<TileCfgW>() : k == 1 ? tile_scratch_bytes<TileCfgL>() : tile_scratch_bytes<TileCfgG3>();
             t.grid = t.groups = 1;
 #endif
             if (dput(c, T_ID[k], &t.d_tiles, t.tiles.data(), t.tiles.size())) return -1;
@@ -1222,7 +1272,7 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     k.tile_scratch = t.d_scratch; k.tile_scratch_per_cta = t.scratch_per_group; k.tile_flist = c->d_tile_flist;
     k.retry_list = c->d_retry_list; k.retry_count = c->d_retry_count;
 #if CL_CUDA
-    cudaStream_t st = cls == 0 ? c->stream : c->stream2;
+    cudaStream_t st = cls == 1 ? c->stream2 : c->stream;
     if (dzero(k.tile_counter, sizeof(uint32_t), st)) return -1;
     if (cls == 0 && c->wtile_global) {
         switch (c->wtile_global) {
@@ -1248,6 +1298,26 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
         default: return launch_wtile_kernel<TileCfgW, 8>(c, k, t.grid, st);
         }
     }
+    if (cls == 2 && c->gtile_cfg == 2) {
+        if (c->gtile_warps == 32) k_postssa_gtile<TileCfgG3, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        else k_postssa_gtile<TileCfgG3, 16, 2><<<t.grid, 512, 0, st>>>(k);
+        CUDA_OK(cudaGetLastError());
+        return 0;
+    }
+    if (cls == 2 && c->gtile_cfg == 1) {
+        if (c->gtile_warps == 32) k_postssa_gtile<TileCfgG2, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        else if (c->gtile_warps == 8) k_postssa_gtile<TileCfgG2, 8, 4><<<t.grid, 256, 0, st>>>(k);
+        else k_postssa_gtile<TileCfgG2, 16, 2><<<t.grid, 512, 0, st>>>(k);
+        CUDA_OK(cudaGetLastError());
+        return 0;
+    }
+    if (cls == 2) {
+        if (c->gtile_warps == 32) k_postssa_gtile<TileCfgG, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        else if (c->gtile_warps == 8) k_postssa_gtile<TileCfgG, 8, 4><<<t.grid, 256, 0, st>>>(k);
+        else k_postssa_gtile<TileCfgG, 16, 2><<<t.grid, 512, 0, st>>>(k);
+        CUDA_OK(cudaGetLastError());
+        return 0;
+    }
     if (c->tile_warps == 32) return launch_tile_kernel<TileCfgL, 32, 1>(c, k, t.grid, st);
     if (c->tile_warps == 8) return launch_tile_kernel<TileCfgL, 8, 1>(c, k, t.grid, st);
     return launch_tile_kernel<TileCfgL, 16, 1>(c, k, t.grid, st);
@@ -1257,7 +1327,10 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     Grp<0> g; g.rank = 0; g.size = 1; g.red = nullptr;
     t_setup(g, P, k.pb);
     if (cls == 0) { static TileS<TileCfgW> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
-    else { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    else if (cls == 1) { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    else { static TileS<TileCfgG> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
     return 0;
 #endif
 }
@@ -1285,6 +1358,7 @@ static int run(cl_ctx *c, KArgs k) {
     if (launch_part(c, 1, k, 0, true)) return -1;
     if (use_tiles) {
         if (launch_tiles(c, k, 1)) return -1;    /* CTA tiles: side stream, after the large functions */
+        if (launch_tiles(c, k, 2)) return -1;    /* big L2-resident tiles */
         if (launch_tiles(c, k, 0)) return -1;    /* warp tiles */
         if (launch_part(c, 0, k, 2)) return -1;  /* small functions outside the tiles */
 #if CL_CUDA
@@ -1445,7 +1519,7 @@ extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
 /* debugging aid: how the last run was partitioned: {tiles, functions in tiles, functions the tile kernel
  * handed back to the general kernel, small functions outside tiles, tile kernel used}            */
 extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
-    out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles;
+    out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size() + c->tc[2].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles;
     return 0;
 }
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }

@@ -50,6 +50,11 @@ struct TPat {
 /* capacities of one tile (compile time: the tile lives in shared memory) */
 struct TileCfgL { static constexpr uint32_t I = 1024, V = 1792, Q = 320, F = 32, B = 96, M = 1024, S = 512, X = 256, E = 512; };
 struct TileCfgS { static constexpr uint32_t I = 576, V = 1024, Q = 192, F = 24, B = 64, M = 512, S = 288, X = 128, E = 256; };
+/* a big tile resident in L2 (global scratch) instead of shared memory: every pass loops many times over
+ * the same code, which is what the instruction cache needs (profiles/r01_tuning.md)          */
+struct TileCfgG { static constexpr uint32_t I = 4096, V = 7168, Q = 1280, F = 128, B = 255, M = 4096, S = 2048, X = 512, E = 2048; };
+struct TileCfgG2 { static constexpr uint32_t I = 8192, V = 14336, Q = 2560, F = 255, B = 255, M = 8192, S = 4096, X = 1024, E = 4096; };
+struct TileCfgG3 { static constexpr uint32_t I = 16384, V = 28672, Q = 5120, F = 255, B = 255, M = 16384, S = 8192, X = 2048, E = 8192; };
 struct TileCfgW { static constexpr uint32_t I = 192, V = 352, Q = 64, F = 3, B = 16, M = 192, S = 96, X = 32, E = 64; };   /* one warp */
 
 /* the pattern table and what t_setup derives from it: shared by the tiles of a CTA */
@@ -101,6 +106,7 @@ template <class C> struct TileG {      /* what lives outside shared memory */
     Stage *stage;             /* [C::S] staged rewrites (L2-resident scratch)   */
     cl_event *ev;             /* [C::E]                                          */
     cl_memref *mem;           /* memrefs of the tile: mutable copy in the output  */
+    Rec *tmp;                 /* [C::I] second stream buffer of tiles too big to permute in registers, else null */
 };
 
 template <class C> CLD bool tf_ok(const TileS<C> &T, uint32_t f) { return *(volatile const uint32_t *)&T.f_stat[f] == 0; }
@@ -158,13 +164,37 @@ template <class G, class C> CLF void t_index(const G &g, TileS<C> &T) {
 
 /* in-place permutation of the stream: record i moves to dst(i) (NONE32 = dropped).
  * Everything is read before anything is written.                              */
-template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T, uint32_t n, F dst) {
+template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T, const TileG<C> &tg, uint32_t n, uint32_t n_new, F dst) {
 #if CL_DEV
     constexpr int K = (int)((C::I + G::THREADS - 1) / G::THREADS);
-    uint4 r[K][4];
-    uint32_t d[K];
+    if (K > 2) {
+        /* through the second buffer: scatter, then copy back */
+        GFOR(g, i, n) if (i < n) {
+            const uint32_t d = dst(i);
+            if (d != NONE32) {
+                uint4 *o = (uint4 *)&tg.tmp[d];
+                o[0] = *(const uint4 *)&T.hdr[i];
+                o[1] = *(const uint4 *)&T.tag[(size_t)i * 8];
+                o[2] = ((const uint4 *)&T.pay[(size_t)i * 8])[0];
+                o[3] = ((const uint4 *)&T.pay[(size_t)i * 8])[1];
+            }
+        }
+        g.sync();
+        GFOR(g, i, n_new) if (i < n_new) {
+            const uint4 *r = (const uint4 *)&tg.tmp[i];
+            *(uint4 *)&T.hdr[i] = r[0];
+            *(uint4 *)&T.tag[(size_t)i * 8] = r[1];
+            ((uint4 *)&T.pay[(size_t)i * 8])[0] = r[2];
+            ((uint4 *)&T.pay[(size_t)i * 8])[1] = r[3];
+        }
+        g.sync();
+        return;
+    }
+    constexpr int KR = K > 2 ? 1 : K;
+    uint4 r[KR][4];
+    uint32_t d[KR];
 #pragma unroll
-    for (int k = 0; k < K; k++) {
+    for (int k = 0; k < KR; k++) {
         const uint32_t i = (uint32_t)k * g.size + g.rank;
         d[k] = i < n ? dst(i) : NONE32;
         if (d[k] != NONE32) {
@@ -176,7 +206,7 @@ template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T,
     }
     g.sync();
 #pragma unroll
-    for (int k = 0; k < K; k++)
+    for (int k = 0; k < KR; k++)
         if (d[k] != NONE32) {
             const uint32_t o = d[k];
             *(uint4 *)&T.hdr[o] = r[k][0];
@@ -194,7 +224,7 @@ template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T,
     }
     for (uint32_t i = 0; i < n; i++)
         if (d[i] != NONE32) { T.hdr[d[i]] = tmp[i].h; memcpy(&T.tag[(size_t)d[i] * 8], tmp[i].tag, 16); memcpy(&T.pay[(size_t)d[i] * 8], tmp[i].pay, 32); }
-    (void)g;
+    (void)g; (void)tg; (void)n_new;
 #endif
 }
 
@@ -399,24 +429,46 @@ template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const Tile
     GFOR(g, k, T.nb * MAX_CLS) if (k < T.nb * MAX_CLS) (&T.ccnt[0][0])[k] = 0;
     if (g.rank == 0) T.n_mt = 0;
     g.sync();
-    GFOR(g, i, T.n) if (i < T.n) {
-        int c = -1;
-        if (T.f_gate[T.fidx[i]]) {
-            c = t_class_of(T, table, T.hdr[i].op);
-            if (c >= 0) a_add(&T.ccnt[T.bidx[i]][c], 1u);
+    /* seed classes (FindSeeds) and the dense list of (anchor, pattern) work items, in stream order */
+    uint32_t *items = (uint32_t *)T.owner;                   /* [2 * C::I]: free until t_select */
+    uint32_t n_items = 0;
+    GFOR(g, i, T.n) {
+        uint32_t pm = 0;
+        if (i < T.n) {
+            int c = -1;
+            const uint32_t f = T.fidx[i];
+            if (T.f_gate[f]) {
+                c = t_class_of(T, table, T.hdr[i].op);
+                if (c >= 0) {
+                    a_add(&T.ccnt[T.bidx[i]][c], 1u);
+                    if (tf_ok(T, f)) {
+                        pm = T.P->anchor_mask[table][c];
+                        if (pm && T.f_odd[f]) { tf_fail(T, f, CL_ST_REDO); pm = 0; }
+                    }
+                }
+            }
+            T.clsid[i] = (uint8_t)c;
         }
-        T.clsid[i] = (uint8_t)c;
+        uint32_t tot;
+#if CL_DEV
+        const uint32_t off = g.exscan((uint32_t)__popc(pm), tot);
+#else
+        uint32_t cnt = 0; for (uint32_t q = pm; q; q &= q - 1) cnt++;
+        const uint32_t off = g.exscan(cnt, tot);
+#endif
+        if (n_items + tot <= 2 * C::I) {
+            uint32_t w = n_items + off;
+            for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) items[w++] = i | pi << 16;
+        } else if (g.rank == 0)
+            T.fail = 1;
+        n_items += tot;
     }
     g.sync();
-    GFOR(g, i, T.n) if (i < T.n) {
-        const unsigned c = T.clsid[i];
-        if (c == 0xFFu) continue;
-        uint32_t pm = T.P->anchor_mask[table][c];
-        if (!pm) continue;
+    if (T.fail) return;
+    GFOR(g, k, n_items) if (k < n_items) {
+        const uint32_t it = items[k], i = it & 0xFFFFu;
         const uint32_t f = T.fidx[i];
-        if (!tf_ok(T, f)) continue;
-        if (T.f_odd[f]) { tf_fail(T, f, CL_ST_REDO); continue; }
-        for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) t_try_anchor(T, tg, table, i, pi, f);
+        if (tf_ok(T, f)) t_try_anchor(T, tg, table, i, it >> 16, f);
     }
     g.sync();
 }
@@ -617,7 +669,7 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     if (tot > C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
     g.sync();
     PROF(g, T.fs, PF_EMIT);
-    t_permute(g, T, n, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] + T.inscnt[p] : NONE32; });
+    t_permute(g, T, tg, n, tot, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] + T.inscnt[p] : NONE32; });
     /* staged records to their place, value table, immediates */
     GFOR(g, j, ns) if (j < ns) {
         const SelRec m = T.sel[j];
@@ -630,12 +682,12 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
 }
 
 /* ordered in-place compaction of the stream by keep[]                         */
-template <class G, class C> CLF void t_compact(const G &g, TileS<C> &T) {
+template <class G, class C> CLF void t_compact(const G &g, TileS<C> &T, const TileG<C> &tg) {
     const uint32_t n = T.n;
     const uint32_t tot = t_scan(g, n, [&](uint32_t p) { return (uint32_t)T.keep[p]; },
                                 [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
     g.sync();
-    t_permute(g, T, n, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] : NONE32; });
+    t_permute(g, T, tg, n, tot, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] : NONE32; });
     t_rebase_blocks(g, T, n, tot);
     t_index(g, T);
 }
@@ -667,7 +719,7 @@ template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<
         if (!dead) break;
         removed += dead;
     }
-    if (removed) t_compact(g, T);
+    if (removed) t_compact(g, T, tg);
 }
 
 /* simplify_packs + _redirect_values (patterns.py:710-764) for the gated functions;
@@ -933,7 +985,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
                                 [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
     if (tot > C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
     g.sync();
-    t_permute(g, T, n, [&](uint32_t p) { return (uint32_t)T.outpos[p] + T.keep[p]; });
+    t_permute(g, T, tg, n, tot, [&](uint32_t p) { return (uint32_t)T.outpos[p] + T.keep[p]; });
     GFOR(g, c, nc) if (c < nc) {
         const TChain ch = T.chain[c];
         const uint32_t f = ch.f;
