@@ -218,6 +218,7 @@ def main():
         fence()
         wall = time.perf_counter() - t1
     st = eng.stats()
+    part = eng.debug_partition() or {}
     if os.environ.get("CL_PROF") and rank == 0:
         prof = eng.debug_profile()
         tot = max(prof.get("total", 1), 1)
@@ -241,7 +242,9 @@ def main():
     achieved = bytes_per_step / (np.mean(dev_ms) / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "kernel": "k_postssa_warp + k_postssa_cta (the whole stage, rank 0)",
+                "kernel": "k_postssa_gtile (tile kernel: small kernels packed into L2-resident tiles) with k_postssa_cta "
+                          "(long-block kernels) beside it and k_postssa_warp_sync for what the tile kernel hands back: "
+                          "the whole stage, rank 0",
                 "algorithmic_bytes_per_launch": bytes_per_step,
                 "bytes_per_sass_inst": bytes_per_step / max(n_sass_rank, 1)}
 
@@ -303,7 +306,8 @@ def main():
                        "corpus": "kernels drawn with replacement from reference-front-half pools (tests/golden/pool_*.npz)",
                        "gen_seconds": round(t_gen, 1), "wall_ms_per_step": t_wall_s / args.steps * 1e3},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": int(part.get("launches", 0)) * args.steps,
+            "partition": part,
             "match_counts": {"selected": int(n_sel), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())},
         }
         print(json.dumps(line))

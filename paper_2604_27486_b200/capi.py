@@ -207,10 +207,11 @@ class Engine:
         """{tiles, tile_funcs, handed_back, outside, used_tiles} of the last run (CUDA / sim builds only)."""
         if not hasattr(self.lib, "cl_debug_partition"):
             return None
-        out = (C.c_uint64 * 5)()
+        out = (C.c_uint64 * 8)()
         self.lib.cl_debug_partition.argtypes = [C.c_void_p, C.c_void_p]
         self.lib.cl_debug_partition(self._ctx, out)
-        return dict(zip(("tiles", "tile_funcs", "handed_back", "outside", "used_tiles"), (int(x) for x in out)))
+        return dict(zip(("tiles", "tile_funcs", "handed_back", "outside", "used_tiles", "launches", "tile_mode", "tile_cfg"),
+                        (int(x) for x in out)))
 
     def device_counts_ptr(self):
         return self.lib.cl_device_counts_ptr(self._ctx)

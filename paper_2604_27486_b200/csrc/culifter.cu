@@ -850,7 +850,7 @@ struct cl_ctx {
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest;          /* small functions that are not in a tile */
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr;
-    uint32_t n_tile_funcs = 0, h_retry = 0; bool used_tiles = false;
+    uint32_t n_tile_funcs = 0, h_retry = 0, n_launches = 0; bool used_tiles = false;
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
     int cta_warps = 8;         /* warps per CTA of the CTA-group kernel (8, 16 or 32) */        /* warps per CTA of the phase-synchronous warp kernel (0 = free-running kernel) */
@@ -1217,6 +1217,7 @@ static int launch_part(cl_ctx *c, int which, KArgs k, int mode = 0, bool side = 
     k.retry_count = which == 2 ? c->d_retry_count : nullptr;
     k.scratch = p.d_scratch; k.scratch_per_group = p.scratch_per_group; k.gcap = p.cap; k.hot_bytes = p.hot_bytes;
     if (dzero(k.work_counter, sizeof(uint32_t), st)) return -1;
+    c->n_launches++;
 #if CL_CUDA
     if (which == 0 && c->warp_sync) {
         switch (c->warp_sync) {
@@ -1271,6 +1272,7 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     k.tiles = t.d_tiles; k.n_tiles = (uint32_t)t.tiles.size(); k.tile_counter = t.d_counter;
     k.tile_scratch = t.d_scratch; k.tile_scratch_per_cta = t.scratch_per_group; k.tile_flist = c->d_tile_flist;
     k.retry_list = c->d_retry_list; k.retry_count = c->d_retry_count;
+    c->n_launches++;
 #if CL_CUDA
     cudaStream_t st = cls == 1 ? c->stream2 : c->stream;
     if (dzero(k.tile_counter, sizeof(uint32_t), st)) return -1;
@@ -1347,6 +1349,7 @@ static int run(cl_ctx *c, KArgs k) {
     /* the tile kernel takes the production run of the post-SSA stage; match lists
      * (emit_matches / MATCH_ONLY), the raw stage and tables with a pattern that has
      * no join plan go through the general kernels                                  */
+    c->n_launches = 0;
     bool use_tiles = c->n_tile_funcs && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
     for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_tiles = use_tiles && c->h_pb.p[pi].join_ok;
 #if CL_CUDA
@@ -1519,7 +1522,8 @@ extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
 /* debugging aid: how the last run was partitioned: {tiles, functions in tiles, functions the tile kernel
  * handed back to the general kernel, small functions outside tiles, tile kernel used}            */
 extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
-    out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size() + c->tc[2].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles;
+    out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size() + c->tc[2].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles; out[5] = c->n_launches;
+    out[6] = c->tile_mode; out[7] = c->gtile_cfg;
     return 0;
 }
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }
