@@ -101,6 +101,7 @@ struct KArgs {
     /* tile kernel (tile.cuh) */
     const TileDesc *tiles; uint32_t n_tiles; uint32_t *tile_counter;
     const uint32_t *tile_flist;
+    uint32_t *retry_big_list, *retry_big_count; uint32_t small_max;   /* hand-backs above small_max go to the CTA-group kernel */
     uint8_t *tile_scratch; unsigned long long tile_scratch_per_cta;   /* per group */
 };
 
@@ -585,6 +586,7 @@ CLHD TileIO tile_io(const KArgs &a) {
     for (int k = 0; k < 4; k++) io.cap[k] = a.cap[k];
     io.cursor = a.cursor; io.stats = a.stats;
     io.retry_list = a.retry_list; io.retry_count = a.retry_count;
+    io.retry_big_list = a.retry_big_list; io.retry_big_count = a.retry_big_count; io.small_max = a.small_max;
     io.flist = a.tile_flist;
     return io;
 }
@@ -805,7 +807,7 @@ enum {
     B_O_HDR, B_O_TAG, B_O_PAY, B_O_IMM, B_O_ALIVE, B_O_DEF_IID, B_O_ORIGIN, B_O_EXT_TAG, B_O_EXT_PAY, B_O_MEM,
     B_O_BLK, B_O_BLK_START, B_O_BLK_CNT, B_O_EV, B_O_FUNC,
     B_LIST0, B_LIST1, B_LIST2, B_COUNTER0, B_COUNTER1, B_COUNTER2, B_SCRATCH0, B_SCRATCH1, B_SCRATCH2,
-    B_RETRY_LIST, B_RETRY_WORDS, B_TILES0, B_TILES1, B_TILES2, B_TILE_COUNTER0, B_TILE_COUNTER1, B_TILE_COUNTER2, B_TILE_SCRATCH0, B_TILE_SCRATCH1, B_TILE_SCRATCH2, B_TILE_FLIST, B_REST_LIST,
+    B_RETRY_LIST, B_RETRY_WORDS, B_TILES0, B_TILES1, B_TILES2, B_TILE_COUNTER0, B_TILE_COUNTER1, B_TILE_COUNTER2, B_TILE_SCRATCH0, B_TILE_SCRATCH1, B_TILE_SCRATCH2, B_TILE_FLIST, B_REST_LIST, B_BIG_REST_LIST, B_RETRY_BIG,
     B_D_OFF, B_D_SUMS, B_D_HDR, B_D_TAG, B_D_PAY, B_D_IMM, B_D_ALIVE, B_D_DEF_IID, B_D_ORIGIN, B_D_EV,
     B_D_BLK_OFF, B_D_IMM_OFF, B_D_VAL_OFF, B_D_FUNC, B_SR_MAP, B__N
 };
@@ -847,9 +849,11 @@ struct cl_ctx {
     } tc[3];                   /* [2]: big CTA tiles resident in L2 (global scratch) */
     int gtile_warps = 32, gtile_ctas = 1, gtile_cfg = -1;    /* cfg 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
     int tile_mode_env = -1, gtile_cfg_env = -1;
+    int tile_long = 0;         /* 1: long-block kernels (above small_max records) also go into the big tiles (measured: no gain over the CTA-group kernel) */
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
-    std::vector<uint32_t> rest;          /* small functions that are not in a tile */
-    uint32_t *d_tile_flist = nullptr, *d_rest = nullptr;
+    std::vector<uint32_t> rest, big_rest; /* small / large functions that are not in a tile */
+    uint32_t *d_tile_flist = nullptr, *d_rest = nullptr, *d_big_rest = nullptr;
+    uint32_t *d_retry_big = nullptr, *d_retry_big_count = nullptr, *d_retry_big_counter = nullptr;   /* large functions the tile kernel hands back */
     uint32_t n_tile_funcs = 0, h_retry = 0, n_launches = 0; bool used_tiles = false;
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
@@ -904,6 +908,7 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 7;
     if (const char *e = getenv("CL_GTILE_WARPS")) { const int v = atoi(e); c->gtile_warps = (v == 8 || v == 32) ? v : 16; }
+    if (const char *e = getenv("CL_TILE_LONG")) c->tile_long = atoi(e) != 0;
     if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(2, std::max(0, atoi(e)));
     if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(4, std::max(1, atoi(e)));
     if (const char *e = getenv("CL_TILE_WARPS")) { const int v = atoi(e); c->tile_warps = (v == 8 || v == 32) ? v : 16; }
@@ -1084,7 +1089,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             uint64_t n_small = 0;
             for (uint32_t f = 0; f < F; f++) {
                 const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
-                if (n <= c->small_max && n > c->thread_max) n_small += n;
+                if (n > c->thread_max && (n <= c->small_max || (c->tile_long && tile_icap(n) <= TileCfgG3::I))) n_small += n;
             }
             int n_sm = 148;
 #if CL_CUDA
@@ -1101,17 +1106,20 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
                        gQ = gc == 2 ? TileCfgG3::Q : gc == 1 ? TileCfgG2::Q : TileCfgG::Q, gB = gc == 2 ? TileCfgG3::B : gc == 1 ? TileCfgG2::B : TileCfgG::B,
                        gF = gc == 2 ? TileCfgG3::F : gc == 1 ? TileCfgG2::F : TileCfgG::F;
         std::vector<Need> cls[3];
+        c->big_rest.clear();
         for (uint32_t f = 0; f < F; f++) {
             const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
             const uint32_t n = in->blk_off[b1] - in->blk_off[b0], nb = b1 - b0;
-            if (!(n <= c->small_max && n > c->thread_max)) continue;
+            if (n <= c->thread_max) continue;
+            const bool small = n <= c->small_max;
             const uint32_t nimm = in->imm_off[f + 1] - in->imm_off[f];
             const Need nd = { tile_icap(n), tile_vcap(in->func[f].next_vid, n), tile_qcap(nimm, n), nb, f };
             const bool plain = in->ext_off[f + 1] == in->ext_off[f] && nb > 0;
-            if (plain && (c->tile_mode & 1) && nd.I <= TileCfgW::I && nd.V <= TileCfgW::V && nd.Q <= TileCfgW::Q && nd.B <= TileCfgW::B) cls[0].push_back(nd);
-            else if (plain && (c->tile_mode & 2) && nd.I <= TileCfgL::I && nd.V <= TileCfgL::V && nd.Q <= TileCfgL::Q && nd.B <= TileCfgL::B) cls[1].push_back(nd);
-            else if (plain && (c->tile_mode & 4) && nd.I <= gI && nd.V <= gV && nd.Q <= gQ && nd.B <= gB) cls[2].push_back(nd);
-            else c->rest.push_back(f);
+            if (small && plain && (c->tile_mode & 1) && nd.I <= TileCfgW::I && nd.V <= TileCfgW::V && nd.Q <= TileCfgW::Q && nd.B <= TileCfgW::B) cls[0].push_back(nd);
+            else if (small && plain && (c->tile_mode & 2) && nd.I <= TileCfgL::I && nd.V <= TileCfgL::V && nd.Q <= TileCfgL::Q && nd.B <= TileCfgL::B) cls[1].push_back(nd);
+            else if (plain && (small || c->tile_long) && (c->tile_mode & 4) && nd.I <= gI && nd.V <= gV && nd.Q <= gQ && nd.B <= gB) cls[2].push_back(nd);   /* long-block kernels too */
+            else if (small) c->rest.push_back(f);
+            else c->big_rest.push_back(f);
         }
         const uint32_t capI[3] = { TileCfgW::I, TileCfgL::I, gI }, capV[3] = { TileCfgW::V, TileCfgL::V, gV },
                        capQ[3] = { TileCfgW::Q, TileCfgL::Q, gQ }, capB[3] = { TileCfgW::B, TileCfgL::B, gB },
@@ -1171,6 +1179,12 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         if (dput(c, B_TILE_FLIST, &c->d_tile_flist, c->tile_flist.data(), c->tile_flist.size())) return -1;
     }
     if (dput(c, B_REST_LIST, &c->d_rest, c->rest.data(), c->rest.size())) return -1;
+    if (dput(c, B_BIG_REST_LIST, &c->d_big_rest, c->big_rest.data(), c->big_rest.size())) return -1;
+    {
+        uint32_t *w = nullptr;
+        if (dget(c, B_RETRY_BIG, &w, (size_t)c->part[1].list.size() + 4)) return -1;
+        c->d_retry_big_count = w; c->d_retry_big_counter = w + 1; c->d_retry_big = w + 4;
+    }
 
     /* result buffers (worst-case growth, G3/G4) */
     KArgs &k = c->k;
@@ -1206,15 +1220,20 @@ static int launch_part(cl_ctx *c, int which, KArgs k, int mode = 0, bool side = 
     cudaStream_t st = c->stream; (void)side;
 #endif
     Part &p = c->part[which];
-    const bool retry = mode == 1;
+    const bool retry = mode == 1 || mode == 3;
     if (mode == 0 && p.list.empty()) return 0;
     if (mode == 2 && c->rest.empty()) return 0;
-    k.list = retry ? c->d_retry_list : mode == 2 ? c->d_rest : p.d_list;
-    k.n_list = retry ? (uint32_t)std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs) : mode == 2 ? (uint32_t)c->rest.size() : (uint32_t)p.list.size();
-    k.n_list_ptr = retry ? c->d_retry_count : nullptr;
-    k.work_counter = retry ? c->d_retry_counter : p.d_counter;
+    if (mode == 4 && c->big_rest.empty()) return 0;
+    if (mode == 3 && p.list.empty()) return 0;             /* no large function at all */
+    if (mode == 1 && p.grid == 0) return 0;                /* no small function at all */
+    k.list = mode == 1 ? c->d_retry_list : mode == 3 ? c->d_retry_big : mode == 2 ? c->d_rest : mode == 4 ? c->d_big_rest : p.d_list;
+    k.n_list = mode == 1 ? (uint32_t)std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs) : mode == 3 ? (uint32_t)p.list.size()
+             : mode == 2 ? (uint32_t)c->rest.size() : mode == 4 ? (uint32_t)c->big_rest.size() : (uint32_t)p.list.size();
+    k.n_list_ptr = mode == 1 ? c->d_retry_count : mode == 3 ? c->d_retry_big_count : nullptr;
+    k.work_counter = mode == 1 ? c->d_retry_counter : mode == 3 ? c->d_retry_big_counter : p.d_counter;
     k.retry_list = which == 2 ? c->d_retry_list : nullptr;
     k.retry_count = which == 2 ? c->d_retry_count : nullptr;
+    (void)retry;
     k.scratch = p.d_scratch; k.scratch_per_group = p.scratch_per_group; k.gcap = p.cap; k.hot_bytes = p.hot_bytes;
     if (dzero(k.work_counter, sizeof(uint32_t), st)) return -1;
     c->n_launches++;
@@ -1272,6 +1291,7 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     k.tiles = t.d_tiles; k.n_tiles = (uint32_t)t.tiles.size(); k.tile_counter = t.d_counter;
     k.tile_scratch = t.d_scratch; k.tile_scratch_per_cta = t.scratch_per_group; k.tile_flist = c->d_tile_flist;
     k.retry_list = c->d_retry_list; k.retry_count = c->d_retry_count;
+    k.retry_big_list = c->d_retry_big; k.retry_big_count = c->d_retry_big_count; k.small_max = c->small_max;
     c->n_launches++;
 #if CL_CUDA
     cudaStream_t st = cls == 1 ? c->stream2 : c->stream;
@@ -1358,8 +1378,9 @@ static int run(cl_ctx *c, KArgs k) {
     CUDA_OK(cudaEventRecord(c->ev_fork, c->stream));
     CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
 #endif
-    if (launch_part(c, 1, k, 0, true)) return -1;
+    if (c->d_retry_big_count && dzero(c->d_retry_big_count, sizeof(uint32_t), c->stream)) return -1;
     if (use_tiles) {
+        if (launch_part(c, 1, k, 4, true)) return -1;     /* large functions outside the tiles: side stream */
         if (launch_tiles(c, k, 1)) return -1;    /* CTA tiles: side stream, after the large functions */
         if (launch_tiles(c, k, 2)) return -1;    /* big L2-resident tiles */
         if (launch_tiles(c, k, 0)) return -1;    /* warp tiles */
@@ -1369,7 +1390,9 @@ static int run(cl_ctx *c, KArgs k) {
         CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
 #endif
         if (launch_part(c, 0, k, 1)) return -1;  /* what the tile kernels handed back */
+        if (launch_part(c, 1, k, 3)) return -1;
     } else {
+        if (launch_part(c, 1, k, 0, true)) return -1;
         if (launch_part(c, 2, k)) return -1;
         if (launch_part(c, 0, k)) return -1;
         if (!c->part[2].list.empty() && launch_part(c, 0, k, 1)) return -1; /* what outgrew the thread kernel */
@@ -1384,10 +1407,13 @@ static int run(cl_ctx *c, KArgs k) {
     if (d2h(c->h_prof, c->d_prof, sizeof c->h_prof, c->stream)) return -1;
     c->h_retry = 0; c->used_tiles = use_tiles;
     if (c->d_retry_count && d2h(&c->h_retry, c->d_retry_count, sizeof(uint32_t), c->stream)) return -1;
+    uint32_t h_retry_big = 0;
+    if (c->d_retry_big_count && d2h(&h_retry_big, c->d_retry_big_count, sizeof(uint32_t), c->stream)) return -1;
 #if CL_CUDA
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
 #endif
+    c->h_retry += h_retry_big;
     c->have_out = true;
     return 0;
 }

@@ -29,6 +29,10 @@
  */
 #pragma once
 #include "core.cuh"
+#if !CL_DEV
+#include <stdio.h>
+#include <stdlib.h>
+#endif
 
 namespace clk {
 
@@ -85,6 +89,8 @@ template <class C> struct TileS {
     uint32_t bo[C::B + 1], bo2[C::B + 1], b_first[C::B];
     cl_blk blk[C::B];
     uint32_t ccnt[C::B][MAX_CLS];
+    uint32_t cbase[C::B][MAX_CLS];          /* over-budget blocks: members of the class before the block (tile wide count) */
+    uint16_t b_over[C::B];                  /* classes of the block whose product order must be computed exactly */
     uint8_t bfun[C::B];
     /* functions: slices of the tile-wide value / immediate / memref index spaces */
     uint32_t f_vbase[C::F + 1], f_qbase[C::F + 1], f_mbase[C::F + 1];
@@ -386,7 +392,7 @@ template <class C> CLF void t_try_anchor(TileS<C> &T, const TileG<C> &tg, unsign
         const opnd o = t_slot(T, idx[from], has_guard(hf) + p.join_slot[k]);
         if (!is_value(o)) {
             const unsigned ko = kind_of(o.tag);       /* a non-SSA link: the literal product decides */
-            if (ko == CL_K_RZ || ko == CL_K_URZ || ko == CL_K_PRED) tf_fail(T, f, CL_ST_REDO);
+            if (ko == CL_K_RZ || ko == CL_K_URZ || ko == CL_K_PRED) tf_fail(T, f, CL_ST_REDO + 1);
             return;
         }
         const uint32_t dp = o.pay < C::V ? T.defpos[o.pay] : NONE32;
@@ -404,8 +410,7 @@ template <class C> CLF void t_try_anchor(TileS<C> &T, const TileG<C> &tg, unsign
         if (prod > T.P->pb.budget) {
             unsigned long long r = 0;
             for (unsigned t = 0; t < nt; t++) {
-                uint32_t ci = 0;
-                for (uint32_t j = lo; j < idx[t]; j++) ci += T.clsid[j] == (uint8_t)cl[t];
+                const uint32_t ci = (uint32_t)T.outpos[idx[t]] - T.cbase[b][cl[t]];      /* index inside its candidate list (t_match) */
                 r = t == 0 ? ci : r * cn[t] + ci;
             }
             if (r >= T.P->pb.budget) return;
@@ -443,7 +448,7 @@ template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const Tile
                     a_add(&T.ccnt[T.bidx[i]][c], 1u);
                     if (tf_ok(T, f)) {
                         pm = T.P->anchor_mask[table][c];
-                        if (pm && T.f_odd[f]) { tf_fail(T, f, CL_ST_REDO); pm = 0; }
+                        if (pm && T.f_odd[f]) { tf_fail(T, f, CL_ST_REDO + 2); pm = 0; }
                     }
                 }
             }
@@ -465,6 +470,35 @@ template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const Tile
     }
     g.sync();
     if (T.fail) return;
+    /* budget (G1): where the product of the candidate-list sizes of a pattern exceeds it, a tuple counts only
+     * if its rank in itertools.product order is below it; the rank needs every member's index inside its
+     * candidate list = members of its class before it in the block: one tile-wide scan per class concerned */
+    {
+        uint32_t need = 0;
+        GFOR(g, b, T.nb) if (b < T.nb) {
+            uint32_t m = 0;
+            for (unsigned pi = 0; pi < T.P->pb.n_patterns; pi++) {
+                const cl_pattern &p = T.P->pb.p[pi];
+                if (p.table != table) continue;
+                unsigned long long prod = 1;
+                uint32_t cm = 0;
+                for (unsigned t = 0; t < p.n_templates; t++) { const int c = t_class_of(T, table, p.t[t].op); prod *= T.ccnt[b][c]; cm |= 1u << c; }
+                if (prod > T.P->pb.budget) m |= cm;
+            }
+            T.b_over[b] = (uint16_t)m;
+            need |= m;
+        }
+        for (unsigned c = 0; c < T.P->n_cls[table]; c++) {
+            if (!g.any((need >> c) & 1u)) continue;
+            t_scan(g, T.n, [&](uint32_t j) { return (uint32_t)(T.clsid[j] == c); },
+                   [&](uint32_t j, uint32_t x) {
+                       if (T.clsid[j] == c) T.outpos[j] = (uint16_t)x;
+                       const uint32_t b = T.bidx[j];
+                       if (j == T.bo[b]) T.cbase[b][c] = x;
+                   });
+        }
+        g.sync();
+    }
     GFOR(g, k, n_items) if (k < n_items) {
         const uint32_t it = items[k], i = it & 0xFFFFu;
         const uint32_t f = T.fidx[i];
@@ -600,7 +634,7 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
         for (unsigned t = 0; t < m.n; t++) { c.idx[t] = m.pos[t]; c.h[t] = T.hdr[c.idx[t]]; }
         for (unsigned t = m.n; t < 3; t++) c.idx[t] = NONE32;
         st.ok = run_rewrite(c);
-        if (c.overflow) tf_fail(T, f, CL_ST_REDO);
+        if (c.overflow) tf_fail(T, f, CL_ST_REDO + 3);
         if (st.ok && st.rm) {
             /* G5: does a removed record use a value defined in a later block of its function? */
             bool hazard = false;
@@ -611,7 +645,7 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
                     hazard |= dp != NONE32 && T.bidx[dp] > m.blk;
                 });
             }
-            if (hazard) tf_fail(T, f, CL_ST_REDO);
+            if (hazard) tf_fail(T, f, CL_ST_REDO + 4);
         }
     }
     g.sync();
@@ -632,7 +666,7 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
         st.vbase = T.f_vbase[f] + T.f_nvid[f] + rv; st.ibase = T.f_niid[f] + ri; st.mbase = T.f_qbase[f] + T.f_nimm[f] + rq;
         if (j + 1 == ns || T.fidx[T.sel[j + 1].pos[0]] != f) {
             /* last match of its function: the function's new counters; over its slices -> general kernel */
-            if (st.vbase + st.nv > T.f_vbase[f + 1] || st.mbase + st.nq > T.f_qbase[f + 1]) tf_fail(T, f, CL_ST_REDO);
+            if (st.vbase + st.nv > T.f_vbase[f + 1] || st.mbase + st.nq > T.f_qbase[f + 1]) tf_fail(T, f, CL_ST_REDO + 5);
             T.f_aux[f] = j;
         }
     }
@@ -750,12 +784,12 @@ template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const T
         if (plo == NONE32 || phi == NONE32) continue;
         const cl_hdr dlo = T.hdr[plo], dhi = T.hdr[phi];
         if (!(dlo.op == CL_OP_UNPACK64 && has_mod(s, dlo, CL_MB_LO) && dhi.op == CL_OP_UNPACK64 && has_mod(s, dhi, CL_MB_HI))) continue;
-        if (!dlo.n_uses || !dhi.n_uses) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (!dlo.n_uses || !dhi.n_uses) { tf_fail(T, f, CL_ST_REDO + 6); continue; }
         const opnd slo = t_slot(T, plo, use0(dlo)), shi = t_slot(T, phi, use0(dhi));
         if (!(is_value(slo) && is_value(shi) && slo.pay == shi.pay)) continue;
-        if (!h.n_defs) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (!h.n_defs) { tf_fail(T, f, CL_ST_REDO + 7); continue; }
         const opnd d = t_slot(T, i, def0(h));
-        if (!is_value(d)) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (!is_value(d)) { tf_fail(T, f, CL_ST_REDO + 8); continue; }
         if (d.pay < C::V) T.redirect[d.pay] = slo.pay;
         a_add(&T.f_red[f], 1u);
         mine++;
@@ -829,7 +863,7 @@ template <class G, class C> CLF void t_tag(const G &g, TileS<C> &T) {
  * The reference rewrites chain after chain on a rebuilt def-use graph; a later
  * chain sees an earlier one only if its search walks over that chain's add or
  * MUFU.  Functions where an accepted add reaches another accepted chain within
- * three hops, adds with two reciprocal operands and every exception path of the
+ * two hops, adds with two reciprocal operands and every exception path of the
  * reference are redone by the sequential kernel.                            */
 enum { RF_R0 = 1, RF_R1 = 2, RF_R2 = 4, RF_R3 = 8, RF_SEED = 16, RF_Q = 32, RF_MUFU = 128 };
 template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const TileG<C> &tg) {
@@ -854,7 +888,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
             if (is_value(src) && src.pay < C::V) {
                 const uint32_t dp = T.defpos[src.pay];
                 if (dp != NONE32 && T.hdr[dp].op == CL_OP_I2F) {
-                    if (!h.n_defs || !is_value(t_slot(T, i, def0(h)))) tf_fail(T, f, CL_ST_REDO);   /* IndexError / AttributeError */
+                    if (!h.n_defs || !is_value(t_slot(T, i, def0(h)))) tf_fail(T, f, CL_ST_REDO + 9);   /* IndexError / AttributeError */
                     else fl |= RF_MUFU;
                 }
             }
@@ -898,9 +932,9 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
             hits++; mp = dp; rcp = v;
         });
         if (!hits) continue;
-        if (hits > 1 || has_guard(h) || (h.flags & CL_IF_EXT)) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (hits > 1 || has_guard(h) || (h.flags & CL_IF_EXT)) { tf_fail(T, f, CL_ST_REDO + 10); continue; }
         if (!(T.flag[i] & RF_R3)) continue;
-        if (T.bidx[mp] != T.bidx[i] || !h.n_defs || !is_value(t_slot(T, i, def0(h)))) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (T.bidx[mp] != T.bidx[i] || !h.n_defs || !is_value(t_slot(T, i, def0(h)))) { tf_fail(T, f, CL_ST_REDO + 11); continue; }
         const uint32_t c = a_add(&T.n_chain, 1u);
         if (c < C::X) {
             TChain ch;
@@ -914,38 +948,88 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     g.sync();
     const uint32_t nc = T.n_chain;
     if (nc == 0 || T.fail) return;
-    /* interference: does an accepted add reach another chain's add or MUFU within three hops? */
-    for (unsigned k = 1; k <= 3; k++) {
-        const uint32_t cur = 0x100u << k;
-        GFOR(g, i, n) if (i < n && (T.flag[i] & (RF_SEED | RF_Q))) {
-            if (!tf_ok(T, T.fidx[i])) continue;
-            t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) valbits[v] |= cur; });
-        }
-        g.sync();
-        GFOR(g, i, n) if (i < n && !(T.flag[i] & RF_Q)) {
-            if (!tf_ok(T, T.fidx[i])) continue;
-            bool r = false;
-            t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { r |= v < C::V && (valbits[v] & cur); });
-            if (r) T.flag[i] |= RF_Q;
-        }
-        g.sync();
+    /* interference.  _reaches_f2i reads the user lists of the records at distance 0..2 of the add it starts
+     * from (at distance 3 only the opcode), and a rewritten chain changes the user lists of its MUFU's and
+     * its add's results.  Chains are rewritten in (MUFU, add) position order, so chain B can only see a
+     * chain A of smaller order whose add or MUFU lies within two def-use hops of B's add.  Propagate, over
+     * two hops backwards, the smallest order of the seeds (adds and MUFUs of accepted chains) a record
+     * reaches: owner[i] = { low: own seed order, high: smallest order reached in one hop }.          */
+    uint32_t *mk1 = T.redirect, *mk2 = T.usecnt;
+    GFOR(g, v, T.vtot) if (v < T.vtot) { mk1[v] = NONE32; mk2[v] = NONE32; }
+    GFOR(g, i, n) if (i < n) T.owner[i] = NONE64;
+    g.sync();
+    GFOR(g, c, nc) if (c < nc) {
+        const TChain ch = T.chain[c];
+        const uint32_t key = (uint32_t)ch.mufu << 16 | ch.add;
+        a_min32((uint32_t *)&T.owner[ch.add], key);           /* little endian: the low word */
+        a_min32((uint32_t *)&T.owner[ch.mufu], key);
     }
+    g.sync();
+    GFOR(g, i, n) if (i < n && (T.flag[i] & RF_SEED)) {
+        if (!tf_ok(T, T.fidx[i])) continue;
+        const uint32_t key = (uint32_t)T.owner[i];
+        t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) a_min32(&mk1[v], key); });
+    }
+    g.sync();
+    GFOR(g, i, n) if (i < n) {
+        if (!tf_ok(T, T.fidx[i])) continue;
+        uint32_t q1 = NONE32;
+        t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { if (v < C::V && mk1[v] < q1) q1 = mk1[v]; });
+        if (q1 != NONE32) T.owner[i] = (T.owner[i] & 0xFFFFFFFFull) | (unsigned long long)q1 << 32;
+    }
+    g.sync();
+    GFOR(g, i, n) if (i < n && T.owner[i] != NONE64) {
+        if (!tf_ok(T, T.fidx[i])) continue;
+        const uint32_t own = (uint32_t)T.owner[i], q1 = (uint32_t)(T.owner[i] >> 32);
+        const uint32_t key = own < q1 ? own : q1;
+        t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) a_min32(&mk2[v], key); });
+    }
+    g.sync();
+    GFOR(g, c, nc) if (c < nc) {
+        const TChain ch = T.chain[c];
+        const uint32_t key = (uint32_t)ch.mufu << 16 | ch.add;
+        uint32_t q = (uint32_t)(T.owner[ch.add] >> 32);
+        t_value_defs(T, T.hdr[ch.add], ch.add, [&](uint32_t v) { if (v < C::V && mk2[v] < q) q = mk2[v]; });
+        if (q < key) T.flag[ch.add] |= RF_Q;
+    }
+    g.sync();
     /* rank, ids, value table; vmap (usecnt[]) = add result -> its float view */
     GFOR(g, v, T.vtot) if (v < T.vtot) T.usecnt[v] = NONE32;
     g.sync();
+    /* number of a chain inside its function = chains of earlier MUFUs (scan over the records) + chains of
+     * the same MUFU with an earlier add (a short list per MUFU: owner[m] low word = head, TChain.rank = next) */
+    GFOR(g, i, n) if (i < n) T.owner[i] = 0xFFFFFFFFull;                  /* high word: chains of this MUFU */
+    g.sync();
     GFOR(g, c, nc) if (c < nc) {
         TChain &ch = T.chain[c];
-        const uint32_t f = ch.f;
-        if ((T.flag[ch.add] & RF_Q) != 0) { tf_fail(T, f, CL_ST_REDO); continue; }
-        uint32_t rank = 0;
-        const uint32_t key = (uint32_t)ch.mufu << 16 | ch.add;
-        for (uint32_t o = 0; o < nc; o++) {
-            const TChain &x = T.chain[o];
-            rank += x.f == f && ((uint32_t)x.mufu << 16 | x.add) < key;
-        }
-        ch.rank = (uint16_t)rank;
-        a_add(&T.f_aux[f], 1u);
+        if ((T.flag[ch.add] & RF_Q) != 0) { tf_fail(T, ch.f, CL_ST_REDO + 12); continue; }
+#if CL_DEV
+        ch.rank = (uint16_t)atomicExch((uint32_t *)&T.owner[ch.mufu], c);
+        atomicAdd((uint32_t *)&T.owner[ch.mufu] + 1, 1u);
+#else
+        ch.rank = (uint16_t)(uint32_t)T.owner[ch.mufu];
+        T.owner[ch.mufu] = ((T.owner[ch.mufu] >> 32) + 1) << 32 | c;
+#endif
+        a_add(&T.f_aux[ch.f], 1u);
     }
+    g.sync();
+    t_scan(g, n, [&](uint32_t j) { return (uint32_t)(T.owner[j] >> 32); },
+           [&](uint32_t j, uint32_t x) {
+               T.outpos[j] = (uint16_t)x;
+               const uint32_t f = T.fidx[j];
+               if (j == T.bo[T.f_b0[f]]) T.f_first[f] = x;
+           });
+    g.sync();
+    GFOR(g, c, nc) if (c < nc) {
+        const TChain ch = T.chain[c];
+        if (!tf_ok(T, ch.f)) continue;
+        uint32_t within = 0;
+        for (uint32_t o = (uint32_t)T.owner[ch.mufu] & 0xFFFFu; o != 0xFFFFu; o = T.chain[o].rank)
+            within += T.chain[o].add < ch.add;
+        T.sel_at[ch.add] = (uint16_t)((uint32_t)T.outpos[ch.mufu] - T.f_first[ch.f] + within);
+    }
+    g.sync();
+    GFOR(g, c, nc) if (c < nc) { TChain &ch = T.chain[c]; if (tf_ok(T, ch.f)) ch.rank = T.sel_at[ch.add]; }
     g.sync();
     GFOR(g, c, nc) if (c < nc) {
         const TChain ch = T.chain[c];
@@ -953,7 +1037,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         if (!tf_ok(T, f)) continue;
         const uint32_t vb = T.f_vbase[f];
         const uint32_t vi = vb + T.f_nvid[f] + 2u * ch.rank, vf = vi + 1u, iid = T.f_niid[f] + 2u * ch.rank;
-        if (vf >= T.f_vbase[f + 1]) { tf_fail(T, f, CL_ST_REDO); continue; }
+        if (vf >= T.f_vbase[f + 1]) { tf_fail(T, f, CL_ST_REDO + 13); continue; }
         /* _insert_reciprocal_bitcasts :863-888 (origin codes carry function-local vids) */
         T.alive[vi] = 1; T.origin[vi] = CL_ORG_BITS | (ch.rcp - vb); T.def_iid[vi] = (int32_t)iid;
         T.alive[vf] = 1; T.origin[vf] = CL_ORG_F | (ch.addv - vb); T.def_iid[vf] = (int32_t)(iid + 1u);
@@ -1024,6 +1108,7 @@ struct TileIO {                /* the part of KArgs the tile kernel needs (see c
     unsigned long long cap[4];
     unsigned long long *cursor, *stats;
     uint32_t *retry_list, *retry_count;
+    uint32_t *retry_big_list, *retry_big_count; uint32_t small_max;
     const uint32_t *flist;     /* function ids of all tiles                          */
 };
 struct TFuncOut { cl_func f; uint32_t inst_start, n_inst, imm_start, n_imm, val_start, ev_start, n_ev, pad; };
@@ -1145,6 +1230,9 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
         const bool tile_ok = !T.fail;
         for (uint32_t f = 0; f < nf; f++) {
             const bool ok = tile_ok && T.f_stat[f] == 0;
+#if !CL_DEV
+            if (!ok && getenv("CL_TILE_DEBUG")) fprintf(stderr, "tile hand-back: function %u (%u records) reason %u tile_fail %u\n", T.f_gf[f], T.f_nin[f], T.f_stat[f], T.fail);
+#endif
             if (!ok && T.f_stat[f] == 0) T.f_stat[f] = CL_ST_REDO;
             T.f_oi[f] = oi; T.f_oq[f] = oq; T.f_ov[f] = ov; T.f_oe[f] = oe;
             if (ok) { oi += T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]]; oq += T.f_nimm[f]; ov += T.f_nvid[f]; oe += T.f_nev[f]; }
@@ -1166,7 +1254,11 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
     const bool fits = T.work != 0;
     TFuncOut *o_func = (TFuncOut *)a.o_func;
     GFOR(g, f, nf) if (f < nf) {
-        if (T.f_stat[f] != 0) { a.retry_list[a_add(a.retry_count, 1u)] = T.f_gf[f]; continue; }
+        if (T.f_stat[f] != 0) {
+            if (T.f_nin[f] > a.small_max) a.retry_big_list[a_add(a.retry_big_count, 1u)] = T.f_gf[f];
+            else a.retry_list[a_add(a.retry_count, 1u)] = T.f_gf[f];
+            continue;
+        }
         const uint32_t cnt = T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]];
         TFuncOut o;
         o.f.next_vid = T.f_nvid[f]; o.f.next_iid = T.f_niid[f]; o.f.next_temp_reg = T.f_ntemp[f];
