@@ -54,12 +54,25 @@ def parse_args():
                     help="SASS instructions in the whole corpus (all ranks)")
     ap.add_argument("--seed", type=int, default=100)
     ap.add_argument("--cpu-sample", type=float, default=1.5e6, help="SASS instructions of the CPU-baseline sample")
+    ap.add_argument("--chunks", type=int, default=8, help="e2e: chunks the corpus is streamed in")
+    ap.add_argument("--depth", type=int, default=3, help="e2e: contexts (chunks in flight)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
 from paper_2604_27486_b200.sharding import allgather_counts, materialize, plan_shards  # noqa: E402
+
+
+def pinned_like_array(a: np.ndarray):
+    """Copy of an array in pinned host memory (the numpy view keeps the owning tensor alive)."""
+    import torch
+    a = np.ascontiguousarray(a)
+    t = torch.empty(max(a.nbytes, 16), dtype=torch.uint8, pin_memory=True)
+    v = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+    v[...] = a
+    return v
+
 
 
 def pinned_like(corpus: Corpus):
@@ -248,41 +261,47 @@ def main():
                 "algorithmic_bytes_per_launch": bytes_per_step,
                 "bytes_per_sass_inst": bytes_per_step / max(n_sass_rank, 1)}
 
-    # end to end through the C ABI with pinned host buffers
+    # end to end through the public batch API with pinned HOST buffers: the corpus flows chunk by chunk
+    # (contiguous function ranges) through a few contexts, so H2D, kernels and D2H of different chunks overlap
     e2e = None
     if not args.no_e2e:
-        host_in = pinned_like(corpus)
-        h2d = host_in.nbytes()
-        eng.upload(host_in); eng.run_postssa(); out = eng.download()       # sizes the pinned result buffers
-        d2h = out.nbytes() + out.events.nbytes
-        host_out = pinned_like(out)
-        ev_out = np.zeros(len(out.events) + 1024, out.events.dtype)
-        del out
-        import ctypes as C
-        from paper_2604_27486_b200 import capi
+        from paper_2604_27486_b200.capi import Pipeline
+        ranges = corpus.split(args.chunks)
+        host_in = [pinned_like(corpus.slice_funcs(f0, f1)) for f0, f1 in ranges]
+        h2d = sum(c.nbytes() for c in host_in)
+        pipe = Pipeline(device=local, depth=args.depth)
+        first, _, _ = pipe.run_postssa(host_in)                 # sizes the pinned result holders (and warms up)
+        d2h = sum(o.nbytes() + o.events.nbytes for o in first)
+        holders = []
+        for o in first:
+            h = pinned_like(o)
+            h.events = pinned_like_array(np.zeros(len(o.events) + 16, o.events.dtype))
+            holders.append(h)
+        n_out_e2e = sum(o.n_insts for o in first)
+        del first
 
         def e2e_step():
-            eng.upload(host_in)
-            eng.run_postssa()
-            sizes = (C.c_uint64 * 6)()
-            eng._check(eng.lib.cl_out_sizes(eng._ctx, sizes))
-            stc = capi._struct_of(host_out, eng._keep[1])
-            eng._check(eng.lib.cl_download(eng._ctx, C.byref(stc), capi._ptr(ev_out)))
+            outs, st_sum, _ = pipe.run_postssa(host_in, into=holders)
+            return sum(o.n_insts for o in outs)
 
         for _ in range(max(1, args.warmup - 1)):
             e2e_step()
         fence()
         t2 = time.perf_counter()
         for _ in range(args.steps):
-            e2e_step()
+            got = e2e_step()
         fence()
+        assert got == n_out_e2e == n_out, (got, n_out_e2e, n_out)     # the chunked run is the same job
         te = torch.tensor([time.perf_counter() - t2], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n_sass_all * args.steps / float(te.cpu()[0]), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.cpu()[0]) / args.steps * 1e3,
-               "path": "cl_upload (pinned H2D) + cl_run_postssa + cl_download (device densify + pinned D2H)"}
+               "path": f"capi.Pipeline: {len(host_in)} chunks (function ranges) through {args.depth} contexts; per chunk "
+                       "cl_upload (pinned H2D) + cl_run_postssa + cl_download (device densify + pinned D2H), overlapped across chunks"}
+        pipe.close()
+        del holders, host_in
 
     cpu = None
     if rank == 0 and not args.no_cpu and world == 1:

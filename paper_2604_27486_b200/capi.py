@@ -161,23 +161,38 @@ class Engine:
         m = np.array([tuple(e) for e in sr_map], SR_ENTRY) if len(sr_map) else np.zeros(0, SR_ENTRY)
         self._check(self.lib.cl_run_raw(self._ctx, passes, _ptr(m), len(m)))
 
-    def download(self) -> Corpus:
+    def download(self, into: Corpus | None = None) -> Corpus:
+        """Result of the last run as a dense corpus.  ``into``: caller-owned arrays
+        (e.g. pinned host memory) at least as large as the result; the returned
+        corpus is made of views of them trimmed to the actual sizes."""
         sizes = (C.c_uint64 * 6)()
         self._check(self.lib.cl_out_sizes(self._ctx, sizes))
         n_inst, n_ext, n_mem, n_imm, n_val, n_ev = (int(x) for x in sizes)
         src = self._src
         F, B = src.n_funcs, src.n_blocks
-        out = Corpus(
-            func=np.zeros(F, L.FUNC), func_blk_off=np.zeros(F + 1, np.uint32),
-            ext_off=np.zeros(F + 1, np.uint32), mem_off=np.zeros(F + 1, np.uint32),
-            imm_off=np.zeros(F + 1, np.uint32), val_off=np.zeros(F + 1, np.uint32),
-            blk=np.zeros(B, L.BLK), blk_off=np.zeros(B + 1, np.uint32),
-            hdr=np.zeros(n_inst, L.HDR), tag=np.zeros((n_inst, 8), np.uint16),
-            pay=np.zeros((n_inst, 8), np.uint32), ext_tag=np.zeros(n_ext, np.uint16),
-            ext_pay=np.zeros(n_ext, np.uint32), mem=np.zeros(n_mem, L.MEMREF),
-            imm=np.zeros(n_imm, L.IMM), val_alive=np.zeros(n_val, np.uint8),
-            val_def_iid=np.zeros(n_val, np.int32), val_origin=np.zeros(n_val, np.uint32),
-            events=np.zeros(n_ev, L.EVENT), functions=src.functions, raw=src.raw)
+        want = dict(func=F, func_blk_off=F + 1, ext_off=F + 1, mem_off=F + 1, imm_off=F + 1, val_off=F + 1,
+                    blk=B, blk_off=B + 1, hdr=n_inst, tag=n_inst, pay=n_inst, ext_tag=n_ext, ext_pay=n_ext,
+                    mem=n_mem, imm=n_imm, val_alive=n_val, val_def_iid=n_val, val_origin=n_val)
+        if into is not None:
+            for name, n in want.items():
+                if len(getattr(into, name)) < n:
+                    raise EngineError(f"download: array {name} holds {len(getattr(into, name))} rows, result has {n}")
+            if len(into.events) < n_ev:
+                raise EngineError(f"download: events array holds {len(into.events)} rows, result has {n_ev}")
+            out = Corpus(**{name: getattr(into, name)[:n] for name, n in want.items()},
+                         events=into.events[:n_ev], functions=src.functions, raw=src.raw)
+        else:
+            out = Corpus(
+                func=np.zeros(F, L.FUNC), func_blk_off=np.zeros(F + 1, np.uint32),
+                ext_off=np.zeros(F + 1, np.uint32), mem_off=np.zeros(F + 1, np.uint32),
+                imm_off=np.zeros(F + 1, np.uint32), val_off=np.zeros(F + 1, np.uint32),
+                blk=np.zeros(B, L.BLK), blk_off=np.zeros(B + 1, np.uint32),
+                hdr=np.zeros(n_inst, L.HDR), tag=np.zeros((n_inst, 8), np.uint16),
+                pay=np.zeros((n_inst, 8), np.uint32), ext_tag=np.zeros(n_ext, np.uint16),
+                ext_pay=np.zeros(n_ext, np.uint32), mem=np.zeros(n_mem, L.MEMREF),
+                imm=np.zeros(n_imm, L.IMM), val_alive=np.zeros(n_val, np.uint8),
+                val_def_iid=np.zeros(n_val, np.int32), val_origin=np.zeros(n_val, np.uint32),
+                events=np.zeros(n_ev, L.EVENT), functions=src.functions, raw=src.raw)
         st = _struct_of(out, self._keep[1])
         self._check(self.lib.cl_download(self._ctx, C.byref(st), _ptr(out.events)))
         return out
@@ -218,3 +233,60 @@ class Engine:
 
     def stream(self):
         return self.lib.cl_stream(self._ctx)
+
+
+class Pipeline:
+    """Chunks of a corpus through ``depth`` contexts of one device, so that the
+    host-to-device copy of one chunk, the kernels of another and the
+    device-to-host copy of a third overlap (each context has its own streams).
+    Functions are independent (``ssir.py:215-235``), so a chunk is any
+    contiguous function range (``Corpus.split`` / ``Corpus.slice_funcs``) and
+    the results are those of one big run, chunk by chunk."""
+
+    def __init__(self, device: int = 0, depth: int = 3, lib_path=None, patterns=None):
+        self.engines = [Engine(lib_path, device, patterns) for _ in range(max(1, depth))]
+
+    def close(self):
+        for e in self.engines:
+            e.close()
+
+    def run_postssa(self, chunks, passes=L.PASS_ALL, max_rounds=4, into=None):
+        """``chunks``: list of corpora (pinned host arrays make the copies
+        asynchronous); ``into``: optional list of result holders (see
+        ``Engine.download``).  Returns (results, summed stats, device ms summed over chunks)."""
+        import threading
+        n = len(chunks)
+        results, stats, ms = [None] * n, [None] * n, [0.0] * n
+        errors = []
+        lock = threading.Lock()
+        cursor = [0]
+
+        def worker(eng):
+            while True:
+                with lock:
+                    k = cursor[0]
+                    cursor[0] += 1
+                if k >= n or errors:
+                    return
+                try:
+                    eng.upload(chunks[k])
+                    eng.run_postssa(passes, max_rounds)
+                    results[k] = eng.download(into[k] if into is not None else None)
+                    stats[k] = eng.stats().copy()
+                    ms[k] = eng.last_run_ms()
+                except Exception as e:  # noqa: BLE001 - re-raised on the caller's thread
+                    errors.append(e)
+                    return
+
+        threads = [threading.Thread(target=worker, args=(e,)) for e in self.engines[:max(1, min(n, len(self.engines)))]]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+        total = np.zeros(1, STATS)[0]
+        for s in stats:
+            for name in STATS.names:
+                total[name] += s[name]
+        return results, total, float(sum(ms))

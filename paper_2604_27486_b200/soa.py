@@ -103,6 +103,36 @@ class Corpus:
                 diffs.append(f"{a}: {len(bad)} rows differ, first {bad[:5].tolist()}")
         return diffs
 
+    def slice_funcs(self, f0: int, f1: int) -> "Corpus":
+        """Functions [f0, f1) as a corpus of their own.  Every index inside a
+        function is function-local, so the big arrays are plain views and only the
+        CSR offset arrays are rebased (copies of f1 - f0 + 1 words each)."""
+        b0, b1 = int(self.func_blk_off[f0]), int(self.func_blk_off[f1])
+        i0, i1 = int(self.blk_off[b0]), int(self.blk_off[b1])
+        e0, e1 = int(self.ext_off[f0]), int(self.ext_off[f1])
+        m0, m1 = int(self.mem_off[f0]), int(self.mem_off[f1])
+        q0, q1 = int(self.imm_off[f0]), int(self.imm_off[f1])
+        v0, v1 = int(self.val_off[f0]), int(self.val_off[f1])
+        return Corpus(
+            func=self.func[f0:f1], func_blk_off=self.func_blk_off[f0:f1 + 1] - np.uint32(b0),
+            ext_off=self.ext_off[f0:f1 + 1] - np.uint32(e0), mem_off=self.mem_off[f0:f1 + 1] - np.uint32(m0),
+            imm_off=self.imm_off[f0:f1 + 1] - np.uint32(q0), val_off=self.val_off[f0:f1 + 1] - np.uint32(v0),
+            blk=self.blk[b0:b1], blk_off=self.blk_off[b0:b1 + 1] - np.uint32(i0),
+            hdr=self.hdr[i0:i1], tag=self.tag[i0:i1], pay=self.pay[i0:i1],
+            ext_tag=self.ext_tag[e0:e1], ext_pay=self.ext_pay[e0:e1], mem=self.mem[m0:m1], imm=self.imm[q0:q1],
+            val_alive=self.val_alive[v0:v1], val_def_iid=self.val_def_iid[v0:v1], val_origin=self.val_origin[v0:v1],
+            functions=self.functions[f0:f1] if self.functions else [], raw=self.raw)
+
+    def split(self, n_chunks: int):
+        """Contiguous function ranges of about equal record count: [(f0, f1), ...]."""
+        F = self.n_funcs
+        if F == 0:
+            return []
+        first = self.blk_off[self.func_blk_off[:-1]].astype(np.int64)       # first record of every function
+        cuts = np.searchsorted(first, np.arange(1, n_chunks) * (self.n_insts / n_chunks))
+        edges = np.unique(np.concatenate(([0], cuts, [F])))
+        return [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
     def save(self, path):
         np.savez_compressed(path, raw=np.array(self.raw),
                             events=self.events,
