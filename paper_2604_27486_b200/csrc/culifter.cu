@@ -13,6 +13,8 @@
  */
 #include "core.cuh"
 #include "tile.cuh"
+#include "kargs.h"
+#include "stream.h"
 
 #include <algorithm>
 #include <cstdio>
@@ -63,46 +65,6 @@ static const uint8_t H_OPFLAGS[] = {
 #define CL_OP(name, flags) (uint8_t)(flags),
 #include "../../include/culifter_ops.h"
 #undef CL_OP
-};
-
-/* ----------------------------------------------------------- kernel params */
-struct FuncOut {               /* where a function's result lives (device)       */
-    cl_func f;
-    uint32_t inst_start, n_inst, imm_start, n_imm, val_start, ev_start, n_ev, pad;
-};
-enum { CUR_INST = 0, CUR_IMM, CUR_VAL, CUR_EV, CUR__N };
-
-struct KArgs {
-    cl_corpus in;              /* device pointers                               */
-    const cl_pattern_blob *pb;
-    const uint8_t *opflags;
-    /* results: dense, in completion order; FuncOut says where                 */
-    cl_hdr *o_hdr; uint16_t *o_tag; uint32_t *o_pay;
-    cl_imm *o_imm;
-    uint8_t *o_alive; int32_t *o_def_iid; uint32_t *o_origin;
-    uint16_t *o_ext_tag; uint32_t *o_ext_pay; cl_memref *o_mem;      /* input offsets */
-    cl_blk *o_blk; uint32_t *o_blk_start, *o_blk_cnt;                /* by global block */
-    cl_event *o_ev;
-    FuncOut *o_func;
-    unsigned long long cap[CUR__N];
-    unsigned long long *cursor;          /* [CUR__N]                            */
-    unsigned long long *stats;           /* cl_stats as u64[]                   */
-    unsigned long long *prof;            /* [PF__N] cycle counters               */
-    /* work */
-    const uint32_t *list; uint32_t n_list; uint32_t *work_counter;
-    const uint32_t *n_list_ptr;          /* non-null: the list length lives on the device (retry list) */
-    uint32_t *retry_list, *retry_count;  /* non-null: functions that outgrow this kernel's tight work
-                                            memory are queued for the roomy one instead of failing   */
-    uint8_t *scratch; unsigned long long scratch_per_group;
-    Caps gcap;                 /* capacities of the scratch placement            */
-    uint32_t hot_bytes;        /* shared memory per group for the hot arrays     */
-    uint32_t passes, max_rounds, emit_matches, raw_passes;
-    const cl_sr_entry *sr; uint32_t n_sr;
-    /* tile kernel (tile.cuh) */
-    const TileDesc *tiles; uint32_t n_tiles; uint32_t *tile_counter;
-    const uint32_t *tile_flist;
-    uint32_t *retry_big_list, *retry_big_count; uint32_t small_max;   /* hand-backs above small_max go to the CTA-group kernel */
-    uint8_t *tile_scratch; unsigned long long tile_scratch_per_cta;   /* per group */
 };
 
 /* ------------------------------------------------------ work memory layout */
@@ -820,6 +782,9 @@ struct cl_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t stream2 = nullptr;     /* the CTA-group kernel runs beside the warp kernel */
     int n_sm = 148;
+    int n_sm_or_1() const { return n_sm; }
+#else
+    int n_sm_or_1() const { return 1; }
 #endif
     cl_pattern_blob h_pb{};
     bool have_pb = false, have_in = false, have_out = false;
@@ -855,6 +820,8 @@ struct cl_ctx {
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr, *d_big_rest = nullptr;
     uint32_t *d_retry_big = nullptr, *d_retry_big_count = nullptr, *d_retry_big_counter = nullptr;   /* large functions the tile kernel hands back */
     uint32_t n_tile_funcs = 0, h_retry = 0, n_launches = 0; bool used_tiles = false;
+    int stream_mode = 1;       /* 1: the production post-SSA stage runs as corpus-wide streaming passes (stream.cuh); 0: tile kernels */
+    cls_ctx *cls = nullptr; bool used_stream = false;
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
     int cta_warps = 8;         /* warps per CTA of the CTA-group kernel (8, 16 or 32) */        /* warps per CTA of the phase-synchronous warp kernel (0 = free-running kernel) */
@@ -906,6 +873,7 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_THREAD_MAX")) c->thread_max = CL_CUDA ? (uint32_t)atoi(e) : 0;
     if (const char *e = getenv("CL_WARP_SYNC")) { const int v = atoi(e); c->warp_sync = (v == 0 || v == 8 || v == 16 || v == 32 || v == 33) ? v : 32; }
     if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
+    if (const char *e = getenv("CL_STREAM")) c->stream_mode = atoi(e) != 0;
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 7;
     if (const char *e = getenv("CL_GTILE_WARPS")) { const int v = atoi(e); c->gtile_warps = (v == 8 || v == 32) ? v : 16; }
     if (const char *e = getenv("CL_TILE_LONG")) c->tile_long = atoi(e) != 0;
@@ -939,6 +907,7 @@ extern "C" void cl_destroy(cl_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
 #endif
+    cls_destroy(c->cls);
     for (DBuf &b : c->buf) dfree(b.p);
     dfree(c->d_opflags); dfree(c->d_pb); dfree(c->d_cursor); dfree(c->d_stats);
 #if CL_CUDA
@@ -1140,7 +1109,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     }
     {
         uint32_t *words = nullptr;
-        if (dget(c, B_RETRY_LIST, &c->d_retry_list, std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs))) return -1;
+        if (dget(c, B_RETRY_LIST, &c->d_retry_list, c->stream_mode ? (size_t)F : std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs))) return -1;
         if (dget(c, B_RETRY_WORDS, &words, 4)) return -1;
         c->d_retry_count = words; c->d_retry_counter = words + 1;
     }
@@ -1227,7 +1196,7 @@ static int launch_part(cl_ctx *c, int which, KArgs k, int mode = 0, bool side = 
     if (mode == 3 && p.list.empty()) return 0;             /* no large function at all */
     if (mode == 1 && p.grid == 0) return 0;                /* no small function at all */
     k.list = mode == 1 ? c->d_retry_list : mode == 3 ? c->d_retry_big : mode == 2 ? c->d_rest : mode == 4 ? c->d_big_rest : p.d_list;
-    k.n_list = mode == 1 ? (uint32_t)std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs) : mode == 3 ? (uint32_t)p.list.size()
+    k.n_list = mode == 1 ? (c->stream_mode ? c->F : (uint32_t)std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs)) : mode == 3 ? (uint32_t)p.list.size()
              : mode == 2 ? (uint32_t)c->rest.size() : mode == 4 ? (uint32_t)c->big_rest.size() : (uint32_t)p.list.size();
     k.n_list_ptr = mode == 1 ? c->d_retry_count : mode == 3 ? c->d_retry_big_count : nullptr;
     k.work_counter = mode == 1 ? c->d_retry_counter : mode == 3 ? c->d_retry_big_counter : p.d_counter;
@@ -1379,7 +1348,22 @@ static int run(cl_ctx *c, KArgs k) {
     CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
 #endif
     if (c->d_retry_big_count && dzero(c->d_retry_big_count, sizeof(uint32_t), c->stream)) return -1;
-    if (use_tiles) {
+    bool use_stream = c->stream_mode && c->F && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
+    for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_stream = use_stream && c->h_pb.p[pi].join_ok;
+    c->used_stream = use_stream;
+    if (use_stream) {
+        /* corpus-wide streaming passes; what they hand back (hazards, overflow slots) goes to the general kernels */
+        if (!c->cls && cls_create(&c->cls, c->device, c->n_sm_or_1())) FAIL("cls_create failed");
+        cls_job job;
+        job.k = k;
+        job.retry_list = c->d_retry_list; job.retry_count = c->d_retry_count;
+        job.retry_big_list = c->d_retry_big; job.retry_big_count = c->d_retry_big_count; job.small_max = c->small_max;
+        job.n_inst = c->n_inst; job.n_val = c->n_val; job.n_imm = c->n_imm;
+        c->n_launches++;
+        if (cls_run(c->cls, &job, (void *)(uintptr_t)c->stream, g_err, sizeof g_err)) return -1;
+        if (launch_part(c, 0, k, 1)) return -1;
+        if (launch_part(c, 1, k, 3)) return -1;
+    } else if (use_tiles) {
         if (launch_part(c, 1, k, 4, true)) return -1;     /* large functions outside the tiles: side stream */
         if (launch_tiles(c, k, 1)) return -1;    /* CTA tiles: side stream, after the large functions */
         if (launch_tiles(c, k, 2)) return -1;    /* big L2-resident tiles */
@@ -1405,7 +1389,7 @@ static int run(cl_ctx *c, KArgs k) {
     if (d2h(c->h_cursor, c->d_cursor, sizeof c->h_cursor, c->stream)) return -1;
     if (d2h(&c->stats, c->d_stats, sizeof(cl_stats), c->stream)) return -1;
     if (d2h(c->h_prof, c->d_prof, sizeof c->h_prof, c->stream)) return -1;
-    c->h_retry = 0; c->used_tiles = use_tiles;
+    c->h_retry = 0; c->used_tiles = use_tiles && !use_stream;
     if (c->d_retry_count && d2h(&c->h_retry, c->d_retry_count, sizeof(uint32_t), c->stream)) return -1;
     uint32_t h_retry_big = 0;
     if (c->d_retry_big_count && d2h(&h_retry_big, c->d_retry_big_count, sizeof(uint32_t), c->stream)) return -1;
@@ -1549,7 +1533,7 @@ extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
  * handed back to the general kernel, small functions outside tiles, tile kernel used}            */
 extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
     out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size() + c->tc[2].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles; out[5] = c->n_launches;
-    out[6] = c->tile_mode; out[7] = c->gtile_cfg;
+    out[6] = c->used_stream ? 8 : c->tile_mode; out[7] = c->gtile_cfg;
     return 0;
 }
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }

@@ -29,6 +29,7 @@
  */
 #pragma once
 #include "core.cuh"
+#include "kargs.h"
 #if !CL_DEV
 #include <stdio.h>
 #include <stdlib.h>
@@ -38,7 +39,6 @@ namespace clk {
 
 static constexpr uint32_t CL_ST_REDO = 100;     /* internal: redo this function on the general kernel */
 
-struct TileDesc { uint32_t first, nf; };      /* functions flist[first .. first + nf) */
 
 struct TMatch { uint16_t pos[3]; uint8_t pat, n; };
 struct TChain { uint16_t add, mufu; uint32_t rcp, addv; uint8_t f, ok; uint16_t rank; };

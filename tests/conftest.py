@@ -28,3 +28,16 @@ def sim_engine():
 def cuda_engine():
     import helpers
     return helpers.cuda_engine()
+
+
+@pytest.fixture(scope="session")
+def sim_tile_engine():
+    """context with the streaming path off: the tile kernels take the production run"""
+    import helpers
+    return helpers.sim_engine(stream=False)
+
+
+@pytest.fixture(scope="session")
+def cuda_tile_engine():
+    import helpers
+    return helpers.cuda_engine(stream=False)

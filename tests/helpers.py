@@ -41,11 +41,12 @@ def build_oracle():
 
 def build_sim():
     """One-lane CPU build of the device code (tests/sim): logic checks without a GPU."""
-    srcs = [CSRC / "culifter.cu", CSRC / "core.cuh", ROOT / "include" / "culifter.h"]
+    srcs = [CSRC / n for n in ("culifter.cu", "stream.cu", "core.cuh", "tile.cuh", "stream.cuh", "stream.h", "kargs.h")]
+    srcs.append(ROOT / "include" / "culifter.h")
     if not SIM_LIB.exists() or any(s.stat().st_mtime > SIM_LIB.stat().st_mtime for s in srcs):
         SIM_LIB.parent.mkdir(parents=True, exist_ok=True)
         subprocess.run(["g++", "-x", "c++", "-std=c++17", "-O1", "-g", "-DCL_SIM", "-fPIC", "-shared",
-                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu")], check=True)
+                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu"), str(CSRC / "stream.cu")], check=True)
     return SIM_LIB
 
 
@@ -53,12 +54,28 @@ def oracle_engine():
     return Engine(build_oracle())
 
 
-def sim_engine():
-    return Engine(build_sim())
+def _engine_with_env(path, **env):
+    """cl_create reads the tuning knobs from the environment once, per context."""
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        return Engine(path)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
-def cuda_engine():
-    return Engine()          # the product library; raises without GPU / without the .so
+def sim_engine(stream=True):
+    return _engine_with_env(build_sim(), CL_STREAM=int(stream))
+
+
+def cuda_engine(stream=True):
+    # the product library; raises without GPU / without the .so
+    return _engine_with_env(None, CL_STREAM=int(stream))
 
 
 def state_of(fn):

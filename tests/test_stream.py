@@ -1,9 +1,9 @@
-"""The tile kernel (csrc/tile.cuh: a run of small functions resident in shared
-memory, one thread per record / candidate / match) against the oracle on
-corpora drawn from the reference-front-half pools.  The production run (no
-match lists requested) is the one that takes this path; functions it cannot do
-exactly are handed back to the general kernel, so the result must be bit-equal
-either way -- and the hand-back rate must stay small."""
+"""The streaming path (csrc/stream.cuh: the whole corpus in corpus-wide index
+spaces, every pass one sweep of the cooperatively launched grid) against the
+oracle on corpora drawn from the reference-front-half pools.  The production
+run (no match lists requested) takes this path; functions it cannot do exactly
+are handed back to the general kernel, so the result must be bit-equal either
+way -- and the hand-back rate must stay small."""
 import numpy as np
 import pytest
 
@@ -25,38 +25,37 @@ def _check(engine, oracle, kind, n_sass, seed, passes=15, max_back=0.05):
     part = engine.debug_partition()
     want = _run(oracle, corpus, passes)
     assert not helpers.corpora_equal(got, want)
-    assert part["used_tiles"] == 1 and part["tile_funcs"] > 0
-    assert part["handed_back"] <= max_back * part["tile_funcs"] + 2, part
+    assert part["tile_mode"] == 8, part              # the streaming path ran
+    assert part["handed_back"] <= max_back * corpus.n_funcs + 2, part
     return part
 
 
 @pytest.mark.parametrize("kind,n_sass", [("sm52", 60_000), ("sm75", 60_000), ("sm90", 60_000), ("mixed", 120_000)])
-def test_tile_logic_sim(sim_tile_engine, oracle_engine, kind, n_sass):
-    """one-lane CPU build of the tile code (logic only)"""
-    _check(sim_tile_engine, oracle_engine, kind, n_sass, seed=11)
+def test_stream_logic_sim(sim_engine, oracle_engine, kind, n_sass):
+    """one-lane CPU build of the streaming code (logic only)"""
+    _check(sim_engine, oracle_engine, kind, n_sass, seed=11)
 
 
 @pytest.mark.parametrize("passes", [1, 2, 4, 8, 6, 7])
-def test_tile_pass_subsets_sim(sim_tile_engine, oracle_engine, passes):
-    _check(sim_tile_engine, oracle_engine, "mixed", 40_000, seed=3, passes=passes, max_back=1.0)
+def test_stream_pass_subsets_sim(sim_engine, oracle_engine, passes):
+    _check(sim_engine, oracle_engine, "mixed", 40_000, seed=3, passes=passes, max_back=1.0)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("kind,n_sass,seed", [("sm52", 400_000, 1), ("sm75", 400_000, 2), ("sm90", 400_000, 3),
                                               ("mixed", 1_500_000, 4), ("mixed", 300_000, 5)])
-def test_tile_cuda_bit_equal_to_oracle(cuda_tile_engine, oracle_engine, kind, n_sass, seed):
-    _check(cuda_tile_engine, oracle_engine, kind, n_sass, seed)
+def test_stream_cuda_bit_equal_to_oracle(cuda_engine, oracle_engine, kind, n_sass, seed):
+    _check(cuda_engine, oracle_engine, kind, n_sass, seed)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("passes", [1, 2, 4, 8, 6, 7])
-def test_tile_cuda_pass_subsets(cuda_tile_engine, oracle_engine, passes):
-    _check(cuda_tile_engine, oracle_engine, "mixed", 200_000, seed=6, passes=passes, max_back=1.0)
+def test_stream_cuda_pass_subsets(cuda_engine, oracle_engine, passes):
+    _check(cuda_engine, oracle_engine, "mixed", 200_000, seed=6, passes=passes, max_back=1.0)
 
 
 @pytest.mark.gpu
-def test_tile_cuda_repeatable(cuda_tile_engine):
-    cuda_engine = cuda_tile_engine
+def test_stream_cuda_repeatable(cuda_engine):
     """the same upload run twice gives the same bytes (no order-dependent races)"""
     corpus = synth.build_corpus("mixed", 500_000, seed=9)[0]
     cuda_engine.upload(corpus)
