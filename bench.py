@@ -232,7 +232,9 @@ def main():
         wall = time.perf_counter() - t1
     st = eng.stats()
     part = eng.debug_partition() or {}
-    if os.environ.get("CL_PROF") and rank == 0:
+    if os.environ.get("CL_PROF") and rank == 0 and part.get("tile_mode") == 8:
+        print("stream phases (ms, last step):", eng.debug_stream_profile(), file=sys.stderr)
+    elif os.environ.get("CL_PROF") and rank == 0:
         prof = eng.debug_profile()
         tot = max(prof.get("total", 1), 1)
         print("phase cycles (share of group time):", {k: round(v / tot, 3) for k, v in prof.items() if v}, file=sys.stderr)
@@ -266,6 +268,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         from paper_2604_27486_b200.capi import Pipeline
+        eng.close()                                             # its device buffers make room for the pipeline's contexts
+        del lib_counts
         ranges = corpus.split(args.chunks)
         host_in = [pinned_like(corpus.slice_funcs(f0, f1)) for f0, f1 in ranges]
         h2d = sum(c.nbytes() for c in host_in)
@@ -292,6 +296,9 @@ def main():
             got = e2e_step()
         fence()
         assert got == n_out_e2e == n_out, (got, n_out_e2e, n_out)     # the chunked run is the same job
+        if os.environ.get("CL_TRACE") and rank == 0:
+            for kk, tr in enumerate(pipe.last_trace):
+                print(f"chunk {kk}: ctx {tr[0]} upload {tr[1]*1e3:7.1f}..{tr[2]*1e3:7.1f} run {tr[3]*1e3:7.1f}..{tr[4]*1e3:7.1f} download ..{tr[5]*1e3:7.1f} ms", file=sys.stderr)
         te = torch.tensor([time.perf_counter() - t2], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -299,7 +306,8 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.cpu()[0]) / args.steps * 1e3,
                "path": f"capi.Pipeline: {len(host_in)} chunks (function ranges) through {args.depth} contexts; per chunk "
-                       "cl_upload (pinned H2D) + cl_run_postssa + cl_download (device densify + pinned D2H), overlapped across chunks"}
+                       "cl_upload (pinned H2D) + cl_run_postssa + cl_download (device densify + pinned D2H); upload, run and download are "
+                       "stage threads, so the three overlap across chunks"}
         pipe.close()
         del holders, host_in
 

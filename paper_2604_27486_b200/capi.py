@@ -218,6 +218,22 @@ class Engine:
         self.lib.cl_debug_profile(self._ctx, buf, 16)
         return dict(zip(self.PROFILE_SLOTS, (int(x) for x in buf)))
 
+    STREAM_SLOTS = ("load", "usecount", "seed", "items", "budget", "unify", "select", "selscan", "plan", "bases", "mark",
+                    "permute", "stage", "simplify", "dce", "recip", "tag", "store", "gate")
+
+    def debug_stream_profile(self):
+        """Milliseconds per phase of the streaming path's last run and its fixpoint iteration counts."""
+        if not hasattr(self.lib, "cl_debug_stream_profile"):
+            return {}
+        buf = (C.c_ulonglong * 24)()
+        it = (C.c_uint32 * 4)()
+        self.lib.cl_debug_stream_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+        if not self.lib.cl_debug_stream_profile(self._ctx, buf, 24, it):
+            return {}
+        d = {k: round(int(v) / 1e6, 3) for k, v in zip(self.STREAM_SLOTS, buf)}
+        d["iters"] = {"select": int(it[0]), "dce": int(it[1]), "rounds": int(it[2])}
+        return d
+
     def debug_partition(self):
         """{tiles, tile_funcs, handed_back, outside, used_tiles} of the last run (CUDA / sim builds only)."""
         if not hasattr(self.lib, "cl_debug_partition"):
@@ -253,38 +269,82 @@ class Pipeline:
     def run_postssa(self, chunks, passes=L.PASS_ALL, max_rounds=4, into=None):
         """``chunks``: list of corpora (pinned host arrays make the copies
         asynchronous); ``into``: optional list of result holders (see
-        ``Engine.download``).  Returns (results, summed stats, device ms summed over chunks)."""
-        import threading
-        n = len(chunks)
-        results, stats, ms = [None] * n, [None] * n, [0.0] * n
-        errors = []
-        lock = threading.Lock()
-        cursor = [0]
+        ``Engine.download``).  Returns (results, summed stats, device ms summed over chunks).
 
-        def worker(eng):
-            while True:
-                with lock:
-                    k = cursor[0]
-                    cursor[0] += 1
-                if k >= n or errors:
-                    return
-                try:
-                    eng.upload(chunks[k])
-                    eng.run_postssa(passes, max_rounds)
+        Three stage threads (upload, run, download) hand chunks to each other
+        through queues; chunk k lives in context k mod depth from its upload to
+        its download.  Symmetric workers (one thread per context doing all three
+        steps) fall into lock step -- all upload, then all run, then all
+        download -- and overlap nothing (measured)."""
+        import queue
+        import threading
+        import time
+        n = len(chunks)
+        results, stats, ms, trace = [None] * n, [None] * n, [0.0] * n, [[0, 0.0, 0.0, 0.0, 0.0, 0.0] for _ in range(n)]
+        errors = []
+        t_begin = time.perf_counter()
+        free_ctx, q_run, q_down = queue.Queue(), queue.Queue(), queue.Queue()
+        for i in range(len(self.engines)):
+            free_ctx.put(i)
+
+        def now():
+            return time.perf_counter() - t_begin
+
+        def uploader():
+            try:
+                for k in range(n):
+                    i = free_ctx.get()
+                    if i is None or errors:
+                        break
+                    trace[k][0], trace[k][1] = i, now()
+                    self.engines[i].upload(chunks[k])
+                    trace[k][2] = now()
+                    q_run.put((k, i))
+            except Exception as e:  # noqa: BLE001 - re-raised on the caller's thread
+                errors.append(e)
+            q_run.put(None)
+
+        def runner():
+            try:
+                while True:
+                    item = q_run.get()
+                    if item is None or errors:
+                        break
+                    k, i = item
+                    trace[k][3] = now()
+                    self.engines[i].run_postssa(passes, max_rounds)
+                    trace[k][4] = now()
+                    q_down.put(item)
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+                free_ctx.put(None)
+            q_down.put(None)
+
+        def downloader():
+            try:
+                while True:
+                    item = q_down.get()
+                    if item is None or errors:
+                        break
+                    k, i = item
+                    eng = self.engines[i]
                     results[k] = eng.download(into[k] if into is not None else None)
                     stats[k] = eng.stats().copy()
                     ms[k] = eng.last_run_ms()
-                except Exception as e:  # noqa: BLE001 - re-raised on the caller's thread
-                    errors.append(e)
-                    return
+                    trace[k][5] = now()
+                    free_ctx.put(i)
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+                free_ctx.put(None)
 
-        threads = [threading.Thread(target=worker, args=(e,)) for e in self.engines[:max(1, min(n, len(self.engines)))]]
+        threads = [threading.Thread(target=f) for f in (uploader, runner, downloader)]
         for t in threads:
             t.start()
         for t in threads:
             t.join()
         if errors:
             raise errors[0]
+        self.last_trace = trace      # per chunk: [context, upload start, upload end, run start, run end, download end] in seconds
         total = np.zeros(1, STATS)[0]
         for s in stats:
             for name in STATS.names:

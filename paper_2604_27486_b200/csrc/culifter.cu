@@ -1049,8 +1049,8 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     }
     /* tiles: small functions without overflow slots, by size class, packed in size order */
     for (auto &t : c->tc) t.tiles.clear();
-    c->tile_flist.clear(); c->rest.clear(); c->n_tile_funcs = 0;
-    {
+    c->tile_flist.clear(); c->rest.clear(); c->big_rest.clear(); c->n_tile_funcs = 0;
+    if (!c->stream_mode) {       /* the streaming path needs no host-side plan */
         struct Need { uint32_t I, V, Q, B, f; };
         /* tile size by corpus size: the bigger the tile the better the passes amortise (profiles/r01_tuning.md),
          * as long as there are a few tiles per SM                                                              */
@@ -1535,6 +1535,10 @@ extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
     out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size() + c->tc[2].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles; out[5] = c->n_launches;
     out[6] = c->used_stream ? 8 : c->tile_mode; out[7] = c->gtile_cfg;
     return 0;
+}
+/* debugging aid: nanoseconds per phase of the streaming path's last run + {select, dce, rounds} iteration counts */
+extern "C" int cl_debug_stream_profile(cl_ctx *c, unsigned long long *prof, int n, uint32_t *iters) {
+    return c->cls ? cls_profile(c->cls, prof, n, iters) : 0;
 }
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }
 extern "C" int cl_last_run_ms(cl_ctx *c, float *ms) { *ms = c->last_ms; return 0; }

@@ -2,6 +2,9 @@
  * work buffers sized from the corpus totals, one cooperative launch per run.
  * Compiled with -DCL_SIM by g++ it runs the same code with a one-lane group on
  * host memory (tests/sim only).                                               */
+/* core.cuh defines its non-inline device functions with external linkage and is also part of culifter.cu:
+ * this translation unit gets its own copy of the namespace */
+#define clk clk_stream
 #include "stream.cuh"
 #include "stream.h"
 
@@ -20,7 +23,7 @@
 using namespace clk;
 
 #ifndef CLS_MINB
-#define CLS_MINB 2            /* CTAs of 256 threads per SM the register budget is set for */
+#define CLS_MINB 4            /* CTAs of 256 threads per SM the register budget is set for */
 #endif
 
 #if CLS_CUDA
@@ -31,6 +34,7 @@ __global__ void __launch_bounds__(256, CLS_MINB) k_stream(StreamS *T, StreamP *P
     g.rank = blockIdx.x * 256u + threadIdx.x; g.size = gridDim.x * 256u;
     g.part = part; g.slots = slots; g.turn = 0;
     g.cta.rank = threadIdx.x; g.cta.size = 256; g.cta.red = red;
+    if (g.rank == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(T->prof_t0));
     s_setup(g, *P, pb);
     s_run(g, *T, a);
 }
@@ -43,6 +47,7 @@ struct cls_ctx {
     size_t next = 0, held = 0;
     unsigned long long launches = 0;
     StreamS *d_T = nullptr; StreamP *d_P = nullptr; uint32_t *d_part = nullptr, *d_slots = nullptr;
+    StreamS *last_T = nullptr;
 };
 
 #define CLS_FAIL(...) do { snprintf(err, errlen, __VA_ARGS__); return -1; } while (0)
@@ -92,6 +97,20 @@ void cls_destroy(cls_ctx *c) {
     delete c;
 }
 void cls_info(const cls_ctx *c, unsigned long long out[4]) { out[0] = c->grid; out[1] = c->launches; out[2] = c->held; out[3] = 0; }
+/* nanoseconds per phase and fixpoint iteration counts of the last run (synchronises the device) */
+int cls_profile(const cls_ctx *c, unsigned long long *prof, int n, uint32_t iters[4]) {
+    if (!c || !c->last_T) return 0;
+    StreamS h;
+#if CLS_CUDA
+    if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+    if (cudaMemcpy(&h, c->last_T, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+#else
+    memcpy(&h, c->last_T, sizeof h);
+#endif
+    for (int i = 0; i < n && i < SP__N; i++) prof[i] = h.prof[i];
+    for (int i = 0; i < 4; i++) iters[i] = h.iters[i];
+    return SP__N;
+}
 
 int cls_run(cls_ctx *c, const cls_job *job, void *stream, char *err, size_t errlen) {
     const KArgs &k = job->k;
@@ -155,6 +174,7 @@ int cls_run(cls_ctx *c, const cls_job *job, void *stream, char *err, size_t errl
     io.retry_big_list = job->retry_big_list; io.retry_big_count = job->retry_big_count; io.small_max = job->small_max;
     io.passes = k.passes; io.max_rounds = k.max_rounds;
     c->launches++;
+    c->last_T = d_T;
 #if CLS_CUDA
     cudaStream_t st = (cudaStream_t)stream;
     if (!c->grid) {

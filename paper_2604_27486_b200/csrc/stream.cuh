@@ -55,6 +55,8 @@ struct StreamP {
 };
 
 struct StreamCaps { uint32_t I, V, Q, M, S, X, E; };
+enum { SP_LOAD = 0, SP_USECOUNT, SP_SEED, SP_ITEMS, SP_BUDGET, SP_UNIFY, SP_SELECT, SP_SELSCAN, SP_PLAN, SP_BASES, SP_MARK, SP_PERMUTE,
+       SP_STAGE, SP_SIMPLIFY, SP_DCE, SP_RECIP, SP_TAG, SP_STORE, SP_GATE, SP__N = 24 };
 
 /* everything the passes touch; lives in global memory, arrays sized by the host (stream.cu) */
 struct StreamS {
@@ -86,6 +88,8 @@ struct StreamS {
     StreamCaps cap;
     uint32_t n, nb, nf, n_mt, n_sel, n_ev, fail, vtot, qtot, n_chain, n_items, work;
     uint32_t res[4];                                             /* places reserved in the result buffers */
+    unsigned long long prof[SP__N], prof_t0;                     /* nanoseconds per phase (lane 0 of the grid) */
+    uint32_t iters[4];                                           /* select / dce fixpoint iterations, rounds */
 };
 
 struct StreamIO {              /* the part of KArgs the stream kernel needs */
@@ -125,6 +129,13 @@ struct GridGrp {
         if (threadIdx.x == 0 && c) atomicOr(s, 1u);
         sync();
         return *(volatile uint32_t *)s != 0;
+    }
+    CLD uint32_t any_bits(uint32_t x) const {           /* bitwise or over the grid */
+        const uint32_t w = __reduce_or_sync(0xFFFFFFFFu, x);
+        uint32_t *s = turn_slot();
+        if ((threadIdx.x & 31u) == 0 && w) atomicOr(s, w);
+        sync();
+        return *(volatile uint32_t *)s;
     }
     CLD uint32_t sum(uint32_t x) const {
         const uint32_t c = cta.sum(x);
@@ -182,7 +193,9 @@ CLD uint32_t g_wrank(const Grp<0> &) { return 0; }
 CLD uint32_t g_wcount(const Grp<0> &) { return 1; }
 CLD uint32_t g_lane(const Grp<0> &) { return 0; }
 CLD uint32_t g_lanes(const Grp<0> &) { return 1; }
+CLD uint32_t g_any_bits(const Grp<0> &, uint32_t x) { return x; }
 #if CL_DEV
+CLD uint32_t g_any_bits(const GridGrp &g, uint32_t x) { return g.any_bits(x); }
 CLD uint32_t g_wrank(const GridGrp &g) { return g.wrank(); }
 CLD uint32_t g_wcount(const GridGrp &g) { return g.wcount(); }
 CLD uint32_t g_lane(const GridGrp &g) { return g.lane(); }
@@ -201,6 +214,19 @@ template <class FIN, class FOUT> CLD uint32_t s_scan(const Grp<0> &, uint32_t n,
 #define WFOR(g, f, n) for (uint32_t f = g_wrank(g); f < (n); f += g_wcount(g))
 #define LFOR(g, k, n) for (uint32_t k = g_lane(g); k < (n); k += g_lanes(g))
 
+/* phase clock: lane 0 of the grid charges the time since the previous mark to `slot` */
+template <class G> CLD void s_mark(const G &g, StreamS &T, int slot) {
+#if CL_DEV
+    if (g.rank == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        T.prof[slot] += t - T.prof_t0;
+        T.prof_t0 = t;
+    }
+#else
+    (void)g; (void)T; (void)slot;
+#endif
+}
 CLD bool sf_ok(const StreamS &T, uint32_t f) { return *(volatile const uint32_t *)&T.f_stat[f] == 0; }
 CLD void sf_fail(StreamS &T, uint32_t f, uint32_t code) { a_cas0(&T.f_stat[f], code); }
 CLD void s_fail(StreamS &T) { *(volatile uint32_t *)&T.fail = 1; }
@@ -309,6 +335,10 @@ template <class G> CLD void s_rebase_blocks(const G &g, StreamS &T, uint32_t n_o
     g.sync();
     if (g.rank == 0) { uint32_t *x = T.bo; T.bo = T.bo2; T.bo2 = x; T.n = n_new; T.fs.bo = T.bo; }
     g.sync();
+    /* function-relative positions are compared as 16-bit numbers (s_key, chain order) */
+    const uint32_t nf = T.nf;
+    SFOR(g, f, nf) if (T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]] > 0xFFFFu) sf_fail(T, f, CLS_REDO + 14);
+    g.sync();
 }
 
 /* ------------------------------------------------------------------ def-use */
@@ -340,6 +370,7 @@ template <class G> CLF void s_usecount(const G &g, StreamS &T) {
                 a_add(&T.usecnt[T.blk[b].term_pay[k]], 1u);
     }
     g.sync();
+    s_mark(g, T, SP_USECOUNT);
 }
 
 /* ----------------------------------------------------------------- matching */
@@ -508,6 +539,7 @@ template <class G> CLF void s_match(const G &g, StreamS &T, unsigned table) {
         T.clsid[i] = (uint8_t)c;
     }
     g.sync();
+    s_mark(g, T, SP_SEED);
     /* the dense list of (anchor, pattern) work items, in stream order */
     unsigned long long *items = T.owner;                   /* [I]: free until s_select */
     auto mask_of = [&](uint32_t i) -> uint32_t {
@@ -526,6 +558,7 @@ template <class G> CLF void s_match(const G &g, StreamS &T, unsigned table) {
             for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) { if (x < cap_items) items[x] = (unsigned long long)pi << 32 | i; x++; }
         });
     if (n_items > cap_items) { if (g.rank == 0) s_fail(T); g.sync(); return; }
+    s_mark(g, T, SP_ITEMS);
     /* budget (G1): where the product of the candidate-list sizes of a pattern exceeds it, a tuple counts only
      * if its rank in itertools.product order is below it; the rank needs every member's index inside its
      * candidate list = members of its class before it in the block: one stream-wide scan per class concerned */
@@ -545,8 +578,7 @@ template <class G> CLF void s_match(const G &g, StreamS &T, unsigned table) {
             T.b_over[b] = (uint16_t)m;
             need |= m;
         }
-        uint32_t all_need = 0;
-        for (unsigned c = 0; c < T.P->n_cls[table]; c++) if (g.any((need >> c) & 1u)) all_need |= 1u << c;
+        const uint32_t all_need = g_any_bits(g, need);
         for (unsigned c = 0; c < T.P->n_cls[table]; c++) {
             if (!((all_need >> c) & 1u)) continue;
             s_scan(g, n, [&](uint32_t j) { return (uint32_t)(T.clsid[j] == c); },
@@ -557,12 +589,14 @@ template <class G> CLF void s_match(const G &g, StreamS &T, unsigned table) {
                    });
         }
     }
+    s_mark(g, T, SP_BUDGET);
     SFOR(g, k, n_items) {
         const unsigned long long it = items[k];
         const uint32_t i = (uint32_t)it, f = T.fidx[i];
         if (sf_ok(T, f)) s_try_anchor(T, table, i, (unsigned)(it >> 32), f);
     }
     g.sync();
+    s_mark(g, T, SP_UNIFY);
 }
 
 /* select_matches (patterns.py:241-252) for all blocks at once; the key orders
@@ -608,8 +642,10 @@ template <class G> CLF uint32_t s_select(const G &g, StreamS &T) {
             } else
                 left = true;
         }
+        if (g.rank == 0) T.iters[0]++;
         if (!g.any(left)) break;
     }
+    s_mark(g, T, SP_SELECT);
     const uint32_t capS = T.cap.S;
     const uint32_t count = s_scan(g, n, [&](uint32_t p) { return (uint32_t)(T.sel_at[p] != NONE32); },
         [&](uint32_t p, uint32_t x) {
@@ -622,6 +658,7 @@ template <class G> CLF uint32_t s_select(const G &g, StreamS &T) {
             a_add(&T.f_stats[T.fidx[p]][16 + m.pat], 1u);
         });
     if (count > capS) { if (g.rank == 0) s_fail(T); g.sync(); return 0; }
+    s_mark(g, T, SP_SELSCAN);
     return count;
 }
 
@@ -716,6 +753,7 @@ template <class G> CLF void s_apply_patterns(const G &g, StreamS &T, unsigned ta
         T.mstate[j] = st.nq;                                   /* [ns] <= [M] */
     }
     g.sync();
+    s_mark(g, T, SP_PLAN);
     /* exclusive scans in select order (stream wide; rebased per function below): id bases (G3) */
     s_scan(g, ns, [&](uint32_t j) { return cnt_v[j]; }, [&](uint32_t j, uint32_t x) { base[j] = x; });
     s_scan(g, ns, [&](uint32_t j) { return cnt_i[j]; }, [&](uint32_t j, uint32_t x) { base[j] |= (unsigned long long)x << 32; });
@@ -736,6 +774,7 @@ template <class G> CLF void s_apply_patterns(const G &g, StreamS &T, unsigned ta
         }
     }
     g.sync();
+    s_mark(g, T, SP_BASES);
     SFOR(g, f, nf) if (T.f_first[f] != NONE32 && sf_ok(T, f)) {
         const Stage &st = T.stage[T.f_aux[f]];
         T.f_nvid[f] = st.vbase + st.nv - T.f_vbase[f]; T.f_niid[f] = st.ibase + st.ni; T.f_nimm[f] = st.mbase + st.nq - T.f_qbase[f];
@@ -766,7 +805,9 @@ template <class G> CLF void s_apply_patterns(const G &g, StreamS &T, unsigned ta
     const uint32_t tot = s_scan(g, n, [&](uint32_t p) { return (uint32_t)T.keep[p] + T.inscnt[p]; },
                                 [&](uint32_t p, uint32_t x) { T.outpos[p] = x; });
     if (tot > T.cap.I) { if (g.rank == 0) s_fail(T); g.sync(); return; }
+    s_mark(g, T, SP_MARK);
     s_permute(g, T, n, [&](uint32_t p) { return T.keep[p] ? T.outpos[p] + T.inscnt[p] : NONE32; });
+    s_mark(g, T, SP_PERMUTE);
     /* staged records to their place, value table, immediates */
     SFOR(g, j, ns) {
         const SelRec m = T.sel[j];
@@ -776,6 +817,7 @@ template <class G> CLF void s_apply_patterns(const G &g, StreamS &T, unsigned ta
     }
     g.sync();
     s_rebase_blocks(g, T, n, tot);
+    s_mark(g, T, SP_STAGE);
 }
 
 /* ordered compaction of the stream by keep[]                                   */
@@ -809,10 +851,12 @@ template <class G> CLF void s_dce(const G &g, StreamS &T) {
             s_value_operands(T, h, i, [&](uint32_t v) { if (v < V) a_sub(&T.usecnt[v], 1u); });
         }
         const uint32_t dead = g.sum(mine);
+        if (g.rank == 0) T.iters[1]++;
         if (!dead) break;
         removed += dead;
     }
     if (removed) s_compact(g, T);
+    s_mark(g, T, SP_DCE);
 }
 
 /* simplify_packs + _redirect_values (patterns.py:710-764) for the gated functions;
@@ -854,7 +898,7 @@ template <class G> CLF void s_simplify(const G &g, StreamS &T) {
         mine++;
     }
     const uint32_t changed = g.sum(mine);
-    if (!changed) return;
+    if (!changed) { s_mark(g, T, SP_SIMPLIFY); return; }
     SFOR(g, i, n) {
         const uint32_t f = T.fidx[i];
         if (!T.f_red[f] || !sf_ok(T, f)) continue;
@@ -878,6 +922,7 @@ template <class G> CLF void s_simplify(const G &g, StreamS &T) {
             if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE) T.blk[b].term_pay[k] = s_final_of(T, T.blk[b].term_pay[k]);
     }
     g.sync();
+    s_mark(g, T, SP_SIMPLIFY);
 }
 
 /* tag_cuda_objects (patterns.py:895-916)                                      */
@@ -1263,7 +1308,7 @@ template <class G> CLF void s_load(const G &g, StreamS &T, const StreamIO &a) {
 /* results of the live functions in function order at one reserved place; the others are queued for the
  * general kernel                                                                                       */
 template <class G> CLF void s_store(const G &g, StreamS &T, const StreamIO &a) {
-    const uint32_t nf = T.nf, nb = T.nb, n = T.n;
+    const uint32_t nf = T.nf, n = T.n;
     const bool all_ok = !T.fail;
     auto live = [&](uint32_t f) { return all_ok && T.f_stat[f] == 0; };
     const uint32_t oi = s_scan(g, nf, [&](uint32_t f) { return live(f) ? T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]] : 0u; }, [&](uint32_t f, uint32_t x) { T.f_oi[f] = x; });
@@ -1388,6 +1433,7 @@ template <class G> CLD bool s_any_gate(const G &g, StreamS &T) {
 template <class G> CLF void s_run(const G &g, StreamS &T, const StreamIO &a) {
     const uint32_t passes = a.passes, max_rounds = a.max_rounds;
     s_load(g, T, a);
+    s_mark(g, T, SP_LOAD);
     const uint32_t nf = T.nf;
     if (!T.fail && (passes & CL_PASS_XMAD)) {
         s_set_gate(g, T, 0);
@@ -1396,13 +1442,16 @@ template <class G> CLF void s_run(const G &g, StreamS &T, const StreamIO &a) {
             if (!T.fail) { s_set_gate(g, T, 0); s_dce(g, T); }
         }
     }
-    if (!T.fail && (passes & CL_PASS_RECIPROCAL)) s_reciprocal(g, T);
+    s_mark(g, T, SP_GATE);
+    if (!T.fail && (passes & CL_PASS_RECIPROCAL)) { s_reciprocal(g, T); s_mark(g, T, SP_RECIP); }
     if (!T.fail && (passes & CL_PASS_AGGREGATE)) {
         SFOR(g, f, nf) T.f_active[f] = 1;
         g.sync();
         for (uint32_t round = 0; round < max_rounds && !T.fail; round++) {
             s_set_gate(g, T, 1);
             if (!s_any_gate(g, T)) break;
+            if (g.rank == 0) T.iters[2]++;
+            s_mark(g, T, SP_GATE);
             SFOR(g, f, nf) T.f_chg[f] = 0;
             g.sync();
             s_apply_patterns(g, T, 0, 2 + round);
@@ -1416,9 +1465,12 @@ template <class G> CLF void s_run(const G &g, StreamS &T, const StreamIO &a) {
         }
         if (!T.fail) { s_set_gate(g, T, 3); s_dce(g, T); }
     }
+    s_mark(g, T, SP_GATE);
     if (!T.fail && (passes & CL_PASS_TAG)) s_tag(g, T);
     g.sync();
+    s_mark(g, T, SP_TAG);
     s_store(g, T, a);
+    s_mark(g, T, SP_STORE);
 }
 
 /* once per launch: seed classes of both tables, anchors, unification constraints */

@@ -16,3 +16,4 @@ void cls_destroy(cls_ctx *c);
 int cls_run(cls_ctx *c, const cls_job *job, void *stream, char *err, size_t errlen);
 /* {grid, launches, device bytes held} of the last run */
 void cls_info(const cls_ctx *c, unsigned long long out[4]);
+int cls_profile(const cls_ctx *c, unsigned long long *prof, int n, uint32_t iters[4]);
