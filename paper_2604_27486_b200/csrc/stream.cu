@@ -109,6 +109,8 @@ int cls_profile(const cls_ctx *c, unsigned long long *prof, int n, uint32_t iter
 #endif
     for (int i = 0; i < n && i < SP__N; i++) prof[i] = h.prof[i];
     for (int i = 0; i < 4; i++) iters[i] = h.iters[i];
+    if (getenv("CL_PROF")) for (uint32_t r = 0; r < h.n_apply && r < 8; r++)
+        fprintf(stderr, "apply_patterns call %u: items %u raw matches %u selected %u (stream %u records)\n", r, h.rstat[r][1], h.rstat[r][2], h.rstat[r][3], h.n);
     return SP__N;
 }
 

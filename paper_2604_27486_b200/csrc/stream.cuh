@@ -88,8 +88,11 @@ struct StreamS {
     StreamCaps cap;
     uint32_t n, nb, nf, n_mt, n_sel, n_ev, fail, vtot, qtot, n_chain, n_items, work;
     uint32_t res[4];                                             /* places reserved in the result buffers */
+    uint32_t du_ok;                                              /* usecnt / defpos describe the stream for the gated functions */
     unsigned long long prof[SP__N], prof_t0;                     /* nanoseconds per phase (lane 0 of the grid) */
     uint32_t iters[4];                                           /* select / dce fixpoint iterations, rounds */
+    uint32_t rstat[8][4];                                        /* per apply_patterns call: gated records, work items, raw matches, selected */
+    uint32_t n_apply;
 };
 
 struct StreamIO {              /* the part of KArgs the stream kernel needs */
@@ -161,13 +164,20 @@ CLD uint32_t a_inc_agg(uint32_t *p) {
 /* exclusive scan over items [0, n) in order, grid wide: every CTA owns a contiguous run of items,
  * sums it, waits for the others, rescans it from its base.  `in` is evaluated twice per item.     */
 template <class FIN, class FOUT> CLD uint32_t s_scan(const GridGrp &g, uint32_t n, FIN in, FOUT out) {
-    const uint32_t nc = gridDim.x, bt = blockDim.x, c = blockIdx.x, t = threadIdx.x;
+    constexpr uint32_t K = 8;                                   /* consecutive items per thread and step: K loads in flight */
+    const uint32_t nc = gridDim.x, bt = blockDim.x, c = blockIdx.x, t = threadIdx.x, step = bt * K;
     uint32_t L = (n + nc - 1) / nc;
-    L = (L + bt - 1) / bt * bt;
+    L = (L + step - 1) / step * step;
     const unsigned long long lo64 = (unsigned long long)c * L;
     const uint32_t lo = lo64 < n ? (uint32_t)lo64 : n, hi = n - lo < L ? n : lo + L;
     uint32_t s = 0;
-    for (uint32_t j = lo + t; j < hi; j += bt) s += in(j);
+    for (uint32_t j0 = lo + t * K; j0 < hi; j0 += step) {
+        uint32_t x[K];
+#pragma unroll
+        for (uint32_t k = 0; k < K; k++) x[k] = j0 + k < hi ? in(j0 + k) : 0u;
+#pragma unroll
+        for (uint32_t k = 0; k < K; k++) s += x[k];
+    }
     const uint32_t tot = g.cta.sum(s);
     if (t == 0) g.part[c] = tot;
     g.sync();
@@ -176,12 +186,17 @@ template <class FIN, class FOUT> CLD uint32_t s_scan(const GridGrp &g, uint32_t 
     before = g.cta.sum(before);
     all = g.cta.sum(all);
     uint32_t run = before;
-    for (uint32_t j0 = lo; j0 < hi; j0 += bt) {
-        const uint32_t j = j0 + t;
-        const uint32_t x = j < hi ? in(j) : 0u;
+    for (uint32_t base = lo; base < hi; base += step) {
+        const uint32_t j0 = base + t * K;
+        uint32_t x[K], mine = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < K; k++) { x[k] = j0 + k < hi ? in(j0 + k) : 0u; }
+#pragma unroll
+        for (uint32_t k = 0; k < K; k++) mine += x[k];
         uint32_t tt;
-        const uint32_t o = g.cta.exscan(x, tt);
-        if (j < hi) out(j, run + o);
+        uint32_t o = run + g.cta.exscan(mine, tt);
+#pragma unroll
+        for (uint32_t k = 0; k < K; k++) { if (j0 + k < hi) out(j0 + k, o); o += x[k]; }
         run += tt;
     }
     g.sync();
@@ -228,7 +243,9 @@ template <class G> CLD void s_mark(const G &g, StreamS &T, int slot) {
 #endif
 }
 CLD bool sf_ok(const StreamS &T, uint32_t f) { return *(volatile const uint32_t *)&T.f_stat[f] == 0; }
-CLD void sf_fail(StreamS &T, uint32_t f, uint32_t code) { a_cas0(&T.f_stat[f], code); }
+/* a failed function leaves the gate at once, so sweeps that look at the gate need no second look-up */
+CLD void sf_fail(StreamS &T, uint32_t f, uint32_t code) { a_cas0(&T.f_stat[f], code); *(volatile uint8_t *)&T.f_gate[f] = 0; }
+CLD bool sf_on(const StreamS &T, uint32_t f) { return *(volatile const uint8_t *)&T.f_gate[f] != 0; }
 CLD void s_fail(StreamS &T) { *(volatile uint32_t *)&T.fail = 1; }
 
 CLD void s_event(StreamS &T, uint32_t f, uint32_t seq, uint32_t kind, uint32_t idx, uint32_t a, uint32_t b) {
@@ -333,7 +350,7 @@ template <class G> CLD void s_rebase_blocks(const G &g, StreamS &T, uint32_t n_o
     const uint32_t nb = T.nb;
     SFOR(g, b, nb + 1) { const uint32_t old = T.bo[b]; T.bo2[b] = old < n_old ? T.outpos[old] : n_new; }
     g.sync();
-    if (g.rank == 0) { uint32_t *x = T.bo; T.bo = T.bo2; T.bo2 = x; T.n = n_new; T.fs.bo = T.bo; }
+    if (g.rank == 0) { uint32_t *x = T.bo; T.bo = T.bo2; T.bo2 = x; T.n = n_new; T.fs.bo = T.bo; T.du_ok = 0; }
     g.sync();
     /* function-relative positions are compared as 16-bit numbers (s_key, chain order) */
     const uint32_t nf = T.nf;
@@ -342,14 +359,18 @@ template <class G> CLD void s_rebase_blocks(const G &g, StreamS &T, uint32_t n_o
 }
 
 /* ------------------------------------------------------------------ def-use */
-/* ssa.py:613-636 for every live function at once                               */
+/* ssa.py:613-636 for every gated live function at once (the others' words keep what they held) */
 template <class G> CLF void s_usecount(const G &g, StreamS &T) {
-    const uint32_t vtot = T.vtot, n = T.n, nb = T.nb, V = T.cap.V;
-    SFOR(g, v, vtot) { T.usecnt[v] = 0; T.defpos[v] = NONE32; }
+    const uint32_t n = T.n, nb = T.nb, nf = T.nf, V = T.cap.V;
+    WFOR(g, f, nf) {
+        if (!sf_on(T, f)) continue;
+        const uint32_t vb = T.f_vbase[f], room = T.f_vbase[f + 1] - vb;
+        LFOR(g, v, room) { T.usecnt[vb + v] = 0; T.defpos[vb + v] = NONE32; }
+    }
     g.sync();
     SFOR(g, i, n) {
         const uint32_t f = T.fidx[i];
-        if (!sf_ok(T, f)) continue;
+        if (!sf_on(T, f)) continue;
         const RecR r = s_rec(T, i);
         const unsigned d0 = def0(r.h), nd = (unsigned)r.h.n_defs + r.h.n_aux;
         bool odd = false;
@@ -364,11 +385,13 @@ template <class G> CLF void s_usecount(const G &g, StreamS &T) {
         r_value_operands(T, r, [&](uint32_t v) { if (v < V) a_add(&T.usecnt[v], 1u); });
     }
     SFOR(g, b, nb) {
-        if (!sf_ok(T, T.bfun[b])) continue;
+        const uint32_t f = T.bfun[b];
+        if (!sf_on(T, f)) continue;
         for (int k = 0; k < 2; k++)
             if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE && T.blk[b].term_pay[k] < V)
                 a_add(&T.usecnt[T.blk[b].term_pay[k]], 1u);
     }
+    if (g.rank == 0) T.du_ok = 1;
     g.sync();
     s_mark(g, T, SP_USECOUNT);
 }
@@ -558,6 +581,7 @@ template <class G> CLF void s_match(const G &g, StreamS &T, unsigned table) {
             for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) { if (x < cap_items) items[x] = (unsigned long long)pi << 32 | i; x++; }
         });
     if (n_items > cap_items) { if (g.rank == 0) s_fail(T); g.sync(); return; }
+    if (g.rank == 0) T.n_items = n_items;
     s_mark(g, T, SP_ITEMS);
     /* budget (G1): where the product of the candidate-list sizes of a pattern exceeds it, a tuple counts only
      * if its rank in itertools.product order is below it; the rank needs every member's index inside its
@@ -708,10 +732,13 @@ CLF void s_apply_stage(StreamS &T, Stage &st, uint32_t out, uint32_t f, uint32_t
  * function would be seen by that block's escape test in the reference (G5):
  * such functions are redone sequentially.                                   */
 template <class G> CLF void s_apply_patterns(const G &g, StreamS &T, unsigned table, uint32_t phase) {
-    s_usecount(g, T);
+    if (!T.du_ok) s_usecount(g, T);
     s_match(g, T, table);
+    const uint32_t call = T.n_apply;
+    if (g.rank == 0 && call < 8) { T.rstat[call][1] = T.n_items; T.rstat[call][2] = T.n_mt; T.n_apply = call + 1; }
     if (T.fail || T.n_mt == 0) return;
     const uint32_t ns = s_select(g, T);
+    if (g.rank == 0 && call < 8) T.rstat[call][3] = ns;
     if (T.fail || ns == 0) return;
     const uint32_t n = T.n, nf = T.nf, nb = T.nb, V = T.cap.V;
     SFOR(g, p, n) { T.keep[p] = 1; T.inscnt[p] = 0; }
@@ -818,6 +845,7 @@ template <class G> CLF void s_apply_patterns(const G &g, StreamS &T, unsigned ta
     g.sync();
     s_rebase_blocks(g, T, n, tot);
     s_mark(g, T, SP_STAGE);
+    s_usecount(g, T);                        /* for simplify_packs / remove_dead_pseudo of this round */
 }
 
 /* ordered compaction of the stream by keep[]                                   */
@@ -828,32 +856,48 @@ template <class G> CLF void s_compact(const G &g, StreamS &T) {
     s_rebase_blocks(g, T, n, tot);
 }
 
-/* remove_dead_pseudo (patterns.py:771-791) for the functions with f_gate set   */
+/* remove_dead_pseudo (patterns.py:771-791) for the functions with f_gate set.  The first sweep visits the
+ * records; pure records that survive it are the only ones that can still die: later rounds of the fixpoint
+ * walk that list                                                                                            */
 template <class G> CLF void s_dce(const G &g, StreamS &T) {
-    s_usecount(g, T);
+    if (!T.du_ok) s_usecount(g, T);
     const uint32_t n = T.n, V = T.cap.V;
-    SFOR(g, i, n) T.keep[i] = 1;
+    uint32_t *list = (uint32_t *)T.owner;                 /* [<= n] <= [2 I] */
+    if (g.rank == 0) T.n_items = 0;
     g.sync();
+    auto try_kill = [&](uint32_t i, const cl_hdr &h) -> bool {
+        unsigned nd = 0; bool used = false;
+        s_value_defs(T, h, i, [&](uint32_t v) { nd++; used |= v < V && *(volatile uint32_t *)&T.usecnt[v] != 0; });
+        if (!nd) return true;                               /* never dies: not a candidate either */
+        if (used) return false;
+        T.keep[i] = 0;
+        s_value_defs(T, h, i, [&](uint32_t v) { if (v < V) T.alive[v] = 0; });
+        s_value_operands(T, h, i, [&](uint32_t v) { if (v < V) a_sub(&T.usecnt[v], 1u); });
+        return true;
+    };
+    uint32_t mine = 0;
+    SFOR(g, i, n) {
+        T.keep[i] = 1;
+        const uint32_t f = T.fidx[i];
+        if (!sf_on(T, f)) continue;
+        const cl_hdr h = T.hdr[i];
+        if (h.op >= CL_OP__COUNT || !(T.fs.opflags[h.op] & CL_OPF_PURE)) continue;
+        if (try_kill(i, h)) mine += T.keep[i] == 0;
+        else list[a_inc_agg(&T.n_items)] = i;
+    }
     uint32_t removed = 0;
     for (;;) {
-        uint32_t mine = 0;
-        SFOR(g, i, n) if (T.keep[i]) {
-            const uint32_t f = T.fidx[i];
-            if (!T.f_gate[f] || !sf_ok(T, f)) continue;
-            const cl_hdr h = T.hdr[i];
-            if (h.op >= CL_OP__COUNT || !(T.fs.opflags[h.op] & CL_OPF_PURE)) continue;
-            unsigned nd = 0; bool used = false;
-            s_value_defs(T, h, i, [&](uint32_t v) { nd++; used |= v < V && *(volatile uint32_t *)&T.usecnt[v] != 0; });
-            if (!nd || used) continue;
-            T.keep[i] = 0;
-            mine++;
-            s_value_defs(T, h, i, [&](uint32_t v) { if (v < V) T.alive[v] = 0; });
-            s_value_operands(T, h, i, [&](uint32_t v) { if (v < V) a_sub(&T.usecnt[v], 1u); });
-        }
         const uint32_t dead = g.sum(mine);
         if (g.rank == 0) T.iters[1]++;
         if (!dead) break;
         removed += dead;
+        mine = 0;
+        const uint32_t nl = T.n_items;
+        SFOR(g, k, nl) {
+            const uint32_t i = list[k];
+            if (!T.keep[i] || !sf_ok(T, T.fidx[i])) continue;
+            if (try_kill(i, T.hdr[i])) mine++;
+        }
     }
     if (removed) s_compact(g, T);
     s_mark(g, T, SP_DCE);
@@ -867,17 +911,21 @@ CLD uint32_t s_final_of(const StreamS &T, uint32_t v) {
 }
 template <class G> CLF void s_simplify(const G &g, StreamS &T) {
     const FS &s = T.fs;
-    s_usecount(g, T);
+    if (!T.du_ok) s_usecount(g, T);
     const uint32_t n = T.n, nf = T.nf, nb = T.nb, V = T.cap.V;
-    SFOR(g, v, T.vtot) T.redirect[v] = NONE32;
-    SFOR(g, f, nf) T.f_red[f] = 0;
+    WFOR(g, f, nf) {
+        if (g_lane(g) == 0) T.f_red[f] = 0;
+        if (!sf_on(T, f)) continue;
+        const uint32_t vb = T.f_vbase[f], room = T.f_vbase[f + 1] - vb;
+        LFOR(g, v, room) T.redirect[vb + v] = NONE32;
+    }
     g.sync();
     uint32_t mine = 0;
     SFOR(g, i, n) {
         const cl_hdr h = T.hdr[i];
         if (h.op != CL_OP_PACK64 || h.n_uses != 2) continue;
         const uint32_t f = T.fidx[i];
-        if (!T.f_gate[f] || !sf_ok(T, f)) continue;
+        if (!sf_on(T, f)) continue;
         const unsigned u0 = use0(h);
         const opnd lo = s_slot(T, i, u0), hi = s_slot(T, i, u0 + 1);
         if (!is_value(lo) || !is_value(hi)) continue;
@@ -899,6 +947,22 @@ template <class G> CLF void s_simplify(const G &g, StreamS &T) {
     }
     const uint32_t changed = g.sum(mine);
     if (!changed) { s_mark(g, T, SP_SIMPLIFY); return; }
+    /* the use counts follow the redirects (every use site of the old value becomes one of the new) */
+    auto move_use = [&](uint32_t v) {
+        const uint32_t fo = s_final_of(T, v);
+        if (fo != v && v < V) { a_sub(&T.usecnt[v], 1u); if (fo < V) a_add(&T.usecnt[fo], 1u); }
+    };
+    SFOR(g, i, n) {
+        const uint32_t f = T.fidx[i];
+        if (!T.f_red[f] || !sf_ok(T, f)) continue;
+        s_value_operands(T, T.hdr[i], i, move_use);
+    }
+    SFOR(g, b, nb) {
+        const uint32_t f = T.bfun[b];
+        if (!T.f_red[f] || !sf_ok(T, f)) continue;
+        for (int k = 0; k < 2; k++) if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE) move_use(T.blk[b].term_pay[k]);
+    }
+    g.sync();
     SFOR(g, i, n) {
         const uint32_t f = T.fidx[i];
         if (!T.f_red[f] || !sf_ok(T, f)) continue;
@@ -963,45 +1027,56 @@ template <class G> CLF void s_tag(const G &g, StreamS &T) {
 enum { SRF_R0 = 1, SRF_R1 = 2, SRF_R2 = 4, SRF_R3 = 8, SRF_SEED = 16, SRF_Q = 32, SRF_MUFU = 128 };
 template <class G> CLF void s_reciprocal(const G &g, StreamS &T) {
     const FS &s = T.fs;
-    const uint32_t n = T.n, nf = T.nf, V = T.cap.V, vtot = T.vtot;
-    s_usecount(g, T);
+    const uint32_t n = T.n, nf = T.nf, V = T.cap.V;
     SFOR(g, f, nf) { T.f_aux[f] = 0; T.f_gate[f] = 0; }
     if (g.rank == 0) T.n_chain = 0;
     g.sync();
-    /* R_0 and the MUFU.RCP records fed by an I2F */
+    /* only functions that hold a MUFU.RCP take part */
     bool mine = false;
     SFOR(g, i, n) {
         const cl_hdr h = T.hdr[i];
-        uint8_t fl = h.op == CL_OP_F2I ? (uint8_t)(SRF_R0 | SRF_R1 | SRF_R2 | SRF_R3) : (uint8_t)0;
+        if (h.op != CL_OP_MUFU || !has_mod(s, h, CL_MB_RCP) || !h.n_uses) continue;
         const uint32_t f = T.fidx[i];
+        if (sf_ok(T, f)) { T.f_gate[f] = 1; mine = true; }
+    }
+    if (!g.any(mine)) return;
+    s_usecount(g, T);
+    /* R_0 and the MUFU.RCP records fed by an I2F */
+    SFOR(g, i, n) {
+        const uint32_t f = T.fidx[i];
+        if (!T.f_gate[f]) continue;
+        const cl_hdr h = T.hdr[i];
+        uint8_t fl = h.op == CL_OP_F2I ? (uint8_t)(SRF_R0 | SRF_R1 | SRF_R2 | SRF_R3) : (uint8_t)0;
         if (h.op == CL_OP_MUFU && sf_ok(T, f) && has_mod(s, h, CL_MB_RCP) && h.n_uses) {
             const opnd src = s_slot(T, i, use0(h));
             if (is_value(src) && src.pay < V) {
                 const uint32_t dp = T.defpos[src.pay];
                 if (dp != NONE32 && T.hdr[dp].op == CL_OP_I2F) {
                     if (!h.n_defs || !is_value(s_slot(T, i, def0(h)))) sf_fail(T, f, CLS_REDO + 9);   /* IndexError / AttributeError */
-                    else { fl |= SRF_MUFU; T.f_gate[f] = 1; mine = true; }
+                    else fl |= SRF_MUFU;
                 }
             }
         }
         T.flag[i] = fl;
-        T.keep[i] = 0; T.inscnt[i] = 0;
     }
-    if (!g.any(mine)) return;
     uint32_t *valbits = T.redirect;
-    SFOR(g, v, vtot) valbits[v] = 0;
+    WFOR(g, f, nf) {
+        if (!T.f_gate[f]) continue;
+        const uint32_t vb = T.f_vbase[f], room = T.f_vbase[f + 1] - vb;
+        LFOR(g, v, room) valbits[vb + v] = 0;
+    }
     g.sync();
     for (unsigned k = 1; k <= 3; k++) {
         const uint8_t prev = (uint8_t)(1u << (k - 1)), cur = (uint8_t)(1u << k);
         SFOR(g, i, n) if (T.flag[i] & prev) {
             const uint32_t f = T.fidx[i];
-            if (!T.f_gate[f] || !sf_ok(T, f)) continue;
+            if (!sf_on(T, f)) continue;
             s_value_operands(T, T.hdr[i], i, [&](uint32_t v) { if (v < V) valbits[v] |= cur; });
         }
         g.sync();
         SFOR(g, i, n) if (!(T.flag[i] & cur)) {
             const uint32_t f = T.fidx[i];
-            if (!T.f_gate[f] || !sf_ok(T, f)) continue;
+            if (!sf_on(T, f)) continue;
             bool r = false;
             s_value_defs(T, T.hdr[i], i, [&](uint32_t v) { r |= v < V && (valbits[v] & cur); });
             if (r) T.flag[i] |= (uint8_t)((0xFu << k) & 0xFu);        /* R_k implies R_k+1.. */
@@ -1011,7 +1086,7 @@ template <class G> CLF void s_reciprocal(const G &g, StreamS &T) {
     /* accepted chains */
     SFOR(g, i, n) {
         const uint32_t f = T.fidx[i];
-        if (!T.f_gate[f] || !sf_ok(T, f)) continue;
+        if (!sf_on(T, f)) continue;
         const cl_hdr h = T.hdr[i];
         if (h.op != CL_OP_IADD && h.op != CL_OP_IADD3) continue;
         bool any_imm = false;
@@ -1044,6 +1119,7 @@ template <class G> CLF void s_reciprocal(const G &g, StreamS &T) {
     g.sync();
     const uint32_t nc = T.n_chain;
     if (nc == 0 || T.fail) return;
+    SFOR(g, i, n) { T.keep[i] = 0; T.inscnt[i] = 0; }
     /* interference (tile.cuh): _reaches_f2i reads the user lists of the records at distance 0..2 of the add it
      * starts from, and a rewritten chain changes the user lists of its MUFU's and its add's results.  Chains are
      * rewritten in (MUFU, add) position order, so chain B can only see a chain A of smaller order whose add or
@@ -1051,7 +1127,11 @@ template <class G> CLF void s_reciprocal(const G &g, StreamS &T) {
      * the function's first record (16 bits, s_load hands bigger functions back).
      * owner[i] = { low: own seed order, high: smallest order reached in one hop }.                          */
     uint32_t *mk1 = T.redirect, *mk2 = T.usecnt;
-    SFOR(g, v, vtot) { mk1[v] = NONE32; mk2[v] = NONE32; }
+    WFOR(g, f, nf) {
+        if (!T.f_gate[f]) continue;
+        const uint32_t vb = T.f_vbase[f], room = T.f_vbase[f + 1] - vb;
+        LFOR(g, v, room) { mk1[vb + v] = NONE32; mk2[vb + v] = NONE32; }
+    }
     SFOR(g, i, n) if (T.f_gate[T.fidx[i]]) T.owner[i] = NONE64;
     g.sync();
     auto key_of = [&](const SChain &ch) -> uint32_t {
@@ -1066,14 +1146,15 @@ template <class G> CLF void s_reciprocal(const G &g, StreamS &T) {
     }
     g.sync();
     SFOR(g, i, n) if (T.flag[i] & SRF_SEED) {
-        if (!sf_ok(T, T.fidx[i])) continue;
+        const uint32_t f = T.fidx[i];
+        if (!sf_on(T, f)) continue;
         const uint32_t key = (uint32_t)T.owner[i];
         s_value_operands(T, T.hdr[i], i, [&](uint32_t v) { if (v < V) a_min32(&mk1[v], key); });
     }
     g.sync();
     SFOR(g, i, n) {
         const uint32_t f = T.fidx[i];
-        if (!T.f_gate[f] || !sf_ok(T, f)) continue;
+        if (!sf_on(T, f)) continue;
         uint32_t q1 = NONE32;
         s_value_defs(T, T.hdr[i], i, [&](uint32_t v) { if (v < V && mk1[v] < q1) q1 = mk1[v]; });
         if (q1 != NONE32) T.owner[i] = (T.owner[i] & 0xFFFFFFFFull) | (unsigned long long)q1 << 32;
@@ -1081,7 +1162,7 @@ template <class G> CLF void s_reciprocal(const G &g, StreamS &T) {
     g.sync();
     SFOR(g, i, n) {
         const uint32_t f = T.fidx[i];
-        if (!T.f_gate[f] || !sf_ok(T, f) || T.owner[i] == NONE64) continue;
+        if (!sf_on(T, f) || T.owner[i] == NONE64) continue;
         const uint32_t own = (uint32_t)T.owner[i], q1 = (uint32_t)(T.owner[i] >> 32);
         const uint32_t key = own < q1 ? own : q1;
         s_value_operands(T, T.hdr[i], i, [&](uint32_t v) { if (v < V) a_min32(&mk2[v], key); });
@@ -1096,7 +1177,11 @@ template <class G> CLF void s_reciprocal(const G &g, StreamS &T) {
     }
     g.sync();
     /* rank, ids, value table; vmap (usecnt[]) = add result -> its float view */
-    SFOR(g, v, vtot) T.usecnt[v] = NONE32;
+    WFOR(g, f, nf) {
+        if (!T.f_gate[f]) continue;
+        const uint32_t vb = T.f_vbase[f], room = T.f_vbase[f + 1] - vb;
+        LFOR(g, v, room) T.usecnt[vb + v] = NONE32;
+    }
     /* number of a chain inside its function = chains of earlier MUFUs (scan over the records) + chains of
      * the same MUFU with an earlier add (a short list per MUFU: owner[m] low word = head, SChain.rank = next) */
     SFOR(g, i, n) if (T.f_gate[T.fidx[i]]) T.owner[i] = 0xFFFFFFFFull;        /* high word: chains of this MUFU */
@@ -1412,8 +1497,11 @@ template <class G> CLF void s_store(const G &g, StreamS &T, const StreamIO &a) {
 
 /* the four calls of pipeline.py:165-169 on every function of the corpus        */
 template <class G> CLF void s_set_gate(const G &g, StreamS &T, int mode) {
-    /* 0: live sm52 functions, 1: live active functions, 2: live functions with redirects, 3: all live */
+    /* 0: live sm52 functions, 1: live active functions, 2: live functions with redirects, 3: all live.
+     * Modes 1 and 2 only ever narrow the gate inside the aggregation loop, so use counts stay valid for it;
+     * modes 0 and 3 start over.                                                                           */
     const uint32_t nf = T.nf;
+    if (g.rank == 0 && (mode == 0 || mode == 3)) T.du_ok = 0;
     SFOR(g, f, nf) {
         bool on = sf_ok(T, f);
         if (mode == 0) on = on && T.f_arch[f] == CL_ARCH_SM52;
@@ -1436,16 +1524,17 @@ template <class G> CLF void s_run(const G &g, StreamS &T, const StreamIO &a) {
     s_mark(g, T, SP_LOAD);
     const uint32_t nf = T.nf;
     if (!T.fail && (passes & CL_PASS_XMAD)) {
-        s_set_gate(g, T, 0);
+        s_set_gate(g, T, 0);       /* also: du_ok = 0 (the gate widened or changed) */
         if (s_any_gate(g, T)) {
             s_apply_patterns(g, T, 1, 0);
-            if (!T.fail) { s_set_gate(g, T, 0); s_dce(g, T); }
+            if (!T.fail) s_dce(g, T);
         }
     }
     s_mark(g, T, SP_GATE);
     if (!T.fail && (passes & CL_PASS_RECIPROCAL)) { s_reciprocal(g, T); s_mark(g, T, SP_RECIP); }
     if (!T.fail && (passes & CL_PASS_AGGREGATE)) {
         SFOR(g, f, nf) T.f_active[f] = 1;
+        if (g.rank == 0) T.du_ok = 0;
         g.sync();
         for (uint32_t round = 0; round < max_rounds && !T.fail; round++) {
             s_set_gate(g, T, 1);

@@ -99,12 +99,13 @@ template <class C> struct TileS {
     uint32_t f_chg[C::F], f_red[C::F], f_first[C::F], f_aux[C::F], f_nin[C::F];
     uint32_t f_oi[C::F], f_oq[C::F], f_ov[C::F], f_oe[C::F];
     uint32_t f_stats[C::F][64];
-    uint8_t f_arch[C::F], f_active[C::F], f_odd[C::F], f_gate[C::F];
+    uint8_t f_arch[C::F], f_active[C::F], f_odd[C::F], f_gate[C::F], f_rgate[C::F];
     /* the one function state of the tile + tile scalars */
     const struct TileP *P;
     FS fs;
     unsigned long long prof[PF__N];
     uint32_t n, nb, nf, n_mt, n_sel, n_ev, fail, vtot, qtot, n_chain, work;
+    uint32_t du_ok, n_list;       /* du_ok: usecnt / defpos describe the stream (every live function) */
     uint32_t red[40];
 };
 
@@ -253,7 +254,7 @@ template <class G, class C> CLD void t_rebase_blocks(const G &g, TileS<C> &T, ui
     GFOR(g, b, T.nb + 1) if (b <= T.nb) { const uint32_t old = T.bo[b]; T.bo2[b] = old < n_old ? (uint32_t)T.outpos[old] : n_new; }
     g.sync();
     GFOR(g, b, T.nb + 1) if (b <= T.nb) T.bo[b] = T.bo2[b];
-    if (g.rank == 0) T.n = n_new;
+    if (g.rank == 0) { T.n = n_new; T.du_ok = 0; }
     g.sync();
 }
 
@@ -284,6 +285,7 @@ template <class G, class C> CLF void t_usecount(const G &g, TileS<C> &T, const T
             if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE && T.blk[b].term_pay[k] < C::V)
                 a_add(&T.usecnt[T.blk[b].term_pay[k]], 1u);
     }
+    if (g.rank == 0) T.du_ok = 1;
     g.sync();
 }
 
@@ -608,7 +610,7 @@ template <class C> CLF void t_apply_stage(TileS<C> &T, Stage &st, uint32_t out) 
  * such functions are redone sequentially.                                   */
 template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, const TileG<C> &tg, unsigned table,
                                                       uint32_t phase) {
-    t_usecount(g, T, tg);
+    if (!T.du_ok) t_usecount(g, T, tg);
     t_match(g, T, tg, table);
     if (T.fail || T.n_mt == 0) return;
     const uint32_t ns = t_select(g, T);
@@ -713,6 +715,7 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     g.sync();
     t_rebase_blocks(g, T, n, tot);
     t_index(g, T);
+    t_usecount(g, T, tg);                    /* for simplify_packs / remove_dead_pseudo of this round */
 }
 
 /* ordered in-place compaction of the stream by keep[]                         */
@@ -726,32 +729,48 @@ template <class G, class C> CLF void t_compact(const G &g, TileS<C> &T, const Ti
     t_index(g, T);
 }
 
-/* remove_dead_pseudo (patterns.py:771-791) for the functions with f_gate set   */
+/* remove_dead_pseudo (patterns.py:771-791) for the functions with f_gate set.  The first sweep visits the
+ * records; pure records that survive it are the only ones that can still die: the later rounds of the
+ * fixpoint walk that list                                                                               */
 template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<C> &tg) {
     PROF(g, T.fs, PF_DCE);
-    t_usecount(g, T, tg);
-    GFOR(g, i, T.n) if (i < T.n) T.keep[i] = 1;
+    if (!T.du_ok) t_usecount(g, T, tg);
+    uint32_t *list = (uint32_t *)T.owner;                 /* [<= I] */
+    if (g.rank == 0) T.n_list = 0;
     g.sync();
+    auto try_kill = [&](uint32_t i, const cl_hdr &h) -> bool {
+        unsigned nd = 0; bool used = false;
+        t_value_defs(T, h, i, [&](uint32_t v) { nd++; used |= v < C::V && *(volatile uint32_t *)&T.usecnt[v] != 0; });
+        if (!nd) return true;                               /* never dies: not a candidate either */
+        if (used) return false;
+        T.keep[i] = 0;
+        t_value_defs(T, h, i, [&](uint32_t v) { if (v < C::V) T.alive[v] = 0; });
+        t_value_operands(T, tg, h, i, [&](uint32_t v) { if (v < C::V) a_sub(&T.usecnt[v], 1u); });
+        return true;
+    };
+    uint32_t mine = 0;
+    GFOR(g, i, T.n) if (i < T.n) {
+        T.keep[i] = 1;
+        const uint32_t f = T.fidx[i];
+        if (!T.f_gate[f] || !tf_ok(T, f)) continue;
+        const cl_hdr h = T.hdr[i];
+        if (h.op >= CL_OP__COUNT || !(T.fs.opflags[h.op] & CL_OPF_PURE)) continue;
+        if (try_kill(i, h)) mine += T.keep[i] == 0;
+        else list[a_add(&T.n_list, 1u)] = i;
+    }
     uint32_t removed = 0;
     for (;;) {
-        uint32_t mine = 0;
-        GFOR(g, i, T.n) if (i < T.n && T.keep[i]) {
-            const uint32_t f = T.fidx[i];
-            if (!T.f_gate[f] || !tf_ok(T, f)) continue;
-            const cl_hdr h = T.hdr[i];
-            if (h.op >= CL_OP__COUNT || !(T.fs.opflags[h.op] & CL_OPF_PURE)) continue;
-            unsigned nd = 0; bool used = false;
-            t_value_defs(T, h, i, [&](uint32_t v) { nd++; used |= v < C::V && *(volatile uint32_t *)&T.usecnt[v] != 0; });
-            if (!nd || used) continue;
-            T.keep[i] = 0;
-            mine++;
-            t_value_defs(T, h, i, [&](uint32_t v) { if (v < C::V) T.alive[v] = 0; });
-            t_value_operands(T, tg, h, i, [&](uint32_t v) { if (v < C::V) a_sub(&T.usecnt[v], 1u); });
-        }
         const uint32_t dead = g.sum(mine);
         g.sync();
         if (!dead) break;
         removed += dead;
+        mine = 0;
+        const uint32_t nl = T.n_list;
+        GFOR(g, k, nl) if (k < nl) {
+            const uint32_t i = list[k];
+            if (!T.keep[i] || !tf_ok(T, T.fidx[i])) continue;
+            if (try_kill(i, T.hdr[i])) mine++;
+        }
     }
     if (removed) t_compact(g, T, tg);
 }
@@ -765,7 +784,7 @@ template <class C> CLD uint32_t t_final_of(const TileS<C> &T, uint32_t v) {
 template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const TileG<C> &tg) {
     PROF(g, T.fs, PF_SIMPLIFY);
     const FS &s = T.fs;
-    t_usecount(g, T, tg);
+    if (!T.du_ok) t_usecount(g, T, tg);
     GFOR(g, v, T.vtot) if (v < T.vtot) T.redirect[v] = NONE32;
     GFOR(g, f, T.nf) if (f < T.nf) T.f_red[f] = 0;
     g.sync();
@@ -797,6 +816,22 @@ template <class G, class C> CLF void t_simplify(const G &g, TileS<C> &T, const T
     const uint32_t changed = g.sum(mine);
     g.sync();
     if (!changed) return;
+    /* the use counts follow the redirects (every use site of the old value becomes one of the new) */
+    auto move_use = [&](uint32_t v) {
+        const uint32_t fo = t_final_of(T, v);
+        if (fo != v && v < C::V) { a_sub(&T.usecnt[v], 1u); if (fo < C::V) a_add(&T.usecnt[fo], 1u); }
+    };
+    GFOR(g, i, T.n) if (i < T.n) {
+        const uint32_t f = T.fidx[i];
+        if (!T.f_red[f] || !tf_ok(T, f)) continue;
+        t_value_operands(T, tg, T.hdr[i], i, move_use);
+    }
+    GFOR(g, b, T.nb) if (b < T.nb) {
+        const uint32_t f = T.bfun[b];
+        if (!T.f_red[f] || !tf_ok(T, f)) continue;
+        for (int k = 0; k < 2; k++) if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE) move_use(T.blk[b].term_pay[k]);
+    }
+    g.sync();
     GFOR(g, i, T.n) if (i < T.n) {
         const uint32_t f = T.fidx[i];
         if (!T.f_red[f] || !tf_ok(T, f)) continue;
@@ -869,10 +904,14 @@ enum { RF_R0 = 1, RF_R1 = 2, RF_R2 = 4, RF_R3 = 8, RF_SEED = 16, RF_Q = 32, RF_M
 template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const TileG<C> &tg) {
     PROF(g, T.fs, PF_RECIP);
     const FS &s = T.fs;
+    /* only functions that hold a MUFU.RCP take part (f_rgate; cleared by t_load) */
     bool mine = false;
-    GFOR(g, i, T.n) if (i < T.n) { const cl_hdr h = T.hdr[i]; mine |= h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP); }
+    GFOR(g, i, T.n) if (i < T.n) {
+        const cl_hdr h = T.hdr[i];
+        if (h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP)) { mine = true; T.f_rgate[T.fidx[i]] = 1; }
+    }
     if (!g.any(mine)) return;
-    t_usecount(g, T, tg);
+    if (!T.du_ok) t_usecount(g, T, tg);
     const uint32_t n = T.n;
     uint32_t *valbits = T.redirect;
     GFOR(g, v, T.vtot) if (v < T.vtot) valbits[v] = 0;
@@ -880,9 +919,10 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     if (g.rank == 0) T.n_chain = 0;
     /* R_0 and the MUFU.RCP records fed by an I2F */
     GFOR(g, i, n) if (i < n) {
+        const uint32_t f = T.fidx[i];
+        if (!T.f_rgate[f]) continue;
         const cl_hdr h = T.hdr[i];
         uint8_t fl = h.op == CL_OP_F2I ? (uint8_t)(RF_R0 | RF_R1 | RF_R2 | RF_R3) : (uint8_t)0;
-        const uint32_t f = T.fidx[i];
         if (h.op == CL_OP_MUFU && tf_ok(T, f) && has_mod(s, h, CL_MB_RCP) && h.n_uses) {
             const opnd src = t_slot(T, i, use0(h));
             if (is_value(src) && src.pay < C::V) {
@@ -894,17 +934,16 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
             }
         }
         T.flag[i] = fl;
-        T.keep[i] = 0; T.inscnt[i] = 0;
     }
     g.sync();
     for (unsigned k = 1; k <= 3; k++) {
         const uint8_t prev = (uint8_t)(1u << (k - 1)), cur = (uint8_t)(1u << k);
-        GFOR(g, i, n) if (i < n && (T.flag[i] & prev)) {
+        GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && (T.flag[i] & prev)) {
             if (!tf_ok(T, T.fidx[i])) continue;
             t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) valbits[v] |= cur; });
         }
         g.sync();
-        GFOR(g, i, n) if (i < n && !(T.flag[i] & cur)) {
+        GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && !(T.flag[i] & cur)) {
             if (!tf_ok(T, T.fidx[i])) continue;
             bool r = false;
             t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { r |= v < C::V && (valbits[v] & cur); });
@@ -914,10 +953,10 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     }
     /* accepted chains */
     GFOR(g, i, n) if (i < n) {
+        const uint32_t f = T.fidx[i];
+        if (!T.f_rgate[f] || !tf_ok(T, f)) continue;
         const cl_hdr h = T.hdr[i];
         if (h.op != CL_OP_IADD && h.op != CL_OP_IADD3) continue;
-        const uint32_t f = T.fidx[i];
-        if (!tf_ok(T, f)) continue;
         bool any_imm = false;
         const unsigned u0 = use0(h);
         for (unsigned k = 0; k < h.n_uses; k++) any_imm |= is_imm(t_slot(T, i, u0 + k));
@@ -948,6 +987,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     g.sync();
     const uint32_t nc = T.n_chain;
     if (nc == 0 || T.fail) return;
+    GFOR(g, i, n) if (i < n) { T.keep[i] = 0; T.inscnt[i] = 0; }
     /* interference.  _reaches_f2i reads the user lists of the records at distance 0..2 of the add it starts
      * from (at distance 3 only the opcode), and a rewritten chain changes the user lists of its MUFU's and
      * its add's results.  Chains are rewritten in (MUFU, add) position order, so chain B can only see a
@@ -965,13 +1005,13 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         a_min32((uint32_t *)&T.owner[ch.mufu], key);
     }
     g.sync();
-    GFOR(g, i, n) if (i < n && (T.flag[i] & RF_SEED)) {
+    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && (T.flag[i] & RF_SEED)) {
         if (!tf_ok(T, T.fidx[i])) continue;
         const uint32_t key = (uint32_t)T.owner[i];
         t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) a_min32(&mk1[v], key); });
     }
     g.sync();
-    GFOR(g, i, n) if (i < n) {
+    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]]) {
         if (!tf_ok(T, T.fidx[i])) continue;
         uint32_t q1 = NONE32;
         t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { if (v < C::V && mk1[v] < q1) q1 = mk1[v]; });
@@ -1139,7 +1179,7 @@ template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, TileG<C> &t
     if (g.rank == 0) {
         T.fs.mem = tg.mem;
         T.nf = nf;
-        T.n_ev = 0; T.fail = 0; T.n_chain = 0; T.n_mt = 0; T.n_sel = 0;
+        T.n_ev = 0; T.fail = 0; T.n_chain = 0; T.n_mt = 0; T.n_sel = 0; T.du_ok = 0; T.n_list = 0;
     }
     GFOR(g, f, nf) if (f < nf) {
         const uint32_t gf = a.flist[td.first + f];
@@ -1153,7 +1193,7 @@ template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, TileG<C> &t
         T.f_mbase[f] = in.mem_off[gf]; T.f_nin[f] = nrec;
         T.f_oi[f] = tile_vcap(fn.next_vid, nrec); T.f_oq[f] = tile_qcap(nimm, nrec);     /* slice sizes, scanned below */
         T.f_ov[f] = b1 - b0;
-        T.f_active[f] = 0; T.f_gate[f] = 0; T.f_chg[f] = 0; T.f_red[f] = 0; T.f_aux[f] = 0;
+        T.f_active[f] = 0; T.f_gate[f] = 0; T.f_rgate[f] = 0; T.f_chg[f] = 0; T.f_red[f] = 0; T.f_aux[f] = 0;
     }
     GFOR(g, k, nf * 64) if (k < nf * 64) (&T.f_stats[0][0])[k] = 0;
     g.sync();
@@ -1355,7 +1395,7 @@ template <class G, class C> CLF void t_run_tile(const G &g, TileS<C> &T, TileG<C
         t_set_gate(g, T, 0);
         if (t_any_gate(g, T)) {
             t_apply_patterns(g, T, tg, 1, 0);
-            if (!T.fail) { t_set_gate(g, T, 0); t_dce(g, T, tg); }
+            if (!T.fail) t_dce(g, T, tg);
         }
     }
     if (!T.fail && (passes & CL_PASS_RECIPROCAL)) t_reciprocal(g, T, tg);
