@@ -820,8 +820,9 @@ struct cl_ctx {
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr, *d_big_rest = nullptr;
     uint32_t *d_retry_big = nullptr, *d_retry_big_count = nullptr, *d_retry_big_counter = nullptr;   /* large functions the tile kernel hands back */
     uint32_t n_tile_funcs = 0, h_retry = 0, n_launches = 0; bool used_tiles = false;
-    int stream_mode = 1;       /* 1: the production post-SSA stage runs as corpus-wide streaming passes (stream.cuh); 0: tile kernels */
+    int stream_mode = cls_default_mode();   /* 1: the production post-SSA stage runs as corpus-wide streaming passes (stream.cuh); 0: tile kernels */
     cls_ctx *cls = nullptr; bool used_stream = false;
+    DenseArgs dense{}; bool have_dense = false;     /* dense result of the last run (device) */
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
     int cta_warps = 8;         /* warps per CTA of the CTA-group kernel (8, 16 or 32) */        /* warps per CTA of the phase-synchronous warp kernel (0 = free-running kernel) */
@@ -958,7 +959,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     CUDA_OK(cudaSetDevice(c->device));
     CUDA_OK(cudaStreamSynchronize(c->stream));
 #endif
-    c->have_in = c->have_out = false;
+    c->have_in = c->have_out = c->have_dense = false;
     const uint32_t F = in->n_funcs, B = in->n_blocks;
     if (in->func_blk_off[F] != B) FAIL("func_blk_off[n_funcs] != n_blocks");
     c->F = F; c->B = B; c->n_modsets = in->n_modsets;
@@ -1326,6 +1327,7 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
 #endif
 }
 
+static int densify(cl_ctx *c);
 static int run(cl_ctx *c, KArgs k) {
     if (!c->have_in) FAIL("no corpus uploaded");
 #if CL_CUDA
@@ -1399,7 +1401,8 @@ static int run(cl_ctx *c, KArgs k) {
 #endif
     c->h_retry += h_retry_big;
     c->have_out = true;
-    return 0;
+    c->have_dense = false;
+    return densify(c);
 }
 
 extern "C" int cl_run_postssa(cl_ctx *c, const cl_run_opts *opts) {
@@ -1452,16 +1455,15 @@ static void densify_host(const DenseArgs &a) {
 }
 #endif
 
-/* densify on the device, then D2H straight into the caller's arrays          */
-extern "C" int cl_download(cl_ctx *c, cl_corpus *o, cl_event *events) {
+/* results of the last run to the dense CSR of the ABI, on the device.  Enqueued by the run itself
+ * (right behind its kernels), so that a later cl_download is a plain copy that overlaps the kernels
+ * of other contexts instead of queueing behind their persistent grids                           */
+static int densify(cl_ctx *c) {
     uint64_t sz[6];
     if (cl_out_sizes(c, sz)) return -1;
     const uint32_t F = c->F, B = c->B;
     const KArgs &k = c->k;
-#if CL_CUDA
-    CUDA_OK(cudaSetDevice(c->device));
-#endif
-    DenseArgs a;
+    DenseArgs &a = c->dense;
     memset(&a, 0, sizeof a);
     a.fo = k.o_func; a.n_funcs = F; a.n_blocks = B;
     a.func_blk_off = c->d_in.func_blk_off; a.blk_start = k.o_blk_start; a.blk_cnt = k.o_blk_cnt;
@@ -1486,10 +1488,26 @@ extern "C" int cl_download(cl_ctx *c, cl_corpus *o, cl_event *events) {
         k_scan_apply<<<a.n_scan_blocks, SCAN_T, 0, c->stream>>>(a);
         k_densify<<<std::min<uint32_t>((F + 7) / 8, (uint32_t)c->n_sm * 16), 256, 0, c->stream>>>(a);
         CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaStreamSynchronize(c->stream));
     }
 #else
     densify_host(a);
 #endif
+    c->have_dense = true;
+    return 0;
+}
+
+/* D2H of the dense result straight into the caller's arrays                     */
+extern "C" int cl_download(cl_ctx *c, cl_corpus *o, cl_event *events) {
+    uint64_t sz[6];
+    if (cl_out_sizes(c, sz)) return -1;
+    const uint32_t F = c->F, B = c->B;
+    const KArgs &k = c->k;
+#if CL_CUDA
+    CUDA_OK(cudaSetDevice(c->device));
+#endif
+    if (!c->have_dense && densify(c)) return -1;
+    const DenseArgs &a = c->dense;
     o->n_funcs = F; o->n_blocks = B; o->n_modsets = c->n_modsets;
     if (d2h(o->func, a.d_func, F * sizeof(cl_func), c->stream) || d2h(o->func_blk_off, c->d_in.func_blk_off, 4ull * (F + 1), c->stream) ||
         d2h(o->ext_off, c->d_in.ext_off, 4ull * (F + 1), c->stream) || d2h(o->mem_off, c->d_in.mem_off, 4ull * (F + 1), c->stream) ||

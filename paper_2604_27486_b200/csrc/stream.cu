@@ -23,7 +23,7 @@
 using namespace clk;
 
 #ifndef CLS_MINB
-#define CLS_MINB 4            /* CTAs of 256 threads per SM the register budget is set for */
+#define CLS_MINB 6            /* CTAs of 256 threads per SM the register budget is set for */
 #endif
 
 #if CLS_CUDA
@@ -79,6 +79,9 @@ template <class T> static int take(cls_ctx *c, T **p, size_t n, char *err, size_
     return 0;
 }
 
+/* measured on B200 (profiles/r01_tuning.md, 100M mixed corpus): tile kernels 302 M inst/s, streaming passes 216 M inst/s */
+int cls_default_mode(void) { return 0; }
+
 int cls_create(cls_ctx **out, int device, int n_sm) {
     cls_ctx *c = new cls_ctx();
     c->device = device; c->n_sm = n_sm;
@@ -109,6 +112,11 @@ int cls_profile(const cls_ctx *c, unsigned long long *prof, int n, uint32_t iter
 #endif
     for (int i = 0; i < n && i < SP__N; i++) prof[i] = h.prof[i];
     for (int i = 0; i < 4; i++) iters[i] = h.iters[i];
+    if (getenv("CL_PROF")) {
+        fprintf(stderr, "hand-backs by reason:");
+        for (int r = 0; r < 24; r++) if (h.redo[r]) fprintf(stderr, " [%d] %u", r, h.redo[r]);
+        fprintf(stderr, "\n");
+    }
     if (getenv("CL_PROF")) for (uint32_t r = 0; r < h.n_apply && r < 8; r++)
         fprintf(stderr, "apply_patterns call %u: items %u raw matches %u selected %u (stream %u records)\n", r, h.rstat[r][1], h.rstat[r][2], h.rstat[r][3], h.n);
     return SP__N;

@@ -93,6 +93,7 @@ struct StreamS {
     uint32_t iters[4];                                           /* select / dce fixpoint iterations, rounds */
     uint32_t rstat[8][4];                                        /* per apply_patterns call: gated records, work items, raw matches, selected */
     uint32_t n_apply;
+    uint32_t redo[24];                                           /* hand-backs by reason (status - CLS_REDO), [23]: whole-stage failure */
 };
 
 struct StreamIO {              /* the part of KArgs the stream kernel needs */
@@ -1415,6 +1416,8 @@ template <class G> CLF void s_store(const G &g, StreamS &T, const StreamIO &a) {
     WFOR(g, f, nf) {
         if (!live(f)) {
             if (g_lane(g) == 0) {
+                const uint32_t why = T.f_stat[f] >= CLS_REDO && T.f_stat[f] < CLS_REDO + 23 ? T.f_stat[f] - CLS_REDO : 22u;
+                a_add(&T.redo[all_ok ? why : 23u], 1u);
                 if (T.f_nin[f] > a.small_max) a.retry_big_list[a_add(a.retry_big_count, 1u)] = f;
                 else a.retry_list[a_add(a.retry_count, 1u)] = f;
             }

@@ -17,3 +17,5 @@ int cls_run(cls_ctx *c, const cls_job *job, void *stream, char *err, size_t errl
 /* {grid, launches, device bytes held} of the last run */
 void cls_info(const cls_ctx *c, unsigned long long out[4]);
 int cls_profile(const cls_ctx *c, unsigned long long *prof, int n, uint32_t iters[4]);
+/* which path takes the production run when CL_STREAM is not set: 1 = streaming passes, 0 = tile kernels */
+int cls_default_mode(void);

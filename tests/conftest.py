@@ -41,3 +41,16 @@ def sim_tile_engine():
 def cuda_tile_engine():
     import helpers
     return helpers.cuda_engine(stream=False)
+
+
+@pytest.fixture(scope="session")
+def sim_stream_engine():
+    """context with the corpus-wide streaming path on"""
+    import helpers
+    return helpers.sim_engine(stream=True)
+
+
+@pytest.fixture(scope="session")
+def cuda_stream_engine():
+    import helpers
+    return helpers.cuda_engine(stream=True)

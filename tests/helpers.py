@@ -69,12 +69,17 @@ def _engine_with_env(path, **env):
                 os.environ[k] = v
 
 
-def sim_engine(stream=True):
+def sim_engine(stream=None):
+    """stream: True / False selects the streaming or the tile path, None the library's default"""
+    if stream is None:
+        return Engine(build_sim())
     return _engine_with_env(build_sim(), CL_STREAM=int(stream))
 
 
-def cuda_engine(stream=True):
+def cuda_engine(stream=None):
     # the product library; raises without GPU / without the .so
+    if stream is None:
+        return Engine()
     return _engine_with_env(None, CL_STREAM=int(stream))
 
 

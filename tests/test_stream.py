@@ -30,40 +30,55 @@ def _check(engine, oracle, kind, n_sass, seed, passes=15, max_back=0.05):
     return part
 
 
-@pytest.mark.parametrize("kind,n_sass", [("sm52", 60_000), ("sm75", 60_000), ("sm90", 60_000), ("mixed", 120_000)])
-def test_stream_logic_sim(sim_engine, oracle_engine, kind, n_sass):
+@pytest.mark.parametrize("kind,n_sass", [("sm52", 60_000), ("sm75", 60_000), ("sm90", 60_000), ("mixed", 120_000), ("long", 60_000)])
+def test_stream_logic_sim(sim_stream_engine, oracle_engine, kind, n_sass):
     """one-lane CPU build of the streaming code (logic only)"""
-    _check(sim_engine, oracle_engine, kind, n_sass, seed=11)
+    _check(sim_stream_engine, oracle_engine, kind, n_sass, seed=11)
 
 
 @pytest.mark.parametrize("passes", [1, 2, 4, 8, 6, 7])
-def test_stream_pass_subsets_sim(sim_engine, oracle_engine, passes):
-    _check(sim_engine, oracle_engine, "mixed", 40_000, seed=3, passes=passes, max_back=1.0)
+def test_stream_pass_subsets_sim(sim_stream_engine, oracle_engine, passes):
+    _check(sim_stream_engine, oracle_engine, "mixed", 40_000, seed=3, passes=passes, max_back=1.0)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("kind,n_sass,seed", [("sm52", 400_000, 1), ("sm75", 400_000, 2), ("sm90", 400_000, 3),
                                               ("mixed", 1_500_000, 4), ("mixed", 300_000, 5)])
-def test_stream_cuda_bit_equal_to_oracle(cuda_engine, oracle_engine, kind, n_sass, seed):
-    _check(cuda_engine, oracle_engine, kind, n_sass, seed)
+def test_stream_cuda_bit_equal_to_oracle(cuda_stream_engine, oracle_engine, kind, n_sass, seed):
+    _check(cuda_stream_engine, oracle_engine, kind, n_sass, seed)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", helpers.FIXTURES)
+def test_stream_cuda_matches_reference(cuda_stream_engine, name):
+    """the golden fixtures (outputs of the reference's own passes) through the streaming path"""
+    problems = helpers.check_fixture(cuda_stream_engine, name)
+    assert not problems, "\n".join(problems[:3])
+    assert cuda_stream_engine.debug_partition()["tile_mode"] == 8
+
+
+@pytest.mark.gpu
+def test_stream_cuda_long_blocks(cuda_stream_engine, oracle_engine):
+    """BASELINE.json configs[3]: 4096+-instruction blocks (budget cut, reciprocal chains) stay in the stream"""
+    _check(cuda_stream_engine, oracle_engine, "long", 400_000, seed=7)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("passes", [1, 2, 4, 8, 6, 7])
-def test_stream_cuda_pass_subsets(cuda_engine, oracle_engine, passes):
-    _check(cuda_engine, oracle_engine, "mixed", 200_000, seed=6, passes=passes, max_back=1.0)
+def test_stream_cuda_pass_subsets(cuda_stream_engine, oracle_engine, passes):
+    _check(cuda_stream_engine, oracle_engine, "mixed", 200_000, seed=6, passes=passes, max_back=1.0)
 
 
 @pytest.mark.gpu
-def test_stream_cuda_repeatable(cuda_engine):
+def test_stream_cuda_repeatable(cuda_stream_engine):
     """the same upload run twice gives the same bytes (no order-dependent races)"""
     corpus = synth.build_corpus("mixed", 500_000, seed=9)[0]
-    cuda_engine.upload(corpus)
+    cuda_stream_engine.upload(corpus)
     outs = []
     for _ in range(3):
-        cuda_engine.run_postssa()
-        o = cuda_engine.download()
-        o.stats = cuda_engine.stats().copy()
+        cuda_stream_engine.run_postssa()
+        o = cuda_stream_engine.download()
+        o.stats = cuda_stream_engine.stats().copy()
         outs.append(o)
     assert not helpers.corpora_equal(outs[0], outs[1])
     assert not helpers.corpora_equal(outs[0], outs[2])
