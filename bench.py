@@ -54,7 +54,7 @@ def parse_args():
                     help="SASS instructions in the whole corpus (all ranks)")
     ap.add_argument("--seed", type=int, default=100)
     ap.add_argument("--cpu-sample", type=float, default=1.5e6, help="SASS instructions of the CPU-baseline sample")
-    ap.add_argument("--chunks", type=int, default=8, help="e2e: chunks the corpus is streamed in")
+    ap.add_argument("--chunks", type=int, default=16, help="e2e: chunks the corpus is streamed in")
     ap.add_argument("--depth", type=int, default=3, help="e2e: contexts (chunks in flight)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -257,9 +257,11 @@ def main():
     achieved = bytes_per_step / (np.mean(dev_ms) / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "kernel": "k_postssa_gtile (tile kernel: small kernels packed into L2-resident tiles) with k_postssa_cta "
-                          "(long-block kernels) beside it and k_postssa_warp_sync for what the tile kernel hands back: "
-                          "the whole stage, rank 0",
+                "kernel": ("k_stream (corpus-wide streaming passes, one cooperative launch) with the per-function kernels for what it "
+                           "hands back: the whole stage, rank 0") if part.get("tile_mode") == 8 else
+                          ("k_postssa_gtile (tile kernel: small kernels packed into tiles of 16 384 records) with k_postssa_cta "
+                           "(long-block kernels) beside it and k_postssa_warp_sync for what the tile kernel hands back: "
+                           "the whole stage, rank 0"),
                 "algorithmic_bytes_per_launch": bytes_per_step,
                 "bytes_per_sass_inst": bytes_per_step / max(n_sass_rank, 1)}
 

@@ -19,7 +19,7 @@ for l in lines[start + 1:]:
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", l)
     if m: off2line[int(m.group(1), 16)] = cur
 root = "/root/repo/paper_2604_27486_b200/csrc/"
-srcs = {f: open(root + f).read().split("\n") for f in ("tile.cuh", "core.cuh")}
+srcs = {f: open(root + f).read().split("\n") for f in ("tile.cuh", "core.cuh", "stream.cuh")}
 def func_of(f, l):
     if f not in srcs: return f
     for k in range(min(l, len(srcs[f])) - 1, -1, -1):
