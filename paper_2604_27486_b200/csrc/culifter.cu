@@ -994,7 +994,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         const uint32_t n = in->blk_off[b1] - in->blk_off[b0];
         if (in->val_off[f + 1] - in->val_off[f] != in->func[f].next_vid)
             FAIL("function %u: value region holds %u entries, next_vid is %u", f, in->val_off[f + 1] - in->val_off[f], in->func[f].next_vid);
-        const int k = n <= c->thread_max ? 2 : n <= c->small_max ? 0 : 1;
+        const int k = (c->thread_max && n <= c->thread_max) ? 2 : n <= c->small_max ? 0 : 1;     /* thread_max 0: no thread kernel, record-less functions included */
         if (k == 1) big.emplace_back(~n, f); else if (k == 2) tiny.emplace_back(n, f);
         else mid.emplace_back((in->func[f].arch == CL_ARCH_SM52 ? 0u : 0x80000000u) | (0x7FFFFFFFu - n), f);   /* by arch (sm52 runs an extra pass), then size */
         n_max[k] = std::max(n_max[k], n);
@@ -1059,7 +1059,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             uint64_t n_small = 0;
             for (uint32_t f = 0; f < F; f++) {
                 const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
-                if (n > c->thread_max && (n <= c->small_max || (c->tile_long && tile_icap(n) <= TileCfgG3::I))) n_small += n;
+                if (!(c->thread_max && n <= c->thread_max) && (n <= c->small_max || (c->tile_long && tile_icap(n) <= TileCfgG3::I))) n_small += n;
             }
             int n_sm = 148;
 #if CL_CUDA
@@ -1080,7 +1080,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         for (uint32_t f = 0; f < F; f++) {
             const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
             const uint32_t n = in->blk_off[b1] - in->blk_off[b0], nb = b1 - b0;
-            if (n <= c->thread_max) continue;
+            if (c->thread_max && n <= c->thread_max) continue;
             const bool small = n <= c->small_max;
             const uint32_t nimm = in->imm_off[f + 1] - in->imm_off[f];
             const Need nd = { tile_icap(n), tile_vcap(in->func[f].next_vid, n), tile_qcap(nimm, n), nb, f };
