@@ -399,7 +399,7 @@ template <class G> CLF void s_usecount(const G &g, StreamS &T) {
 
 /* ----------------------------------------------------------------- matching */
 /* operand_key equality (patterns.py:109-127) of two operands                   */
-CLD bool s_key_equal(const StreamS &T, opnd a, opnd b) {
+CLN bool s_key_equal(const StreamS &T, opnd a, opnd b) {
     unsigned ka = kind_of(a.tag), kb = kind_of(b.tag);
     if (ka == CL_K_URZ) ka = CL_K_RZ;
     if (kb == CL_K_URZ) kb = CL_K_RZ;
@@ -418,7 +418,7 @@ CLD bool s_key_equal(const StreamS &T, opnd a, opnd b) {
     return a.pay == b.pay;
 }
 /* _match_opcode + the slot-local part of _unify (patterns.py:155-178, :130-152) */
-CLD bool s_match_local(const StreamS &T, const cl_template &t, const cl_hdr &h, uint32_t i) {
+CLN bool s_match_local(const StreamS &T, const cl_template &t, const cl_hdr &h, uint32_t i) {
     if (h.op != t.op) return false;
     const cl_modset &ms = T.fs.ms[h.modset];
     if ((ms.mask & t.mods_all) != t.mods_all) return false;
@@ -450,15 +450,18 @@ CLD bool s_match_local(const StreamS &T, const cl_template &t, const cl_hdr &h, 
 }
 /* do two records share a value (defs and value operands of both)?  One edge of
  * _connected (patterns.py:219-238)                                            */
-CLD bool s_linked(const StreamS &T, uint32_t i, uint32_t j) {
+CLN bool s_linked(const StreamS &T, uint32_t i, uint32_t j) {
+    /* kept small and out of line: inlined with its nested loops it made the unify loop 244 KB of code */
     const cl_hdr hi = T.hdr[i], hj = T.hdr[j];
+    uint32_t a[16];                       /* <= 8 slots, a MemRef slot carries two values */
+    unsigned na = 0;
+    auto push = [&](uint32_t v) { if (na < 16) a[na++] = v; };
+    s_value_defs(T, hi, i, push);
+    s_value_operands(T, hi, i, push);
     bool hit = false;
-    auto probe = [&](uint32_t v) {
-        s_value_defs(T, hj, j, [&](uint32_t w) { hit |= v == w; });
-        s_value_operands(T, hj, j, [&](uint32_t w) { hit |= v == w; });
-    };
-    s_value_defs(T, hi, i, probe);
-    if (!hit) s_value_operands(T, hi, i, probe);
+    auto probe = [&](uint32_t w) { for (unsigned k = 0; k < na; k++) hit |= a[k] == w; };
+    s_value_defs(T, hj, j, probe);
+    s_value_operands(T, hj, j, probe);
     return hit;
 }
 /* one candidate tuple of match_patterns (patterns.py:199-215)                  */

@@ -291,7 +291,7 @@ template <class G, class C> CLF void t_usecount(const G &g, TileS<C> &T, const T
 
 /* ----------------------------------------------------------------- matching */
 /* operand_key equality (patterns.py:109-127) of two operands                   */
-template <class C> CLD bool t_key_equal(const TileS<C> &T, const TileG<C> &tg, opnd a, opnd b) {
+template <class C> CLN bool t_key_equal(const TileS<C> &T, const TileG<C> &tg, opnd a, opnd b) {
     unsigned ka = kind_of(a.tag), kb = kind_of(b.tag);
     if (ka == CL_K_URZ) ka = CL_K_RZ;
     if (kb == CL_K_URZ) kb = CL_K_RZ;
@@ -310,7 +310,7 @@ template <class C> CLD bool t_key_equal(const TileS<C> &T, const TileG<C> &tg, o
     return a.pay == b.pay;
 }
 /* _match_opcode + the slot-local part of _unify (patterns.py:155-178, :130-152) */
-template <class C> CLD bool t_match_local(const TileS<C> &T, const cl_template &t, const cl_hdr &h, uint32_t i) {
+template <class C> CLN bool t_match_local(const TileS<C> &T, const cl_template &t, const cl_hdr &h, uint32_t i) {
     if (h.op != t.op) return false;
     const cl_modset &ms = T.fs.ms[h.modset];
     if ((ms.mask & t.mods_all) != t.mods_all) return false;
@@ -342,15 +342,18 @@ template <class C> CLD bool t_match_local(const TileS<C> &T, const cl_template &
 }
 /* do two records share a value (defs and value operands of both)?  One edge of
  * _connected (patterns.py:219-238)                                            */
-template <class C> CLD bool t_linked(const TileS<C> &T, const TileG<C> &tg, uint32_t i, uint32_t j) {
+template <class C> CLN bool t_linked(const TileS<C> &T, const TileG<C> &tg, uint32_t i, uint32_t j) {
+    /* kept small and out of line: inlined with its nested loops it made the unify loop 244 KB of code */
     const cl_hdr hi = T.hdr[i], hj = T.hdr[j];
+    uint32_t a[16];                       /* <= 8 slots, a MemRef slot carries two values */
+    unsigned na = 0;
+    auto push = [&](uint32_t v) { if (na < 16) a[na++] = v; };
+    t_value_defs(T, hi, i, push);
+    t_value_operands(T, tg, hi, i, push);
     bool hit = false;
-    auto probe = [&](uint32_t v) {
-        t_value_defs(T, hj, j, [&](uint32_t w) { hit |= v == w; });
-        t_value_operands(T, tg, hj, j, [&](uint32_t w) { hit |= v == w; });
-    };
-    t_value_defs(T, hi, i, probe);
-    if (!hit) t_value_operands(T, tg, hi, i, probe);
+    auto probe = [&](uint32_t w) { for (unsigned k = 0; k < na; k++) hit |= a[k] == w; };
+    t_value_defs(T, hj, j, probe);
+    t_value_operands(T, tg, hj, j, probe);
     return hit;
 }
 /* one candidate tuple of match_patterns (patterns.py:199-215)                  */
