@@ -254,9 +254,19 @@ def main():
     except OSError:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    # DRAM bytes of the dominant kernel per launch: from the committed ncu --set full capture of this very
+    # workload (profiles/r01_traffic.json); null for any other workload or path
+    traffic = None
+    try:
+        tr = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())["k_postssa_gtile"]
+        if (args.workload == "mixed" and world == 1 and part.get("tile_mode") != 8
+                and abs(n_sass_all - tr["workload_sass_insts"]) < 0.01 * tr["workload_sass_insts"]):
+            traffic = tr["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
     achieved = bytes_per_step / (np.mean(dev_ms) / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "kernel": ("k_stream (corpus-wide streaming passes, one cooperative launch) with the per-function kernels for what it "
                            "hands back: the whole stage, rank 0") if part.get("tile_mode") == 8 else
                           ("k_postssa_gtile (tile kernel: small kernels packed into tiles of 16 384 records) with k_postssa_cta "

@@ -283,9 +283,11 @@ class Pipeline:
         results, stats, ms, trace = [None] * n, [None] * n, [0.0] * n, [[0, 0.0, 0.0, 0.0, 0.0, 0.0] for _ in range(n)]
         errors = []
         t_begin = time.perf_counter()
-        free_ctx, q_run, q_down = queue.Queue(), queue.Queue(), queue.Queue()
-        for i in range(len(self.engines)):
-            free_ctx.put(i)
+        q_run, q_down = queue.Queue(), queue.Queue()
+        # chunk k always takes context k mod depth: a context sees the same chunks every time the same list is
+        # streamed again, so its grow-only device buffers stop growing (a reallocation synchronises the device)
+        depth = len(self.engines)
+        free = [threading.Semaphore(1) for _ in range(depth)]
 
         def now():
             return time.perf_counter() - t_begin
@@ -293,8 +295,9 @@ class Pipeline:
         def uploader():
             try:
                 for k in range(n):
-                    i = free_ctx.get()
-                    if i is None or errors:
+                    i = k % depth
+                    free[i].acquire()
+                    if errors:
                         break
                     trace[k][0], trace[k][1] = i, now()
                     self.engines[i].upload(chunks[k])
@@ -317,7 +320,8 @@ class Pipeline:
                     q_down.put(item)
             except Exception as e:  # noqa: BLE001
                 errors.append(e)
-                free_ctx.put(None)
+                for sem in free:
+                    sem.release()
             q_down.put(None)
 
         def downloader():
@@ -332,10 +336,11 @@ class Pipeline:
                     stats[k] = eng.stats().copy()
                     ms[k] = eng.last_run_ms()
                     trace[k][5] = now()
-                    free_ctx.put(i)
+                    free[i].release()
             except Exception as e:  # noqa: BLE001
                 errors.append(e)
-                free_ctx.put(None)
+                for sem in free:
+                    sem.release()
 
         threads = [threading.Thread(target=f) for f in (uploader, runner, downloader)]
         for t in threads:
