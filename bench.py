@@ -35,6 +35,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")     # before CUDA starts: see capi.py
 
 from paper_2604_27486_b200 import synth  # noqa: E402
 from paper_2604_27486_b200.soa import Corpus  # noqa: E402
@@ -54,7 +55,7 @@ def parse_args():
                     help="SASS instructions in the whole corpus (all ranks)")
     ap.add_argument("--seed", type=int, default=100)
     ap.add_argument("--cpu-sample", type=float, default=1.5e6, help="SASS instructions of the CPU-baseline sample")
-    ap.add_argument("--chunks", type=int, default=16, help="e2e: chunks the corpus is streamed in")
+    ap.add_argument("--chunks", type=int, default=8, help="e2e: chunks the corpus is streamed in")
     ap.add_argument("--depth", type=int, default=3, help="e2e: contexts (chunks in flight)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -310,7 +311,7 @@ def main():
         assert got == n_out_e2e == n_out, (got, n_out_e2e, n_out)     # the chunked run is the same job
         if os.environ.get("CL_TRACE") and rank == 0:
             for kk, tr in enumerate(pipe.last_trace):
-                print(f"chunk {kk}: ctx {tr[0]} upload {tr[1]*1e3:7.1f}..{tr[2]*1e3:7.1f} run {tr[3]*1e3:7.1f}..{tr[4]*1e3:7.1f} download ..{tr[5]*1e3:7.1f} ms", file=sys.stderr)
+                print(f"chunk {kk}: ctx {tr[0]} upload {tr[1]*1e3:7.1f}..{tr[2]*1e3:7.1f} run {tr[3]*1e3:7.1f}..{tr[4]*1e3:7.1f} download ..{tr[5]*1e3:7.1f} ms; kernels {tr[6]:6.1f} ms", file=sys.stderr)
         te = torch.tensor([time.perf_counter() - t2], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)

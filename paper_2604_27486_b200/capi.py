@@ -10,6 +10,7 @@ nothing in the package does.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
@@ -17,6 +18,12 @@ import numpy as np
 from . import layout as L
 from .patterns import BLOB, PATTERN, SLOT, TEMPLATE, compile_patterns
 from .soa import Corpus
+
+# Streams are multiplexed onto CUDA_DEVICE_MAX_CONNECTIONS hardware queues (default 8); two streams that share a
+# queue serialise falsely.  The pipeline runs 2 streams per context: measured on B200, a chunk's kernels waited a full
+# H2D copy of another context (+50 % run time on every other chunk) with the default.  Read when the CUDA context
+# is created, so it has to be in the environment before the first CUDA call of the process.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 PKG = Path(__file__).resolve().parent
 PRODUCT_LIB = PKG / "csrc" / "libculifter.so"
@@ -288,6 +295,11 @@ class Pipeline:
         # streamed again, so its grow-only device buffers stop growing (a reallocation synchronises the device)
         depth = len(self.engines)
         free = [threading.Semaphore(1) for _ in range(depth)]
+        import os
+        strict = os.environ.get("CL_PIPE_STRICT", "1") != "0"
+        free_q = queue.Queue()
+        for i in range(depth):
+            free_q.put(i)
 
         def now():
             return time.perf_counter() - t_begin
@@ -295,9 +307,12 @@ class Pipeline:
         def uploader():
             try:
                 for k in range(n):
-                    i = k % depth
-                    free[i].acquire()
-                    if errors:
+                    if strict:
+                        i = k % depth
+                        free[i].acquire()
+                    else:
+                        i = free_q.get()
+                    if errors or i is None:
                         break
                     trace[k][0], trace[k][1] = i, now()
                     self.engines[i].upload(chunks[k])
@@ -320,6 +335,7 @@ class Pipeline:
                     q_down.put(item)
             except Exception as e:  # noqa: BLE001
                 errors.append(e)
+                free_q.put(None)
                 for sem in free:
                     sem.release()
             q_down.put(None)
@@ -336,9 +352,11 @@ class Pipeline:
                     stats[k] = eng.stats().copy()
                     ms[k] = eng.last_run_ms()
                     trace[k][5] = now()
-                    free[i].release()
+                    trace[k].append(ms[k])
+                    free[i].release() if strict else free_q.put(i)
             except Exception as e:  # noqa: BLE001
                 errors.append(e)
+                free_q.put(None)
                 for sem in free:
                     sem.release()
 

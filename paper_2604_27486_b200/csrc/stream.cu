@@ -27,6 +27,13 @@ using namespace clk;
 #endif
 
 #if CLS_CUDA
+/* the run's state block and the reduction words arrive as a kernel parameter, not as an H2D copy / memset: copy-engine
+ * work of one context queues behind the bulk transfers of the others in the chunked pipeline                        */
+static_assert(sizeof(StreamS) <= 3800, "StreamS travels as a kernel parameter");
+__global__ void k_stream_init(StreamS *T, StreamS h, uint32_t *slots) {
+    *T = h;
+    for (int i = 0; i < 16; i++) slots[i] = 0;
+}
 __global__ void __launch_bounds__(256, CLS_MINB) k_stream(StreamS *T, StreamP *P, const cl_pattern_blob *pb, StreamIO a,
                                                            uint32_t *part, uint32_t *slots) {
     __shared__ uint32_t red[40];
@@ -195,8 +202,8 @@ int cls_run(cls_ctx *c, const cls_job *job, void *stream, char *err, size_t errl
         c->grid = per_sm * c->n_sm;
         if (c->grid > 4096) c->grid = 4096;
     }
-    CLS_OK(cudaMemcpyAsync(d_T, &h, sizeof h, cudaMemcpyHostToDevice, st));
-    CLS_OK(cudaMemsetAsync(d_slots, 0, 16 * sizeof(uint32_t), st));
+    k_stream_init<<<1, 1, 0, st>>>(d_T, h, d_slots);
+    CLS_OK(cudaGetLastError());
     const cl_pattern_blob *pb = k.pb;
     void *args[] = { &d_T, &d_P, &pb, &io, &d_part, &d_slots };
     CLS_OK(cudaLaunchCooperativeKernel((void *)k_stream, dim3(c->grid), dim3(256), args, 0, st));
