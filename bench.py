@@ -55,8 +55,9 @@ def parse_args():
                     help="SASS instructions in the whole corpus (all ranks)")
     ap.add_argument("--seed", type=int, default=100)
     ap.add_argument("--cpu-sample", type=float, default=1.5e6, help="SASS instructions of the CPU-baseline sample")
-    ap.add_argument("--chunks", type=int, default=8, help="e2e: chunks the corpus is streamed in")
-    ap.add_argument("--depth", type=int, default=3, help="e2e: contexts (chunks in flight)")
+    ap.add_argument("--chunks", type=int, default=16, help="e2e: chunks the corpus is streamed in")
+    ap.add_argument("--depth", type=int, default=4, help="e2e: contexts (chunks in flight)")
+    ap.add_argument("--runners", type=int, default=2, help="e2e: run threads (kernels of two chunks back to back)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -286,7 +287,7 @@ def main():
         ranges = corpus.split(args.chunks)
         host_in = [pinned_like(corpus.slice_funcs(f0, f1)) for f0, f1 in ranges]
         h2d = sum(c.nbytes() for c in host_in)
-        pipe = Pipeline(device=local, depth=args.depth)
+        pipe = Pipeline(device=local, depth=args.depth, runners=args.runners)
         first, _, _ = pipe.run_postssa(host_in)                 # sizes the pinned result holders (and warms up)
         d2h = sum(o.nbytes() + o.events.nbytes for o in first)
         holders = []
@@ -318,7 +319,7 @@ def main():
         e2e = {"value": n_sass_all * args.steps / float(te.cpu()[0]), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.cpu()[0]) / args.steps * 1e3,
-               "path": f"capi.Pipeline: {len(host_in)} chunks (function ranges) through {args.depth} contexts; per chunk "
+               "path": f"capi.Pipeline: {len(host_in)} chunks (function ranges) through {args.depth} contexts, {args.runners} run threads; per chunk "
                        "cl_upload (pinned H2D) + cl_run_postssa + cl_download (device densify + pinned D2H); upload, run and download are "
                        "stage threads, so the three overlap across chunks"}
         pipe.close()

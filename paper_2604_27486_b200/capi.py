@@ -266,8 +266,9 @@ class Pipeline:
     contiguous function range (``Corpus.split`` / ``Corpus.slice_funcs``) and
     the results are those of one big run, chunk by chunk."""
 
-    def __init__(self, device: int = 0, depth: int = 3, lib_path=None, patterns=None):
+    def __init__(self, device: int = 0, depth: int = 3, lib_path=None, patterns=None, runners: int = 1):
         self.engines = [Engine(lib_path, device, patterns) for _ in range(max(1, depth))]
+        self.runners = runners
 
     def close(self):
         for e in self.engines:
@@ -297,6 +298,9 @@ class Pipeline:
         free = [threading.Semaphore(1) for _ in range(depth)]
         import os
         strict = os.environ.get("CL_PIPE_STRICT", "1") != "0"
+        # two run threads: the tail of one chunk's persistent kernels overlaps the head of the next chunk's
+        n_runners = max(1, min(int(os.environ.get("CL_PIPE_RUNNERS", self.runners)), depth))
+        done, done_lock = [0], threading.Lock()
         free_q = queue.Queue()
         for i in range(depth):
             free_q.put(i)
@@ -320,7 +324,8 @@ class Pipeline:
                     q_run.put((k, i))
             except Exception as e:  # noqa: BLE001 - re-raised on the caller's thread
                 errors.append(e)
-            q_run.put(None)
+            for _ in range(n_runners):
+                q_run.put(None)
 
         def runner():
             try:
@@ -338,7 +343,10 @@ class Pipeline:
                 free_q.put(None)
                 for sem in free:
                     sem.release()
-            q_down.put(None)
+            with done_lock:
+                done[0] += 1
+                if done[0] == n_runners:
+                    q_down.put(None)
 
         def downloader():
             try:
@@ -360,7 +368,7 @@ class Pipeline:
                 for sem in free:
                     sem.release()
 
-        threads = [threading.Thread(target=f) for f in (uploader, runner, downloader)]
+        threads = [threading.Thread(target=f) for f in (uploader, downloader, *([runner] * n_runners))]
         for t in threads:
             t.start()
         for t in threads:
