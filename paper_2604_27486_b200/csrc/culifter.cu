@@ -570,7 +570,7 @@ CLHD TileIO tile_io(const KArgs &a) {
     return io;
 }
 /* persistent loop of one group (a warp or a CTA) over the tiles of its size class */
-template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const TileP &P, const KArgs &a, uint32_t group, Rec *tmp = nullptr) {
+template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const TileP &P, const KArgs &a, uint32_t group, uint8_t *planes = nullptr) {
     const unsigned long long t_begin = now();
     if (g.rank == 0) {
         FS &s = T.fs;
@@ -578,7 +578,12 @@ template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const Ti
         T.P = &P;
         s.pb = &P.pb; s.ms = a.in.modsets; s.opflags = a.opflags; s.solo = g.size == 1;
         s.passes = a.passes; s.max_rounds = a.max_rounds; s.emit_matches = 0;
-        s.S.hdr = T.hdr; s.S.tag = T.tag; s.S.pay = T.pay;
+        if constexpr (C::PP) {       /* big tiles: two buffers per plane in scratch (128 bytes per record) */
+            T.hdr.a = (cl_hdr *)planes; T.hdr.b = (cl_hdr *)(planes + (size_t)16 * C::I);
+            T.tag.a = (uint16_t *)(planes + (size_t)32 * C::I); T.tag.b = (uint16_t *)(planes + (size_t)48 * C::I);
+            T.pay.a = (uint32_t *)(planes + (size_t)64 * C::I); T.pay.b = (uint32_t *)(planes + (size_t)96 * C::I);
+        }
+        s.S.hdr = T.hdr.ptr(); s.S.tag = T.tag.ptr(); s.S.pay = T.pay.ptr();
         s.usecnt = T.usecnt; s.defpos = T.defpos; s.redirect = T.redirect; s.origin = T.origin;
         s.def_iid = T.def_iid; s.alive = T.alive; s.imm = T.imm;
         s.cap.I = C::I; s.cap.V = C::V; s.cap.Q = C::Q; s.cap.B = C::B; s.cap.M = C::M; s.cap.S = C::S; s.cap.E = C::E;
@@ -592,7 +597,7 @@ template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const Ti
     tg.stage = (Stage *)scr;
     tg.ev = (cl_event *)(scr + ((sizeof(Stage) * C::S + 255) & ~(size_t)255));
     tg.mem = a.o_mem;
-    tg.tmp = tmp;
+    tg.tmp = nullptr;
     const TileIO io = tile_io(a);
     for (;;) {
         uint32_t w = 0;
@@ -634,7 +639,7 @@ template <class C, int WARPS, int MINB> __global__ void __launch_bounds__(WARPS 
 }
 /* big tiles resident in L2 (global scratch): a CTA is one group; scratch = stages, events, the tile, a second stream buffer */
 template <class C> CLHD size_t gtile_scratch_bytes() {
-    return tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255) + ((sizeof(Rec) * C::I + 255) & ~(size_t)255);
+    return tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255) + (((size_t)128 * C::I + 255) & ~(size_t)255);
 }
 template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, MINB) k_postssa_gtile(KArgs a) {
     __shared__ TileP P;
@@ -644,7 +649,7 @@ template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, 
     __shared__ uint32_t red[40];
     g.red = red;
     t_setup(g, P, a.pb);
-    tile_loop(g, T, P, a, blockIdx.x, (Rec *)(base + tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255)));
+    tile_loop(g, T, P, a, blockIdx.x, base + tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255));
 }
 /* experiment: the same warp tiles with the tile state in L2-resident scratch instead of shared
  * memory (more warps in flight, longer access latency)                                       */
@@ -1337,9 +1342,9 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     t_setup(g, P, k.pb);
     if (cls == 0) { static TileS<TileCfgW> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
     else if (cls == 1) { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
-    else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
-    else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
-    else { static TileS<TileCfgG> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; alignas(16) static uint8_t pl[128 * TileCfgG3::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
+    else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; alignas(16) static uint8_t pl[128 * TileCfgG2::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
+    else { static TileS<TileCfgG> T; alignas(16) static uint8_t pl[128 * TileCfgG::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     return 0;
 #endif
 }

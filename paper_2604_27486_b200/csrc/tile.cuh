@@ -52,14 +52,14 @@ struct TPat {
 };
 
 /* capacities of one tile (compile time: the tile lives in shared memory) */
-struct TileCfgL { static constexpr uint32_t I = 1024, V = 1792, Q = 320, F = 32, B = 96, M = 1024, S = 512, X = 256, E = 512; };
-struct TileCfgS { static constexpr uint32_t I = 576, V = 1024, Q = 192, F = 24, B = 64, M = 512, S = 288, X = 128, E = 256; };
+struct TileCfgL { static constexpr bool PP = false; static constexpr uint32_t I = 1024, V = 1792, Q = 320, F = 32, B = 96, M = 1024, S = 512, X = 256, E = 512; };
+struct TileCfgS { static constexpr bool PP = false; static constexpr uint32_t I = 576, V = 1024, Q = 192, F = 24, B = 64, M = 512, S = 288, X = 128, E = 256; };
 /* a big tile resident in L2 (global scratch) instead of shared memory: every pass loops many times over
  * the same code, which is what the instruction cache needs (profiles/r01_tuning.md)          */
-struct TileCfgG { static constexpr uint32_t I = 4096, V = 7168, Q = 1280, F = 128, B = 255, M = 4096, S = 2048, X = 512, E = 2048; };
-struct TileCfgG2 { static constexpr uint32_t I = 8192, V = 14336, Q = 2560, F = 255, B = 255, M = 8192, S = 4096, X = 1024, E = 4096; };
-struct TileCfgG3 { static constexpr uint32_t I = 16384, V = 28672, Q = 5120, F = 255, B = 255, M = 16384, S = 8192, X = 2048, E = 8192; };
-struct TileCfgW { static constexpr uint32_t I = 192, V = 352, Q = 64, F = 3, B = 16, M = 192, S = 96, X = 32, E = 64; };   /* one warp */
+struct TileCfgG { static constexpr bool PP = true; static constexpr uint32_t I = 4096, V = 7168, Q = 1280, F = 128, B = 255, M = 4096, S = 2048, X = 512, E = 2048; };
+struct TileCfgG2 { static constexpr bool PP = true; static constexpr uint32_t I = 8192, V = 14336, Q = 2560, F = 255, B = 255, M = 8192, S = 4096, X = 1024, E = 4096; };
+struct TileCfgG3 { static constexpr bool PP = true; static constexpr uint32_t I = 16384, V = 28672, Q = 5120, F = 255, B = 255, M = 16384, S = 8192, X = 2048, E = 8192; };
+struct TileCfgW { static constexpr bool PP = false; static constexpr uint32_t I = 192, V = 352, Q = 64, F = 3, B = 16, M = 192, S = 96, X = 32, E = 64; };   /* one warp */
 
 /* the pattern table and what t_setup derives from it: shared by the tiles of a CTA */
 struct TileP {
@@ -70,10 +70,27 @@ struct TileP {
     uint8_t op_cls[2][CL_OP__COUNT];      /* opcode id -> seed class of the table, 0xFF none */
 };
 
+/* a plane of the tile's stream: an array inside the tile (shared-memory tiles, permuted through registers) or a
+ * pair of buffers in scratch that a permutation flips (big tiles: the stream is written once per permutation
+ * instead of being scattered to a side buffer and copied back -- half the DRAM traffic of a permutation)      */
+template <class E, uint32_t N, bool PP> struct PlaneT;
+template <class E, uint32_t N> struct PlaneT<E, N, false> {
+    alignas(16) E a[N];
+    CLMEM E &operator[](size_t i) { return a[i]; }
+    CLMEM const E &operator[](size_t i) const { return a[i]; }
+    CLMEM E *ptr() { return a; }
+};
+template <class E, uint32_t N> struct PlaneT<E, N, true> {
+    E *a, *b;
+    CLMEM E &operator[](size_t i) { return a[i]; }
+    CLMEM const E &operator[](size_t i) const { return a[i]; }
+    CLMEM E *ptr() { return a; }
+    CLMEM void flip() { E *t = a; a = b; b = t; }
+};
 template <class C> struct TileS {
-    alignas(16) cl_hdr hdr[C::I];
-    alignas(16) uint16_t tag[C::I * 8];
-    alignas(16) uint32_t pay[C::I * 8];
+    PlaneT<cl_hdr, C::I, C::PP> hdr;
+    PlaneT<uint16_t, C::I * 8, C::PP> tag;
+    PlaneT<uint32_t, C::I * 8, C::PP> pay;
     unsigned long long owner[C::I];
     uint32_t usecnt[C::V], defpos[C::V], redirect[C::V], origin[C::V];
     int32_t def_iid[C::V];
@@ -172,6 +189,28 @@ template <class G, class C> CLF void t_index(const G &g, TileS<C> &T) {
 /* in-place permutation of the stream: record i moves to dst(i) (NONE32 = dropped).
  * Everything is read before anything is written.                              */
 template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T, const TileG<C> &tg, uint32_t n, uint32_t n_new, F dst) {
+    if constexpr (C::PP) {
+        /* into the other buffer of every plane, then the buffers flip */
+        GFOR(g, i, n) if (i < n) {
+            const uint32_t d = dst(i);
+            if (d != NONE32) {
+                const uint4 r0 = *(const uint4 *)&T.hdr[i], r1 = *(const uint4 *)&T.tag[(size_t)i * 8];
+                const uint4 r2 = ((const uint4 *)&T.pay[(size_t)i * 8])[0], r3 = ((const uint4 *)&T.pay[(size_t)i * 8])[1];
+                *(uint4 *)&T.hdr.b[d] = r0;
+                *(uint4 *)&T.tag.b[(size_t)d * 8] = r1;
+                ((uint4 *)&T.pay.b[(size_t)d * 8])[0] = r2;
+                ((uint4 *)&T.pay.b[(size_t)d * 8])[1] = r3;
+            }
+        }
+        g.sync();
+        if (g.rank == 0) {
+            T.hdr.flip(); T.tag.flip(); T.pay.flip();
+            T.fs.S.hdr = T.hdr.ptr(); T.fs.S.tag = T.tag.ptr(); T.fs.S.pay = T.pay.ptr();
+        }
+        g.sync();
+        (void)tg; (void)n_new;
+        return;
+    } else {
 #if CL_DEV
     constexpr int K = (int)((C::I + G::THREADS - 1) / G::THREADS);
     if (K > 2) {
@@ -233,6 +272,7 @@ template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T,
         if (d[i] != NONE32) { T.hdr[d[i]] = tmp[i].h; memcpy(&T.tag[(size_t)d[i] * 8], tmp[i].tag, 16); memcpy(&T.pay[(size_t)d[i] * 8], tmp[i].pay, 32); }
     (void)g; (void)tg; (void)n_new;
 #endif
+    }
 }
 
 /* running exclusive scan over items [0, n) in order; returns the total        */

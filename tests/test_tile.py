@@ -36,6 +36,16 @@ def test_tile_logic_sim(sim_tile_engine, oracle_engine, kind, n_sass):
     _check(sim_tile_engine, oracle_engine, kind, n_sass, seed=11)
 
 
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_big_tile_logic_sim(oracle_engine, cfg):
+    """the big-tile form the GPU uses at scale (planes in scratch, flipped by every permutation), forced on the
+    one-lane build: 4096- and 16384-record tiles"""
+    eng = helpers._engine_with_env(helpers.build_sim(), CL_STREAM=0, CL_TILE=4, CL_GTILE_CFG=cfg)
+    for kind, n_sass in (("mixed", 150_000), ("sm52", 60_000)):
+        part = _check(eng, oracle_engine, kind, n_sass, seed=13)
+        assert part["tile_mode"] == 4 and part["tile_cfg"] == cfg
+
+
 @pytest.mark.parametrize("passes", [1, 2, 4, 8, 6, 7])
 def test_tile_pass_subsets_sim(sim_tile_engine, oracle_engine, passes):
     _check(sim_tile_engine, oracle_engine, "mixed", 40_000, seed=3, passes=passes, max_back=1.0)
