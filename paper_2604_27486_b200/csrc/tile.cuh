@@ -37,6 +37,10 @@
 
 namespace clk {
 
+/* a record removed by remove_dead_pseudo stays in place as a tombstone (no arities, no guard, an opcode id no table
+ * ever hands out: layout.py caps ids below 0xFFFF) until the next rewrite permutation or the store drops it: no
+ * compaction pass, positions and def-use stay valid                                                            */
+static constexpr uint16_t CL_OP_TOMB = 0xFFFF;
 static constexpr uint32_t CL_ST_REDO = 100;     /* internal: redo this function on the general kernel */
 
 
@@ -123,6 +127,7 @@ template <class C> struct TileS {
     unsigned long long prof[PF__N];
     uint32_t n, nb, nf, n_mt, n_sel, n_ev, fail, vtot, qtot, n_chain, work;
     uint32_t du_ok, n_list;       /* du_ok: usecnt / defpos describe the stream (every live function) */
+    uint32_t tombs;               /* the stream holds tombstones */
     uint32_t red[40];
 };
 
@@ -660,7 +665,8 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     if (T.fail || ns == 0) return;
     const uint32_t n = T.n;
     PROF(g, T.fs, PF_PLAN);
-    GFOR(g, p, n) if (p < n) { T.keep[p] = 1; T.inscnt[p] = 0; }
+    if (T.tombs) { GFOR(g, p, n) if (p < n) { T.keep[p] = T.hdr[p].op != CL_OP_TOMB; T.inscnt[p] = 0; } }     /* the permutation drops them */
+    else GFOR(g, p, n) if (p < n) { T.keep[p] = 1; T.inscnt[p] = 0; }
     GFOR(g, f, T.nf) if (f < T.nf) T.f_first[f] = NONE32;
     GFOR(g, b, T.nb) if (b < T.nb) T.b_first[b] = NONE32;
     g.sync();
@@ -757,6 +763,7 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     }
     g.sync();
     t_rebase_blocks(g, T, n, tot);
+    if (g.rank == 0) T.tombs = 0;
     t_index(g, T);
     t_usecount(g, T, tg);                    /* for simplify_packs / remove_dead_pseudo of this round */
 }
@@ -815,7 +822,15 @@ template <class G, class C> CLF void t_dce(const G &g, TileS<C> &T, const TileG<
             if (try_kill(i, T.hdr[i])) mine++;
         }
     }
-    if (removed) t_compact(g, T, tg);
+    if (removed) {
+        GFOR(g, i, T.n) if (i < T.n && !T.keep[i]) {
+            cl_hdr h = T.hdr[i];
+            h.op = CL_OP_TOMB; h.modset = 0; h.n_defs = h.n_aux = h.n_uses = 0; h.flags = 0; h.ext = 0;
+            T.hdr[i] = h;
+        }
+        if (g.rank == 0) T.tombs = 1;
+        g.sync();
+    }
 }
 
 /* simplify_packs + _redirect_values (patterns.py:710-764) for the gated functions;
@@ -1222,7 +1237,7 @@ template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, TileG<C> &t
     if (g.rank == 0) {
         T.fs.mem = tg.mem;
         T.nf = nf;
-        T.n_ev = 0; T.fail = 0; T.n_chain = 0; T.n_mt = 0; T.n_sel = 0; T.du_ok = 0; T.n_list = 0;
+        T.n_ev = 0; T.fail = 0; T.n_chain = 0; T.n_mt = 0; T.n_sel = 0; T.du_ok = 0; T.n_list = 0; T.tombs = 0;
     }
     GFOR(g, f, nf) if (f < nf) {
         const uint32_t gf = a.flist[td.first + f];
@@ -1308,6 +1323,11 @@ template <class G, class C> CLF void t_load(const G &g, TileS<C> &T, TileG<C> &t
 template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const TileG<C> &tg, const TileIO &a) {
     PROF(g, T.fs, PF_STORE);
     const uint32_t nf = T.nf;
+    /* tombstones leave here: live(x) = live records before position x */
+    const uint32_t n_live = t_scan(g, T.n, [&](uint32_t p) { return (uint32_t)(T.hdr[p].op != CL_OP_TOMB); },
+                                   [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
+    g.sync();
+    auto live = [&](uint32_t x) -> uint32_t { return x < T.n ? (uint32_t)T.outpos[x] : n_live; };
     if (g.rank == 0) {
         uint32_t oi = 0, oq = 0, ov = 0, oe = 0;
         const bool tile_ok = !T.fail;
@@ -1318,7 +1338,7 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
 #endif
             if (!ok && T.f_stat[f] == 0) T.f_stat[f] = CL_ST_REDO;
             T.f_oi[f] = oi; T.f_oq[f] = oq; T.f_ov[f] = ov; T.f_oe[f] = oe;
-            if (ok) { oi += T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]]; oq += T.f_nimm[f]; ov += T.f_nvid[f]; oe += T.f_nev[f]; }
+            if (ok) { oi += live(T.bo[T.f_b0[f + 1]]) - live(T.bo[T.f_b0[f]]); oq += T.f_nimm[f]; ov += T.f_nvid[f]; oe += T.f_nev[f]; }
         }
         const uint32_t ri = (uint32_t)a_add64(&a.cursor[0], oi), rq = (uint32_t)a_add64(&a.cursor[1], oq),
                        rv = (uint32_t)a_add64(&a.cursor[2], ov), re = (uint32_t)a_add64(&a.cursor[3], oe);
@@ -1342,7 +1362,7 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
             else a.retry_list[a_add(a.retry_count, 1u)] = T.f_gf[f];
             continue;
         }
-        const uint32_t cnt = T.bo[T.f_b0[f + 1]] - T.bo[T.f_b0[f]];
+        const uint32_t cnt = live(T.bo[T.f_b0[f + 1]]) - live(T.bo[T.f_b0[f]]);
         TFuncOut o;
         o.f.next_vid = T.f_nvid[f]; o.f.next_iid = T.f_niid[f]; o.f.next_temp_reg = T.f_ntemp[f];
         o.f.arch = T.f_arch[f]; o.f.status = (uint8_t)(fits ? CL_ST_OK : CL_ST_CAPACITY); o.f.reserved = 0;
@@ -1357,8 +1377,8 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
         for (int k = 0; k < 2; k++) bk.term_pay[k] = t_rebase(T, f, bk.term_tag[k], bk.term_pay[k], false);
         const uint32_t gb = T.f_gb0[f] + (b - T.f_b0[f]);
         a.o_blk[gb] = bk;
-        a.o_blk_start[gb] = fits ? T.f_oi[f] + (T.bo[b] - T.bo[T.f_b0[f]]) : 0u;
-        a.o_blk_cnt[gb] = fits ? T.bo[b + 1] - T.bo[b] : 0u;
+        a.o_blk_start[gb] = fits ? T.f_oi[f] + (live(T.bo[b]) - live(T.bo[T.f_b0[f]])) : 0u;
+        a.o_blk_cnt[gb] = fits ? live(T.bo[b + 1]) - live(T.bo[b]) : 0u;
     }
     /* memrefs of the live functions back to function-local value ids (dead ones are reloaded by the general kernel) */
     for (uint32_t f = 0; f < nf; f++) {
@@ -1373,8 +1393,8 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
     if (fits) {
         GFOR(g, i, T.n) if (i < T.n) {
             const uint32_t f = T.fidx[i];
-            if (T.f_stat[f] != 0) continue;
-            const size_t d = (size_t)T.f_oi[f] + (i - T.bo[T.f_b0[f]]);
+            if (T.f_stat[f] != 0 || T.hdr[i].op == CL_OP_TOMB) continue;
+            const size_t d = (size_t)T.f_oi[f] + (live(i) - live(T.bo[T.f_b0[f]]));
             uint4 tg4 = *(const uint4 *)&T.tag[(size_t)i * 8];
             uint4 p0 = ((const uint4 *)&T.pay[(size_t)i * 8])[0], p1 = ((const uint4 *)&T.pay[(size_t)i * 8])[1];
             const uint16_t *tags = (const uint16_t *)&tg4;
