@@ -570,14 +570,19 @@ template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T) {
     GFOR(g, p, n) if (p < n) { T.keep[p] = 0; T.sel_at[p] = 0xFFFFu; }
     g.sync();
     for (;;) {
-        GFOR(g, p, n) if (p < n && !T.keep[p]) T.owner[p] = NONE64;
-        g.sync();
+        /* only the positions undecided matches still bid for are reset (not every record of the tile) */
         GFOR(g, m, nm) if (m < nm && T.mstate[m] == MS_UNDECIDED) {
             const TMatch r = T.mt[m];
             bool clash = false;
             for (unsigned t = 0; t < r.n; t++) clash |= T.keep[r.pos[t]] != 0;
             if (clash) T.mstate[m] = MS_REJECTED;
-            else { const unsigned long long key = t_key(r); for (unsigned t = 0; t < r.n; t++) a_min64(&T.owner[r.pos[t]], key); }
+            else for (unsigned t = 0; t < r.n; t++) T.owner[r.pos[t]] = NONE64;
+        }
+        g.sync();
+        GFOR(g, m, nm) if (m < nm && T.mstate[m] == MS_UNDECIDED) {
+            const TMatch r = T.mt[m];
+            const unsigned long long key = t_key(r);
+            for (unsigned t = 0; t < r.n; t++) a_min64(&T.owner[r.pos[t]], key);
         }
         g.sync();
         bool left = false;
@@ -765,7 +770,9 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     t_rebase_blocks(g, T, n, tot);
     if (g.rank == 0) T.tombs = 0;
     t_index(g, T);
-    t_usecount(g, T, tg);                    /* for simplify_packs / remove_dead_pseudo of this round */
+    /* for simplify_packs / remove_dead_pseudo of this round.  (Keeping def-use valid across the permutation instead --
+     * remapping defpos through outpos, moving the use counts of removed / inserted records -- was measured: no gain.) */
+    t_usecount(g, T, tg);
 }
 
 /* ordered in-place compaction of the stream by keep[]                         */
