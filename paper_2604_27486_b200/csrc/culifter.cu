@@ -56,6 +56,7 @@ static int d2h(void *h, const void *d, size_t n, cudaStream_t st) { if (n) CUDA_
 /* Zeroing as a kernel, not cudaMemsetAsync: the driver may hand a memset to a copy engine, where the few words a
  * run clears queue behind another context's bulk D2H / H2D (measured in the chunked pipeline: +13 ms on every
  * run that started while a neighbour's download was in flight).                                             */
+static thread_local unsigned g_aux_launches = 0;      /* zeroing / densify kernels launched by this thread since the run began */
 __global__ void k_zero(uint32_t *p, size_t n_words) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_words; i += (size_t)gridDim.x * blockDim.x) p[i] = 0;
 }
@@ -65,6 +66,7 @@ static int dzero(void *d, size_t n, cudaStream_t st) {
         const size_t w = n / 4;
         k_zero<<<(unsigned)std::min<size_t>((w + 255) / 256, 1184), 256, 0, st>>>((uint32_t *)d, w);
         CUDA_OK(cudaGetLastError());
+        g_aux_launches++;
     } else
         CUDA_OK(cudaMemsetAsync(d, 0, n, st));
     return 0;
@@ -1363,6 +1365,9 @@ static int run(cl_ctx *c, KArgs k) {
      * (emit_matches / MATCH_ONLY), the raw stage and tables with a pattern that has
      * no join plan go through the general kernels                                  */
     c->n_launches = 0;
+#if CL_CUDA
+    g_aux_launches = 0;
+#endif
     bool use_tiles = c->n_tile_funcs && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
     for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_tiles = use_tiles && c->h_pb.p[pi].join_ok;
 #if CL_CUDA
@@ -1424,7 +1429,11 @@ static int run(cl_ctx *c, KArgs k) {
     c->h_retry += h_retry_big;
     c->have_out = true;
     c->have_dense = false;
-    return densify(c);
+    if (densify(c)) return -1;
+#if CL_CUDA
+    c->n_launches += g_aux_launches + (use_stream ? 1u : 0u);      /* every kernel of the run: main, zeroing, densify (streaming: + its init kernel) */
+#endif
+    return 0;
 }
 
 extern "C" int cl_run_postssa(cl_ctx *c, const cl_run_opts *opts) {
@@ -1510,6 +1519,7 @@ static int densify(cl_ctx *c) {
         k_scan_apply<<<a.n_scan_blocks, SCAN_T, 0, c->stream>>>(a);
         k_densify<<<std::min<uint32_t>((F + 7) / 8, (uint32_t)c->n_sm * 16), 256, 0, c->stream>>>(a);
         CUDA_OK(cudaGetLastError());
+        g_aux_launches += 4;
         CUDA_OK(cudaStreamSynchronize(c->stream));
     }
 #else
