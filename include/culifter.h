@@ -32,8 +32,9 @@
  *
  * At the ABI boundary every stream is a dense CSR (offset arrays of length
  * n+1).  On the device every function's result is written once, at an
- * atomically reserved place (completion order); cl_download() densifies it
- * to function order on the device before the D2H copy.
+ * atomically reserved place (completion order); the run densifies it to
+ * function order on the device as its last step, so cl_download() is a plain
+ * D2H copy (it overlaps the kernels of other contexts: capi.Pipeline).
  */
 #ifndef CULIFTER_H
 #define CULIFTER_H

@@ -1061,7 +1061,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
      * reaches: owner[i] = { low: own seed order, high: smallest order reached in one hop }.          */
     uint32_t *mk1 = T.redirect, *mk2 = T.usecnt;
     GFOR(g, v, T.vtot) if (v < T.vtot) { mk1[v] = NONE32; mk2[v] = NONE32; }
-    GFOR(g, i, n) if (i < n) T.owner[i] = NONE64;
+    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]]) T.owner[i] = NONE64;
     g.sync();
     GFOR(g, c, nc) if (c < nc) {
         const TChain ch = T.chain[c];
@@ -1083,7 +1083,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         if (q1 != NONE32) T.owner[i] = (T.owner[i] & 0xFFFFFFFFull) | (unsigned long long)q1 << 32;
     }
     g.sync();
-    GFOR(g, i, n) if (i < n && T.owner[i] != NONE64) {
+    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && T.owner[i] != NONE64) {
         if (!tf_ok(T, T.fidx[i])) continue;
         const uint32_t own = (uint32_t)T.owner[i], q1 = (uint32_t)(T.owner[i] >> 32);
         const uint32_t key = own < q1 ? own : q1;
@@ -1103,7 +1103,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     g.sync();
     /* number of a chain inside its function = chains of earlier MUFUs (scan over the records) + chains of
      * the same MUFU with an earlier add (a short list per MUFU: owner[m] low word = head, TChain.rank = next) */
-    GFOR(g, i, n) if (i < n) T.owner[i] = 0xFFFFFFFFull;                  /* high word: chains of this MUFU */
+    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]]) T.owner[i] = 0xFFFFFFFFull;   /* high word: chains of this MUFU */
     g.sync();
     GFOR(g, c, nc) if (c < nc) {
         TChain &ch = T.chain[c];
@@ -1118,7 +1118,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         a_add(&T.f_aux[ch.f], 1u);
     }
     g.sync();
-    t_scan(g, n, [&](uint32_t j) { return (uint32_t)(T.owner[j] >> 32); },
+    t_scan(g, n, [&](uint32_t j) { return T.f_rgate[T.fidx[j]] ? (uint32_t)(T.owner[j] >> 32) : 0u; },
            [&](uint32_t j, uint32_t x) {
                T.outpos[j] = (uint16_t)x;
                const uint32_t f = T.fidx[j];
