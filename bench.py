@@ -12,9 +12,13 @@ allgather of the per-pattern match counters.
 
   value        device-resident: input already in HBM, CUDA-event time of the
                stage (max over ranks); inputs are far larger than L2.
-  e2e          through the C ABI with pinned HOST buffers: cl_upload (H2D) +
-               cl_run_postssa + cl_download (device densify + D2H) per step.
-  roofline     algorithmic bytes / kernel time vs MEASURED_PEAKS.json hbm_gbs.
+  e2e          through the public batch API (capi.Pipeline) with pinned HOST
+               buffers: per chunk cl_upload (H2D) + cl_run_postssa (kernels +
+               device densify) + cl_download (D2H); upload, run and download are
+               stage threads over a few contexts, so the three overlap across chunks.
+  roofline     algorithmic bytes / kernel time vs MEASURED_PEAKS.json hbm_gbs;
+               `traffic` = DRAM bytes of the dominant kernel per launch from the
+               committed ncu capture of this workload (profiles/r01_traffic.json).
   cpu_baseline the oracle (C port of the reference) on this box's host cores,
                bounded sample of the same corpus.
 
