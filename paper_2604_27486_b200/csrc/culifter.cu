@@ -15,6 +15,7 @@
 #include "tile.cuh"
 #include "kargs.h"
 #include "stream.h"
+#include "fused.h"
 
 #include <algorithm>
 
@@ -846,6 +847,8 @@ struct cl_ctx {
     uint32_t n_tile_funcs = 0, h_retry = 0, n_launches = 0; bool used_tiles = false;
     int stream_mode = cls_default_mode();   /* 1: the production post-SSA stage runs as corpus-wide streaming passes (stream.cuh); 0: tile kernels */
     cls_ctx *cls = nullptr; bool used_stream = false;
+    /* the function-resident path (fused.cuh): default for the post-SSA stage */
+    int fused_mode = 1; clf_ctx *clf = nullptr; bool fused_ok = false, used_fused = false;
     DenseArgs dense{}; bool have_dense = false;     /* dense result of the last run (device) */
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
@@ -899,6 +902,8 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_WARP_SYNC")) { const int v = atoi(e); c->warp_sync = (v == 0 || v == 8 || v == 16 || v == 32 || v == 33) ? v : 32; }
     if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
     if (const char *e = getenv("CL_STREAM")) c->stream_mode = atoi(e) != 0;
+    if (const char *e = getenv("CL_FUSED")) c->fused_mode = atoi(e) != 0;
+    if (getenv("CL_STREAM") || getenv("CL_TILE")) { if (!getenv("CL_FUSED")) c->fused_mode = 0; }   /* an explicitly selected older path */
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 7;
     if (const char *e = getenv("CL_GTILE_WARPS")) { const int v = atoi(e); c->gtile_warps = (v == 8 || v == 32) ? v : 16; }
     if (const char *e = getenv("CL_TILE_LONG")) c->tile_long = atoi(e) != 0;
@@ -933,6 +938,7 @@ extern "C" void cl_destroy(cl_ctx *c) {
     cudaStreamSynchronize(c->stream);
 #endif
     cls_destroy(c->cls);
+    clf_destroy(c->clf);
     for (DBuf &b : c->buf) dfree(b.p);
     dfree(c->d_opflags); dfree(c->d_pb); dfree(c->d_cursor); dfree(c->d_stats);
 #if CL_CUDA
@@ -959,6 +965,12 @@ extern "C" int cl_set_patterns(cl_ctx *c, const void *blob, size_t nbytes) {
     CUDA_OK(cudaStreamSynchronize(c->stream));
 #endif
     c->have_pb = true;
+    if (!c->clf && clf_create(&c->clf, c->device, c->n_sm_or_1())) FAIL("clf_create failed");
+    {
+        const int r = clf_set_patterns(c->clf, &c->h_pb, (void *)(uintptr_t)c->stream, g_err, sizeof g_err);
+        if (r < 0) return -1;
+        c->fused_ok = r == 1;
+    }
     return 0;
 }
 extern "C" int cl_set_threads(cl_ctx *, int) { return 0; }
@@ -1075,7 +1087,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     /* tiles: small functions without overflow slots, by size class, packed in size order */
     for (auto &t : c->tc) t.tiles.clear();
     c->tile_flist.clear(); c->rest.clear(); c->big_rest.clear(); c->n_tile_funcs = 0;
-    if (!c->stream_mode) {       /* the streaming path needs no host-side plan */
+    if (!c->stream_mode && !(c->fused_mode && (c->fused_ok || !c->have_pb))) {       /* the streaming and the fused path need no host-side plan */
         struct Need { uint32_t I, V, Q, B, f; };
         /* tile size by corpus size: the bigger the tile the better the passes amortise (profiles/r01_tuning.md),
          * as long as there are a few tiles per SM                                                              */
@@ -1134,7 +1146,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     }
     {
         uint32_t *words = nullptr;
-        if (dget(c, B_RETRY_LIST, &c->d_retry_list, c->stream_mode ? (size_t)F : std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs))) return -1;
+        if (dget(c, B_RETRY_LIST, &c->d_retry_list, (size_t)F)) return -1;
         if (dget(c, B_RETRY_WORDS, &words, 4)) return -1;
         c->d_retry_count = words; c->d_retry_counter = words + 1;
     }
@@ -1221,7 +1233,7 @@ static int launch_part(cl_ctx *c, int which, KArgs k, int mode = 0, bool side = 
     if (mode == 3 && p.list.empty()) return 0;             /* no large function at all */
     if (mode == 1 && p.grid == 0) return 0;                /* no small function at all */
     k.list = mode == 1 ? c->d_retry_list : mode == 3 ? c->d_retry_big : mode == 2 ? c->d_rest : mode == 4 ? c->d_big_rest : p.d_list;
-    k.n_list = mode == 1 ? (c->stream_mode ? c->F : (uint32_t)std::max<size_t>(c->part[2].list.size(), c->n_tile_funcs)) : mode == 3 ? (uint32_t)p.list.size()
+    k.n_list = mode == 1 ? c->F : mode == 3 ? (uint32_t)p.list.size()
              : mode == 2 ? (uint32_t)c->rest.size() : mode == 4 ? (uint32_t)c->big_rest.size() : (uint32_t)p.list.size();
     k.n_list_ptr = mode == 1 ? c->d_retry_count : mode == 3 ? c->d_retry_big_count : nullptr;
     k.work_counter = mode == 1 ? c->d_retry_counter : mode == 3 ? c->d_retry_big_counter : p.d_counter;
@@ -1380,7 +1392,20 @@ static int run(cl_ctx *c, KArgs k) {
     bool use_stream = c->stream_mode && c->F && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
     for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_stream = use_stream && c->h_pb.p[pi].join_ok;
     c->used_stream = use_stream;
-    if (use_stream) {
+    const bool use_fused = c->fused_mode && c->fused_ok && c->F && !k.raw_passes;
+    c->used_fused = use_fused;
+    if (use_fused) {
+        /* one function resident in shared memory per group (fused.cuh); hand-backs and everything too
+         * large for a shared-memory slice (long blocks) go to the general kernels                  */
+        use_stream = false; use_tiles = false; c->used_stream = false;
+        KArgs kf = k;
+        kf.retry_list = c->d_retry_list; kf.retry_count = c->d_retry_count;
+        kf.retry_big_list = c->d_retry_big; kf.retry_big_count = c->d_retry_big_count; kf.small_max = c->small_max;
+        if (clf_run(c->clf, &kf, c->F, (void *)(uintptr_t)c->stream, g_err, sizeof g_err)) return -1;
+        { unsigned long long info[4]; clf_info(c->clf, info); c->n_launches += (uint32_t)info[0]; }
+        if (launch_part(c, 0, k, 1)) return -1;
+        if (launch_part(c, 1, k, 3)) return -1;
+    } else if (use_stream) {
         /* corpus-wide streaming passes; what they hand back (hazards, overflow slots) goes to the general kernels */
         if (!c->cls && cls_create(&c->cls, c->device, c->n_sm_or_1())) FAIL("cls_create failed");
         cls_job job;
@@ -1413,7 +1438,6 @@ static int run(cl_ctx *c, KArgs k) {
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
     CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    CUDA_OK(cudaEventRecord(c->ev1, c->stream));
 #endif
     if (d2h(c->h_cursor, c->d_cursor, sizeof c->h_cursor, c->stream)) return -1;
     if (d2h(&c->stats, c->d_stats, sizeof(cl_stats), c->stream)) return -1;
@@ -1424,13 +1448,13 @@ static int run(cl_ctx *c, KArgs k) {
     if (c->d_retry_big_count && d2h(&h_retry_big, c->d_retry_big_count, sizeof(uint32_t), c->stream)) return -1;
 #if CL_CUDA
     CUDA_OK(cudaStreamSynchronize(c->stream));
-    CUDA_OK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
 #endif
     c->h_retry += h_retry_big;
     c->have_out = true;
     c->have_dense = false;
-    if (densify(c)) return -1;
+    if (densify(c)) return -1;             /* the dense result of the ABI is part of the timed stage */
 #if CL_CUDA
+    CUDA_OK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
     c->n_launches += g_aux_launches + (use_stream ? 1u : 0u);      /* every kernel of the run: main, zeroing, densify (streaming: + its init kernel) */
 #endif
     return 0;
@@ -1520,8 +1544,9 @@ static int densify(cl_ctx *c) {
         k_densify<<<std::min<uint32_t>((F + 7) / 8, (uint32_t)c->n_sm * 16), 256, 0, c->stream>>>(a);
         CUDA_OK(cudaGetLastError());
         g_aux_launches += 4;
-        CUDA_OK(cudaStreamSynchronize(c->stream));
     }
+    CUDA_OK(cudaEventRecord(c->ev1, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
 #else
     densify_host(a);
 #endif
@@ -1583,7 +1608,7 @@ extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
  * handed back to the general kernel, small functions outside tiles, tile kernel used}            */
 extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
     out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size() + c->tc[2].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles; out[5] = c->n_launches;
-    out[6] = c->used_stream ? 8 : c->tile_mode; out[7] = c->gtile_cfg;
+    out[6] = c->used_fused ? 16 : c->used_stream ? 8 : c->tile_mode; out[7] = c->gtile_cfg;
     return 0;
 }
 /* debugging aid: nanoseconds per phase of the streaming path's last run + {select, dce, rounds} iteration counts */

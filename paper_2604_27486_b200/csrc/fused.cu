@@ -1,0 +1,304 @@
+/* fused.cu -- kernels and host side of the function-resident path (fused.cuh).
+ *
+ * Three launches of one persistent kernel template, one per size class of the
+ * resident function (shared-memory slice per group):
+ *
+ *   class S   1 warp  per function, 16 groups per SM   functions up to 104 records
+ *   class L   2 warps per function,  8 groups per SM   up to 208 records
+ *   class X   4 warps per function,  4 groups per SM   up to 416 records
+ *
+ * Every group pulls functions off a counter.  Class S walks all functions and
+ * appends what is too large for it to class L's list, L does the same for X;
+ * what X cannot take and everything a group hands back goes to the retry lists
+ * of the general per-function kernels (culifter.cu).  No host-side planning.
+ *
+ * Compiled with -DCL_SIM by g++ this file is the one-lane CPU build of the same
+ * device code (tests/sim), never loaded by the package.
+ */
+#include "fused.cuh"
+#include "fused.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#if defined(__CUDACC__) && !defined(CL_SIM)
+#include <cuda_runtime.h>
+#define CLF_CUDA 1
+#else
+#define CLF_CUDA 0
+#endif
+
+using namespace clk;
+
+static_assert(sizeof(FProg) % 16 == 0, "FProg is copied in 16-byte pieces");
+static_assert(sizeof(KArgs) % 8 == 0, "KArgs is copied in 8-byte pieces");
+
+static const uint8_t F_H_OPFLAGS[] = {
+#define CL_OP(name, flags) (uint8_t)(flags),
+#include "../../include/culifter_ops.h"
+#undef CL_OP
+};
+
+/* ------------------------------------------------ pattern table compiler */
+/* cl_pattern_blob -> FProg; false when the fused kernels cannot run the table */
+static bool fprog_build(const cl_pattern_blob &pb, FProg &P, char *why, size_t whylen) {
+    memset(&P, 0, sizeof P);
+    P.n_patterns = pb.n_patterns; P.budget = pb.budget;
+    memcpy(P.group_pos, pb.group_pos, sizeof P.group_pos);
+    memcpy(P.isetp64_ms, pb.isetp64_ms, sizeof P.isetp64_ms);
+    memset(P.op_cls, SF_NOCLS, sizeof P.op_cls);
+    for (unsigned k = 0; k < (unsigned)CL_OP__COUNT; k++) P.opflags[k] = F_H_OPFLAGS[k];
+    uint16_t cls_op[2][MAX_CLS];
+    for (unsigned table = 0; table < 2; table++) {
+        unsigned n_cls = 0;
+        for (unsigned pi = 0; pi < pb.n_patterns; pi++) {
+            const cl_pattern &p = pb.p[pi];
+            if (p.table != table) continue;
+            if (p.n_templates == 3) P.three[table] = 1;
+            for (unsigned t = 0; t < p.n_templates; t++) {
+                bool seen = false;
+                for (unsigned c = 0; c < n_cls; c++) seen |= cls_op[table][c] == p.t[t].op;
+                if (seen) continue;
+                if (n_cls >= (unsigned)MAX_CLS) { snprintf(why, whylen, "more than %d distinct template opcodes in one table", MAX_CLS); return false; }
+                if (p.t[t].op >= CL_OP__COUNT) { snprintf(why, whylen, "template opcode outside the fixed table"); return false; }
+                cls_op[table][n_cls++] = p.t[t].op;
+            }
+        }
+        P.n_cls[table] = n_cls;
+        for (unsigned c = 0; c < n_cls; c++) P.op_cls[table][cls_op[table][c]] = (uint8_t)c;
+    }
+    for (unsigned pi = 0; pi < pb.n_patterns; pi++) {
+        const cl_pattern &p = pb.p[pi];
+        FPat &q = P.p[pi];
+        if (!p.join_ok) { snprintf(why, whylen, "pattern %u has no join plan", pi); return false; }
+        q.nt = p.n_templates; q.rewrite = p.rewrite; q.table = p.table;
+        for (unsigned k = 0; k < 3; k++) { q.order[k] = p.join_order[k]; q.from[k] = p.join_from[k]; q.jslot[k] = p.join_slot[k]; }
+        P.anchor_mask[p.table][P.op_cls[p.table][p.t[p.join_order[0]].op]] |= (uint16_t)(1u << pi);
+        uint8_t ft[CL_MAX_VARS], fk[CL_MAX_VARS], mt[CL_MAX_GROUPS], mg[CL_MAX_GROUPS];
+        memset(ft, 0xFF, sizeof ft); memset(mt, 0xFF, sizeof mt);
+        memset(fk, 0, sizeof fk); memset(mg, 0, sizeof mg);
+        for (unsigned t = 0; t < p.n_templates; t++) {
+            const cl_template &tm = p.t[t];
+            FTmpl &ft_ = q.t[t];
+            ft_.mods_all = tm.mods_all; ft_.mods_none = tm.mods_none; ft_.op = tm.op;
+            ft_.n_defs = tm.n_defs; ft_.n_aux = tm.n_aux; ft_.n_uses = tm.n_uses; ft_.n_mv = tm.n_modvars;
+            ft_.cls = P.op_cls[p.table][tm.op];
+            for (unsigned k = 0; k < tm.n_modvars && k < 2; k++) {
+                ft_.mv_group[k] = tm.modvar_group[k];
+                const unsigned mv = tm.modvar_var[k] & (CL_MAX_GROUPS - 1);
+                if (mt[mv] == 0xFF) { mt[mv] = (uint8_t)t; mg[mv] = tm.modvar_group[k]; }
+                else {
+                    if (q.n_mpairs >= 4) { snprintf(why, whylen, "pattern %u: too many modifier-variable bindings", pi); return false; }
+                    uint8_t *m = q.mpair[q.n_mpairs++]; m[0] = mt[mv]; m[1] = mg[mv]; m[2] = (uint8_t)t; m[3] = tm.modvar_group[k];
+                }
+            }
+            const unsigned ns = (unsigned)tm.n_defs + tm.n_aux + tm.n_uses;
+            if (ns > 8) { snprintf(why, whylen, "pattern %u: template with more than 8 slots", pi); return false; }
+            for (unsigned k = 0; k < ns; k++) {
+                const cl_slot &sl = tm.slot[k];
+                bool test = sl.kind == CL_S_RZ || sl.kind == CL_S_PT || sl.kind == CL_S_IMM;
+                if (sl.kind == CL_S_VAR) {
+                    test = sl.neg || sl.bitnot || sl.half;
+                    const unsigned v = sl.var & (CL_MAX_VARS - 1);
+                    if (ft[v] == 0xFF) { ft[v] = (uint8_t)t; fk[v] = (uint8_t)k; }
+                    else {
+                        if (q.n_pairs >= F_MAX_PAIRS) { snprintf(why, whylen, "pattern %u: too many variable occurrences", pi); return false; }
+                        uint8_t *m = q.pair[q.n_pairs++]; m[0] = ft[v]; m[1] = fk[v]; m[2] = (uint8_t)t; m[3] = (uint8_t)k;
+                    }
+                } else if (sl.kind != CL_S_ANY && !test) { snprintf(why, whylen, "pattern %u: unknown slot kind", pi); return false; }
+                if (test) {
+                    if (ft_.n_chk >= 8) { snprintf(why, whylen, "pattern %u: too many slot tests", pi); return false; }
+                    FChk &c = ft_.chk[ft_.n_chk++];
+                    c.imm = sl.imm; c.slot = (uint8_t)k; c.kind = sl.kind; c.neg = sl.neg; c.bitnot = sl.bitnot; c.half = sl.half;
+                }
+            }
+        }
+        if (p.rewrite == CL_RW_XMAD) {
+            const uint8_t vars[3] = { p.var_a, p.var_b, p.var_c };
+            for (unsigned k = 0; k < 3; k++) {
+                if (vars[k] >= CL_MAX_VARS || ft[vars[k]] == 0xFF) { snprintf(why, whylen, "pattern %u: xmad plan without $a $b $c", pi); return false; }
+                q.var_t[k] = ft[vars[k]]; q.var_k[k] = fk[vars[k]];
+            }
+        }
+        if (p.rewrite == CL_RW_ISETP64) {
+            /* "mod:cond" / "mod:bop" of the first template that binds them (template 0 in the reference's table) */
+            q.cond_group = q.bop_group = 0;
+            bool hc = false, hb = false;
+            const cl_template &t0 = p.t[0];
+            for (unsigned k = 0; k < t0.n_modvars && k < 2; k++) {
+                if (t0.modvar_var[k] == p.modvar_cond) { q.cond_group = t0.modvar_group[k]; hc = true; }
+                if (t0.modvar_var[k] == p.modvar_bop) { q.bop_group = t0.modvar_group[k]; hb = true; }
+            }
+            if (!hc || !hb) { snprintf(why, whylen, "pattern %u: isetp64 plan needs cond and bop on the first template", pi); return false; }
+        }
+    }
+    P.ok = 1;
+    return true;
+}
+
+/* ------------------------------------------------------------------ kernels */
+CLHD size_t f_prog_bytes() { return (sizeof(FProg) + sizeof(KArgs) + 255) & ~(size_t)255; }
+template <class C> CLHD size_t f_slice_bytes() { return (sizeof(FW<C>) + 127) & ~(size_t)127; }
+
+#if CLF_CUDA
+template <class C, int NW, int NG> __global__ void __launch_bounds__(NW *NG * 32, 1) k_fused(KArgs a, const FProg *gp, FLoop L) {
+    extern __shared__ uint4 dyn_smem[];
+    FProg &P = *(FProg *)dyn_smem;
+    KArgs &A = *(KArgs *)((uint8_t *)dyn_smem + sizeof(FProg));
+    {
+        const uint4 *src = (const uint4 *)gp;
+        uint4 *dst = (uint4 *)&P;
+        for (uint32_t i = threadIdx.x; i < sizeof(FProg) / 16; i += blockDim.x) dst[i] = src[i];
+        const unsigned long long *sa = (const unsigned long long *)&a;
+        unsigned long long *da = (unsigned long long *)&A;
+        for (uint32_t i = threadIdx.x; i < sizeof(KArgs) / 8; i += blockDim.x) da[i] = sa[i];
+    }
+    __syncthreads();
+    const uint32_t grp = threadIdx.x / (NW * 32);
+    FW<C> &W = *(FW<C> *)((uint8_t *)dyn_smem + f_prog_bytes() + (size_t)grp * f_slice_bytes<C>());
+    FG<NW> g; g.rank = threadIdx.x % (NW * 32); g.size = NW * 32; g.bar = 1 + grp; g.red = W.gred;
+    FEnv e; e.P = &P; e.a = &A; e.ms = A.in.modsets; e.imm_in = nullptr;
+    f_loop(g, W, e, L, blockIdx.x * NG + grp);
+}
+__global__ void k_fused_zero(uint32_t *p, uint32_t n) { if (threadIdx.x < n) p[threadIdx.x] = 0; }
+#endif
+
+/* --------------------------------------------------------------------- host */
+enum { FC_COUNT_L = 0, FC_COUNT_X, FC_WORK_S, FC_WORK_L, FC_WORK_X, FC__N = 8 };
+struct clf_ctx {
+    int device = 0, n_sm = 1;
+    FProg h_prog;
+    bool ok = false;
+    FProg *d_prog = nullptr;
+    uint32_t *d_words = nullptr;           /* FC_* counters */
+    uint32_t *d_list[2] = { nullptr, nullptr }; size_t list_cap = 0;
+    cl_event *d_mev = nullptr; size_t mev_cap_bytes = 0;
+    unsigned launches = 0;
+    bool attr_set = false;
+};
+
+#if CLF_CUDA
+#define F_CUDA_OK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { snprintf(err, errlen, "%s: %s", #x, cudaGetErrorString(e_)); return -1; } } while (0)
+static int f_alloc(void **p, size_t n, char *err, size_t errlen) { F_CUDA_OK(cudaMalloc(p, n ? n : 16)); return 0; }
+static void f_free(void *p) { if (p) cudaFree(p); }
+#else
+static int f_alloc(void **p, size_t n, char *err, size_t errlen) { *p = malloc(n ? n : 16); if (!*p) { snprintf(err, errlen, "out of memory"); return -1; } return 0; }
+static void f_free(void *p) { free(p); }
+#endif
+
+int clf_create(clf_ctx **out, int device, int n_sm) {
+    clf_ctx *c = new clf_ctx();
+    c->device = device; c->n_sm = n_sm > 0 ? n_sm : 1;
+    char err[128];
+    void *p = nullptr;
+    if (f_alloc(&p, sizeof(FProg), err, sizeof err)) { delete c; return -1; }
+    c->d_prog = (FProg *)p;
+    if (f_alloc(&p, sizeof(uint32_t) * FC__N, err, sizeof err)) { f_free(c->d_prog); delete c; return -1; }
+    c->d_words = (uint32_t *)p;
+    *out = c;
+    return 0;
+}
+void clf_destroy(clf_ctx *c) {
+    if (!c) return;
+    f_free(c->d_prog); f_free(c->d_words); f_free(c->d_list[0]); f_free(c->d_list[1]); f_free(c->d_mev);
+    delete c;
+}
+int clf_set_patterns(clf_ctx *c, const cl_pattern_blob *blob, void *stream, char *err, size_t errlen) {
+    char why[160] = "";
+    c->ok = fprog_build(*blob, c->h_prog, why, sizeof why);
+    if (getenv("CL_FUSED_DEBUG") && !c->ok) fprintf(stderr, "fused path off: %s\n", why);
+#if CLF_CUDA
+    F_CUDA_OK(cudaMemcpyAsync(c->d_prog, &c->h_prog, sizeof(FProg), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    F_CUDA_OK(cudaStreamSynchronize((cudaStream_t)stream));
+#else
+    memcpy(c->d_prog, &c->h_prog, sizeof(FProg));
+    (void)stream; (void)err; (void)errlen;
+#endif
+    return c->ok ? 1 : 0;
+}
+void clf_info(const clf_ctx *c, unsigned long long out[4]) {
+    out[0] = c->launches; out[1] = out[2] = out[3] = 0;
+}
+
+#if CLF_CUDA
+template <class C, int NW, int NG> static int f_launch(clf_ctx *c, const KArgs &k, const FLoop &L, uint32_t grid, cudaStream_t st, char *err, size_t errlen) {
+    const size_t smem = f_prog_bytes() + (size_t)NG * f_slice_bytes<C>();
+    static bool attr = false;
+    if (!attr) { F_CUDA_OK(cudaFuncSetAttribute(k_fused<C, NW, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
+    k_fused<C, NW, NG><<<grid, NW * NG * 32, smem, st>>>(k, c->d_prog, L);
+    F_CUDA_OK(cudaGetLastError());
+    c->launches++;
+    return 0;
+}
+#endif
+
+#ifndef CLF_GROUPS_S
+#define CLF_GROUPS_S 14
+#endif
+#ifndef CLF_GROUPS_L
+#define CLF_GROUPS_L 7
+#endif
+#ifndef CLF_GROUPS_X
+#define CLF_GROUPS_X 3
+#endif
+
+int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, size_t errlen) {
+    if (!c->ok) { snprintf(err, errlen, "fused path: pattern table not supported"); return -1; }
+    KArgs k = *kp;
+    c->launches = 0;
+    if (c->list_cap < F) {
+        for (int i = 0; i < 2; i++) { f_free(c->d_list[i]); c->d_list[i] = nullptr; }
+        const size_t want = (size_t)F + F / 16 + 64;
+        void *p = nullptr;
+        for (int i = 0; i < 2; i++) { if (f_alloc(&p, want * sizeof(uint32_t), err, errlen)) return -1; c->d_list[i] = (uint32_t *)p; }
+        c->list_cap = want;
+    }
+    const bool emit = k.emit_matches || (k.passes & CL_PASS_MATCH_ONLY);
+    const uint32_t groups[3] = { (uint32_t)c->n_sm * CLF_GROUPS_S, (uint32_t)c->n_sm * CLF_GROUPS_L, (uint32_t)c->n_sm * CLF_GROUPS_X };
+    const uint32_t mcap[3] = { emit ? 12 * FCfgS::M : 0u, emit ? 12 * FCfgL::M : 0u, emit ? 12 * FCfgX::M : 0u };
+    {
+        size_t need = 0;
+        need = std::max(need, groups[0] * f_scratch_bytes<FCfgS>(mcap[0]));
+        need = std::max(need, groups[1] * f_scratch_bytes<FCfgL>(mcap[1]));
+        need = std::max(need, groups[2] * f_scratch_bytes<FCfgX>(mcap[2]));
+        if (c->mev_cap_bytes < need) {
+            f_free(c->d_mev); c->d_mev = nullptr;
+            void *p = nullptr;
+            if (f_alloc(&p, need, err, errlen)) return -1;
+            c->d_mev = (cl_event *)p; c->mev_cap_bytes = need;
+        }
+    }
+    FLoop L[3];
+    for (int i = 0; i < 3; i++) {
+        L[i].list = i == 0 ? nullptr : c->d_list[i - 1];
+        L[i].n_list_ptr = i == 0 ? nullptr : c->d_words + FC_COUNT_L + (i - 1);
+        L[i].n_list = i == 0 ? F : 0;
+        L[i].counter = c->d_words + FC_WORK_S + i;
+        L[i].next_list = i < 2 ? c->d_list[i] : nullptr;
+        L[i].next_count = i < 2 ? c->d_words + FC_COUNT_L + i : nullptr;
+        L[i].scr = (uint8_t *)c->d_mev;
+        L[i].mev_cap = mcap[i];
+    }
+#if CLF_CUDA
+    cudaStream_t st = (cudaStream_t)stream;
+    k_fused_zero<<<1, 32, 0, st>>>(c->d_words, FC__N);
+    F_CUDA_OK(cudaGetLastError());
+    c->launches++;
+    const uint32_t grid = (uint32_t)c->n_sm;
+    if (f_launch<FCfgS, 1, CLF_GROUPS_S>(c, k, L[0], std::min<uint32_t>(grid, (F + CLF_GROUPS_S - 1) / CLF_GROUPS_S), st, err, errlen)) return -1;
+    if (f_launch<FCfgL, 2, CLF_GROUPS_L>(c, k, L[1], grid, st, err, errlen)) return -1;
+    if (f_launch<FCfgX, 4, CLF_GROUPS_X>(c, k, L[2], grid, st, err, errlen)) return -1;
+#else
+    (void)stream;
+    memset(c->d_words, 0, sizeof(uint32_t) * FC__N);
+    FEnv e; e.P = c->d_prog; e.a = &k; e.ms = k.in.modsets; e.imm_in = nullptr;
+    FG<0> g; g.rank = 0; g.size = 1; g.bar = 0;
+    { static FW<FCfgS> W; g.red = W.gred; f_loop(g, W, e, L[0], 0); }
+    { static FW<FCfgL> W; g.red = W.gred; f_loop(g, W, e, L[1], 0); }
+    { static FW<FCfgX> W; g.red = W.gred; f_loop(g, W, e, L[2], 0); }
+    c->launches = 3;
+#endif
+    return 0;
+}

@@ -41,12 +41,12 @@ def build_oracle():
 
 def build_sim():
     """One-lane CPU build of the device code (tests/sim): logic checks without a GPU."""
-    srcs = [CSRC / n for n in ("culifter.cu", "stream.cu", "core.cuh", "tile.cuh", "stream.cuh", "stream.h", "kargs.h")]
+    srcs = [CSRC / n for n in ("culifter.cu", "stream.cu", "fused.cu", "core.cuh", "tile.cuh", "stream.cuh", "fused.cuh", "stream.h", "fused.h", "kargs.h")]
     srcs.append(ROOT / "include" / "culifter.h")
     if not SIM_LIB.exists() or any(s.stat().st_mtime > SIM_LIB.stat().st_mtime for s in srcs):
         SIM_LIB.parent.mkdir(parents=True, exist_ok=True)
         subprocess.run(["g++", "-x", "c++", "-std=c++17", "-O1", "-g", "-DCL_SIM", "-fPIC", "-shared",
-                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu"), str(CSRC / "stream.cu")], check=True)
+                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu"), str(CSRC / "stream.cu"), str(CSRC / "fused.cu")], check=True)
     return SIM_LIB
 
 
