@@ -15,6 +15,9 @@
  * Compiled with -DCL_SIM by g++ this file is the one-lane CPU build of the same
  * device code (tests/sim), never loaded by the package.
  */
+/* core.cuh defines its non-inline device functions with external linkage and is also part of culifter.cu:
+ * this translation unit gets its own copy of the namespace */
+#define clk clk_fused
 #include "fused.cuh"
 #include "fused.h"
 
@@ -139,8 +142,9 @@ static bool fprog_build(const cl_pattern_blob &pb, FProg &P, char *why, size_t w
 }
 
 /* ------------------------------------------------------------------ kernels */
-CLHD size_t f_prog_bytes() { return (sizeof(FProg) + sizeof(KArgs) + 255) & ~(size_t)255; }
-template <class C> CLHD size_t f_slice_bytes() { return (sizeof(FW<C>) + 127) & ~(size_t)127; }
+constexpr size_t F_SMEM_MAX = 232448;      /* 227 KB: the most dynamic shared memory a CTA can opt in to on sm_100 */
+CLHD constexpr size_t f_prog_bytes() { return (sizeof(FProg) + sizeof(KArgs) + 15) & ~(size_t)15; }
+template <class C> CLHD constexpr size_t f_slice_bytes() { return (sizeof(FW<C>) + 15) & ~(size_t)15; }
 
 #if CLF_CUDA
 template <class C, int NW, int NG> __global__ void __launch_bounds__(NW *NG * 32, 1) k_fused(KArgs a, const FProg *gp, FLoop L) {
@@ -162,18 +166,68 @@ template <class C, int NW, int NG> __global__ void __launch_bounds__(NW *NG * 32
     FEnv e; e.P = &P; e.a = &A; e.ms = A.in.modsets; e.imm_in = nullptr;
     f_loop(g, W, e, L, blockIdx.x * NG + grp);
 }
-__global__ void k_fused_zero(uint32_t *p, uint32_t n) { if (threadIdx.x < n) p[threadIdx.x] = 0; }
+__global__ void k_fused_zero(uint32_t *p, uint32_t n) { for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = 0; }
+#endif
+
+/* ---------------------------------------------------- size-sorted work list */
+/* The groups of a CTA walk through the passes in lock step, so a batch should hold functions of about equal
+ * cost: counting sort of the functions by (size class, architecture, record count) on the device.  Functions
+ * beyond the largest class go straight to the retry lists of the general kernels.                        */
+static constexpr uint32_t FS_NBITS = 10, FS_BINS = 4u << (FS_NBITS + 1);
+CLHD uint32_t f_sort_key(const cl_corpus &in, uint32_t f) {
+    const uint32_t n = in.blk_off[in.func_blk_off[f + 1]] - in.blk_off[in.func_blk_off[f]];
+    const uint32_t cls = n <= FCfgS::IN ? 0u : n <= FCfgL::IN ? 1u : n <= FCfgX::IN ? 2u : 3u;
+    const uint32_t nn = cls == 3 ? 0u : n;
+    return cls << (FS_NBITS + 1) | (in.func[f].arch == CL_ARCH_SM52 ? 1u : 0u) << FS_NBITS | nn;
+}
+#if CLF_CUDA
+__global__ void k_fsort_hist(cl_corpus in, uint32_t F, uint32_t *hist) {
+    for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) atomicAdd(&hist[f_sort_key(in, f)], 1u);
+}
+__global__ void __launch_bounds__(1024) k_fsort_scan(uint32_t *hist, uint32_t *bounds) {      /* one CTA: exclusive scan of the bins in place */
+    __shared__ uint32_t part[1024];
+    constexpr uint32_t PER = FS_BINS / 1024;
+    uint32_t loc[PER], sum = 0;
+    for (uint32_t k = 0; k < PER; k++) { loc[k] = hist[threadIdx.x * PER + k]; sum += loc[k]; }
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (uint32_t d = 1; d < 1024; d <<= 1) {
+        const uint32_t t = threadIdx.x >= d ? part[threadIdx.x - d] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += t;
+        __syncthreads();
+    }
+    uint32_t run = part[threadIdx.x] - sum;
+    for (uint32_t k = 0; k < PER; k++) {
+        const uint32_t bin = threadIdx.x * PER + k;
+        hist[bin] = run;
+        if ((bin & ((2u << FS_NBITS) - 1u)) == 0) bounds[bin >> (FS_NBITS + 1)] = run;      /* first bin of a size class */
+        run += loc[k];
+    }
+    if (threadIdx.x == 1023) bounds[4] = run;
+}
+__global__ void k_fsort_scatter(KArgs a, uint32_t F, uint32_t *cursor, uint32_t *list) {
+    for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        const uint32_t key = f_sort_key(a.in, f);
+        list[atomicAdd(&cursor[key], 1u)] = f;
+        if (key >> (FS_NBITS + 1) == 3) {        /* too large for every class */
+            const uint32_t n = a.in.blk_off[a.in.func_blk_off[f + 1]] - a.in.blk_off[a.in.func_blk_off[f]];
+            if (n > a.small_max) a.retry_big_list[atomicAdd(a.retry_big_count, 1u)] = f;
+            else a.retry_list[atomicAdd(a.retry_count, 1u)] = f;
+        }
+    }
+}
 #endif
 
 /* --------------------------------------------------------------------- host */
-enum { FC_COUNT_L = 0, FC_COUNT_X, FC_WORK_S, FC_WORK_L, FC_WORK_X, FC__N = 8 };
+enum { FC_COUNT_L = 0, FC_COUNT_X, FC_WORK_S, FC_WORK_L, FC_WORK_X, FC_BOUNDS = 8 /* [5]: start of each size class in the sorted list */, FC_HIST = 16, FC__N = FC_HIST + (4u << 11) };
 struct clf_ctx {
     int device = 0, n_sm = 1;
     FProg h_prog;
     bool ok = false;
     FProg *d_prog = nullptr;
     uint32_t *d_words = nullptr;           /* FC_* counters */
-    uint32_t *d_list[2] = { nullptr, nullptr }; size_t list_cap = 0;
+    uint32_t *d_list[3] = { nullptr, nullptr, nullptr }; size_t list_cap = 0;      /* [0] [1]: overflow lists of classes L, X; [2]: all functions, sorted */
     cl_event *d_mev = nullptr; size_t mev_cap_bytes = 0;
     unsigned launches = 0;
     bool attr_set = false;
@@ -202,7 +256,7 @@ int clf_create(clf_ctx **out, int device, int n_sm) {
 }
 void clf_destroy(clf_ctx *c) {
     if (!c) return;
-    f_free(c->d_prog); f_free(c->d_words); f_free(c->d_list[0]); f_free(c->d_list[1]); f_free(c->d_mev);
+    f_free(c->d_prog); f_free(c->d_words); f_free(c->d_list[0]); f_free(c->d_list[1]); f_free(c->d_list[2]); f_free(c->d_mev);
     delete c;
 }
 int clf_set_patterns(clf_ctx *c, const cl_pattern_blob *blob, void *stream, char *err, size_t errlen) {
@@ -224,9 +278,9 @@ void clf_info(const clf_ctx *c, unsigned long long out[4]) {
 
 #if CLF_CUDA
 template <class C, int NW, int NG> static int f_launch(clf_ctx *c, const KArgs &k, const FLoop &L, uint32_t grid, cudaStream_t st, char *err, size_t errlen) {
-    const size_t smem = f_prog_bytes() + (size_t)NG * f_slice_bytes<C>();
-    static bool attr = false;
-    if (!attr) { F_CUDA_OK(cudaFuncSetAttribute(k_fused<C, NW, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
+    constexpr size_t smem = f_prog_bytes() + (size_t)NG * f_slice_bytes<C>();
+    static_assert(smem <= F_SMEM_MAX, "the groups of a CTA do not fit the SM's shared memory");
+    F_CUDA_OK(cudaFuncSetAttribute(k_fused<C, NW, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_fused<C, NW, NG><<<grid, NW * NG * 32, smem, st>>>(k, c->d_prog, L);
     F_CUDA_OK(cudaGetLastError());
     c->launches++;
@@ -235,7 +289,7 @@ template <class C, int NW, int NG> static int f_launch(clf_ctx *c, const KArgs &
 #endif
 
 #ifndef CLF_GROUPS_S
-#define CLF_GROUPS_S 14
+#define CLF_GROUPS_S 13
 #endif
 #ifndef CLF_GROUPS_L
 #define CLF_GROUPS_L 7
@@ -249,10 +303,10 @@ int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, si
     KArgs k = *kp;
     c->launches = 0;
     if (c->list_cap < F) {
-        for (int i = 0; i < 2; i++) { f_free(c->d_list[i]); c->d_list[i] = nullptr; }
+        for (int i = 0; i < 3; i++) { f_free(c->d_list[i]); c->d_list[i] = nullptr; }
         const size_t want = (size_t)F + F / 16 + 64;
         void *p = nullptr;
-        for (int i = 0; i < 2; i++) { if (f_alloc(&p, want * sizeof(uint32_t), err, errlen)) return -1; c->d_list[i] = (uint32_t *)p; }
+        for (int i = 0; i < 3; i++) { if (f_alloc(&p, want * sizeof(uint32_t), err, errlen)) return -1; c->d_list[i] = (uint32_t *)p; }
         c->list_cap = want;
     }
     const bool emit = k.emit_matches || (k.passes & CL_PASS_MATCH_ONLY);
@@ -272,9 +326,10 @@ int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, si
     }
     FLoop L[3];
     for (int i = 0; i < 3; i++) {
-        L[i].list = i == 0 ? nullptr : c->d_list[i - 1];
-        L[i].n_list_ptr = i == 0 ? nullptr : c->d_words + FC_COUNT_L + (i - 1);
-        L[i].n_list = i == 0 ? F : 0;
+        L[i].list = c->d_list[2];
+        L[i].bounds = c->d_words + FC_BOUNDS + i;
+        L[i].list2 = i == 0 ? nullptr : c->d_list[i - 1];
+        L[i].n_list2_ptr = i == 0 ? nullptr : c->d_words + FC_COUNT_L + (i - 1);
         L[i].counter = c->d_words + FC_WORK_S + i;
         L[i].next_list = i < 2 ? c->d_list[i] : nullptr;
         L[i].next_count = i < 2 ? c->d_words + FC_COUNT_L + i : nullptr;
@@ -283,16 +338,35 @@ int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, si
     }
 #if CLF_CUDA
     cudaStream_t st = (cudaStream_t)stream;
-    k_fused_zero<<<1, 32, 0, st>>>(c->d_words, FC__N);
+    static_assert(FC_HIST + FS_BINS == FC__N, "histogram bins");
+    const uint32_t grid = (uint32_t)c->n_sm, sgrid = std::min<uint32_t>((F + 255) / 256, grid * 8);
+    k_fused_zero<<<8, 1024, 0, st>>>(c->d_words, FC__N);
+    k_fsort_hist<<<sgrid, 256, 0, st>>>(k.in, F, c->d_words + FC_HIST);
+    k_fsort_scan<<<1, 1024, 0, st>>>(c->d_words + FC_HIST, c->d_words + FC_BOUNDS);
+    k_fsort_scatter<<<sgrid, 256, 0, st>>>(k, F, c->d_words + FC_HIST, c->d_list[2]);
     F_CUDA_OK(cudaGetLastError());
-    c->launches++;
-    const uint32_t grid = (uint32_t)c->n_sm;
-    if (f_launch<FCfgS, 1, CLF_GROUPS_S>(c, k, L[0], std::min<uint32_t>(grid, (F + CLF_GROUPS_S - 1) / CLF_GROUPS_S), st, err, errlen)) return -1;
+    c->launches += 4;
+    if (f_launch<FCfgS, 1, CLF_GROUPS_S>(c, k, L[0], grid, st, err, errlen)) return -1;
     if (f_launch<FCfgL, 2, CLF_GROUPS_L>(c, k, L[1], grid, st, err, errlen)) return -1;
     if (f_launch<FCfgX, 4, CLF_GROUPS_X>(c, k, L[2], grid, st, err, errlen)) return -1;
 #else
     (void)stream;
     memset(c->d_words, 0, sizeof(uint32_t) * FC__N);
+    {   /* the same counting sort on the host */
+        uint32_t *hist = c->d_words + FC_HIST, *bounds = c->d_words + FC_BOUNDS;
+        for (uint32_t f = 0; f < F; f++) hist[f_sort_key(k.in, f)]++;
+        uint32_t run = 0;
+        for (uint32_t b = 0; b < FS_BINS; b++) { const uint32_t n = hist[b]; hist[b] = run; if ((b & ((2u << FS_NBITS) - 1u)) == 0) bounds[b >> (FS_NBITS + 1)] = run; run += n; }
+        bounds[4] = run;
+        for (uint32_t f = 0; f < F; f++) {
+            const uint32_t key = f_sort_key(k.in, f);
+            c->d_list[2][hist[key]++] = f;
+            if (key >> (FS_NBITS + 1) == 3) {
+                const uint32_t n = k.in.blk_off[k.in.func_blk_off[f + 1]] - k.in.blk_off[k.in.func_blk_off[f]];
+                if (n > k.small_max) k.retry_big_list[(*k.retry_big_count)++] = f; else k.retry_list[(*k.retry_count)++] = f;
+            }
+        }
+    }
     FEnv e; e.P = c->d_prog; e.a = &k; e.ms = k.in.modsets; e.imm_in = nullptr;
     FG<0> g; g.rank = 0; g.size = 1; g.bar = 0;
     { static FW<FCfgS> W; g.red = W.gred; f_loop(g, W, e, L[0], 0); }

@@ -145,13 +145,16 @@ template <> struct FG<0> {
     CLMEM unsigned long long min64(unsigned long long x) const { return x; }
 };
 
+/* uniform strided loop over the lanes of a group (like GFOR of core.cuh), never unrolled: code size is what bounds this stage */
+#define FFOR(g, i, n) _Pragma("unroll 1") for (uint32_t _b##i = 0, i = (g).rank; _b##i < (n); _b##i += (g).size, i += (g).size)
+
 /* ------------------------------------------------------- size classes */
 /* I: record slots of the arena, IN: largest input the class accepts, V: values,
  * B: blocks, MR: memrefs, Q: new immediates, L: def_iid updates, M: raw matches
  * of one round, E: events (group-private global scratch, not shared memory)  */
-struct FCfgS { static constexpr uint32_t I = 128, IN = 104, V = 176, VIN = 144, B = 12, MR = 28, Q = 16, L = 256, M = 48, E = 64; };
-struct FCfgL { static constexpr uint32_t I = 256, IN = 208, V = 352, VIN = 288, B = 24, MR = 56, Q = 32, L = 512, M = 96, E = 128; };
-struct FCfgX { static constexpr uint32_t I = 512, IN = 416, V = 704, VIN = 576, B = 48, MR = 112, Q = 64, L = 1024, M = 192, E = 256; };
+struct FCfgS { static constexpr uint32_t I = 128, IN = 104, V = 176, VIN = 144, B = 12, MR = 28, Q = 16, L = 256, M = 48, E = 64, TQ = 24; };
+struct FCfgL { static constexpr uint32_t I = 256, IN = 208, V = 352, VIN = 288, B = 24, MR = 56, Q = 32, L = 512, M = 96, E = 128, TQ = 32; };
+struct FCfgX { static constexpr uint32_t I = 512, IN = 416, V = 704, VIN = 576, B = 48, MR = 112, Q = 64, L = 1024, M = 192, E = 256, TQ = 96; };
 
 enum { SF_LIVE = 1, SF_PURE = 2, SF_INS = 4 /* waits in an insertion list for the next rebuild */, SF_TAKEN = 8, SF_CLS_SHIFT = 4, SF_NOCLS = 15 };
 enum { FF_ODD = 1, FF_RZDEF = 2, FF_PREDDEF = 4, FF_RCP = 8, FF_WLOVER = 16, FF_SWEPT = 32 };
@@ -167,12 +170,14 @@ template <class C> struct FW {                 /* one function resident in a gro
     alignas(16) uint16_t tag[C::I * 8];
     alignas(16) uint32_t pay[C::I * 8];
     alignas(16) cl_imm newimm[C::Q];
+    cl_imm timm[C::TQ];                         /* immediates of the rewrites being planned (staged until their index is known) */
     cl_event *ev;                               /* [C::E] events of the function: group-private global scratch */
     FDLog *dlog;                                /* [C::L] def_iid updates in program order: same scratch         */
     cl_blk blk[C::B];
     cl_memref mem[C::MR];
     uint32_t usecnt[C::V];
     uint32_t ccnt[C::B][MAX_CLS];
+    uint32_t acnt[2 * (MAX_CLS + 4)];           /* anchors per seed class, then the fill cursors (f_match) */
     FMatch mt[C::M];
     unsigned long long prof[PF__N], prof_t;   /* cycles per phase (lane 0), flushed at the end of the loop */
     uint32_t fstat[64];
@@ -181,7 +186,7 @@ template <class C> struct FW {                 /* one function resident in a gro
     uint32_t f, n_in, nb, nv_in, nq_in, n_mem, arch, i0, b0, q0, m0, v0;
     uint32_t n_slots, n_pos, cur, next_vid, next_iid, next_temp, n_newimm, n_log, n_mt, n_sel;
     uint32_t wl_tail, n_ev, fail, dirty, flags, nred, big_blocks, n_mev;
-    uint32_t r_inst, r_imm, r_val, r_ev, work, ret, n_free, pad1;
+    uint32_t r_inst, r_imm, r_val, r_ev, work, ret, n_free, n_timm;
     uint16_t defslot[C::V], redirect[C::V], vtmp[C::V];
     uint16_t norigin[C::V];                     /* ValueInfo.origin of the values created here: kind << 14 | vid (f_origin) */
     uint16_t ord[2][C::I], posof[C::I], insslot[C::I], outpos[C::I], wl[C::I];
@@ -220,23 +225,51 @@ template <class C> CLD cl_imm f_imm_at(const FW<C> &W, const FEnv &e, uint32_t i
     return W.newimm[(idx - W.nq_in) & (C::Q - 1)];
 }
 template <class C> CLD bool f_live(const FW<C> &W, uint32_t s) { return (W.sflag[s] & SF_LIVE) != 0; }
-/* value_operands (ssa.py:599-610) / all_defs                                  */
-template <class C, class F> CLD void f_value_operands(const FW<C> &W, const cl_hdr &h, uint32_t s, F fn) {
-    if (has_guard(h)) { const opnd g = f_slot(W, s, 0); if (is_value(g)) fn(g.pay); }
-    const unsigned u0 = use0(h);
-    for (unsigned k = 0; k < h.n_uses; k++) {
-        const opnd u = f_slot(W, s, u0 + k);
-        if (is_value(u)) fn(u.pay);
-        else if (kind_of(u.tag) == CL_K_MEMREF) {
-            const cl_memref &m = W.mem[u.pay < C::MR ? u.pay : 0];
-            if (kind_of(m.base_tag) == CL_K_VALUE) fn(m.base_pay);
-            if (kind_of(m.ureg_tag) == CL_K_VALUE) fn(m.ureg_pay);
+/* value_operands (ssa.py:599-610) / all_defs of one record, as a packed list of value ids.
+ * Out of line and rolled: every pass asks for them, and the unrolled, inlined form of these
+ * loops was most of the kernel's code (the stage is instruction-fetch bound).               */
+struct FVals { unsigned long long lo, hi; uint32_t n; };
+CLD uint32_t f_val(const FVals &u, uint32_t k) { return (uint32_t)((k < 4 ? u.lo : u.hi) >> ((k & 3u) * 16u)) & 0xFFFFu; }
+CLD void f_val_push(FVals &u, uint32_t v) {
+    if (v > 0xFFFFu) v = 0xFFFFu;                    /* no such value: callers range-check */
+    if (u.n < 4) u.lo |= (unsigned long long)v << (u.n * 16u);
+    else if (u.n < 8) u.hi |= (unsigned long long)v << ((u.n - 4u) * 16u);
+    u.n++;                                           /* n > 8: more value operands than the list holds (f_index hands the function back) */
+}
+template <class C> CLN FVals f_uses(const FW<C> &W, uint32_t s) {
+    FVals u; u.lo = u.hi = 0; u.n = 0;
+    const cl_hdr h = W.hdr[s];
+    if (has_guard(h)) { const opnd g = f_slot(W, s, 0); if (is_value(g)) f_val_push(u, g.pay); }
+    const unsigned u0 = use0(h), u1 = u0 + h.n_uses;
+#pragma unroll 1
+    for (unsigned k = u0; k < u1 && k < 8; k++) {
+        const opnd o = f_slot(W, s, k);
+        if (is_value(o)) f_val_push(u, o.pay);
+        else if (kind_of(o.tag) == CL_K_MEMREF) {
+            const cl_memref &m = W.mem[o.pay < C::MR ? o.pay : 0];
+            if (kind_of(m.base_tag) == CL_K_VALUE) f_val_push(u, m.base_pay);
+            if (kind_of(m.ureg_tag) == CL_K_VALUE) f_val_push(u, m.ureg_pay);
         }
     }
+    return u;
 }
-template <class C, class F> CLD void f_value_defs(const FW<C> &W, const cl_hdr &h, uint32_t s, F fn) {
-    const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
-    for (unsigned k = 0; k < nd; k++) { const opnd d = f_slot(W, s, d0 + k); if (is_value(d)) fn(d.pay); }
+template <class C> CLN FVals f_defs(const FW<C> &W, uint32_t s) {
+    FVals u; u.lo = u.hi = 0; u.n = 0;
+    const cl_hdr h = W.hdr[s];
+    const unsigned d0 = def0(h), d1 = d0 + h.n_defs + h.n_aux;
+#pragma unroll 1
+    for (unsigned k = d0; k < d1 && k < 8; k++) { const opnd d = f_slot(W, s, k); if (is_value(d)) f_val_push(u, d.pay); }
+    return u;
+}
+template <class C, class F> CLD void f_value_operands(const FW<C> &W, const cl_hdr &, uint32_t s, F fn) {
+    const FVals u = f_uses(W, s);
+#pragma unroll 1
+    for (uint32_t k = 0; k < u.n && k < 8; k++) fn(f_val(u, k));
+}
+template <class C, class F> CLD void f_value_defs(const FW<C> &W, const cl_hdr &, uint32_t s, F fn) {
+    const FVals u = f_defs(W, s);
+#pragma unroll 1
+    for (uint32_t k = 0; k < u.n && k < 8; k++) fn(f_val(u, k));
 }
 /* DCE worklist: the defining record of a value whose use count reached zero  */
 template <class C> CLD void f_push_wl(FW<C> &W, uint32_t ds) {
@@ -246,7 +279,7 @@ template <class C> CLD void f_push_wl(FW<C> &W, uint32_t ds) {
     if (k < C::I) W.wl[k] = (uint16_t)ds;
     else W.flags |= FF_WLOVER;                   /* racing lanes write the same bit */
 }
-template <class C> CLD void f_dec_use(FW<C> &W, uint32_t v) {
+template <class C> CLN void f_dec_use(FW<C> &W, uint32_t v) {
     if (v >= C::V) return;
     if (a_sub(&W.usecnt[v], 1u) == 1u) f_push_wl(W, W.defslot[v]);
 }
@@ -286,22 +319,22 @@ template <class G, class C> CLF bool f_load(const G &g, FW<C> &W, FEnv &e, uint3
         W.i0 = i0; W.b0 = b0; W.q0 = q0; W.m0 = m0; W.v0 = v0;
         W.n_slots = n; W.n_pos = n; W.cur = 0; W.next_vid = fn.next_vid; W.next_iid = fn.next_iid; W.next_temp = fn.next_temp_reg;
         W.n_newimm = 0; W.n_log = 0; W.n_mt = 0; W.n_sel = 0; W.wl_tail = 0; W.n_ev = 0; W.fail = 0; W.dirty = 0;
-        W.flags = 0; W.nred = 0; W.big_blocks = 0; W.n_mev = 0; W.ret = 0; W.n_free = 0;
+        W.flags = 0; W.nred = 0; W.big_blocks = 0; W.n_mev = 0; W.ret = 0; W.n_free = 0; W.n_timm = 0;
         if (in.ext_off[f + 1] != in.ext_off[f] || nb == 0) W.fail = F_REDO + 1;      /* overflow slots: general kernel */
     }
     e.imm_in = in.imm + q0;
     {
         const uint4 *sh = (const uint4 *)(in.hdr + i0), *st = (const uint4 *)(in.tag + (size_t)i0 * 8), *sp = (const uint4 *)(in.pay + (size_t)i0 * 8);
         uint4 *dh = (uint4 *)W.hdr, *dt = (uint4 *)W.tag, *dp = (uint4 *)W.pay;
-        GFOR(g, i, n) if (i < n) { dh[i] = sh[i]; dt[i] = st[i]; }
-        GFOR(g, i, 2 * n) if (i < 2 * n) dp[i] = sp[i];
+        FFOR(g, i, n) if (i < n) { dh[i] = sh[i]; dt[i] = st[i]; }
+        FFOR(g, i, 2 * n) if (i < 2 * n) dp[i] = sp[i];
     }
-    GFOR(g, b, nb + 1) if (b <= nb) W.bo[b] = (uint16_t)(in.blk_off[b0 + b] - i0);
-    GFOR(g, b, nb) if (b < nb) W.blk[b] = in.blk[b0 + b];
-    GFOR(g, m, nm) if (m < nm) W.mem[m] = in.mem[m0 + m];
-    GFOR(g, v, fn.next_vid) if (v < fn.next_vid) { W.alive[v] = in.val_alive[v0 + v]; W.usecnt[v] = 0; W.defslot[v] = F_NONE; }
-    GFOR(g, k, 64) if (k < 64) W.fstat[k] = 0;
-    GFOR(g, i, n) if (i < n) { W.ord[0][i] = (uint16_t)i; W.posof[i] = (uint16_t)i; W.inscnt[i] = 0; }
+    FFOR(g, b, nb + 1) if (b <= nb) W.bo[b] = (uint16_t)(in.blk_off[b0 + b] - i0);
+    FFOR(g, b, nb) if (b < nb) W.blk[b] = in.blk[b0 + b];
+    FFOR(g, m, nm) if (m < nm) W.mem[m] = in.mem[m0 + m];
+    FFOR(g, v, fn.next_vid) if (v < fn.next_vid) { W.alive[v] = in.val_alive[v0 + v]; W.usecnt[v] = 0; W.defslot[v] = F_NONE; }
+    FFOR(g, k, 64) if (k < 64) W.fstat[k] = 0;
+    FFOR(g, i, n) if (i < n) { W.ord[0][i] = (uint16_t)i; W.posof[i] = (uint16_t)i; W.inscnt[i] = 0; }
     g.sync();
     return true;
 }
@@ -314,7 +347,7 @@ template <class G, class C> CLF void f_index(const G &g, FW<C> &W, const FEnv &e
     const FProg &P = *e.P;
     const uint32_t n = W.n_in, nb = W.nb;
     uint32_t fl = 0;
-    GFOR(g, s, n) if (s < n) {
+    FFOR(g, s, n) if (s < n) {
         const cl_hdr h = W.hdr[s];
         uint32_t lo = 0, hi = nb;                    /* last b with bo[b] <= s */
         while (lo + 1 < hi) { const uint32_t mid = (lo + hi) >> 1; if (W.bo[mid] <= s) lo = mid; else hi = mid; }
@@ -325,6 +358,7 @@ template <class G, class C> CLF void f_index(const G &g, FW<C> &W, const FEnv &e
         if (h.flags & CL_IF_EXT) { fl |= FF_ODD; continue; }
         if (h.op == CL_OP_MUFU && ((e.ms[h.modset].mask >> CL_MB_RCP) & 1u)) fl |= FF_RCP;
         const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
+#pragma unroll 1
         for (unsigned k = 0; k < nd; k++) {
             const opnd d = f_slot(W, s, d0 + k);
             const unsigned kd = kind_of(d.tag);
@@ -333,9 +367,15 @@ template <class G, class C> CLF void f_index(const G &g, FW<C> &W, const FEnv &e
             else if (kd == CL_K_PRED) fl |= FF_PREDDEF;
             else fl |= FF_ODD;
         }
-        f_value_operands(W, h, s, [&](uint32_t v) { if (v < W.nv_in) a_add(&W.usecnt[v], 1u); else fl |= FF_ODD; });
+        {
+            const FVals u = f_uses(W, s);
+            if (u.n > 8) fl |= FF_ODD;                 /* more value operands than FVals holds */
+#pragma unroll 1
+            for (uint32_t k = 0; k < u.n && k < 8; k++) { const uint32_t v = f_val(u, k); if (v < W.nv_in) a_add(&W.usecnt[v], 1u); else fl |= FF_ODD; }
+        }
     }
-    GFOR(g, b, nb) if (b < nb)
+    FFOR(g, b, nb) if (b < nb)
+#pragma unroll 1
         for (int k = 0; k < 2; k++)
             if (kind_of(W.blk[b].term_tag[k]) == CL_K_VALUE) { const uint32_t v = W.blk[b].term_pay[k]; if (v < W.nv_in) a_add(&W.usecnt[v], 1u); else fl |= FF_ODD; }
 #if CL_DEV
@@ -351,7 +391,7 @@ template <class G, class C> CLF void f_index(const G &g, FW<C> &W, const FEnv &e
 template <class G, class C> CLF void f_reclass(const G &g, FW<C> &W, const FEnv &e, unsigned table) {
     const FProg &P = *e.P;
     const uint32_t n = W.n_slots;
-    GFOR(g, s, n) if (s < n) W.sflag[s] = (uint8_t)((W.sflag[s] & 15u) | f_cls(P, table, W.hdr[s].op) << SF_CLS_SHIFT);
+    FFOR(g, s, n) if (s < n) W.sflag[s] = (uint8_t)((W.sflag[s] & 15u) | f_cls(P, table, W.hdr[s].op) << SF_CLS_SHIFT);
     g.sync();
 }
 
@@ -363,7 +403,7 @@ template <class G, class C> CLF void f_rebuild(const G &g, FW<C> &W) {
     const uint16_t *oo = W.ord[cur];
     uint16_t *on = W.ord[cur ^ 1];
     uint32_t run = 0;
-    GFOR(g, p, n) {
+    FFOR(g, p, n) {
         uint32_t c = 0, me = 0;
         if (p < n) {
             const uint32_t s = oo[p];
@@ -389,11 +429,11 @@ template <class G, class C> CLF void f_rebuild(const G &g, FW<C> &W) {
     }
     g.sync();
     uint16_t *nbo = W.sel;                         /* free outside select .. rewrite */
-    GFOR(g, b, W.nb + 1) if (b <= W.nb) { const uint32_t old = W.bo[b]; nbo[b] = old < n ? W.outpos[old] : (uint16_t)run; }
+    FFOR(g, b, W.nb + 1) if (b <= W.nb) { const uint32_t old = W.bo[b]; nbo[b] = old < n ? W.outpos[old] : (uint16_t)run; }
     g.sync();
-    GFOR(g, b, W.nb + 1) if (b <= W.nb) W.bo[b] = nbo[b];
+    FFOR(g, b, W.nb + 1) if (b <= W.nb) W.bo[b] = nbo[b];
     const uint32_t nz = run > n ? run : n;
-    GFOR(g, p, nz) if (p < nz) { W.inscnt[p] = 0; if (p < run) W.sflag[on[p]] &= (uint8_t)~SF_INS; }
+    FFOR(g, p, nz) if (p < nz) { W.inscnt[p] = 0; if (p < run) W.sflag[on[p]] &= (uint8_t)~SF_INS; }
     if (g.rank == 0) { W.n_pos = run; W.cur = cur ^ 1; W.dirty = 0; }
     g.sync();
 }
@@ -426,8 +466,10 @@ template <class C> CLN bool f_match_local(const FW<C> &W, const FEnv &e, const F
     const cl_modset &ms = e.ms[h.modset];
     if ((ms.mask & t.mods_all) != t.mods_all) return false;
     if (ms.mask & t.mods_none) return false;
+#pragma unroll 1
     for (unsigned k = 0; k < t.n_mv; k++) if (ms.first[t.mv_group[k]] == 0xFF) return false;
     const unsigned g0 = has_guard(h);
+#pragma unroll 1
     for (unsigned q = 0; q < t.n_chk; q++) {
         const FChk &c = t.chk[q];
         const opnd o = f_slot(W, s, g0 + c.slot);
@@ -454,6 +496,7 @@ template <class C> CLN uint32_t f_class_rank(const FW<C> &W, uint32_t s) {
     const uint32_t b = W.sblk[s], cls = W.sflag[s] >> SF_CLS_SHIFT, p1 = W.posof[s];
     const uint16_t *o = W.ord[W.cur];
     uint32_t r = 0;
+#pragma unroll 1
     for (uint32_t p = W.bo[b]; p < p1; p++) { const uint32_t q = o[p]; r += (W.sflag[q] & SF_LIVE) && (uint32_t)(W.sflag[q] >> SF_CLS_SHIFT) == cls; }
     return r;
 }
@@ -472,6 +515,7 @@ template <class C> CLF void f_try_anchor(FW<C> &W, const FEnv &e, uint32_t s, un
     h[ta] = W.hdr[s];
     if (!f_match_local(W, e, p.t[ta], h[ta], s)) return;
     const uint32_t blk = W.sblk[s];
+#pragma unroll 1
     for (unsigned k = 1; k < nt; k++) {
         const unsigned t = p.order[k], from = p.from[k];
         const opnd o = f_slot(W, idx[from], has_guard(h[from]) + p.jslot[k]);
@@ -489,10 +533,12 @@ template <class C> CLF void f_try_anchor(FW<C> &W, const FEnv &e, uint32_t s, un
         idx[t] = dp;
     }
     if (nt > 1 && !(W.posof[idx[0]] < W.posof[idx[1]] && (nt < 3 || W.posof[idx[1]] < W.posof[idx[2]]))) return;
+#pragma unroll 1
     for (unsigned q = 0; q < p.n_mpairs; q++) {
         const uint8_t *m = p.mpair[q];
         if (e.ms[h[m[0]].modset].first[m[1]] != e.ms[h[m[2]].modset].first[m[3]]) return;
     }
+#pragma unroll 1
     for (unsigned q = 0; q < p.n_pairs; q++) {
         const uint8_t *m = p.pair[q];
         if (!f_key_equal(W, e, f_slot(W, idx[m[0]], has_guard(h[m[0]]) + m[1]), f_slot(W, idx[m[2]], has_guard(h[m[2]]) + m[3]))) return;
@@ -500,9 +546,11 @@ template <class C> CLF void f_try_anchor(FW<C> &W, const FEnv &e, uint32_t s, un
     /* budget (G1): only where the product of the candidate-list sizes can exceed it */
     if (W.big_blocks && nt > 1) {
         unsigned long long prod = 1;
+#pragma unroll 1
         for (unsigned t = 0; t < nt; t++) prod *= W.ccnt[blk][p.t[t].cls];
         if (prod > e.P->budget) {
             unsigned long long r = 0;
+#pragma unroll 1
             for (unsigned t = 0; t < nt; t++) r = (t ? r * W.ccnt[blk][p.t[t].cls] : 0ull) + f_class_rank(W, idx[t]);
             if (r >= e.P->budget) return;
         }
@@ -524,7 +572,7 @@ template <class G, class C> CLF void f_match(const G &g, FW<C> &W, const FEnv &e
     if (g.rank == 0) { W.n_mt = 0; W.n_sel = 0; }
     /* blocks long enough for a candidate product above the budget (37^3 > 50 000): class counts */
     bool big = false;
-    GFOR(g, b, W.nb) if (b < W.nb) {
+    FFOR(g, b, W.nb) if (b < W.nb) {
         const uint32_t len = W.bo[b + 1] - W.bo[b];
         big |= (unsigned long long)len * len * (P.three[table] ? len : 1u) > P.budget;
     }
@@ -533,19 +581,38 @@ template <class G, class C> CLF void f_match(const G &g, FW<C> &W, const FEnv &e
     const uint16_t *o = W.ord[W.cur];
     const uint32_t n = W.n_pos;
     if (big) {
-        GFOR(g, k, W.nb * MAX_CLS) if (k < W.nb * MAX_CLS) (&W.ccnt[0][0])[k] = 0;
+        FFOR(g, k, W.nb * MAX_CLS) if (k < W.nb * MAX_CLS) (&W.ccnt[0][0])[k] = 0;
         g.sync();
-        GFOR(g, p, n) if (p < n) {
+        FFOR(g, p, n) if (p < n) {
             const uint32_t s = o[p], fl = W.sflag[s];
             if ((fl & SF_LIVE) && (fl >> SF_CLS_SHIFT) != SF_NOCLS) a_add(&W.ccnt[W.sblk[s]][fl >> SF_CLS_SHIFT], 1u);
         }
     }
+    /* the anchor records, sorted by seed class (counting sort: count, place), so that the lanes of a group
+     * work on the same pattern at the same time: one dense loop per pattern instead of one sparse,
+     * divergent sweep over the records (measured: 2.5 of 32 lanes active)                            */
+    uint16_t *list = W.outpos;                       /* free between rebuild and simplify */
+    FFOR(g, k, 2 * (MAX_CLS + 4)) if (k < 2 * (MAX_CLS + 4)) W.acnt[k] = 0;
     g.sync();
-    GFOR(g, p, n) if (p < n) {
-        const uint32_t s = o[p], fl = W.sflag[s];
-        if (!(fl & SF_LIVE) || (fl >> SF_CLS_SHIFT) == SF_NOCLS) continue;
-        uint32_t pm = P.anchor_mask[table][fl >> SF_CLS_SHIFT];
-        for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) f_try_anchor(W, e, s, pi);
+    FFOR(g, p, n) if (p < n) {
+        const uint32_t s = o[p], fl = W.sflag[s], c = fl >> SF_CLS_SHIFT;
+        if ((fl & SF_LIVE) && c != SF_NOCLS && P.anchor_mask[table][c]) a_add(&W.acnt[c], 1u);
+    }
+    g.sync();
+    uint32_t *fill = W.acnt + MAX_CLS + 4;
+    if (g.rank == 0) { uint32_t run = 0; for (unsigned c = 0; c < (unsigned)MAX_CLS; c++) { fill[c] = run; run += W.acnt[c]; } }
+    g.sync();
+    FFOR(g, p, n) if (p < n) {
+        const uint32_t s = o[p], fl = W.sflag[s], c = fl >> SF_CLS_SHIFT;
+        if ((fl & SF_LIVE) && c != SF_NOCLS && P.anchor_mask[table][c]) list[a_add(&fill[c], 1u)] = (uint16_t)s;
+    }
+    g.sync();
+#pragma unroll 1
+    for (unsigned pi = 0; pi < P.n_patterns; pi++) {
+        const FPat &p = P.p[pi];
+        if (p.table != table) continue;
+        const uint32_t ac = p.t[p.order[0]].cls, cnt = W.acnt[ac], lo = fill[ac] - cnt;
+        FFOR(g, k, cnt) if (k < cnt) f_try_anchor(W, e, list[lo + k], pi);
     }
     g.sync();
 }
@@ -561,12 +628,14 @@ template <class C> CLD unsigned long long f_key(const FW<C> &W, const FMatch &m)
 template <class G, class C> CLF void f_select(const G &g, FW<C> &W) {
     const uint32_t nm = f_rd(g, &W.n_mt);
     uint32_t nsel = 0;
+#pragma unroll 1
     for (;;) {
         unsigned long long best = NONE64;
         uint32_t bi = 0;
-        GFOR(g, m, nm) if (m < nm && W.mstate[m] == MS_UNDECIDED) {
+        FFOR(g, m, nm) if (m < nm && W.mstate[m] == MS_UNDECIDED) {
             const FMatch r = W.mt[m];
             bool clash = false;
+#pragma unroll 1
             for (unsigned t = 0; t < r.n; t++) clash |= (W.sflag[r.slot[t]] & SF_TAKEN) != 0;
             if (clash) { W.mstate[m] = MS_REJECTED; continue; }
             const unsigned long long key = f_key(W, r);
@@ -578,13 +647,14 @@ template <class G, class C> CLF void f_select(const G &g, FW<C> &W) {
             const FMatch r = W.mt[bi];
             W.mstate[bi] = MS_SELECTED;
             W.sel[nsel] = (uint16_t)bi;
+#pragma unroll 1
             for (unsigned t = 0; t < r.n; t++) W.sflag[r.slot[t]] |= SF_TAKEN;
             a_add(&W.fstat[16 + r.pat], 1u);
         }
         nsel++;
         g.sync();
     }
-    GFOR(g, j, nsel) if (j < nsel) { const FMatch r = W.mt[W.sel[j]]; for (unsigned t = 0; t < r.n; t++) W.sflag[r.slot[t]] &= (uint8_t)~SF_TAKEN; }
+    FFOR(g, j, nsel) if (j < nsel) { const FMatch r = W.mt[W.sel[j]]; for (unsigned t = 0; t < r.n; t++) W.sflag[r.slot[t]] &= (uint8_t)~SF_TAKEN; }
     if (g.rank == 0) W.n_sel = nsel;
     g.sync();
 }
@@ -597,28 +667,29 @@ template <class G, class C> CLF void f_emit_matches(const G &g, FW<C> &W, const 
     g.sync();
     if (!f_oks(g, W)) return;
     /* ccnt of every block that holds a match */
-    GFOR(g, k, W.nb * MAX_CLS) if (k < W.nb * MAX_CLS) (&W.ccnt[0][0])[k] = 0;
+    FFOR(g, k, W.nb * MAX_CLS) if (k < W.nb * MAX_CLS) (&W.ccnt[0][0])[k] = 0;
     g.sync();
     {
         const uint16_t *o = W.ord[W.cur];
-        GFOR(g, p, W.n_pos) if (p < W.n_pos) {
+        FFOR(g, p, W.n_pos) if (p < W.n_pos) {
             const uint32_t s = o[p], fl = W.sflag[s];
             if ((fl & SF_LIVE) && (fl >> SF_CLS_SHIFT) != SF_NOCLS) a_add(&W.ccnt[W.sblk[s]][fl >> SF_CLS_SHIFT], 1u);
         }
     }
     g.sync();
-    GFOR(g, m, nm) if (m < nm) {
+    FFOR(g, m, nm) if (m < nm) {
         const FMatch r = W.mt[m];
         const FPat &p = e.P->p[r.pat];
         const uint32_t b = W.sblk[r.slot[0]], lo = W.bo[b];
         unsigned long long rank = 0;
+#pragma unroll 1
         for (unsigned t = 0; t < r.n; t++) rank = (t ? rank * W.ccnt[b][p.t[t].cls] : 0ull) + f_class_rank(W, r.slot[t]);
         cl_event ev; ev.func = W.f; ev.seq = phase << 28 | b; ev.kind = CL_EV_MATCH; ev.idx = (uint32_t)r.pat << 20 | (uint32_t)rank;
         ev.a = r.pat; ev.b = W.posof[r.slot[0]] - lo; ev.c = r.n > 1 ? W.posof[r.slot[1]] - lo : NONE32; ev.d = r.n > 2 ? W.posof[r.slot[2]] - lo : NONE32;
         out[base + m] = ev;
     }
     /* selected matches: rank inside their block's select list */
-    GFOR(g, j, nsel) if (j < nsel) {
+    FFOR(g, j, nsel) if (j < nsel) {
         const FMatch r = W.mt[W.sel[j]];
         const uint32_t b = W.sblk[r.slot[0]], lo = W.bo[b];
         uint32_t jb = j;
@@ -637,48 +708,65 @@ template <class G, class C> CLF void f_emit_matches(const G &g, FW<C> &W, const 
  * straight from the function's counters; new records go to the arena tail and
  * become part of the stream only when the rewrite succeeds (a refused rewrite
  * keeps the ids, values and immediates it allocated: G4).                    */
+static constexpr uint16_t F_T_REL = 1u << 15;      /* slot payload is relative to the match's id bases (patched after the scan) */
+static constexpr int F_RW_IMMS = 6;                 /* immediates one rewrite may create */
 template <class C> struct FRW {
     FW<C> *W; const FEnv *e;
     uint32_t s[3]; cl_hdr h[3];
     unsigned n, pat;
     uint32_t ns[8], nins;          /* record slots of the plan's insert list */
+    uint32_t nv, ni, nq;           /* values / instruction ids / immediates allocated so far, relative to the match */
+    uint32_t tq[F_RW_IMMS];        /* staged immediates (FW::timm), creation order */
     uint32_t rm, retag, esc;       /* esc: bit 4t + k = def k of record t escapes (snapshot of the block's start) */
     uint32_t over;                 /* capacity of the slice exceeded: 1 values, 2 immediates, 4 def_iid log, 8 record slots */
 };
-/* a record slot: a freed one first, else the arena grows                      */
+/* a record slot: a freed one first, else the arena grows (any lane, any time between two frees) */
 template <class C> CLD uint32_t f_alloc_slot(FW<C> &W) {
-    if (W.n_free) return W.fre[--W.n_free];
+#if CL_DEV
+    const int old = atomicSub((int *)&W.n_free, 1);
+    if (old > 0) return W.fre[old - 1];
+    atomicAdd((int *)&W.n_free, 1);
+    const uint32_t s = atomicAdd(&W.n_slots, 1u);
+    if (s < C::I) return s;
+    atomicSub(&W.n_slots, 1u);
+    return F_NONE;
+#else
+    if ((int)W.n_free > 0) return W.fre[--W.n_free];
     if (W.n_slots < C::I) return W.n_slots++;
     return F_NONE;
+#endif
 }
 /* a removed record: its slot is free again, the values it defined have no defining record */
-template <class C> CLD void f_release(FW<C> &W, uint32_t s) {
-    const cl_hdr h = W.hdr[s];
-    f_value_defs(W, h, s, [&](uint32_t v) { if (v < C::V && W.defslot[v] == s) W.defslot[v] = F_NONE; });
+template <class C> CLD void f_free_slot(FW<C> &W, uint32_t s) {
     const uint32_t k = a_add(&W.n_free, 1u);
     if (k < C::I) W.fre[k] = (uint16_t)s;
 }
+template <class C> CLN void f_release(FW<C> &W, uint32_t s) {
+    const cl_hdr h = W.hdr[s];
+    f_value_defs(W, h, s, [&](uint32_t v) { if (v < C::V && W.defslot[v] == s) W.defslot[v] = F_NONE; });
+    f_free_slot(W, s);
+}
 template <class C> CLD opnd frw_value(FRW<C> &c) {                 /* LiftedFunction.new_value("pair") */
-    FW<C> &W = *c.W;
-    const uint32_t v = W.next_vid;
-    opnd o; o.tag = CL_K_VALUE; o.pay = v;
-    if (v < C::V) { W.next_vid = v + 1; W.alive[v] = 1; W.usecnt[v] = 0; W.defslot[v] = F_NONE; W.norigin[v] = 1u << 14; } else c.over |= 1u;
+    opnd o; o.tag = (uint16_t)(CL_K_VALUE | F_T_REL); o.pay = c.nv++;
     return o;
 }
 template <class C> CLD opnd frw_imm(FRW<C> &c, unsigned long long bits, unsigned long long text, bool hextext) {
     FW<C> &W = *c.W;
-    opnd o; o.tag = (uint16_t)(CL_K_IMM | (hextext ? CL_T_IMM_HEXTEXT : 0)); o.pay = W.nq_in + W.n_newimm;
-    if (W.n_newimm < C::Q) { W.newimm[W.n_newimm].bits = bits; W.newimm[W.n_newimm].text = text; W.n_newimm++; } else c.over |= 2u;
+    opnd o; o.tag = (uint16_t)(CL_K_IMM | F_T_REL | (hextext ? CL_T_IMM_HEXTEXT : 0)); o.pay = c.nq;
+    const uint32_t t = c.nq < (uint32_t)F_RW_IMMS ? a_add(&W.n_timm, 1u) : (uint32_t)C::TQ;
+    if (t < C::TQ) { W.timm[t].bits = bits; W.timm[t].text = text; c.tq[c.nq] = t; c.nq++; } else c.over |= 2u;
     return o;
 }
-template <class C> CLD void frw_set_def_iid(FRW<C> &c, uint32_t vid, uint32_t iid) {
-    FW<C> &W = *c.W;
-    if (W.n_log < C::L) { W.dlog[W.n_log].vid = vid; W.dlog[W.n_log].iid = (int32_t)iid; W.n_log++; } else c.over |= 4u;
+/* bits / spelling of an immediate operand, staged or already in the function's table */
+template <class C> CLD cl_imm frw_imm_of(const FRW<C> &c, opnd o) {
+    if (o.tag & F_T_REL) return c.W->timm[c.tq[o.pay < (uint32_t)F_RW_IMMS ? o.pay : 0]];
+    return f_imm_at(*c.W, *c.e, o.pay);
 }
-/* make_inst (ssir.py:237-241) + append to the plan's insert list; returns the iid */
+/* make_inst (ssir.py:237-241) + append to the plan's insert list; returns the (relative) iid.  The value the
+ * record defines gets def_iid = this iid (patterns.py:297,309,356,384...): the log entry is written at commit */
 template <class C> CLN uint32_t frw_emit(FRW<C> &c, uint16_t op, uint16_t modset, opnd def, const opnd *uses, unsigned nu) {
     FW<C> &W = *c.W;
-    const uint32_t iid = W.next_iid++;
+    const uint32_t iid = c.ni++;
     const uint32_t s = c.nins < 8 ? f_alloc_slot(W) : (uint32_t)F_NONE;
     if (s == F_NONE) { c.over |= 8u; return iid; }
     cl_hdr h;
@@ -686,6 +774,7 @@ template <class C> CLN uint32_t frw_emit(FRW<C> &c, uint16_t op, uint16_t modset
     W.hdr[s] = h;
     uint16_t *tg = &W.tag[s * 8]; uint32_t *py = &W.pay[s * 8];
     tg[0] = def.tag; py[0] = def.pay;
+#pragma unroll 1
     for (unsigned k = 0; k < 7; k++) { tg[1 + k] = k < nu ? uses[k].tag : (uint16_t)0; py[1 + k] = k < nu ? uses[k].pay : 0u; }
     W.sflag[s] = 0;
     c.ns[c.nins++] = s;
@@ -697,16 +786,23 @@ template <class C> CLD void frw_drop(FRW<C> &c, opnd o) { if (is_value(o) && o.p
  * for every def of every selected match of a block before the block's first
  * rewrite (f_escape_bits), so the rewrites can update the use counts as they go. */
 template <class C> CLN uint32_t f_escape_bits(const FW<C> &W, const FMatch &m) {
-    cl_hdr h[3];
-    for (unsigned t = 0; t < m.n; t++) h[t] = W.hdr[m.slot[t]];
+    FVals us[3];
+#pragma unroll 1
+    for (unsigned t = 0; t < 3; t++) { if (t < m.n) us[t] = f_uses(W, m.slot[t]); else us[t].n = 0; }
     uint32_t bits = 0;
+#pragma unroll 1
     for (unsigned t = 0; t < m.n; t++) {
-        const unsigned d0 = def0(h[t]), nd = (unsigned)h[t].n_defs + h[t].n_aux;
+        const cl_hdr h = W.hdr[m.slot[t]];
+        const unsigned d0 = def0(h), nd = (unsigned)h.n_defs + h.n_aux;
+#pragma unroll 1
         for (unsigned k = 0; k < nd && k < 4; k++) {
             const opnd d = f_slot(W, m.slot[t], d0 + k);
             if (!is_value(d) || d.pay >= C::V) continue;
             uint32_t inside = 0;
-            for (unsigned u = 0; u < m.n; u++) f_value_operands(W, h[u], m.slot[u], [&](uint32_t v) { inside += v == d.pay; });
+#pragma unroll 1
+            for (unsigned u = 0; u < m.n; u++)
+#pragma unroll 1
+                for (uint32_t q = 0; q < us[u].n && q < 8; q++) inside += f_val(us[u], q) == d.pay;
             if (W.usecnt[d.pay] != inside) bits |= 1u << (4 * t + k);
         }
     }
@@ -716,13 +812,16 @@ template <class C> CLD bool frw_escapes(const FRW<C> &c, unsigned t, unsigned k)
 /* _safe (patterns.py:266-275)                                                 */
 template <class C> CLN bool frw_safe(FRW<C> &c, const opnd *redef, unsigned nredef) {
     FW<C> &W = *c.W;
+#pragma unroll 1
     for (unsigned t = 0; t < c.n; t++) {
         const unsigned d0 = def0(c.h[t]), nd = (unsigned)c.h[t].n_defs + c.h[t].n_aux;
         if (nd > 4) { f_fail(W, F_REDO + 24); return false; }
+#pragma unroll 1
         for (unsigned k = 0; k < nd; k++) {
             const opnd d = f_slot(W, c.s[t], d0 + k);
             if (!is_value(d)) continue;
             bool re = false;
+#pragma unroll 1
             for (unsigned j = 0; j < nredef; j++) re |= is_value(redef[j]) && redef[j].pay == d.pay;
             if (!re && frw_escapes(c, t, k)) return false;
         }
@@ -752,26 +851,25 @@ template <class C> CLN opnd frw_pack_pair(FRW<C> &c, opnd lo, opnd hi) {
     u[0] = lo_zero ? frw_imm(c, 0, 0, true) : strip(lo);
     u[1] = hi_zero ? frw_imm(c, 0, 0, true) : strip(hi);
     const uint32_t iid = frw_emit(c, CL_OP_PACK64, CL_MS_NONE, d, u, 2);
-    frw_set_def_iid(c, d.pay, iid);
     return d;
 }
 /* _unpack_into (patterns.py:303-311)                                          */
 template <class C> CLN void frw_unpack_into(FRW<C> &c, opnd src, opnd lo_ref, opnd hi_ref) {
     FW<C> &W = *c.W;
     const opnd refs[2] = { lo_ref, hi_ref };
+#pragma unroll 1
     for (int k = 0; k < 2; k++) {
         if (!is_value(refs[k])) continue;
         const opnd d = value_ref(refs[k].pay);
         const uint32_t iid = frw_emit(c, CL_OP_UNPACK64, k ? CL_MS_HI : CL_MS_LO, d, &src, 1);
         if (!(d.pay < C::V && W.alive[d.pay])) { f_fail(W, F_REDO + 5); return; }        /* KeyError */
-        frw_set_def_iid(c, d.pay, iid);
-    }
+        }
 }
 /* fn.values[res.vid].def_iid = agg.iid                                        */
 template <class C> CLD bool frw_redefine(FRW<C> &c, opnd res, uint32_t iid) {
     FW<C> &W = *c.W;
     if (!is_value(res) || !(res.pay < C::V && W.alive[res.pay])) { f_fail(W, F_REDO + 6); return false; }   /* AttributeError / KeyError */
-    frw_set_def_iid(c, res.pay, iid);
+    (void)iid;
     return true;
 }
 template <class C> CLD opnd frw_use(const FRW<C> &c, unsigned t, unsigned k) { return f_slot(*c.W, c.s[t], use0(c.h[t]) + k); }
@@ -785,6 +883,7 @@ template <class C> CLN bool frw_iadd364(FRW<C> &c) {
     if (!frw_safe(c, redef, 2)) return false;
     opnd ops[3];
     unsigned nops = 0;
+#pragma unroll 1
     for (unsigned k = 0; k < 3; k++) {
         const opnd lo_op = frw_use(c, 0, k), hi_op = frw_use(c, 1, k);
         const bool neg_lo = o_neg(lo_op), not_hi = o_not(hi_op);
@@ -796,7 +895,7 @@ template <class C> CLN bool frw_iadd364(FRW<C> &c) {
             opnd p = frw_pack_pair(c, strip(lo_op), strip(hi_op));
             if (is_none(p)) return false;
             if (is_imm(p)) {                       /* Imm(-p.int_value(64) & M64, p.text) :348 */
-                const cl_imm im = f_imm_at(*c.W, *c.e, p.pay);
+                const cl_imm im = frw_imm_of(c, p);
                 ops[nops++] = frw_imm(c, 0ull - im.bits, im.text, (p.tag & CL_T_IMM_HEXTEXT) != 0);
             } else {
                 p.tag |= CL_T_NEG;
@@ -808,7 +907,6 @@ template <class C> CLN bool frw_iadd364(FRW<C> &c) {
     if (!nops) return false;
     const opnd d = frw_value(c);
     const uint32_t iid = frw_emit(c, CL_OP_IADD364, CL_MS_NONE, d, ops, nops);
-    frw_set_def_iid(c, d.pay, iid);
     frw_unpack_into(c, d, redef[0], redef[1]);
     frw_drop(c, carry);
     c.rm = 3;
@@ -847,7 +945,6 @@ template <class C> CLN bool frw_lea64(FRW<C> &c) {
     const opnd d = frw_value(c);
     const opnd u[3] = { b64, a64, frw_use(c, 0, 2) };
     const uint32_t iid = frw_emit(c, CL_OP_LEA64, CL_MS_NONE, d, u, 3);
-    frw_set_def_iid(c, d.pay, iid);
     frw_unpack_into(c, d, redef[0], redef[1]);
     frw_drop(c, carry);
     c.rm = 3;
@@ -857,6 +954,7 @@ template <class C> CLN bool frw_lea64(FRW<C> &c) {
  * pack always goes, a feeder only when its result does not escape (G8)        */
 template <class C> CLN bool frw_finish_pack(FRW<C> &c, unsigned n_feed) {
     c.rm = 1u << n_feed;
+#pragma unroll 1
     for (unsigned t = 0; t < n_feed; t++) {
         const opnd d = frw_def(c, t, 0);
         if (!is_value(d)) { f_fail(*c.W, F_REDO + 8); return false; }
@@ -924,7 +1022,9 @@ template <class C> CLN bool frw_xmad(FRW<C> &c) {
     if (!is_value(dres)) { f_fail(*c.W, F_REDO + 14); return false; }
     const uint32_t iid = frw_emit(c, CL_OP_IMAD, CL_MS_NONE, value_ref(dres.pay), u, 3);
     if (!frw_redefine(c, dres, iid)) return false;
+#pragma unroll 1
     for (unsigned t = 0; t < 2; t++)
+#pragma unroll 1
         for (unsigned k = 0; k < c.h[t].n_defs; k++) frw_drop(c, frw_def(c, t, k));
     c.rm = 7;
     return true;
@@ -945,26 +1045,45 @@ template <class C> CLN bool frw_run(FRW<C> &c) {
     return false;
 }
 
-/* one selected match: plan, then commit or refuse (lane 0).  The use counts
- * follow the edit at once; the escape tests of the block's other matches were
- * taken before (c.esc), which is the reference's per-block def-use snapshot
- * (patterns.py:674,706).                                                      */
-template <class C> CLF bool f_rewrite_one(FW<C> &W, const FEnv &e, unsigned table, uint32_t phase, const FMatch m, uint32_t esc, uint32_t rank_in_block) {
+/* The plan of one selected match becomes part of the function, or is refused:
+ * the ids it allocated relative to the match get their bases (exclusive scan
+ * over the matches of the batch in select order = the reference's allocation
+ * order, G3; a refused plan keeps its ids, values and immediates, G4).  The use
+ * counts follow the edit at once; the escape tests of the block's other matches
+ * were taken before (c.esc), which is the reference's per-block def-use snapshot
+ * (patterns.py:674,706).  Runs on many lanes at once, one match each.         */
+template <class C> CLF void f_commit(FW<C> &W, const FEnv &e, unsigned table, uint32_t phase, const FMatch m, FRW<C> &c, bool ok,
+                                     uint32_t vbase, uint32_t ibase, uint32_t qbase, uint32_t lbase, uint32_t rank_in_block) {
     const FProg &P = *e.P;
     const uint32_t b = W.sblk[m.slot[0]];
-    FRW<C> c;
-    c.W = &W; c.e = &e; c.n = m.n; c.pat = m.pat; c.nins = 0; c.rm = 0; c.retag = 0; c.over = 0; c.esc = esc;
-    for (unsigned t = 0; t < 3; t++) { c.s[t] = t < m.n ? m.slot[t] : (uint32_t)m.slot[0]; c.h[t] = W.hdr[c.s[t]]; }
-    const bool ok = frw_run(c);
-    if (c.over) { W.fail = F_REDO + 40 + c.over; return false; }
-    if (W.fail) return false;
-    if (!ok) {
-        for (uint32_t r = c.nins; r-- > 0;) W.fre[W.n_free++] = (uint16_t)c.ns[r];      /* the plan is dropped, its ids are not (G4) */
-        W.fstat[48 + m.pat]++;
-        f_event(W, phase << 28 | b, CL_EV_REFUSED, rank_in_block, m.pat, W.blk[b].bid, 0, 0);
-        return false;
+#pragma unroll 1
+    for (uint32_t k = 0; k < c.nv; k++) {
+        const uint32_t v = vbase + k;
+        W.alive[v] = 1; W.usecnt[v] = 0; W.defslot[v] = F_NONE; W.norigin[v] = 1u << 14;
     }
-    /* commit: removed records first (their values lose their defining record) */
+#pragma unroll 1
+    for (uint32_t k = 0; k < c.nq; k++) W.newimm[qbase - W.nq_in + k] = W.timm[c.tq[k]];
+#pragma unroll 1
+    for (uint32_t r = 0; r < c.nins; r++) {
+        const uint32_t s = c.ns[r];
+        const uint32_t iid = W.hdr[s].iid + ibase, ns = 1u + W.hdr[s].n_uses;
+        W.hdr[s].iid = iid;
+#pragma unroll 1
+        for (uint32_t k = 0; k < ns; k++) {
+            const uint16_t t = W.tag[s * 8 + k];
+            if (t & F_T_REL) { W.pay[s * 8 + k] += kind_of(t) == CL_K_VALUE ? vbase : qbase; W.tag[s * 8 + k] = (uint16_t)(t & ~F_T_REL); }
+        }
+        W.dlog[lbase + r].vid = W.pay[s * 8]; W.dlog[lbase + r].iid = (int32_t)iid;     /* value.def_iid = inst.iid */
+    }
+    if (!ok) {
+#pragma unroll 1
+        for (uint32_t r = 0; r < c.nins; r++) f_free_slot(W, c.ns[r]);          /* the plan is dropped, its ids are not (G4) */
+        a_add(&W.fstat[48 + m.pat], 1u);
+        f_event(W, phase << 28 | b, CL_EV_REFUSED, rank_in_block, m.pat, W.blk[b].bid, 0, 0);
+        return;
+    }
+    /* removed records first (their values lose their defining record) */
+#pragma unroll 1
     for (unsigned t = 0; t < m.n; t++) if (c.rm >> t & 1u) {
         const uint32_t s = m.slot[t];
         W.sflag[s] = 0;
@@ -972,6 +1091,7 @@ template <class C> CLF bool f_rewrite_one(FW<C> &W, const FEnv &e, unsigned tabl
         f_release(W, s);
     }
     const uint32_t anchor = m.slot[m.n - 1], ap = W.posof[anchor];
+#pragma unroll 1
     for (uint32_t r = 0; r < c.nins; r++) {
         const uint32_t s = c.ns[r];
         const cl_hdr h = W.hdr[s];
@@ -986,63 +1106,73 @@ template <class C> CLF bool f_rewrite_one(FW<C> &W, const FEnv &e, unsigned tabl
         f_value_operands(W, h, s, [&](uint32_t v) { f_inc_use(W, v); });
     }
     if (c.nins) { W.insslot[ap] = (uint16_t)c.ns[0]; W.inscnt[ap] = 1; }
-    /* a new pure record nobody reads is dead on arrival */
-    for (uint32_t r = 0; r < c.nins; r++) {
-        const uint32_t s = c.ns[r];
-        if (!(W.sflag[s] & SF_PURE)) continue;
-        const opnd d = f_slot(W, s, 0);
-        if (is_value(d) && d.pay < C::V && W.usecnt[d.pay] == 0) f_push_wl(W, s);
-    }
-    if (c.retag) {
+    if (c.retag) {                                  /* _rw_imad_wide :414-418 */
         cl_hdr &h = W.hdr[m.slot[0]];
         h.modset = e.ms[h.modset].minus_wide;
         h.op = CL_OP_IMAD64;
         W.sflag[m.slot[0]] = (uint8_t)((W.sflag[m.slot[0]] & 15u) | f_cls(P, table, CL_OP_IMAD64) << SF_CLS_SHIFT);
     }
     if (c.nins || c.rm) W.dirty = 1;
-    W.fstat[32 + m.pat]++;
-    return true;
+    a_add(&W.fstat[32 + m.pat], 1u);
 }
 
-/* _apply_patterns (patterns.py:671-707), the rewrite half: selected matches in
- * order, block by block; returns the number of successful rewrites           */
+/* _apply_patterns (patterns.py:671-707), the rewrite half: blocks in order; the
+ * selected matches of a block are planned side by side, one lane each; returns
+ * the number of successful rewrites                                           */
 template <class G, class C> CLF uint32_t f_rewrite(const G &g, FW<C> &W, const FEnv &e, unsigned table, uint32_t phase) {
     const uint32_t nsel = f_rd(g, &W.n_sel);
     if (g.rank == 0) W.ret = 0;
     uint32_t j0 = 0;
-    while (j0 < nsel) {
+    bool good = true;
+    while (j0 < nsel && good) {
         const uint32_t b = W.sblk[W.mt[W.sel[j0]].slot[0]];
         uint32_t j1 = j0 + 1;
         while (j1 < nsel && W.sblk[W.mt[W.sel[j1]].slot[0]] == b) j1++;
         g.sync();
-        GFOR(g, q, j1 - j0) if (q < j1 - j0) W.esc[j0 + q] = (uint16_t)f_escape_bits(W, W.mt[W.sel[j0 + q]]);
-        g.sync();
-        if (g.rank == 0) {
-            uint32_t total = 0;
-            for (uint32_t j = j0; j < j1 && W.fail == 0; j++) total += f_rewrite_one(W, e, table, phase, W.mt[W.sel[j]], W.esc[j], j - j0);
-            W.ret += total;
+        FFOR(g, q, j1 - j0) if (q < j1 - j0) W.esc[j0 + q] = (uint16_t)f_escape_bits(W, W.mt[W.sel[j0 + q]]);
+#pragma unroll 1
+        for (uint32_t c0 = j0; c0 < j1 && good; c0 += g.size) {
+            if (g.rank == 0) W.n_timm = 0;
+            g.sync();
+            const uint32_t nv0 = W.next_vid, ni0 = W.next_iid, nq0 = W.nq_in + W.n_newimm, nl0 = W.n_log;
+            const uint32_t j = c0 + g.rank;
+            const bool act = j < j1;
+            FRW<C> c;
+            c.W = &W; c.e = &e; c.n = 0; c.pat = 0; c.nins = 0; c.nv = 0; c.ni = 0; c.nq = 0; c.rm = 0; c.retag = 0; c.over = 0; c.esc = 0;
+            FMatch m; m.n = 0; m.pat = 0; m.slot[0] = m.slot[1] = m.slot[2] = 0;
+            bool ok = false;
+            if (act) {
+                m = W.mt[W.sel[j]];
+                c.n = m.n; c.pat = m.pat; c.esc = W.esc[j];
+#pragma unroll 1
+                for (unsigned t = 0; t < 3; t++) { c.s[t] = t < m.n ? m.slot[t] : (uint32_t)m.slot[0]; c.h[t] = W.hdr[c.s[t]]; }
+                ok = frw_run(c);
+                if (c.over) f_fail(W, F_REDO + 40 + c.over);
+            }
+            /* id bases: two packed scans (11 bits per count: at most 8 of each per match, 128 lanes) */
+            uint32_t t1, t2;
+            const uint32_t x1 = g.exscan(c.nv | c.ni << 11 | c.nq << 22, t1), x2 = g.exscan(c.nins | (ok ? 1u : 0u) << 11, t2);
+            const uint32_t vb = x1 & 0x7FFu, ib = (x1 >> 11) & 0x7FFu, qb = x1 >> 22, lb = x2 & 0x7FFu;
+            const uint32_t tv = t1 & 0x7FFu, ti = (t1 >> 11) & 0x7FFu, tq = t1 >> 22, tl = t2 & 0x7FFu, tok = t2 >> 11;
+            if (g.rank == 0 && (nv0 + tv > C::V || nq0 - W.nq_in + tq > C::Q || nl0 + tl > C::L)) f_fail(W, F_REDO + 45);
+            g.sync();
+            if (!f_oks(g, W)) { good = false; break; }
+            if (act) f_commit(W, e, table, phase, m, c, ok, nv0 + vb, ni0 + ib, nq0 + qb, nl0 + lb, j - j0);
+            g.sync();
+            if (g.rank == 0) { W.next_vid = nv0 + tv; W.next_iid = ni0 + ti; W.n_newimm = nq0 - W.nq_in + tq; W.n_log = nl0 + tl; W.ret += tok; }
+            /* a new pure record nobody reads is dead on arrival */
+            if (act && ok) for (uint32_t r = 0; r < c.nins; r++) {
+                const uint32_t s = c.ns[r];
+                if (!(W.sflag[s] & SF_PURE)) continue;
+                const opnd d = f_slot(W, s, 0);
+                if (is_value(d) && d.pay < C::V && W.usecnt[d.pay] == 0) f_push_wl(W, s);
+            }
+            g.sync();
         }
-        g.sync();
-        if (!f_oks(g, W)) break;
         j0 = j1;
     }
     g.sync();
     return f_rd(g, &W.ret);
-}
-
-/* one round of _apply_patterns: match + select every block, then rewrite     */
-template <class G, class C> CLF uint32_t f_apply(const G &g, FW<C> &W, const FEnv &e, unsigned table, uint32_t phase, cl_event *mev, uint32_t mev_cap) {
-    if (f_rd(g, &W.dirty)) { f_rebuild(g, W); f_prof(g, W, PF_MOVE); }
-    f_match(g, W, e, table);
-    f_prof(g, W, PF_MATCH);
-    if (!f_oks(g, W) || f_rd(g, &W.n_mt) == 0) return 0;
-    f_select(g, W);
-    f_prof(g, W, PF_SELECT);
-    if (mev) { f_emit_matches(g, W, e, phase, mev, mev_cap); if (!f_oks(g, W)) return 0; }
-    if (e.a->passes & CL_PASS_MATCH_ONLY) return 0;
-    const uint32_t r = f_rewrite(g, W, e, table, phase);
-    f_prof(g, W, PF_PLAN);
-    return r;
 }
 
 /* ------------------------------------------------------- dead pseudo ops */
@@ -1051,7 +1181,7 @@ template <class G, class C> CLF uint32_t f_apply(const G &g, FW<C> &W, const FEn
  * of "dead", reached here by chaotic iteration.  The first call looks at every
  * record; afterwards a record can only die when one of its values loses its
  * last user (or when it is inserted unused), and those are on the worklist.   */
-template <class C> CLD void f_try_kill(FW<C> &W, uint32_t s) {
+template <class C> CLN void f_try_kill(FW<C> &W, uint32_t s) {
     const uint32_t fl = W.sflag[s];
     if ((fl & (SF_LIVE | SF_PURE)) != (SF_LIVE | SF_PURE)) return;
     const cl_hdr h = W.hdr[s];
@@ -1076,20 +1206,21 @@ template <class G, class C> CLF void f_dce(const G &g, FW<C> &W) {
     g.sync();
     uint32_t head = 0;
     bool sweep = !(f_rd(g, &W.flags) & FF_SWEPT);
+#pragma unroll 1
     for (;;) {
         const uint32_t fl = f_rd(g, &W.flags), tl = f_rd(g, &W.wl_tail);
         if (sweep || (fl & FF_WLOVER)) {            /* first call, or the worklist lost entries: look at every record */
             if (g.rank == 0) { W.flags = (fl | FF_SWEPT) & ~(uint32_t)FF_WLOVER; W.wl_tail = 0; }
             g.sync();
             const uint32_t n = W.n_slots;
-            GFOR(g, s, n) if (s < n) f_try_kill(W, s);
+            FFOR(g, s, n) if (s < n) f_try_kill(W, s);
             g.sync();
             head = 0; sweep = false;
             continue;
         }
         const uint32_t tail = tl < C::I ? tl : C::I;
         if (head >= tail) break;
-        GFOR(g, k, tail - head) if (k < tail - head) f_try_kill(W, W.wl[head + k]);
+        FFOR(g, k, tail - head) if (k < tail - head) f_try_kill(W, W.wl[head + k]);
         head = tail;
         g.sync();
     }
@@ -1108,7 +1239,7 @@ template <class G, class C> CLF uint32_t f_simplify(const G &g, FW<C> &W, const 
     g.sync();
     const uint32_t n = W.n_slots;
     uint16_t *cand = W.outpos;                     /* (d, s) pairs; free between rebuilds */
-    GFOR(g, s, n) if (s < n) {
+    FFOR(g, s, n) if (s < n) {
         if (!f_live(W, s)) continue;
         const cl_hdr h = W.hdr[s];
         if (h.op != CL_OP_PACK64 || h.n_uses != 2) continue;
@@ -1135,9 +1266,9 @@ template <class G, class C> CLF uint32_t f_simplify(const G &g, FW<C> &W, const 
     const uint32_t changed = f_rd(g, &W.nred);
     if (!f_oks(g, W) || !changed) return changed;
     const uint32_t nv = W.next_vid;
-    GFOR(g, v, nv) if (v < nv) W.redirect[v] = F_NONE;
+    FFOR(g, v, nv) if (v < nv) W.redirect[v] = F_NONE;
     g.sync();
-    GFOR(g, k, changed) if (k < changed) W.redirect[cand[2 * k]] = cand[2 * k + 1];
+    FFOR(g, k, changed) if (k < changed) W.redirect[cand[2 * k]] = cand[2 * k + 1];
     g.sync();
     /* the use counts follow the redirects (every use site of the old value becomes one of the new) */
     auto move_use = [&](uint32_t v) {
@@ -1146,13 +1277,15 @@ template <class G, class C> CLF uint32_t f_simplify(const G &g, FW<C> &W, const 
         f_inc_use(W, fo);
         f_dec_use(W, v);
     };
-    GFOR(g, s, n) if (s < n && f_live(W, s)) f_value_operands(W, W.hdr[s], s, move_use);
-    GFOR(g, b, W.nb) if (b < W.nb)
+    FFOR(g, s, n) if (s < n && f_live(W, s)) f_value_operands(W, W.hdr[s], s, move_use);
+    FFOR(g, b, W.nb) if (b < W.nb)
+#pragma unroll 1
         for (int k = 0; k < 2; k++) if (kind_of(W.blk[b].term_tag[k]) == CL_K_VALUE) move_use(W.blk[b].term_pay[k]);
     g.sync();
-    GFOR(g, s, n) if (s < n && f_live(W, s)) {
+    FFOR(g, s, n) if (s < n && f_live(W, s)) {
         const cl_hdr h = W.hdr[s];
         const unsigned u0 = use0(h);
+#pragma unroll 1
         for (unsigned k = 0; k < h.n_uses; k++) {
             const opnd u = f_slot(W, s, u0 + k);
             if (is_value(u)) { if (u.pay < C::V && W.redirect[u.pay] != F_NONE) W.pay[s * 8 + u0 + k] = f_final_of(W, u.pay); }
@@ -1164,7 +1297,8 @@ template <class G, class C> CLF uint32_t f_simplify(const G &g, FW<C> &W, const 
         }
         if (has_guard(h)) { const opnd gd = f_slot(W, s, 0); if (is_value(gd)) W.pay[s * 8] = f_final_of(W, gd.pay); }
     }
-    GFOR(g, b, W.nb) if (b < W.nb)
+    FFOR(g, b, W.nb) if (b < W.nb)
+#pragma unroll 1
         for (int k = 0; k < 2; k++) if (kind_of(W.blk[b].term_tag[k]) == CL_K_VALUE) W.blk[b].term_pay[k] = f_final_of(W, W.blk[b].term_pay[k]);
     g.sync();
     f_dce(g, W);
@@ -1174,7 +1308,7 @@ template <class G, class C> CLF uint32_t f_simplify(const G &g, FW<C> &W, const 
 /* tag_cuda_objects (patterns.py:895-916)                                      */
 template <class G, class C> CLF void f_tag(const G &g, FW<C> &W, const FEnv &e) {
     const uint32_t n = W.n_slots;
-    GFOR(g, s, n) if (s < n && f_live(W, s)) {
+    FFOR(g, s, n) if (s < n && f_live(W, s)) {
         cl_hdr h = W.hdr[s];
         if (h.op != CL_OP_BAR && h.op != CL_OP_WARPSYNC && h.op != CL_OP_SHFL) continue;
         unsigned kind = 0, use = 7;
@@ -1182,9 +1316,11 @@ template <class G, class C> CLF void f_tag(const G &g, FW<C> &W, const FEnv &e) 
         if (h.op == CL_OP_BAR) {
             if ((e.ms[h.modset].mask >> CL_MB_SYNC) & 1u) {
                 kind = 1;
+#pragma unroll 1
                 for (unsigned k = 0; k < h.n_uses && k < 7; k++) if (is_imm(f_slot(W, s, u0 + k))) use = k;
             }
         } else if (h.op == CL_OP_WARPSYNC) {
+#pragma unroll 1
             for (unsigned k = 0; k < h.n_uses && k < 7; k++) {
                 const opnd u = f_slot(W, s, u0 + k);
                 if (is_imm(u)) { if (f_imm_at(W, e, u.pay).bits == 0xFFFFFFFFull) { kind = 2; use = k; } break; }
@@ -1221,10 +1357,10 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
     uint8_t *valbits = (uint8_t *)W.redirect;       /* [V]  per value (propagation)     */
     FChain *chain = (FChain *)W.mt;                 /* [M]                              */
     uint8_t *crank = W.mstate;                      /* [M]  rank of the chain           */
-    GFOR(g, v, nv) if (v < nv) valbits[v] = 0;
+    FFOR(g, v, nv) if (v < nv) valbits[v] = 0;
     if (g.rank == 0) W.n_mt = 0;
     /* R_0 and the MUFU.RCP records fed by an I2F */
-    GFOR(g, s, n) if (s < n) {
+    FFOR(g, s, n) if (s < n) {
         uint8_t fl = 0;
         if (f_live(W, s)) {
             const cl_hdr h = W.hdr[s];
@@ -1243,11 +1379,12 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
         rflag[s] = fl;
     }
     g.sync();
+#pragma unroll 1
     for (unsigned k = 1; k <= 3; k++) {
         const uint8_t prev = (uint8_t)(1u << (k - 1)), cur = (uint8_t)(1u << k);
-        GFOR(g, s, n) if (s < n && (rflag[s] & prev)) f_value_operands(W, W.hdr[s], s, [&](uint32_t v) { if (v < C::V) valbits[v] |= cur; });
+        FFOR(g, s, n) if (s < n && (rflag[s] & prev)) f_value_operands(W, W.hdr[s], s, [&](uint32_t v) { if (v < C::V) valbits[v] |= cur; });
         g.sync();
-        GFOR(g, s, n) if (s < n && f_live(W, s) && !(rflag[s] & cur)) {
+        FFOR(g, s, n) if (s < n && f_live(W, s) && !(rflag[s] & cur)) {
             bool r = false;
             f_value_defs(W, W.hdr[s], s, [&](uint32_t v) { r |= v < C::V && (valbits[v] & cur); });
             if (r) rflag[s] |= (uint8_t)((0xFu << k) & 0xFu);        /* R_k implies R_k+1.. */
@@ -1255,11 +1392,12 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
         g.sync();
     }
     /* accepted chains */
-    GFOR(g, s, n) if (s < n && f_live(W, s)) {
+    FFOR(g, s, n) if (s < n && f_live(W, s)) {
         const cl_hdr h = W.hdr[s];
         if (h.op != CL_OP_IADD && h.op != CL_OP_IADD3) continue;
         bool any_imm = false;
         const unsigned u0 = use0(h);
+#pragma unroll 1
         for (unsigned k = 0; k < h.n_uses; k++) any_imm |= is_imm(f_slot(W, s, u0 + k));
         if (!any_imm) continue;
         unsigned hits = 0;
@@ -1284,9 +1422,10 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
     if (!f_oks(g, W) || nc == 0) return;
     if (nc > 127) { if (g.rank == 0) f_fail(W, F_REDO + 34); g.sync(); return; }
     /* order of the chains = the reference's processing order */
-    GFOR(g, c, nc) if (c < nc) {
+    FFOR(g, c, nc) if (c < nc) {
         const uint32_t key = (uint32_t)W.posof[chain[c].mufu] << 16 | W.posof[chain[c].add];
         uint32_t r = 0;
+#pragma unroll 1
         for (uint32_t o = 0; o < nc; o++) r += ((uint32_t)W.posof[chain[o].mufu] << 16 | W.posof[chain[o].add]) < key;
         crank[c] = (uint8_t)r;
     }
@@ -1294,21 +1433,24 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
     uint16_t *own = W.insslot, *rch = W.wl;          /* per slot: own seed order, smallest order reached in one hop */
     uint16_t *vch = W.vtmp;                          /* per value: chain whose add defines it                       */
     uint32_t *qmin = &W.ccnt[0][0];                  /* per chain: smallest order reached in two hops                */
-    GFOR(g, s, n) if (s < n) { own[s] = F_NONE; rch[s] = F_NONE; }
-    GFOR(g, v, nv) if (v < nv) vch[v] = F_NONE;
-    GFOR(g, c, nc) if (c < nc) qmin[c] = NONE32;
+    FFOR(g, s, n) if (s < n) { own[s] = F_NONE; rch[s] = F_NONE; }
+    FFOR(g, v, nv) if (v < nv) vch[v] = F_NONE;
+    FFOR(g, c, nc) if (c < nc) qmin[c] = NONE32;
     g.sync();
-    GFOR(g, c, nc) if (c < nc) {
+    FFOR(g, c, nc) if (c < nc) {
         const FChain ch = chain[c];
         own[ch.add] = crank[c];
         bool first = true;                           /* the earliest chain of a MUFU names it */
+#pragma unroll 1
         for (uint32_t o = 0; o < nc; o++) first &= !(chain[o].mufu == ch.mufu && crank[o] < crank[c]);
         if (first) own[ch.mufu] = crank[c];
         f_value_defs(W, W.hdr[ch.add], ch.add, [&](uint32_t v) { if (v < C::V) vch[v] = (uint16_t)c; });
     }
     g.sync();
     if (g.rank == 0) {
+#pragma unroll 1
         for (uint32_t c = 0; c < nc; c++) {
+#pragma unroll 1
             for (int w = 0; w < 2; w++) {
                 const uint32_t u = w ? chain[c].mufu : chain[c].add;
                 const uint16_t key = own[u];
@@ -1320,13 +1462,13 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
         }
     }
     g.sync();
-    GFOR(g, s, n) if (s < n && f_live(W, s)) {
+    FFOR(g, s, n) if (s < n && f_live(W, s)) {
         const uint32_t key = own[s] < rch[s] ? own[s] : rch[s];
         if (key == F_NONE) continue;
         f_value_operands(W, W.hdr[s], s, [&](uint32_t v) { if (v < C::V && vch[v] != F_NONE) a_min32(&qmin[vch[v]], key); });
     }
     g.sync();
-    GFOR(g, c, nc) if (c < nc) {
+    FFOR(g, c, nc) if (c < nc) {
         const uint32_t q = qmin[c] < rch[chain[c].add] ? qmin[c] : rch[chain[c].add];
         if (q < crank[c]) f_fail(W, F_REDO + 35);
     }
@@ -1336,9 +1478,9 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
     const uint32_t a0 = W.n_slots, v0 = W.next_vid, i0 = W.next_iid, l0 = W.n_log, e0 = W.n_ev;
     if (a0 + 2 * nc > C::I || v0 + 2 * nc > C::V || l0 + 2 * nc > C::L || e0 + nc > C::E) { if (g.rank == 0) f_fail(W, F_REDO + 41); g.sync(); return; }
     uint16_t *vmap = W.redirect;                     /* add result -> its float view */
-    GFOR(g, v, nv) if (v < nv) vmap[v] = F_NONE;
+    FFOR(g, v, nv) if (v < nv) vmap[v] = F_NONE;
     g.sync();
-    GFOR(g, c, nc) if (c < nc) {
+    FFOR(g, c, nc) if (c < nc) {
         const FChain ch = chain[c];
         const uint32_t r = crank[c], vi = v0 + 2 * r, vf = vi + 1, iid = i0 + 2 * r, sa = a0 + 2 * r;
         const cl_hdr ah = W.hdr[ch.add];
@@ -1347,17 +1489,20 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
         W.dlog[l0 + 2 * r].vid = vi; W.dlog[l0 + 2 * r].iid = (int32_t)iid;
         W.dlog[l0 + 2 * r + 1].vid = vf; W.dlog[l0 + 2 * r + 1].iid = (int32_t)(iid + 1);
         const unsigned u0 = use0(ah);
+#pragma unroll 1
         for (unsigned k = 0; k < ah.n_uses; k++) {
             const opnd x = f_slot(W, ch.add, u0 + k);
             if (is_value(x) && x.pay == ch.rcp) W.pay[ch.add * 8 + u0 + k] = vi;
         }
         vmap[ch.addv] = (uint16_t)vf;
+#pragma unroll 1
         for (unsigned q = 0; q < 2; q++) {
             const uint32_t s = sa + q;
             cl_hdr h;
             h.iid = iid + q; h.op = CL_OP_BITCAST; h.modset = q ? CL_MS_I2F : CL_MS_F2I;
             h.n_defs = 1; h.n_aux = 0; h.n_uses = 1; h.flags = 0; h.ext = 0;
             W.hdr[s] = h;
+#pragma unroll 1
             for (unsigned k = 0; k < 8; k++) { W.tag[s * 8 + k] = k < 2 ? (uint16_t)CL_K_VALUE : (uint16_t)0; W.pay[s * 8 + k] = 0; }
             W.pay[s * 8] = vi + q; W.pay[s * 8 + 1] = q ? ch.addv : ch.rcp;
             W.sflag[s] = (uint8_t)(SF_LIVE | SF_PURE | SF_INS | f_cls(*e.P, 0, CL_OP_BITCAST) << SF_CLS_SHIFT);
@@ -1373,9 +1518,10 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
     }
     g.sync();
     /* every user of an add result (top-level uses only :878-883) reads the float view */
-    GFOR(g, s, a0) if (s < a0 && f_live(W, s)) {
+    FFOR(g, s, a0) if (s < a0 && f_live(W, s)) {
         const cl_hdr h = W.hdr[s];
         const unsigned u0 = use0(h);
+#pragma unroll 1
         for (unsigned k = 0; k < h.n_uses; k++) {
             const opnd x = f_slot(W, s, u0 + k);
             if (is_value(x) && x.pay < nv && vmap[x.pay] != F_NONE) {
@@ -1390,6 +1536,7 @@ template <class G, class C> CLF void f_reciprocal(const G &g, FW<C> &W, const FE
     if (g.rank == 0) {
         W.n_slots = a0 + 2 * nc; W.next_vid = v0 + 2 * nc; W.next_iid = i0 + 2 * nc; W.n_log = l0 + 2 * nc; W.n_ev = e0 + nc; W.dirty = 1;
         /* a float view nobody reads is dead on arrival (removed by the next remove_dead_pseudo) */
+#pragma unroll 1
         for (uint32_t c = 0; c < nc; c++) if (W.usecnt[v0 + 2 * c + 1] == 0) f_push_wl(W, a0 + 2 * c + 1);
     }
     g.sync();
@@ -1425,107 +1572,80 @@ template <class G, class C> CLF void f_store(const G &g, FW<C> &W, const FEnv &e
         a.o_func[f] = o;
     }
     const uint32_t b0 = W.b0, nb = W.nb;
-    GFOR(g, b, nb) if (b < nb) {
+    FFOR(g, b, nb) if (b < nb) {
         a.o_blk[b0 + b] = W.blk[b];
         a.o_blk_start[b0 + b] = fits ? r_inst + W.bo[b] : 0u;
         a.o_blk_cnt[b0 + b] = fits ? (uint32_t)(W.bo[b + 1] - W.bo[b]) : 0u;
     }
-    GFOR(g, m, W.n_mem) if (m < W.n_mem) a.o_mem[W.m0 + m] = W.mem[m];
+    FFOR(g, m, W.n_mem) if (m < W.n_mem) a.o_mem[W.m0 + m] = W.mem[m];
     if (!fits) return;
     {
         const uint16_t *o = W.ord[W.cur];
         uint4 *dh = (uint4 *)(a.o_hdr + r_inst), *dt = (uint4 *)(a.o_tag + (size_t)r_inst * 8), *dp = (uint4 *)(a.o_pay + (size_t)r_inst * 8);
         const uint4 *sh = (const uint4 *)W.hdr, *st = (const uint4 *)W.tag, *sp = (const uint4 *)W.pay;
-        GFOR(g, p, n) if (p < n) { const uint32_t s = o[p]; dh[p] = sh[s]; dt[p] = st[s]; }
-        GFOR(g, q, 2 * n) if (q < 2 * n) { const uint32_t s = o[q >> 1]; dp[q] = sp[2 * s + (q & 1u)]; }
+        FFOR(g, p, n) if (p < n) { const uint32_t s = o[p]; dh[p] = sh[s]; dt[p] = st[s]; }
+        FFOR(g, q, 2 * n) if (q < 2 * n) { const uint32_t s = o[q >> 1]; dp[q] = sp[2 * s + (q & 1u)]; }
     }
     {
         const cl_imm *src = a.in.imm + W.q0;
-        GFOR(g, q, nq) if (q < nq) a.o_imm[r_imm + q] = q < W.nq_in ? src[q] : W.newimm[q - W.nq_in];
+        FFOR(g, q, nq) if (q < nq) a.o_imm[r_imm + q] = q < W.nq_in ? src[q] : W.newimm[q - W.nq_in];
     }
     {
         const int32_t *sd = a.in.val_def_iid + W.v0;
-        GFOR(g, v, nv) if (v < nv) {
+        FFOR(g, v, nv) if (v < nv) {
             a.o_alive[r_val + v] = W.alive[v];
             a.o_def_iid[r_val + v] = v < W.nv_in ? sd[v] : -1;
             a.o_origin[r_val + v] = v < W.nv_in ? (uint32_t)CL_ORG_HOST : f_origin(W.norigin[v]);
         }
     }
-    GFOR(g, k, W.n_ev) if (k < W.n_ev) a.o_ev[r_ev + k] = W.ev[k];
-    GFOR(g, k, n_mev) if (k < n_mev) a.o_ev[r_ev + W.n_ev + k] = mev[k];
+    FFOR(g, k, W.n_ev) if (k < W.n_ev) a.o_ev[r_ev + k] = W.ev[k];
+    FFOR(g, k, n_mev) if (k < n_mev) a.o_ev[r_ev + W.n_ev + k] = mev[k];
     g.sync();
     /* def_iid updates in program order (a value redefined twice keeps the last) */
     if (g.rank == 0) for (uint32_t k = 0; k < W.n_log; k++) a.o_def_iid[r_val + W.dlog[k].vid] = W.dlog[k].iid;
 }
 
-/* --------------------------------------------------------------- one function */
-enum { FR_DONE = 0, FR_NOFIT = 1, FR_REDO = 2 };
-template <class G, class C> CLF int f_run_function(const G &g, FW<C> &W, FEnv &e, uint32_t f, cl_event *mev, uint32_t mev_cap) {
-    const KArgs &a = *e.a;
-    f_prof(g, W, PF_SETUP);
-    if (!f_load(g, W, e, f)) return FR_NOFIT;
-    f_prof(g, W, PF_LOAD);
-    const bool xm = (a.passes & CL_PASS_XMAD) && W.arch == CL_ARCH_SM52;
-    const bool match_only = (a.passes & CL_PASS_MATCH_ONLY) != 0;
-    const unsigned table = match_only ? ((a.passes & CL_PASS_MATCH_XMAD) ? 1u : 0u) : (xm ? 1u : 0u);
-    const bool emit = a.emit_matches || match_only;
-    if (g.rank == 0 && emit && !mev) f_fail(W, F_REDO + 23);
-    g.sync();
-    if (f_oks(g, W)) f_index(g, W, e, table);
-    f_prof(g, W, PF_USECOUNT);
-    cl_event *mv = emit ? mev : nullptr;
-    if (match_only) {
-        if (f_oks(g, W)) f_apply(g, W, e, table, 0, mv, mev_cap);
-    } else {
-        if (xm && f_oks(g, W)) {
-            f_apply(g, W, e, 1, 0, mv, mev_cap);
-            if (f_oks(g, W)) f_dce(g, W);
-            f_prof(g, W, PF_DCE);
-            if ((a.passes & (CL_PASS_AGGREGATE | CL_PASS_RECIPROCAL)) && f_oks(g, W)) f_reclass(g, W, e, 0);
-            f_prof(g, W, PF_SEED);
-        }
-        if ((a.passes & CL_PASS_RECIPROCAL) && (f_rd(g, &W.flags) & FF_RCP) && f_oks(g, W)) {
-            if (f_rd(g, &W.dirty)) f_rebuild(g, W);
-            f_reciprocal(g, W, e);
-            f_prof(g, W, PF_RECIP);
-        }
-        if ((a.passes & CL_PASS_AGGREGATE) && f_oks(g, W)) {
-            for (uint32_t round = 0; round < a.max_rounds; round++) {
-                uint32_t n = f_apply(g, W, e, 0, 2 + round, mv, mev_cap);
-                if (!f_oks(g, W)) break;
-                n += f_simplify(g, W, e);
-                f_prof(g, W, PF_SIMPLIFY);
-                if (!f_oks(g, W) || !n) break;
-            }
-            if (f_oks(g, W)) f_dce(g, W);
-            f_prof(g, W, PF_DCE);
-        }
-        if ((a.passes & CL_PASS_TAG) && f_oks(g, W)) f_tag(g, W, e);
-        f_prof(g, W, PF_TAG);
-    }
-    g.sync();
-    if (!f_oks(g, W)) return FR_REDO;
-    if (f_rd(g, &W.dirty)) f_rebuild(g, W);
-    f_prof(g, W, PF_MOVE);
-    f_store(g, W, e, mv);
-    f_prof(g, W, PF_STORE);
-    return FR_DONE;
+/* ------------------------------------------------------------ the CTA's loop */
+/* CTA-wide barrier / vote between the phases (all groups of the CTA)         */
+CLD void f_cta_sync() {
+#if CL_DEV
+    __syncthreads();
+#endif
+}
+CLD bool f_cta_or(bool x) {
+#if CL_DEV
+    return __syncthreads_or(x) != 0;
+#else
+    return x;
+#endif
 }
 
-/* persistent loop of one group over the functions of its size class; what does
- * not fit goes to the next class's list, hand-backs to the general kernel      */
 template <class C> CLHD size_t f_scratch_bytes(uint32_t mev_cap) { return (size_t)(C::E + mev_cap) * sizeof(cl_event) + (size_t)C::L * sizeof(FDLog); }
 struct FLoop {
-    const uint32_t *list; const uint32_t *n_list_ptr; uint32_t n_list;     /* list == null: functions [0, n_list) */
+    /* work of this class: entries [bounds[0], bounds[1]) of the size-sorted function list (device side counting
+     * sort, fused.cu), then what the class before could not take (list2, n_list2 on the device)              */
+    const uint32_t *list; const uint32_t *bounds;
+    const uint32_t *list2; const uint32_t *n_list2_ptr;
     uint32_t *counter;
     uint32_t *next_list, *next_count;       /* functions too large for this class (null: retry lists)           */
     uint8_t *scr; uint32_t mev_cap;         /* per group global scratch: C::E events of the function, mev_cap match events (emit_matches), C::L def_iid updates */
 };
+
+/* Persistent loop of the groups of one CTA over the functions of their size
+ * class.  The groups take one function each and walk through the passes in
+ * LOCK STEP (a CTA barrier between two phases): the stage is a few hundred KB
+ * of code, far beyond the instruction cache, and warps that each sit in a
+ * different phase of a different function spend their time on instruction
+ * fetch misses (measured: 2 M cycles per function free-running).  In lock
+ * step an SM runs one phase's code at a time for all its resident functions.
+ * What does not fit the class goes to the next class's list, hand-backs to the
+ * general kernel.                                                            */
 template <class G, class C> CLF void f_loop(const G &g, FW<C> &W, FEnv &e, const FLoop &L, uint32_t group) {
     const KArgs &a = *e.a;
-    const uint32_t n_list = L.n_list_ptr ? *L.n_list_ptr : L.n_list;
+    const uint32_t lo1 = L.bounds[0], n1 = L.bounds[1] - lo1, n2 = L.n_list2_ptr ? *L.n_list2_ptr : 0u, n_list = n1 + n2;
     unsigned long long n_in = 0, n_out = 0, n_ev = 0;
     if (g.rank == 0) {
+#pragma unroll 1
         for (int k = 0; k < PF__N; k++) W.prof[k] = 0;
         W.prof_t = now();
         uint8_t *scr = L.scr + (size_t)group * f_scratch_bytes<C>(L.mev_cap);
@@ -1534,40 +1654,139 @@ template <class G, class C> CLF void f_loop(const G &g, FW<C> &W, FEnv &e, const
     }
     g.sync();
     cl_event *mev = L.mev_cap ? W.ev + C::E : nullptr;
+    const bool match_only = (a.passes & CL_PASS_MATCH_ONLY) != 0;
+    const bool emit = a.emit_matches || match_only;
+    cl_event *mv = emit ? mev : nullptr;
+#pragma unroll 1
     for (;;) {
+        /* ---- take a function, load it */
         g.sync();
         if (g.rank == 0) W.work = a_add(L.counter, 1u);
         g.sync();
         const uint32_t w = f_rd(g, &W.work);
-        if (w >= n_list) break;
-        const uint32_t f = L.list ? L.list[w] : w;
-        const int r = f_run_function(g, W, e, f, mev, L.mev_cap);
-        if (r == FR_DONE) {
+        const bool have = w < n_list;
+        if (!f_cta_or(have)) break;
+        const uint32_t f = have ? (w < n1 ? L.list[lo1 + w] : L.list2[w - n1]) : 0u;
+        f_prof(g, W, PF_SETUP);
+        bool fit = have && f_load(g, W, e, f);
+        f_prof(g, W, PF_LOAD);
+        const bool xm = fit && (a.passes & CL_PASS_XMAD) && W.arch == CL_ARCH_SM52;
+        const unsigned table = match_only ? ((a.passes & CL_PASS_MATCH_XMAD) ? 1u : 0u) : (xm ? 1u : 0u);
+        if (fit && g.rank == 0 && emit && !mev) f_fail(W, F_REDO + 23);
+        g.sync();
+        /* `on`: this group still works on its function */
+#define F_ON (fit && f_oks(g, W))
+        f_cta_sync();
+        if (F_ON) f_index(g, W, e, table);
+        f_prof(g, W, PF_USECOUNT);
+        f_cta_sync();
+        if (match_only) {
+            /* match_patterns + select_matches only */
+            if (F_ON) f_match(g, W, e, table);
+            f_cta_sync();
+            if (F_ON && f_rd(g, &W.n_mt)) { f_select(g, W); f_emit_matches(g, W, e, 0, mv, L.mev_cap); }
+            f_cta_sync();
+        } else {
+            /* ---- normalize_xmad (patterns.py:805-810) */
+            if (f_cta_or(xm)) {
+                uint32_t nm = 0;
+                if (xm && F_ON) { f_match(g, W, e, 1); nm = f_rd(g, &W.n_mt); }
+                f_prof(g, W, PF_MATCH);
+                f_cta_sync();
+                if (xm && nm && F_ON) f_select(g, W);
+                f_prof(g, W, PF_SELECT);
+                f_cta_sync();
+                if (xm && nm && mv && F_ON) f_emit_matches(g, W, e, 0, mv, L.mev_cap);
+                if (xm && nm && F_ON) f_rewrite(g, W, e, 1, 0);
+                f_prof(g, W, PF_PLAN);
+                f_cta_sync();
+                if (xm && F_ON) f_dce(g, W);
+                if (xm && (a.passes & (CL_PASS_AGGREGATE | CL_PASS_RECIPROCAL)) && F_ON) f_reclass(g, W, e, 0);
+                f_prof(g, W, PF_DCE);
+                f_cta_sync();
+            }
+            /* ---- normalize_reciprocal (patterns.py:817-847) */
+            {
+                const bool rc = fit && (a.passes & CL_PASS_RECIPROCAL) && (f_rd(g, &W.flags) & FF_RCP);
+                if (f_cta_or(rc)) {
+                    if (rc && F_ON) {
+                        if (f_rd(g, &W.dirty)) f_rebuild(g, W);
+                        f_reciprocal(g, W, e);
+                    }
+                    f_prof(g, W, PF_RECIP);
+                    f_cta_sync();
+                }
+            }
+            /* ---- apply_aggregations (patterns.py:794-802) */
+            if (a.passes & CL_PASS_AGGREGATE) {
+                bool more = fit;
+#pragma unroll 1
+                for (uint32_t round = 0; round < a.max_rounds; round++) {
+                    if (!f_cta_or(more)) break;
+                    uint32_t nm = 0, n = 0;
+                    if (more && F_ON) {
+                        if (f_rd(g, &W.dirty)) f_rebuild(g, W);
+                        f_prof(g, W, PF_MOVE);
+                        f_match(g, W, e, 0);
+                        nm = f_rd(g, &W.n_mt);
+                    }
+                    f_prof(g, W, PF_MATCH);
+                    f_cta_sync();
+                    if (more && nm && F_ON) f_select(g, W);
+                    f_prof(g, W, PF_SELECT);
+                    f_cta_sync();
+                    if (more && nm && mv && F_ON) f_emit_matches(g, W, e, 2 + round, mv, L.mev_cap);
+                    if (more && nm && F_ON) n = f_rewrite(g, W, e, 0, 2 + round);
+                    f_prof(g, W, PF_PLAN);
+                    f_cta_sync();
+                    if (more && F_ON) n += f_simplify(g, W, e);
+                    f_prof(g, W, PF_SIMPLIFY);
+                    f_cta_sync();
+                    if (!n) more = false;
+                }
+                if (F_ON) f_dce(g, W);
+                f_prof(g, W, PF_DCE);
+                f_cta_sync();
+            }
+            if ((a.passes & CL_PASS_TAG) && F_ON) f_tag(g, W, e);
+            f_prof(g, W, PF_TAG);
+        }
+        /* ---- store, or route the function elsewhere */
+        g.sync();
+        const bool done = F_ON;
+#undef F_ON
+        if (done) {
+            if (f_rd(g, &W.dirty)) f_rebuild(g, W);
+            f_prof(g, W, PF_MOVE);
+            f_store(g, W, e, mv);
+            f_prof(g, W, PF_STORE);
+            g.sync();
+            FFOR(g, k, 64) if (k < 64 && W.fstat[k]) a_add64(&a.stats[k], W.fstat[k]);
+            if (g.rank == 0) { n_in += W.n_in; n_out += W.n_pos; n_ev += W.n_ev + (mv ? W.n_mev : 0u); }
 #if !CL_DEV
             if (getenv("CL_FUSED_STATS")) fprintf(stderr, "fused done: n_in %u slots %u out %u nv_in %u nv %u newimm %u log %u ev %u\n", W.n_in, W.n_slots, W.n_pos, W.nv_in, W.next_vid, W.n_newimm, W.n_log, W.n_ev);
 #endif
-            g.sync();
-            GFOR(g, k, 64) if (k < 64 && W.fstat[k]) a_add64(&a.stats[k], W.fstat[k]);
-            if (g.rank == 0) { n_in += W.n_in; n_out += W.n_pos; n_ev += W.n_ev + (mev ? W.n_mev : 0u); }
-            continue;
-        }
+        } else if (have) {
 #if !CL_DEV
-        if (r == FR_REDO && getenv("CL_FUSED_DEBUG")) fprintf(stderr, "fused hand-back: function %u (%u records) reason %u\n", f, W.n_in, W.fail);
+            if (fit && getenv("CL_FUSED_DEBUG")) fprintf(stderr, "fused hand-back: function %u (%u records) reason %u\n", f, W.n_in, W.fail);
 #endif
-        if (g.rank == 0) {
-            /* too large for this class, or outgrew its slice while running: the next class has more room */
-            if ((r == FR_NOFIT || (W.fail > F_REDO + 40 && W.fail < F_REDO + 60)) && L.next_list) L.next_list[a_add(L.next_count, 1u)] = f;
-            else {
-                const cl_corpus &in = a.in;
-                const uint32_t n = in.blk_off[in.func_blk_off[f + 1]] - in.blk_off[in.func_blk_off[f]];
-                if (n > a.small_max) a.retry_big_list[a_add(a.retry_big_count, 1u)] = f;
-                else a.retry_list[a_add(a.retry_count, 1u)] = f;
+            if (g.rank == 0) {
+                /* too large for this class, or outgrew its slice while running: the next class has more room */
+                if ((!fit || (W.fail > F_REDO + 40 && W.fail < F_REDO + 60)) && L.next_list) L.next_list[a_add(L.next_count, 1u)] = f;
+                else {
+                    const cl_corpus &in = a.in;
+                    const uint32_t n = in.blk_off[in.func_blk_off[f + 1]] - in.blk_off[in.func_blk_off[f]];
+                    if (n > a.small_max) a.retry_big_list[a_add(a.retry_big_count, 1u)] = f;
+                    else a.retry_list[a_add(a.retry_count, 1u)] = f;
+                }
             }
         }
+        f_cta_sync();
     }
     if (g.rank == 0) {
         a_add64(&a.stats[64], n_in); a_add64(&a.stats[65], n_out); a_add64(&a.stats[66], n_ev);
         unsigned long long tot = 0;
+#pragma unroll 1
         for (int k = 1; k < PF__N; k++) { tot += W.prof[k]; if (W.prof[k]) a_add64(&a.prof[k], W.prof[k]); }
         a_add64(&a.prof[PF_TOTAL], tot);
     }
