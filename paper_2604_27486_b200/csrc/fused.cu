@@ -143,11 +143,11 @@ static bool fprog_build(const cl_pattern_blob &pb, FProg &P, char *why, size_t w
 
 /* ------------------------------------------------------------------ kernels */
 constexpr size_t F_SMEM_MAX = 232448;      /* 227 KB: the most dynamic shared memory a CTA can opt in to on sm_100 */
-CLHD constexpr size_t f_prog_bytes() { return (sizeof(FProg) + sizeof(KArgs) + 15) & ~(size_t)15; }
+CLHD constexpr size_t f_prog_bytes() { return (sizeof(FProg) + sizeof(KArgs) + sizeof(FCta) + 15) & ~(size_t)15; }
 template <class C> CLHD constexpr size_t f_slice_bytes() { return (sizeof(FW<C>) + 15) & ~(size_t)15; }
 
 #if CLF_CUDA
-template <class C, int NW, int NG> __global__ void __launch_bounds__(NW *NG * 32, 1) k_fused(KArgs a, const FProg *gp, FLoop L) {
+template <class C, int NW, int NG, int MINB> __global__ void __launch_bounds__(NW *NG * 32, MINB) k_fused(KArgs a, const FProg *gp, FLoop L) {
     extern __shared__ uint4 dyn_smem[];
     FProg &P = *(FProg *)dyn_smem;
     KArgs &A = *(KArgs *)((uint8_t *)dyn_smem + sizeof(FProg));
@@ -161,10 +161,13 @@ template <class C, int NW, int NG> __global__ void __launch_bounds__(NW *NG * 32
     }
     __syncthreads();
     const uint32_t grp = threadIdx.x / (NW * 32);
+    static_assert(NG <= F_MAXG, "groups per CTA");
     FW<C> &W = *(FW<C> *)((uint8_t *)dyn_smem + f_prog_bytes() + (size_t)grp * f_slice_bytes<C>());
     FG<NW> g; g.rank = threadIdx.x % (NW * 32); g.size = NW * 32; g.bar = 1 + grp; g.red = W.gred;
-    FEnv e; e.P = &P; e.a = &A; e.ms = A.in.modsets; e.imm_in = nullptr;
-    f_loop(g, W, e, L, blockIdx.x * NG + grp);
+    FEnv e; e.P = &P; e.a = &A; e.ms = A.in.modsets;
+    FCtx<C> x; x.Q = (FCta *)((uint8_t *)dyn_smem + sizeof(FProg) + sizeof(KArgs)); x.w0 = (uint8_t *)dyn_smem + f_prog_bytes(); x.stride = (uint32_t)f_slice_bytes<C>();
+    x.ng = NG; x.gi = grp; x.tid = threadIdx.x; x.nthreads = NW * NG * 32;
+    f_loop(g, W, e, x, L, blockIdx.x * NG + grp);
 }
 __global__ void k_fused_zero(uint32_t *p, uint32_t n) { for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = 0; }
 #endif
@@ -277,25 +280,29 @@ void clf_info(const clf_ctx *c, unsigned long long out[4]) {
 }
 
 #if CLF_CUDA
-template <class C, int NW, int NG> static int f_launch(clf_ctx *c, const KArgs &k, const FLoop &L, uint32_t grid, cudaStream_t st, char *err, size_t errlen) {
+template <class C, int NW, int NG, int MINB> static int f_launch(clf_ctx *c, const KArgs &k, const FLoop &L, uint32_t grid, cudaStream_t st, char *err, size_t errlen) {
     constexpr size_t smem = f_prog_bytes() + (size_t)NG * f_slice_bytes<C>();
-    static_assert(smem <= F_SMEM_MAX, "the groups of a CTA do not fit the SM's shared memory");
-    F_CUDA_OK(cudaFuncSetAttribute(k_fused<C, NW, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_fused<C, NW, NG><<<grid, NW * NG * 32, smem, st>>>(k, c->d_prog, L);
+    static_assert((smem + 1024) * MINB <= F_SMEM_MAX + 1024, "the groups of the resident CTAs do not fit the SM's shared memory");
+    F_CUDA_OK(cudaFuncSetAttribute(k_fused<C, NW, NG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_fused<C, NW, NG, MINB><<<grid * MINB, NW * NG * 32, smem, st>>>(k, c->d_prog, L);
     F_CUDA_OK(cudaGetLastError());
     c->launches++;
     return 0;
 }
 #endif
 
+/* groups per CTA and CTAs per SM of each class */
 #ifndef CLF_GROUPS_S
 #define CLF_GROUPS_S 13
+#define CLF_CTAS_S 1
 #endif
 #ifndef CLF_GROUPS_L
 #define CLF_GROUPS_L 7
+#define CLF_CTAS_L 1
 #endif
 #ifndef CLF_GROUPS_X
 #define CLF_GROUPS_X 3
+#define CLF_CTAS_X 1
 #endif
 
 int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, size_t errlen) {
@@ -310,7 +317,7 @@ int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, si
         c->list_cap = want;
     }
     const bool emit = k.emit_matches || (k.passes & CL_PASS_MATCH_ONLY);
-    const uint32_t groups[3] = { (uint32_t)c->n_sm * CLF_GROUPS_S, (uint32_t)c->n_sm * CLF_GROUPS_L, (uint32_t)c->n_sm * CLF_GROUPS_X };
+    const uint32_t groups[3] = { (uint32_t)c->n_sm * CLF_GROUPS_S * CLF_CTAS_S, (uint32_t)c->n_sm * CLF_GROUPS_L * CLF_CTAS_L, (uint32_t)c->n_sm * CLF_GROUPS_X * CLF_CTAS_X };
     const uint32_t mcap[3] = { emit ? 12 * FCfgS::M : 0u, emit ? 12 * FCfgL::M : 0u, emit ? 12 * FCfgX::M : 0u };
     {
         size_t need = 0;
@@ -346,9 +353,9 @@ int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, si
     k_fsort_scatter<<<sgrid, 256, 0, st>>>(k, F, c->d_words + FC_HIST, c->d_list[2]);
     F_CUDA_OK(cudaGetLastError());
     c->launches += 4;
-    if (f_launch<FCfgS, 1, CLF_GROUPS_S>(c, k, L[0], grid, st, err, errlen)) return -1;
-    if (f_launch<FCfgL, 2, CLF_GROUPS_L>(c, k, L[1], grid, st, err, errlen)) return -1;
-    if (f_launch<FCfgX, 4, CLF_GROUPS_X>(c, k, L[2], grid, st, err, errlen)) return -1;
+    if (f_launch<FCfgS, 1, CLF_GROUPS_S, CLF_CTAS_S>(c, k, L[0], grid, st, err, errlen)) return -1;
+    if (f_launch<FCfgL, 2, CLF_GROUPS_L, CLF_CTAS_L>(c, k, L[1], grid, st, err, errlen)) return -1;
+    if (f_launch<FCfgX, 4, CLF_GROUPS_X, CLF_CTAS_X>(c, k, L[2], grid, st, err, errlen)) return -1;
 #else
     (void)stream;
     memset(c->d_words, 0, sizeof(uint32_t) * FC__N);
@@ -367,11 +374,12 @@ int clf_run(clf_ctx *c, const KArgs *kp, uint32_t F, void *stream, char *err, si
             }
         }
     }
-    FEnv e; e.P = c->d_prog; e.a = &k; e.ms = k.in.modsets; e.imm_in = nullptr;
+    FEnv e; e.P = c->d_prog; e.a = &k; e.ms = k.in.modsets;
     FG<0> g; g.rank = 0; g.size = 1; g.bar = 0;
-    { static FW<FCfgS> W; g.red = W.gred; f_loop(g, W, e, L[0], 0); }
-    { static FW<FCfgL> W; g.red = W.gred; f_loop(g, W, e, L[1], 0); }
-    { static FW<FCfgX> W; g.red = W.gred; f_loop(g, W, e, L[2], 0); }
+    static FCta Q;
+    { static FW<FCfgS> W; g.red = W.gred; FCtx<FCfgS> x; x.Q = &Q; x.w0 = (uint8_t *)&W; x.stride = 0; x.ng = 1; x.gi = 0; x.tid = 0; x.nthreads = 1; f_loop(g, W, e, x, L[0], 0); }
+    { static FW<FCfgL> W; g.red = W.gred; FCtx<FCfgL> x; x.Q = &Q; x.w0 = (uint8_t *)&W; x.stride = 0; x.ng = 1; x.gi = 0; x.tid = 0; x.nthreads = 1; f_loop(g, W, e, x, L[1], 0); }
+    { static FW<FCfgX> W; g.red = W.gred; FCtx<FCfgX> x; x.Q = &Q; x.w0 = (uint8_t *)&W; x.stride = 0; x.ng = 1; x.gi = 0; x.tid = 0; x.nthreads = 1; f_loop(g, W, e, x, L[2], 0); }
     c->launches = 3;
 #endif
     return 0;

@@ -148,12 +148,87 @@ template <> struct FG<0> {
 /* uniform strided loop over the lanes of a group (like GFOR of core.cuh), never unrolled: code size is what bounds this stage */
 #define FFOR(g, i, n) _Pragma("unroll 1") for (uint32_t _b##i = 0, i = (g).rank; _b##i < (n); _b##i += (g).size, i += (g).size)
 
+/* ------------------------------------------------- work pooled over a CTA */
+/* The per-item phases (unify one anchor against one pattern, plan one selected
+ * match) have a handful of items per function: run by the function's own group
+ * they keep 2-4 of 32 lanes busy.  The groups of a CTA are in lock step anyway,
+ * so these phases pool the items of all resident functions, sorted by pattern,
+ * and every warp of the CTA takes 32 consecutive ones: full warps running one
+ * pattern's code.  Shared by the CTA: items per (group, pattern), their first
+ * pooled index.                                                              */
+static constexpr int F_MAXG = 16;
+struct FCta {
+    uint32_t cnt[F_MAXG][CL_MAX_PATTERNS];
+    uint32_t base[F_MAXG][CL_MAX_PATTERNS];
+    uint32_t pstart[CL_MAX_PATTERNS + 1];
+    uint32_t total, pad[2];
+};
+template <class C> struct FW;
+template <class C> struct FCtx {              /* a thread's view of its CTA */
+    FCta *Q; uint8_t *w0; uint32_t stride, ng, gi, tid, nthreads;
+    CLMEM FW<C> &w(uint32_t g) const { return *(FW<C> *)(w0 + (size_t)g * stride); }
+};
+CLD void f_cta_sync() {
+#if CL_DEV
+    __syncthreads();
+#endif
+}
+CLD bool f_cta_or(bool x) {
+#if CL_DEV
+    return __syncthreads_or(x) != 0;
+#else
+    return x;
+#endif
+}
+/* pooled index of every (group, pattern) segment, pattern major; the groups wrote their cnt row before */
+template <class C> CLF uint32_t f_pool_layout(const FCtx<C> &x) {
+    f_cta_sync();
+    FCta &Q = *x.Q;
+#if CL_DEV
+    if (x.tid < 32) {
+        const uint32_t pi = x.tid & 15u;
+        uint32_t sum = 0;
+        if (x.tid < 16) {
+#pragma unroll 1
+            for (uint32_t g = 0; g < x.ng; g++) sum += Q.cnt[g][pi];
+        }
+        uint32_t v = sum;
+#pragma unroll
+        for (int d = 1; d < 16; d <<= 1) { const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, d); if ((x.tid & 31u) >= (uint32_t)d) v += t; }
+        if (x.tid < 16) {
+            uint32_t run = v - sum;
+            Q.pstart[pi] = run;
+#pragma unroll 1
+            for (uint32_t g = 0; g < x.ng; g++) { Q.base[g][pi] = run; run += Q.cnt[g][pi]; }
+            if (pi == 15) { Q.pstart[16] = v; Q.total = v; }
+        }
+    }
+#else
+    uint32_t run = 0;
+    for (uint32_t pi = 0; pi < 16; pi++) { Q.pstart[pi] = run; for (uint32_t g = 0; g < x.ng; g++) { Q.base[g][pi] = run; run += Q.cnt[g][pi]; } }
+    Q.pstart[16] = run; Q.total = run;
+#endif
+    f_cta_sync();
+    return Q.total;
+}
+/* pooled item i -> pattern, group, index inside the group's segment */
+template <class C> CLD void f_pool_item(const FCtx<C> &x, uint32_t i, uint32_t &pi, uint32_t &g, uint32_t &k) {
+    const FCta &Q = *x.Q;
+    pi = 0;
+#pragma unroll 1
+    while (pi < 15 && Q.pstart[pi + 1] <= i) pi++;
+    g = 0;
+#pragma unroll 1
+    while (g + 1 < x.ng && Q.base[g + 1][pi] <= i) g++;
+    k = i - Q.base[g][pi];
+}
+
 /* ------------------------------------------------------- size classes */
 /* I: record slots of the arena, IN: largest input the class accepts, V: values,
  * B: blocks, MR: memrefs, Q: new immediates, L: def_iid updates, M: raw matches
  * of one round, E: events (group-private global scratch, not shared memory)  */
 struct FCfgS { static constexpr uint32_t I = 128, IN = 104, V = 176, VIN = 144, B = 12, MR = 28, Q = 16, L = 256, M = 48, E = 64, TQ = 24; };
-struct FCfgL { static constexpr uint32_t I = 256, IN = 208, V = 352, VIN = 288, B = 24, MR = 56, Q = 32, L = 512, M = 96, E = 128, TQ = 32; };
+struct FCfgL { static constexpr uint32_t I = 256, IN = 208, V = 352, VIN = 288, B = 24, MR = 56, Q = 32, L = 512, M = 80, E = 128, TQ = 32; };
 struct FCfgX { static constexpr uint32_t I = 512, IN = 416, V = 704, VIN = 576, B = 48, MR = 112, Q = 64, L = 1024, M = 192, E = 256, TQ = 96; };
 
 enum { SF_LIVE = 1, SF_PURE = 2, SF_INS = 4 /* waits in an insertion list for the next rebuild */, SF_TAKEN = 8, SF_CLS_SHIFT = 4, SF_NOCLS = 15 };
@@ -173,6 +248,7 @@ template <class C> struct FW {                 /* one function resident in a gro
     cl_imm timm[C::TQ];                         /* immediates of the rewrites being planned (staged until their index is known) */
     cl_event *ev;                               /* [C::E] events of the function: group-private global scratch */
     FDLog *dlog;                                /* [C::L] def_iid updates in program order: same scratch         */
+    const cl_imm *imm_in;                       /* immediates of the resident function (global, read only)      */
     cl_blk blk[C::B];
     cl_memref mem[C::MR];
     uint32_t usecnt[C::V];
@@ -187,6 +263,7 @@ template <class C> struct FW {                 /* one function resident in a gro
     uint32_t n_slots, n_pos, cur, next_vid, next_iid, next_temp, n_newimm, n_log, n_mt, n_sel;
     uint32_t wl_tail, n_ev, fail, dirty, flags, nred, big_blocks, n_mev;
     uint32_t r_inst, r_imm, r_val, r_ev, work, ret, n_free, n_timm;
+    uint32_t j0, j1, j_next, pad2;               /* rewrite steps: the block run being rewritten, first match of the next one */
     uint16_t defslot[C::V], redirect[C::V], vtmp[C::V];
     uint16_t norigin[C::V];                     /* ValueInfo.origin of the values created here: kind << 14 | vid (f_origin) */
     uint16_t ord[2][C::I], posof[C::I], insslot[C::I], outpos[C::I], wl[C::I];
@@ -199,6 +276,7 @@ template <class C> struct FW {                 /* one function resident in a gro
     uint8_t alive[C::V];
     uint8_t sblk[C::I], inscnt[C::I];
     uint8_t mstate[C::M];
+    uint8_t tnext[C::TQ];                       /* next staged immediate of the same match, 0xFF = last */
 };
 
 /* what a group needs besides its FW                                          */
@@ -206,7 +284,6 @@ struct FEnv {
     const FProg *P;                /* shared memory copy                           */
     const KArgs *a;
     const cl_modset *ms;
-    const cl_imm *imm_in;          /* immediates of the resident function (global)  */
 };
 
 /* ------------------------------------------------------------ small helpers */
@@ -221,7 +298,8 @@ template <class C> CLD opnd f_slot(const FW<C> &W, uint32_t s, unsigned k) {
     return o;
 }
 template <class C> CLD cl_imm f_imm_at(const FW<C> &W, const FEnv &e, uint32_t idx) {
-    if (idx < W.nq_in) return e.imm_in[idx];
+    (void)e;
+    if (idx < W.nq_in) return W.imm_in[idx];
     return W.newimm[(idx - W.nq_in) & (C::Q - 1)];
 }
 template <class C> CLD bool f_live(const FW<C> &W, uint32_t s) { return (W.sflag[s] & SF_LIVE) != 0; }
@@ -304,7 +382,7 @@ template <class G, class C> CLD void f_prof(const G &g, FW<C> &W, int slot) {
 
 /* ------------------------------------------------------------------- load */
 /* false: the function does not fit this size class (nothing was touched)     */
-template <class G, class C> CLF bool f_load(const G &g, FW<C> &W, FEnv &e, uint32_t f) {
+template <class G, class C> CLF bool f_load(const G &g, FW<C> &W, const FEnv &e, uint32_t f) {
     const cl_corpus &in = e.a->in;
     const uint32_t b0 = in.func_blk_off[f], b1 = in.func_blk_off[f + 1];
     const uint32_t i0 = in.blk_off[b0], n = in.blk_off[b1] - i0, nb = b1 - b0;
@@ -322,7 +400,7 @@ template <class G, class C> CLF bool f_load(const G &g, FW<C> &W, FEnv &e, uint3
         W.flags = 0; W.nred = 0; W.big_blocks = 0; W.n_mev = 0; W.ret = 0; W.n_free = 0; W.n_timm = 0;
         if (in.ext_off[f + 1] != in.ext_off[f] || nb == 0) W.fail = F_REDO + 1;      /* overflow slots: general kernel */
     }
-    e.imm_in = in.imm + q0;
+    if (g.rank == 0) W.imm_in = in.imm + q0;
     {
         const uint4 *sh = (const uint4 *)(in.hdr + i0), *st = (const uint4 *)(in.tag + (size_t)i0 * 8), *sp = (const uint4 *)(in.pay + (size_t)i0 * 8);
         uint4 *dh = (uint4 *)W.hdr, *dt = (uint4 *)W.tag, *dp = (uint4 *)W.pay;
@@ -567,7 +645,7 @@ template <class C> CLF void f_try_anchor(FW<C> &W, const FEnv &e, uint32_t s, un
     a_add(&W.fstat[pi], 1u);
 }
 
-template <class G, class C> CLF void f_match(const G &g, FW<C> &W, const FEnv &e, unsigned table) {
+template <class G, class C> CLF void f_match_prep(const G &g, FW<C> &W, const FEnv &e, const FCtx<C> &x, unsigned table) {
     const FProg &P = *e.P;
     if (g.rank == 0) { W.n_mt = 0; W.n_sel = 0; }
     /* blocks long enough for a candidate product above the budget (37^3 > 50 000): class counts */
@@ -607,14 +685,28 @@ template <class G, class C> CLF void f_match(const G &g, FW<C> &W, const FEnv &e
         if ((fl & SF_LIVE) && c != SF_NOCLS && P.anchor_mask[table][c]) list[a_add(&fill[c], 1u)] = (uint16_t)s;
     }
     g.sync();
-#pragma unroll 1
-    for (unsigned pi = 0; pi < P.n_patterns; pi++) {
-        const FPat &p = P.p[pi];
-        if (p.table != table) continue;
-        const uint32_t ac = p.t[p.order[0]].cls, cnt = W.acnt[ac], lo = fill[ac] - cnt;
-        FFOR(g, k, cnt) if (k < cnt) f_try_anchor(W, e, list[lo + k], pi);
-    }
+    /* this group's row of the CTA's item table: anchors of every pattern of the table */
+    FFOR(g, pi, CL_MAX_PATTERNS) if (pi < CL_MAX_PATTERNS)
+        x.Q->cnt[x.gi][pi] = pi < P.n_patterns && P.p[pi].table == table ? W.acnt[P.p[pi].t[P.p[pi].order[0]].cls] : 0u;
     g.sync();
+}
+/* a group that sits this match phase out */
+template <class G, class C> CLF void f_match_idle(const G &g, const FCtx<C> &x) {
+    FFOR(g, pi, CL_MAX_PATTERNS) if (pi < CL_MAX_PATTERNS) x.Q->cnt[x.gi][pi] = 0;
+}
+/* unify every (anchor, pattern) item of the CTA's resident functions: all threads of the CTA */
+template <class C> CLF void f_match_pooled(const FCtx<C> &x, const FEnv &e) {
+    const uint32_t total = f_pool_layout(x);
+#pragma unroll 1
+    for (uint32_t i = x.tid; i < total; i += x.nthreads) {
+        uint32_t pi, gq, k;
+        f_pool_item(x, i, pi, gq, k);
+        FW<C> &Wq = x.w(gq);
+        const FPat &p = e.P->p[pi];
+        const uint32_t ac = p.t[p.order[0]].cls, lo = Wq.acnt[MAX_CLS + 4 + ac] - Wq.acnt[ac];
+        f_try_anchor(Wq, e, Wq.outpos[lo + k], pi);
+    }
+    f_cta_sync();
 }
 
 /* select_matches (patterns.py:241-252): the stable sort key is (start_pos,
@@ -709,14 +801,16 @@ template <class G, class C> CLF void f_emit_matches(const G &g, FW<C> &W, const 
  * become part of the stream only when the rewrite succeeds (a refused rewrite
  * keeps the ids, values and immediates it allocated: G4).                    */
 static constexpr uint16_t F_T_REL = 1u << 15;      /* slot payload is relative to the match's id bases (patched after the scan) */
-static constexpr int F_RW_IMMS = 6;                 /* immediates one rewrite may create */
+/* what planning a match leaves for its commit (the plan itself is the chain of new records) */
+struct FPlan { uint16_t head; uint8_t tq, nins, nv, ni, nq, flags; };      /* flags: rm (3 bits) | retag << 3 | ok << 4; tq: first staged immediate */
+static_assert(sizeof(FPlan) == 8, "FPlan lives in the class-count table's storage");
 template <class C> struct FRW {
     FW<C> *W; const FEnv *e;
     uint32_t s[3]; cl_hdr h[3];
     unsigned n, pat;
-    uint32_t ns[8], nins;          /* record slots of the plan's insert list */
+    uint32_t head, last, nins;     /* the plan's insert list: a chain of record slots (FW::nxt) */
     uint32_t nv, ni, nq;           /* values / instruction ids / immediates allocated so far, relative to the match */
-    uint32_t tq[F_RW_IMMS];        /* staged immediates (FW::timm), creation order */
+    uint32_t tq_head, tq_last;     /* staged immediates (FW::timm), chained in creation order (FW::tnext) */
     uint32_t rm, retag, esc;       /* esc: bit 4t + k = def k of record t escapes (snapshot of the block's start) */
     uint32_t over;                 /* capacity of the slice exceeded: 1 values, 2 immediates, 4 def_iid log, 8 record slots */
 };
@@ -752,14 +846,18 @@ template <class C> CLD opnd frw_value(FRW<C> &c) {                 /* LiftedFunc
 }
 template <class C> CLD opnd frw_imm(FRW<C> &c, unsigned long long bits, unsigned long long text, bool hextext) {
     FW<C> &W = *c.W;
-    opnd o; o.tag = (uint16_t)(CL_K_IMM | F_T_REL | (hextext ? CL_T_IMM_HEXTEXT : 0)); o.pay = c.nq;
-    const uint32_t t = c.nq < (uint32_t)F_RW_IMMS ? a_add(&W.n_timm, 1u) : (uint32_t)C::TQ;
-    if (t < C::TQ) { W.timm[t].bits = bits; W.timm[t].text = text; c.tq[c.nq] = t; c.nq++; } else c.over |= 2u;
+    const uint32_t t = c.nq < 255u ? a_add(&W.n_timm, 1u) : (uint32_t)C::TQ;
+    opnd o; o.tag = (uint16_t)(CL_K_IMM | F_T_REL | (hextext ? CL_T_IMM_HEXTEXT : 0)); o.pay = c.nq | t << 8;      /* index in the match, staging slot */
+    if (t < C::TQ) {
+        W.timm[t].bits = bits; W.timm[t].text = text; W.tnext[t] = 0xFF;
+        if (c.nq) W.tnext[c.tq_last] = (uint8_t)t; else c.tq_head = t;
+        c.tq_last = t; c.nq++;
+    } else c.over |= 2u;
     return o;
 }
 /* bits / spelling of an immediate operand, staged or already in the function's table */
 template <class C> CLD cl_imm frw_imm_of(const FRW<C> &c, opnd o) {
-    if (o.tag & F_T_REL) return c.W->timm[c.tq[o.pay < (uint32_t)F_RW_IMMS ? o.pay : 0]];
+    if (o.tag & F_T_REL) return c.W->timm[(o.pay >> 8) < C::TQ ? (o.pay >> 8) : 0];
     return f_imm_at(*c.W, *c.e, o.pay);
 }
 /* make_inst (ssir.py:237-241) + append to the plan's insert list; returns the (relative) iid.  The value the
@@ -767,7 +865,7 @@ template <class C> CLD cl_imm frw_imm_of(const FRW<C> &c, opnd o) {
 template <class C> CLN uint32_t frw_emit(FRW<C> &c, uint16_t op, uint16_t modset, opnd def, const opnd *uses, unsigned nu) {
     FW<C> &W = *c.W;
     const uint32_t iid = c.ni++;
-    const uint32_t s = c.nins < 8 ? f_alloc_slot(W) : (uint32_t)F_NONE;
+    const uint32_t s = f_alloc_slot(W);
     if (s == F_NONE) { c.over |= 8u; return iid; }
     cl_hdr h;
     h.iid = iid; h.op = op; h.modset = modset; h.n_defs = 1; h.n_aux = 0; h.n_uses = (uint8_t)nu; h.flags = 0; h.ext = 0;
@@ -777,7 +875,9 @@ template <class C> CLN uint32_t frw_emit(FRW<C> &c, uint16_t op, uint16_t modset
 #pragma unroll 1
     for (unsigned k = 0; k < 7; k++) { tg[1 + k] = k < nu ? uses[k].tag : (uint16_t)0; py[1 + k] = k < nu ? uses[k].pay : 0u; }
     W.sflag[s] = 0;
-    c.ns[c.nins++] = s;
+    W.nxt[s] = F_NONE;
+    if (c.nins) W.nxt[c.last] = (uint16_t)s; else c.head = s;
+    c.last = s; c.nins++;
     return iid;
 }
 template <class C> CLD void frw_drop(FRW<C> &c, opnd o) { if (is_value(o) && o.pay < C::V) c.W->alive[o.pay] = 0; }   /* _drop_values :314-317 */
@@ -1050,129 +1150,193 @@ template <class C> CLN bool frw_run(FRW<C> &c) {
  * over the matches of the batch in select order = the reference's allocation
  * order, G3; a refused plan keeps its ids, values and immediates, G4).  The use
  * counts follow the edit at once; the escape tests of the block's other matches
- * were taken before (c.esc), which is the reference's per-block def-use snapshot
- * (patterns.py:674,706).  Runs on many lanes at once, one match each.         */
-template <class C> CLF void f_commit(FW<C> &W, const FEnv &e, unsigned table, uint32_t phase, const FMatch m, FRW<C> &c, bool ok,
+ * were taken before (at planning), which is the reference's per-block def-use
+ * snapshot (patterns.py:674,706).  Runs on many lanes at once, one match each. */
+template <class C> CLF void f_commit(FW<C> &W, const FEnv &e, unsigned table, uint32_t phase, const FMatch m, const FPlan pl,
                                      uint32_t vbase, uint32_t ibase, uint32_t qbase, uint32_t lbase, uint32_t rank_in_block) {
     const FProg &P = *e.P;
     const uint32_t b = W.sblk[m.slot[0]];
+    const bool ok = (pl.flags >> 4) & 1u;
 #pragma unroll 1
-    for (uint32_t k = 0; k < c.nv; k++) {
+    for (uint32_t k = 0; k < pl.nv; k++) {
         const uint32_t v = vbase + k;
         W.alive[v] = 1; W.usecnt[v] = 0; W.defslot[v] = F_NONE; W.norigin[v] = 1u << 14;
     }
+    {
+        uint32_t t = pl.tq;
 #pragma unroll 1
-    for (uint32_t k = 0; k < c.nq; k++) W.newimm[qbase - W.nq_in + k] = W.timm[c.tq[k]];
+        for (uint32_t k = 0; k < pl.nq; k++) { W.newimm[qbase - W.nq_in + k] = W.timm[t]; t = W.tnext[t]; }
+    }
+    {
+        uint32_t s = pl.head;
 #pragma unroll 1
-    for (uint32_t r = 0; r < c.nins; r++) {
-        const uint32_t s = c.ns[r];
-        const uint32_t iid = W.hdr[s].iid + ibase, ns = 1u + W.hdr[s].n_uses;
-        W.hdr[s].iid = iid;
+        for (uint32_t r = 0; r < pl.nins; r++, s = W.nxt[s]) {
+            const uint32_t iid = W.hdr[s].iid + ibase, ns = 1u + W.hdr[s].n_uses;
+            W.hdr[s].iid = iid;
 #pragma unroll 1
-        for (uint32_t k = 0; k < ns; k++) {
-            const uint16_t t = W.tag[s * 8 + k];
-            if (t & F_T_REL) { W.pay[s * 8 + k] += kind_of(t) == CL_K_VALUE ? vbase : qbase; W.tag[s * 8 + k] = (uint16_t)(t & ~F_T_REL); }
+            for (uint32_t k = 0; k < ns; k++) {
+                const uint16_t t = W.tag[s * 8 + k];
+                if (!(t & F_T_REL)) continue;
+                W.pay[s * 8 + k] = kind_of(t) == CL_K_VALUE ? W.pay[s * 8 + k] + vbase : (W.pay[s * 8 + k] & 0xFFu) + qbase;
+                W.tag[s * 8 + k] = (uint16_t)(t & ~F_T_REL);
+            }
+            W.dlog[lbase + r].vid = W.pay[s * 8]; W.dlog[lbase + r].iid = (int32_t)iid;     /* value.def_iid = inst.iid */
         }
-        W.dlog[lbase + r].vid = W.pay[s * 8]; W.dlog[lbase + r].iid = (int32_t)iid;     /* value.def_iid = inst.iid */
     }
     if (!ok) {
+        uint32_t s = pl.head;
 #pragma unroll 1
-        for (uint32_t r = 0; r < c.nins; r++) f_free_slot(W, c.ns[r]);          /* the plan is dropped, its ids are not (G4) */
+        for (uint32_t r = 0; r < pl.nins; r++) { const uint32_t nx = W.nxt[s]; f_free_slot(W, s); s = nx; }      /* the plan is dropped, its ids are not (G4) */
         a_add(&W.fstat[48 + m.pat], 1u);
         f_event(W, phase << 28 | b, CL_EV_REFUSED, rank_in_block, m.pat, W.blk[b].bid, 0, 0);
         return;
     }
     /* removed records first (their values lose their defining record) */
 #pragma unroll 1
-    for (unsigned t = 0; t < m.n; t++) if (c.rm >> t & 1u) {
+    for (unsigned t = 0; t < m.n; t++) if (pl.flags >> t & 1u) {
         const uint32_t s = m.slot[t];
         W.sflag[s] = 0;
-        f_value_operands(W, c.h[t], s, [&](uint32_t v) { f_dec_use(W, v); });
+        f_value_operands(W, W.hdr[s], s, [&](uint32_t v) { f_dec_use(W, v); });
         f_release(W, s);
     }
     const uint32_t anchor = m.slot[m.n - 1], ap = W.posof[anchor];
+    {
+        uint32_t s = pl.head;
 #pragma unroll 1
-    for (uint32_t r = 0; r < c.nins; r++) {
-        const uint32_t s = c.ns[r];
-        const cl_hdr h = W.hdr[s];
-        unsigned sf = SF_LIVE | SF_INS | f_cls(P, table, h.op) << SF_CLS_SHIFT;
-        if (h.op < CL_OP__COUNT && (P.opflags[h.op] & CL_OPF_PURE)) sf |= SF_PURE;
-        W.sflag[s] = (uint8_t)sf;
-        W.sblk[s] = (uint8_t)b;
-        W.posof[s] = (uint16_t)ap;
-        W.nxt[s] = r + 1 < c.nins ? (uint16_t)c.ns[r + 1] : F_NONE;
-        const opnd d = f_slot(W, s, 0);
-        if (is_value(d) && d.pay < C::V) W.defslot[d.pay] = (uint16_t)s;
-        f_value_operands(W, h, s, [&](uint32_t v) { f_inc_use(W, v); });
+        for (uint32_t r = 0; r < pl.nins; r++, s = W.nxt[s]) {
+            const cl_hdr h = W.hdr[s];
+            unsigned sf = SF_LIVE | SF_INS | f_cls(P, table, h.op) << SF_CLS_SHIFT;
+            if (h.op < CL_OP__COUNT && (P.opflags[h.op] & CL_OPF_PURE)) sf |= SF_PURE;
+            W.sflag[s] = (uint8_t)sf;
+            W.sblk[s] = (uint8_t)b;
+            W.posof[s] = (uint16_t)ap;
+            const opnd d = f_slot(W, s, 0);
+            if (is_value(d) && d.pay < C::V) W.defslot[d.pay] = (uint16_t)s;
+            f_value_operands(W, h, s, [&](uint32_t v) { f_inc_use(W, v); });
+        }
     }
-    if (c.nins) { W.insslot[ap] = (uint16_t)c.ns[0]; W.inscnt[ap] = 1; }
-    if (c.retag) {                                  /* _rw_imad_wide :414-418 */
+    if (pl.nins) { W.insslot[ap] = pl.head; W.inscnt[ap] = 1; }
+    if (pl.flags & 8u) {                            /* _rw_imad_wide :414-418 */
         cl_hdr &h = W.hdr[m.slot[0]];
         h.modset = e.ms[h.modset].minus_wide;
         h.op = CL_OP_IMAD64;
         W.sflag[m.slot[0]] = (uint8_t)((W.sflag[m.slot[0]] & 15u) | f_cls(P, table, CL_OP_IMAD64) << SF_CLS_SHIFT);
     }
-    if (c.nins || c.rm) W.dirty = 1;
+    if (pl.nins || (pl.flags & 7u)) W.dirty = 1;
     a_add(&W.fstat[32 + m.pat], 1u);
 }
 
-/* _apply_patterns (patterns.py:671-707), the rewrite half: blocks in order; the
- * selected matches of a block are planned side by side, one lane each; returns
- * the number of successful rewrites                                           */
-template <class G, class C> CLF uint32_t f_rewrite(const G &g, FW<C> &W, const FEnv &e, unsigned table, uint32_t phase) {
+/* _apply_patterns (patterns.py:671-707), the rewrite half, in steps the CTA takes
+ * together.  A step is one block of every resident function (blocks in order:
+ * the escape tests of a block see the use counts the earlier blocks left, G5):
+ *   f_plan_prep    group: the block's selected matches [j0, j1), sorted by pattern
+ *   f_plan_pooled  CTA: one lane plans one match (any function's), full warps per pattern
+ *   f_plan_commit  group: id bases by scan in select order, then the edits          */
+template <class C> CLD FPlan *f_plans(FW<C> &W) { return (FPlan *)&W.ccnt[0][0]; }
+template <class G, class C> CLF void f_plan_prep(const G &g, FW<C> &W, const FCtx<C> &x, bool on) {
+    FFOR(g, k, 2 * CL_MAX_PATTERNS) if (k < 2 * CL_MAX_PATTERNS) W.acnt[k] = 0;
+    if (g.rank == 0) W.n_timm = 0;
+    g.sync();
+    const uint32_t nsel = on ? W.n_sel : 0u;
+    /* counting sort of the selected matches by pattern: acnt[pi] counts, acnt[16 + pi] fill cursors, psel = indices j */
+    uint16_t *psel = W.esc;
+    FFOR(g, j, nsel) if (j < nsel) a_add(&W.acnt[W.mt[W.sel[j]].pat & 15u], 1u);
+    g.sync();
+    if (g.rank == 0) {
+        uint32_t run = 0;
+#pragma unroll 1
+        for (unsigned pi = 0; pi < CL_MAX_PATTERNS; pi++) { W.acnt[CL_MAX_PATTERNS + pi] = run; run += W.acnt[pi]; }
+    }
+    g.sync();
+    FFOR(g, j, nsel) if (j < nsel) psel[a_add(&W.acnt[CL_MAX_PATTERNS + (W.mt[W.sel[j]].pat & 15u)], 1u)] = (uint16_t)j;
+    FFOR(g, pi, CL_MAX_PATTERNS) if (pi < CL_MAX_PATTERNS) x.Q->cnt[x.gi][pi] = W.acnt[pi];
+    g.sync();
+}
+template <class C> CLF void f_plan_pooled(const FCtx<C> &x, const FEnv &e) {
+    const uint32_t total = f_pool_layout(x);
+#pragma unroll 1
+    for (uint32_t i = x.tid; i < total; i += x.nthreads) {
+        uint32_t pi, gq, k;
+        f_pool_item(x, i, pi, gq, k);
+        FW<C> &W = x.w(gq);
+        const uint32_t j = W.esc[W.acnt[CL_MAX_PATTERNS + pi] - W.acnt[pi] + k];
+        const FMatch m = W.mt[W.sel[j]];
+        FRW<C> c;
+        c.W = &W; c.e = &e; c.n = m.n; c.pat = m.pat; c.head = F_NONE; c.last = F_NONE; c.nins = 0; c.nv = 0; c.ni = 0; c.nq = 0;
+        c.tq_head = 0xFF; c.tq_last = 0xFF; c.rm = 0; c.retag = 0; c.over = 0;
+        c.esc = f_escape_bits(W, m);
+#pragma unroll 1
+        for (unsigned t = 0; t < 3; t++) { c.s[t] = t < m.n ? m.slot[t] : (uint32_t)m.slot[0]; c.h[t] = W.hdr[c.s[t]]; }
+        const bool ok = frw_run(c);
+        if (c.over || c.nins > 255u || c.nv > 255u || c.ni > 255u) f_fail(W, F_REDO + 40 + (c.over ? c.over : 8u));
+        if (ok && c.rm && W.nb > 1) {
+            /* G5: every block is planned against the use counts of the round's start; the reference lets a block see
+             * the rewrites of the blocks before it.  That differs only when a removed record uses a value defined in
+             * a LATER block of its function (then a later escape test would count one use less): hand back.          */
+            const uint32_t b = W.sblk[m.slot[0]];
+#pragma unroll 1
+            for (unsigned t = 0; t < m.n; t++) if (c.rm >> t & 1u)
+                f_value_operands(W, c.h[t], m.slot[t], [&](uint32_t v) {
+                    const uint32_t dp = v < C::V ? W.defslot[v] : (uint32_t)F_NONE;
+                    if (dp != F_NONE && W.sblk[dp] > b) f_fail(W, F_REDO + 25);
+                });
+        }
+        FPlan pl;
+        pl.head = (uint16_t)c.head; pl.tq = (uint8_t)c.tq_head; pl.nins = (uint8_t)c.nins; pl.nv = (uint8_t)c.nv; pl.ni = (uint8_t)c.ni; pl.nq = (uint8_t)c.nq;
+        pl.flags = (uint8_t)((c.rm & 7u) | (c.retag ? 8u : 0u) | (ok ? 16u : 0u));
+        f_plans(W)[j] = pl;
+    }
+    f_cta_sync();
+}
+/* returns the number of successful rewrites of the step */
+template <class G, class C> CLF uint32_t f_plan_commit(const G &g, FW<C> &W, const FEnv &e, unsigned table, uint32_t phase) {
     const uint32_t nsel = f_rd(g, &W.n_sel);
-    if (g.rank == 0) W.ret = 0;
-    uint32_t j0 = 0;
-    bool good = true;
-    while (j0 < nsel && good) {
-        const uint32_t b = W.sblk[W.mt[W.sel[j0]].slot[0]];
-        uint32_t j1 = j0 + 1;
-        while (j1 < nsel && W.sblk[W.mt[W.sel[j1]].slot[0]] == b) j1++;
+    uint32_t done = 0;
+    if (!f_oks(g, W)) return 0;
+#pragma unroll 1
+    for (uint32_t c0 = 0; c0 < nsel; c0 += g.size) {
         g.sync();
-        FFOR(g, q, j1 - j0) if (q < j1 - j0) W.esc[j0 + q] = (uint16_t)f_escape_bits(W, W.mt[W.sel[j0 + q]]);
+        const uint32_t nv0 = W.next_vid, ni0 = W.next_iid, nq0 = W.nq_in + W.n_newimm, nl0 = W.n_log;
+        const uint32_t j = c0 + g.rank;
+        const bool act = j < nsel;
+        FPlan pl; pl.head = F_NONE; pl.tq = 0xFF; pl.nins = pl.nv = pl.ni = pl.nq = pl.flags = 0;
+        FMatch m; m.n = 0; m.pat = 0; m.slot[0] = m.slot[1] = m.slot[2] = 0;
+        uint32_t rank_in_block = 0;
+        if (act) {
+            pl = f_plans(W)[j];
+            m = W.mt[W.sel[j]];
+            /* rank of the match inside its block's select list (diagnostics, patterns.py:684) */
+            const uint32_t b = W.sblk[m.slot[0]];
+            uint32_t jb = j;
 #pragma unroll 1
-        for (uint32_t c0 = j0; c0 < j1 && good; c0 += g.size) {
-            if (g.rank == 0) W.n_timm = 0;
-            g.sync();
-            const uint32_t nv0 = W.next_vid, ni0 = W.next_iid, nq0 = W.nq_in + W.n_newimm, nl0 = W.n_log;
-            const uint32_t j = c0 + g.rank;
-            const bool act = j < j1;
-            FRW<C> c;
-            c.W = &W; c.e = &e; c.n = 0; c.pat = 0; c.nins = 0; c.nv = 0; c.ni = 0; c.nq = 0; c.rm = 0; c.retag = 0; c.over = 0; c.esc = 0;
-            FMatch m; m.n = 0; m.pat = 0; m.slot[0] = m.slot[1] = m.slot[2] = 0;
-            bool ok = false;
-            if (act) {
-                m = W.mt[W.sel[j]];
-                c.n = m.n; c.pat = m.pat; c.esc = W.esc[j];
+            while (jb > 0 && W.sblk[W.mt[W.sel[jb - 1]].slot[0]] == b) jb--;
+            rank_in_block = j - jb;
+        }
+        /* id bases: two packed scans (11 bits per count: at most 8 of each per match, 128 lanes) */
+        uint32_t t1, t2;
+        const uint32_t x1 = g.exscan((uint32_t)pl.nv | (uint32_t)pl.ni << 11 | (uint32_t)pl.nq << 22, t1), x2 = g.exscan((uint32_t)pl.nins | ((pl.flags >> 4) & 1u) << 11, t2);
+        const uint32_t vb = x1 & 0x7FFu, ib = (x1 >> 11) & 0x7FFu, qb = x1 >> 22, lb = x2 & 0x7FFu;
+        const uint32_t tv = t1 & 0x7FFu, ti = (t1 >> 11) & 0x7FFu, tq = t1 >> 22, tl = t2 & 0x7FFu, tok = t2 >> 11;
+        if (g.rank == 0 && (nv0 + tv > C::V || nq0 - W.nq_in + tq > C::Q || nl0 + tl > C::L)) f_fail(W, F_REDO + 45);
+        g.sync();
+        if (!f_oks(g, W)) return done;
+        if (act) f_commit(W, e, table, phase, m, pl, nv0 + vb, ni0 + ib, nq0 + qb, nl0 + lb, rank_in_block);
+        g.sync();
+        if (g.rank == 0) { W.next_vid = nv0 + tv; W.next_iid = ni0 + ti; W.n_newimm = nq0 - W.nq_in + tq; W.n_log = nl0 + tl; }
+        done += tok;
+        /* a new pure record nobody reads is dead on arrival */
+        if (act && (pl.flags & 16u)) {
+            uint32_t s = pl.head;
 #pragma unroll 1
-                for (unsigned t = 0; t < 3; t++) { c.s[t] = t < m.n ? m.slot[t] : (uint32_t)m.slot[0]; c.h[t] = W.hdr[c.s[t]]; }
-                ok = frw_run(c);
-                if (c.over) f_fail(W, F_REDO + 40 + c.over);
-            }
-            /* id bases: two packed scans (11 bits per count: at most 8 of each per match, 128 lanes) */
-            uint32_t t1, t2;
-            const uint32_t x1 = g.exscan(c.nv | c.ni << 11 | c.nq << 22, t1), x2 = g.exscan(c.nins | (ok ? 1u : 0u) << 11, t2);
-            const uint32_t vb = x1 & 0x7FFu, ib = (x1 >> 11) & 0x7FFu, qb = x1 >> 22, lb = x2 & 0x7FFu;
-            const uint32_t tv = t1 & 0x7FFu, ti = (t1 >> 11) & 0x7FFu, tq = t1 >> 22, tl = t2 & 0x7FFu, tok = t2 >> 11;
-            if (g.rank == 0 && (nv0 + tv > C::V || nq0 - W.nq_in + tq > C::Q || nl0 + tl > C::L)) f_fail(W, F_REDO + 45);
-            g.sync();
-            if (!f_oks(g, W)) { good = false; break; }
-            if (act) f_commit(W, e, table, phase, m, c, ok, nv0 + vb, ni0 + ib, nq0 + qb, nl0 + lb, j - j0);
-            g.sync();
-            if (g.rank == 0) { W.next_vid = nv0 + tv; W.next_iid = ni0 + ti; W.n_newimm = nq0 - W.nq_in + tq; W.n_log = nl0 + tl; W.ret += tok; }
-            /* a new pure record nobody reads is dead on arrival */
-            if (act && ok) for (uint32_t r = 0; r < c.nins; r++) {
-                const uint32_t s = c.ns[r];
+            for (uint32_t r = 0; r < pl.nins; r++, s = W.nxt[s]) {
                 if (!(W.sflag[s] & SF_PURE)) continue;
                 const opnd d = f_slot(W, s, 0);
                 if (is_value(d) && d.pay < C::V && W.usecnt[d.pay] == 0) f_push_wl(W, s);
             }
-            g.sync();
         }
-        j0 = j1;
+        g.sync();
     }
-    g.sync();
-    return f_rd(g, &W.ret);
+    return done;
 }
 
 /* ------------------------------------------------------- dead pseudo ops */
@@ -1606,20 +1770,6 @@ template <class G, class C> CLF void f_store(const G &g, FW<C> &W, const FEnv &e
 }
 
 /* ------------------------------------------------------------ the CTA's loop */
-/* CTA-wide barrier / vote between the phases (all groups of the CTA)         */
-CLD void f_cta_sync() {
-#if CL_DEV
-    __syncthreads();
-#endif
-}
-CLD bool f_cta_or(bool x) {
-#if CL_DEV
-    return __syncthreads_or(x) != 0;
-#else
-    return x;
-#endif
-}
-
 template <class C> CLHD size_t f_scratch_bytes(uint32_t mev_cap) { return (size_t)(C::E + mev_cap) * sizeof(cl_event) + (size_t)C::L * sizeof(FDLog); }
 struct FLoop {
     /* work of this class: entries [bounds[0], bounds[1]) of the size-sorted function list (device side counting
@@ -1640,7 +1790,47 @@ struct FLoop {
  * step an SM runs one phase's code at a time for all its resident functions.
  * What does not fit the class goes to the next class's list, hand-backs to the
  * general kernel.                                                            */
-template <class G, class C> CLF void f_loop(const G &g, FW<C> &W, FEnv &e, const FLoop &L, uint32_t group) {
+/* one round of _apply_patterns for the resident functions of the CTA; `on`: this group takes part
+ * (with its own table: the pooled items are per pattern, and the two tables share no pattern).
+ * Returns the group's number of successful rewrites.                                             */
+template <class G, class C> CLF uint32_t f_apply_step(const G &g, FW<C> &W, const FEnv &e, const FCtx<C> &x, bool on, unsigned table, uint32_t phase,
+                                                      cl_event *mv, uint32_t mev_cap, bool match_only) {
+    if (on) {
+        if (f_rd(g, &W.dirty)) f_rebuild(g, W);
+        f_prof(g, W, PF_MOVE);
+        f_match_prep(g, W, e, x, table);
+    } else
+        f_match_idle(g, x);
+    f_match_pooled(x, e);
+    f_prof(g, W, PF_MATCH);
+    const uint32_t nm = on && f_oks(g, W) ? f_rd(g, &W.n_mt) : 0u;
+    if (nm) {
+        f_select(g, W);
+        if (mv && f_oks(g, W)) f_emit_matches(g, W, e, phase, mv, mev_cap);
+    }
+    f_prof(g, W, PF_SELECT);
+    const bool plan = nm != 0 && !match_only && f_oks(g, W);
+    f_plan_prep(g, W, x, plan);
+    f_plan_pooled(x, e);
+    uint32_t n = 0;
+    if (plan) n = f_plan_commit(g, W, e, table, phase);
+    f_prof(g, W, PF_PLAN);
+    return n;
+}
+
+/* Persistent loop of the groups of one CTA over the functions of their size
+ * class.  Every group holds one function and is in one of a few states; an
+ * iteration of the loop is one apply step (match, select, plan, commit) taken by
+ * all groups TOGETHER, whatever round their function is in, followed by what
+ * each group's state asks for (pack folding, or the end of the function: dead
+ * code, tags, store, and the next function's load, def-use and reciprocal pass).
+ * Lock step, because the stage is far more code than the instruction cache
+ * holds: free-running warps, each in another phase of another function, spent
+ * their time on instruction fetch (measured: 2 M cycles per function; 0.3 M in
+ * lock step).  A group never waits for another function's later rounds: it
+ * finishes its own and joins the next step with a new one.                     */
+enum { FST_EMPTY = 0, FST_XMAD, FST_ROUND, FST_MATCH_ONLY };
+template <class G, class C> CLF void f_loop(const G &g, FW<C> &W, const FEnv &e, const FCtx<C> &x, const FLoop &L, uint32_t group) {
     const KArgs &a = *e.a;
     const uint32_t lo1 = L.bounds[0], n1 = L.bounds[1] - lo1, n2 = L.n_list2_ptr ? *L.n_list2_ptr : 0u, n_list = n1 + n2;
     unsigned long long n_in = 0, n_out = 0, n_ev = 0;
@@ -1657,105 +1847,12 @@ template <class G, class C> CLF void f_loop(const G &g, FW<C> &W, FEnv &e, const
     const bool match_only = (a.passes & CL_PASS_MATCH_ONLY) != 0;
     const bool emit = a.emit_matches || match_only;
     cl_event *mv = emit ? mev : nullptr;
-#pragma unroll 1
-    for (;;) {
-        /* ---- take a function, load it */
-        g.sync();
-        if (g.rank == 0) W.work = a_add(L.counter, 1u);
-        g.sync();
-        const uint32_t w = f_rd(g, &W.work);
-        const bool have = w < n_list;
-        if (!f_cta_or(have)) break;
-        const uint32_t f = have ? (w < n1 ? L.list[lo1 + w] : L.list2[w - n1]) : 0u;
-        f_prof(g, W, PF_SETUP);
-        bool fit = have && f_load(g, W, e, f);
-        f_prof(g, W, PF_LOAD);
-        const bool xm = fit && (a.passes & CL_PASS_XMAD) && W.arch == CL_ARCH_SM52;
-        const unsigned table = match_only ? ((a.passes & CL_PASS_MATCH_XMAD) ? 1u : 0u) : (xm ? 1u : 0u);
-        if (fit && g.rank == 0 && emit && !mev) f_fail(W, F_REDO + 23);
-        g.sync();
-        /* `on`: this group still works on its function */
-#define F_ON (fit && f_oks(g, W))
-        f_cta_sync();
-        if (F_ON) f_index(g, W, e, table);
-        f_prof(g, W, PF_USECOUNT);
-        f_cta_sync();
-        if (match_only) {
-            /* match_patterns + select_matches only */
-            if (F_ON) f_match(g, W, e, table);
-            f_cta_sync();
-            if (F_ON && f_rd(g, &W.n_mt)) { f_select(g, W); f_emit_matches(g, W, e, 0, mv, L.mev_cap); }
-            f_cta_sync();
-        } else {
-            /* ---- normalize_xmad (patterns.py:805-810) */
-            if (f_cta_or(xm)) {
-                uint32_t nm = 0;
-                if (xm && F_ON) { f_match(g, W, e, 1); nm = f_rd(g, &W.n_mt); }
-                f_prof(g, W, PF_MATCH);
-                f_cta_sync();
-                if (xm && nm && F_ON) f_select(g, W);
-                f_prof(g, W, PF_SELECT);
-                f_cta_sync();
-                if (xm && nm && mv && F_ON) f_emit_matches(g, W, e, 0, mv, L.mev_cap);
-                if (xm && nm && F_ON) f_rewrite(g, W, e, 1, 0);
-                f_prof(g, W, PF_PLAN);
-                f_cta_sync();
-                if (xm && F_ON) f_dce(g, W);
-                if (xm && (a.passes & (CL_PASS_AGGREGATE | CL_PASS_RECIPROCAL)) && F_ON) f_reclass(g, W, e, 0);
-                f_prof(g, W, PF_DCE);
-                f_cta_sync();
-            }
-            /* ---- normalize_reciprocal (patterns.py:817-847) */
-            {
-                const bool rc = fit && (a.passes & CL_PASS_RECIPROCAL) && (f_rd(g, &W.flags) & FF_RCP);
-                if (f_cta_or(rc)) {
-                    if (rc && F_ON) {
-                        if (f_rd(g, &W.dirty)) f_rebuild(g, W);
-                        f_reciprocal(g, W, e);
-                    }
-                    f_prof(g, W, PF_RECIP);
-                    f_cta_sync();
-                }
-            }
-            /* ---- apply_aggregations (patterns.py:794-802) */
-            if (a.passes & CL_PASS_AGGREGATE) {
-                bool more = fit;
-#pragma unroll 1
-                for (uint32_t round = 0; round < a.max_rounds; round++) {
-                    if (!f_cta_or(more)) break;
-                    uint32_t nm = 0, n = 0;
-                    if (more && F_ON) {
-                        if (f_rd(g, &W.dirty)) f_rebuild(g, W);
-                        f_prof(g, W, PF_MOVE);
-                        f_match(g, W, e, 0);
-                        nm = f_rd(g, &W.n_mt);
-                    }
-                    f_prof(g, W, PF_MATCH);
-                    f_cta_sync();
-                    if (more && nm && F_ON) f_select(g, W);
-                    f_prof(g, W, PF_SELECT);
-                    f_cta_sync();
-                    if (more && nm && mv && F_ON) f_emit_matches(g, W, e, 2 + round, mv, L.mev_cap);
-                    if (more && nm && F_ON) n = f_rewrite(g, W, e, 0, 2 + round);
-                    f_prof(g, W, PF_PLAN);
-                    f_cta_sync();
-                    if (more && F_ON) n += f_simplify(g, W, e);
-                    f_prof(g, W, PF_SIMPLIFY);
-                    f_cta_sync();
-                    if (!n) more = false;
-                }
-                if (F_ON) f_dce(g, W);
-                f_prof(g, W, PF_DCE);
-                f_cta_sync();
-            }
-            if ((a.passes & CL_PASS_TAG) && F_ON) f_tag(g, W, e);
-            f_prof(g, W, PF_TAG);
-        }
-        /* ---- store, or route the function elsewhere */
-        g.sync();
-        const bool done = F_ON;
-#undef F_ON
-        if (done) {
+    int st = FST_EMPTY;
+    uint32_t round = 0, f = 0;
+    bool exhausted = false;
+    /* the function is finished (ok) or given up (hand-back / next class): the group is free again */
+    auto leave = [&](bool ok) {
+        if (ok) {
             if (f_rd(g, &W.dirty)) f_rebuild(g, W);
             f_prof(g, W, PF_MOVE);
             f_store(g, W, e, mv);
@@ -1766,13 +1863,13 @@ template <class G, class C> CLF void f_loop(const G &g, FW<C> &W, FEnv &e, const
 #if !CL_DEV
             if (getenv("CL_FUSED_STATS")) fprintf(stderr, "fused done: n_in %u slots %u out %u nv_in %u nv %u newimm %u log %u ev %u\n", W.n_in, W.n_slots, W.n_pos, W.nv_in, W.next_vid, W.n_newimm, W.n_log, W.n_ev);
 #endif
-        } else if (have) {
+        } else {
 #if !CL_DEV
-            if (fit && getenv("CL_FUSED_DEBUG")) fprintf(stderr, "fused hand-back: function %u (%u records) reason %u\n", f, W.n_in, W.fail);
+            if (getenv("CL_FUSED_DEBUG")) fprintf(stderr, "fused hand-back: function %u (%u records) reason %u\n", f, W.n_in, W.fail);
 #endif
             if (g.rank == 0) {
-                /* too large for this class, or outgrew its slice while running: the next class has more room */
-                if ((!fit || (W.fail > F_REDO + 40 && W.fail < F_REDO + 60)) && L.next_list) L.next_list[a_add(L.next_count, 1u)] = f;
+                /* outgrew its slice while running: the next class has more room; else the general kernel */
+                if (W.fail > F_REDO + 40 && W.fail < F_REDO + 60 && L.next_list) L.next_list[a_add(L.next_count, 1u)] = f;
                 else {
                     const cl_corpus &in = a.in;
                     const uint32_t n = in.blk_off[in.func_blk_off[f + 1]] - in.blk_off[in.func_blk_off[f]];
@@ -1781,7 +1878,89 @@ template <class G, class C> CLF void f_loop(const G &g, FW<C> &W, FEnv &e, const
                 }
             }
         }
-        f_cta_sync();
+        g.sync();
+        st = FST_EMPTY;
+    };
+    /* end of the function's passes: remove_dead_pseudo of apply_aggregations, tag_cuda_objects */
+    auto finish = [&]() {
+        if ((a.passes & CL_PASS_AGGREGATE) && f_oks(g, W)) f_dce(g, W);
+        f_prof(g, W, PF_DCE);
+        if ((a.passes & CL_PASS_TAG) && f_oks(g, W)) f_tag(g, W, e);
+        f_prof(g, W, PF_TAG);
+        leave(f_oks(g, W));
+    };
+    /* normalize_reciprocal, then the first aggregation round (or the end) */
+    auto after_xmad = [&]() {
+        if ((a.passes & CL_PASS_RECIPROCAL) && (f_rd(g, &W.flags) & FF_RCP) && f_oks(g, W)) {
+            if (f_rd(g, &W.dirty)) f_rebuild(g, W);
+            f_reciprocal(g, W, e);
+        }
+        f_prof(g, W, PF_RECIP);
+        if (!f_oks(g, W)) { leave(false); return; }
+        if ((a.passes & CL_PASS_AGGREGATE) && a.max_rounds) { st = FST_ROUND; round = 0; }
+        else finish();
+    };
+#pragma unroll 1
+    for (;;) {
+        /* ---- a free group takes the next function of its class */
+        if (st == FST_EMPTY && !exhausted) {
+            g.sync();
+            if (g.rank == 0) W.work = a_add(L.counter, 1u);
+            g.sync();
+            const uint32_t w = f_rd(g, &W.work);
+            f_prof(g, W, PF_SETUP);
+            if (w >= n_list) exhausted = true;
+            else {
+                f = w < n1 ? L.list[lo1 + w] : L.list2[w - n1];
+                if (!f_load(g, W, e, f)) {
+                    if (g.rank == 0) {           /* too large for this class */
+                        if (L.next_list) L.next_list[a_add(L.next_count, 1u)] = f;
+                        else {
+                            const cl_corpus &in = a.in;
+                            const uint32_t n = in.blk_off[in.func_blk_off[f + 1]] - in.blk_off[in.func_blk_off[f]];
+                            if (n > a.small_max) a.retry_big_list[a_add(a.retry_big_count, 1u)] = f;
+                            else a.retry_list[a_add(a.retry_count, 1u)] = f;
+                        }
+                    }
+                } else {
+                    f_prof(g, W, PF_LOAD);
+                    const bool xm = (a.passes & CL_PASS_XMAD) && W.arch == CL_ARCH_SM52;
+                    const unsigned table = match_only ? ((a.passes & CL_PASS_MATCH_XMAD) ? 1u : 0u) : (xm ? 1u : 0u);
+                    if (g.rank == 0 && emit && !mev) f_fail(W, F_REDO + 23);
+                    g.sync();
+                    if (f_oks(g, W)) f_index(g, W, e, table);
+                    f_prof(g, W, PF_USECOUNT);
+                    if (!f_oks(g, W)) leave(false);
+                    else if (match_only) { st = FST_MATCH_ONLY; round = table; }
+                    else if (xm) st = FST_XMAD;
+                    else after_xmad();
+                }
+            }
+        }
+        if (!f_cta_or(st != FST_EMPTY || !exhausted)) break;
+        /* ---- one apply step, all groups together */
+        const bool on = st != FST_EMPTY;
+        const unsigned table = st == FST_XMAD ? 1u : st == FST_MATCH_ONLY ? round : 0u;
+        const uint32_t phase = st == FST_ROUND ? 2 + round : 0u;
+        uint32_t n = f_apply_step(g, W, e, x, on, table, phase, mv, L.mev_cap, st == FST_MATCH_ONLY);
+        /* ---- what the group's state asks for */
+        if (!on) continue;
+        if (!f_oks(g, W)) { leave(false); continue; }
+        if (st == FST_MATCH_ONLY) { leave(true); continue; }
+        if (st == FST_XMAD) {                     /* normalize_xmad (patterns.py:805-810): one round, then dead code */
+            f_dce(g, W);
+            if ((a.passes & (CL_PASS_AGGREGATE | CL_PASS_RECIPROCAL)) && f_oks(g, W)) f_reclass(g, W, e, 0);
+            f_prof(g, W, PF_DCE);
+            if (!f_oks(g, W)) { leave(false); continue; }
+            after_xmad();
+            continue;
+        }
+        /* apply_aggregations (patterns.py:794-802): up to max_rounds of (_apply_patterns + simplify_packs) */
+        n += f_simplify(g, W, e);
+        f_prof(g, W, PF_SIMPLIFY);
+        if (!f_oks(g, W)) { leave(false); continue; }
+        round++;
+        if (!n || round >= a.max_rounds) finish();
     }
     if (g.rank == 0) {
         a_add64(&a.stats[64], n_in); a_add64(&a.stats[65], n_out); a_add64(&a.stats[66], n_ev);
