@@ -848,7 +848,9 @@ struct cl_ctx {
     int stream_mode = cls_default_mode();   /* 1: the production post-SSA stage runs as corpus-wide streaming passes (stream.cuh); 0: tile kernels */
     cls_ctx *cls = nullptr; bool used_stream = false;
     /* the function-resident path (fused.cuh): default for the post-SSA stage */
-    int fused_mode = 1; clf_ctx *clf = nullptr; bool fused_ok = false, used_fused = false;
+    int fused_mode = -1;       /* 1: every post-SSA run, 0: never, -1: the runs that ask for match lists (emit_matches, MATCH_ONLY): there the tile
+                                  kernel cannot serve and the fused kernels are the production path; plain runs take the tile kernel (faster, measured) */
+    clf_ctx *clf = nullptr; bool fused_ok = false, used_fused = false;
     DenseArgs dense{}; bool have_dense = false;     /* dense result of the last run (device) */
     uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
     int warp_sync = 33;
@@ -903,7 +905,6 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
     if (const char *e = getenv("CL_STREAM")) c->stream_mode = atoi(e) != 0;
     if (const char *e = getenv("CL_FUSED")) c->fused_mode = atoi(e) != 0;
-    if (getenv("CL_STREAM") || getenv("CL_TILE")) { if (!getenv("CL_FUSED")) c->fused_mode = 0; }   /* an explicitly selected older path */
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 7;
     if (const char *e = getenv("CL_GTILE_WARPS")) { const int v = atoi(e); c->gtile_warps = (v == 8 || v == 32) ? v : 16; }
     if (const char *e = getenv("CL_TILE_LONG")) c->tile_long = atoi(e) != 0;
@@ -1087,7 +1088,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     /* tiles: small functions without overflow slots, by size class, packed in size order */
     for (auto &t : c->tc) t.tiles.clear();
     c->tile_flist.clear(); c->rest.clear(); c->big_rest.clear(); c->n_tile_funcs = 0;
-    if (!c->stream_mode && !(c->fused_mode && (c->fused_ok || !c->have_pb))) {       /* the streaming and the fused path need no host-side plan */
+    if (!c->stream_mode && !(c->fused_mode == 1 && (c->fused_ok || !c->have_pb))) {       /* the streaming and the fused path need no host-side plan */
         struct Need { uint32_t I, V, Q, B, f; };
         /* tile size by corpus size: the bigger the tile the better the passes amortise (profiles/r01_tuning.md),
          * as long as there are a few tiles per SM                                                              */
@@ -1392,7 +1393,8 @@ static int run(cl_ctx *c, KArgs k) {
     bool use_stream = c->stream_mode && c->F && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
     for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_stream = use_stream && c->h_pb.p[pi].join_ok;
     c->used_stream = use_stream;
-    const bool use_fused = c->fused_mode && c->fused_ok && c->F && !k.raw_passes;
+    const bool wants_lists = k.emit_matches || (k.passes & CL_PASS_MATCH_ONLY);
+    const bool use_fused = c->fused_ok && c->F && !k.raw_passes && (c->fused_mode == 1 || (c->fused_mode == -1 && wants_lists));
     c->used_fused = use_fused;
     if (use_fused) {
         /* one function resident in shared memory per group (fused.cuh); hand-backs and everything too
