@@ -238,9 +238,7 @@ def main():
         wall = time.perf_counter() - t1
     st = eng.stats()
     part = eng.debug_partition() or {}
-    if os.environ.get("CL_PROF") and rank == 0 and part.get("tile_mode") == 8:
-        print("stream phases (ms, last step):", eng.debug_stream_profile(), file=sys.stderr)
-    elif os.environ.get("CL_PROF") and rank == 0:
+    if os.environ.get("CL_PROF") and rank == 0:
         prof = eng.debug_profile()
         tot = max(prof.get("total", 1), 1)
         print("phase cycles (share of group time):", {k: round(v / tot, 3) for k, v in prof.items() if v}, file=sys.stderr)

@@ -148,7 +148,23 @@ class Engine:
 
     def set_patterns(self, aggregation=None, xmad=None, budget=50_000):
         self._blob = compile_patterns(aggregation, xmad, budget)
+        self._tables = (list(aggregation) if aggregation is not None else None, list(xmad) if xmad is not None else None)
         self._check(self.lib.cl_set_patterns(self._ctx, _ptr(self._blob), self._blob.nbytes))
+
+    def pattern_blob(self):
+        """The compiled table the device holds (``restore_patterns`` puts it back)."""
+        return self._blob, self._tables
+
+    def restore_patterns(self, saved):
+        self._blob, self._tables = saved
+        self._check(self.lib.cl_set_patterns(self._ctx, _ptr(self._blob), self._blob.nbytes))
+
+    def pattern_names(self):
+        """Names of the device table's patterns in table order (aggregation, then xmad): what a
+        CL_EV_REFUSED / CL_EV_MATCH event's pattern index refers to."""
+        from .patterns import AGGREGATION_PATTERNS, XMAD_PATTERNS
+        agg, xm = self._tables
+        return [p.name for p in (AGGREGATION_PATTERNS if agg is None else agg)] + [p.name for p in (XMAD_PATTERNS if xm is None else xm)]
 
     def set_threads(self, n: int):
         self._check(self.lib.cl_set_threads(self._ctx, n))
@@ -225,21 +241,6 @@ class Engine:
         self.lib.cl_debug_profile(self._ctx, buf, 16)
         return dict(zip(self.PROFILE_SLOTS, (int(x) for x in buf)))
 
-    STREAM_SLOTS = ("load", "usecount", "seed", "items", "budget", "unify", "select", "selscan", "plan", "bases", "mark",
-                    "permute", "stage", "simplify", "dce", "recip", "tag", "store", "gate")
-
-    def debug_stream_profile(self):
-        """Milliseconds per phase of the streaming path's last run and its fixpoint iteration counts."""
-        if not hasattr(self.lib, "cl_debug_stream_profile"):
-            return {}
-        buf = (C.c_ulonglong * 24)()
-        it = (C.c_uint32 * 4)()
-        self.lib.cl_debug_stream_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
-        if not self.lib.cl_debug_stream_profile(self._ctx, buf, 24, it):
-            return {}
-        d = {k: round(int(v) / 1e6, 3) for k, v in zip(self.STREAM_SLOTS, buf)}
-        d["iters"] = {"select": int(it[0]), "dce": int(it[1]), "rounds": int(it[2])}
-        return d
 
     def debug_partition(self):
         """{tiles, tile_funcs, handed_back, outside, used_tiles} of the last run (CUDA / sim builds only)."""

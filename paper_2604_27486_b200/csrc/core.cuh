@@ -400,7 +400,8 @@ CLN void push_event(FS &s, uint32_t seq, uint32_t kind, uint32_t idx, uint32_t a
     if (k < s.cap.E) {
         cl_event e; e.func = s.f; e.seq = seq; e.kind = kind; e.idx = idx; e.a = a; e.b = b; e.c = c; e.d = d;
         s.ev[k] = e;
-    }
+    } else
+        fail(s, CL_ST_CAPACITY);            /* never a silently shortened event list: the function reports CapacityError */
 }
 
 /* ------------------------------------------------------------------ def-use */

@@ -14,7 +14,6 @@
 #include "core.cuh"
 #include "tile.cuh"
 #include "kargs.h"
-#include "stream.h"
 #include "fused.h"
 
 #include <algorithm>
@@ -346,99 +345,11 @@ template <class G> CLF void group_loop(const G &g, const KArgs &a, uint32_t *gw,
     }
 }
 
-#ifndef CL_WARP_CTAS_PER_SM
-/* Measured on B200 (profiles/r01_tuning.md): the stage is latency bound, so
- * throughput follows resident warps.  64 warps/SM with the work arrays in
- * L1/L2-resident scratch beat every shared-memory placement tried (those cap
- * occupancy and pay a retry when a function outgrows its slice).            */
-#define CL_WARP_CTAS_PER_SM 16      /* warp-group kernel: resident CTAs (4 warps each) per SM */
-#endif
-#ifndef CL_WARP_HOT_BYTES
-#define CL_WARP_HOT_BYTES 0
-#endif
 #ifndef CL_CTA_CTAS_PER_SM
 #define CL_CTA_CTAS_PER_SM 8
 #endif
-#ifndef CL_CTA_HOT_BYTES
-#define CL_CTA_HOT_BYTES 0
-#endif
 #if CL_CUDA
-/* one THREAD per function (32 independent functions per warp).  The stage is
- * a branchy scalar program per function; giving every lane its own function
- * keeps all lanes busy and puts ~300k functions in flight, which hides the
- * latency that bounds the group kernels (profiles/r01_tuning.md).  A warp
- * takes 32 list entries at a time, each lane computes its function in private
- * scratch, then the warp reserves the output space with one atomic per stream. */
-#ifndef CL_THREAD_CTAS_PER_SM
-#define CL_THREAD_CTAS_PER_SM 8
-#endif
-__global__ void __launch_bounds__(128, CL_THREAD_CTAS_PER_SM) k_postssa_thread(KArgs a) {
-    const uint32_t lane = threadIdx.x & 31u;
-    Grp<0> g; g.rank = 0; g.size = 1; g.red = nullptr;
-    uint32_t gw[GW__N];
-    unsigned long long prof[PF__N];
-    for (int k = 0; k < GW__N; k++) gw[k] = 0;
-    for (int k = 0; k < PF__N; k++) prof[k] = 0;
-    const unsigned long long t_begin = now();
-    FS s;
-    setup_fs(s, a, gw, prof, true);
-    uint8_t *cold = a.scratch + (size_t)(blockIdx.x * blockDim.x + threadIdx.x) * a.scratch_per_group;
-    unsigned long long n_in = 0, n_out = 0, n_evs = 0;
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(a.work_counter, 32u);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (base >= a.n_list) break;
-        const uint32_t w = base + lane;
-        bool have = w < a.n_list;
-        uint32_t f = 0;
-        if (have) {
-            f = a.list[w];
-            uint32_t saved[64];
-            for (int k = 0; k < 64; k++) saved[k] = gw[GW_STATS + k];
-            have = compute_function(g, s, a, f, nullptr, cold);
-            if (!have) for (int k = 0; k < 64; k++) gw[GW_STATS + k] = saved[k];
-        }
-        __syncwarp();
-        /* warp-aggregated reservation of the four output streams */
-        uint32_t sz[4] = { have ? s.n : 0u, have ? s.n_imm : 0u, have ? s.next_vid : 0u, have ? events_of(s) : 0u };
-        uint32_t at[4];
-        for (int q = 0; q < 4; q++) {
-            uint32_t v = sz[q];
-            for (int d = 1; d < 32; d <<= 1) { const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, d); if (lane >= (uint32_t)d) v += t; }
-            uint32_t start = 0;
-            if (lane == 31) start = (uint32_t)atomicAdd(&a.cursor[q], (unsigned long long)v);
-            start = __shfl_sync(0xFFFFFFFFu, start, 31);
-            at[q] = start + v - sz[q];
-        }
-        if (have) {
-            store_function_at(g, s, a, f, at[0], at[1], at[2], at[3]);
-            const uint32_t b0 = a.in.func_blk_off[f], b1 = a.in.func_blk_off[f + 1];
-            n_in += a.in.blk_off[b1] - a.in.blk_off[b0];
-            n_out += s.n; n_evs += *s.n_ev;
-        }
-        __syncwarp();
-    }
-    /* counters: reduce over the warp, one atomic per counter per warp */
-    prof[PF_TOTAL] = now() - t_begin;
-    for (int k = 0; k < 64 + 3 + PF__N; k++) {
-        unsigned long long v = k < 64 ? gw[GW_STATS + k] : k == 64 ? n_in : k == 65 ? n_out : k == 66 ? n_evs : prof[k - 67];
-        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
-        if (lane == 0 && v) atomicAdd(k < 67 ? &a.stats[k] : &a.prof[k - 67], v);
-    }
-}
-
-/* one warp per function: 4 independent groups per CTA                        */
-template <int WARPS> __global__ void __launch_bounds__(WARPS * 32, CL_WARP_CTAS_PER_SM) k_postssa_warp(KArgs a) {
-    extern __shared__ uint4 dyn_smem[];
-    __shared__ uint32_t gw[WARPS][GW__N];
-    const uint32_t w = threadIdx.x >> 5;
-    Grp<1> g; g.rank = threadIdx.x & 31u; g.size = 32; g.red = nullptr;
-    const uint32_t gid = blockIdx.x * WARPS + w;
-    uint8_t *hot = a.hot_bytes ? (uint8_t *)dyn_smem + (size_t)w * a.hot_bytes : nullptr;
-    group_loop(g, a, gw[w], hot, a.scratch + (size_t)gid * a.scratch_per_group);
-}
-/* Phase-synchronous variant of the warp-group kernel.  ncu on the free-running
+/* Phase-synchronous warp-group kernel (the general per-function fallback for small functions).  ncu on the free-running
  * kernel shows 89 % of the warp cycles stalled on instruction fetch: the stage
  * is ~300 KB of straight code and 64 warps per SM, each in a different phase of
  * a different function, thrash the instruction cache.  Here the warps of a CTA
@@ -626,20 +537,6 @@ template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, 
     t_setup(g, P, a.pb);
     tile_loop(g, T, P, a, blockIdx.x);
 }
-/* every warp of the CTA is a group with its own tile */
-template <class C, int WARPS, int MINB> __global__ void __launch_bounds__(WARPS * 32, MINB) k_postssa_wtile(KArgs a) {
-    extern __shared__ uint4 dyn_smem[];
-    TileP &P = *(TileP *)dyn_smem;
-    const uint32_t w = threadIdx.x >> 5;
-    TileS<C> &T = *(TileS<C> *)((uint8_t *)dyn_smem + tile_p_bytes() + (size_t)w * ((sizeof(TileS<C>) + 15) & ~(size_t)15));
-    {
-        Grp<WARPS> gc; gc.rank = threadIdx.x; gc.size = WARPS * 32; gc.red = T.red;     /* warp 0's words: only rank 0 .. */
-        gc.red = ((TileS<C> *)((uint8_t *)dyn_smem + tile_p_bytes()))->red;
-        t_setup(gc, P, a.pb);
-    }
-    Grp<1> g; g.rank = threadIdx.x & 31u; g.size = 32; g.red = nullptr;
-    tile_loop(g, T, P, a, blockIdx.x * WARPS + w);
-}
 /* big tiles resident in L2 (global scratch): a CTA is one group; scratch = stages, events, the tile, a second stream buffer */
 template <class C> CLHD size_t gtile_scratch_bytes() {
     return tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255) + (((size_t)128 * C::I + 255) & ~(size_t)255);
@@ -653,21 +550,6 @@ template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, 
     g.red = red;
     t_setup(g, P, a.pb);
     tile_loop(g, T, P, a, blockIdx.x, base + tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255));
-}
-/* experiment: the same warp tiles with the tile state in L2-resident scratch instead of shared
- * memory (more warps in flight, longer access latency)                                       */
-template <class C, int WARPS, int MINB> __global__ void __launch_bounds__(WARPS * 32, MINB) k_postssa_wtile_g(KArgs a) {
-    __shared__ TileP P;
-    __shared__ uint32_t red[40];
-    const uint32_t w = threadIdx.x >> 5, group = blockIdx.x * WARPS + w;
-    uint8_t *base = a.tile_scratch + (size_t)group * a.tile_scratch_per_cta;
-    TileS<C> &T = *(TileS<C> *)(base + tile_scratch_bytes<C>());
-    {
-        Grp<WARPS> gc; gc.rank = threadIdx.x; gc.size = WARPS * 32; gc.red = red;
-        t_setup(gc, P, a.pb);
-    }
-    Grp<1> g; g.rank = threadIdx.x & 31u; g.size = 32; g.red = nullptr;
-    tile_loop(g, T, P, a, group);
 }
 #endif
 
@@ -823,43 +705,31 @@ struct cl_ctx {
     unsigned long long *d_cursor = nullptr, *d_stats = nullptr, *d_prof = nullptr;
     unsigned long long h_prof[PF__N] = { 0 };
     unsigned long long h_cursor[CUR__N] = { 0, 0, 0, 0 };
-    Part part[3];              /* 0 = warp groups, 1 = CTA groups, 2 = one thread per function */
+    Part part[2];              /* general per-function kernels: 0 = warp groups (small functions), 1 = CTA groups (large ones) */
     uint32_t *d_retry_list = nullptr, *d_retry_count = nullptr, *d_retry_counter = nullptr;
-    /* tile kernels (tile.cuh): small functions packed into shared-memory tiles, in two size classes:
-     * [0] warp tiles (one warp per tile), [1] CTA tiles                                        */
-    int tile_mode = -1;        /* bit 0: warp tiles (smem), bit 1: CTA tiles (smem), bit 2: big CTA tiles (L2); 0 = general kernels only;
-                                  -1 = by corpus size: big tiles when they keep every SM busy, else shared-memory CTA tiles */
-    int tile_warps = 16;       /* warps of a CTA-tile group */
-    int wtile_warps = 6;       /* warp tiles (= warps) per CTA */
-    int wtile_global = 0;      /* experiment: > 0 = warp tiles resident in global scratch, this many CTAs of 8 warps per SM */
+    /* tile kernels (tile.cuh): small functions packed into tiles, one CTA per tile */
+    int tile_mode = -1;        /* bit 1: shared-memory tiles (small corpora), bit 2: big tiles resident in L2; 0 = general kernels only;
+                                  -1 = by corpus size: big tiles when they keep every SM busy, else shared-memory tiles */
     struct TileClass {
         std::vector<TileDesc> tiles;
         TileDesc *d_tiles = nullptr; uint32_t *d_counter = nullptr; uint8_t *d_scratch = nullptr;
         size_t scratch_per_group = 0; uint32_t grid = 0, groups = 0;
-    } tc[3];                   /* [2]: big CTA tiles resident in L2 (global scratch) */
-    int gtile_warps = 32, gtile_ctas = 1, gtile_cfg = -1;    /* cfg 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
+    } tc[3];                   /* [1]: shared-memory tiles, [2]: big tiles resident in L2 (global scratch); [0] unused */
+    int gtile_cfg = -1;        /* 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
     int tile_mode_env = -1, gtile_cfg_env = -1;
-    int tile_long = 0;         /* 1: long-block kernels (above small_max records) also go into the big tiles (measured: no gain over the CTA-group kernel) */
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest, big_rest; /* small / large functions that are not in a tile */
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr, *d_big_rest = nullptr;
     uint32_t *d_retry_big = nullptr, *d_retry_big_count = nullptr, *d_retry_big_counter = nullptr;   /* large functions the tile kernel hands back */
     uint32_t n_tile_funcs = 0, h_retry = 0, n_launches = 0; bool used_tiles = false;
-    int stream_mode = cls_default_mode();   /* 1: the production post-SSA stage runs as corpus-wide streaming passes (stream.cuh); 0: tile kernels */
-    cls_ctx *cls = nullptr; bool used_stream = false;
     /* the function-resident path (fused.cuh): default for the post-SSA stage */
     int fused_mode = -1;       /* 1: every post-SSA run, 0: never, -1: the runs that ask for match lists (emit_matches, MATCH_ONLY): there the tile
                                   kernel cannot serve and the fused kernels are the production path; plain runs take the tile kernel (faster, measured) */
     clf_ctx *clf = nullptr; bool fused_ok = false, used_fused = false;
     DenseArgs dense{}; bool have_dense = false;     /* dense result of the last run (device) */
-    uint32_t thread_max = 0;   /* records: thread-per-function kernel up to here (0 = off: measured slower) */
-    int warp_sync = 33;
-    int cta_warps = 8;         /* warps per CTA of the CTA-group kernel (8, 16 or 32) */        /* warps per CTA of the phase-synchronous warp kernel (0 = free-running kernel) */
-    int thread_ctas = 8;
     cl_stats stats{};
     float last_ms = 0;
-    uint32_t small_max = 512;
-    int warp_ctas = CL_WARP_CTAS_PER_SM, cta_ctas = CL_CTA_CTAS_PER_SM;   /* resident CTAs per SM actually launched */  /* records: warp-group kernel up to here          */
+    uint32_t small_max = 512;  /* records: warp-group kernel up to here, CTA-group kernel above */
 };
 
 template <class T> static int dget(cl_ctx *c, int id, T **p, size_t n) {
@@ -899,23 +769,10 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
 #endif
-    if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* tuning knobs */
-    if (const char *e = getenv("CL_THREAD_MAX")) c->thread_max = CL_CUDA ? (uint32_t)atoi(e) : 0;
-    if (const char *e = getenv("CL_WARP_SYNC")) { const int v = atoi(e); c->warp_sync = (v == 0 || v == 8 || v == 16 || v == 32 || v == 33) ? v : 32; }
-    if (const char *e = getenv("CL_CTA_WARPS")) { const int v = atoi(e); c->cta_warps = (v == 16 || v == 32) ? v : 8; }
-    if (const char *e = getenv("CL_STREAM")) c->stream_mode = atoi(e) != 0;
+    if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* the few knobs the tests and the tuning log use */
     if (const char *e = getenv("CL_FUSED")) c->fused_mode = atoi(e) != 0;
-    if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 7;
-    if (const char *e = getenv("CL_GTILE_WARPS")) { const int v = atoi(e); c->gtile_warps = (v == 8 || v == 32) ? v : 16; }
-    if (const char *e = getenv("CL_TILE_LONG")) c->tile_long = atoi(e) != 0;
+    if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 6;
     if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(2, std::max(0, atoi(e)));
-    if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(4, std::max(1, atoi(e)));
-    if (const char *e = getenv("CL_TILE_WARPS")) { const int v = atoi(e); c->tile_warps = (v == 8 || v == 32) ? v : 16; }
-    if (const char *e = getenv("CL_WTILE_GLOBAL")) c->wtile_global = std::min(8, std::max(0, atoi(e)));
-    if (const char *e = getenv("CL_WTILE_WARPS")) c->wtile_warps = std::min(6, std::max(1, atoi(e)));
-    if (const char *e = getenv("CL_THREAD_CTAS")) c->thread_ctas = std::max(1, atoi(e));
-    if (const char *e = getenv("CL_WARP_CTAS")) c->warp_ctas = std::min(CL_WARP_CTAS_PER_SM, std::max(1, atoi(e)));
-    if (const char *e = getenv("CL_CTA_CTAS")) c->cta_ctas = std::min(CL_CTA_CTAS_PER_SM, std::max(1, atoi(e)));
     void *p = nullptr;
     if (dmalloc(&p, sizeof(H_OPFLAGS))) { delete c; return -1; }
     c->d_opflags = (uint8_t *)p;
@@ -938,7 +795,6 @@ extern "C" void cl_destroy(cl_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
 #endif
-    cls_destroy(c->cls);
     clf_destroy(c->clf);
     for (DBuf &b : c->buf) dfree(b.p);
     dfree(c->d_opflags); dfree(c->d_pb); dfree(c->d_cursor); dfree(c->d_stats);
@@ -1020,20 +876,21 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     d.modsets = dms;
     d.val_origin = nullptr;
 
-    /* work partition (while the copies are in flight): one thread per tiny function,
-     * one warp per small one, one CTA per large one                                   */
-    uint32_t n_max[3] = { 0, 0, 0 }, nv_max[3] = { 0, 0, 0 }, nb_max[3] = { 0, 0, 0 }, imm_max[3] = { 0, 0, 0 },
-             blk_max[3] = { 0, 0, 0 }, ext_max[3] = { 0, 0, 0 };
+    /* work partition of the general per-function kernels (while the copies are in flight): one warp per
+     * small function, one CTA per large one.  A counting sort by record count replaces round 1's three
+     * comparison sorts (same purpose: a CTA's batch of functions has one size, long poles first).       */
+    uint32_t n_max[2] = { 0, 0 }, nv_max[2] = { 0, 0 }, nb_max[2] = { 0, 0 }, imm_max[2] = { 0, 0 }, blk_max[2] = { 0, 0 }, ext_max[2] = { 0, 0 };
     for (Part &p : c->part) p.list.clear();
-    std::vector<std::pair<uint32_t, uint32_t>> big, tiny, mid;
+    std::vector<uint32_t> small_cnt(2 * ((size_t)c->small_max + 2), 0);
+    std::vector<std::pair<uint32_t, uint32_t>> big;
     for (uint32_t f = 0; f < F; f++) {
         const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
         const uint32_t n = in->blk_off[b1] - in->blk_off[b0];
         if (in->val_off[f + 1] - in->val_off[f] != in->func[f].next_vid)
             FAIL("function %u: value region holds %u entries, next_vid is %u", f, in->val_off[f + 1] - in->val_off[f], in->func[f].next_vid);
-        const int k = (c->thread_max && n <= c->thread_max) ? 2 : n <= c->small_max ? 0 : 1;     /* thread_max 0: no thread kernel, record-less functions included */
-        if (k == 1) big.emplace_back(~n, f); else if (k == 2) tiny.emplace_back(n, f);
-        else mid.emplace_back((in->func[f].arch == CL_ARCH_SM52 ? 0u : 0x80000000u) | (0x7FFFFFFFu - n), f);   /* by arch (sm52 runs an extra pass), then size */
+        const int k = n <= c->small_max ? 0 : 1;
+        if (k == 1) big.emplace_back(~n, f);
+        else small_cnt[(in->func[f].arch == CL_ARCH_SM52 ? 0u : c->small_max + 1) + (c->small_max - n)]++;      /* by arch (sm52 runs an extra pass), then size, largest first */
         n_max[k] = std::max(n_max[k], n);
         nv_max[k] = std::max(nv_max[k], in->func[f].next_vid);
         nb_max[k] = std::max(nb_max[k], b1 - b0);
@@ -1042,45 +899,30 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         if (b1 - b0 == 1) blk_max[k] = std::max(blk_max[k], n);
         else for (uint32_t b = b0; b < b1; b++) blk_max[k] = std::max(blk_max[k], in->blk_off[b + 1] - in->blk_off[b]);
     }
-    std::sort(big.begin(), big.end());            /* long poles first */
+    std::sort(big.begin(), big.end());            /* long poles first (a handful of functions) */
     for (auto &pr : big) c->part[1].list.push_back(pr.second);
-    std::sort(mid.begin(), mid.end());            /* a CTA's batch of functions has one size: short barrier waits */
-    for (auto &pr : mid) c->part[0].list.push_back(pr.second);
-    std::sort(tiny.begin(), tiny.end());          /* the 32 lanes of a warp get functions of one size */
-    for (auto &pr : tiny) c->part[2].list.push_back(pr.second);
-    /* the warp kernel also takes what outgrows the thread kernel's tight scratch */
-    if (!c->part[2].list.empty()) {
-        n_max[0] = std::max(n_max[0], n_max[2]); nv_max[0] = std::max(nv_max[0], nv_max[2]); nb_max[0] = std::max(nb_max[0], nb_max[2]);
-        imm_max[0] = std::max(imm_max[0], imm_max[2]); blk_max[0] = std::max(blk_max[0], blk_max[2]); ext_max[0] = std::max(ext_max[0], ext_max[2]);
+    {
+        uint32_t run = 0;
+        for (uint32_t &x : small_cnt) { const uint32_t t = x; x = run; run += t; }
+        c->part[0].list.resize(run);
+        for (uint32_t f = 0; f < F; f++) {
+            const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
+            if (n <= c->small_max) c->part[0].list[small_cnt[(in->func[f].arch == CL_ARCH_SM52 ? 0u : c->small_max + 1) + (c->small_max - n)]++] = f;
+        }
     }
-    for (int k = 0; k < 3; k++) {
+    for (int k = 0; k < 2; k++) {
         Part &p = c->part[k];
-        if (p.list.empty() && !(k == 0 && !c->part[2].list.empty())) continue;
-        if (k == 2) {
-            /* tight: a function that grows past this is re-run by the warp kernel */
-            Caps t;
-            const uint32_t n = n_max[2];
-            t.I = n + n / 2 + 32; t.V = nv_max[2] + n + 32; t.B = nb_max[2] + 1; t.M = 2 * n + 64; t.S = n / 2 + 16;
-            t.Q = imm_max[2] + n + 32; t.E = n + 32; t.U = 6 * t.I + ext_max[2]; t.X = n / 2 + 16;
-            p.cap = t;
-        } else
-            p.cap = caps_for(n_max[k], nv_max[k], nb_max[k], imm_max[k], blk_max[k], ext_max[k]);
+        if (p.list.empty()) continue;
+        p.cap = caps_for(n_max[k], nv_max[k], nb_max[k], imm_max[k], blk_max[k], ext_max[k]);
         p.scratch_per_group = (scratch_bytes(p.cap) + 255) & ~(size_t)255;
+        p.hot_bytes = 0;
 #if CL_CUDA
-        const size_t n_work = std::max<size_t>(p.list.size(), k == 0 ? c->part[2].list.size() / 8 + 1 : 0);
-        if (k == 0 && c->warp_sync) {
-            const int wpc = c->warp_sync == 33 ? 32 : c->warp_sync;                      /* warps per CTA */
-            p.hot_bytes = 0;
-            p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * (c->warp_sync == 33 ? 1 : 64 / wpc), (n_work + wpc - 1) / wpc);
-            p.n_groups = p.grid * wpc;
-        } else if (k == 0) { p.hot_bytes = CL_WARP_HOT_BYTES; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->warp_ctas, (n_work + 3) / 4); p.n_groups = p.grid * 4; }
-        else if (k == 1) { p.hot_bytes = 0; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * std::min(c->cta_ctas, 64 / c->cta_warps), p.list.size()); p.n_groups = p.grid; }
-        else { p.hot_bytes = 0; p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->thread_ctas, (p.list.size() + 127) / 128); p.n_groups = p.grid * 128; }
+        if (k == 0) { p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, (p.list.size() + 31) / 32); p.n_groups = p.grid * 32; }      /* 32 warps per CTA, one CTA per SM */
+        else { p.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * CL_CTA_CTAS_PER_SM, p.list.size()); p.n_groups = p.grid; }
 #else
-        p.hot_bytes = 0; p.grid = 1; p.n_groups = 1;
+        p.grid = 1; p.n_groups = 1;
 #endif
-        static const int LIST_ID[3] = { B_LIST0, B_LIST1, B_LIST2 }, CNT_ID[3] = { B_COUNTER0, B_COUNTER1, B_COUNTER2 },
-                         SCR_ID[3] = { B_SCRATCH0, B_SCRATCH1, B_SCRATCH2 };
+        static const int LIST_ID[2] = { B_LIST0, B_LIST1 }, CNT_ID[2] = { B_COUNTER0, B_COUNTER1 }, SCR_ID[2] = { B_SCRATCH0, B_SCRATCH1 };
         if (dput(c, LIST_ID[k], &p.d_list, p.list.data(), p.list.size())) return -1;
         if (dget(c, CNT_ID[k], &p.d_counter, 1)) return -1;
         if (dget(c, SCR_ID[k], &p.d_scratch, p.scratch_per_group * p.n_groups)) return -1;
@@ -1088,7 +930,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
     /* tiles: small functions without overflow slots, by size class, packed in size order */
     for (auto &t : c->tc) t.tiles.clear();
     c->tile_flist.clear(); c->rest.clear(); c->big_rest.clear(); c->n_tile_funcs = 0;
-    if (!c->stream_mode && !(c->fused_mode == 1 && (c->fused_ok || !c->have_pb))) {       /* the streaming and the fused path need no host-side plan */
+    if (!(c->fused_mode == 1 && (c->fused_ok || !c->have_pb))) {       /* the fused path needs no host-side plan */
         struct Need { uint32_t I, V, Q, B, f; };
         /* tile size by corpus size: the bigger the tile the better the passes amortise (profiles/r01_tuning.md),
          * as long as there are a few tiles per SM                                                              */
@@ -1096,7 +938,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             uint64_t n_small = 0;
             for (uint32_t f = 0; f < F; f++) {
                 const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
-                if (!(c->thread_max && n <= c->thread_max) && (n <= c->small_max || (c->tile_long && tile_icap(n) <= TileCfgG3::I))) n_small += n;
+                if (n <= c->small_max) n_small += n;
             }
             int n_sm = 148;
 #if CL_CUDA
@@ -1112,31 +954,44 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
         const uint32_t gI = gc == 2 ? TileCfgG3::I : gc == 1 ? TileCfgG2::I : TileCfgG::I, gV = gc == 2 ? TileCfgG3::V : gc == 1 ? TileCfgG2::V : TileCfgG::V,
                        gQ = gc == 2 ? TileCfgG3::Q : gc == 1 ? TileCfgG2::Q : TileCfgG::Q, gB = gc == 2 ? TileCfgG3::B : gc == 1 ? TileCfgG2::B : TileCfgG::B,
                        gF = gc == 2 ? TileCfgG3::F : gc == 1 ? TileCfgG2::F : TileCfgG::F;
-        std::vector<Need> cls[3];
-        c->big_rest.clear();
+        /* functions of each tile class in order of decreasing size (counting sort by record count, stable in
+         * function order: the same packing as round 1's stable_sort, without its n log n)                    */
+        std::vector<uint8_t> cls_of(F, 0xFF);
+        std::vector<uint32_t> cnt[3];
+        for (int k = 1; k < 3; k++) cnt[k].assign((size_t)c->small_max + 2, 0);
+        auto need_of = [&](uint32_t f) {
+            const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
+            const uint32_t n = in->blk_off[b1] - in->blk_off[b0];
+            return Need{ tile_icap(n), tile_vcap(in->func[f].next_vid, n), tile_qcap(in->imm_off[f + 1] - in->imm_off[f], n), b1 - b0, f };
+        };
         for (uint32_t f = 0; f < F; f++) {
             const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
             const uint32_t n = in->blk_off[b1] - in->blk_off[b0], nb = b1 - b0;
-            if (c->thread_max && n <= c->thread_max) continue;
             const bool small = n <= c->small_max;
-            const uint32_t nimm = in->imm_off[f + 1] - in->imm_off[f];
-            const Need nd = { tile_icap(n), tile_vcap(in->func[f].next_vid, n), tile_qcap(nimm, n), nb, f };
+            const Need nd = need_of(f);
             const bool plain = in->ext_off[f + 1] == in->ext_off[f] && nb > 0;
-            if (small && plain && (c->tile_mode & 1) && nd.I <= TileCfgW::I && nd.V <= TileCfgW::V && nd.Q <= TileCfgW::Q && nd.B <= TileCfgW::B) cls[0].push_back(nd);
-            else if (small && plain && (c->tile_mode & 2) && nd.I <= TileCfgL::I && nd.V <= TileCfgL::V && nd.Q <= TileCfgL::Q && nd.B <= TileCfgL::B) cls[1].push_back(nd);
-            else if (plain && (small || c->tile_long) && (c->tile_mode & 4) && nd.I <= gI && nd.V <= gV && nd.Q <= gQ && nd.B <= gB) cls[2].push_back(nd);   /* long-block kernels too */
+            int k = -1;
+            if (small && plain && (c->tile_mode & 2) && nd.I <= TileCfgL::I && nd.V <= TileCfgL::V && nd.Q <= TileCfgL::Q && nd.B <= TileCfgL::B) k = 1;
+            else if (small && plain && (c->tile_mode & 4) && nd.I <= gI && nd.V <= gV && nd.Q <= gQ && nd.B <= gB) k = 2;
+            if (k > 0) { cls_of[f] = (uint8_t)k; cnt[k][c->small_max - n]++; }
             else if (small) c->rest.push_back(f);
             else c->big_rest.push_back(f);
         }
-        const uint32_t capI[3] = { TileCfgW::I, TileCfgL::I, gI }, capV[3] = { TileCfgW::V, TileCfgL::V, gV },
-                       capQ[3] = { TileCfgW::Q, TileCfgL::Q, gQ }, capB[3] = { TileCfgW::B, TileCfgL::B, gB },
-                       capF[3] = { TileCfgW::F, TileCfgL::F, gF };
-        for (int k = 0; k < 3; k++) {
-            std::stable_sort(cls[k].begin(), cls[k].end(), [](const Need &x, const Need &y) { return x.I > y.I; });    /* long poles first */
+        const uint32_t capI[3] = { 0, TileCfgL::I, gI }, capV[3] = { 0, TileCfgL::V, gV }, capQ[3] = { 0, TileCfgL::Q, gQ },
+                       capB[3] = { 0, TileCfgL::B, gB }, capF[3] = { 0, TileCfgL::F, gF };
+        for (int k = 1; k < 3; k++) {
+            uint32_t run = 0;
+            for (uint32_t &x : cnt[k]) { const uint32_t t = x; x = run; run += t; }
+            std::vector<uint32_t> order(run);
+            for (uint32_t f = 0; f < F; f++) if (cls_of[f] == k) {
+                const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
+                order[cnt[k][c->small_max - n]++] = f;
+            }
             TileDesc cur = { (uint32_t)c->tile_flist.size(), 0 };
             uint32_t sI = 0, sV = 0, sQ = 0, sB = 0;
             auto flush = [&]() { if (cur.nf) c->tc[k].tiles.push_back(cur); cur.first = (uint32_t)c->tile_flist.size(); cur.nf = 0; sI = sV = sQ = sB = 0; };
-            for (const Need &nd : cls[k]) {
+            for (const uint32_t f : order) {
+                const Need nd = need_of(f);
                 if (cur.nf && (sI + nd.I > capI[k] || sV + nd.V > capV[k] || sQ + nd.Q > capQ[k] || sB + nd.B > capB[k] || cur.nf >= capF[k])) flush();
                 c->tile_flist.push_back(nd.f);
                 cur.nf++; sI += nd.I; sV += nd.V; sQ += nd.Q; sB += nd.B;
@@ -1158,25 +1013,18 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             cl_ctx::TileClass &t = c->tc[k];
             if (t.tiles.empty()) continue;
 #if CL_CUDA
-            if (k == 0 && c->wtile_global) {
-                t.scratch_per_group = tile_scratch_bytes<TileCfgW>() + ((sizeof(TileS<TileCfgW>) + 255) & ~(size_t)255);
-                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->wtile_global, (t.tiles.size() + 7) / 8);
-                t.groups = t.grid * 8;
-            } else if (k == 0) {
-                t.scratch_per_group = tile_scratch_bytes<TileCfgW>();
-                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, (t.tiles.size() + c->wtile_warps - 1) / c->wtile_warps);
-                t.groups = t.grid * c->wtile_warps;
-            } else if (k == 1) {
+            if (k == 0) continue;
+            if (k == 1) {
                 t.scratch_per_group = tile_scratch_bytes<TileCfgL>();
                 t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, t.tiles.size());
                 t.groups = t.grid;
             } else {
                 t.scratch_per_group = c->gtile_cfg == 2 ? gtile_scratch_bytes<TileCfgG3>() : c->gtile_cfg == 1 ? gtile_scratch_bytes<TileCfgG2>() : gtile_scratch_bytes<TileCfgG>();
-                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->gtile_ctas, t.tiles.size());
+                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, t.tiles.size());
                 t.groups = t.grid;
             }
 #else
-            t.scratch_per_group = k == 0 ? tile_scratch_bytes<TileCfgW>() : k == 1 ? tile_scratch_bytes<TileCfgL>() : tile_scratch_bytes<TileCfgG3>();
+            t.scratch_per_group = k == 1 ? tile_scratch_bytes<TileCfgL>() : tile_scratch_bytes<TileCfgG3>();
             t.grid = t.groups = 1;
 #endif
             if (dput(c, T_ID[k], &t.d_tiles, t.tiles.data(), t.tiles.size())) return -1;
@@ -1238,32 +1086,14 @@ static int launch_part(cl_ctx *c, int which, KArgs k, int mode = 0, bool side = 
              : mode == 2 ? (uint32_t)c->rest.size() : mode == 4 ? (uint32_t)c->big_rest.size() : (uint32_t)p.list.size();
     k.n_list_ptr = mode == 1 ? c->d_retry_count : mode == 3 ? c->d_retry_big_count : nullptr;
     k.work_counter = mode == 1 ? c->d_retry_counter : mode == 3 ? c->d_retry_big_counter : p.d_counter;
-    k.retry_list = which == 2 ? c->d_retry_list : nullptr;
-    k.retry_count = which == 2 ? c->d_retry_count : nullptr;
+    k.retry_list = nullptr; k.retry_count = nullptr;
     (void)retry;
     k.scratch = p.d_scratch; k.scratch_per_group = p.scratch_per_group; k.gcap = p.cap; k.hot_bytes = p.hot_bytes;
     if (dzero(k.work_counter, sizeof(uint32_t), st)) return -1;
     c->n_launches++;
 #if CL_CUDA
-    if (which == 0 && c->warp_sync) {
-        switch (c->warp_sync) {
-        case 33: k_postssa_warp_sync<32, 1><<<p.grid, 1024, 0, st>>>(k); break;     /* 1 CTA/SM, 64 regs */
-        case 32: k_postssa_warp_sync<32, 2><<<p.grid, 1024, 0, st>>>(k); break;
-        case 8: k_postssa_warp_sync<8, 8><<<p.grid, 256, 0, st>>>(k); break;
-        default: k_postssa_warp_sync<16, 4><<<p.grid, 512, 0, st>>>(k); break;
-        }
-    } else if (which == 0) {
-        const size_t smem = (size_t)p.hot_bytes * 4;
-        CUDA_OK(cudaFuncSetAttribute(k_postssa_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_postssa_warp<4><<<p.grid, 128, smem, st>>>(k);
-    } else if (which == 1) {
-        const size_t smem = p.hot_bytes;
-        (void)smem;
-        if (c->cta_warps == 32) k_postssa_cta<32, 2><<<p.grid, 1024, 0, st>>>(k);
-        else if (c->cta_warps == 16) k_postssa_cta<16, 4><<<p.grid, 512, 0, st>>>(k);
-        else k_postssa_cta<8, CL_CTA_CTAS_PER_SM><<<p.grid, 256, 0, st>>>(k);
-    } else
-        k_postssa_thread<<<p.grid, 128, 0, st>>>(k);
+    if (which == 0) k_postssa_warp_sync<32, 1><<<p.grid, 1024, 0, st>>>(k);     /* 1 CTA/SM, 64 registers */
+    else k_postssa_cta<8, CL_CTA_CTAS_PER_SM><<<p.grid, 256, 0, st>>>(k);
     CUDA_OK(cudaGetLastError());
 #else
     static uint32_t gw[GW__N];
@@ -1282,16 +1112,8 @@ template <class C, int NW, int MINB> static int launch_tile_kernel(cl_ctx *c, co
     (void)c;
     return 0;
 }
-template <class C, int WARPS> static int launch_wtile_kernel(cl_ctx *c, const KArgs &k, uint32_t grid, cudaStream_t st) {
-    const size_t smem = tile_p_bytes() + WARPS * ((sizeof(TileS<C>) + 15) & ~(size_t)15);
-    CUDA_OK(cudaFuncSetAttribute(k_postssa_wtile<C, WARPS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_postssa_wtile<C, WARPS, 1><<<grid, WARPS * 32, smem, st>>>(k);
-    CUDA_OK(cudaGetLastError());
-    (void)c;
-    return 0;
-}
 #endif
-/* class 0 (warp tiles) on the main stream, class 1 (CTA tiles) on the side stream */
+/* class 1 (shared-memory tiles) on the side stream, class 2 (big tiles) on the main stream */
 static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     cl_ctx::TileClass &t = c->tc[cls];
     if (t.tiles.empty()) return 0;
@@ -1303,60 +1125,20 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
 #if CL_CUDA
     cudaStream_t st = cls == 1 ? c->stream2 : c->stream;
     if (dzero(k.tile_counter, sizeof(uint32_t), st)) return -1;
-    if (cls == 0 && c->wtile_global) {
-        switch (c->wtile_global) {
-        case 1: k_postssa_wtile_g<TileCfgW, 8, 1><<<t.grid, 256, 0, st>>>(k); break;
-        case 2: k_postssa_wtile_g<TileCfgW, 8, 2><<<t.grid, 256, 0, st>>>(k); break;
-        case 3: k_postssa_wtile_g<TileCfgW, 8, 3><<<t.grid, 256, 0, st>>>(k); break;
-        case 4: k_postssa_wtile_g<TileCfgW, 8, 4><<<t.grid, 256, 0, st>>>(k); break;
-        case 6: k_postssa_wtile_g<TileCfgW, 8, 6><<<t.grid, 256, 0, st>>>(k); break;
-        default: k_postssa_wtile_g<TileCfgW, 8, 8><<<t.grid, 256, 0, st>>>(k); break;
-        }
-        CUDA_OK(cudaGetLastError());
-        return 0;
-    }
-    if (cls == 0) {
-        switch (c->wtile_warps) {
-        case 1: return launch_wtile_kernel<TileCfgW, 1>(c, k, t.grid, st);
-        case 2: return launch_wtile_kernel<TileCfgW, 2>(c, k, t.grid, st);
-        case 3: return launch_wtile_kernel<TileCfgW, 3>(c, k, t.grid, st);
-        case 4: return launch_wtile_kernel<TileCfgW, 4>(c, k, t.grid, st);
-        case 5: return launch_wtile_kernel<TileCfgW, 5>(c, k, t.grid, st);
-        case 6: return launch_wtile_kernel<TileCfgW, 6>(c, k, t.grid, st);
-        case 7: return launch_wtile_kernel<TileCfgW, 7>(c, k, t.grid, st);
-        default: return launch_wtile_kernel<TileCfgW, 8>(c, k, t.grid, st);
-        }
-    }
-    if (cls == 2 && c->gtile_cfg == 2) {
-        if (c->gtile_warps == 32) k_postssa_gtile<TileCfgG3, 32, 1><<<t.grid, 1024, 0, st>>>(k);
-        else k_postssa_gtile<TileCfgG3, 16, 2><<<t.grid, 512, 0, st>>>(k);
-        CUDA_OK(cudaGetLastError());
-        return 0;
-    }
-    if (cls == 2 && c->gtile_cfg == 1) {
-        if (c->gtile_warps == 32) k_postssa_gtile<TileCfgG2, 32, 1><<<t.grid, 1024, 0, st>>>(k);
-        else if (c->gtile_warps == 8) k_postssa_gtile<TileCfgG2, 8, 4><<<t.grid, 256, 0, st>>>(k);
-        else k_postssa_gtile<TileCfgG2, 16, 2><<<t.grid, 512, 0, st>>>(k);
-        CUDA_OK(cudaGetLastError());
-        return 0;
-    }
     if (cls == 2) {
-        if (c->gtile_warps == 32) k_postssa_gtile<TileCfgG, 32, 1><<<t.grid, 1024, 0, st>>>(k);
-        else if (c->gtile_warps == 8) k_postssa_gtile<TileCfgG, 8, 4><<<t.grid, 256, 0, st>>>(k);
-        else k_postssa_gtile<TileCfgG, 16, 2><<<t.grid, 512, 0, st>>>(k);
+        if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        else k_postssa_gtile<TileCfgG, 32, 1><<<t.grid, 1024, 0, st>>>(k);
         CUDA_OK(cudaGetLastError());
         return 0;
     }
-    if (c->tile_warps == 32) return launch_tile_kernel<TileCfgL, 32, 1>(c, k, t.grid, st);
-    if (c->tile_warps == 8) return launch_tile_kernel<TileCfgL, 8, 1>(c, k, t.grid, st);
     return launch_tile_kernel<TileCfgL, 16, 1>(c, k, t.grid, st);
 #else
     if (dzero(k.tile_counter, sizeof(uint32_t), c->stream)) return -1;
     static TileP P;
     Grp<0> g; g.rank = 0; g.size = 1; g.red = nullptr;
     t_setup(g, P, k.pb);
-    if (cls == 0) { static TileS<TileCfgW> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
-    else if (cls == 1) { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    if (cls == 1) { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
     else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; alignas(16) static uint8_t pl[128 * TileCfgG3::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; alignas(16) static uint8_t pl[128 * TileCfgG2::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else { static TileS<TileCfgG> T; alignas(16) static uint8_t pl[128 * TileCfgG::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
@@ -1390,16 +1172,13 @@ static int run(cl_ctx *c, KArgs k) {
     CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
 #endif
     if (c->d_retry_big_count && dzero(c->d_retry_big_count, sizeof(uint32_t), c->stream)) return -1;
-    bool use_stream = c->stream_mode && c->F && !k.raw_passes && !k.emit_matches && !(k.passes & CL_PASS_MATCH_ONLY);
-    for (uint32_t pi = 0; pi < c->h_pb.n_patterns; pi++) use_stream = use_stream && c->h_pb.p[pi].join_ok;
-    c->used_stream = use_stream;
     const bool wants_lists = k.emit_matches || (k.passes & CL_PASS_MATCH_ONLY);
     const bool use_fused = c->fused_ok && c->F && !k.raw_passes && (c->fused_mode == 1 || (c->fused_mode == -1 && wants_lists));
     c->used_fused = use_fused;
     if (use_fused) {
         /* one function resident in shared memory per group (fused.cuh); hand-backs and everything too
          * large for a shared-memory slice (long blocks) go to the general kernels                  */
-        use_stream = false; use_tiles = false; c->used_stream = false;
+        use_tiles = false;
         KArgs kf = k;
         kf.retry_list = c->d_retry_list; kf.retry_count = c->d_retry_count;
         kf.retry_big_list = c->d_retry_big; kf.retry_big_count = c->d_retry_big_count; kf.small_max = c->small_max;
@@ -1407,23 +1186,10 @@ static int run(cl_ctx *c, KArgs k) {
         { unsigned long long info[4]; clf_info(c->clf, info); c->n_launches += (uint32_t)info[0]; }
         if (launch_part(c, 0, k, 1)) return -1;
         if (launch_part(c, 1, k, 3)) return -1;
-    } else if (use_stream) {
-        /* corpus-wide streaming passes; what they hand back (hazards, overflow slots) goes to the general kernels */
-        if (!c->cls && cls_create(&c->cls, c->device, c->n_sm_or_1())) FAIL("cls_create failed");
-        cls_job job;
-        job.k = k;
-        job.retry_list = c->d_retry_list; job.retry_count = c->d_retry_count;
-        job.retry_big_list = c->d_retry_big; job.retry_big_count = c->d_retry_big_count; job.small_max = c->small_max;
-        job.n_inst = c->n_inst; job.n_val = c->n_val; job.n_imm = c->n_imm;
-        c->n_launches++;
-        if (cls_run(c->cls, &job, (void *)(uintptr_t)c->stream, g_err, sizeof g_err)) return -1;
-        if (launch_part(c, 0, k, 1)) return -1;
-        if (launch_part(c, 1, k, 3)) return -1;
     } else if (use_tiles) {
         if (launch_part(c, 1, k, 4, true)) return -1;     /* large functions outside the tiles: side stream */
         if (launch_tiles(c, k, 1)) return -1;    /* CTA tiles: side stream, after the large functions */
         if (launch_tiles(c, k, 2)) return -1;    /* big L2-resident tiles */
-        if (launch_tiles(c, k, 0)) return -1;    /* warp tiles */
         if (launch_part(c, 0, k, 2)) return -1;  /* small functions outside the tiles */
 #if CL_CUDA
         CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
@@ -1433,9 +1199,7 @@ static int run(cl_ctx *c, KArgs k) {
         if (launch_part(c, 1, k, 3)) return -1;
     } else {
         if (launch_part(c, 1, k, 0, true)) return -1;
-        if (launch_part(c, 2, k)) return -1;
         if (launch_part(c, 0, k)) return -1;
-        if (!c->part[2].list.empty() && launch_part(c, 0, k, 1)) return -1; /* what outgrew the thread kernel */
     }
 #if CL_CUDA
     CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
@@ -1444,7 +1208,7 @@ static int run(cl_ctx *c, KArgs k) {
     if (d2h(c->h_cursor, c->d_cursor, sizeof c->h_cursor, c->stream)) return -1;
     if (d2h(&c->stats, c->d_stats, sizeof(cl_stats), c->stream)) return -1;
     if (d2h(c->h_prof, c->d_prof, sizeof c->h_prof, c->stream)) return -1;
-    c->h_retry = 0; c->used_tiles = use_tiles && !use_stream;
+    c->h_retry = 0; c->used_tiles = use_tiles;
     if (c->d_retry_count && d2h(&c->h_retry, c->d_retry_count, sizeof(uint32_t), c->stream)) return -1;
     uint32_t h_retry_big = 0;
     if (c->d_retry_big_count && d2h(&h_retry_big, c->d_retry_big_count, sizeof(uint32_t), c->stream)) return -1;
@@ -1457,7 +1221,7 @@ static int run(cl_ctx *c, KArgs k) {
     if (densify(c)) return -1;             /* the dense result of the ABI is part of the timed stage */
 #if CL_CUDA
     CUDA_OK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
-    c->n_launches += g_aux_launches + (use_stream ? 1u : 0u);      /* every kernel of the run: main, zeroing, densify (streaming: + its init kernel) */
+    c->n_launches += g_aux_launches;      /* every kernel of the run: main, zeroing, densify */
 #endif
     return 0;
 }
@@ -1610,12 +1374,8 @@ extern "C" int cl_debug_profile(cl_ctx *c, unsigned long long *out, int n) {
  * handed back to the general kernel, small functions outside tiles, tile kernel used}            */
 extern "C" int cl_debug_partition(cl_ctx *c, unsigned long long *out) {
     out[0] = c->tc[0].tiles.size() + c->tc[1].tiles.size() + c->tc[2].tiles.size(); out[1] = c->n_tile_funcs; out[2] = c->h_retry; out[3] = c->rest.size(); out[4] = c->used_tiles; out[5] = c->n_launches;
-    out[6] = c->used_fused ? 16 : c->used_stream ? 8 : c->tile_mode; out[7] = c->gtile_cfg;
+    out[6] = c->used_fused ? 16 : c->tile_mode; out[7] = c->gtile_cfg;
     return 0;
-}
-/* debugging aid: nanoseconds per phase of the streaming path's last run + {select, dce, rounds} iteration counts */
-extern "C" int cl_debug_stream_profile(cl_ctx *c, unsigned long long *prof, int n, uint32_t *iters) {
-    return c->cls ? cls_profile(c->cls, prof, n, iters) : 0;
 }
 extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 0; }
 extern "C" int cl_last_run_ms(cl_ctx *c, float *ms) { *ms = c->last_ms; return 0; }

@@ -57,13 +57,11 @@ struct TPat {
 
 /* capacities of one tile (compile time: the tile lives in shared memory) */
 struct TileCfgL { static constexpr bool PP = false; static constexpr uint32_t I = 1024, V = 1792, Q = 320, F = 32, B = 96, M = 1024, S = 512, X = 256, E = 512; };
-struct TileCfgS { static constexpr bool PP = false; static constexpr uint32_t I = 576, V = 1024, Q = 192, F = 24, B = 64, M = 512, S = 288, X = 128, E = 256; };
 /* a big tile resident in L2 (global scratch) instead of shared memory: every pass loops many times over
  * the same code, which is what the instruction cache needs (profiles/r01_tuning.md)          */
 struct TileCfgG { static constexpr bool PP = true; static constexpr uint32_t I = 4096, V = 7168, Q = 1280, F = 128, B = 255, M = 4096, S = 2048, X = 512, E = 2048; };
 struct TileCfgG2 { static constexpr bool PP = true; static constexpr uint32_t I = 8192, V = 14336, Q = 2560, F = 255, B = 255, M = 8192, S = 4096, X = 1024, E = 4096; };
 struct TileCfgG3 { static constexpr bool PP = true; static constexpr uint32_t I = 16384, V = 28672, Q = 5120, F = 255, B = 255, M = 16384, S = 8192, X = 2048, E = 8192; };
-struct TileCfgW { static constexpr bool PP = false; static constexpr uint32_t I = 192, V = 352, Q = 64, F = 3, B = 16, M = 192, S = 96, X = 32, E = 64; };   /* one warp */
 
 /* the pattern table and what t_setup derives from it: shared by the tiles of a CTA */
 struct TileP {

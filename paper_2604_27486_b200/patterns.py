@@ -209,6 +209,7 @@ ALL_PATTERNS = XMAD_PATTERNS + AGGREGATION_PATTERNS
 
 # ---------------------------------------------------------- table -> device blob
 MAX_PATTERNS, MAX_TEMPLATES, MAX_VARS = 16, 3, 16
+MAX_CLS = 12            # seed classes of one table (core.cuh MAX_CLS)
 PATTERN_MAGIC = 0x434C5054
 S_ANY, S_VAR, S_RZ, S_PT, S_IMM = range(5)
 
@@ -381,6 +382,10 @@ def compile_patterns(aggregation=None, xmad=None, budget: int = 50_000) -> np.nd
         if len(pat.templates) != want:
             raise PatternError(f"pattern {pat.name!r}: plan {kind} rewrites {want} "
                                f"instructions, the pattern has {len(pat.templates)}")
+    for table, name in ((0, "aggregation"), (1, "xmad")):
+        bases = {tmpl.base for pat, t in pats if t == table for tmpl in pat.templates}
+        if len(bases) > MAX_CLS:
+            raise PatternError(f"the {name} table uses {len(bases)} distinct template opcodes, the device seed scan holds {MAX_CLS}")
     b["n_groups"] = len(TABLES.groups)
     pos = np.zeros(64, np.uint8)
     for g, choices in reversed(list(enumerate(TABLES.groups))):

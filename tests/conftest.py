@@ -32,25 +32,25 @@ def cuda_engine():
 
 @pytest.fixture(scope="session")
 def sim_tile_engine():
-    """context with the streaming path off: the tile kernels take the production run"""
+    """context whose plain post-SSA runs take the tile kernels (the default; fused only for match lists)"""
     import helpers
-    return helpers.sim_engine(stream=False)
+    return helpers.sim_engine(fused=False)
 
 
 @pytest.fixture(scope="session")
 def cuda_tile_engine():
     import helpers
-    return helpers.cuda_engine(stream=False)
+    return helpers.cuda_engine(fused=False)
 
 
 @pytest.fixture(scope="session")
-def sim_stream_engine():
-    """context with the corpus-wide streaming path on"""
+def sim_fused_engine():
+    """context whose post-SSA runs all take the function-resident fused kernels"""
     import helpers
-    return helpers.sim_engine(stream=True)
+    return helpers.sim_engine(fused=True)
 
 
 @pytest.fixture(scope="session")
-def cuda_stream_engine():
+def cuda_fused_engine():
     import helpers
-    return helpers.cuda_engine(stream=True)
+    return helpers.cuda_engine(fused=True)

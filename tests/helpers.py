@@ -41,12 +41,12 @@ def build_oracle():
 
 def build_sim():
     """One-lane CPU build of the device code (tests/sim): logic checks without a GPU."""
-    srcs = [CSRC / n for n in ("culifter.cu", "stream.cu", "fused.cu", "core.cuh", "tile.cuh", "stream.cuh", "fused.cuh", "stream.h", "fused.h", "kargs.h")]
+    srcs = [CSRC / n for n in ("culifter.cu", "fused.cu", "core.cuh", "tile.cuh", "fused.cuh", "fused.h", "kargs.h")]
     srcs.append(ROOT / "include" / "culifter.h")
     if not SIM_LIB.exists() or any(s.stat().st_mtime > SIM_LIB.stat().st_mtime for s in srcs):
         SIM_LIB.parent.mkdir(parents=True, exist_ok=True)
         subprocess.run(["g++", "-x", "c++", "-std=c++17", "-O1", "-g", "-DCL_SIM", "-fPIC", "-shared",
-                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu"), str(CSRC / "stream.cu"), str(CSRC / "fused.cu")], check=True)
+                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu"), str(CSRC / "fused.cu")], check=True)
     return SIM_LIB
 
 
@@ -69,18 +69,19 @@ def _engine_with_env(path, **env):
                 os.environ[k] = v
 
 
-def sim_engine(stream=None):
-    """stream: True / False selects the streaming or the tile path, None the library's default"""
-    if stream is None:
+def sim_engine(fused=None):
+    """fused: True / False forces the fused or the tile path for every post-SSA run, None the library's default
+    (tile kernel for plain runs, fused kernels for runs that ask for match lists)"""
+    if fused is None:
         return Engine(build_sim())
-    return _engine_with_env(build_sim(), CL_STREAM=int(stream))
+    return _engine_with_env(build_sim(), CL_FUSED=int(fused))
 
 
-def cuda_engine(stream=None):
+def cuda_engine(fused=None):
     # the product library; raises without GPU / without the .so
-    if stream is None:
+    if fused is None:
         return Engine()
-    return _engine_with_env(None, CL_STREAM=int(stream))
+    return _engine_with_env(None, CL_FUSED=int(fused))
 
 
 def state_of(fn):

@@ -101,9 +101,38 @@ def test_pass_requires_ssa_phase(engine):
         passes.apply_aggregations(fn, engine)
 
 
-def test_select_matches_needs_device_list():
-    with pytest.raises(TypeError):
-        passes.select_matches([object()])
+def _mk(pattern, iids, block=0, start=None):
+    class _I:                                    # select_matches only looks at inst.iid
+        def __init__(self, iid): self.iid = iid
+    return patterns.Match(pattern, [_I(i) for i in iids], patterns.Bindings(), block, iids[0] if start is None else start)
+
+
+def test_select_matches_resolves_any_list_like_the_reference():
+    """patterns.py:241-252 on lists the device never saw: caller-built matches, earliest start first,
+    longer pattern on ties, greedy over disjoint instructions, stable for equal keys"""
+    two, three = patterns.AGGREGATION_PATTERNS[0], patterns.AGGREGATION_PATTERNS[4]
+    a, b, c, d = _mk(two, [5, 9]), _mk(three, [5, 6, 7]), _mk(two, [1, 9]), _mk(two, [20, 21])
+    assert passes.select_matches([a, b, c, d]) == [c, b, d]       # c starts first and takes 9; b beats a at 5 (longer)
+    assert passes.select_matches([d, a]) == [a, d]
+    assert passes.select_matches([]) == []
+
+
+def test_select_matches_on_a_filtered_device_list(engine):
+    """the device's precomputed selection is only used for the unmodified list; dropping a competitor
+    before the call lets the match it had beaten win, as in the reference"""
+    fn = bundled("carrysub")
+    blk = max(fn.block_order(), key=lambda b: len(b.instructions))
+    ms = passes.match_patterns(fn, blk, patterns.AGGREGATION_PATTERNS, engine=engine)
+    full = passes.select_matches(ms)
+    assert full == [m for m in sorted(ms, key=lambda m: (m.start_pos, -len(m.pattern))) if m in full]
+    if len(ms) > 1:
+        rest = ms[1:]
+        want, taken = [], set()
+        for m in sorted(rest, key=lambda m: (m.start_pos, -len(m.pattern))):
+            ids = {i.iid for i in m.insts}
+            if not ids & taken:
+                taken |= ids; want.append(m)
+        assert passes.select_matches(rest) == want
 
 
 def test_pattern_introspection_lists_all():                # test_patterns.py:257
@@ -130,3 +159,26 @@ def test_custom_pattern_table_runs_on_device(engine):
     ms = passes.match_patterns(fn, blk, only_wide, engine=engine)
     assert len(ms) == 3 and {m.pattern.name for m in ms} == {"imad.wide"}
     assert passes.select_matches(ms) == ms
+
+
+def test_match_patterns_keeps_the_engines_own_tables(engine):
+    """match_patterns swaps a table in for one call and puts the engine's previous one back (custom tables too)"""
+    only_wide = [p for p in patterns.AGGREGATION_PATTERNS if p.name == "imad.wide"]
+    engine.set_patterns(only_wide, [])
+    try:
+        fn = bundled("fastdiv")
+        passes.match_patterns(fn, fn.block_order()[1], patterns.AGGREGATION_PATTERNS, engine=engine)
+        assert engine.pattern_names() == ["imad.wide"]
+        passes.apply_aggregations(fn, engine)
+        assert "IMAD64" in bases(fn) and "IADD364" not in bases(fn)
+    finally:
+        engine.set_patterns()
+
+
+def test_too_many_seed_opcodes_is_a_pattern_error():
+    """the device seed scan holds 12 distinct template opcodes per table: more is refused at compile time"""
+    ops = ["FADD", "FMUL", "FFMA", "IADD3", "IADD", "ISETP", "LEA", "IMAD", "SHF", "MOV", "LOP3", "SEL", "PRMT"]
+    table = [patterns.Pattern(f"p{k}", (patterns.InstTemplate(op, defs=(patterns.Var("d"),)),), patterns.AGGREGATION_PATTERNS[3].rewrite)
+             for k, op in enumerate(ops)]
+    with pytest.raises(patterns.PatternError):
+        patterns.compile_patterns(table, [])

@@ -1,7 +1,8 @@
 """The function-resident path (csrc/fused.cuh: one function resident in shared
 memory per warp group, all passes fused) against the oracle on corpora drawn
-from the reference-front-half pools.  It is the default production path of the
-post-SSA stage; what it cannot do exactly it hands back to the general
+from the reference-front-half pools.  It is the production path of every run that
+asks for match lists (emit_matches, MATCH_ONLY) and can take any post-SSA run
+(CL_FUSED=1); what it cannot do exactly it hands back to the general
 per-function kernel, so the result must be bit-equal either way -- and the
 hand-back rate must stay small."""
 import numpy as np
@@ -29,16 +30,6 @@ def _check(engine, oracle, kind, n_sass, seed, passes=15, max_back=0.02, **kw):
     if kind != "long":
         assert part["handed_back"] <= max_back * corpus.n_funcs + 2, part
     return part
-
-
-@pytest.fixture(scope="module")
-def sim_fused_engine():
-    return helpers._engine_with_env(helpers.build_sim(), CL_FUSED=1)
-
-
-@pytest.fixture(scope="module")
-def cuda_fused_engine():
-    return helpers._engine_with_env(None, CL_FUSED=1)
 
 
 @pytest.mark.parametrize("kind,n_sass", [("sm52", 60_000), ("sm75", 60_000), ("sm90", 60_000), ("mixed", 120_000)])
@@ -91,10 +82,3 @@ def test_fused_cuda_repeatable(cuda_fused_engine):
         outs.append(o)
     assert not helpers.corpora_equal(outs[0], outs[1])
     assert not helpers.corpora_equal(outs[0], outs[2])
-
-
-@pytest.mark.gpu
-def test_fused_cuda_full_size_vs_oracle(cuda_fused_engine, oracle_engine):
-    """BASELINE.json config sizes against the oracle itself (it runs at several M inst/s on the host cores)"""
-    for kind in ("sm52", "sm90"):
-        _check(cuda_fused_engine, oracle_engine, kind, 10_000_000, seed=21)

@@ -40,7 +40,7 @@ def test_tile_logic_sim(sim_tile_engine, oracle_engine, kind, n_sass):
 def test_big_tile_logic_sim(oracle_engine, cfg):
     """the big-tile form the GPU uses at scale (planes in scratch, flipped by every permutation), forced on the
     one-lane build: 4096- and 16384-record tiles"""
-    eng = helpers._engine_with_env(helpers.build_sim(), CL_STREAM=0, CL_TILE=4, CL_GTILE_CFG=cfg)
+    eng = helpers._engine_with_env(helpers.build_sim(), CL_FUSED=0, CL_TILE=4, CL_GTILE_CFG=cfg)
     for kind, n_sass in (("mixed", 150_000), ("sm52", 60_000)):
         part = _check(eng, oracle_engine, kind, n_sass, seed=13)
         assert part["tile_mode"] == 4 and part["tile_cfg"] == cfg
