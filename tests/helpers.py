@@ -23,7 +23,7 @@ ORACLE_LIB = ROOT / "oracle" / "liboracle.so"
 SIM_LIB = ROOT / "tests" / "sim" / "libculifter_sim.so"
 CSRC = ROOT / "paper_2604_27486_b200" / "csrc"
 
-_ALL = sorted(p.name[:-len(".pkl.gz")] for p in GOLDEN.glob("*.pkl.gz"))
+_ALL = sorted(p.name[:-len(".pkl.gz")] for p in GOLDEN.glob("*.pkl.gz") if not p.name.startswith("pool_"))
 RAW_FIXTURES = [n for n in _ALL if n.startswith("raw_")]
 FIXTURES = [n for n in _ALL if n not in RAW_FIXTURES]
 STATUS_ERROR = {2: "AttributeError", 3: "AssertionError", 4: "KeyError", 6: "IndexError"}
@@ -82,6 +82,19 @@ def cuda_engine(fused=None):
     if fused is None:
         return Engine()
     return _engine_with_env(None, CL_FUSED=int(fused))
+
+
+def engine_patterns(engine):
+    """Pattern objects in the order of the engine's device table (aggregation, then xmad)."""
+    from paper_2604_27486_b200 import passes
+    return passes._engine_patterns(engine)
+
+
+def state_digest(state) -> bytes:
+    """sha1 of the canonical JSON of a state_of() dict: what tools/make_pools.py stores for the reference's result"""
+    import hashlib
+    import json
+    return hashlib.sha1(json.dumps(state, sort_keys=True, default=str).encode()).digest()
 
 
 def state_of(fn):

@@ -72,18 +72,23 @@ EXIT
 
 
 def expected(fns, passes):
-    out = []
+    """-> (states, match lists): what the reference's passes make of every function, and the
+    (pattern.name, positions) lists its match_patterns / select_matches returned on the way."""
+    out, mlists = [], []
     for fn in fns:
         ref = R.clone(fn)
+        ms = []
         err = R.run_postssa(ref, xmad=bool(passes & 1), recip=bool(passes & 2),
-                            aggregate=bool(passes & 4), tag=bool(passes & 8))
+                            aggregate=bool(passes & 4), tag=bool(passes & 8), matches=ms)
         out.append({"error": type(err).__name__} if err is not None else R.state_of(ref))
-    return out
+        mlists.append(None if err is not None else [(ph, bi, [tuple(x) for x in raw], [tuple(x) for x in sel]) for ph, bi, raw, sel in ms])
+    return out, mlists
 
 
 def write(name, fns, passes=15):
+    exp, mlists = expected(fns, passes)
     fix = {"name": name, "passes": passes, "functions": [ir.convert(f) for f in fns],
-           "expect": expected(fns, passes)}
+           "expect": exp, "matches": mlists}
     path = OUT / f"{name}.pkl.gz"
     with gzip.open(path, "wb", compresslevel=9) as fh:
         pickle.dump(fix, fh, protocol=4)
@@ -152,6 +157,13 @@ def main():
     for kind, seed, n in (("sm90", 11, 40), ("sm52", 12, 40), ("sm75", 13, 30), ("long", 14, 3)):
         arch, text = gen_sass.gen_corpus(seed, kind, n, near_miss=0.15)
         write(f"synth_{kind}", R.ssa_functions(text, arch))
+    # BASELINE.json configs[3] at its defining size: one 4096- and one 8192-instruction block (budget cut of
+    # patterns.py:194-198 active, reciprocal chains interleaved with IADD3 pairs); ~2 minutes of reference time
+    import random
+    rng = random.Random(4096)
+    text = "".join(gen_sass.gen_function(rng, f"long{size}", "sm90", gen_sass.MIX_LONG, 1, (size, size), 0.1, window=16)
+                   for size in (4096, 8192))
+    write("long_blocks", R.ssa_functions(text, "sm90"))
 
 
 if __name__ == "__main__":

@@ -1,24 +1,38 @@
 """Build the kernel pools behind paper_2604_27486_b200/synth.py (in-container
-only: the SASS text goes through the reference's own front half).
+only: the SASS text goes through the reference's own front half, and the
+expected results come from the reference's own passes).
 
-    python tools/make_pools.py            # writes tests/golden/pool_<kind>.npz
+    python tools/make_pools.py            # writes tests/golden/pool_<kind>*.{npz,pkl.gz}
+
+Per kind three files:
+  pool_<kind>.npz          the kernels as an encoded corpus (what build_corpus draws from)
+  pool_<kind>_objs.pkl.gz  the same kernels as LiftedFunction objects (SSA phase, the
+                           reference front half's output), so a test can check that the
+                           encoded pool IS those kernels and decode results into them
+  pool_<kind>_expect.npz   per kernel: sha1 of the reference's state after its own passes
+                           (pipeline.py:165-169; dump, diagnostics, boundaries, tags, id
+                           counters, value table) or the name of the exception it raises
+Every byte the benchmark corpora hold is therefore pinned to the Python reference:
+a corpus is a seeded multiset of these kernels.
 """
-import sys, time
+import gzip, hashlib, pickle, sys, time
 from multiprocessing import Pool as MPool
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent))
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import random
+import numpy as np
 import refharness as R
 import gen_sass
 from paper_2604_27486_b200 import ir, soa, synth
 
-SPEC = {  # kind: (functions, chunk) -- sized so each pool is a few hundred k records at most
-    "sm90": 3000, "sm75": 2000, "sm52": 3000, "long": 12,
+SPEC = {  # kind: kernels
+    "sm90": 6000, "sm75": 5000, "sm52": 5000, "long": 24,
 }
+LONG_SIZES = [4096] * 12 + [8192] * 8 + [16384] * 4     # BASELINE.json configs[3]: 4096+ instructions per block
 
 
-def gen_text(kind, seed, n):
+def gen_text(kind, seed, n, first=0):
     rng = random.Random(seed)
     out = []
     for i in range(n):
@@ -30,38 +44,60 @@ def gen_text(kind, seed, n):
         elif kind == "sm75":
             out.append(gen_sass.gen_function(rng, name, "sm75", gen_sass.MIX_SM90, rng.choice([1, 2, 3]), (8, 40), 0.1))
         else:
-            size = (4096, 8192, 16384)[i % 3]
+            size = LONG_SIZES[(first + i) % len(LONG_SIZES)]
             out.append(gen_sass.gen_function(rng, name, "sm90", gen_sass.MIX_LONG, 1, (size, size), 0.1, window=16))
     return out
 
 
+def state_digest(state) -> bytes:
+    """sha1 of the canonical JSON of a state_of() dict (tests/helpers.py computes the same for device results)"""
+    import json
+    return hashlib.sha1(json.dumps(state, sort_keys=True, default=str).encode()).digest()
+
+
 def work(args):
-    kind, seed, n = args
+    kind, seed, n, first = args
     arch = {"sm52": "sm52", "sm90": "sm90", "sm75": "sm75", "long": "sm90"}[kind]
-    texts = gen_text(kind, seed, n)
-    fns, n_sass = [], []
+    texts = gen_text(kind, seed, n, first)
+    fns, n_sass, digests, errors = [], [], [], []
     for t in texts:
         got = R.ssa_functions(t, arch)
         assert len(got) == 1
         fns.append(ir.convert(got[0]))
         n_sass.append(sum(1 for ln in t.splitlines() if ln and not ln.startswith(".text")))
-    return fns, n_sass
+        ref = R.clone(got[0])
+        err = R.run_postssa(ref)
+        errors.append("" if err is None else type(err).__name__)
+        digests.append(bytes(20) if err is not None else state_digest(R.state_of(ref)))
+    return fns, n_sass, digests, errors
 
 
 def main():
-    for kind, total in SPEC.items():
+    kinds = sys.argv[1:] or list(SPEC)
+    for kind in kinds:
+        total = SPEC[kind]
         t0 = time.time()
         chunk = 1 if kind == "long" else 100
-        jobs = [(kind, 1000 + k, min(chunk, total - k * chunk)) for k in range((total + chunk - 1) // chunk)]
+        jobs = [(kind, 1000 + k, min(chunk, total - k * chunk), k * chunk) for k in range((total + chunk - 1) // chunk)]
+        if kind == "long":
+            jobs.sort(key=lambda j: -LONG_SIZES[j[3] % len(LONG_SIZES)])       # the 16384-instruction blocks take minutes: start them first
         with MPool(8) as mp:
-            res = mp.map(work, jobs)
+            res = mp.map(work, jobs, chunksize=1)
+        if kind == "long":
+            res = [r for _, r in sorted(zip(jobs, res), key=lambda jr: jr[0][3])]
         fns = [f for r in res for f in r[0]]
         n_sass = [n for r in res for n in r[1]]
+        digests = np.frombuffer(b"".join(d for r in res for d in r[2]), np.uint8).reshape(-1, 20)
+        errors = np.array([e for r in res for e in r[3]])
         corpus = soa.encode(fns)
         path = synth.POOL_DIR / f"pool_{kind}.npz"
         synth.save_pool(path, corpus, n_sass, kind)
+        with gzip.open(synth.POOL_DIR / f"pool_{kind}_objs.pkl.gz", "wb", compresslevel=9) as fh:
+            pickle.dump(fns, fh, protocol=4)
+        np.savez_compressed(synth.POOL_DIR / f"pool_{kind}_expect.npz", sha1=digests, error=errors)
         print(f"{path.name}: {len(fns)} kernels, {sum(n_sass)} SASS insts, {corpus.n_insts} records, "
-              f"{path.stat().st_size / 1e6:.2f} MB, {time.time() - t0:.0f}s", flush=True)
+              f"{path.stat().st_size / 1e6:.2f} MB (+ objects {(synth.POOL_DIR / f'pool_{kind}_objs.pkl.gz').stat().st_size / 1e6:.2f} MB), "
+              f"{int((errors != '').sum())} reference errors, {time.time() - t0:.0f}s", flush=True)
 
 
 if __name__ == "__main__":

@@ -89,12 +89,48 @@ def corpus_files():
     return sorted((REF_PKG / "corpus").rglob("*.sass"))
 
 
-def run_postssa(fn, xmad=True, recip=True, aggregate=True, tag=True, snapshots=None):
+def run_postssa(fn, xmad=True, recip=True, aggregate=True, tag=True, snapshots=None, matches=None):
     """The four hot-path calls of ``pipeline.py:165-169`` on ``fn`` in place.
-    Returns the exception (reference reports it per function) or None."""
+    Returns the exception (reference reports it per function) or None.
+
+    ``matches``: a list that receives, for every block the reference matched in
+    (``_apply_patterns``, patterns.py:676), ``(phase, block index, raw, selected)``
+    with ``raw`` / ``selected`` = ``[(pattern name, positions...)]`` exactly as
+    ``match_patterns`` / ``select_matches`` returned them (list order kept);
+    phase 0 = the xmad round, 2 + r = aggregation round r -- the numbering of the
+    device's CL_EV_MATCH events."""
     load()
     from sasslift import patterns as patmod
     from sasslift.ssir import dump
+    saved = (patmod.match_patterns, patmod.select_matches, patmod._apply_patterns)
+    if matches is not None:
+        state = {"phase": 0, "agg_rounds": 0, "cur": None}
+        order = {b.bid: k for k, b in enumerate(fn.block_order())}
+
+        def apply_patterns(f, pats):
+            if pats is patmod.XMAD_PATTERNS:
+                state["phase"] = 0
+            else:
+                state["phase"] = 2 + state["agg_rounds"]
+                state["agg_rounds"] += 1
+            return saved[2](f, pats)
+
+        def match_patterns(f, blk, pats, du=None):
+            ms = saved[0](f, blk, pats, du)
+            pos = {i.iid: k for k, i in enumerate(blk.instructions)}
+            state["cur"] = (blk, pos)
+            if ms:
+                matches.append([state["phase"], order[blk.bid], [(m.pattern.name,) + tuple(pos[i.iid] for i in m.insts) for m in ms], []])
+            return ms
+
+        def select_matches(ms):
+            sel = saved[1](ms)
+            if ms:
+                pos = state["cur"][1]
+                matches[-1][3] = [(m.pattern.name,) + tuple(pos[i.iid] for i in m.insts) for m in sel]
+            return sel
+
+        patmod.match_patterns, patmod.select_matches, patmod._apply_patterns = match_patterns, select_matches, apply_patterns
     try:
         for name, on, call in (("xmad", xmad, patmod.normalize_xmad),
                                ("recip", recip, patmod.normalize_reciprocal),
@@ -106,6 +142,8 @@ def run_postssa(fn, xmad=True, recip=True, aggregate=True, tag=True, snapshots=N
                 snapshots[name] = dump(fn)
     except Exception as e:  # noqa: BLE001 - mirrors pipeline.py:182
         return e
+    finally:
+        patmod.match_patterns, patmod.select_matches, patmod._apply_patterns = saved
     return None
 
 
