@@ -2,11 +2,11 @@
 only: the SASS text goes through the reference's own front half, and the
 expected results come from the reference's own passes).
 
-    python tools/make_pools.py            # writes tests/golden/pool_<kind>*.{npz,pkl.gz}
+    python tools/make_pools.py            # writes tests/golden/pool_<kind>*.{npz,pkl.xz}
 
 Per kind three files:
   pool_<kind>.npz          the kernels as an encoded corpus (what build_corpus draws from)
-  pool_<kind>_objs.pkl.gz  the same kernels as LiftedFunction objects (SSA phase, the
+  pool_<kind>_objs.pkl.xz  the same kernels as LiftedFunction objects (SSA phase, the
                            reference front half's output), so a test can check that the
                            encoded pool IS those kernels and decode results into them
   pool_<kind>_expect.npz   per kernel: sha1 of the reference's state after its own passes
@@ -15,7 +15,7 @@ Per kind three files:
 Every byte the benchmark corpora hold is therefore pinned to the Python reference:
 a corpus is a seeded multiset of these kernels.
 """
-import gzip, hashlib, pickle, sys, time
+import hashlib, lzma, pickle, sys, time
 from multiprocessing import Pool as MPool
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent))
@@ -92,11 +92,10 @@ def main():
         corpus = soa.encode(fns)
         path = synth.POOL_DIR / f"pool_{kind}.npz"
         synth.save_pool(path, corpus, n_sass, kind)
-        with gzip.open(synth.POOL_DIR / f"pool_{kind}_objs.pkl.gz", "wb", compresslevel=9) as fh:
-            pickle.dump(fns, fh, protocol=4)
+        (synth.POOL_DIR / f"pool_{kind}_objs.pkl.xz").write_bytes(lzma.compress(pickle.dumps(fns, protocol=4), preset=6))
         np.savez_compressed(synth.POOL_DIR / f"pool_{kind}_expect.npz", sha1=digests, error=errors)
         print(f"{path.name}: {len(fns)} kernels, {sum(n_sass)} SASS insts, {corpus.n_insts} records, "
-              f"{path.stat().st_size / 1e6:.2f} MB (+ objects {(synth.POOL_DIR / f'pool_{kind}_objs.pkl.gz').stat().st_size / 1e6:.2f} MB), "
+              f"{path.stat().st_size / 1e6:.2f} MB (+ objects {(synth.POOL_DIR / f'pool_{kind}_objs.pkl.xz').stat().st_size / 1e6:.2f} MB), "
               f"{int((errors != '').sum())} reference errors, {time.time() - t0:.0f}s", flush=True)
 
 
