@@ -164,20 +164,3 @@ def build_corpus(kind: str, n_sass: int, seed: int = 0):
         order = rng.permutation(corpus.n_funcs)
         corpus = take_functions(corpus, order)
     return corpus, total, info
-
-
-def shard_by_blocks(corpus: Corpus, n_shards: int):
-    """Corpus sharder (north star subsystem 5): greedy longest-first bin packing
-    of kernels by basic-block count; returns the function indices of each shard.
-    No data crosses shards afterwards (functions are independent)."""
-    nb = np.diff(corpus.func_blk_off.astype(np.int64))
-    order = np.argsort(-nb, kind="stable")
-    if n_shards == 1:
-        return [np.arange(corpus.n_funcs)]
-    # longest-first round robin with a snake order is LPT-equivalent for near-uniform kernels
-    # and O(F); the handful of heavy kernels go first, one per shard.
-    shard = np.empty(corpus.n_funcs, np.int64)
-    pos = np.arange(corpus.n_funcs)
-    cyc = pos % (2 * n_shards)
-    shard[order] = np.where(cyc < n_shards, cyc, 2 * n_shards - 1 - cyc)
-    return [np.sort(np.nonzero(shard == s)[0]) for s in range(n_shards)]
