@@ -7,20 +7,25 @@ normalize_reciprocal, apply_aggregations, tag_cuda_objects) over this rank's
 shard of the synthetic mixed-architecture corpus (BASELINE.json configs[4]:
 40 % sm90 / 40 % sm75 / 20 % sm52 kernels plus long-block kernels).  The
 corpus is fixed (strong scaling): kernels are partitioned across ranks by
-basic-block count, no data crosses ranks, and each step ends with an NCCL
-allgather of the per-pattern match counters.
+LPT on instruction records, no data crosses ranks, and each step ends with an
+NCCL allgather of the per-pattern match counters.
 
   value        device-resident: input already in HBM, CUDA-event time of the
-               stage (max over ranks); inputs are far larger than L2.
+               stage INCLUDING the densification to the ABI's dense result
+               (max over ranks); inputs are far larger than L2.
   e2e          through the public batch API (capi.Pipeline) with pinned HOST
                buffers: per chunk cl_upload (H2D) + cl_run_postssa (kernels +
                device densify) + cl_download (D2H); upload, run and download are
                stage threads over a few contexts, so the three overlap across chunks.
   roofline     algorithmic bytes / kernel time vs MEASURED_PEAKS.json hbm_gbs;
                `traffic` = DRAM bytes of the dominant kernel per launch from the
-               committed ncu capture of this workload (profiles/r01_traffic.json).
+               committed ncu capture of this workload (profiles/r02_traffic.json).
   cpu_baseline the oracle (C port of the reference) on this box's host cores,
                bounded sample of the same corpus.
+  configs      (N = 1) the other BASELINE.json configs, each with its own value,
+               roofline fraction and CPU sample: bundled corpus, sm52-10M with the
+               RAW stage (OpModTransform + SRSubstituteReverse via cl_run_raw, then
+               XmadToImad), sm90-10M (all sequence patterns), long blocks.
 
 `--impl reference` times that CPU port alone (rank 0 only).
 """
@@ -54,7 +59,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="mixed", choices=["mixed", "sm90", "sm52", "sm75", "long"])
+    ap.add_argument("--workload", default="mixed", choices=["mixed", "sm90", "sm52", "sm75", "long", "raw_x4", "raw_sr"])
     ap.add_argument("--insts", type=float, default=float(os.environ.get("CL_BENCH_INSTS", 100e6)),
                     help="SASS instructions in the whole corpus (all ranks)")
     ap.add_argument("--seed", type=int, default=100)
@@ -64,6 +69,8 @@ def parse_args():
     ap.add_argument("--runners", type=int, default=2, help="e2e: run threads (kernels of two chunks back to back)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config legs (BASELINE.json configs[0..3])")
+    ap.add_argument("--passes", type=int, default=15, help="CL_PASS_* mask of the headline leg")
     return ap.parse_args()
 
 
@@ -162,6 +169,107 @@ def cpu_leg(corpus: Corpus, n_sass, threads, steps=1, warmup=0):
     return n_sass * len(times) / sum(times), float(np.mean(times))
 
 
+def roofline_of(bytes_per_step, ms, peak, n_sass):
+    achieved = bytes_per_step / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "algorithmic_bytes_per_launch": int(bytes_per_step), "bytes_per_sass_inst": bytes_per_step / max(n_sass, 1)}
+
+
+def timed(eng, run, steps, warmup):
+    """W untimed + K timed runs of `run` on an uploaded corpus: mean device ms (CUDA events inside the library)."""
+    import torch
+    for _ in range(warmup):
+        run()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(steps):
+        run()
+        ms.append(eng.last_run_ms())
+    torch.cuda.synchronize()
+    return float(np.mean(ms))
+
+
+def config_legs(eng, peak, threads, steps, warmup, with_cpu):
+    """BASELINE.json configs[0..3] on one GPU: device-resident throughput, roofline fraction, CPU sample."""
+    import gzip
+    import pickle
+    from paper_2604_27486_b200 import layout as L, passes as P, soa
+    out = []
+
+    def cpu_sample(kind, seed, n, passes_mask=15, raw=0):
+        if not with_cpu:
+            return None
+        c, ns, _ = synth.build_corpus(kind, n, seed=seed)
+        from paper_2604_27486_b200.capi import Engine
+        o = Engine(ROOT / "oracle" / "liboracle.so")
+        o.set_threads(threads)
+        o.upload(c)
+        if raw:
+            o.run_raw(raw, P._sr_map())
+        else:
+            o.run_postssa(passes_mask)
+        sec = o.last_run_ms() / 1e3
+        o.close()
+        return {"value": ns / sec, "unit": UNIT, "cores": threads, "kind": "port", "sample": f"{ns} SASS instructions of the same corpus, {sec:.2f} s"}
+
+    def postssa_leg(name, corpus, n_sass, passes_mask, what, cpu):
+        eng.upload(corpus)
+        ms = timed(eng, lambda: eng.run_postssa(passes_mask), steps, warmup)
+        st = eng.stats()
+        b = algorithmic_bytes(corpus, int(st["n_inst_out"]), int(st["selected"].sum()))
+        part = eng.debug_partition() or {}
+        return {"config": name, "workload": what, "metric": METRIC, "value": n_sass / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                "steps": steps, "warmup": warmup, "sass_insts": int(n_sass), "records": int(corpus.n_insts), "kernels": int(corpus.n_funcs),
+                "roofline": roofline_of(b, ms, peak, n_sass), "cpu_baseline": cpu, "gpu_launches": int(part.get("launches", 0)) * steps,
+                "match_counts": {"selected": int(st["selected"].sum()), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())}}
+
+    # configs[0]: the reference's bundled corpus (22 functions, 261 SASS instructions), tiled for timing only
+    with gzip.open(ROOT / "tests" / "golden" / "bundled.pkl.gz", "rb") as fh:
+        fns = pickle.load(fh)["functions"]
+    one = soa.encode(fns)
+    k = 4096
+    tiled = synth.take_functions(one, np.tile(np.arange(one.n_funcs), k))
+    n_bundled = 261 * k
+    cpu = None
+    if with_cpu:
+        from paper_2604_27486_b200.capi import Engine
+        o = Engine(ROOT / "oracle" / "liboracle.so"); o.set_threads(threads)
+        small = synth.take_functions(one, np.tile(np.arange(one.n_funcs), 256))
+        o.upload(small); o.run_postssa(); sec = o.last_run_ms() / 1e3; o.close()
+        cpu = {"value": 261 * 256 / sec, "unit": UNIT, "cores": threads, "kind": "port", "sample": f"the bundled corpus x 256, {sec:.2f} s"}
+    out.append(postssa_leg("bundled", tiled, n_bundled, 15, f"pkg/corpus listings (22 functions, 261 SASS instructions) x {k}, full post-SSA stage", cpu))
+
+    # configs[1]: sm52, 10 M instructions: OpModTransform + SRSubstituteReverse (raw stage) + XmadToImad
+    legs, total_ms, n_ref = [], 0.0, None
+    for name, kind, raw in (("OpModTransform (cl_run_raw X4)", "raw_x4", L.RAW_X4), ("SRSubstituteReverse (cl_run_raw SR)", "raw_sr", L.RAW_SR)):
+        c, ns, _ = synth.build_corpus(kind, 10_000_000, seed=52)
+        eng.upload(c)
+        ms = timed(eng, lambda: eng.run_raw(raw, P._sr_map()), steps, warmup)
+        n_out = int(eng.stats()["n_inst_out"])
+        b = 64 * (c.n_insts + n_out) + 8 * c.n_funcs
+        legs.append({"pass": name, "ms_per_step": ms, "value": ns / (ms / 1e3), "sass_insts": int(ns), "records_in": int(c.n_insts), "records_out": n_out,
+                     "roofline": roofline_of(b, ms, peak, ns), "cpu_baseline": cpu_sample(kind, 52, 300_000, raw=raw)})
+        total_ms += ms
+        n_ref = ns
+    c, ns, _ = synth.build_corpus("sm52", 10_000_000, seed=52)
+    xm = postssa_leg("sm52-10M/xmad", c, ns, L.PASS_XMAD, "XmadToImad (normalize_xmad only)", cpu_sample("sm52", 52, 300_000, L.PASS_XMAD))
+    legs.append({"pass": "XmadToImad (cl_run_postssa XMAD)", "ms_per_step": xm["ms_per_step"], "value": xm["value"], "sass_insts": int(ns),
+                 "roofline": xm["roofline"], "cpu_baseline": xm["cpu_baseline"], "match_counts": xm["match_counts"]})
+    total_ms += xm["ms_per_step"]
+    out.append({"config": "sm52-10M", "workload": "SM52 XMAD-heavy synthetic corpus, 10 M instructions: OpModTransform + SRSubstituteReverse + XmadToImad",
+                "metric": METRIC, "value": n_ref / (total_ms / 1e3), "unit": UNIT, "ms_per_step": total_ms, "steps": steps, "warmup": warmup,
+                "sass_insts": int(n_ref), "passes": legs,
+                "roofline": {"bound": "hbm", "frac": sum(l["roofline"]["algorithmic_bytes_per_launch"] for l in legs) / (total_ms / 1e3) / 1e9 / peak,
+                             "achieved": sum(l["roofline"]["algorithmic_bytes_per_launch"] for l in legs) / (total_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s"}})
+
+    # configs[2]: sm90, 10 M instructions, all sequence patterns; configs[3]: long unrolled blocks
+    for name, kind, n, what in (("sm90-10M", "sm90", 10_000_000, "SM90 synthetic corpus, 10 M instructions, all 8 sequence patterns, full post-SSA stage"),
+                                ("long-blocks", "long", 4_000_000, "single-block kernels of 4096 / 8192 / 16384 instructions with reciprocal chains, 4 M instructions, full post-SSA stage")):
+        c, ns, _ = synth.build_corpus(kind, n, seed=90 if kind == "sm90" else 4096)
+        out.append(postssa_leg(name, c, ns, 15, what, cpu_sample(kind, 90, 300_000)))
+    return out
+
+
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", 0))
@@ -215,7 +323,7 @@ def main():
     lib_counts = torch.as_tensor(_Raw(eng.device_counts_ptr()), device="cuda")
 
     def step():
-        eng.run_postssa()
+        eng.run_postssa(args.passes)
         if world > 1:                      # the only inter-GPU traffic: match counters
             counts.copy_(lib_counts)
             allgather_counts(counts, world)
@@ -259,25 +367,21 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     # DRAM bytes of the dominant kernel per launch: from the committed ncu --set full capture of this very
-    # workload (profiles/r01_traffic.json); null for any other workload or path
-    traffic = None
+    # workload (profiles/r02_traffic.json); null for any other workload or path
+    traffic, kernel_name = None, "k_postssa_gtile"
     try:
-        tr = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())["k_postssa_gtile"]
-        if (args.workload == "mixed" and world == 1 and part.get("tile_mode") != 8
+        tr = json.loads((ROOT / "profiles" / "r02_traffic.json").read_text())["k_postssa_gtile"]
+        if (args.workload == "mixed" and world == 1 and part.get("tile_mode") == 4 and args.passes == 15
                 and abs(n_sass_all - tr["workload_sass_insts"]) < 0.01 * tr["workload_sass_insts"]):
             traffic = tr["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         pass
-    achieved = bytes_per_step / (np.mean(dev_ms) / 1e3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "kernel": ("k_stream (corpus-wide streaming passes, one cooperative launch) with the per-function kernels for what it "
-                           "hands back: the whole stage, rank 0") if part.get("tile_mode") == 8 else
-                          ("k_postssa_gtile (tile kernel: small kernels packed into tiles of 16 384 records) with k_postssa_cta "
-                           "(long-block kernels) beside it and k_postssa_warp_sync for what the tile kernel hands back: "
-                           "the whole stage, rank 0"),
-                "algorithmic_bytes_per_launch": bytes_per_step,
-                "bytes_per_sass_inst": bytes_per_step / max(n_sass_rank, 1)}
+    roofline = roofline_of(bytes_per_step, float(np.mean(dev_ms)), peak, n_sass_rank)
+    roofline.update({"traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                     "kernel": ("k_fused (one function resident in shared memory per warp group) with the per-function kernels for what it hands back: the whole stage, rank 0"
+                                if part.get("tile_mode") == 16 else
+                                "k_postssa_gtile (tile kernel: small kernels packed into tiles of up to 16 384 records) with k_postssa_cta (long-block "
+                                "kernels) beside it, k_postssa_warp_sync for what the tile kernel hands back and the densify kernels: the whole stage, rank 0")})
 
     # end to end through the public batch API with pinned HOST buffers: the corpus flows chunk by chunk
     # (contiguous function ranges) through a few contexts, so H2D, kernels and D2H of different chunks overlap
@@ -336,6 +440,12 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{int(ns2.sum())} SASS instructions ({sample_c.n_insts} records) of the same corpus, {sec:.1f} s"}
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs and args.workload == "mixed":
+        eng2 = Engine(device=local)
+        configs = config_legs(eng2, peak, threads, max(2, min(args.steps, 3)), max(3, args.warmup), not args.no_cpu)
+        eng2.close()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -344,14 +454,15 @@ def main():
             "config": {"workload": f"{args.workload}-{n_sass_all / 1e6:.1f}M SASS instructions (BASELINE.json configs[4]: "
                                    f"40% sm90 / 40% sm75 / 20% sm52 kernels + long-block kernels), full post-SSA stage",
                        "kernels": int(len(kid)), "ssa_records_rank0": int(corpus.n_insts), "sass_rank0": n_sass_rank,
-                       "sharding": f"{world} shard(s) by basic-block count, no data-path collective, allgather of match counts",
+                       "sharding": f"{world} shard(s) by kernel (LPT on instruction records), no data-path collective, allgather of match counts",
                        "l2": "inputs larger than L2 (no flush needed)", "seed": args.seed,
-                       "corpus": "kernels drawn with replacement from reference-front-half pools (tests/golden/pool_*.npz)",
+                       "corpus": "kernels drawn with replacement from reference-front-half pools (tests/golden/pool_*.npz: 16 000 + 24 long-block kernels, each pinned to the reference by digest)",
                        "gen_seconds": round(t_gen, 1), "wall_ms_per_step": t_wall_s / args.steps * 1e3},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": int(part.get("launches", 0)) * args.steps,
             "partition": part,
             "match_counts": {"selected": int(n_sel), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())},
+            "configs": configs,
         }
         print(json.dumps(line))
     if world > 1:

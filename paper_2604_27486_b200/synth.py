@@ -32,7 +32,9 @@ from .soa import Corpus
 
 POOL_DIR = Path(__file__).resolve().parent.parent / "tests" / "golden"
 KINDS = ("sm52", "sm75", "sm90", "long")
-MIXED = (("sm90", 0.3995), ("sm75", 0.40), ("sm52", 0.20), ("long", 0.0005))
+# mixed corpus (BASELINE.json configs[4]): its sprinkle of long-block kernels is drawn from the 4096-instruction
+# ones ("long4k", as in round 1); the 8192- and 16384-instruction blocks are configs[3]'s workload ("long")
+MIXED = (("sm90", 0.3995), ("sm75", 0.40), ("sm52", 0.20), ("long4k", 0.0005))
 
 
 @dataclass
@@ -69,6 +71,7 @@ def load_pool(kind: str, path=None) -> Pool:
     if ((c.tag[(c.tag & 15) == L.K_IMM] & L.T_IMM_HEXTEXT) != 0).any():
         raise ValueError("pool holds device-created immediates")
     c.imm["text"] = st_map[c.imm["text"].astype(np.int64)]
+    c.raw = str(z["kind"]).startswith("raw")          # raw-stage pools: one block per function holding fn.raw_instructions
     return Pool(c, z["n_sass"].astype(np.int64), str(z["kind"]))
 
 
@@ -113,7 +116,7 @@ def take_functions(c: Corpus, picks: np.ndarray) -> Corpus:
                   imm_off=imm_off, val_off=val_off, blk=c.blk[blk_idx], blk_off=blk_off,
                   hdr=c.hdr[inst_idx], tag=c.tag[inst_idx], pay=c.pay[inst_idx], ext_tag=ext_tag,
                   ext_pay=ext_pay, mem=mem, imm=imm, val_alive=alive, val_def_iid=def_iid,
-                  val_origin=origin)
+                  val_origin=origin, raw=c.raw)
 
 
 def concat(parts) -> Corpus:
@@ -137,7 +140,12 @@ _POOLS = {}
 
 def pool(kind: str) -> Pool:
     if kind not in _POOLS:
-        _POOLS[kind] = load_pool(kind)
+        if kind == "long4k":                 # the long pool's 4096-instruction kernels
+            p = pool("long")
+            keep = np.nonzero(p.n_sass <= 5000)[0]
+            _POOLS[kind] = Pool(take_functions(p.corpus, keep), p.n_sass[keep], kind)
+        else:
+            _POOLS[kind] = load_pool(kind)
     return _POOLS[kind]
 
 

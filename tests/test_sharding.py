@@ -46,6 +46,20 @@ def _worker(rank, world, port, n_sass, out_dir):
     dist.destroy_process_group()
 
 
+def _single(n_sass, out_dir):
+    """the single-process run, in a fresh process like the ranks: interned ids (opcodes, modifier tuples, strings) are
+    process-local tables filled in load order, so results are compared between processes with the same history"""
+    sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
+    import helpers
+    from paper_2604_27486_b200 import synth
+    whole = synth.build_corpus("mixed", n_sass, seed=7)[0]
+    eng = helpers.sim_engine()
+    eng.upload(whole); eng.run_postssa()
+    eng.download().save(Path(out_dir) / "single.npz")
+    with open(Path(out_dir) / "single_counts.pkl", "wb") as fh:
+        pickle.dump(_counts(eng.stats()), fh)
+
+
 @pytest.mark.timeout(300)
 def test_two_rank_sharding_matches_single_process(tmp_path):
     import helpers
@@ -55,6 +69,7 @@ def test_two_rank_sharding_matches_single_process(tmp_path):
     n_sass, world, port = 60_000, 2, 29611
     ctx = mp.get_context("spawn")
     procs = [ctx.Process(target=_worker, args=(r, world, port, n_sass, str(tmp_path))) for r in range(world)]
+    procs.append(ctx.Process(target=_single, args=(n_sass, str(tmp_path))))
     for p in procs:
         p.start()
     for p in procs:
@@ -63,10 +78,8 @@ def test_two_rank_sharding_matches_single_process(tmp_path):
     allc, balance = pickle.load(open(tmp_path / "counts.pkl", "rb"))
     assert allc.shape[0] == world and balance["records"] < 1.02, balance
     whole = synth.build_corpus("mixed", n_sass, seed=7)[0]
-    eng = helpers.sim_engine()
-    eng.upload(whole); eng.run_postssa()
-    single = eng.download()
-    assert np.array_equal(allc.sum(axis=0), _counts(eng.stats()))                 # the allgathered counters
+    single = Corpus.load(tmp_path / "single.npz")
+    assert np.array_equal(allc.sum(axis=0), pickle.load(open(tmp_path / "single_counts.pkl", "rb")))   # the allgathered counters
     plan = sharding.shard_plan(whole, world)
     union = sharding.unshard([Corpus.load(tmp_path / f"shard{r}.npz") for r in range(world)], plan)
     assert not union.equal(single)                                                # ... and every byte of the streams

@@ -72,8 +72,47 @@ def work(args):
     return fns, n_sass, digests, errors
 
 
+def raw_work(args):
+    """Raw-stage pools (BASELINE.json configs[1]: OpModTransform + SRSubstituteReverse on sm52): the sm52 pool's
+    listings as PARSED functions (input of normalize_instruction, frontend.py:523) and after the reference's own
+    normalize + register widening (input of substitute_special_registers, frontend.py:697)."""
+    seed, n = args
+    R.load()
+    from sasslift import frontend
+    x4_in, sr_in, n_sass = [], [], []
+    for t in gen_text("sm52", seed, n):
+        for fn in R.raw_functions(t, "sm52", normalize=False):
+            x4_in.append(ir.convert(fn))
+            out = []
+            for inst in fn.raw_instructions:
+                out.extend(frontend.normalize_instruction(fn, inst))
+            fn.raw_instructions = out
+            for inst in fn.raw_instructions:
+                frontend.expand_implicit_registers(inst, "sm52")
+            sr_in.append(ir.convert(fn))
+            n_sass.append(sum(1 for ln in t.splitlines() if ln and not ln.startswith(".text")))
+    return x4_in, sr_in, n_sass
+
+
+def main_raw():
+    t0 = time.time()
+    total, chunk = SPEC["sm52"], 100
+    with MPool(8) as mp:
+        res = mp.map(raw_work, [(1000 + k, min(chunk, total - k * chunk)) for k in range((total + chunk - 1) // chunk)], chunksize=1)
+    n_sass = [n for r in res for n in r[2]]
+    for name, idx in (("raw_x4", 0), ("raw_sr", 1)):
+        fns = [f for r in res for f in r[idx]]
+        corpus = soa.encode(fns, raw=True)
+        path = synth.POOL_DIR / f"pool_{name}.npz"
+        synth.save_pool(path, corpus, n_sass, name)
+        print(f"{path.name}: {len(fns)} kernels, {sum(n_sass)} SASS insts, {corpus.n_insts} records, {path.stat().st_size / 1e6:.2f} MB, {time.time() - t0:.0f}s", flush=True)
+
+
 def main():
-    kinds = sys.argv[1:] or list(SPEC)
+    kinds = sys.argv[1:] or list(SPEC) + ["raw"]
+    if "raw" in kinds:
+        main_raw()
+        kinds = [k for k in kinds if k != "raw"]
     for kind in kinds:
         total = SPEC[kind]
         t0 = time.time()
