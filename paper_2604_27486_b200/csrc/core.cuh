@@ -20,6 +20,8 @@
 #include "../../include/culifter.h"
 #include <stdint.h>
 #include <string.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #if defined(__CUDACC__) && !defined(CL_SIM)
 #define CL_DEV 1
@@ -79,6 +81,27 @@ CLD void a_min32(uint32_t *p, uint32_t v) {
     atomicMin(p, v);
 #else
     if (v < *p) *p = v;
+#endif
+}
+CLD uint32_t a_or(uint32_t *p, uint32_t v) {
+#if CL_DEV
+    return atomicOr(p, v);
+#else
+    uint32_t o = *p; *p |= v; return o;
+#endif
+}
+/* append to a list whose cursor is *counter: one atomic per warp for the lanes that call it together */
+CLD uint32_t a_append(uint32_t *counter) {
+#if CL_DEV
+    const unsigned act = __activemask();
+    const unsigned lane = threadIdx.x & 31u;
+    const int lead = __ffs((int)act) - 1;
+    uint32_t base = 0;
+    if ((int)lane == lead) base = atomicAdd(counter, (uint32_t)__popc(act));
+    base = __shfl_sync(act, base, lead);
+    return base + (uint32_t)__popc(act & ((1u << lane) - 1u));
+#else
+    return (*counter)++;
 #endif
 }
 CLD unsigned long long a_add64(unsigned long long *p, unsigned long long v) {
@@ -1538,7 +1561,13 @@ template <class G> CLF void tag_cuda_objects(const G &g, FS &s) {
  *              + the inserted bitcasts chained from xhead[v]
  * where root(v) is the original value a renamed value (.bits / .f) took its
  * sites from -- and the group materialises the inserted records at the end. */
+#if !CL_DEV
+static unsigned long long g_dbg_refs = 0, g_dbg_chains = 0;
+#endif
 CLN bool rec_references(const FS &s, uint32_t i, uint32_t vid) {
+#if !CL_DEV
+    g_dbg_refs++;
+#endif
     const cl_hdr h = s.S.hdr[i];
     bool r = false;
     for_value_operands(s, h, i, [&](uint32_t v) { r |= v == vid; });
@@ -1620,19 +1649,36 @@ template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
     }
     g.sync();
     uint32_t nx = 0, n_events = 0, vid = s.next_vid, iid = s.next_iid;
-    if (g.rank == 0) {
-        for (uint32_t bi = 0; bi < s.nb && !status(s); bi++) {
-            for (uint32_t i = s.bo[bi]; i < s.bo[bi + 1] && !status(s); i++) {
-                const cl_hdr h = s.S.hdr[i];
-                if (h.op != CL_OP_MUFU || !has_mod(s, h, CL_MB_RCP) || !h.n_uses) continue;
-                opnd src = get_use(s, h, i, 0);
-                if (!is_value(src) || src.pay >= s.cap.V) continue;
-                /* du.def_inst of the source: original values only (bitcast results never feed a MUFU's I2F test) */
-                {
-                    uint32_t dp = src.pay < nv ? s.defpos[src.pay] : NONE32;
-                    bool is_i2f = dp != NONE32 && s.S.hdr[dp].op == CL_OP_I2F;
-                    if (!is_i2f) continue;
+    /* the MUFU.RCP records fed by an I2F, in stream order: found by all lanes (ordered compaction into outpos[],
+     * free until the materialisation below), so that the sequential part walks a handful of candidates instead
+     * of every record of the function (a 20 000-record block spent 2/3 of its stage in that walk).  The test
+     * reads nothing a chain rewrite changes: rewrites touch the uses of adds and of their users' operands, and a
+     * MUFU whose source is an add result is no candidate before (IADD) or after (BITCAST) the rewrite.        */
+    uint32_t n_cand = 0;
+    GFOR(g, i, s.n) {
+        bool c = false;
+        if (i < s.n) {
+            const cl_hdr h = s.S.hdr[i];
+            if (h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP) && h.n_uses) {
+                const opnd src = get_use(s, h, i, 0);
+                if (is_value(src) && src.pay < s.cap.V) {
+                    /* du.def_inst of the source: original values only (bitcast results never feed a MUFU's I2F test) */
+                    const uint32_t dp = src.pay < nv ? s.defpos[src.pay] : NONE32;
+                    c = dp != NONE32 && s.S.hdr[dp].op == CL_OP_I2F;
                 }
+            }
+        }
+        uint32_t t;
+        const uint32_t o = g.flag_exscan(c, t);
+        if (c) s.outpos[n_cand + o] = i;
+        n_cand += t;
+    }
+    g.sync();
+    if (g.rank == 0) {
+        for (uint32_t ci_ = 0; ci_ < n_cand && !status(s); ci_++) {
+            {
+                const uint32_t i = s.outpos[ci_], bi = block_of(s, i);
+                const cl_hdr h = s.S.hdr[i];
                 if (!h.n_defs) { fail(s, CL_ST_INDEX_ERROR); break; }
                 opnd rcp = get_def(s, h, i, 0);
                 if (!is_value(rcp)) { fail(s, CL_ST_ATTRIBUTE_ERROR); break; }
@@ -1662,6 +1708,10 @@ template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
                 }
                 for (uint32_t ai = 0; ai < n_adds && !status(s); ai++) {
                     const uint32_t a = adds[ai];
+#if !CL_DEV
+                    g_dbg_chains++;
+                    if (getenv("CL_DEBUG_REDO")) fprintf(stderr, "recip: chain query %llu, rec_references so far %llu (n=%u)\n", g_dbg_chains, g_dbg_refs, s.n);
+#endif
                     if (!Reach<3>::run(s, false, a)) continue;
                     if (nx + 2 > s.cap.X || vid + 2 > s.cap.V) { fail(s, CL_ST_CAPACITY); break; }
                     const cl_hdr ah = s.S.hdr[a];

@@ -714,9 +714,9 @@ struct cl_ctx {
         std::vector<TileDesc> tiles;
         TileDesc *d_tiles = nullptr; uint32_t *d_counter = nullptr; uint8_t *d_scratch = nullptr;
         size_t scratch_per_group = 0; uint32_t grid = 0, groups = 0;
-    } tc[3];                   /* [1]: shared-memory tiles, [2]: big tiles resident in L2 (global scratch); [0] unused */
+    } tc[3];                   /* [0]: one long block per tile (TileCfgG4), [1]: shared-memory tiles, [2]: big tiles in global scratch */
     int gtile_cfg = -1;        /* 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
-    int tile_mode_env = -1, gtile_cfg_env = -1;
+    int tile_mode_env = -1, gtile_cfg_env = -1, gtile_ctas = 2;   /* two 1024-thread CTAs per SM at 32 registers: +27 % over one at 64 (latency bound: resident warps are what counts) */
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest, big_rest; /* small / large functions that are not in a tile */
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr, *d_big_rest = nullptr;
@@ -773,6 +773,7 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_FUSED")) c->fused_mode = atoi(e) != 0;
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 6;
     if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(2, std::max(0, atoi(e)));
+    if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(2, std::max(1, atoi(e)));
     void *p = nullptr;
     if (dmalloc(&p, sizeof(H_OPFLAGS))) { delete c; return -1; }
     c->d_opflags = (uint8_t *)p;
@@ -938,7 +939,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             uint64_t n_small = 0;
             for (uint32_t f = 0; f < F; f++) {
                 const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
-                if (n <= c->small_max) n_small += n;
+                if (tile_icap(n) <= TileCfgG4::I) n_small += n;          /* everything a tile can take */
             }
             int n_sm = 148;
 #if CL_CUDA
@@ -958,7 +959,11 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
          * function order: the same packing as round 1's stable_sort, without its n log n)                    */
         std::vector<uint8_t> cls_of(F, 0xFF);
         std::vector<uint32_t> cnt[3];
-        for (int k = 1; k < 3; k++) cnt[k].assign((size_t)c->small_max + 2, 0);
+        /* big tiles also take the functions above small_max that fit one (a 4096-instruction block is a tile of its
+         * own): the passes of tile.cuh are data parallel inside a block, the CTA kernel walks its chains and
+         * matches with one lane.  What they hand back goes to the CTA kernel (retry_big).                      */
+        const uint32_t tile_max = std::max(c->small_max, (c->tile_mode & 4) ? (uint32_t)TileCfgG4::I : 0u);
+        for (int k = 0; k < 3; k++) cnt[k].assign((size_t)tile_max + 2, 0);
         auto need_of = [&](uint32_t f) {
             const uint32_t b0 = in->func_blk_off[f], b1 = in->func_blk_off[f + 1];
             const uint32_t n = in->blk_off[b1] - in->blk_off[b0];
@@ -972,20 +977,21 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             const bool plain = in->ext_off[f + 1] == in->ext_off[f] && nb > 0;
             int k = -1;
             if (small && plain && (c->tile_mode & 2) && nd.I <= TileCfgL::I && nd.V <= TileCfgL::V && nd.Q <= TileCfgL::Q && nd.B <= TileCfgL::B) k = 1;
-            else if (small && plain && (c->tile_mode & 4) && nd.I <= gI && nd.V <= gV && nd.Q <= gQ && nd.B <= gB) k = 2;
-            if (k > 0) { cls_of[f] = (uint8_t)k; cnt[k][c->small_max - n]++; }
+            else if (n <= tile_max && plain && (c->tile_mode & 4) && nd.I <= gI && nd.V <= gV && nd.Q <= gQ && nd.B <= gB) k = 2;
+            else if (n <= tile_max && plain && (c->tile_mode & 4) && nd.I <= TileCfgG4::I && nd.V <= TileCfgG4::V && nd.Q <= TileCfgG4::Q && nd.B <= TileCfgG4::B) k = 0;
+            if (k >= 0) { cls_of[f] = (uint8_t)k; cnt[k][tile_max - n]++; }
             else if (small) c->rest.push_back(f);
             else c->big_rest.push_back(f);
         }
-        const uint32_t capI[3] = { 0, TileCfgL::I, gI }, capV[3] = { 0, TileCfgL::V, gV }, capQ[3] = { 0, TileCfgL::Q, gQ },
-                       capB[3] = { 0, TileCfgL::B, gB }, capF[3] = { 0, TileCfgL::F, gF };
-        for (int k = 1; k < 3; k++) {
+        const uint32_t capI[3] = { TileCfgG4::I, TileCfgL::I, gI }, capV[3] = { TileCfgG4::V, TileCfgL::V, gV }, capQ[3] = { TileCfgG4::Q, TileCfgL::Q, gQ },
+                       capB[3] = { TileCfgG4::B, TileCfgL::B, gB }, capF[3] = { TileCfgG4::F, TileCfgL::F, gF };
+        for (int k = 0; k < 3; k++) {
             uint32_t run = 0;
             for (uint32_t &x : cnt[k]) { const uint32_t t = x; x = run; run += t; }
             std::vector<uint32_t> order(run);
             for (uint32_t f = 0; f < F; f++) if (cls_of[f] == k) {
                 const uint32_t n = in->blk_off[in->func_blk_off[f + 1]] - in->blk_off[in->func_blk_off[f]];
-                order[cnt[k][c->small_max - n]++] = f;
+                order[cnt[k][tile_max - n]++] = f;
             }
             TileDesc cur = { (uint32_t)c->tile_flist.size(), 0 };
             uint32_t sI = 0, sV = 0, sQ = 0, sB = 0;
@@ -1013,18 +1019,21 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             cl_ctx::TileClass &t = c->tc[k];
             if (t.tiles.empty()) continue;
 #if CL_CUDA
-            if (k == 0) continue;
-            if (k == 1) {
+            if (k == 0) {
+                t.scratch_per_group = gtile_scratch_bytes<TileCfgG4>();
+                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->gtile_ctas, t.tiles.size());
+                t.groups = t.grid;
+            } else if (k == 1) {
                 t.scratch_per_group = tile_scratch_bytes<TileCfgL>();
                 t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, t.tiles.size());
                 t.groups = t.grid;
             } else {
                 t.scratch_per_group = c->gtile_cfg == 2 ? gtile_scratch_bytes<TileCfgG3>() : c->gtile_cfg == 1 ? gtile_scratch_bytes<TileCfgG2>() : gtile_scratch_bytes<TileCfgG>();
-                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, t.tiles.size());
+                t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->gtile_ctas, t.tiles.size());
                 t.groups = t.grid;
             }
 #else
-            t.scratch_per_group = k == 1 ? tile_scratch_bytes<TileCfgL>() : tile_scratch_bytes<TileCfgG3>();
+            t.scratch_per_group = k == 1 ? tile_scratch_bytes<TileCfgL>() : k == 0 ? tile_scratch_bytes<TileCfgG4>() : tile_scratch_bytes<TileCfgG3>();
             t.grid = t.groups = 1;
 #endif
             if (dput(c, T_ID[k], &t.d_tiles, t.tiles.data(), t.tiles.size())) return -1;
@@ -1123,12 +1132,24 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     k.retry_big_list = c->d_retry_big; k.retry_big_count = c->d_retry_big_count; k.small_max = c->small_max;
     c->n_launches++;
 #if CL_CUDA
-    cudaStream_t st = cls == 1 ? c->stream2 : c->stream;
+    cudaStream_t st = cls == 2 ? c->stream : c->stream2;
     if (dzero(k.tile_counter, sizeof(uint32_t), st)) return -1;
+    if (cls == 0) {
+        if (c->gtile_ctas == 2) k_postssa_gtile<TileCfgG4, 32, 2><<<t.grid, 1024, 0, st>>>(k);
+        else k_postssa_gtile<TileCfgG4, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        CUDA_OK(cudaGetLastError());
+        return 0;
+    }
     if (cls == 2) {
-        if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 1><<<t.grid, 1024, 0, st>>>(k);
-        else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 1><<<t.grid, 1024, 0, st>>>(k);
-        else k_postssa_gtile<TileCfgG, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        if (c->gtile_ctas == 2) {
+            if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 2><<<t.grid, 1024, 0, st>>>(k);
+            else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 2><<<t.grid, 1024, 0, st>>>(k);
+            else k_postssa_gtile<TileCfgG, 32, 2><<<t.grid, 1024, 0, st>>>(k);
+        } else {
+            if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+            else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+            else k_postssa_gtile<TileCfgG, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+        }
         CUDA_OK(cudaGetLastError());
         return 0;
     }
@@ -1139,6 +1160,7 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     Grp<0> g; g.rank = 0; g.size = 1; g.red = nullptr;
     t_setup(g, P, k.pb);
     if (cls == 1) { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
+    else if (cls == 0) { static TileS<TileCfgG4> T; alignas(16) static uint8_t pl[128 * TileCfgG4::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; alignas(16) static uint8_t pl[128 * TileCfgG3::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; alignas(16) static uint8_t pl[128 * TileCfgG2::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else { static TileS<TileCfgG> T; alignas(16) static uint8_t pl[128 * TileCfgG::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
@@ -1188,6 +1210,7 @@ static int run(cl_ctx *c, KArgs k) {
         if (launch_part(c, 1, k, 3)) return -1;
     } else if (use_tiles) {
         if (launch_part(c, 1, k, 4, true)) return -1;     /* large functions outside the tiles: side stream */
+        if (launch_tiles(c, k, 0)) return -1;    /* one long block per tile: side stream, long poles first */
         if (launch_tiles(c, k, 1)) return -1;    /* CTA tiles: side stream, after the large functions */
         if (launch_tiles(c, k, 2)) return -1;    /* big L2-resident tiles */
         if (launch_part(c, 0, k, 2)) return -1;  /* small functions outside the tiles */

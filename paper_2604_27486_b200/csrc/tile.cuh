@@ -63,6 +63,9 @@ struct TileCfgG { static constexpr bool PP = true; static constexpr uint32_t I =
 struct TileCfgG2 { static constexpr bool PP = true; static constexpr uint32_t I = 8192, V = 14336, Q = 2560, F = 255, B = 255, M = 8192, S = 4096, X = 1024, E = 4096; };
 struct TileCfgG3 { static constexpr bool PP = true; static constexpr uint32_t I = 16384, V = 28672, Q = 5120, F = 255, B = 255, M = 16384, S = 8192, X = 2048, E = 8192; };
 
+/* one long unrolled block per tile: a 16 384-instruction block is ~19 500 records (positions stay below 65 536) */
+struct TileCfgG4 { static constexpr bool PP = true; static constexpr uint32_t I = 32768, V = 57344, Q = 10240, F = 255, B = 255, M = 32768, S = 16384, X = 4096, E = 16384; };
+
 /* the pattern table and what t_setup derives from it: shared by the tiles of a CTA */
 struct TileP {
     cl_pattern_blob pb;
@@ -971,62 +974,83 @@ template <class G, class C> CLF void t_tag(const G &g, TileS<C> &T) {
  * two hops, adds with two reciprocal operands and every exception path of the
  * reference are redone by the sequential kernel.                            */
 enum { RF_R0 = 1, RF_R1 = 2, RF_R2 = 4, RF_R3 = 8, RF_SEED = 16, RF_Q = 32, RF_MUFU = 128 };
+/* one byte of a per-record flag array (4-byte aligned) as an atomic OR; returns the byte before */
+CLD uint32_t t_flag_or(uint8_t *flags, uint32_t i, uint32_t bits) {
+    const uint32_t sh = (i & 3u) * 8u;
+    return (a_or((uint32_t *)flags + (i >> 2), bits << sh) >> sh) & 0xFFu;
+}
+/* backward propagation of "an F2I is reachable in <= k hops" over the def-use graph, level by level on work
+ * lists: W[w0, w1) holds the records that became reachable at the level before; the defining record of every
+ * value such a record reads becomes reachable one hop later.  Work is proportional to the cones of the F2I
+ * records, not to the tile.  `blocked`: records with RF_SEED in T.flag pass nothing on (paths through them
+ * do not count).  Returns the end of the list.                                                          */
+template <class G, class C> CLD uint32_t t_reach_levels(const G &g, TileS<C> &T, const TileG<C> &tg, uint8_t *fl, uint32_t *W,
+                                                        uint32_t w0, uint32_t w1, bool blocked) {
+    for (unsigned k = 1; k <= 3; k++) {
+        const uint32_t bits = (0xFu << k) & 0xFu, bit = 1u << k;
+        GFOR(g, q, w1 - w0) if (q < w1 - w0) {
+            const uint32_t i = W[w0 + q], f = T.fidx[i];
+            if (!T.f_rgate[f] || !tf_ok(T, f)) continue;
+            if (blocked && (T.flag[i] & RF_SEED)) continue;
+            t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) {
+                const uint32_t dp = v < C::V ? T.defpos[v] : NONE32;
+                if (dp == NONE32 || (fl[dp] & bit)) return;
+                const uint32_t before = t_flag_or(fl, dp, bits);
+                if (!(before & bit) && k < 3) W[a_append(&T.n_list)] = dp;      /* first to reach it */
+            });
+        }
+        g.sync();
+        w0 = w1; w1 = T.n_list;
+        g.sync();
+        if (w1 == w0) break;
+    }
+    return w1;
+}
 template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const TileG<C> &tg) {
     PROF(g, T.fs, PF_RECIP);
     const FS &s = T.fs;
-    /* only functions that hold a MUFU.RCP take part (f_rgate; cleared by t_load) */
-    bool mine = false;
-    GFOR(g, i, T.n) if (i < T.n) {
-        const cl_hdr h = T.hdr[i];
-        if (h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP)) { mine = true; T.f_rgate[T.fidx[i]] = 1; }
-    }
-    if (!g.any(mine)) return;
     if (!T.du_ok) t_usecount(g, T, tg);
     const uint32_t n = T.n;
-    uint32_t *valbits = T.redirect;
-    GFOR(g, v, T.vtot) if (v < T.vtot) valbits[v] = 0;
+    uint32_t *W = (uint32_t *)T.owner;                    /* [2 I] work lists (every record enters at most once per propagation) */
+    uint16_t *cands = T.outpos;                           /* [I] IADD / IADD3 records, candidates for the add of a chain          */
+    uint8_t *fl2 = T.clsid;                               /* [I] reach flags of the propagation that avoids the chain records    */
     GFOR(g, f, T.nf) if (f < T.nf) T.f_aux[f] = 0;
-    if (g.rank == 0) T.n_chain = 0;
-    /* R_0 and the MUFU.RCP records fed by an I2F */
+    if (g.rank == 0) { T.n_chain = 0; T.n_list = 0; T.work = 0; }
+    g.sync();
+    /* one sweep: R_0 (the F2I records, start of the work list), the MUFU.RCP records fed by an I2F (only functions
+     * holding one take part: f_rgate, cleared by t_load), the IADD / IADD3 records                                   */
+    bool mine = false;
     GFOR(g, i, n) if (i < n) {
         const uint32_t f = T.fidx[i];
-        if (!T.f_rgate[f]) continue;
         const cl_hdr h = T.hdr[i];
-        uint8_t fl = h.op == CL_OP_F2I ? (uint8_t)(RF_R0 | RF_R1 | RF_R2 | RF_R3) : (uint8_t)0;
-        if (h.op == CL_OP_MUFU && tf_ok(T, f) && has_mod(s, h, CL_MB_RCP) && h.n_uses) {
-            const opnd src = t_slot(T, i, use0(h));
-            if (is_value(src) && src.pay < C::V) {
-                const uint32_t dp = T.defpos[src.pay];
-                if (dp != NONE32 && T.hdr[dp].op == CL_OP_I2F) {
-                    if (!h.n_defs || !is_value(t_slot(T, i, def0(h)))) tf_fail(T, f, CL_ST_REDO + 9);   /* IndexError / AttributeError */
-                    else fl |= RF_MUFU;
+        uint8_t fl = 0;
+        if (h.op == CL_OP_F2I) { fl = (uint8_t)(RF_R0 | RF_R1 | RF_R2 | RF_R3); W[a_append(&T.n_list)] = i; }
+        else if (h.op == CL_OP_IADD || h.op == CL_OP_IADD3) cands[a_append(&T.work)] = (uint16_t)i;
+        else if (h.op == CL_OP_MUFU && has_mod(s, h, CL_MB_RCP)) {
+            T.f_rgate[f] = 1;
+            if (tf_ok(T, f) && h.n_uses) {
+                const opnd src = t_slot(T, i, use0(h));
+                if (is_value(src) && src.pay < C::V) {
+                    const uint32_t dp = T.defpos[src.pay];
+                    if (dp != NONE32 && T.hdr[dp].op == CL_OP_I2F) {
+                        if (!h.n_defs || !is_value(t_slot(T, i, def0(h)))) tf_fail(T, f, CL_ST_REDO + 9);   /* IndexError / AttributeError */
+                        else { fl |= RF_MUFU; mine = true; }
+                    }
                 }
             }
         }
-        T.flag[i] = fl;
+        T.flag[i] = fl; fl2[i] = fl & 0xFu;
     }
+    if (!g.any(mine)) return;
     g.sync();
-    for (unsigned k = 1; k <= 3; k++) {
-        const uint8_t prev = (uint8_t)(1u << (k - 1)), cur = (uint8_t)(1u << k);
-        GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && (T.flag[i] & prev)) {
-            if (!tf_ok(T, T.fidx[i])) continue;
-            t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) valbits[v] |= cur; });
-        }
-        g.sync();
-        GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && !(T.flag[i] & cur)) {
-            if (!tf_ok(T, T.fidx[i])) continue;
-            bool r = false;
-            t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { r |= v < C::V && (valbits[v] & cur); });
-            if (r) T.flag[i] |= (uint8_t)((0xFu << k) & 0xFu);        /* R_k implies R_k+1.. */
-        }
-        g.sync();
-    }
+    const uint32_t n_f2i = T.n_list, n_cand = T.work;
+    g.sync();
+    uint32_t w_end = t_reach_levels(g, T, tg, T.flag, W, 0, n_f2i, false);
     /* accepted chains */
-    GFOR(g, i, n) if (i < n) {
-        const uint32_t f = T.fidx[i];
+    GFOR(g, q, n_cand) if (q < n_cand) {
+        const uint32_t i = cands[q], f = T.fidx[i];
         if (!T.f_rgate[f] || !tf_ok(T, f)) continue;
         const cl_hdr h = T.hdr[i];
-        if (h.op != CL_OP_IADD && h.op != CL_OP_IADD3) continue;
         bool any_imm = false;
         const unsigned u0 = use0(h);
         for (unsigned k = 0; k < h.n_uses; k++) any_imm |= is_imm(t_slot(T, i, u0 + k));
@@ -1041,8 +1065,8 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
             hits++; mp = dp; rcp = v;
         });
         if (!hits) continue;
+        if (!(T.flag[i] & RF_R3)) continue;          /* no F2I within three hops before any rewrite, none after: rewrites only lengthen paths */
         if (hits > 1 || has_guard(h) || (h.flags & CL_IF_EXT)) { tf_fail(T, f, CL_ST_REDO + 10); continue; }
-        if (!(T.flag[i] & RF_R3)) continue;
         if (T.bidx[mp] != T.bidx[i] || !h.n_defs || !is_value(t_slot(T, i, def0(h)))) { tf_fail(T, f, CL_ST_REDO + 11); continue; }
         const uint32_t c = a_add(&T.n_chain, 1u);
         if (c < C::X) {
@@ -1051,58 +1075,34 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
             T.chain[c] = ch;
         } else
             T.fail = 1;
-        T.flag[i] |= RF_SEED;
-        T.flag[mp] |= RF_SEED;
+        t_flag_or(T.flag, i, RF_SEED);
+        t_flag_or(T.flag, mp, RF_SEED);
+        a_add(&T.f_aux[f], 1u);
     }
     g.sync();
     const uint32_t nc = T.n_chain;
     if (nc == 0 || T.fail) return;
+    /* interference.  The reference rewrites chain after chain on a rebuilt def-use graph, and a rewritten chain
+     * lengthens by one hop every path through the result of its add or of its MUFU.  A chain whose add reaches an
+     * F2I within three hops on a path that passes through NO record of an accepted chain (its own add is the
+     * start, not a passage) is accepted whatever was rewritten before it: reach flags of a second propagation in
+     * which the chain records pass nothing on (functions with one chain need none).  A chain that reaches its F2I
+     * only through other chains depends on their order: the function is redone by the sequential kernel.      */
+    bool multi = false;
+    GFOR(g, f, T.nf) if (f < T.nf) multi |= T.f_aux[f] > 1;
+    if (g.any(multi)) {
+        if (w_end + n_f2i > 2 * C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
+        GFOR(g, q, n_f2i) if (q < n_f2i) W[w_end + q] = W[q];
+        if (g.rank == 0) T.n_list = w_end + n_f2i;
+        g.sync();
+        t_reach_levels(g, T, tg, fl2, W, w_end, w_end + n_f2i, true);
+        GFOR(g, c, nc) if (c < nc) {
+            const TChain ch = T.chain[c];
+            if (T.f_aux[ch.f] > 1 && !(fl2[ch.add] & RF_R3)) T.flag[ch.add] |= RF_Q;
+        }
+        g.sync();
+    }
     GFOR(g, i, n) if (i < n) { T.keep[i] = 0; T.inscnt[i] = 0; }
-    /* interference.  _reaches_f2i reads the user lists of the records at distance 0..2 of the add it starts
-     * from (at distance 3 only the opcode), and a rewritten chain changes the user lists of its MUFU's and
-     * its add's results.  Chains are rewritten in (MUFU, add) position order, so chain B can only see a
-     * chain A of smaller order whose add or MUFU lies within two def-use hops of B's add.  Propagate, over
-     * two hops backwards, the smallest order of the seeds (adds and MUFUs of accepted chains) a record
-     * reaches: owner[i] = { low: own seed order, high: smallest order reached in one hop }.          */
-    uint32_t *mk1 = T.redirect, *mk2 = T.usecnt;
-    GFOR(g, v, T.vtot) if (v < T.vtot) { mk1[v] = NONE32; mk2[v] = NONE32; }
-    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]]) T.owner[i] = NONE64;
-    g.sync();
-    GFOR(g, c, nc) if (c < nc) {
-        const TChain ch = T.chain[c];
-        const uint32_t key = (uint32_t)ch.mufu << 16 | ch.add;
-        a_min32((uint32_t *)&T.owner[ch.add], key);           /* little endian: the low word */
-        a_min32((uint32_t *)&T.owner[ch.mufu], key);
-    }
-    g.sync();
-    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && (T.flag[i] & RF_SEED)) {
-        if (!tf_ok(T, T.fidx[i])) continue;
-        const uint32_t key = (uint32_t)T.owner[i];
-        t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) a_min32(&mk1[v], key); });
-    }
-    g.sync();
-    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]]) {
-        if (!tf_ok(T, T.fidx[i])) continue;
-        uint32_t q1 = NONE32;
-        t_value_defs(T, T.hdr[i], i, [&](uint32_t v) { if (v < C::V && mk1[v] < q1) q1 = mk1[v]; });
-        if (q1 != NONE32) T.owner[i] = (T.owner[i] & 0xFFFFFFFFull) | (unsigned long long)q1 << 32;
-    }
-    g.sync();
-    GFOR(g, i, n) if (i < n && T.f_rgate[T.fidx[i]] && T.owner[i] != NONE64) {
-        if (!tf_ok(T, T.fidx[i])) continue;
-        const uint32_t own = (uint32_t)T.owner[i], q1 = (uint32_t)(T.owner[i] >> 32);
-        const uint32_t key = own < q1 ? own : q1;
-        t_value_operands(T, tg, T.hdr[i], i, [&](uint32_t v) { if (v < C::V) a_min32(&mk2[v], key); });
-    }
-    g.sync();
-    GFOR(g, c, nc) if (c < nc) {
-        const TChain ch = T.chain[c];
-        const uint32_t key = (uint32_t)ch.mufu << 16 | ch.add;
-        uint32_t q = (uint32_t)(T.owner[ch.add] >> 32);
-        t_value_defs(T, T.hdr[ch.add], ch.add, [&](uint32_t v) { if (v < C::V && mk2[v] < q) q = mk2[v]; });
-        if (q < key) T.flag[ch.add] |= RF_Q;
-    }
-    g.sync();
     /* rank, ids, value table; vmap (usecnt[]) = add result -> its float view */
     GFOR(g, v, T.vtot) if (v < T.vtot) T.usecnt[v] = NONE32;
     g.sync();
@@ -1120,7 +1120,6 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         ch.rank = (uint16_t)(uint32_t)T.owner[ch.mufu];
         T.owner[ch.mufu] = ((T.owner[ch.mufu] >> 32) + 1) << 32 | c;
 #endif
-        a_add(&T.f_aux[ch.f], 1u);
     }
     g.sync();
     t_scan(g, n, [&](uint32_t j) { return T.f_rgate[T.fidx[j]] ? (uint32_t)(T.owner[j] >> 32) : 0u; },
@@ -1205,7 +1204,9 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
 /* capacities a function gets inside a tile (host planner and device agree)    */
 CLHD uint32_t tile_icap(uint32_t nrec) { return nrec + nrec / 2 + 8; }
 CLHD uint32_t tile_vcap(uint32_t nvid, uint32_t nrec) { return nvid + nrec + 8; }
-CLHD uint32_t tile_qcap(uint32_t nimm, uint32_t nrec) { return nimm + nrec / 2 + 8; }
+/* new immediates: the growth allowance flattens above 512 records (a 9 600-record block fits the 5 120 of a big
+ * tile); an overflow of the slice is detected and the function redone by the general kernel                    */
+CLHD uint32_t tile_qcap(uint32_t nimm, uint32_t nrec) { return nimm + (nrec <= 512 ? nrec / 2 : 256 + (nrec - 512) / 8) + 8; }
 
 struct TileIO {                /* the part of KArgs the tile kernel needs (see culifter.cu) */
     cl_corpus in;
@@ -1370,6 +1371,9 @@ template <class G, class C> CLF void t_store(const G &g, TileS<C> &T, const Tile
     TFuncOut *o_func = (TFuncOut *)a.o_func;
     GFOR(g, f, nf) if (f < nf) {
         if (T.f_stat[f] != 0) {
+#if !CL_DEV
+            if (getenv("CL_DEBUG_REDO")) fprintf(stderr, "tile hand-back: function %u (%u records) status %u\n", T.f_gf[f], T.f_nin[f], T.f_stat[f]);
+#endif
             if (T.f_nin[f] > a.small_max) a.retry_big_list[a_add(a.retry_big_count, 1u)] = T.f_gf[f];
             else a.retry_list[a_add(a.retry_count, 1u)] = T.f_gf[f];
             continue;
