@@ -69,6 +69,7 @@ def parse_args():
     ap.add_argument("--runners", type=int, default=2, help="e2e: run threads (kernels of two chunks back to back)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-objects", action="store_true", help="skip the objects-in / objects-out leg (e2e_objects)")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config legs (BASELINE.json configs[0..3])")
     ap.add_argument("--passes", type=int, default=15, help="CL_PASS_* mask of the headline leg")
     return ap.parse_args()
@@ -270,6 +271,42 @@ def config_legs(eng, peak, threads, steps, warmup, with_cpu):
     return out
 
 
+def objects_leg(eng, n_target=1_000_000):
+    """Objects in -> objects out: what a `sasslift` user of the drop-in sees.  LiftedFunction objects
+    (the synth_sm90 fixture of the reference's front half, unpickled as many times as it takes) -> soa.encode (C
+    encoder) -> cl_upload / cl_run_postssa / cl_download -> soa.apply (objects mutated in place)."""
+    import gzip
+    import pickle
+    from paper_2604_27486_b200 import soa
+    from paper_2604_27486_b200 import patterns as PT
+    blob = gzip.open(ROOT / "tests" / "golden" / "synth_sm90.pkl.gz", "rb").read()
+    one = pickle.loads(blob)["functions"]
+    lines = {id(i.raw) for fn in one for b in fn.block_order() for i in b.instructions if getattr(i, "raw", None) is not None}
+    recs = sum(len(b.instructions) for fn in one for b in fn.block_order())
+    n_sass_one = max(len(lines), 1)
+    copies = max(1, int(round(n_target / n_sass_one)))
+    fns = []
+    for _ in range(copies):
+        fns.extend(pickle.loads(blob)["functions"])
+    t0 = time.perf_counter()
+    corpus = soa.encode(fns)
+    t1 = time.perf_counter()
+    eng.upload(corpus)
+    eng.run_postssa()
+    out = eng.download()
+    t2 = time.perf_counter()
+    out.functions = fns
+    soa.apply(out, patterns=PT.pattern_list())
+    t3 = time.perf_counter()
+    n = n_sass_one * copies
+    return {"value": n / (t3 - t0), "unit": UNIT, "sass_insts": n, "ssa_records": recs * copies, "functions": len(fns),
+            "encode_inst_per_s": n / (t1 - t0), "device_inst_per_s": n / (t2 - t1), "decode_inst_per_s": n / (t3 - t2),
+            "seconds": {"encode": t1 - t0, "upload_run_download": t2 - t1, "apply": t3 - t2},
+            "path": "LiftedFunction objects -> soa.encode (csrc/codec.c) -> cl_upload + cl_run_postssa + cl_download -> soa.apply; one host thread",
+            "note": "bounded by building / reading Python objects (apply creates every operand object anew): the device stage is "
+                    "three orders of magnitude faster, which is why the batch API (e2e) takes encoded corpora"}
+
+
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", 0))
@@ -440,6 +477,11 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{int(ns2.sum())} SASS instructions ({sample_c.n_insts} records) of the same corpus, {sec:.1f} s"}
 
+    e2e_objects = None
+    if rank == 0 and world == 1 and not args.no_objects and args.workload == "mixed":
+        eng3 = Engine(device=local)
+        e2e_objects = objects_leg(eng3)
+        eng3.close()
     configs = None
     if rank == 0 and world == 1 and not args.no_configs and args.workload == "mixed":
         eng2 = Engine(device=local)
@@ -462,6 +504,7 @@ def main():
             "gpu_launches": int(part.get("launches", 0)) * args.steps,
             "partition": part,
             "match_counts": {"selected": int(n_sel), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())},
+            "e2e_objects": e2e_objects,
             "configs": configs,
         }
         print(json.dumps(line))

@@ -233,8 +233,49 @@ def _cuda_object_flags(inst):
     return kind << IF_OBJ_SHIFT | 7 << IF_OBJUSE_SHIFT
 
 
+def _load_codec():
+    """The C encoder (csrc/codec.c, built in-tree by ``__graft_entry__.build``)."""
+    try:
+        from . import _codec
+    except ImportError as e:
+        raise ImportError(
+            "paper_2604_27486_b200/_codec*.so is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (gcc, CPython headers)") from e
+    return _codec
+
+
 def encode(functions, raw: bool = False) -> Corpus:
-    """Pack functions (SSA/NORMALIZED phase, or RAW when ``raw``) into a corpus."""
+    """Pack functions (SSA/NORMALIZED phase, or RAW when ``raw``) into a corpus.
+
+    SSA-phase functions go through the C encoder (``csrc/codec.c``: the same
+    walk as :func:`encode_py`, about ten times faster; ``tests/test_codec.py``
+    holds the two byte-equal on every fixture).  RAW-phase corpora (the two
+    front-half passes) keep the Python walk."""
+    functions = list(functions)
+    if raw:
+        return encode_py(functions, raw=True)
+    z = _load_codec().encode(functions, TABLES, ARCHS, EncodeError)
+
+    def arr(name, dt, shape=None):
+        a = np.frombuffer(z[name], dtype=dt).copy()
+        return a.reshape(shape) if shape else a
+    cnt = arr("blk_cnt", np.uint32)
+    blk_off = np.zeros(len(cnt) + 1, np.uint32)
+    np.cumsum(cnt, out=blk_off[1:])
+    val_off = arr("val_off", np.uint32)
+    return Corpus(
+        func=arr("func", FUNC), func_blk_off=arr("func_blk_off", np.uint32), ext_off=arr("ext_off", np.uint32),
+        mem_off=arr("mem_off", np.uint32), imm_off=arr("imm_off", np.uint32), val_off=val_off,
+        blk=arr("blk", BLK), blk_off=blk_off, hdr=arr("hdr", HDR),
+        tag=arr("tag", np.uint16, (-1, SLOTS)), pay=arr("pay", np.uint32, (-1, SLOTS)),
+        ext_tag=arr("ext_tag", np.uint16), ext_pay=arr("ext_pay", np.uint32),
+        mem=arr("mem", MEMREF), imm=arr("imm", IMM),
+        val_alive=arr("val_alive", np.uint8), val_def_iid=arr("val_def_iid", np.int32),
+        val_origin=np.zeros(int(val_off[-1]), np.uint32), functions=functions, raw=False)
+
+
+def encode_py(functions, raw: bool = False) -> Corpus:
+    """The encoder as a plain Python walk: reference implementation of :func:`encode`, and the RAW-phase path."""
     functions = list(functions)
     F = len(functions)
     func = np.zeros(F, FUNC)
@@ -338,31 +379,48 @@ def encode(functions, raw: bool = False) -> Corpus:
 
 
 # ------------------------------------------------------------------- decoding
+class _Lists:
+    """The planes of a corpus as plain Python lists: element access on numpy
+    structured arrays costs more than building the operand objects."""
+
+    def __init__(self, c: Corpus):
+        H = c.hdr
+        self.iid, self.op, self.modset = H["iid"].tolist(), H["op"].tolist(), H["modset"].tolist()
+        self.nd, self.na, self.nu = H["n_defs"].tolist(), H["n_aux"].tolist(), H["n_uses"].tolist()
+        self.flags, self.ext = H["flags"].tolist(), H["ext"].tolist()
+        self.tag, self.pay = c.tag.tolist(), c.pay.tolist()
+        self.ext_tag, self.ext_pay = c.ext_tag.tolist(), c.ext_pay.tolist()
+        self.imm = list(zip(c.imm["bits"].tolist(), c.imm["text"].tolist()))
+        M = c.mem
+        self.mem = list(zip(M["base_tag"].tolist(), M["base_pay"].tolist(), M["ureg_tag"].tolist(),
+                            M["ureg_pay"].tolist(), M["off_hi"].tolist(), M["off_lo"].tolist()))
+
+
 class _FnDec:
-    def __init__(self, c: Corpus, f: int, ns):
+    def __init__(self, c: Corpus, f: int, ns, lists: _Lists = None):
+        L = lists or _Lists(c)
         self.ns = ns
-        self.imm = c.imm[c.imm_off[f]:c.imm_off[f + 1]]
-        self.mem = c.mem[c.mem_off[f]:c.mem_off[f + 1]]
-        self.ext_tag = c.ext_tag[c.ext_off[f]:c.ext_off[f + 1]]
-        self.ext_pay = c.ext_pay[c.ext_off[f]:c.ext_off[f + 1]]
+        self.L = L
+        self.q0, self.m0, self.e0 = int(c.imm_off[f]), int(c.mem_off[f]), int(c.ext_off[f])
 
 
 def decode_operand(tag, pay, fd: _FnDec):
     ns = fd.ns
-    tag, pay = int(tag), int(pay)
     kind = tag & 15
-    neg, bnot, absolute = bool(tag & T_NEG), bool(tag & T_NOT), bool(tag & T_ABS)
-    half = _HALF_INV[(tag >> T_HALF_SHIFT) & 3]
     if kind == K_VALUE:
-        return ns.ValueRef(pay, neg, absolute, bnot, half)
+        return ns.ValueRef(pay, bool(tag & T_NEG), bool(tag & T_ABS), bool(tag & T_NOT),
+                           _HALF_INV[(tag >> T_HALF_SHIFT) & 3])
+    neg = bool(tag & T_NEG)
     if kind == K_IMM:
-        bits, text = (int(x) for x in fd.imm[pay])
+        bits, text = fd.L.imm[fd.q0 + pay]
         s = hex(text) if tag & T_IMM_HEXTEXT else TABLES.strings[text]
         return ns.Imm(bits, s, bool(tag & T_IMM_FLOAT), neg)
+    bnot, absolute = bool(tag & T_NOT), bool(tag & T_ABS)
     if kind in (K_RZ, K_URZ):
         return ns.ZeroReg(kind == K_URZ, neg, bnot)
     if kind == K_PRED:
         return ns.Pred(pay, neg)
+    half = _HALF_INV[(tag >> T_HALF_SHIFT) & 3]
     if kind == K_REG:
         return ns.Reg(pay & 0xFFFF, pay >> 16, neg, absolute, bnot, half,
                       bool(tag & T_REUSE))
@@ -374,27 +432,25 @@ def decode_operand(tag, pay, fd: _FnDec):
     if kind == K_SREG:
         return ns.SReg(TABLES.strings[pay])
     if kind == K_MEMREF:
-        m = fd.mem[pay]
-        base = None if int(m["base_tag"]) & 15 == K_NONE else \
-            decode_operand(m["base_tag"], m["base_pay"], fd)
-        ureg = None if int(m["ureg_tag"]) & 15 == K_NONE else \
-            decode_operand(m["ureg_tag"], m["ureg_pay"], fd)
-        return ns.MemRef(base, ureg, int(m["off_hi"]) << 32 | int(m["off_lo"]))
+        bt, bp, ut, up, hi, lo = fd.L.mem[fd.m0 + pay]
+        base = None if bt & 15 == K_NONE else decode_operand(bt, bp, fd)
+        ureg = None if ut & 15 == K_NONE else decode_operand(ut, up, fd)
+        return ns.MemRef(base, ureg, hi << 32 | lo)
     raise ValueError(f"bad operand tag {tag:#x}")
 
 
 def decode_slots(c: Corpus, i: int, fd: _FnDec):
     """-> (guard, defs, aux, uses) operand objects of record ``i``."""
-    h = c.hdr[i]
-    flags = int(h["flags"])
-    nd, na, nu = int(h["n_defs"]), int(h["n_aux"]), int(h["n_uses"])
+    L = fd.L
+    flags = L.flags[i]
+    nd, na, nu = L.nd[i], L.na[i], L.nu[i]
     g = 1 if flags & IF_GUARD else 0
     total = g + nd + na + nu
     if flags & IF_EXT:
-        e = int(h["ext"])
-        tg, py = fd.ext_tag[e:e + total], fd.ext_pay[e:e + total]
+        e = fd.e0 + L.ext[i]
+        tg, py = L.ext_tag[e:e + total], L.ext_pay[e:e + total]
     else:
-        tg, py = c.tag[i], c.pay[i]
+        tg, py = L.tag[i], L.pay[i]
     ops = [decode_operand(tg[k], py[k], fd) for k in range(total)]
     guard = ops[0] if g else None
     return guard, ops[g:g + nd], ops[g + nd:g + nd + na], ops[g + nd + na:]
@@ -425,9 +481,12 @@ def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True) ->
     ev_by_func = {}
     for ev in c_out.events:          # cl_download returns them in append order
         ev_by_func.setdefault(int(ev["func"]), []).append(ev)
+    L = _Lists(c_out)
+    op_name, modset_tuple = TABLES.op_name, TABLES.modset_tuple
+    opcode_cache = {}
     for f, fn in enumerate(functions):
         fns = ns or _namespace_of(fn)
-        fd = _FnDec(c_out, f, fns)
+        fd = _FnDec(c_out, f, fns, L)
         if c_out.raw:
             old = {inst.iid: inst for inst in fn.raw_instructions}
             containers = [None]
@@ -440,23 +499,25 @@ def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True) ->
             lo, hi = int(c_out.blk_off[b0 + k]), int(c_out.blk_off[b0 + k + 1])
             out = []
             for i in range(lo, hi):
-                h = c_out.hdr[i]
                 guard, defs, aux, uses = decode_slots(c_out, i, fd)
-                opcode = fns.Opcode(TABLES.op_name[int(h["op"])],
-                                    TABLES.modset_tuple[int(h["modset"])])
-                inst = old.get(int(h["iid"]))
+                okey = (fns.Opcode, L.op[i], L.modset[i])          # Opcode is frozen: one object per (class, op, modifiers)
+                opcode = opcode_cache.get(okey)
+                if opcode is None:
+                    opcode = opcode_cache[okey] = fns.Opcode(op_name[L.op[i]], modset_tuple[L.modset[i]])
+                iid = L.iid[i]
+                inst = old.get(iid)
                 if inst is None:
-                    inst = fns.Instruction(int(h["iid"]), opcode, guard, defs, uses, aux)
+                    inst = fns.Instruction(iid, opcode, guard, defs, uses, aux)
                 else:
                     if inst.opcode != opcode:
                         inst.opcode = opcode
                     inst.guard, inst.defs, inst.aux_defs, inst.uses = guard, defs, aux, uses
-                flags = int(h["flags"])
+                flags = L.flags[i]
                 if flags & IF_SYNTH and "synthetic" not in inst.meta:
                     inst.meta["synthetic"] = "x4-scale" if opcode.base == "SHL" \
                         else "sr-substitute"
                     if inst.raw is None and not flags & IF_EXT:
-                        donor = old.get(int(h["ext"]))
+                        donor = old.get(L.ext[i])
                         inst.raw = donor.raw if donor is not None else None
                 obj = (flags >> IF_OBJ_SHIFT) & 3
                 if obj and tagged:
@@ -476,29 +537,30 @@ def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True) ->
                 rec = c_out.blk[b0 + k]
                 for j, attr in enumerate(("cond", "guard")):
                     if int(rec["term_tag"][j]) & 15 != K_NONE:
-                        setattr(term, attr, decode_operand(rec["term_tag"][j],
-                                                           rec["term_pay"][j], fd))
+                        setattr(term, attr, decode_operand(int(rec["term_tag"][j]),
+                                                           int(rec["term_pay"][j]), fd))
         # value table
         fr = c_out.func[f]
         v0 = int(c_out.val_off[f])
         nv_new = int(fr["next_vid"])
-        alive = c_out.val_alive[v0:v0 + nv_new]
-        defi = c_out.val_def_iid[v0:v0 + nv_new]
-        orig = c_out.val_origin[v0:v0 + nv_new]
+        alive = c_out.val_alive[v0:v0 + nv_new].tolist()
+        defi = c_out.val_def_iid[v0:v0 + nv_new].tolist()
+        orig = c_out.val_origin[v0:v0 + nv_new].tolist()
         new_origin = {}
+        values, nv_old = fn.values, fn._next_vid
         for vid in range(nv_new):
-            info = fn.values.get(vid)
-            if vid >= fn._next_vid:
+            info = values.get(vid)
+            if vid >= nv_old:
                 new_origin[vid] = _origin_string(fn, orig[vid], new_origin)
             if not alive[vid]:
                 if info is not None:
-                    del fn.values[vid]
+                    del values[vid]
                 continue
-            d = int(defi[vid])
+            d = defi[vid]
             if info is None:
-                if vid < fn._next_vid:
+                if vid < nv_old:
                     raise ValueError(f"{fn.name}: %v{vid} resurrected by decode")
-                fn.values[vid] = fns.ValueInfo(vid, new_origin[vid], None if d < 0 else d)
+                values[vid] = fns.ValueInfo(vid, new_origin[vid], None if d < 0 else d)
             else:
                 info.def_iid = None if d < 0 else d
         fn._next_vid = nv_new
