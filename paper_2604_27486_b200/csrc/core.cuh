@@ -1561,13 +1561,7 @@ template <class G> CLF void tag_cuda_objects(const G &g, FS &s) {
  *              + the inserted bitcasts chained from xhead[v]
  * where root(v) is the original value a renamed value (.bits / .f) took its
  * sites from -- and the group materialises the inserted records at the end. */
-#if !CL_DEV
-static unsigned long long g_dbg_refs = 0, g_dbg_chains = 0;
-#endif
 CLN bool rec_references(const FS &s, uint32_t i, uint32_t vid) {
-#if !CL_DEV
-    g_dbg_refs++;
-#endif
     const cl_hdr h = s.S.hdr[i];
     bool r = false;
     for_value_operands(s, h, i, [&](uint32_t v) { r |= v == vid; });
@@ -1620,6 +1614,49 @@ CLD uint32_t block_of(const FS &s, uint32_t pos) {
     while (lo + 1 < hi) { const uint32_t mid = (lo + hi) / 2; if (s.bo[mid] <= pos) lo = mid; else hi = mid; }
     return lo;
 }
+
+/* read-only dry run of one chain candidate (the MUFU.RCP at position i): its record, the use list of its result,
+ * those users (the adds), the use lists of their results and the records two hops on -- what the sequential
+ * rewrite and its _reaches_f2i walk will read.  Returns a digest so that the loads are not optimised away.  */
+#if CL_DEV
+CLN uint32_t recip_touch(const FS &s, uint32_t i, uint32_t nv) {
+    uint32_t acc = 0;
+    const cl_hdr h = s.S.hdr[i];
+    if (!h.n_defs || (h.flags & CL_IF_EXT)) return 0;
+    const opnd rcp = get_def(s, h, i, 0);
+    if (!is_value(rcp) || rcp.pay >= nv) return 0;
+    acc += s.xhead[rcp.pay] + s.root[rcp.pay];
+    uint32_t e0 = s.redirect[rcp.pay], e1 = s.redirect[rcp.pay + 1];
+    if (e1 > e0 + 16) e1 = e0 + 16;
+    for (uint32_t e = e0; e < e1; e++) {
+        const uint32_t p = s.site[e];
+        const cl_hdr ah = s.S.hdr[p];
+        acc += s.S.tag[(size_t)p * 8] + s.S.pay[(size_t)p * 8];
+        if ((ah.op != CL_OP_IADD && ah.op != CL_OP_IADD3) || !ah.n_defs || (ah.flags & CL_IF_EXT)) continue;
+        const opnd d = get_def(s, ah, p, 0);
+        if (!is_value(d) || d.pay >= nv) continue;
+        acc += s.xhead[d.pay] + s.root[d.pay];
+        uint32_t f0 = s.redirect[d.pay], f1 = s.redirect[d.pay + 1];
+        if (f1 > f0 + 16) f1 = f0 + 16;
+        for (uint32_t f = f0; f < f1; f++) {
+            const uint32_t p2 = s.site[f];
+            const cl_hdr h2 = s.S.hdr[p2];
+            acc += s.S.tag[(size_t)p2 * 8] + s.S.pay[(size_t)p2 * 8];
+            if (!h2.n_defs || (h2.flags & CL_IF_EXT)) continue;
+            const opnd d2 = get_def(s, h2, p2, 0);
+            if (!is_value(d2) || d2.pay >= nv) continue;
+            acc += s.xhead[d2.pay];
+            uint32_t q0 = s.redirect[d2.pay], q1 = s.redirect[d2.pay + 1];
+            if (q1 > q0 + 8) q1 = q0 + 8;
+            for (uint32_t q = q0; q < q1; q++) {
+                const uint32_t p3 = s.site[q];
+                acc += s.S.hdr[p3].op + s.S.tag[(size_t)p3 * 8] + s.S.pay[(size_t)p3 * 8];
+            }
+        }
+    }
+    return acc;
+}
+#endif
 
 template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
     PROF(g, s, PF_RECIP);
@@ -1674,8 +1711,32 @@ template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
         n_cand += t;
     }
     g.sync();
-    if (g.rank == 0) {
-        for (uint32_t ci_ = 0; ci_ < n_cand && !status(s); ci_++) {
+    /* The chains are rewritten by lane 0 in stream order (each sees the rewrites before it); one chain is ~70
+     * dependent loads, i.e. DRAM latency times 70.  The other warps run ahead of it: while lane 0 rewrites one
+     * batch of candidates they read what the next batch will read (recip_touch: a dry run without side effects),
+     * so that lane 0 finds its records, use lists and users in L1.                                           */
+    constexpr uint32_t BATCH = 64;
+    const uint32_t h0 = g.size > 32 ? 32u : 1u, nh = g.size > h0 ? (g.size - h0 < BATCH ? g.size - h0 : BATCH) : 0u;
+    auto touch = [&](uint32_t cb) {
+#if CL_DEV
+        if (g.rank >= h0 && g.rank < h0 + nh)
+            for (uint32_t k = g.rank - h0; k < BATCH && cb + k < n_cand; k += nh) {
+                const uint32_t acc = recip_touch(s, s.outpos[cb + k], nv);
+                asm volatile("" ::"r"(acc));
+            }
+#else
+        (void)cb; (void)h0; (void)nh;
+#endif
+    };
+    touch(0);
+    g.sync();
+    {
+    PROF(g, s, PF_SETUP);                       /* profile build: the sequential part of the pass */
+    for (uint32_t cb = 0; cb < n_cand; cb += BATCH) {
+      if (g.rank != 0) touch(cb + BATCH);
+      else {
+        const uint32_t ce = cb + BATCH < n_cand ? cb + BATCH : n_cand;
+        for (uint32_t ci_ = cb; ci_ < ce && !status(s); ci_++) {
             {
                 const uint32_t i = s.outpos[ci_], bi = block_of(s, i);
                 const cl_hdr h = s.S.hdr[i];
@@ -1708,10 +1769,6 @@ template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
                 }
                 for (uint32_t ai = 0; ai < n_adds && !status(s); ai++) {
                     const uint32_t a = adds[ai];
-#if !CL_DEV
-                    g_dbg_chains++;
-                    if (getenv("CL_DEBUG_REDO")) fprintf(stderr, "recip: chain query %llu, rec_references so far %llu (n=%u)\n", g_dbg_chains, g_dbg_refs, s.n);
-#endif
                     if (!Reach<3>::run(s, false, a)) continue;
                     if (nx + 2 > s.cap.X || vid + 2 > s.cap.V) { fail(s, CL_ST_CAPACITY); break; }
                     const cl_hdr ah = s.S.hdr[a];
@@ -1767,14 +1824,17 @@ template <class G> CLF void normalize_reciprocal(const G &g, FS &s) {
                 }
             }
         }
+      }
+      g.sync();
     }
-    g.sync();
+    }
     nx = g.bcast0(nx); vid = g.bcast0(vid); iid = g.bcast0(iid);
     if (status(s)) return;
     s.next_vid = vid; s.next_iid = iid;
     if (nx == 0) return;
     if (s.n + nx > s.cap.I) { fail(s, CL_ST_CAPACITY); g.sync(); return; }
     /* materialise: right-align, then expand leftwards in order */
+    PROF(g, s, 15);
     const uint32_t n = s.n, shift = s.cap.I - n;
     uint32_t run2 = 0;
     GFOR(g, i, n) {

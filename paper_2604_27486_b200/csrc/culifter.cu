@@ -496,6 +496,8 @@ template <class G, class C> CLF void tile_loop(const G &g, TileS<C> &T, const Ti
             T.hdr.a = (cl_hdr *)planes; T.hdr.b = (cl_hdr *)(planes + (size_t)16 * C::I);
             T.tag.a = (uint16_t *)(planes + (size_t)32 * C::I); T.tag.b = (uint16_t *)(planes + (size_t)48 * C::I);
             T.pay.a = (uint32_t *)(planes + (size_t)64 * C::I); T.pay.b = (uint32_t *)(planes + (size_t)96 * C::I);
+            T.fidx.a = planes + (size_t)128 * C::I; T.fidx.b = planes + (size_t)129 * C::I;
+            T.bidx.a = planes + (size_t)130 * C::I; T.bidx.b = planes + (size_t)131 * C::I;
         }
         s.S.hdr = T.hdr.ptr(); s.S.tag = T.tag.ptr(); s.S.pay = T.pay.ptr();
         s.usecnt = T.usecnt; s.defpos = T.defpos; s.redirect = T.redirect; s.origin = T.origin;
@@ -539,7 +541,7 @@ template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, 
 }
 /* big tiles resident in L2 (global scratch): a CTA is one group; scratch = stages, events, the tile, a second stream buffer */
 template <class C> CLHD size_t gtile_scratch_bytes() {
-    return tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255) + (((size_t)128 * C::I + 255) & ~(size_t)255);
+    return tile_scratch_bytes<C>() + ((sizeof(TileS<C>) + 255) & ~(size_t)255) + (((size_t)132 * C::I + 255) & ~(size_t)255);
 }
 template <class C, int NW, int MINB> __global__ void __launch_bounds__(NW * 32, MINB) k_postssa_gtile(KArgs a) {
     __shared__ TileP P;
@@ -716,7 +718,7 @@ struct cl_ctx {
         size_t scratch_per_group = 0; uint32_t grid = 0, groups = 0;
     } tc[3];                   /* [0]: one long block per tile (TileCfgG4), [1]: shared-memory tiles, [2]: big tiles in global scratch */
     int gtile_cfg = -1;        /* 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
-    int tile_mode_env = -1, gtile_cfg_env = -1, gtile_ctas = 2;   /* two 1024-thread CTAs per SM at 32 registers: +27 % over one at 64 (latency bound: resident warps are what counts) */
+    int tile_mode_env = -1, gtile_cfg_env = -1, gtile_ctas = 2, gtile_nw = 32;   /* two 1024-thread CTAs per SM at 32 registers: +27 % over one at 64 (latency bound: resident warps are what counts) */
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest, big_rest; /* small / large functions that are not in a tile */
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr, *d_big_rest = nullptr;
@@ -773,7 +775,8 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_FUSED")) c->fused_mode = atoi(e) != 0;
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 6;
     if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(2, std::max(0, atoi(e)));
-    if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(2, std::max(1, atoi(e)));
+    if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(4, std::max(1, atoi(e)));
+    if (const char *e = getenv("CL_GTILE_NW")) c->gtile_nw = atoi(e);
     void *p = nullptr;
     if (dmalloc(&p, sizeof(H_OPFLAGS))) { delete c; return -1; }
     c->d_opflags = (uint8_t *)p;
@@ -1141,7 +1144,10 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
         return 0;
     }
     if (cls == 2) {
-        if (c->gtile_ctas == 2) {
+        if (c->gtile_cfg == 2 && c->gtile_nw == 16 && c->gtile_ctas == 4) k_postssa_gtile<TileCfgG3, 16, 4><<<t.grid, 512, 0, st>>>(k);
+        else if (c->gtile_cfg == 2 && c->gtile_nw == 16 && c->gtile_ctas == 3) k_postssa_gtile<TileCfgG3, 16, 3><<<t.grid, 512, 0, st>>>(k);
+        else if (c->gtile_cfg == 2 && c->gtile_nw == 24 && c->gtile_ctas == 2) k_postssa_gtile<TileCfgG3, 24, 2><<<t.grid, 768, 0, st>>>(k);
+        else if (c->gtile_ctas == 2) {
             if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 2><<<t.grid, 1024, 0, st>>>(k);
             else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 2><<<t.grid, 1024, 0, st>>>(k);
             else k_postssa_gtile<TileCfgG, 32, 2><<<t.grid, 1024, 0, st>>>(k);
@@ -1160,10 +1166,10 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     Grp<0> g; g.rank = 0; g.size = 1; g.red = nullptr;
     t_setup(g, P, k.pb);
     if (cls == 1) { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
-    else if (cls == 0) { static TileS<TileCfgG4> T; alignas(16) static uint8_t pl[128 * TileCfgG4::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
-    else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; alignas(16) static uint8_t pl[128 * TileCfgG3::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
-    else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; alignas(16) static uint8_t pl[128 * TileCfgG2::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
-    else { static TileS<TileCfgG> T; alignas(16) static uint8_t pl[128 * TileCfgG::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
+    else if (cls == 0) { static TileS<TileCfgG4> T; alignas(16) static uint8_t pl[132 * TileCfgG4::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
+    else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; alignas(16) static uint8_t pl[132 * TileCfgG3::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
+    else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; alignas(16) static uint8_t pl[132 * TileCfgG2::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
+    else { static TileS<TileCfgG> T; alignas(16) static uint8_t pl[132 * TileCfgG::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     return 0;
 #endif
 }

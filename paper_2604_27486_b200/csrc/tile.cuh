@@ -37,6 +37,13 @@
 
 namespace clk {
 
+/* the two unify helpers: out of line by default (code size; the stage was instruction-fetch bound in round 1) */
+#ifdef CL_INLINE_UNIFY
+#define CLU CLD
+#else
+#define CLU CLN
+#endif
+
 /* a record removed by remove_dead_pseudo stays in place as a tombstone (no arities, no guard, an opcode id no table
  * ever hands out: layout.py caps ids below 0xFFFF) until the next rewrite permutation or the store drops it: no
  * compaction pass, positions and def-use stay valid                                                            */
@@ -104,7 +111,10 @@ template <class C> struct TileS {
     TMatch mt[C::M];
     TChain chain[C::X];
     uint16_t outpos[C::I], sel_at[C::I];
-    uint8_t keep[C::I], inscnt[C::I], clsid[C::I], fidx[C::I], bidx[C::I], flag[C::I];
+    uint8_t keep[C::I], inscnt[C::I], clsid[C::I], flag[C::I];
+    /* function / block index of every record: moved along by the permutations of a big tile (a second buffer
+     * each), recomputed from the block offsets (t_index) in a shared-memory tile                             */
+    PlaneT<uint8_t, C::I, C::PP> fidx, bidx;
     uint8_t alive[C::V];
     uint8_t mstate[C::M];
     /* blocks */
@@ -206,11 +216,12 @@ template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T,
                 *(uint4 *)&T.tag.b[(size_t)d * 8] = r1;
                 ((uint4 *)&T.pay.b[(size_t)d * 8])[0] = r2;
                 ((uint4 *)&T.pay.b[(size_t)d * 8])[1] = r3;
+                T.fidx.b[d] = T.fidx[i]; T.bidx.b[d] = T.bidx[i];
             }
         }
         g.sync();
         if (g.rank == 0) {
-            T.hdr.flip(); T.tag.flip(); T.pay.flip();
+            T.hdr.flip(); T.tag.flip(); T.pay.flip(); T.fidx.flip(); T.bidx.flip();
             T.fs.S.hdr = T.hdr.ptr(); T.fs.S.tag = T.tag.ptr(); T.fs.S.pay = T.pay.ptr();
         }
         g.sync();
@@ -337,7 +348,7 @@ template <class G, class C> CLF void t_usecount(const G &g, TileS<C> &T, const T
 
 /* ----------------------------------------------------------------- matching */
 /* operand_key equality (patterns.py:109-127) of two operands                   */
-template <class C> CLN bool t_key_equal(const TileS<C> &T, const TileG<C> &tg, opnd a, opnd b) {
+template <class C> CLU bool t_key_equal(const TileS<C> &T, const TileG<C> &tg, opnd a, opnd b) {
     unsigned ka = kind_of(a.tag), kb = kind_of(b.tag);
     if (ka == CL_K_URZ) ka = CL_K_RZ;
     if (kb == CL_K_URZ) kb = CL_K_RZ;
@@ -356,7 +367,7 @@ template <class C> CLN bool t_key_equal(const TileS<C> &T, const TileG<C> &tg, o
     return a.pay == b.pay;
 }
 /* _match_opcode + the slot-local part of _unify (patterns.py:155-178, :130-152) */
-template <class C> CLN bool t_match_local(const TileS<C> &T, const cl_template &t, const cl_hdr &h, uint32_t i) {
+template <class C> CLU bool t_match_local(const TileS<C> &T, const cl_template &t, const cl_hdr &h, uint32_t i) {
     if (h.op != t.op) return false;
     const cl_modset &ms = T.fs.ms[h.modset];
     if ((ms.mask & t.mods_all) != t.mods_all) return false;
@@ -620,7 +631,7 @@ template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T) {
 
 /* fix-up of one staged match once the bases are known (apply_stage of core.cuh
  * without the in-place retag, which the caller does before the stream moves)   */
-template <class C> CLF void t_apply_stage(TileS<C> &T, Stage &st, uint32_t out) {
+template <class C> CLF void t_apply_stage(TileS<C> &T, Stage &st, uint32_t out, uint32_t f, uint32_t blk) {
     for (unsigned k = 0; k < st.nv; k++) {
         const uint32_t v = st.vbase + k;
         if (v >= C::V) continue;
@@ -636,6 +647,7 @@ template <class C> CLF void t_apply_stage(TileS<C> &T, Stage &st, uint32_t out) 
         h.iid = st.ibase + q.iid; h.op = q.op; h.modset = q.modset;
         h.n_defs = q.n_defs; h.n_aux = 0; h.n_uses = q.n_uses; h.flags = 0; h.ext = 0;
         T.hdr[o] = h;
+        T.fidx[o] = (uint8_t)f; T.bidx[o] = (uint8_t)blk;
         const unsigned ns = (unsigned)q.n_defs + q.n_uses;
 #pragma unroll
         for (unsigned k = 0; k < 8; k++) {
@@ -771,13 +783,15 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     /* staged records to their place, value table, immediates */
     GFOR(g, j, ns) if (j < ns) {
         const SelRec m = T.sel[j];
-        if (!tf_ok(T, T.fidx[m.pos[0]])) continue;
-        t_apply_stage(T, tg.stage[j], T.outpos[m.pos[m.n - 1]]);
+        uint32_t f;                                  /* m.pos[] are positions before the permutation */
+        if constexpr (C::PP) f = T.fidx.b[m.pos[0]]; else f = T.fidx[m.pos[0]];
+        if (!tf_ok(T, f)) continue;
+        t_apply_stage(T, tg.stage[j], T.outpos[m.pos[m.n - 1]], f, m.blk);
     }
     g.sync();
     t_rebase_blocks(g, T, n, tot);
     if (g.rank == 0) T.tombs = 0;
-    t_index(g, T);
+    if constexpr (!C::PP) t_index(g, T);
     /* for simplify_packs / remove_dead_pseudo of this round.  (Keeping def-use valid across the permutation instead --
      * remapping defpos through outpos, moving the use counts of removed / inserted records -- was measured: no gain.) */
     t_usecount(g, T, tg);
@@ -791,7 +805,7 @@ template <class G, class C> CLF void t_compact(const G &g, TileS<C> &T, const Ti
     g.sync();
     t_permute(g, T, tg, n, tot, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] : NONE32; });
     t_rebase_blocks(g, T, n, tot);
-    t_index(g, T);
+    if constexpr (!C::PP) t_index(g, T);
 }
 
 /* remove_dead_pseudo (patterns.py:771-791) for the functions with f_gate set.  The first sweep visits the
@@ -1006,6 +1020,96 @@ template <class G, class C> CLD uint32_t t_reach_levels(const G &g, TileS<C> &T,
     }
     return w1;
 }
+/* The chains the two propagations leave undecided (an F2I within three hops, but only on paths through other
+ * chains), decided exactly and in the reference's order (MUFU position, then add position).  What an accepted
+ * chain A changes for a later one (_insert_reciprocal_bitcasts, patterns.py:863-888): the result of its add is
+ * read through the new BITCAST.I2F by every top-level use (guards and address bases keep reading it directly),
+ * and its add reads the MUFU result through the new BITCAST.F2I: those def-use edges count two hops.  Chain B
+ * is accepted iff an F2I lies within weighted distance three of its add, with the chains accepted before it as
+ * the two-hop edges: three sweeps over the function's records per chain (cost 0, 1, 2 frontiers), whole CTA.
+ * Rejected chains leave the list; returns its new length.                                                 */
+static constexpr uint32_t T_MAX_UNDECIDED = 32;
+template <class G, class C> CLF uint32_t t_decide_chains(const G &g, TileS<C> &T, const TileG<C> &tg, uint32_t *ul, uint32_t n_u,
+                                                         uint32_t nc, uint8_t *cost) {
+    uint32_t *vcost = T.redirect;                        /* [V] cost of the record defining the value, NONE32 = not reached */
+    uint16_t *chain_of = T.sel_at;                       /* [I] chain whose add the record is, 0xFFFF = none */
+    auto key_of = [&](const TChain &c) { return (uint32_t)c.mufu << 16 | c.add; };
+    GFOR(g, i, T.n) if (i < T.n) chain_of[i] = 0xFFFFu;
+    g.sync();
+    GFOR(g, c, nc) if (c < nc) { TChain &ch = T.chain[c]; chain_of[ch.add] = (uint16_t)c; ch.ok = (T.flag[ch.add] & RF_Q) ? 2 : 1; }
+    if (g.rank == 0)                                     /* a handful: insertion sort by chain order */
+        for (uint32_t a = 1; a < n_u; a++) {
+            const uint32_t x = ul[a]; uint32_t b = a;
+            while (b > 0 && key_of(T.chain[ul[b - 1]]) > key_of(T.chain[x])) { ul[b] = ul[b - 1]; b--; }
+            ul[b] = x;
+        }
+    g.sync();
+    for (uint32_t q = 0; q < n_u; q++) {
+        const uint32_t cb = ul[q];
+        const TChain B = T.chain[cb];
+        const uint32_t f = B.f, kb = key_of(B);
+        if (!tf_ok(T, f)) continue;                      /* uniform: every lane reads the same word after the sync */
+        const uint32_t i0 = T.bo[T.f_b0[f]], i1 = T.bo[T.f_b0[f + 1]], v0 = T.f_vbase[f], v1 = T.f_vbase[f + 1];
+        GFOR(g, v, v1 - v0) if (v < v1 - v0) vcost[v0 + v] = NONE32;
+        GFOR(g, i, i1 - i0) if (i < i1 - i0) cost[i0 + i] = 0xFF;
+        if (g.rank == 0) T.work = 0;
+        g.sync();
+        if (g.rank == 0) cost[B.add] = 0;
+        g.sync();
+        for (uint32_t c = 0; c < 3; c++) {
+            GFOR(g, i, i1 - i0) if (i < i1 - i0 && cost[i0 + i] == c)
+                t_value_defs(T, T.hdr[i0 + i], i0 + i, [&](uint32_t v) { if (v < C::V) vcost[v] = c; });
+            g.sync();
+            GFOR(g, ii, i1 - i0) if (ii < i1 - i0) {
+                const uint32_t u = i0 + ii;
+                const cl_hdr h = T.hdr[u];
+                uint32_t best = 0xFF;
+                auto edge = [&](uint32_t v, bool top) {
+                    if (v >= C::V || vcost[v] != c) return;
+                    const uint32_t r = T.defpos[v];
+                    uint32_t w = 1;
+                    if (r != NONE32 && top) {
+                        const uint32_t ca = chain_of[r];           /* r is the add of an accepted earlier chain */
+                        if (ca != 0xFFFFu && T.chain[ca].ok == 1 && key_of(T.chain[ca]) < kb) w = 2;
+                        const uint32_t cu = chain_of[u];           /* u is the add of one, reading its MUFU's result */
+                        if (cu != 0xFFFFu && T.chain[cu].ok == 1 && key_of(T.chain[cu]) < kb && T.chain[cu].mufu == r && T.chain[cu].rcp == v) w = 2;
+                    }
+                    if (c + w < best) best = c + w;
+                };
+                if (has_guard(h)) { const opnd gd = t_slot(T, u, 0); if (is_value(gd)) edge(gd.pay, false); }
+                const unsigned u0 = use0(h);
+                for (unsigned k = 0; k < h.n_uses; k++) {
+                    const opnd x = t_slot(T, u, u0 + k);
+                    if (is_value(x)) edge(x.pay, true);
+                    else if (kind_of(x.tag) == CL_K_MEMREF) {
+                        const cl_memref &m = tg.mem[x.pay];
+                        if (kind_of(m.base_tag) == CL_K_VALUE) edge(m.base_pay, false);
+                        if (kind_of(m.ureg_tag) == CL_K_VALUE) edge(m.ureg_pay, false);
+                    }
+                }
+                if (best <= 3) {
+                    if (h.op == CL_OP_F2I) T.work = 1;
+                    else if (best < cost[u]) cost[u] = (uint8_t)best;
+                }
+            }
+            g.sync();
+        }
+        if (g.rank == 0) { T.chain[cb].ok = T.work ? 1 : 0; T.flag[B.add] &= (uint8_t)~RF_Q; }
+        g.sync();
+    }
+    /* rejected chains leave the list (ordered compaction by one lane: the list is short work next to the sweeps) */
+    if (g.rank == 0) {
+        uint32_t w = 0;
+        for (uint32_t c = 0; c < nc; c++) {
+            const TChain ch = T.chain[c];
+            if (ch.ok == 0) { T.f_aux[ch.f]--; T.flag[ch.add] &= (uint8_t)~RF_SEED; continue; }
+            T.chain[w] = ch; T.chain[w].ok = 1; w++;
+        }
+        T.n_chain = w;
+    }
+    g.sync();
+    return T.n_chain;
+}
 template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const TileG<C> &tg) {
     PROF(g, T.fs, PF_RECIP);
     const FS &s = T.fs;
@@ -1080,7 +1184,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         a_add(&T.f_aux[f], 1u);
     }
     g.sync();
-    const uint32_t nc = T.n_chain;
+    uint32_t nc = T.n_chain;
     if (nc == 0 || T.fail) return;
     /* interference.  The reference rewrites chain after chain on a rebuilt def-use graph, and a rewritten chain
      * lengthens by one hop every path through the result of its add or of its MUFU.  A chain whose add reaches an
@@ -1089,6 +1193,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
      * which the chain records pass nothing on (functions with one chain need none).  A chain that reaches its F2I
      * only through other chains depends on their order: the function is redone by the sequential kernel.      */
     bool multi = false;
+    uint32_t nc_final = nc;
     GFOR(g, f, T.nf) if (f < T.nf) multi |= T.f_aux[f] > 1;
     if (g.any(multi)) {
         if (w_end + n_f2i > 2 * C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
@@ -1096,12 +1201,18 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         if (g.rank == 0) T.n_list = w_end + n_f2i;
         g.sync();
         t_reach_levels(g, T, tg, fl2, W, w_end, w_end + n_f2i, true);
+        if (g.rank == 0) T.n_list = 0;
+        g.sync();
+        uint32_t *ul = W;                                     /* the undecided chains (the work lists are done) */
         GFOR(g, c, nc) if (c < nc) {
             const TChain ch = T.chain[c];
-            if (T.f_aux[ch.f] > 1 && !(fl2[ch.add] & RF_R3)) T.flag[ch.add] |= RF_Q;
+            if (T.f_aux[ch.f] > 1 && !(fl2[ch.add] & RF_R3) && tf_ok(T, ch.f)) { T.flag[ch.add] |= RF_Q; ul[a_append(&T.n_list)] = c; }
         }
         g.sync();
+        const uint32_t n_u = T.n_list;
+        if (n_u && n_u <= T_MAX_UNDECIDED) nc_final = t_decide_chains(g, T, tg, ul, n_u, nc, fl2);
     }
+    nc = nc_final;
     GFOR(g, i, n) if (i < n) { T.keep[i] = 0; T.inscnt[i] = 0; }
     /* rank, ids, value table; vmap (usecnt[]) = add result -> its float view */
     GFOR(g, v, T.vtot) if (v < T.vtot) T.usecnt[v] = NONE32;
@@ -1190,6 +1301,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
             h.iid = iid + q; h.op = CL_OP_BITCAST; h.modset = q ? CL_MS_I2F : CL_MS_F2I;
             h.n_defs = 1; h.n_aux = 0; h.n_uses = 1; h.flags = 0; h.ext = 0;
             T.hdr[o] = h;
+            T.fidx[o] = (uint8_t)f; T.bidx[o] = T.bidx[(uint32_t)T.outpos[ch.add] + 1u];      /* the add itself sits between the two */
             for (unsigned k = 0; k < 8; k++) { T.tag[(size_t)o * 8 + k] = k < 2 ? (uint16_t)CL_K_VALUE : (uint16_t)0; T.pay[(size_t)o * 8 + k] = 0; }
             T.pay[(size_t)o * 8] = vi + q; T.pay[(size_t)o * 8 + 1] = q ? ch.addv : ch.rcp;
         }
@@ -1197,7 +1309,7 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
     g.sync();
     GFOR(g, f, T.nf) if (f < T.nf && T.f_aux[f] && tf_ok(T, f)) { T.f_nvid[f] += 2u * T.f_aux[f]; T.f_niid[f] += 2u * T.f_aux[f]; }
     t_rebase_blocks(g, T, n, tot);
-    t_index(g, T);
+    if constexpr (!C::PP) t_index(g, T);
 }
 
 /* ------------------------------------------------------------ load / store */
