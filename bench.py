@@ -339,9 +339,21 @@ def main():
     import torch.distributed as dist
     from paper_2604_27486_b200.capi import Engine
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # CL_BENCH_SIM=1: dry run of the rank plumbing without a GPU (tests/test_bench_contract.py): the one-lane CPU build
+    # of the device code as the engine, gloo instead of NCCL; its numbers mean nothing and the line says "sim"
+    sim = os.environ.get("CL_BENCH_SIM") == "1"
+    dev = "cpu" if sim else "cuda"
+    if sim:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import helpers
+        sim_lib = helpers.build_sim()
+        args.no_e2e = args.no_cpu = args.no_configs = args.no_objects = True
+        if world > 1:
+            dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        if world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t0 = time.time()
     kinds, pools, kid, pick, ns, nb, shard = plan_shards(args.workload, n_total, args.seed, world)
     mine = np.nonzero(shard == rank)[0]
@@ -350,26 +362,33 @@ def main():
     n_sass_all = int(ns.sum())
     t_gen = time.time() - t0
 
-    eng = Engine(device=local)
+    eng = Engine(sim_lib) if sim else Engine(device=local)
     eng.upload(corpus)
-    counts = torch.zeros(68, dtype=torch.int64, device="cuda")
+    counts = torch.zeros(68, dtype=torch.int64, device=dev)
 
     class _Raw:           # device counters of the library as a CUDA array (no host copy)
         def __init__(self, ptr):
             self.__cuda_array_interface__ = {"shape": (68,), "typestr": "<i8", "data": (ptr, False), "version": 3}
-    lib_counts = torch.as_tensor(_Raw(eng.device_counts_ptr()), device="cuda")
+    if sim:
+        import ctypes
+        lib_counts = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_int64 * 68).from_address(eng.device_counts_ptr())))
+    else:
+        lib_counts = torch.as_tensor(_Raw(eng.device_counts_ptr()), device="cuda")
+
+    gathered = [None]
 
     def step():
         eng.run_postssa(args.passes)
         if world > 1:                      # the only inter-GPU traffic: match counters
             counts.copy_(lib_counts)
-            allgather_counts(counts, world)
+            gathered[0] = allgather_counts(counts, world)
         return eng.last_run_ms()
 
     def fence():
         if world > 1:
             dist.barrier()
-        torch.cuda.synchronize()
+        if not sim:
+            torch.cuda.synchronize()
 
     for _ in range(args.warmup):
         step()
@@ -381,6 +400,8 @@ def main():
             dev_ms.append(step())
         fence()
         wall = time.perf_counter() - t1
+    if sim:
+        dev_ms = [wall / args.steps * 1e3] * args.steps         # the CPU build has no device clock
     st = eng.stats()
     part = eng.debug_partition() or {}
     if os.environ.get("CL_PROF") and rank == 0:
@@ -390,7 +411,7 @@ def main():
     n_out = int(st["n_inst_out"])
     n_sel = int(st["selected"].sum())
     # max over ranks of the device time of the K steps
-    t_dev = torch.tensor([sum(dev_ms) / 1e3, wall], dtype=torch.float64, device="cuda")
+    t_dev = torch.tensor([sum(dev_ms) / 1e3, wall], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
     t_dev_s, t_wall_s = (float(x) for x in t_dev.cpu())
@@ -488,11 +509,17 @@ def main():
         configs = config_legs(eng2, peak, threads, max(2, min(args.steps, 3)), max(3, args.warmup), not args.no_cpu)
         eng2.close()
 
+    # whole-job match counters: this rank's at N = 1, the sum of the allgathered rows of the last step at N > 1
+    whole_job = {"selected": int(n_sel), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())}
+    if world > 1 and gathered[0] is not None:
+        tot = gathered[0].sum(dim=0).cpu().numpy()
+        whole_job = {"selected": int(tot[16:32].sum()), "rewrites": int(tot[32:48].sum()), "refused": int(tot[48:64].sum()),
+                     "per_rank_selected": [int(r[16:32].sum()) for r in gathered[0].cpu().numpy()]}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_dev_s / args.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u32", "data": "synthetic",
+            "dtype": "u32", "data": "synthetic" if not sim else "synthetic (CL_BENCH_SIM dry run on the CPU build: numbers are not measurements)",
             "config": {"workload": f"{args.workload}-{n_sass_all / 1e6:.1f}M SASS instructions (BASELINE.json configs[4]: "
                                    f"40% sm90 / 40% sm75 / 20% sm52 kernels + long-block kernels), full post-SSA stage",
                        "kernels": int(len(kid)), "ssa_records_rank0": int(corpus.n_insts), "sass_rank0": n_sass_rank,
@@ -503,7 +530,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": int(part.get("launches", 0)) * args.steps,
             "partition": part,
-            "match_counts": {"selected": int(n_sel), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())},
+            "match_counts": whole_job,
             "e2e_objects": e2e_objects,
             "configs": configs,
         }

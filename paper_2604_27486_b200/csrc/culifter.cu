@@ -718,7 +718,7 @@ struct cl_ctx {
         size_t scratch_per_group = 0; uint32_t grid = 0, groups = 0;
     } tc[3];                   /* [0]: one long block per tile (TileCfgG4), [1]: shared-memory tiles, [2]: big tiles in global scratch */
     int gtile_cfg = -1;        /* 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
-    int tile_mode_env = -1, gtile_cfg_env = -1, gtile_ctas = 2, gtile_nw = 32;   /* two 1024-thread CTAs per SM at 32 registers: +27 % over one at 64 (latency bound: resident warps are what counts) */
+    int tile_mode_env = -1, gtile_cfg_env = -1, gtile_ctas = 2;   /* two 1024-thread CTAs per SM at 32 registers: +27 % over one at 64 (latency bound: resident warps are what counts) */
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest, big_rest; /* small / large functions that are not in a tile */
     uint32_t *d_tile_flist = nullptr, *d_rest = nullptr, *d_big_rest = nullptr;
@@ -775,8 +775,7 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_FUSED")) c->fused_mode = atoi(e) != 0;
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 6;
     if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(2, std::max(0, atoi(e)));
-    if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(4, std::max(1, atoi(e)));
-    if (const char *e = getenv("CL_GTILE_NW")) c->gtile_nw = atoi(e);
+    if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(2, std::max(1, atoi(e)));
     void *p = nullptr;
     if (dmalloc(&p, sizeof(H_OPFLAGS))) { delete c; return -1; }
     c->d_opflags = (uint8_t *)p;
@@ -1144,10 +1143,7 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
         return 0;
     }
     if (cls == 2) {
-        if (c->gtile_cfg == 2 && c->gtile_nw == 16 && c->gtile_ctas == 4) k_postssa_gtile<TileCfgG3, 16, 4><<<t.grid, 512, 0, st>>>(k);
-        else if (c->gtile_cfg == 2 && c->gtile_nw == 16 && c->gtile_ctas == 3) k_postssa_gtile<TileCfgG3, 16, 3><<<t.grid, 512, 0, st>>>(k);
-        else if (c->gtile_cfg == 2 && c->gtile_nw == 24 && c->gtile_ctas == 2) k_postssa_gtile<TileCfgG3, 24, 2><<<t.grid, 768, 0, st>>>(k);
-        else if (c->gtile_ctas == 2) {
+        if (c->gtile_ctas == 2) {
             if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 2><<<t.grid, 1024, 0, st>>>(k);
             else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 2><<<t.grid, 1024, 0, st>>>(k);
             else k_postssa_gtile<TileCfgG, 32, 2><<<t.grid, 1024, 0, st>>>(k);

@@ -26,3 +26,37 @@ def test_reference_arm_other_ranks_do_nothing():
                          capture_output=True, text=True, timeout=120, check=True,
                          env={**__import__("os").environ, "RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}).stdout
     assert out.strip() == ""
+
+
+def test_two_rank_bench_line_on_the_cpu_build(tmp_path):
+    """`torchrun --nproc-per-node 2 bench.py --gpus 2` end to end without a GPU (CL_BENCH_SIM=1: one-lane CPU build of
+    the device code, gloo): rank environment, LPT shard plan, the allgather of the match counters after every step,
+    max-over-ranks timing and ONE JSON line from rank 0 with the contract's keys.  The whole-job counters must equal
+    the single-rank run of the same corpus: the shards partition it."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, CL_BENCH_SIM="1", MASTER_ADDR="127.0.0.1")
+    common = ["bench.py", "--steps", "1", "--warmup", "1", "--insts", "60000", "--seed", "7"]
+    lines = {}
+    for n in (1, 2):
+        cmd = ([sys.executable] if n == 1 else
+               [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                "--master-port", "29641"]) + common + ["--gpus", str(n)]
+        out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        js = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+        assert len(js) == 1, out.stdout                      # rank 0 alone prints
+        lines[n] = json.loads(js[0])
+    two, one = lines[2], lines[1]
+    assert two["n_gpus"] == 2 and two["scaling"] == "strong" and "dry run" in two["data"]
+    for key in ("metric", "value", "unit", "steps", "warmup", "ms_per_step", "higher_is_better", "vs_baseline", "dtype", "config", "roofline", "gpu_launches"):
+        assert key in two, key
+    assert two["config"]["kernels"] == one["config"]["kernels"]
+    assert two["config"]["sass_rank0"] < one["config"]["sass_rank0"]          # rank 0 holds its shard only
+    for key in ("selected", "rewrites", "refused"):                            # counters are whole-job sums
+        assert two["match_counts"][key] == one["match_counts"][key], key
+    assert sum(two["match_counts"]["per_rank_selected"]) == one["match_counts"]["selected"]
