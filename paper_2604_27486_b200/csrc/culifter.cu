@@ -774,7 +774,7 @@ extern "C" int cl_create(int device, cl_ctx **out) {
     if (const char *e = getenv("CL_SMALL_MAX")) c->small_max = (uint32_t)atoi(e);   /* the few knobs the tests and the tuning log use */
     if (const char *e = getenv("CL_FUSED")) c->fused_mode = atoi(e) != 0;
     if (const char *e = getenv("CL_TILE")) c->tile_mode_env = atoi(e) & 6;
-    if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(2, std::max(0, atoi(e)));
+    if (const char *e = getenv("CL_GTILE_CFG")) c->gtile_cfg_env = std::min(3, std::max(0, atoi(e)));
     if (const char *e = getenv("CL_GTILE_CTAS")) c->gtile_ctas = std::min(2, std::max(1, atoi(e)));
     void *p = nullptr;
     if (dmalloc(&p, sizeof(H_OPFLAGS))) { delete c; return -1; }
@@ -954,9 +954,11 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             if (c->tile_mode_env >= 0) c->tile_mode = c->tile_mode_env;
         }
         const int gc = c->gtile_cfg;
-        const uint32_t gI = gc == 2 ? TileCfgG3::I : gc == 1 ? TileCfgG2::I : TileCfgG::I, gV = gc == 2 ? TileCfgG3::V : gc == 1 ? TileCfgG2::V : TileCfgG::V,
-                       gQ = gc == 2 ? TileCfgG3::Q : gc == 1 ? TileCfgG2::Q : TileCfgG::Q, gB = gc == 2 ? TileCfgG3::B : gc == 1 ? TileCfgG2::B : TileCfgG::B,
-                       gF = gc == 2 ? TileCfgG3::F : gc == 1 ? TileCfgG2::F : TileCfgG::F;
+        const uint32_t gI = gc == 3 ? TileCfgG4::I : gc == 2 ? TileCfgG3::I : gc == 1 ? TileCfgG2::I : TileCfgG::I,
+                       gV = gc == 3 ? TileCfgG4::V : gc == 2 ? TileCfgG3::V : gc == 1 ? TileCfgG2::V : TileCfgG::V,
+                       gQ = gc == 3 ? TileCfgG4::Q : gc == 2 ? TileCfgG3::Q : gc == 1 ? TileCfgG2::Q : TileCfgG::Q,
+                       gB = gc == 3 ? TileCfgG4::B : gc == 2 ? TileCfgG3::B : gc == 1 ? TileCfgG2::B : TileCfgG::B,
+                       gF = gc == 3 ? TileCfgG4::F : gc == 2 ? TileCfgG3::F : gc == 1 ? TileCfgG2::F : TileCfgG::F;
         /* functions of each tile class in order of decreasing size (counting sort by record count, stable in
          * function order: the same packing as round 1's stable_sort, without its n log n)                    */
         std::vector<uint8_t> cls_of(F, 0xFF);
@@ -1030,7 +1032,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
                 t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm, t.tiles.size());
                 t.groups = t.grid;
             } else {
-                t.scratch_per_group = c->gtile_cfg == 2 ? gtile_scratch_bytes<TileCfgG3>() : c->gtile_cfg == 1 ? gtile_scratch_bytes<TileCfgG2>() : gtile_scratch_bytes<TileCfgG>();
+                t.scratch_per_group = c->gtile_cfg == 3 ? gtile_scratch_bytes<TileCfgG4>() : c->gtile_cfg == 2 ? gtile_scratch_bytes<TileCfgG3>() : c->gtile_cfg == 1 ? gtile_scratch_bytes<TileCfgG2>() : gtile_scratch_bytes<TileCfgG>();
                 t.grid = (uint32_t)std::min<size_t>((size_t)c->n_sm * c->gtile_ctas, t.tiles.size());
                 t.groups = t.grid;
             }
@@ -1144,7 +1146,8 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     }
     if (cls == 2) {
         if (c->gtile_ctas == 2) {
-            if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 2><<<t.grid, 1024, 0, st>>>(k);
+            if (c->gtile_cfg == 3) k_postssa_gtile<TileCfgG4, 32, 2><<<t.grid, 1024, 0, st>>>(k);
+            else if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 2><<<t.grid, 1024, 0, st>>>(k);
             else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 2><<<t.grid, 1024, 0, st>>>(k);
             else k_postssa_gtile<TileCfgG, 32, 2><<<t.grid, 1024, 0, st>>>(k);
         } else {

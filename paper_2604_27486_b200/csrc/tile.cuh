@@ -1210,6 +1210,9 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
         }
         g.sync();
         const uint32_t n_u = T.n_list;
+#if !CL_DEV
+        if (n_u && getenv("CL_DEBUG_REDO")) fprintf(stderr, "tile reciprocal: %u chain(s) of %u undecided by the propagations\n", n_u, nc);
+#endif
         if (n_u && n_u <= T_MAX_UNDECIDED) nc_final = t_decide_chains(g, T, tg, ul, n_u, nc, fl2);
     }
     nc = nc_final;
