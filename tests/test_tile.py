@@ -78,3 +78,32 @@ def test_tile_cuda_repeatable(cuda_tile_engine):
         outs.append(o)
     assert not helpers.corpora_equal(outs[0], outs[1])
     assert not helpers.corpora_equal(outs[0], outs[2])
+
+
+# Order-dependent reciprocal chains (tests/golden/chains.pkl.gz, tools/make_chain_golden.py): a chain that reaches its F2I
+# only through another chain's add is accepted or rejected by what was rewritten before it.  The tile path decides these
+# inside the tile (t_decide_chains); the expected states are the reference's own, and nothing may be handed back.
+def _chains_through(engine):
+    problems = helpers.check_fixture(engine, "chains")
+    assert not problems, "\n".join(problems[:3])
+    part = engine.debug_partition()
+    assert part["used_tiles"] == 1 and part["handed_back"] == 0, part
+    fix = helpers.load_fixture("chains")
+    rewritten = {fn.name: len(e["boundaries"]) for fn, e in zip(fix["functions"], fix["expect"])}
+    # the cases differ in what the reference decided: both outcomes of the ordered decision are in the fixture
+    assert rewritten["b_rejected"] == 1 and rewritten["b_accepted"] == 2 and rewritten["b_first"] == 2 and rewritten["a_unreachable"] == 0, rewritten
+
+
+def test_ordered_chain_decisions_sim_tiles(sim_tile_engine):
+    _chains_through(sim_tile_engine)
+
+
+@pytest.mark.parametrize("cfg", [2])
+def test_ordered_chain_decisions_sim_big_tiles(cfg):
+    _chains_through(helpers._engine_with_env(helpers.build_sim(), CL_FUSED=0, CL_TILE=4, CL_GTILE_CFG=cfg))
+
+
+@pytest.mark.gpu
+def test_ordered_chain_decisions_cuda(cuda_tile_engine):
+    _chains_through(cuda_tile_engine)
+    _chains_through(helpers._engine_with_env(None, CL_FUSED=0, CL_TILE=4, CL_GTILE_CFG=2))

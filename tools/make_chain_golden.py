@@ -56,13 +56,10 @@ def main():
     text = "".join(listing(n, body) for n, body in chain_cases())
     for fn in R.ssa_functions(text, "sm90"):
         fns.append(fn)
-    fix = MG.fixture_of("chains", fns, 15) if hasattr(MG, "fixture_of") else None
-    if fix is None:
-        raise SystemExit("make_golden has no fixture_of(): see tools/make_golden.py")
-    with gzip.open(ROOT / "tests" / "golden" / "chains.pkl.gz", "wb") as fh:
-        pickle.dump(fix, fh)
-    for fn, exp in zip(fns, fix["expect"]):
-        print(fn.name, "boundaries:", len(exp.get("meta", {}).get("pattern_boundaries", [])) if isinstance(exp, dict) else "?")
+    MG.write("chains", fns, 15)
+    fix = pickle.load(gzip.open(ROOT / "tests" / "golden" / "chains.pkl.gz", "rb"))
+    for fn, exp in zip(fix["functions"], fix["expect"]):
+        print(fn.name, "->", "error " + exp["error"] if "error" in exp else f"{len(exp.get('pattern_boundaries', []))} chain(s) rewritten: {exp.get('pattern_boundaries')}")
 
 
 if __name__ == "__main__":
