@@ -296,7 +296,7 @@ def objects_leg(eng, n_target=1_000_000):
     out = eng.download()
     t2 = time.perf_counter()
     out.functions = fns
-    soa.apply(out, patterns=PT.pattern_list())
+    soa.apply(out, patterns=PT.pattern_list(), c_in=corpus)
     t3 = time.perf_counter()
     n = n_sass_one * copies
     return {"value": n / (t3 - t0), "unit": UNIT, "sass_insts": n, "ssa_records": recs * copies, "functions": len(fns),
@@ -438,8 +438,8 @@ def main():
     roofline.update({"traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                      "kernel": ("k_fused (one function resident in shared memory per warp group) with the per-function kernels for what it hands back: the whole stage, rank 0"
                                 if part.get("tile_mode") == 16 else
-                                "k_postssa_gtile (tile kernel: small kernels packed into tiles of up to 16 384 records) with k_postssa_cta (long-block "
-                                "kernels) beside it, k_postssa_warp_sync for what the tile kernel hands back and the densify kernels: the whole stage, rank 0")})
+                                "k_postssa_gtile<TileCfgG3,32,2> (tile kernel: kernels packed into tiles of up to 16 384 records, a long block a tile of its own; "
+                                "two 1024-thread CTAs per SM) with the per-function kernels for what it hands back and the densify kernels: the whole stage, rank 0")})
 
     # end to end through the public batch API with pinned HOST buffers: the corpus flows chunk by chunk
     # (contiguous function ranges) through a few contexts, so H2D, kernels and D2H of different chunks overlap

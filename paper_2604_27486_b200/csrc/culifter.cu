@@ -717,7 +717,7 @@ struct cl_ctx {
         TileDesc *d_tiles = nullptr; uint32_t *d_counter = nullptr; uint8_t *d_scratch = nullptr;
         size_t scratch_per_group = 0; uint32_t grid = 0, groups = 0;
     } tc[3];                   /* [0]: one long block per tile (TileCfgG4), [1]: shared-memory tiles, [2]: big tiles in global scratch */
-    int gtile_cfg = -1;        /* 0/1/2: TileCfgG/G2/G3 (4096/8192/16384 records), -1: by corpus size */
+    int gtile_cfg = -1;        /* 0/1/2/3: TileCfgG/G2/G3/G4 (4096/8192/16384/32768 records), -1: by corpus size */
     int tile_mode_env = -1, gtile_cfg_env = -1, gtile_ctas = 2;   /* two 1024-thread CTAs per SM at 32 registers: +27 % over one at 64 (latency bound: resident warps are what counts) */
     std::vector<uint32_t> tile_flist;    /* function ids of all tiles, class 0 first */
     std::vector<uint32_t> rest, big_rest; /* small / large functions that are not in a tile */
@@ -948,7 +948,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
             n_sm = c->n_sm;
 #endif
             const uint64_t per_sm = n_small / (uint64_t)n_sm;
-            c->gtile_cfg = per_sm >= 3 * 9800 ? 2 : per_sm >= 3 * 4900 ? 1 : 0;
+            c->gtile_cfg = per_sm >= 3 * 19600 ? 3 : per_sm >= 3 * 9800 ? 2 : per_sm >= 3 * 4900 ? 1 : 0;
             c->tile_mode = per_sm >= 3 * 2450 ? 4 : 2;
             if (c->gtile_cfg_env >= 0) c->gtile_cfg = c->gtile_cfg_env;
             if (c->tile_mode_env >= 0) c->tile_mode = c->tile_mode_env;
@@ -1151,7 +1151,8 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
             else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 2><<<t.grid, 1024, 0, st>>>(k);
             else k_postssa_gtile<TileCfgG, 32, 2><<<t.grid, 1024, 0, st>>>(k);
         } else {
-            if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+            if (c->gtile_cfg == 3) k_postssa_gtile<TileCfgG4, 32, 1><<<t.grid, 1024, 0, st>>>(k);
+            else if (c->gtile_cfg == 2) k_postssa_gtile<TileCfgG3, 32, 1><<<t.grid, 1024, 0, st>>>(k);
             else if (c->gtile_cfg == 1) k_postssa_gtile<TileCfgG2, 32, 1><<<t.grid, 1024, 0, st>>>(k);
             else k_postssa_gtile<TileCfgG, 32, 1><<<t.grid, 1024, 0, st>>>(k);
         }
@@ -1166,6 +1167,7 @@ static int launch_tiles(cl_ctx *c, KArgs k, int cls) {
     t_setup(g, P, k.pb);
     if (cls == 1) { static TileS<TileCfgL> T; g.red = T.red; tile_loop(g, T, P, k, 0); }
     else if (cls == 0) { static TileS<TileCfgG4> T; alignas(16) static uint8_t pl[132 * TileCfgG4::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
+    else if (c->gtile_cfg == 3) { static TileS<TileCfgG4> T; alignas(16) static uint8_t pl[132 * TileCfgG4::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else if (c->gtile_cfg == 2) { static TileS<TileCfgG3> T; alignas(16) static uint8_t pl[132 * TileCfgG3::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else if (c->gtile_cfg == 1) { static TileS<TileCfgG2> T; alignas(16) static uint8_t pl[132 * TileCfgG2::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }
     else { static TileS<TileCfgG> T; alignas(16) static uint8_t pl[132 * TileCfgG::I]; g.red = T.red; tile_loop(g, T, P, k, 0, pl); }

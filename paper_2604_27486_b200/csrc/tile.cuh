@@ -140,6 +140,7 @@ template <class C> struct TileS {
     uint32_t du_ok, n_list;       /* du_ok: usecnt / defpos describe the stream (every live function) */
     uint32_t tombs;               /* the stream holds tombstones */
     uint32_t red[40];
+    uint32_t pcnt[CL_MAX_PATTERNS], pcur[CL_MAX_PATTERNS];     /* t_sort_by_pattern: items per pattern, fill cursors */
 };
 
 template <class C> struct TileG {      /* what lives outside shared memory */
@@ -474,6 +475,34 @@ template <class C> CLF void t_try_anchor(TileS<C> &T, const TileG<C> &tg, unsign
     a_add(&T.f_stats[f][pi], 1u);
 }
 
+/* Counting sort of n work items by pattern (key(k) < CL_MAX_PATTERNS), so that the lanes of a warp run one pattern's
+ * code: a histogram and a fill pass, the lanes of a warp that hold the same pattern found by match-any and served by ONE
+ * atomic of their leader.  The order inside a pattern is free (matches are keyed, plans are per match); round 1 ran one
+ * ordered compaction -- a CTA-wide scan with two barriers per 1024 items -- PER PATTERN here.                    */
+template <class G, class C, class FK, class FO> CLD void t_sort_by_pattern(const G &g, TileS<C> &T, uint32_t n, FK key, FO out) {
+    GFOR(g, p, CL_MAX_PATTERNS) if (p < CL_MAX_PATTERNS) T.pcnt[p] = 0;
+    g.sync();
+#if CL_DEV
+    auto grouped_add = [&](uint32_t *ctr, unsigned pi) -> uint32_t {      /* slot of this lane among the lanes of its pattern */
+        const unsigned peers = __match_any_sync(__activemask(), pi);
+        const unsigned lane = threadIdx.x & 31u;
+        const int lead = __ffs((int)peers) - 1;
+        uint32_t base = 0;
+        if ((int)lane == lead) base = atomicAdd(&ctr[pi], (uint32_t)__popc(peers));
+        base = __shfl_sync(peers, base, lead);
+        return base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+    };
+#else
+    auto grouped_add = [&](uint32_t *ctr, unsigned pi) -> uint32_t { return ctr[pi]++; };
+#endif
+    GFOR(g, k, n) if (k < n) grouped_add(T.pcnt, key(k));
+    g.sync();
+    if (g.rank == 0) { uint32_t run = 0; for (unsigned p = 0; p < CL_MAX_PATTERNS; p++) { T.pcur[p] = run; run += T.pcnt[p]; } }
+    g.sync();
+    GFOR(g, k, n) if (k < n) out(k, grouped_add(T.pcur, key(k)));
+    g.sync();
+}
+
 template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const TileG<C> &tg, unsigned table) {
     PROF(g, T.fs, PF_MATCH);
     GFOR(g, k, T.nb * MAX_CLS) if (k < T.nb * MAX_CLS) (&T.ccnt[0][0])[k] = 0;
@@ -549,13 +578,7 @@ template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const Tile
      * lanes active in the slot tests)                                                                      */
     uint32_t *sorted = (uint32_t *)tg.stage;                 /* free until the rewrites are planned */
     static_assert(sizeof(Stage) * C::S >= 8 * C::I, "staging area holds the sorted work items");
-    uint32_t base = 0;
-    for (unsigned pi = 0; pi < T.P->pb.n_patterns; pi++) {
-        if (T.P->pb.p[pi].table != table) continue;
-        base += t_scan(g, n_items, [&](uint32_t k) { return (uint32_t)((items[k] >> 16) == pi); },
-                       [&](uint32_t k, uint32_t x) { if ((items[k] >> 16) == pi) sorted[base + x] = items[k]; });
-    }
-    g.sync();
+    t_sort_by_pattern(g, T, n_items, [&](uint32_t k) { return items[k] >> 16; }, [&](uint32_t k, uint32_t at) { sorted[at] = items[k]; });
     GFOR(g, k, n_items) if (k < n_items) {
         const uint32_t it = sorted[k], i = it & 0xFFFFu;
         const uint32_t f = T.fidx[i];
@@ -686,15 +709,7 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     /* plan: one lane per selected match, once; lanes take the matches in pattern order (one ordered compaction
      * per pattern), so that a warp runs one rewrite's code: in select order the planners ran at 2-4 active lanes */
     uint32_t *porder = (uint32_t *)T.owner;                  /* free between the selection and the id scans */
-    {
-        uint32_t base = 0;
-        for (unsigned pi = 0; pi < T.P->pb.n_patterns; pi++) {
-            if (T.P->pb.p[pi].table != table) continue;
-            base += t_scan(g, ns, [&](uint32_t j) { return (uint32_t)(T.sel[j].pat == pi); },
-                           [&](uint32_t j, uint32_t x) { if (T.sel[j].pat == pi) porder[base + x] = j; });
-        }
-        g.sync();
-    }
+    t_sort_by_pattern(g, T, ns, [&](uint32_t j) { return (uint32_t)T.sel[j].pat; }, [&](uint32_t j, uint32_t at) { porder[at] = j; });
     GFOR(g, jq, ns) if (jq < ns) {
         const uint32_t j = porder[jq];
         const SelRec m = T.sel[j];

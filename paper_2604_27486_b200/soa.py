@@ -468,7 +468,52 @@ def _origin_string(fn, code: int, new_origin: dict) -> str:
 _OBJ_KINDS = {1: "block_sync", 2: "warp_group", 3: "collective"}
 
 
-def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True) -> None:
+def unchanged_records(c_in: Corpus, c_out: Corpus) -> np.ndarray:
+    """bool per record of ``c_out``: the stage left it exactly as ``c_in`` had it (same function, same iid, same 64
+    bytes, and the MemRef entries / immediates it points at untouched), so the host object it was encoded from still
+    says the same and ``apply`` need not rebuild its operands.  Vectorised over the whole corpus."""
+    n_out = c_out.n_insts
+    if c_in.n_funcs != c_out.n_funcs or c_in.raw != c_out.raw or n_out == 0 or c_in.n_insts == 0:
+        return np.zeros(n_out, bool)
+
+    def func_of(c):
+        first = c.blk_off[c.func_blk_off].astype(np.int64)                  # first record of every function, then the end
+        return np.repeat(np.arange(c.n_funcs, dtype=np.int64), np.diff(first))
+    f_in, f_out = func_of(c_in), func_of(c_out)
+    k_in = f_in << 32 | c_in.hdr["iid"].astype(np.int64)
+    k_out = f_out << 32 | c_out.hdr["iid"].astype(np.int64)
+    order = np.argsort(k_in, kind="stable")
+    pos = np.searchsorted(k_in[order], k_out)
+    pos[pos >= len(order)] = 0
+    src = order[pos]
+    same = k_in[src] == k_out
+    row = lambda a: np.ascontiguousarray(a).view(np.uint8).reshape(len(a), a.dtype.itemsize)          # noqa: E731
+    same &= (row(c_in.hdr)[src] == row(c_out.hdr)).all(axis=1)
+    same &= (c_in.tag[src] == c_out.tag).all(axis=1) & (c_in.pay[src] == c_out.pay).all(axis=1)
+    same &= (c_out.hdr["flags"] & IF_EXT) == 0                                          # overflow slots: always decoded
+    # what the operands point at: MemRef entries (simplify_packs redirects their bases) and immediates
+    kinds = c_out.tag & 15
+    if len(c_in.mem) == len(c_out.mem) and np.array_equal(c_in.mem_off, c_out.mem_off):
+        mem_same = (row(c_in.mem) == row(c_out.mem)).all(axis=1)
+        is_mem = kinds == K_MEMREF
+        if is_mem.any():
+            r, k = np.nonzero(is_mem)
+            bad = ~mem_same[c_out.mem_off[f_out[r]].astype(np.int64) + c_out.pay[r, k]]
+            same[r[bad]] = False
+    else:
+        same &= ~(kinds == K_MEMREF).any(axis=1)
+    is_imm = kinds == K_IMM
+    if is_imm.any():
+        r, k = np.nonzero(is_imm)
+        gi = c_in.imm_off[f_out[r]].astype(np.int64) + c_out.pay[r, k]
+        go = c_out.imm_off[f_out[r]].astype(np.int64) + c_out.pay[r, k]
+        ok = (c_out.pay[r, k] < (c_in.imm_off[f_out[r] + 1] - c_in.imm_off[f_out[r]]))      # an immediate the input had
+        ok[ok] &= (row(c_in.imm)[gi[ok]] == row(c_out.imm)[go[ok]]).all(axis=1)
+        same[r[~ok]] = False
+    return same
+
+
+def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True, c_in: Corpus = None) -> None:
     """Write a processed corpus back into its ``LiftedFunction`` objects in place.
 
     Surviving instructions keep their identity (``raw``, ``meta``); operands and
@@ -482,6 +527,7 @@ def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True) ->
     for ev in c_out.events:          # cl_download returns them in append order
         ev_by_func.setdefault(int(ev["func"]), []).append(ev)
     L = _Lists(c_out)
+    keep_as_is = unchanged_records(c_in, c_out).tolist() if c_in is not None else None
     op_name, modset_tuple = TABLES.op_name, TABLES.modset_tuple
     opcode_cache = {}
     for f, fn in enumerate(functions):
@@ -499,6 +545,12 @@ def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True) ->
             lo, hi = int(c_out.blk_off[b0 + k]), int(c_out.blk_off[b0 + k + 1])
             out = []
             for i in range(lo, hi):
+                if keep_as_is is not None and keep_as_is[i]:
+                    inst = old.get(L.iid[i])
+                    # untouched by the stage: the object it was encoded from is already what the record says
+                    if inst is not None and not ((L.flags[i] >> IF_OBJ_SHIFT) & 3 and tagged):
+                        out.append(inst)
+                        continue
                 guard, defs, aux, uses = decode_slots(c_out, i, fd)
                 okey = (fns.Opcode, L.op[i], L.modset[i])          # Opcode is frozen: one object per (class, op, modifiers)
                 opcode = opcode_cache.get(okey)

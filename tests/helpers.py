@@ -115,7 +115,11 @@ def run_postssa(engine, functions, passes=15, **kw):
     engine.run_postssa(passes, **kw)
     out = engine.download()
     out.stats = engine.stats().copy()
-    soa.apply(out, functions, patterns=pattern_list(), tagged=bool(passes & 8))
+    # as gpu_normalize does it: records the stage left untouched keep their host objects (c_in); CL_TEST_FULL_DECODE=1
+    # rebuilds every operand instead (tests/test_codec.py compares the two)
+    import os
+    soa.apply(out, functions, patterns=pattern_list(), tagged=bool(passes & 8),
+              c_in=None if os.environ.get("CL_TEST_FULL_DECODE") else corpus)
     return corpus, out
 
 

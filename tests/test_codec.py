@@ -51,3 +51,22 @@ def test_encoder_errors_are_loud():
     inst.uses[0] = object()
     with pytest.raises(soa.EncodeError):
         soa.encode(fns)
+
+
+@pytest.mark.parametrize("name", ["bundled", "synth_sm90", "synth_sm52", "synth_long", "chains"])
+def test_apply_keeping_untouched_records_equals_full_decode(name, monkeypatch):
+    """soa.apply(c_in=...) skips the records the stage left byte-identical; the objects must come out as from a full decode"""
+    from paper_2604_27486_b200 import ir
+    fix = helpers.load_fixture(name)
+    eng = helpers.sim_engine()
+    dumps, kept = [], []
+    for full in (False, True):
+        fns = copy.deepcopy(fix["functions"])
+        if full:
+            monkeypatch.setenv("CL_TEST_FULL_DECODE", "1")
+        corpus, out = helpers.run_postssa(eng, fns, fix["passes"])
+        dumps.append([(ir.dump(fn), sorted(fn.values), fn._next_vid, fn._next_iid, fn.meta.get("cuda_objects"), fn.meta.get("pattern_boundaries"))
+                      for fn in fns])
+        kept.append(int(soa.unchanged_records(corpus, out).sum()))
+    assert dumps[0] == dumps[1]
+    assert kept[0] > 0                                   # the shortcut is actually taken

@@ -36,7 +36,7 @@ def test_tile_logic_sim(sim_tile_engine, oracle_engine, kind, n_sass):
     _check(sim_tile_engine, oracle_engine, kind, n_sass, seed=11)
 
 
-@pytest.mark.parametrize("cfg", [0, 2])
+@pytest.mark.parametrize("cfg", [0, 2, 3])
 def test_big_tile_logic_sim(oracle_engine, cfg):
     """the big-tile form the GPU uses at scale (planes in scratch, flipped by every permutation), forced on the
     one-lane build: 4096- and 16384-record tiles"""
