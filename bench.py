@@ -438,7 +438,7 @@ def main():
     roofline.update({"traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                      "kernel": ("k_fused (one function resident in shared memory per warp group) with the per-function kernels for what it hands back: the whole stage, rank 0"
                                 if part.get("tile_mode") == 16 else
-                                "k_postssa_gtile<TileCfgG3,32,2> (tile kernel: kernels packed into tiles of up to 16 384 records, a long block a tile of its own; "
+                                "k_postssa_gtile<TileCfgG4,32,2> (tile kernel: kernels packed into tiles of up to 32 768 records / 255 kernels, a long block a tile of its own; "
                                 "two 1024-thread CTAs per SM) with the per-function kernels for what it hands back and the densify kernels: the whole stage, rank 0")})
 
     # end to end through the public batch API with pinned HOST buffers: the corpus flows chunk by chunk

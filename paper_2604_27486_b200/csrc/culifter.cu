@@ -1037,7 +1037,7 @@ extern "C" int cl_upload(cl_ctx *c, const cl_corpus *in) {
                 t.groups = t.grid;
             }
 #else
-            t.scratch_per_group = k == 1 ? tile_scratch_bytes<TileCfgL>() : k == 0 ? tile_scratch_bytes<TileCfgG4>() : tile_scratch_bytes<TileCfgG3>();
+            t.scratch_per_group = k == 1 ? tile_scratch_bytes<TileCfgL>() : tile_scratch_bytes<TileCfgG4>();      /* the largest configuration */
             t.grid = t.groups = 1;
 #endif
             if (dput(c, T_ID[k], &t.d_tiles, t.tiles.data(), t.tiles.size())) return -1;

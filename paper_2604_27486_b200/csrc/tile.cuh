@@ -295,15 +295,16 @@ template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T,
 
 /* running exclusive scan over items [0, n) in order; returns the total        */
 template <class G, class FIN, class FOUT> CLD uint32_t t_scan(const G &g, uint32_t n, FIN in, FOUT out) {
-    uint32_t run = 0;
-    GFOR(g, j, n) {
-        const uint32_t x = j < n ? in(j) : 0u;
-        uint32_t t;
-        const uint32_t o = g.exscan(x, t);
-        if (j < n) out(j, run + o);
-        run += t;
-    }
-    return run;
+    /* every lane owns a contiguous run of items: its sum, ONE scan of the sums over the group, then the run again.
+     * (Round 1 scanned chunk by chunk, two barriers per 1024 items: a 12 000-record tile paid 24 per scan.)   */
+    const uint32_t per = (n + g.size - 1) / g.size;
+    const uint32_t lo = g.rank * per < n ? g.rank * per : n, hi = lo + per < n ? lo + per : n;
+    uint32_t sum = 0;
+    for (uint32_t j = lo; j < hi; j++) sum += in(j);
+    uint32_t total;
+    uint32_t run = g.exscan(sum, total);
+    for (uint32_t j = lo; j < hi; j++) { const uint32_t x = in(j); out(j, run); run += x; }
+    return total;
 }
 
 /* new block offsets after a permutation described by outpos[] (position of the
@@ -506,11 +507,12 @@ template <class G, class C, class FK, class FO> CLD void t_sort_by_pattern(const
 template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const TileG<C> &tg, unsigned table) {
     PROF(g, T.fs, PF_MATCH);
     GFOR(g, k, T.nb * MAX_CLS) if (k < T.nb * MAX_CLS) (&T.ccnt[0][0])[k] = 0;
-    if (g.rank == 0) T.n_mt = 0;
+    if (g.rank == 0) { T.n_mt = 0; T.n_list = 0; }
     g.sync();
     /* seed classes (FindSeeds) and the dense list of (anchor, pattern) work items, in stream order */
     uint32_t *items = (uint32_t *)T.owner;                   /* [2 * C::I]: free until t_select */
-    uint32_t n_items = 0;
+    /* the list of (anchor, pattern) work items; its order is free (the counting sort below groups it by pattern, matches
+     * are keyed by position), so a warp reserves room for its items with one atomic: no CTA-wide scan, no barrier */
     GFOR(g, i, T.n) {
         uint32_t pm = 0;
         if (i < T.n) {
@@ -528,20 +530,26 @@ template <class G, class C> CLF void t_match(const G &g, TileS<C> &T, const Tile
             }
             T.clsid[i] = (uint8_t)c;
         }
-        uint32_t tot;
+        uint32_t w;
 #if CL_DEV
-        const uint32_t off = g.exscan((uint32_t)__popc(pm), tot);
+        const uint32_t cnt = (uint32_t)__popc(pm), lane = threadIdx.x & 31u;
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) { const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d); if (lane >= (uint32_t)d) incl += t; }
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        uint32_t base = 0;
+        if (lane == 31 && tot) base = atomicAdd(&T.n_list, tot);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31);
+        w = base + incl - cnt;
 #else
         uint32_t cnt = 0; for (uint32_t q = pm; q; q &= q - 1) cnt++;
-        const uint32_t off = g.exscan(cnt, tot);
+        w = T.n_list; T.n_list += cnt;
 #endif
-        if (n_items + tot <= 2 * C::I) {
-            uint32_t w = n_items + off;
-            for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) items[w++] = i | pi << 16;
-        } else if (g.rank == 0)
-            T.fail = 1;
-        n_items += tot;
+        if (w + cnt <= 2 * C::I) { for (unsigned pi = 0; pm; pi++, pm >>= 1) if (pm & 1u) items[w++] = i | pi << 16; }
+        else if (cnt) T.fail = 1;
     }
+    g.sync();
+    const uint32_t n_items = T.n_list <= 2 * C::I ? T.n_list : 0u;
     g.sync();
     if (T.fail) return;
     /* budget (G1): where the product of the candidate-list sizes of a pattern exceeds it, a tuple counts only
@@ -632,21 +640,17 @@ template <class G, class C> CLF uint32_t t_select(const G &g, TileS<C> &T) {
         g.sync();
         if (!again) break;
     }
-    uint32_t count = 0;
-    GFOR(g, p, n) {
-        const bool fl = p < n && T.sel_at[p] != 0xFFFFu;
-        uint32_t cnt;
-        const uint32_t off = g.flag_exscan(fl, cnt);
-        if (fl && count + off < C::S) {
-            const TMatch m = T.mt[T.sel_at[p]];
-            SelRec r;
-            r.pat = m.pat; r.n = m.n; r.pad0 = r.pad1 = 0; r.blk = T.bidx[p];
-            r.pos[0] = m.pos[0]; r.pos[1] = m.n > 1 ? m.pos[1] : NONE32; r.pos[2] = m.n > 2 ? m.pos[2] : NONE32;
-            T.sel[count + off] = r;
-            a_add(&T.f_stats[T.fidx[p]][16 + m.pat], 1u);
-        }
-        count += cnt;
-    }
+    /* the selected matches in position order (= select order: ids are allocated along it): a scan over contiguous runs */
+    uint32_t count = t_scan(g, n, [&](uint32_t p) { return (uint32_t)(T.sel_at[p] != 0xFFFFu); },
+                            [&](uint32_t p, uint32_t at) {
+                                if (T.sel_at[p] == 0xFFFFu || at >= C::S) return;
+                                const TMatch m = T.mt[T.sel_at[p]];
+                                SelRec r;
+                                r.pat = m.pat; r.n = m.n; r.pad0 = r.pad1 = 0; r.blk = T.bidx[p];
+                                r.pos[0] = m.pos[0]; r.pos[1] = m.n > 1 ? m.pos[1] : NONE32; r.pos[2] = m.n > 2 ? m.pos[2] : NONE32;
+                                T.sel[at] = r;
+                                a_add(&T.f_stats[T.fidx[p]][16 + m.pat], 1u);
+                            });
     if (count > C::S) { if (g.rank == 0) T.fail = 1; count = 0; }
     g.sync();
     return count;

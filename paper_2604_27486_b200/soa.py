@@ -522,6 +522,17 @@ def apply(c_out: Corpus, functions=None, ns=None, patterns=None, tagged=True, c_
     event list / record flags exactly where the reference appends them
     (``patterns.py:684,842,906-915``).
     """
+    import gc
+    gc_was_on = gc.isenabled()
+    gc.disable()           # millions of live operand objects: every generation-2 pass of the collector walks them all
+    try:
+        _apply(c_out, functions, ns, patterns, tagged, c_in)
+    finally:
+        if gc_was_on:
+            gc.enable()
+
+
+def _apply(c_out, functions, ns, patterns, tagged, c_in):
     functions = c_out.functions if functions is None else list(functions)
     ev_by_func = {}
     for ev in c_out.events:          # cl_download returns them in append order
