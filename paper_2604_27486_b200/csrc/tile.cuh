@@ -203,9 +203,41 @@ template <class G, class C> CLF void t_index(const G &g, TileS<C> &T) {
     g.sync();
 }
 
+/* def-use contribution of one record that now sits at position `at` (ssa.build_defuse, ssa.py:613-636): what
+ * t_usecount does per record, from the record's four 128-bit words while a permutation has them in registers
+ * (slots addressed with compile-time indices: no local memory).  Records of tiles have no overflow slots.     */
+template <class C> CLD void t_du_record(TileS<C> &T, const TileG<C> &tg, const uint4 &r0, const uint4 &r1, const uint4 &r2, const uint4 &r3,
+                                        uint32_t at, uint32_t f) {
+    const uint32_t w2 = r0.z;                                   /* n_defs, n_aux, n_uses, flags (cl_hdr bytes 8..11) */
+    const unsigned nd = w2 & 0xFFu, na = (w2 >> 8) & 0xFFu, nu = (w2 >> 16) & 0xFFu;
+    const unsigned g0 = ((w2 >> 24) & CL_IF_GUARD) ? 1u : 0u, d_end = g0 + nd + na, u_end = d_end + nu;
+    const uint32_t tw[4] = { r1.x, r1.y, r1.z, r1.w };
+    const uint32_t pw[8] = { r2.x, r2.y, r2.z, r2.w, r3.x, r3.y, r3.z, r3.w };
+    bool odd = false;
+#pragma unroll
+    for (unsigned k = 0; k < 8; k++) {
+        if (k >= u_end) continue;
+        const uint16_t tag = (uint16_t)(k & 1u ? tw[k >> 1] >> 16 : tw[k >> 1] & 0xFFFFu);
+        const uint32_t pay = pw[k];
+        const unsigned kd = kind_of(tag);
+        if (k >= g0 && k < d_end) {                             /* defs and aux defs */
+            if (kd == CL_K_VALUE) { if (pay < C::V) T.defpos[pay] = at; }
+            else odd |= !(kd == CL_K_RZ || kd == CL_K_URZ || kd == CL_K_PRED);
+        } else if (kd == CL_K_VALUE) {                          /* guard, uses */
+            if (pay < C::V) a_add(&T.usecnt[pay], 1u);
+        } else if (kd == CL_K_MEMREF && k >= d_end) {
+            const cl_memref &m = tg.mem[pay];
+            if (kind_of(m.base_tag) == CL_K_VALUE && m.base_pay < C::V) a_add(&T.usecnt[m.base_pay], 1u);
+            if (kind_of(m.ureg_tag) == CL_K_VALUE && m.ureg_pay < C::V) a_add(&T.usecnt[m.ureg_pay], 1u);
+        }
+    }
+    if (odd) T.f_odd[f] = 1;
+}
+
 /* in-place permutation of the stream: record i moves to dst(i) (NONE32 = dropped).
- * Everything is read before anything is written.                              */
-template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T, const TileG<C> &tg, uint32_t n, uint32_t n_new, F dst) {
+ * Everything is read before anything is written.  COUNT (big tiles): def positions and use counts of the moved
+ * records are taken on the way (the caller has zeroed them and adds what it inserts): no recount sweep after.  */
+template <bool COUNT = false, class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T, const TileG<C> &tg, uint32_t n, uint32_t n_new, F dst) {
     if constexpr (C::PP) {
         /* into the other buffer of every plane, then the buffers flip */
         GFOR(g, i, n) if (i < n) {
@@ -217,7 +249,9 @@ template <class G, class C, class F> CLD void t_permute(const G &g, TileS<C> &T,
                 *(uint4 *)&T.tag.b[(size_t)d * 8] = r1;
                 ((uint4 *)&T.pay.b[(size_t)d * 8])[0] = r2;
                 ((uint4 *)&T.pay.b[(size_t)d * 8])[1] = r3;
-                T.fidx.b[d] = T.fidx[i]; T.bidx.b[d] = T.bidx[i];
+                const uint32_t f = T.fidx[i];
+                T.fidx.b[d] = (uint8_t)f; T.bidx.b[d] = T.bidx[i];
+                if (COUNT && tf_ok(T, f)) t_du_record(T, tg, r0, r1, r2, r3, d, f);
             }
         }
         g.sync();
@@ -798,22 +832,43 @@ template <class G, class C> CLF void t_apply_patterns(const G &g, TileS<C> &T, c
     if (tot > C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
     g.sync();
     PROF(g, T.fs, PF_EMIT);
-    t_permute(g, T, tg, n, tot, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] + T.inscnt[p] : NONE32; });
+    if constexpr (C::PP) {                 /* def-use of the new stream is taken while it is written (see t_du_record) */
+        GFOR(g, v, T.vtot) if (v < T.vtot) { T.usecnt[v] = 0; T.defpos[v] = NONE32; }
+        g.sync();
+    }
+    t_permute<C::PP>(g, T, tg, n, tot, [&](uint32_t p) { return T.keep[p] ? (uint32_t)T.outpos[p] + T.inscnt[p] : NONE32; });
     /* staged records to their place, value table, immediates */
     GFOR(g, j, ns) if (j < ns) {
         const SelRec m = T.sel[j];
         uint32_t f;                                  /* m.pos[] are positions before the permutation */
         if constexpr (C::PP) f = T.fidx.b[m.pos[0]]; else f = T.fidx[m.pos[0]];
         if (!tf_ok(T, f)) continue;
-        t_apply_stage(T, tg.stage[j], T.outpos[m.pos[m.n - 1]], f, m.blk);
+        const uint32_t out0 = T.outpos[m.pos[m.n - 1]];
+        t_apply_stage(T, tg.stage[j], out0, f, m.blk);
+        if constexpr (C::PP) {
+            const Stage &st = tg.stage[j];
+            if (st.ok)
+                for (unsigned r = 0; r < st.nins; r++) {         /* the records just inserted */
+                    const uint32_t o = out0 + r;
+                    t_du_record(T, tg, *(const uint4 *)&T.hdr[o], *(const uint4 *)&T.tag[(size_t)o * 8],
+                                ((const uint4 *)&T.pay[(size_t)o * 8])[0], ((const uint4 *)&T.pay[(size_t)o * 8])[1], o, f);
+                }
+        }
+    }
+    if constexpr (C::PP) {
+        GFOR(g, b, T.nb) if (b < T.nb) {                          /* terminator value uses (ssir.py:378-382) */
+            if (!tf_ok(T, T.bfun[b])) continue;
+            for (int k = 0; k < 2; k++)
+                if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE && T.blk[b].term_pay[k] < C::V) a_add(&T.usecnt[T.blk[b].term_pay[k]], 1u);
+        }
     }
     g.sync();
     t_rebase_blocks(g, T, n, tot);
-    if (g.rank == 0) T.tombs = 0;
+    if (g.rank == 0) { T.tombs = 0; if (C::PP) T.du_ok = 1; }
     if constexpr (!C::PP) t_index(g, T);
-    /* for simplify_packs / remove_dead_pseudo of this round.  (Keeping def-use valid across the permutation instead --
-     * remapping defpos through outpos, moving the use counts of removed / inserted records -- was measured: no gain.) */
-    t_usecount(g, T, tg);
+    /* def-use for simplify_packs / remove_dead_pseudo of this round: taken during the permutation in big tiles,
+     * one recount sweep in shared-memory tiles */
+    if constexpr (C::PP) g.sync(); else t_usecount(g, T, tg);
 }
 
 /* ordered in-place compaction of the stream by keep[]                         */
