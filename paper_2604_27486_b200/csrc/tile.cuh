@@ -1366,7 +1366,11 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
                                 [&](uint32_t p, uint32_t x) { T.outpos[p] = (uint16_t)x; });
     if (tot > C::I) { if (g.rank == 0) T.fail = 1; g.sync(); return; }
     g.sync();
-    t_permute(g, T, tg, n, tot, [&](uint32_t p) { return (uint32_t)T.outpos[p] + T.keep[p]; });
+    if constexpr (C::PP) {                 /* usecnt[] was the float-view map until here; now the def-use of the new stream */
+        GFOR(g, v, T.vtot) if (v < T.vtot) { T.usecnt[v] = 0; T.defpos[v] = NONE32; }
+        g.sync();
+    }
+    t_permute<C::PP>(g, T, tg, n, tot, [&](uint32_t p) { return (uint32_t)T.outpos[p] + T.keep[p]; });
     GFOR(g, c, nc) if (c < nc) {
         const TChain ch = T.chain[c];
         const uint32_t f = ch.f;
@@ -1381,12 +1385,24 @@ template <class G, class C> CLF void t_reciprocal(const G &g, TileS<C> &T, const
             T.fidx[o] = (uint8_t)f; T.bidx[o] = T.bidx[(uint32_t)T.outpos[ch.add] + 1u];      /* the add itself sits between the two */
             for (unsigned k = 0; k < 8; k++) { T.tag[(size_t)o * 8 + k] = k < 2 ? (uint16_t)CL_K_VALUE : (uint16_t)0; T.pay[(size_t)o * 8 + k] = 0; }
             T.pay[(size_t)o * 8] = vi + q; T.pay[(size_t)o * 8 + 1] = q ? ch.addv : ch.rcp;
+            if constexpr (C::PP) {
+                if (vi + q < C::V) T.defpos[vi + q] = o;
+                const uint32_t src = q ? ch.addv : ch.rcp;
+                if (src < C::V) a_add(&T.usecnt[src], 1u);
+            }
+        }
+    }
+    if constexpr (C::PP) {
+        GFOR(g, b, T.nb) if (b < T.nb) {                          /* terminator value uses (ssir.py:378-382) */
+            if (!tf_ok(T, T.bfun[b])) continue;
+            for (int k = 0; k < 2; k++)
+                if (kind_of(T.blk[b].term_tag[k]) == CL_K_VALUE && T.blk[b].term_pay[k] < C::V) a_add(&T.usecnt[T.blk[b].term_pay[k]], 1u);
         }
     }
     g.sync();
     GFOR(g, f, T.nf) if (f < T.nf && T.f_aux[f] && tf_ok(T, f)) { T.f_nvid[f] += 2u * T.f_aux[f]; T.f_niid[f] += 2u * T.f_aux[f]; }
     t_rebase_blocks(g, T, n, tot);
-    if constexpr (!C::PP) t_index(g, T);
+    if constexpr (C::PP) { if (g.rank == 0) T.du_ok = 1; g.sync(); } else t_index(g, T);
 }
 
 /* ------------------------------------------------------------ load / store */
