@@ -1411,3 +1411,15 @@ extern "C" int cl_get_stats(cl_ctx *c, cl_stats *out) { *out = c->stats; return 
 extern "C" int cl_last_run_ms(cl_ctx *c, float *ms) { *ms = c->last_ms; return 0; }
 extern "C" void *cl_device_counts_ptr(cl_ctx *c) { return c->d_stats; }
 extern "C" void *cl_stream(cl_ctx *c) { return (void *)(uintptr_t)c->stream; }
+
+/* For typeseed.cu (same library, not part of the C ABI): the device view of the uploaded corpus, the context's
+ * stream and where the device time of a call is kept.                                                           */
+extern "C" int cli_input_view(cl_ctx *c, cl_corpus *view, void **stream, float **last_ms) {
+    if (!c || !c->have_in) FAIL("no corpus uploaded");
+    *view = c->d_in;
+    view->n_funcs = c->F; view->n_blocks = c->B; view->n_modsets = c->n_modsets;
+    *stream = (void *)(uintptr_t)c->stream;
+    *last_ms = &c->last_ms;
+    return 0;
+}
+extern "C" void cli_set_error(const char *msg) { snprintf(g_err, sizeof g_err, "%s", msg); }

@@ -41,12 +41,12 @@ def build_oracle():
 
 def build_sim():
     """One-lane CPU build of the device code (tests/sim): logic checks without a GPU."""
-    srcs = [CSRC / n for n in ("culifter.cu", "fused.cu", "core.cuh", "tile.cuh", "fused.cuh", "fused.h", "kargs.h")]
-    srcs.append(ROOT / "include" / "culifter.h")
+    srcs = [CSRC / n for n in ("culifter.cu", "fused.cu", "typeseed.cu", "core.cuh", "tile.cuh", "fused.cuh", "fused.h", "kargs.h")]
+    srcs += [ROOT / "include" / "culifter.h", ROOT / "include" / "culifter_types.h"]
     if not SIM_LIB.exists() or any(s.stat().st_mtime > SIM_LIB.stat().st_mtime for s in srcs):
         SIM_LIB.parent.mkdir(parents=True, exist_ok=True)
         subprocess.run(["g++", "-x", "c++", "-std=c++17", "-O1", "-g", "-DCL_SIM", "-fPIC", "-shared",
-                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu"), str(CSRC / "fused.cu")], check=True)
+                        "-o", str(SIM_LIB), str(CSRC / "culifter.cu"), str(CSRC / "fused.cu"), str(CSRC / "typeseed.cu")], check=True)
     return SIM_LIB
 
 

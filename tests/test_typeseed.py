@@ -1,0 +1,97 @@
+"""Type seeding: cl_seed_types against the TypeState the
+reference's own typerec.seed_types (typerec.py:288) produced for the same functions
+(tests/golden/types.pkl.gz, tools/make_types_golden.py).  Bit-exact: masks, roles and the
+link expressions with the reference's dict and list orders."""
+import copy
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import helpers
+from paper_2604_27486_b200 import capi, soa, typerec
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = (ROOT / "include" / "culifter_types.h").read_text()
+DECLARED = sorted(set(re.findall(r"\b(cl_[a-z0-9_]+)\s*\(", HEADER)))
+
+
+def check_against_golden(engine):
+    fix = helpers.load_fixture("types")
+    fns = copy.deepcopy(fix["functions"])
+    states = typerec.seed_types_batch(fns, engine)
+    assert len(states) == len(fix["expect"]) == 57
+    for fn, st, exp in zip(fns, states, fix["expect"]):
+        assert fn.meta["type_state"] is st
+        for key in ("seed_mask", "def_seed_mask", "use_seed_mask", "roles", "link_exprs"):
+            got = getattr(st, key)
+            assert got == exp[key], (fn.name, key)
+            if key == "link_exprs":
+                assert list(got) == list(exp[key]), (fn.name, "link_exprs key order")
+            else:
+                assert sorted(got) == sorted(exp[key]), (fn.name, key)
+
+
+def test_oracle_matches_reference_typestate():
+    check_against_golden(helpers.oracle_engine())
+
+
+def test_sim_matches_reference_typestate():
+    """The device code of csrc/typeseed.cu compiled for the host (one thread): logic check without a GPU."""
+    check_against_golden(helpers.sim_engine())
+
+
+@pytest.mark.parametrize("which", ["product", "oracle"])
+def test_library_exports_the_type_seeding_entry(which):
+    path = capi.PRODUCT_LIB if which == "product" else helpers.build_oracle()
+    lib = ctypes.CDLL(str(path))
+    assert DECLARED == ["cl_seed_types"]
+    assert all(hasattr(lib, n) for n in DECLARED)
+
+
+def test_signature_table_lowering():
+    """Per-id tables: precedence of the reference's if-chain (typerec.py:87-234)."""
+    sk = typerec.SK
+    assert typerec.sig_kind("FSEL") == (sk["FSEL"], 0) and typerec.sig_kind("MUFU") == (sk["FALU"], 0)
+    assert typerec.sig_kind("ULOP3")[0] == sk["IALU"] and typerec.sig_kind("LOP3")[0] == sk["LOP"]
+    assert typerec.sig_kind("LDG") == (sk["LOAD"], 1) and typerec.sig_kind("LDS") == (sk["LOAD"], 0)
+    assert typerec.sig_kind("RED") == (sk["STORE"], 3) and typerec.sig_kind("ATOMS") == (sk["ATOMIC"], 0)
+    assert typerec.sig_kind("BAR")[0] == typerec.sig_kind("NOT_AN_OPCODE")[0] == sk["NONE"]
+    enum = re.search(r"enum cl_sigkind \{(.*?)\};", HEADER, re.S).group(1)
+    names = re.findall(r"CL_SK_([A-Z0-9]+)\b", re.sub(r"/\*.*?\*/", "", enum, flags=re.S))
+    assert names == typerec._SK                      # same order as enum cl_sigkind
+    mt = typerec.mod_type(("F16", "F32"))
+    assert mt[4] == typerec.FLOAT16 and mt[5] == typerec.FLOAT32
+    assert typerec.mod_type(("F64", "S64"))[2:4] == (typerec.FLOAT64, typerec.INT64)
+
+
+def test_key_error_on_dead_value():
+    """A narrowed value that is not in fn.values: the reference's dict raises KeyError (typerec.py:301)."""
+    fix = helpers.load_fixture("types")
+    fn = copy.deepcopy(fix["functions"][0])
+    inst = next(i for b in fn.block_order() for i in b.instructions if i.defs and type(i.defs[0]).__name__ == "ValueRef"
+                and i.opcode.base in ("IADD3", "FADD", "IMAD", "FFMA", "S2R"))
+    del fn.values[inst.defs[0].vid]
+    with pytest.raises(KeyError):
+        typerec.seed_types(fn, helpers.oracle_engine())
+
+
+@pytest.mark.gpu
+def test_cuda_matches_reference_typestate():
+    eng = helpers.cuda_engine()
+    assert eng.backend == "cuda-sm_100a"
+    check_against_golden(eng)
+
+
+@pytest.mark.gpu
+def test_cuda_equals_oracle_on_pool_corpus():
+    """Arrays of cl_seed_types on 200 k instructions of the mixed benchmark corpus: CUDA == oracle, bit for bit."""
+    from paper_2604_27486_b200 import synth
+    corpus = synth.build_corpus("mixed", 200_000, seed=7)[0]
+    a = typerec.seed_corpus(helpers.cuda_engine(), corpus)
+    b = typerec.seed_corpus(helpers.oracle_engine(), corpus)
+    for name in ("val_masks", "role", "link_mask", "link_def", "status"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
+    assert (a.val_masks != 0xFFFFFF).any()
