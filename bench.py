@@ -71,6 +71,8 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-objects", action="store_true", help="skip the objects-in / objects-out leg (e2e_objects)")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config legs (BASELINE.json configs[0..3])")
+    ap.add_argument("--no-typeseed", action="store_true", help="skip the type-seeding leg (SURVEY 8 row f3)")
+    ap.add_argument("--only-typeseed", action="store_true", help="run the type-seeding leg alone and print its object (ncu captures)")
     ap.add_argument("--passes", type=int, default=15, help="CL_PASS_* mask of the headline leg")
     return ap.parse_args()
 
@@ -271,6 +273,53 @@ def config_legs(eng, peak, threads, steps, warmup, with_cpu):
     return out
 
 
+def typeseed_leg(eng, peak, threads, steps, warmup, with_cpu, n_sass=20_000_000):
+    """Type seeding (cl_seed_types, typerec.py:288) on the NORMALISED stream: the mixed corpus goes through the
+    post-SSA stage, its result is the corpus the seeding kernel reads (device resident).  value = SASS instructions
+    of that corpus per second of kernel time (CUDA events inside the call); e2e = the whole C-ABI call with the
+    tables going up and the result arrays coming back to host memory."""
+    from paper_2604_27486_b200 import typerec
+    from paper_2604_27486_b200.capi import Engine
+    c_in, ns, _ = synth.build_corpus("mixed", n_sass, seed=101)
+    eng.upload(c_in)
+    eng.run_postssa(15)
+    corpus = eng.download()
+    del c_in
+    eng.upload(corpus)
+    ms, wall = [], []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        res = typerec.seed_corpus(eng, corpus, None, upload=False)
+        if k >= warmup:
+            wall.append(time.perf_counter() - t0)
+            ms.append(eng.last_run_ms())
+    R, V, B, F = corpus.n_insts, len(corpus.val_alive), corpus.n_blocks, corpus.n_funcs
+    algo = 64 * R + 7 * R + 8 * V + 16 * B + 4 * (B + 3 * F)
+    t = float(np.mean(ms))
+    out = {"config": "typeseed", "workload": f"seed_types over the normalised mixed corpus: {ns} SASS instructions, {R} records, {V} values, {F} kernels",
+           "metric": METRIC, "value": ns / (t / 1e3), "unit": UNIT, "ms_per_step": t, "steps": steps, "warmup": warmup,
+           "gpu_launches": 2 * steps, "kernel": "k_typeseed (+ k_typeseed_prepare: mask fill, record offsets)",
+           "roofline": {"bound": "hbm", "achieved": algo / (t / 1e3) / 1e9, "peak": peak, "unit": "GB/s", "frac": algo / (t / 1e3) / 1e9 / peak,
+                        "traffic": None, "algorithmic_bytes_per_launch": int(algo),
+                        "bytes_per_record": "64 read + 7 written per record, 8 per value (fill + result), 16 per block terminator, CSR offsets"},
+           "e2e": {"value": ns / float(np.mean(wall)), "unit": UNIT, "ms_per_step": float(np.mean(wall)) * 1e3,
+                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(7 * R + 4 * V + F),
+                   "path": "cl_seed_types on the resident corpus: tables up, kernels, result arrays back to (pageable) host memory"},
+           "narrowed_values": int((res.val_masks != 0xFFFFFF).sum()), "transparent_records": int((res.role == 1).sum())}
+    if with_cpu:
+        o = Engine(ROOT / "oracle" / "liboracle.so")
+        typerec.seed_corpus(o, corpus, None)
+        sec = o.last_run_ms() / 1e3
+        ref = typerec.seed_corpus(o, corpus, None, upload=False)
+        sec = min(sec, o.last_run_ms() / 1e3)
+        o.close()
+        same = all(np.array_equal(getattr(res, n), getattr(ref, n)) for n in ("val_masks", "role", "link_mask", "link_def", "status"))
+        out["cpu_baseline"] = {"value": ns / sec, "unit": UNIT, "cores": 1, "kind": "port",
+                               "sample": f"the same corpus ({ns} SASS instructions), best of 2 passes, {sec:.2f} s on one thread"}
+        out["equal_to_oracle"] = bool(same)
+    return out
+
+
 def objects_leg(eng, n_target=1_000_000):
     """Objects in -> objects out: what a `sasslift` user of the drop-in sees.  LiftedFunction objects
     (the synth_sm90 fixture of the reference's front half, unpickled as many times as it takes) -> soa.encode (C
@@ -339,6 +388,18 @@ def main():
     import torch.distributed as dist
     from paper_2604_27486_b200.capi import Engine
 
+    if args.only_typeseed:
+        torch.cuda.set_device(local)
+        pk = 6650.0
+        try:
+            pk = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", pk))
+        except OSError:
+            pass
+        e = Engine(device=local)
+        print(json.dumps(typeseed_leg(e, pk, threads, args.steps, args.warmup, not args.no_cpu)))
+        e.close()
+        return
+
     # CL_BENCH_SIM=1: dry run of the rank plumbing without a GPU (tests/test_bench_contract.py): the one-lane CPU build
     # of the device code as the engine, gloo instead of NCCL; its numbers mean nothing and the line says "sim"
     sim = os.environ.get("CL_BENCH_SIM") == "1"
@@ -347,7 +408,7 @@ def main():
         sys.path.insert(0, str(ROOT / "tests"))
         import helpers
         sim_lib = helpers.build_sim()
-        args.no_e2e = args.no_cpu = args.no_configs = args.no_objects = True
+        args.no_e2e = args.no_cpu = args.no_configs = args.no_objects = args.no_typeseed = True
         if world > 1:
             dist.init_process_group("gloo")
     else:
@@ -509,6 +570,12 @@ def main():
         configs = config_legs(eng2, peak, threads, max(2, min(args.steps, 3)), max(3, args.warmup), not args.no_cpu)
         eng2.close()
 
+    typeseed = None
+    if rank == 0 and world == 1 and not args.no_typeseed and args.workload == "mixed":
+        eng4 = Engine(device=local)
+        typeseed = typeseed_leg(eng4, peak, threads, max(2, min(args.steps, 5)), max(3, args.warmup), not args.no_cpu)
+        eng4.close()
+
     # whole-job match counters: this rank's at N = 1, the sum of the allgathered rows of the last step at N > 1
     whole_job = {"selected": int(n_sel), "rewrites": int(st["rewrites"].sum()), "refused": int(st["refused"].sum())}
     if world > 1 and gathered[0] is not None:
@@ -533,6 +600,7 @@ def main():
             "match_counts": whole_job,
             "e2e_objects": e2e_objects,
             "configs": configs,
+            "typeseed": typeseed,
         }
         print(json.dumps(line))
     if world > 1:

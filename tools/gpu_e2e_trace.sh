@@ -20,7 +20,7 @@ torch.cuda.synchronize(); dt = time.perf_counter() - t
 print("both directions at once, GB/s per direction", 5 * n / dt / 1e9)
 PY
 cat gpurun_out/pcie_probe.txt
-CL_TRACE=1 python bench.py --no-cpu --no-configs --no-objects --steps 3 --warmup 3 > gpurun_out/e2e_trace.json 2> gpurun_out/e2e_trace.err
+CL_TRACE=1 python bench.py --no-cpu --no-configs --no-objects --no-typeseed --steps 3 --warmup 3 > gpurun_out/e2e_trace.json 2> gpurun_out/e2e_trace.err
 grep chunk gpurun_out/e2e_trace.err | tail -16
 python -c "
 import json; d=json.load(open('gpurun_out/e2e_trace.json')); print(d['value']/1e6, d['e2e'])"

@@ -13,7 +13,7 @@ o=d.get('e2e_objects'); print('objects', o and {k:(round(v) if isinstance(v,floa
 for c in d.get('configs') or []:
     print(' ', c['config'], round(c['value']/1e6,1), 'M inst/s', round(c['ms_per_step'],2), 'ms frac', round(c['roofline']['frac'],5), 'cpu', c.get('cpu_baseline') and round(c['cpu_baseline']['value']/1e6,2), [ (l['pass'][:12], round(l['value']/1e6,1)) for l in c.get('passes',[])])
 PY
-B="python bench.py --no-e2e --no-cpu --no-configs --no-objects"
+B="python bench.py --no-e2e --no-cpu --no-configs --no-objects --no-typeseed"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/${T}_launches_default_mixed100M.csv $B --steps 1 --warmup 1 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_postssa_gtile -c 1 -o gpurun_out/${T}_ncu_gtile -f $B --steps 1 --warmup 0 > gpurun_out/${T}_ncu.log 2>&1
 ncu -i gpurun_out/${T}_ncu_gtile.ncu-rep --page details > gpurun_out/${T}_ncu_full_k_postssa_gtile_details.txt
