@@ -14,6 +14,7 @@ into the reference's ``TypeState`` dicts.  All narrowing happens in the kernel.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -196,6 +197,28 @@ def seed_corpus(engine, corpus: soa.Corpus, hints: np.ndarray | None = None, upl
 
 
 @dataclass
+class TypeSet:
+    """Mirror of ``lattice.TypeSet`` (lattice.py:119-145): candidate set plus the conflicted flag."""
+    mask: int = TOP
+    conflicted: bool = False
+
+    def intersect(self, other: int) -> bool:
+        if self.conflicted:
+            if other and self.mask != other:
+                self.mask = other
+                return True
+            return False
+        new = self.mask & other
+        if new == self.mask:
+            return False
+        self.mask = new
+        return True
+
+    def copy(self) -> "TypeSet":
+        return TypeSet(self.mask, self.conflicted)
+
+
+@dataclass
 class TypeState:
     """Mirror of ``typerec.TypeState`` (typerec.py:253-268)."""
     seed_mask: dict = field(default_factory=dict)
@@ -257,16 +280,36 @@ def seed_types_batch(functions, engine=None) -> list:
     from . import passes
     functions = list(functions)
     for fn in functions:
-        fn.require_phase(passes._phase(fn, "NORMALIZED"), passes._phase(fn, "SSA"), passes._phase(fn, "TYPED"))
+        phase = sys.modules[type(fn).__module__].Phase          # the Phase enum of the package fn comes from
+        fn.require_phase(phase.NORMALIZED, phase.SSA, phase.TYPED)   # typerec.py:290
     corpus = soa.encode(functions)
     eng = engine or passes.default_engine()
     res = seed_corpus(eng, corpus, hints_of(functions))
     states = states_of(corpus, res)
-    for fn, st, status in zip(functions, states, res.status.tolist()):
+    for k, (fn, st, status) in enumerate(zip(functions, states, res.status.tolist())):
         if status == L.ST_KEY_ERROR:
             raise KeyError(f"{fn.name}: a narrowed value is not in fn.values (typerec.py:301)")
+        state_cls, set_cls = _classes_for(fn)
+        if state_cls is not TypeState:             # the reference's own objects get the reference's own classes
+            st = state_cls(link_exprs=st.link_exprs, roles=st.roles, seed_mask=st.seed_mask,
+                           def_seed_mask=st.def_seed_mask, use_seed_mask=st.use_seed_mask)
+            states[k] = st
+        for name in ("seed_mask", "def_seed_mask", "use_seed_mask"):     # dict order of fn.values (typerec.py:292)
+            d = getattr(st, name)
+            setattr(st, name, {vid: d[vid] for vid in fn.values})
+        for info in fn.values.values():
+            info.type_state = set_cls()                                  # typerec.py:296
         fn.meta["type_state"] = st
     return states
+
+
+def _classes_for(fn):
+    """(TypeState, TypeSet) classes of the package ``fn`` comes from: the reference's when it is a reference object."""
+    pkg = type(fn).__module__.rsplit(".", 1)[0]
+    tr, lat = sys.modules.get(pkg + ".typerec"), sys.modules.get(pkg + ".lattice")
+    if pkg != __name__.rsplit(".", 1)[0] and tr is not None and lat is not None and hasattr(tr, "TypeState"):
+        return tr.TypeState, lat.TypeSet
+    return TypeState, TypeSet
 
 
 def seed_types(fn, engine=None) -> TypeState:

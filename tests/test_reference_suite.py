@@ -2,7 +2,8 @@
 repo's drop-in: sasslift.patterns.{normalize_xmad, normalize_reciprocal,
 apply_aggregations, tag_cuda_objects, match_patterns, select_matches} and
 sasslift.frontend.{normalize_instruction, substitute_special_registers} are
-replaced by paper_2604_27486_b200.passes.* before the reference's test modules
+replaced by paper_2604_27486_b200.passes.* and sasslift.typerec.seed_types by
+paper_2604_27486_b200.typerec.seed_types (cl_seed_types) before the reference's test modules
 are collected, and the WHOLE suite of /root/reference/pkg/tests (test_patterns,
 test_acceptance, test_fuzz_closure and the ten other modules: frontend, cfg, ssa,
 typerec, emit, interp, cli ... all of which lift through the swapped calls) must
@@ -26,10 +27,11 @@ import os, sys
 sys.dont_write_bytecode = True
 sys.path[:0] = [{root!r}, {root!r} + "/tests", "/root/reference/pkg/src"]
 import helpers
-from paper_2604_27486_b200 import passes
+from paper_2604_27486_b200 import passes, typerec
 passes.set_default_engine(helpers.cuda_engine() if os.environ.get("CL_DROPIN_ENGINE") == "cuda" else helpers.sim_engine())
 import sasslift.patterns as P
 import sasslift.frontend as F
+import sasslift.typerec as T
 CALLS = {{}}
 def _count(name, fn):
     def wrapper(*a, **k):
@@ -41,6 +43,7 @@ for name in ("normalize_xmad", "normalize_reciprocal", "apply_aggregations", "ta
     setattr(P, name, _count(name, getattr(passes, name)))
 for name in ("normalize_instruction", "substitute_special_registers"):
     setattr(F, name, _count(name, getattr(passes, name)))
+setattr(T, "seed_types", _count("seed_types", typerec.seed_types))
 def pytest_sessionfinish(session, exitstatus):
     print("\\nDROPIN-CALLS " + " ".join(f"{{k}}={{v}}" for k, v in sorted(CALLS.items())))
 '''
@@ -72,5 +75,5 @@ def test_reference_tests_pass_through_the_drop_in(tmp_path):
     calls = dict(kv.split("=") for kv in re.search(r"DROPIN-CALLS (.*)", out).group(1).split())
     # the swapped entry points really carried the suite
     for name in ("apply_aggregations", "normalize_xmad", "normalize_reciprocal", "tag_cuda_objects", "match_patterns",
-                 "select_matches", "normalize_instruction", "substitute_special_registers"):
+                 "select_matches", "normalize_instruction", "substitute_special_registers", "seed_types"):
         assert int(calls.get(name, 0)) > 0, (name, calls)
