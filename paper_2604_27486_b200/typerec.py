@@ -173,9 +173,10 @@ class SeedArrays:
     status: np.ndarray
 
 
-def seed_corpus(engine, corpus: soa.Corpus, hints: np.ndarray | None = None, upload: bool = True) -> SeedArrays:
+def seed_corpus(engine, corpus: soa.Corpus, hints: np.ndarray | None = None, upload: bool = True,
+                into: SeedArrays | None = None) -> SeedArrays:
     """``cl_seed_types`` over an encoded corpus (the batch entry; ``upload=False`` reuses the
-    corpus the engine already holds)."""
+    corpus the engine already holds; ``into``: caller-owned result arrays, e.g. pinned host memory)."""
     lib = engine.lib
     if not hasattr(lib, "cl_seed_types"):
         raise RuntimeError("this build of the library has no cl_seed_types (include/culifter_types.h)")
@@ -187,8 +188,17 @@ def seed_corpus(engine, corpus: soa.Corpus, hints: np.ndarray | None = None, upl
     n, nv = corpus.n_insts, len(corpus.val_alive)
     if hints is not None and len(hints) != n:
         raise ValueError(f"hints: {len(hints)} entries for {n} records")
-    res = SeedArrays(np.zeros(nv, np.uint32), np.zeros(n, np.uint8), np.zeros(n, np.uint16),
-                     np.zeros(n, np.uint32), np.zeros(corpus.n_funcs, np.uint8))
+    if into is not None:
+        want = dict(val_masks=(nv, np.uint32), role=(n, np.uint8), link_mask=(n, np.uint16), link_def=(n, np.uint32),
+                    status=(corpus.n_funcs, np.uint8))
+        for name, (cnt, dt) in want.items():
+            a = getattr(into, name)
+            if len(a) < cnt or a.dtype != dt or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"seed_corpus: result array {name} must be contiguous {np.dtype(dt).name}[>= {cnt}]")
+        res = SeedArrays(**{name: getattr(into, name)[:cnt] for name, (cnt, _) in want.items()})
+    else:
+        res = SeedArrays(np.zeros(nv, np.uint32), np.zeros(n, np.uint8), np.zeros(n, np.uint16),
+                         np.zeros(n, np.uint32), np.zeros(corpus.n_funcs, np.uint8))
     st = TypeSeed(*(a.ctypes.data_as(C.c_void_p) for a in (res.val_masks, res.role, res.link_mask, res.link_def, res.status)))
     hp = np.ascontiguousarray(hints, np.uint32).ctypes.data_as(C.c_void_p) if hints is not None else None
     engine._check(lib.cl_seed_types(engine._ctx, ops.ctypes.data_as(C.c_void_p), len(ops),

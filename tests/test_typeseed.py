@@ -95,3 +95,73 @@ def test_cuda_equals_oracle_on_pool_corpus():
     for name in ("val_masks", "role", "link_mask", "link_def", "status"):
         assert np.array_equal(getattr(a, name), getattr(b, name)), name
     assert (a.val_masks != 0xFFFFFF).any()
+
+
+ARRAYS = ("val_masks", "role", "link_mask", "link_def", "status")
+
+
+@pytest.mark.parametrize("name", ["bundled", "synth_sm90", "synth_sm52", "synth_sm75", "synth_long", "chains"])
+def test_device_code_equals_oracle_on_stage_inputs(name):
+    """Same arrays from the device code (one-thread build) and the oracle on the SSA-phase inputs of the stage's goldens
+    (overflow-slot records, wide PHIs, guards, terminator conditions, MemRef bases and uniform registers)."""
+    fns = helpers.load_fixture(name)["functions"]
+    corpus, hints = soa.encode(fns), typerec.hints_of(fns)
+    a = typerec.seed_corpus(helpers.sim_engine(), corpus, hints)
+    b = typerec.seed_corpus(helpers.oracle_engine(), corpus, hints)
+    for n in ARRAYS:
+        assert np.array_equal(getattr(a, n), getattr(b, n)), n
+    assert (a.val_masks[corpus.val_alive.astype(bool)] != 0xFFFFFF).any()
+
+
+def test_caller_owned_result_arrays_and_empty_corpus():
+    fns = helpers.load_fixture("snippets")["functions"]
+    corpus = soa.encode(fns)
+    eng = helpers.oracle_engine()
+    ref = typerec.seed_corpus(eng, corpus)
+    n, nv = corpus.n_insts, len(corpus.val_alive)
+    into = typerec.SeedArrays(np.zeros(nv + 5, np.uint32), np.zeros(n + 5, np.uint8), np.zeros(n + 5, np.uint16),
+                              np.zeros(n + 5, np.uint32), np.zeros(corpus.n_funcs, np.uint8))
+    got = typerec.seed_corpus(eng, corpus, None, upload=False, into=into)
+    for name in ARRAYS:
+        assert np.array_equal(getattr(got, name), getattr(ref, name)), name
+        assert np.shares_memory(getattr(got, name), getattr(into, name))
+    with pytest.raises(ValueError):
+        typerec.seed_corpus(eng, corpus, None, upload=False,
+                            into=typerec.SeedArrays(np.zeros(1, np.uint32), into.role, into.link_mask, into.link_def, into.status))
+    with pytest.raises(ValueError):
+        typerec.seed_corpus(eng, corpus, np.zeros(3, np.uint32), upload=False)
+    empty = corpus.slice_funcs(0, 0)
+    for e in (helpers.oracle_engine(), helpers.sim_engine()):
+        res = typerec.seed_corpus(e, empty)
+        assert len(res.role) == len(res.val_masks) == len(res.status) == 0
+    assert typerec.seed_types_batch([], eng) == []
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["bundled", "synth_long", "long_blocks"])
+def test_cuda_equals_oracle_on_stage_inputs(name):
+    fns = helpers.load_fixture(name)["functions"]
+    corpus, hints = soa.encode(fns), typerec.hints_of(fns)
+    a = typerec.seed_corpus(helpers.cuda_engine(), corpus, hints)
+    b = typerec.seed_corpus(helpers.oracle_engine(), corpus, hints)
+    for n in ARRAYS:
+        assert np.array_equal(getattr(a, n), getattr(b, n)), n
+
+
+@pytest.mark.gpu
+def test_cuda_empty_corpus_and_pinned_result():
+    import torch
+    fns = helpers.load_fixture("snippets")["functions"]
+    corpus = soa.encode(fns)
+    eng = helpers.cuda_engine()
+    res = typerec.seed_corpus(eng, corpus.slice_funcs(0, 0))
+    assert len(res.role) == len(res.val_masks) == len(res.status) == 0
+    n, nv = corpus.n_insts, len(corpus.val_alive)
+    pinned = [torch.empty(k, dtype=dt, pin_memory=True).numpy() for k, dt in
+              ((nv, torch.int32), (n, torch.uint8), (n, torch.int16), (n, torch.int32), (corpus.n_funcs, torch.uint8))]
+    into = typerec.SeedArrays(pinned[0].view(np.uint32), pinned[1], pinned[2].view(np.uint16), pinned[3].view(np.uint32), pinned[4])
+    got = typerec.seed_corpus(eng, corpus, into=into)
+    ref = typerec.seed_corpus(helpers.oracle_engine(), corpus)
+    for name in ARRAYS:
+        assert np.array_equal(getattr(got, name), getattr(ref, name)), name
+    assert eng.last_run_ms() > 0
