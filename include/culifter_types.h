@@ -75,15 +75,28 @@ typedef struct cl_modtype {       /* one per interned modifier tuple (cl_hdr.mod
     uint8_t flags;                /* CL_MT_*: "WIDE" "HI" "F32" "F2I" "I2F" in mods   */
 } cl_modtype;
 
-/* per-record host metadata the stream does not carry (Instruction.meta):
- *   bits 0..3   meta["packed_def_width"]  (0 = absent)            typerec.py:179
- *   bits 4..7   meta["packed_data_width"] (0 = absent, reads as 1) :191
- *   bits 8..15, 16..23, 24..31  meta["tensor_groups"] a, b, c     :209-210    */
+/* Host metadata the stream does not carry (Instruction.meta), as a sparse CSR keyed by the instruction id:
+ * for function f the entries off[f] .. off[f+1]-1, sorted by iid.  Only loads, stores and tensor ops read it, and
+ * the stage never rewrites those, so the same table serves the uploaded corpus and the stage's result.
+ *   val bits 0..3   meta["packed_def_width"]  (0 = absent)            typerec.py:179
+ *       bits 4..7   meta["packed_data_width"] (0 = absent, reads as 1) :191
+ *       bits 8..15, 16..23, 24..31  meta["tensor_groups"] a, b, c     :209-210    */
+typedef struct cl_typehints {
+    const uint32_t *off;          /* [n functions + 1]                                */
+    const uint32_t *iid;          /* [off[n functions]]                               */
+    const uint32_t *val;
+} cl_typehints;
 #define CL_TH_DEFW(h)  ((h) & 15u)
 #define CL_TH_DATAW(h) (((h) >> 4) & 15u)
 #define CL_TH_NA(h)    (((h) >> 8) & 255u)
 #define CL_TH_NB(h)    (((h) >> 16) & 255u)
 #define CL_TH_NC(h)    ((h) >> 24)
+
+/* which records are seeded */
+#define CL_SEED_INPUT  0u   /* the corpus of the last cl_upload                                          */
+#define CL_SEED_RESULT 1u   /* the dense result the last cl_run_postssa left on the device: the stage and the
+                               seeding chain without a host round trip (pipeline.py:165-175); array sizes are
+                               those of cl_out_sizes (records = sizes[0], values = sizes[4])              */
 
 enum cl_role { CL_ROLE_SEED = 0, CL_ROLE_TRANSPARENT = 1, CL_ROLE_CONVERSION = 2 };
 #define CL_LINK_ALL_FROM_15 0x8000u
@@ -100,14 +113,13 @@ typedef struct cl_typeseed {      /* caller-allocated host arrays               
                              fn.values (the reference's dict lookup raises KeyError, :301) */
 } cl_typeseed;
 
-/* seed_types over every function of the uploaded corpus, in one launch.
- * `ops[n_ops]` / `mods[n_mods]` cover every opcode id / modset id the corpus
- * uses (ids beyond the tables are an error); `hint[n records]` may be NULL
- * (no instruction carries the three meta keys).  Device time of the call is
- * reported by cl_last_run_ms.                                                */
-int cl_seed_types(cl_ctx *ctx, const cl_optype *ops, uint32_t n_ops,
+/* seed_types over every function of the context's corpus (`source`), in one launch.
+ * `ops[n_ops]` / `mods[n_mods]` cover every opcode id / modset id the corpus uses (ids beyond the tables are an
+ * error); `hints` may be NULL (no instruction carries the three meta keys).  Device time of the call is reported
+ * by cl_last_run_ms.                                                         */
+int cl_seed_types(cl_ctx *ctx, uint32_t source, const cl_optype *ops, uint32_t n_ops,
                   const cl_modtype *mods, uint32_t n_mods,
-                  const uint32_t *hint, cl_typeseed *out);
+                  const cl_typehints *hints, cl_typeseed *out);
 
 #ifdef __cplusplus
 }

@@ -137,11 +137,16 @@ static void ts_narrow(ts_fn *f, uint32_t vid, unsigned mask, int is_def) {      
     f->masks[vid] &= ~(drop | (is_def ? drop << 8 : drop << 16));
 }
 
-int cl_seed_types(cl_ctx *c, const cl_optype *ops, uint32_t n_ops, const cl_modtype *mods, uint32_t n_mods,
-                  const uint32_t *hint, cl_typeseed *out) {
-    if (!c->have_in) FAIL("cl_seed_types: no corpus uploaded");
-    const cl_corpus *in = &c->in;
-    struct timespec t0, t1; clock_gettime(CLOCK_MONOTONIC, &t0);
+/* the hint of instruction `iid` of function f: binary search in the function's sorted run, 0 when absent */
+static uint32_t ts_hint(const cl_typehints *h, uint32_t f, uint32_t iid) {
+    if (!h) return 0;
+    uint32_t lo = h->off[f], hi = h->off[f + 1];
+    while (lo < hi) { uint32_t mid = lo + (hi - lo) / 2; if (h->iid[mid] < iid) lo = mid + 1; else hi = mid; }
+    return lo < h->off[f + 1] && h->iid[lo] == iid ? h->val[lo] : 0;
+}
+
+static int ts_seed(const cl_corpus *in, const cl_optype *ops, uint32_t n_ops, const cl_modtype *mods, uint32_t n_mods,
+                   const cl_typehints *hints, cl_typeseed *out) {
     ts_sig *sig = malloc(sizeof *sig);
     for (uint32_t f = 0; f < in->n_funcs; f++) {
         ts_fn fs = { out->val_masks + in->val_off[f], in->val_alive + in->val_off[f], in->val_off[f + 1] - in->val_off[f], 0 };
@@ -152,7 +157,7 @@ int cl_seed_types(cl_ctx *c, const cl_optype *ops, uint32_t n_ops, const cl_modt
                 if (r.h.flags & CL_IF_EXT) { r.tag = in->ext_tag + in->ext_off[f] + r.h.ext; r.pay = in->ext_pay + in->ext_off[f] + r.h.ext; }
                 else { r.tag = in->tag + 8ull * i; r.pay = in->pay + 8ull * i; }
                 if (r.h.op >= n_ops || r.h.modset >= n_mods) { free(sig); FAIL("cl_seed_types: opcode / modset id outside the tables"); }
-                ts_signature(&r, ops[r.h.op], mods[r.h.modset], hint ? hint[i] : 0, sig);
+                ts_signature(&r, ops[r.h.op], mods[r.h.modset], ts_hint(hints, f, r.h.iid), sig);
                 out->role[i] = (uint8_t)sig->role;                                  /* :311 */
                 uint32_t link_def = CL_NO_VALUE; uint16_t link_mask = 0;
                 const unsigned d0 = r.g, a0 = d0 + r.h.n_defs, u0 = a0 + r.h.n_aux;
@@ -186,7 +191,41 @@ int cl_seed_types(cl_ctx *c, const cl_optype *ops, uint32_t n_ops, const cl_modt
         out->status[f] = fs.key_error ? CL_ST_KEY_ERROR : CL_ST_OK;
     }
     free(sig);
-    clock_gettime(CLOCK_MONOTONIC, &t1);
-    c->last_ms = (float)((t1.tv_sec - t0.tv_sec) * 1e3 + (t1.tv_nsec - t0.tv_nsec) * 1e-6);
     return 0;
+}
+
+int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, uint32_t n_ops, const cl_modtype *mods, uint32_t n_mods,
+                  const cl_typehints *hints, cl_typeseed *out) {
+    if (!c->have_in) FAIL("cl_seed_types: no corpus uploaded");
+    if (source == CL_SEED_INPUT) {
+        struct timespec t0, t1; clock_gettime(CLOCK_MONOTONIC, &t0);
+        if (ts_seed(&c->in, ops, n_ops, mods, n_mods, hints, out)) return -1;
+        clock_gettime(CLOCK_MONOTONIC, &t1);
+        c->last_ms = (float)((t1.tv_sec - t0.tv_sec) * 1e3 + (t1.tv_nsec - t0.tv_nsec) * 1e-6);
+        return 0;
+    }
+    if (source != CL_SEED_RESULT) FAIL("cl_seed_types: unknown source %u", source);
+    /* the result of the last run as a dense corpus (what cl_download hands out), then the same walk */
+    uint64_t sz[6];
+    if (cl_out_sizes(c, sz)) return -1;
+    const uint32_t F = c->in.n_funcs, B = c->in.n_blocks;
+    cl_corpus r; memset(&r, 0, sizeof r);
+    r.func = malloc(sizeof(cl_func) * (F + 1)); r.func_blk_off = malloc(4ull * (F + 1)); r.ext_off = malloc(4ull * (F + 1));
+    r.mem_off = malloc(4ull * (F + 1)); r.imm_off = malloc(4ull * (F + 1)); r.val_off = malloc(4ull * (F + 1));
+    r.blk = malloc(sizeof(cl_blk) * (B + 1)); r.blk_off = malloc(4ull * (B + 1));
+    r.hdr = malloc(sizeof(cl_hdr) * (sz[0] + 1)); r.tag = malloc(16ull * (sz[0] + 1)); r.pay = malloc(32ull * (sz[0] + 1));
+    r.ext_tag = malloc(2ull * (sz[1] + 1)); r.ext_pay = malloc(4ull * (sz[1] + 1)); r.mem = malloc(sizeof(cl_memref) * (sz[2] + 1));
+    r.imm = malloc(sizeof(cl_imm) * (sz[3] + 1)); r.val_alive = malloc(sz[4] + 1); r.val_def_iid = malloc(4ull * (sz[4] + 1));
+    r.val_origin = malloc(4ull * (sz[4] + 1));
+    int rc = cl_download(c, &r, NULL);
+    if (!rc) {
+        struct timespec t0, t1; clock_gettime(CLOCK_MONOTONIC, &t0);
+        rc = ts_seed(&r, ops, n_ops, mods, n_mods, hints, out);
+        clock_gettime(CLOCK_MONOTONIC, &t1);
+        c->last_ms = (float)((t1.tv_sec - t0.tv_sec) * 1e3 + (t1.tv_nsec - t0.tv_nsec) * 1e-6);
+    }
+    free(r.func); free(r.func_blk_off); free(r.ext_off); free(r.mem_off); free(r.imm_off); free(r.val_off); free(r.blk); free(r.blk_off);
+    free(r.hdr); free(r.tag); free(r.pay); free(r.ext_tag); free(r.ext_pay); free(r.mem); free(r.imm); free(r.val_alive);
+    free(r.val_def_iid); free(r.val_origin);
+    return rc;
 }

@@ -1414,10 +1414,27 @@ extern "C" void *cl_stream(cl_ctx *c) { return (void *)(uintptr_t)c->stream; }
 
 /* For typeseed.cu (same library, not part of the C ABI): the device view of the uploaded corpus, the context's
  * stream and where the device time of a call is kept.                                                           */
-extern "C" int cli_input_view(cl_ctx *c, cl_corpus *view, void **stream, float **last_ms) {
+extern "C" int cli_corpus_view(cl_ctx *c, uint32_t source, cl_corpus *view, uint64_t counts[2], void **stream, float **last_ms) {
     if (!c || !c->have_in) FAIL("no corpus uploaded");
     *view = c->d_in;
     view->n_funcs = c->F; view->n_blocks = c->B; view->n_modsets = c->n_modsets;
+    counts[0] = c->n_inst; counts[1] = c->n_val;
+    if (source == 1) {                         /* CL_SEED_RESULT: the dense result of the last run, as cl_download copies it */
+        uint64_t sz[6];
+        if (cl_out_sizes(c, sz)) return -1;
+#if CL_CUDA
+        CUDA_OK(cudaSetDevice(c->device));
+#endif
+        if (!c->have_dense && densify(c)) return -1;
+        const DenseArgs &a = c->dense;
+        const KArgs &k = c->k;
+        view->blk = k.o_blk; view->blk_off = a.d_blk_off;
+        view->hdr = a.d_hdr; view->tag = a.d_tag; view->pay = a.d_pay;
+        view->ext_tag = k.o_ext_tag; view->ext_pay = k.o_ext_pay; view->mem = k.o_mem;
+        view->imm = a.d_imm; view->imm_off = a.d_imm_off; view->val_off = a.d_val_off;
+        view->val_alive = a.d_alive; view->val_def_iid = a.d_def_iid; view->val_origin = a.d_origin; view->func = a.d_func;
+        counts[0] = sz[0]; counts[1] = sz[4];
+    } else if (source != 0) FAIL("cl_seed_types: unknown source %u", source);
     *stream = (void *)(uintptr_t)c->stream;
     *last_ms = &c->last_ms;
     return 0;

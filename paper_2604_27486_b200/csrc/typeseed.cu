@@ -35,7 +35,7 @@ struct uint4 { uint32_t x, y, z, w; };
 #endif
 
 /* culifter.cu: device view of the corpus a context holds (not part of the C ABI) */
-extern "C" int cli_input_view(cl_ctx *c, cl_corpus *view, void **stream, float **last_ms);
+extern "C" int cli_corpus_view(cl_ctx *c, uint32_t source, cl_corpus *view, uint64_t counts[2], void **stream, float **last_ms);
 extern "C" void cli_set_error(const char *msg);
 #define FAIL(...) do { char b_[400]; snprintf(b_, sizeof b_, __VA_ARGS__); cli_set_error(b_); return -1; } while (0)
 
@@ -44,11 +44,22 @@ extern "C" void cli_set_error(const char *msg);
 struct TsArgs {
     cl_corpus in;                    /* device pointers */
     const uint32_t *func_rec_off;    /* [F+1] first record of every function */
-    const cl_optype *ops; const cl_modtype *mods; const uint32_t *hint;
+    const cl_optype *ops; const cl_modtype *mods;
+    const uint32_t *hint_off, *hint_iid, *hint_val;   /* cl_typehints on the device, hint_off == nullptr: none */
     uint32_t n_ops, n_mods, n_inst, n_val;
     uint32_t *val_masks; uint8_t *role; uint16_t *link_mask; uint32_t *link_def; uint8_t *status;
     uint32_t *bad;                   /* set when a record names an id outside the tables */
 };
+
+/* the hint of instruction `iid` of function f (binary search in the function's sorted run), 0 when absent */
+TS_HD uint32_t ts_hint(const TsArgs &a, uint32_t f, uint32_t iid) {
+    if (!a.hint_off) return 0;
+    uint32_t lo = a.hint_off[f];
+    const uint32_t end = a.hint_off[f + 1];
+    uint32_t hi = end;
+    while (lo < hi) { const uint32_t mid = lo + ((hi - lo) >> 1); if (a.hint_iid[mid] < iid) lo = mid + 1; else hi = mid; }
+    return lo < end && a.hint_iid[lo] == iid ? a.hint_val[lo] : 0u;
+}
 
 TS_HD uint32_t ts_load_mask(uint32_t w) { return w == 2 ? CL_TY_NUM64 : w == 4 ? CL_TY_NUM128 : CL_TY_NUM32; }
 
@@ -155,7 +166,8 @@ TS_D void ts_narrow(const TsArgs &a, uint32_t f, uint32_t v0, uint32_t nv, uint3
 template <bool EXT> TS_D void ts_slots(const TsArgs &a, uint32_t i, uint32_t f, const TsRec &r) {
     const cl_optype ot = a.ops[r.h.op];
     const cl_modtype mt = a.mods[r.h.modset];
-    const uint32_t hint = a.hint ? a.hint[i] : 0u;
+    /* only loads, stores and tensor ops read Instruction.meta */
+    const uint32_t hint = (ot.kind == CL_SK_LOAD || ot.kind == CL_SK_STORE || ot.kind == CL_SK_TENSOR) ? ts_hint(a, f, r.h.iid) : 0u;
     const uint32_t nd = r.h.n_defs, na = r.h.n_aux, nu = r.h.n_uses;
     const uint32_t d0 = r.g, a0 = d0 + nd, u0 = a0 + na, total = u0 + nu;
     const uint32_t v0 = a.in.val_off[f], nv = a.in.val_off[f + 1] - v0;
@@ -305,36 +317,36 @@ __global__ void __launch_bounds__(256) k_typeseed(TsArgs a) {
 #define TS_OK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { rc = -1; snprintf(msg, sizeof msg, "%s: %s", #x, cudaGetErrorString(e_)); goto done; } } while (0)
 #endif
 
-extern "C" int cl_seed_types(cl_ctx *c, const cl_optype *ops, uint32_t n_ops, const cl_modtype *mods, uint32_t n_mods,
-                             const uint32_t *hint, cl_typeseed *out) {
+extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, uint32_t n_ops, const cl_modtype *mods, uint32_t n_mods,
+                             const cl_typehints *hints, cl_typeseed *out) {
     TsArgs a{};
     void *stream_v = nullptr; float *last_ms = nullptr;
-    if (cli_input_view(c, &a.in, &stream_v, &last_ms)) return -1;
+    uint64_t counts[2] = { 0, 0 };
+    if (cli_corpus_view(c, source, &a.in, counts, &stream_v, &last_ms)) return -1;
     const uint32_t F = a.in.n_funcs, B = a.in.n_blocks;
     a.n_ops = n_ops; a.n_mods = n_mods;
     int rc = 0; char msg[400] = "";
 #if TS_CUDA
     cudaStream_t st = (cudaStream_t)stream_v;
-    uint32_t h_counts[2] = { 0, 0 };
     uint8_t *blob = nullptr; cudaEvent_t e0 = nullptr, e1 = nullptr;
-    /* sizes: the corpus arrays are on the device; the record and value counts are their last offsets */
-    TS_OK(cudaMemcpyAsync(&h_counts[0], a.in.blk_off + B, 4, cudaMemcpyDeviceToHost, st));
-    TS_OK(cudaMemcpyAsync(&h_counts[1], a.in.val_off + F, 4, cudaMemcpyDeviceToHost, st));
-    TS_OK(cudaStreamSynchronize(st));
     {
-        a.n_inst = h_counts[0]; a.n_val = h_counts[1];
-        const size_t N = a.n_inst, V = a.n_val;
+        a.n_inst = (uint32_t)counts[0]; a.n_val = (uint32_t)counts[1];
+        const size_t N = a.n_inst, V = a.n_val, H = hints ? hints->off[F] : 0;
         auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
         const size_t o_ops = 0, o_mods = o_ops + up(sizeof(cl_optype) * n_ops), o_hint = o_mods + up(sizeof(cl_modtype) * n_mods),
-                     o_rec = o_hint + up(hint ? 4 * N : 0), o_masks = o_rec + up(4 * ((size_t)F + 1)), o_role = o_masks + up(4 * V),
+                     o_rec = o_hint + (hints ? up(4 * ((size_t)F + 1)) + 2 * up(4 * H) : 0), o_masks = o_rec + up(4 * ((size_t)F + 1)), o_role = o_masks + up(4 * V),
                      o_lm = o_role + up(N), o_ld = o_lm + up(2 * N), o_st = o_ld + up(4 * N), o_bad = o_st + up(F), total = o_bad + 256;
         TS_OK(cudaMalloc((void **)&blob, total));
         TS_OK(cudaMemcpyAsync(blob + o_ops, ops, sizeof(cl_optype) * n_ops, cudaMemcpyHostToDevice, st));
         TS_OK(cudaMemcpyAsync(blob + o_mods, mods, sizeof(cl_modtype) * n_mods, cudaMemcpyHostToDevice, st));
-        if (hint && N) TS_OK(cudaMemcpyAsync(blob + o_hint, hint, 4 * N, cudaMemcpyHostToDevice, st));
+        if (hints) {
+            uint8_t *h0 = blob + o_hint, *h1 = h0 + up(4 * ((size_t)F + 1)), *h2 = h1 + up(4 * H);
+            TS_OK(cudaMemcpyAsync(h0, hints->off, 4 * ((size_t)F + 1), cudaMemcpyHostToDevice, st));
+            if (H) { TS_OK(cudaMemcpyAsync(h1, hints->iid, 4 * H, cudaMemcpyHostToDevice, st)); TS_OK(cudaMemcpyAsync(h2, hints->val, 4 * H, cudaMemcpyHostToDevice, st)); }
+            a.hint_off = (const uint32_t *)h0; a.hint_iid = (const uint32_t *)h1; a.hint_val = (const uint32_t *)h2;
+        }
         TS_OK(cudaMemsetAsync(blob + o_bad, 0, 4, st));
         a.ops = (const cl_optype *)(blob + o_ops); a.mods = (const cl_modtype *)(blob + o_mods);
-        a.hint = hint ? (const uint32_t *)(blob + o_hint) : nullptr;
         a.func_rec_off = (const uint32_t *)(blob + o_rec);
         a.val_masks = (uint32_t *)(blob + o_masks); a.role = blob + o_role; a.link_mask = (uint16_t *)(blob + o_lm);
         a.link_def = (uint32_t *)(blob + o_ld); a.status = blob + o_st; a.bad = (uint32_t *)(blob + o_bad);
@@ -364,8 +376,9 @@ done:
     if (blob) cudaFree(blob);
 #else
     (void)stream_v;
-    a.n_inst = a.in.blk_off[B]; a.n_val = a.in.val_off[F];
-    a.ops = ops; a.mods = mods; a.hint = hint;
+    a.n_inst = (uint32_t)counts[0]; a.n_val = (uint32_t)counts[1];
+    a.ops = ops; a.mods = mods;
+    if (hints) { a.hint_off = hints->off; a.hint_iid = hints->iid; a.hint_val = hints->val; }
     uint32_t *rec_off = (uint32_t *)malloc(4 * ((size_t)F + 1)), bad = 0;
     for (uint32_t f = 0; f <= F; f++) rec_off[f] = a.in.blk_off[a.in.func_blk_off[f]];
     a.func_rec_off = rec_off;

@@ -139,24 +139,46 @@ def mod_table() -> np.ndarray:
     return out
 
 
-def hints_of(functions) -> np.ndarray | None:
-    """u32 per record (corpus order: functions, block_order(), instructions) packing
-    meta["packed_def_width"], meta["packed_data_width"], meta["tensor_groups"]; None when no record has one."""
-    out, any_set = [], False
+@dataclass
+class Hints:
+    """``cl_typehints``: per function a run of (iid, packed meta) sorted by iid."""
+    off: np.ndarray
+    iid: np.ndarray
+    val: np.ndarray
+
+
+def hints_of(functions) -> Hints | None:
+    """The three ``Instruction.meta`` keys the signatures read (``packed_def_width``, ``packed_data_width``,
+    ``tensor_groups``) as a sparse table keyed by iid; None when no instruction has one."""
+    off, iids, vals = [0], [], []
     for fn in functions:
+        rows = []
         for blk in fn.block_order():
             for inst in blk.instructions:
                 m = inst.meta
-                h = 0
-                if m:
-                    g = m.get("tensor_groups") or {}
-                    h = ((m.get("packed_def_width") or 0) & 15) | ((m.get("packed_data_width", 0) or 0) & 15) << 4 \
-                        | (g.get("a", 0) & 255) << 8 | (g.get("b", 0) & 255) << 16 | (g.get("c", 0) & 255) << 24
-                    if "packed_data_width" in m and not m["packed_data_width"]:
-                        raise soa.EncodeError("packed_data_width = 0 cannot be encoded")
-                    any_set |= h != 0
-                out.append(h)
-    return np.asarray(out, np.uint32) if any_set else None
+                if not m:
+                    continue
+                g = m.get("tensor_groups") or {}
+                if "packed_data_width" in m and not m["packed_data_width"]:
+                    raise soa.EncodeError("packed_data_width = 0 cannot be encoded")
+                h = ((m.get("packed_def_width") or 0) & 15) | ((m.get("packed_data_width", 0) or 0) & 15) << 4 \
+                    | (g.get("a", 0) & 255) << 8 | (g.get("b", 0) & 255) << 16 | (g.get("c", 0) & 255) << 24
+                if h:
+                    rows.append((inst.iid, h))
+        rows.sort()
+        iids += [r[0] for r in rows]
+        vals += [r[1] for r in rows]
+        off.append(len(iids))
+    if not iids:
+        return None
+    return Hints(np.asarray(off, np.uint32), np.asarray(iids, np.uint32), np.asarray(vals, np.uint32))
+
+
+class TypeHints(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("off", "iid", "val")]
+
+
+SEED_INPUT, SEED_RESULT = 0, 1
 
 
 class TypeSeed(C.Structure):
@@ -173,21 +195,30 @@ class SeedArrays:
     status: np.ndarray
 
 
-def seed_corpus(engine, corpus: soa.Corpus, hints: np.ndarray | None = None, upload: bool = True,
-                into: SeedArrays | None = None) -> SeedArrays:
+def seed_corpus(engine, corpus: soa.Corpus, hints: Hints | None = None, upload: bool = True,
+                into: SeedArrays | None = None, source: int = SEED_INPUT) -> SeedArrays:
     """``cl_seed_types`` over an encoded corpus (the batch entry; ``upload=False`` reuses the
-    corpus the engine already holds; ``into``: caller-owned result arrays, e.g. pinned host memory)."""
+    corpus the engine already holds; ``into``: caller-owned result arrays, e.g. pinned host memory).
+    ``source=SEED_RESULT`` seeds the result the last ``run_postssa`` left on the device (no host round trip
+    between the stage and the seeding); ``corpus`` is then the corpus that was uploaded."""
     lib = engine.lib
     if not hasattr(lib, "cl_seed_types"):
         raise RuntimeError("this build of the library has no cl_seed_types (include/culifter_types.h)")
-    lib.cl_seed_types.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p,
-                                  C.POINTER(TypeSeed)]
+    lib.cl_seed_types.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32,
+                                  C.POINTER(TypeHints), C.POINTER(TypeSeed)]
     if upload:
+        if source != SEED_INPUT:
+            raise ValueError("seed_corpus: source=SEED_RESULT needs the run that made the result (upload=False)")
         engine.upload(corpus)
     ops, mods = op_table(), mod_table()
     n, nv = corpus.n_insts, len(corpus.val_alive)
-    if hints is not None and len(hints) != n:
-        raise ValueError(f"hints: {len(hints)} entries for {n} records")
+    if source == SEED_RESULT:
+        sizes = (C.c_uint64 * 6)()
+        engine._check(lib.cl_out_sizes(engine._ctx, sizes))
+        n, nv = int(sizes[0]), int(sizes[4])
+    if hints is not None and (len(hints.off) != corpus.n_funcs + 1 or len(hints.iid) != len(hints.val)
+                              or int(hints.off[-1]) != len(hints.iid)):
+        raise ValueError(f"hints: offsets for {len(hints.off) - 1} functions, corpus has {corpus.n_funcs}")
     if into is not None:
         want = dict(val_masks=(nv, np.uint32), role=(n, np.uint8), link_mask=(n, np.uint16), link_def=(n, np.uint32),
                     status=(corpus.n_funcs, np.uint8))
@@ -200,8 +231,11 @@ def seed_corpus(engine, corpus: soa.Corpus, hints: np.ndarray | None = None, upl
         res = SeedArrays(np.zeros(nv, np.uint32), np.zeros(n, np.uint8), np.zeros(n, np.uint16),
                          np.zeros(n, np.uint32), np.zeros(corpus.n_funcs, np.uint8))
     st = TypeSeed(*(a.ctypes.data_as(C.c_void_p) for a in (res.val_masks, res.role, res.link_mask, res.link_def, res.status)))
-    hp = np.ascontiguousarray(hints, np.uint32).ctypes.data_as(C.c_void_p) if hints is not None else None
-    engine._check(lib.cl_seed_types(engine._ctx, ops.ctypes.data_as(C.c_void_p), len(ops),
+    hp = None
+    if hints is not None:
+        keep = [np.ascontiguousarray(x, np.uint32) for x in (hints.off, hints.iid, hints.val)]
+        hp = C.byref(TypeHints(*(x.ctypes.data_as(C.c_void_p) for x in keep)))
+    engine._check(lib.cl_seed_types(engine._ctx, source, ops.ctypes.data_as(C.c_void_p), len(ops),
                                     mods.ctypes.data_as(C.c_void_p), len(mods), hp, C.byref(st)))
     return res
 
