@@ -160,57 +160,97 @@ TS_D void ts_narrow(const TsArgs &a, uint32_t f, uint32_t v0, uint32_t nv, uint3
     if (drop) ts_and(a.val_masks + v0 + vid, ~(drop | (is_def ? drop << 8 : drop << 16)));
 }
 
+/* ------------------------------------------------------------------ signature table
+ * The two switches above are evaluated ONCE on the host into a table the kernel indexes (a switch per slot made
+ * the lanes of a warp, which hold 32 different opcodes, run one after the other: 8 of 32 lanes active).  A row is a
+ * signature kind, or one of five variants picked by the modifier tuple / the operands; a cell is a literal mask,
+ * TS_LINK, or a sentinel naming a per-record parameter (element type of the modifier tuple, load width ...).   */
+enum { TS_ROW_IMAD_WIDE = CL_SK__COUNT, TS_ROW_LEA_HI, TS_ROW_BITCAST_F2I, TS_ROW_BITCAST_I2F, TS_ROW_MOV_LINK, TS_ROWS };
+enum { TS_P_F16 = 0xE1, TS_P_MMA, TS_P_CONVF, TS_P_CONVI, TS_P_F2FD, TS_P_F2FS, TS_P_ATOM, TS_P_LOADW, TS_P_ELEM, TS_P_ACCW };
+struct TsRow { uint16_t def[2]; uint16_t use[8]; uint16_t role, pad; };      /* def: k = 0, k >= 1; use: k = 0..6, k >= 7 */
+
+static void ts_build_table(TsRow *tab) {
+    cl_modtype mt; mt.f16_elem = TS_P_F16; mt.mma_elem = TS_P_MMA; mt.conv_float = TS_P_CONVF; mt.conv_int = TS_P_CONVI;
+    mt.f2f_dst = TS_P_F2FD; mt.f2f_src = TS_P_F2FS; mt.atom_elem = TS_P_ATOM; mt.flags = 0;
+    const cl_optype ot = { 0, 0 };
+    for (uint32_t row = 0; row < TS_ROWS; row++) {
+        uint32_t kind = row, movlink = 0, loadw = TS_P_LOADW;
+        cl_modtype m = mt;
+        switch (row) {
+        case TS_ROW_IMAD_WIDE: kind = CL_SK_IMAD; m.flags = CL_MT_WIDE; break;
+        case TS_ROW_LEA_HI: kind = CL_SK_LEA; m.flags = CL_MT_HI; break;
+        case TS_ROW_BITCAST_F2I: kind = CL_SK_BITCAST; m.flags = CL_MT_F2I; break;
+        case TS_ROW_BITCAST_I2F: kind = CL_SK_BITCAST; m.flags = CL_MT_I2F; break;
+        case TS_ROW_MOV_LINK: kind = CL_SK_MOV; movlink = TS_LINK; loadw = TS_LINK; break;
+        default: break;
+        }
+        for (uint32_t k = 0; k < 2; k++) tab[row].def[k] = (uint16_t)ts_def_c(kind, k, m, loadw, TS_P_ACCW);
+        for (uint32_t k = 0; k < 8; k++) tab[row].use[k] = (uint16_t)ts_use_c(kind, k, 255, ot, m, movlink, TS_P_ELEM, TS_P_ACCW, 0);
+        uint32_t role = CL_ROLE_SEED;
+        switch (kind) {
+        case CL_SK_LOP: case CL_SK_SHF: case CL_SK_SHLR: case CL_SK_SEL: case CL_SK_SELECT: case CL_SK_PHI: case CL_SK_SHUFFLE:
+            role = CL_ROLE_TRANSPARENT; break;
+        case CL_SK_I2F: case CL_SK_F2I: case CL_SK_F2F: case CL_SK_I2I: case CL_SK_FRND: case CL_SK_CAST64: case CL_SK_BITCAST:
+            role = CL_ROLE_CONVERSION; break;
+        default: break;
+        }
+        if (row == TS_ROW_MOV_LINK) role = CL_ROLE_TRANSPARENT;
+        tab[row].role = (uint16_t)role; tab[row].pad = 0;
+    }
+}
+
+/* a table cell with its parameter resolved: p0 / p1 hold the ten per-record parameters, one byte each */
+TS_HD uint32_t ts_cell(uint32_t c, uint64_t p0, uint32_t p1) {
+    const uint32_t i = c - TS_P_F16;
+    if (i >= 10u) return c;
+    return i < 8u ? (uint32_t)(p0 >> (8u * i)) & 0xFFu : (p1 >> (8u * (i - 8u))) & 0xFFu;
+}
+
 /* One record.  EXT = false: the 8 inline slots sit in registers and every slot loop is unrolled over the absolute
  * slot index (no local-memory array); EXT = true (more than 8 slots: wide PHIs, tensor ops): slots are read from
  * the function's overflow region.                                                                              */
-template <bool EXT> TS_D void ts_slots(const TsArgs &a, uint32_t i, uint32_t f, const TsRec &r) {
+template <bool EXT> TS_D void ts_slots(const TsArgs &a, const TsRow *tab, uint32_t i, uint32_t f, const TsRec &r) {
     const cl_optype ot = a.ops[r.h.op];
     const cl_modtype mt = a.mods[r.h.modset];
+    const uint32_t kind = ot.kind;
+    const bool is_load = kind == CL_SK_LOAD, is_store = kind == CL_SK_STORE, is_tensor = kind == CL_SK_TENSOR;
     /* only loads, stores and tensor ops read Instruction.meta */
-    const uint32_t hint = (ot.kind == CL_SK_LOAD || ot.kind == CL_SK_STORE || ot.kind == CL_SK_TENSOR) ? ts_hint(a, f, r.h.iid) : 0u;
+    const uint32_t hint = (a.hint_off && (is_load || is_store || is_tensor)) ? ts_hint(a, f, r.h.iid) : 0u;
     const uint32_t nd = r.h.n_defs, na = r.h.n_aux, nu = r.h.n_uses;
     const uint32_t d0 = r.g, a0 = d0 + nd, u0 = a0 + na, total = u0 + nu;
     const uint32_t v0 = a.in.val_off[f], nv = a.in.val_off[f + 1] - v0;
     const uint32_t addr = (ot.flags & CL_OT_ADDR64) ? CL_TY_INT64 : CL_TY_INT32;
-    const bool memop = ot.kind == CL_SK_LOAD || ot.kind == CL_SK_STORE || ot.kind == CL_SK_ATOMIC;
+    const bool memop = is_load || is_store || kind == CL_SK_ATOMIC;
     const uint32_t n_slots = EXT ? total : 8u;
 #define TS_FOR_SLOTS(s) _Pragma("unroll") for (uint32_t s = 0; s < n_slots; s++)
 #define TS_TAG(s) (EXT ? (uint32_t)r.xt[s] : (uint32_t)r.tag8[s])
 #define TS_PAY(s) (EXT ? r.xp[s] : r.pay8[s])
 
-    /* operand-dependent parts of the signature */
-    uint32_t loadw = 0, movlink = 0, elem = 0;
-    const uint32_t accw = (mt.flags & CL_MT_F32) ? CL_TY_FLOAT32 : CL_TY_INT32;
-    uint32_t role = CL_ROLE_SEED;
-    switch (ot.kind) {
-    case CL_SK_MOV: {                                                     /* typerec.py:135-139 */
-        bool any_value = false, seen = false; uint32_t w = 1;
-        TS_FOR_SLOTS(s) {
-            if (s < u0 || s >= total) continue;
-            const uint32_t t = TS_TAG(s);
-            if (CL_T_KIND(t) == CL_K_VALUE) any_value = true;
-            if (CL_T_KIND(t) == CL_K_CONSTMEM && !seen) { w = CL_T_WIDTH(t); seen = true; }
-        }
-        if (any_value) { loadw = movlink = TS_LINK; role = CL_ROLE_TRANSPARENT; } else loadw = ts_load_mask(w);
-        break; }
-    case CL_SK_LOAD: {                                                    /* :176-181 */
-        uint32_t w = 1;
-        TS_FOR_SLOTS(s) {
-            if (s < d0 || s >= a0) continue;
-            const uint32_t kd = CL_T_KIND(TS_TAG(s));
-            if ((kd == CL_K_REG || kd == CL_K_UREG) && (TS_PAY(s) >> 16) > w) w = TS_PAY(s) >> 16;
-        }
-        if (CL_TH_DEFW(hint)) w = CL_TH_DEFW(hint);
-        loadw = ts_load_mask(w);
-        break; }
-    case CL_SK_STORE: elem = (ot.flags & CL_OT_RED) ? mt.atom_elem : ts_load_mask(CL_TH_DATAW(hint) ? CL_TH_DATAW(hint) : 1u); break;
-    case CL_SK_ATOMIC: elem = mt.atom_elem; break;
-    case CL_SK_LOP: case CL_SK_SHF: case CL_SK_SHLR: case CL_SK_SEL: case CL_SK_SELECT: case CL_SK_PHI: case CL_SK_SHUFFLE:
-        role = CL_ROLE_TRANSPARENT; break;
-    case CL_SK_I2F: case CL_SK_F2I: case CL_SK_F2F: case CL_SK_I2I: case CL_SK_FRND: case CL_SK_CAST64: case CL_SK_BITCAST:
-        role = CL_ROLE_CONVERSION; break;
-    default: break;
+    /* operand-dependent parts of the signature, for every record alike (no branch on the opcode): is a use a value,
+     * width of the first ConstMem use (MOV, typerec.py:135-139), widest Reg / UReg def (loads, :176-181)          */
+    bool any_value = false, seen = false; uint32_t cmw = 1, regw = 1;
+    TS_FOR_SLOTS(s) {
+        const uint32_t t = TS_TAG(s), kd = CL_T_KIND(t);
+        const bool is_use = s >= u0 && s < total, is_def = s >= d0 && s < a0;
+        any_value |= is_use && kd == CL_K_VALUE;
+        if (is_use && kd == CL_K_CONSTMEM && !seen) { cmw = CL_T_WIDTH(t); seen = true; }
+        const uint32_t w = TS_PAY(s) >> 16;
+        if (is_def && (kd == CL_K_REG || kd == CL_K_UREG) && w > regw) regw = w;
     }
+    const uint32_t loadw = ts_load_mask(is_load ? (CL_TH_DEFW(hint) ? CL_TH_DEFW(hint) : regw) : cmw);
+    const uint32_t elem = (is_store && !(ot.flags & CL_OT_RED)) ? ts_load_mask(CL_TH_DATAW(hint) ? CL_TH_DATAW(hint) : 1u) : mt.atom_elem;
+    const uint32_t accw = (mt.flags & CL_MT_F32) ? CL_TY_FLOAT32 : CL_TY_INT32;
+    const uint64_t p0 = (uint64_t)mt.f16_elem | (uint64_t)mt.mma_elem << 8 | (uint64_t)mt.conv_float << 16 | (uint64_t)mt.conv_int << 24
+                        | (uint64_t)mt.f2f_dst << 32 | (uint64_t)mt.f2f_src << 40 | (uint64_t)mt.atom_elem << 48 | (uint64_t)loadw << 56;
+    const uint32_t p1 = elem | accw << 8;
+    uint32_t row = kind;
+    row = (kind == CL_SK_IMAD && (mt.flags & CL_MT_WIDE)) ? (uint32_t)TS_ROW_IMAD_WIDE : row;
+    row = (kind == CL_SK_LEA && (mt.flags & CL_MT_HI)) ? (uint32_t)TS_ROW_LEA_HI : row;
+    row = (kind == CL_SK_BITCAST && (mt.flags & CL_MT_I2F)) ? (uint32_t)TS_ROW_BITCAST_I2F : row;
+    row = (kind == CL_SK_BITCAST && (mt.flags & CL_MT_F2I)) ? (uint32_t)TS_ROW_BITCAST_F2I : row;     /* F2I is tested first (:170) */
+    row = (kind == CL_SK_MOV && any_value) ? (uint32_t)TS_ROW_MOV_LINK : row;
+    const TsRow &sig = tab[row < (uint32_t)TS_ROWS ? row : 0u];
+    const uint32_t n_ab = CL_TH_NA(hint) + CL_TH_NB(hint), n_abc = n_ab + CL_TH_NC(hint);      /* tensor operand groups, :209-214 */
 
     uint32_t link_def = CL_NO_VALUE, link_mask = 0;
     TS_FOR_SLOTS(s) {
@@ -218,38 +258,33 @@ template <bool EXT> TS_D void ts_slots(const TsArgs &a, uint32_t i, uint32_t f, 
         const uint32_t t = TS_TAG(s), kd = CL_T_KIND(t);
         if (kd != CL_K_VALUE && kd != CL_K_MEMREF) continue;
         const uint32_t p = TS_PAY(s);
-        if (s < d0) {                                                     /* guard, :334 */
-            if (kd == CL_K_VALUE) ts_narrow(a, f, v0, nv, p, CL_TY_BOOL, false);
-        } else if (s < a0) {                                              /* defs, :316-322 */
-            if (kd != CL_K_VALUE) continue;
-            const uint32_t c = ts_def_c(ot.kind, s - d0, mt, loadw, accw);
-            if (c == TS_LINK) link_def = p;
-            else if (c) ts_narrow(a, f, v0, nv, p, c, true);
-        } else if (s < u0) {                                              /* aux defs, :323-325: Signature.aux is always Bool */
-            if (kd == CL_K_VALUE) ts_narrow(a, f, v0, nv, p, CL_TY_BOOL, true);
-        } else {                                                          /* uses, :326-333 */
-            const uint32_t k = s - u0;
-            const uint32_t c = (memop && kd == CL_K_MEMREF) ? addr : (ot.kind == CL_SK_LOAD) ? 0u
-                               : ts_use_c(ot.kind, k, nu, ot, mt, movlink, elem, accw, hint);
-            uint32_t ref = CL_NO_VALUE;
-            if (kd == CL_K_VALUE) ref = p;
-            else {
-                const cl_memref m = a.in.mem[a.in.mem_off[f] + p];
-                if (CL_T_KIND(m.base_tag) == CL_K_VALUE) ref = m.base_pay;
-                if (CL_T_KIND(m.ureg_tag) == CL_K_VALUE) ts_narrow(a, f, v0, nv, m.ureg_pay, CL_TY_INT32, false);   /* _slot_values :281 */
-            }
+        const bool is_use = s >= u0, is_defslot = s >= d0 && s < a0, is_memref = kd == CL_K_MEMREF;
+        if (!is_use && is_memref) continue;                               /* defs, aux defs and the guard: values only */
+        const uint32_t k = is_use ? s - u0 : s - d0;
+        /* the constraint: Bool for the guard (:334) and the aux defs (:323-325), else the table cell */
+        uint32_t c = is_use ? sig.use[k < 7u ? k : 7u] : sig.def[k ? 1u : 0u];
+        if (is_use && is_tensor) c = k < n_ab ? (uint32_t)TS_P_MMA : k < n_abc ? (uint32_t)TS_P_ACCW : 0u;
+        c = ts_cell(c, p0, p1);
+        if (is_use && memop && is_memref) c = addr;
+        if (!is_use && !is_defslot) c = CL_TY_BOOL;
+        uint32_t ref = p;
+        if (is_memref) {                                                  /* _slot_values, :273-284 */
+            const cl_memref m = a.in.mem[a.in.mem_off[f] + p];
+            ref = CL_T_KIND(m.base_tag) == CL_K_VALUE ? m.base_pay : CL_NO_VALUE;
+            if (CL_T_KIND(m.ureg_tag) == CL_K_VALUE) ts_narrow(a, f, v0, nv, m.ureg_pay, CL_TY_INT32, false);
             if (ref == CL_NO_VALUE) continue;
-            if (c == TS_LINK) link_mask |= 1u << (k < 15 ? k : 15);
-            else if (c) ts_narrow(a, f, v0, nv, ref, c, false);
         }
+        if (c == TS_LINK) {
+            if (is_use) link_mask |= 1u << (k < 15u ? k : 15u); else link_def = p;
+        } else if (c) ts_narrow(a, f, v0, nv, ref, c, !is_use && s >= d0);
     }
-    a.role[i] = (uint8_t)role; a.link_mask[i] = (uint16_t)link_mask; a.link_def[i] = link_def;
+    a.role[i] = (uint8_t)sig.role; a.link_mask[i] = (uint16_t)link_mask; a.link_def[i] = link_def;
 #undef TS_FOR_SLOTS
 #undef TS_TAG
 #undef TS_PAY
 }
 
-TS_D void ts_record(const TsArgs &a, uint32_t i, uint32_t f) {
+TS_D void ts_record(const TsArgs &a, const TsRow *tab, uint32_t i, uint32_t f) {
     TsRec r;
     const uint4 h4 = ((const uint4 *)a.in.hdr)[i];
     memcpy(&r.h, &h4, 16);
@@ -258,12 +293,12 @@ TS_D void ts_record(const TsArgs &a, uint32_t i, uint32_t f) {
     if (r.h.op >= a.n_ops || r.h.modset >= a.n_mods) { *a.bad = 1; a.role[i] = 0; a.link_mask[i] = 0; a.link_def[i] = CL_NO_VALUE; return; }
     if (r.h.flags & CL_IF_EXT) {
         r.xt = a.in.ext_tag + a.in.ext_off[f] + r.h.ext; r.xp = a.in.ext_pay + a.in.ext_off[f] + r.h.ext;
-        ts_slots<true>(a, i, f, r);
+        ts_slots<true>(a, tab, i, f, r);
     } else {
         const uint4 t4 = ((const uint4 *)a.in.tag)[i];
         const uint4 p0 = ((const uint4 *)a.in.pay)[2 * (size_t)i], p1 = ((const uint4 *)a.in.pay)[2 * (size_t)i + 1];
         memcpy(r.tag8, &t4, 16); memcpy(r.pay8, &p0, 16); memcpy(r.pay8 + 4, &p1, 16);
-        ts_slots<false>(a, i, f, r);
+        ts_slots<false>(a, tab, i, f, r);
     }
 }
 
@@ -299,7 +334,13 @@ __global__ void __launch_bounds__(256) k_typeseed_prepare(TsArgs a, uint32_t *fu
         if (f < a.in.n_funcs) a.status[f] = CL_ST_OK;
     }
 }
-__global__ void __launch_bounds__(256) k_typeseed(TsArgs a) {
+#ifndef TS_MINB
+#define TS_MINB 5          /* resident CTAs per SM asked of ptxas: 46 registers, no spill */
+#endif
+__global__ void __launch_bounds__(256, TS_MINB) k_typeseed(TsArgs a, const TsRow *g_tab) {
+    __shared__ TsRow tab[TS_ROWS];
+    for (uint32_t w = threadIdx.x; w < sizeof(tab) / 4; w += blockDim.x) ((uint32_t *)tab)[w] = ((const uint32_t *)g_tab)[w];
+    __syncthreads();
     const uint32_t n = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
     for (uint32_t base = t - lane; base < a.n_inst; base += n) {
         /* one search per warp: the 32 records of a warp lie in a few neighbouring functions */
@@ -309,7 +350,7 @@ __global__ void __launch_bounds__(256) k_typeseed(TsArgs a) {
         const uint32_t i = base + lane;
         if (i < a.n_inst) {
             while (f + 1 < a.in.n_funcs && a.func_rec_off[f + 1] <= i) f++;
-            ts_record(a, i, f);
+            ts_record(a, tab, i, f);
         }
     }
     for (uint32_t b = t; b < a.in.n_blocks; b += n) ts_block(a, b);
@@ -324,8 +365,11 @@ extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, u
     uint64_t counts[2] = { 0, 0 };
     if (cli_corpus_view(c, source, &a.in, counts, &stream_v, &last_ms)) return -1;
     const uint32_t F = a.in.n_funcs, B = a.in.n_blocks;
+    (void)B;
     a.n_ops = n_ops; a.n_mods = n_mods;
     int rc = 0; char msg[400] = "";
+    static TsRow h_tab[TS_ROWS];
+    ts_build_table(h_tab);
 #if TS_CUDA
     cudaStream_t st = (cudaStream_t)stream_v;
     uint8_t *blob = nullptr; cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -335,7 +379,7 @@ extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, u
         auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
         const size_t o_ops = 0, o_mods = o_ops + up(sizeof(cl_optype) * n_ops), o_hint = o_mods + up(sizeof(cl_modtype) * n_mods),
                      o_rec = o_hint + (hints ? up(4 * ((size_t)F + 1)) + 2 * up(4 * H) : 0), o_masks = o_rec + up(4 * ((size_t)F + 1)), o_role = o_masks + up(4 * V),
-                     o_lm = o_role + up(N), o_ld = o_lm + up(2 * N), o_st = o_ld + up(4 * N), o_bad = o_st + up(F), total = o_bad + 256;
+                     o_lm = o_role + up(N), o_ld = o_lm + up(2 * N), o_st = o_ld + up(4 * N), o_bad = o_st + up(F), o_tab = o_bad + 256, total = o_tab + up(sizeof(TsRow) * TS_ROWS);
         TS_OK(cudaMalloc((void **)&blob, total));
         TS_OK(cudaMemcpyAsync(blob + o_ops, ops, sizeof(cl_optype) * n_ops, cudaMemcpyHostToDevice, st));
         TS_OK(cudaMemcpyAsync(blob + o_mods, mods, sizeof(cl_modtype) * n_mods, cudaMemcpyHostToDevice, st));
@@ -346,6 +390,7 @@ extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, u
             a.hint_off = (const uint32_t *)h0; a.hint_iid = (const uint32_t *)h1; a.hint_val = (const uint32_t *)h2;
         }
         TS_OK(cudaMemsetAsync(blob + o_bad, 0, 4, st));
+        TS_OK(cudaMemcpyAsync(blob + o_tab, h_tab, sizeof(TsRow) * TS_ROWS, cudaMemcpyHostToDevice, st));
         a.ops = (const cl_optype *)(blob + o_ops); a.mods = (const cl_modtype *)(blob + o_mods);
         a.func_rec_off = (const uint32_t *)(blob + o_rec);
         a.val_masks = (uint32_t *)(blob + o_masks); a.role = blob + o_role; a.link_mask = (uint16_t *)(blob + o_lm);
@@ -356,7 +401,7 @@ extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, u
         TS_OK(cudaEventCreate(&e0)); TS_OK(cudaEventCreate(&e1));
         TS_OK(cudaEventRecord(e0, st));
         k_typeseed_prepare<<<grid, 256, 0, st>>>(a, (uint32_t *)(blob + o_rec));
-        k_typeseed<<<grid, 256, 0, st>>>(a);
+        k_typeseed<<<grid, 256, 0, st>>>(a, (const TsRow *)(blob + o_tab));
         TS_OK(cudaGetLastError());
         TS_OK(cudaEventRecord(e1, st));
         uint32_t bad = 0;
@@ -385,7 +430,7 @@ done:
     a.val_masks = out->val_masks; a.role = out->role; a.link_mask = out->link_mask; a.link_def = out->link_def; a.status = out->status; a.bad = &bad;
     for (uint32_t v = 0; v < a.n_val; v++) a.val_masks[v] = 0xFFFFFFu;
     for (uint32_t f = 0; f < F; f++) a.status[f] = CL_ST_OK;
-    for (uint32_t i = 0; i < a.n_inst; i++) ts_record(a, i, ts_func_of(rec_off, F, i));
+    for (uint32_t i = 0; i < a.n_inst; i++) ts_record(a, h_tab, i, ts_func_of(rec_off, F, i));
     for (uint32_t b = 0; b < B; b++) ts_block(a, b);
     free(rec_off);
     if (last_ms) *last_ms = 0;

@@ -25,7 +25,8 @@ CSRC = ROOT / "paper_2604_27486_b200" / "csrc"
 
 _ALL = sorted(p.name[:-len(".pkl.gz")] for p in GOLDEN.glob("*.pkl.gz") if not p.name.startswith("pool_"))
 RAW_FIXTURES = [n for n in _ALL if n.startswith("raw_")]
-FIXTURES = [n for n in _ALL if n not in RAW_FIXTURES]
+TYPE_FIXTURES = [n for n in _ALL if n.startswith("types")]           # type seeding (tests/test_typeseed.py)
+FIXTURES = [n for n in _ALL if n not in RAW_FIXTURES and n not in TYPE_FIXTURES]
 STATUS_ERROR = {2: "AttributeError", 3: "AssertionError", 4: "KeyError", 6: "IndexError"}
 
 

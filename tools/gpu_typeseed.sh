@@ -13,7 +13,7 @@ ncu --set full --clock-control none --import-source on -k regex:^k_typeseed$ -c 
 ncu -i gpurun_out/${T}_ncu_typeseed.ncu-rep --page details > gpurun_out/${T}_ncu_full_k_typeseed_details.txt
 ncu -i gpurun_out/${T}_ncu_typeseed.ncu-rep --page raw --csv > gpurun_out/${T}_ncu_full_k_typeseed_raw.csv
 grep -E "Duration|DRAM Throughput|Memory Throughput|Executed Ipc Active|No Eligible|Registers Per|Achieved Occupancy|Avg. Active Threads|L2 Hit" gpurun_out/${T}_ncu_full_k_typeseed_details.txt
-grep -E "dram__bytes_(read|write).sum" gpurun_out/${T}_ncu_full_k_typeseed_raw.csv | head -3
+
 ncu -i gpurun_out/${T}_ncu_typeseed.ncu-rep --page source --csv > gpurun_out/${T}_ncu_full_k_typeseed_source.csv 2>/dev/null
 rm -f gpurun_out/${T}_ncu_typeseed.ncu-rep
 du -sh gpurun_out
