@@ -300,7 +300,7 @@ def typeseed_leg(eng, peak, threads, steps, warmup, with_cpu, n_sass=20_000_000)
     t = float(np.mean(ms))
     out = {"config": "typeseed", "workload": f"seed_types over the normalised mixed corpus: {ns} SASS instructions, {R} records, {V} values, {F} kernels",
            "metric": METRIC, "value": ns / (t / 1e3), "unit": UNIT, "ms_per_step": t, "steps": steps, "warmup": warmup,
-           "gpu_launches": 2 * steps, "kernel": "k_typeseed (+ k_typeseed_prepare: mask fill, record offsets)",
+           "gpu_launches": 4 * steps, "kernel": "k_typeseed (+ k_typeseed_prepare: mask fill, record offsets; k_typeseed_index: function of every run of 32 records; k_typeseed_check: dead values)",
            "roofline": {"bound": "hbm", "achieved": algo / (t / 1e3) / 1e9, "peak": peak, "unit": "GB/s", "frac": algo / (t / 1e3) / 1e9 / peak,
                         "traffic": None, "algorithmic_bytes_per_launch": int(algo),
                         "bytes_per_record": "64 read + 7 written per record, 8 per value (fill + result), 16 per block terminator, CSR offsets"},

@@ -40,10 +40,13 @@ extern "C" void cli_set_error(const char *msg);
 #define FAIL(...) do { char b_[400]; snprintf(b_, sizeof b_, __VA_ARGS__); cli_set_error(b_); return -1; } while (0)
 
 #define TS_LINK 0x100u
+#define TS_TOP3 0xFFFFFFu        /* seed | def << 8 | use << 16, all at top */
+#define TS_DEAD 0x80000000u      /* fill marker of a vid that is not in fn.values */
 
 struct TsArgs {
     cl_corpus in;                    /* device pointers */
     const uint32_t *func_rec_off;    /* [F+1] first record of every function */
+    const uint32_t *warp_func;       /* [ceil(n_inst / 32)] function of the first record of every run of 32 records */
     const cl_optype *ops; const cl_modtype *mods;
     const uint32_t *hint_off, *hint_iid, *hint_val;   /* cl_typehints on the device, hint_off == nullptr: none */
     uint32_t n_ops, n_mods, n_inst, n_val;
@@ -155,7 +158,9 @@ TS_D void ts_and(uint32_t *p, uint32_t v) {
 }
 /* narrow (typerec.py:300-305) */
 TS_D void ts_narrow(const TsArgs &a, uint32_t f, uint32_t v0, uint32_t nv, uint32_t vid, uint32_t mask, bool is_def) {
-    if (vid >= nv || !a.in.val_alive[v0 + vid]) { a.status[f] = CL_ST_KEY_ERROR; return; }
+    /* a value that is not in fn.values (KeyError upstream): its word carries TS_DEAD from the fill, any narrowing of it
+     * is found by the check pass -- no load of val_alive in front of every red.and                                   */
+    if (vid >= nv) { a.status[f] = CL_ST_KEY_ERROR; return; }
     const uint32_t drop = ~mask & 0xFFu;
     if (drop) ts_and(a.val_masks + v0 + vid, ~(drop | (is_def ? drop << 8 : drop << 16)));
 }
@@ -315,24 +320,34 @@ TS_HD uint32_t ts_func_of(const uint32_t *rec_off, uint32_t F, uint32_t i) {
     return f;
 }
 
-TS_D void ts_block(const TsArgs &a, uint32_t b) {                         /* :342-343 */
+TS_D void ts_block(const TsArgs &a, uint32_t b, uint32_t f) {             /* :342-343 */
     const cl_blk bl = a.in.blk[b];
-    if (CL_T_KIND(bl.term_tag[0]) != CL_K_VALUE && CL_T_KIND(bl.term_tag[1]) != CL_K_VALUE) return;
-    uint32_t f = ts_find(a.in.func_blk_off, a.in.n_funcs, b);
-    while (f + 1 < a.in.n_funcs && a.in.func_blk_off[f + 1] <= b) f++;
     const uint32_t v0 = a.in.val_off[f], nv = a.in.val_off[f + 1] - v0;
     for (int t = 0; t < 2; t++)
         if (CL_T_KIND(bl.term_tag[t]) == CL_K_VALUE) ts_narrow(a, f, v0, nv, bl.term_pay[t], CL_TY_BOOL, false);
+}
+/* after the narrowing: a dead vid whose word moved was narrowed (KeyError upstream); dead words read TOP again */
+TS_D void ts_check_value(const TsArgs &a, uint32_t v) {
+    const uint32_t m = a.val_masks[v];
+    if (!(m & TS_DEAD)) return;
+    if (m != (TS_DEAD | TS_TOP3)) a.status[ts_func_of(a.in.val_off, a.in.n_funcs, v)] = CL_ST_KEY_ERROR;
+    a.val_masks[v] = TS_TOP3;
 }
 
 #if TS_CUDA
 __global__ void __launch_bounds__(256) k_typeseed_prepare(TsArgs a, uint32_t *func_rec_off) {
     const size_t n = (size_t)gridDim.x * blockDim.x, t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    for (size_t v = t; v < a.n_val; v += n) a.val_masks[v] = 0xFFFFFFu;                 /* :292-295: TOP */
+    for (size_t v = t; v < a.n_val; v += n) a.val_masks[v] = a.in.val_alive[v] ? TS_TOP3 : (TS_DEAD | TS_TOP3);   /* :292-295: TOP */
     for (size_t f = t; f <= a.in.n_funcs; f += n) {
         func_rec_off[f] = a.in.blk_off[a.in.func_blk_off[f]];
         if (f < a.in.n_funcs) a.status[f] = CL_ST_OK;
     }
+}
+/* one binary search per run of 32 records, all in parallel (the record kernel used to search with lane 0 of every
+ * warp while 31 lanes waited: 30 % of its stall samples)                                                        */
+__global__ void __launch_bounds__(256) k_typeseed_index(TsArgs a, uint32_t *warp_func) {
+    const uint32_t n = gridDim.x * blockDim.x, n_runs = (a.n_inst + 31) / 32;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_runs; w += n) warp_func[w] = ts_func_of(a.func_rec_off, a.in.n_funcs, w * 32);
 }
 #ifndef TS_MINB
 #define TS_MINB 5          /* resident CTAs per SM asked of ptxas: 46 registers, no spill */
@@ -341,19 +356,18 @@ __global__ void __launch_bounds__(256, TS_MINB) k_typeseed(TsArgs a, const TsRow
     __shared__ TsRow tab[TS_ROWS];
     for (uint32_t w = threadIdx.x; w < sizeof(tab) / 4; w += blockDim.x) ((uint32_t *)tab)[w] = ((const uint32_t *)g_tab)[w];
     __syncthreads();
-    const uint32_t n = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
-    for (uint32_t base = t - lane; base < a.n_inst; base += n) {
-        /* one search per warp: the 32 records of a warp lie in a few neighbouring functions */
-        uint32_t f = 0;
-        if (lane == 0) f = ts_func_of(a.func_rec_off, a.in.n_funcs, base);
-        f = __shfl_sync(0xFFFFFFFFu, f, 0);
-        const uint32_t i = base + lane;
-        if (i < a.n_inst) {
-            while (f + 1 < a.in.n_funcs && a.func_rec_off[f + 1] <= i) f++;
-            ts_record(a, tab, i, f);
-        }
+    const uint32_t n = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t i = t; i < a.n_inst; i += n) {
+        uint32_t f = a.warp_func[i >> 5];                     /* the 32 records of a warp lie in a few neighbouring functions */
+        while (f + 1 < a.in.n_funcs && a.func_rec_off[f + 1] <= i) f++;
+        ts_record(a, tab, i, f);
     }
-    for (uint32_t b = t; b < a.in.n_blocks; b += n) ts_block(a, b);
+    for (uint32_t f = t; f < a.in.n_funcs; f += n)            /* terminator conditions of the function's blocks */
+        for (uint32_t b = a.in.func_blk_off[f]; b < a.in.func_blk_off[f + 1]; b++) ts_block(a, b, f);
+}
+__global__ void __launch_bounds__(256) k_typeseed_check(TsArgs a) {
+    const uint32_t n = gridDim.x * blockDim.x;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n_val; v += n) ts_check_value(a, v);
 }
 #define TS_OK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { rc = -1; snprintf(msg, sizeof msg, "%s: %s", #x, cudaGetErrorString(e_)); goto done; } } while (0)
 #endif
@@ -379,7 +393,7 @@ extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, u
         auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
         const size_t o_ops = 0, o_mods = o_ops + up(sizeof(cl_optype) * n_ops), o_hint = o_mods + up(sizeof(cl_modtype) * n_mods),
                      o_rec = o_hint + (hints ? up(4 * ((size_t)F + 1)) + 2 * up(4 * H) : 0), o_masks = o_rec + up(4 * ((size_t)F + 1)), o_role = o_masks + up(4 * V),
-                     o_lm = o_role + up(N), o_ld = o_lm + up(2 * N), o_st = o_ld + up(4 * N), o_bad = o_st + up(F), o_tab = o_bad + 256, total = o_tab + up(sizeof(TsRow) * TS_ROWS);
+                     o_lm = o_role + up(N), o_ld = o_lm + up(2 * N), o_st = o_ld + up(4 * N), o_bad = o_st + up(F), o_tab = o_bad + 256, o_wf = o_tab + up(sizeof(TsRow) * TS_ROWS), total = o_wf + up(4 * ((N + 31) / 32 + 1));
         TS_OK(cudaMalloc((void **)&blob, total));
         TS_OK(cudaMemcpyAsync(blob + o_ops, ops, sizeof(cl_optype) * n_ops, cudaMemcpyHostToDevice, st));
         TS_OK(cudaMemcpyAsync(blob + o_mods, mods, sizeof(cl_modtype) * n_mods, cudaMemcpyHostToDevice, st));
@@ -392,7 +406,7 @@ extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, u
         TS_OK(cudaMemsetAsync(blob + o_bad, 0, 4, st));
         TS_OK(cudaMemcpyAsync(blob + o_tab, h_tab, sizeof(TsRow) * TS_ROWS, cudaMemcpyHostToDevice, st));
         a.ops = (const cl_optype *)(blob + o_ops); a.mods = (const cl_modtype *)(blob + o_mods);
-        a.func_rec_off = (const uint32_t *)(blob + o_rec);
+        a.func_rec_off = (const uint32_t *)(blob + o_rec); a.warp_func = (const uint32_t *)(blob + o_wf);
         a.val_masks = (uint32_t *)(blob + o_masks); a.role = blob + o_role; a.link_mask = (uint16_t *)(blob + o_lm);
         a.link_def = (uint32_t *)(blob + o_ld); a.status = blob + o_st; a.bad = (uint32_t *)(blob + o_bad);
         int dev = 0, n_sm = 148;
@@ -401,7 +415,9 @@ extern "C" int cl_seed_types(cl_ctx *c, uint32_t source, const cl_optype *ops, u
         TS_OK(cudaEventCreate(&e0)); TS_OK(cudaEventCreate(&e1));
         TS_OK(cudaEventRecord(e0, st));
         k_typeseed_prepare<<<grid, 256, 0, st>>>(a, (uint32_t *)(blob + o_rec));
+        k_typeseed_index<<<grid, 256, 0, st>>>(a, (uint32_t *)(blob + o_wf));
         k_typeseed<<<grid, 256, 0, st>>>(a, (const TsRow *)(blob + o_tab));
+        k_typeseed_check<<<grid, 256, 0, st>>>(a);
         TS_OK(cudaGetLastError());
         TS_OK(cudaEventRecord(e1, st));
         uint32_t bad = 0;
@@ -428,10 +444,12 @@ done:
     for (uint32_t f = 0; f <= F; f++) rec_off[f] = a.in.blk_off[a.in.func_blk_off[f]];
     a.func_rec_off = rec_off;
     a.val_masks = out->val_masks; a.role = out->role; a.link_mask = out->link_mask; a.link_def = out->link_def; a.status = out->status; a.bad = &bad;
-    for (uint32_t v = 0; v < a.n_val; v++) a.val_masks[v] = 0xFFFFFFu;
+    for (uint32_t v = 0; v < a.n_val; v++) a.val_masks[v] = a.in.val_alive[v] ? TS_TOP3 : (TS_DEAD | TS_TOP3);
     for (uint32_t f = 0; f < F; f++) a.status[f] = CL_ST_OK;
     for (uint32_t i = 0; i < a.n_inst; i++) ts_record(a, h_tab, i, ts_func_of(rec_off, F, i));
-    for (uint32_t b = 0; b < B; b++) ts_block(a, b);
+    for (uint32_t f = 0; f < F; f++)
+        for (uint32_t b = a.in.func_blk_off[f]; b < a.in.func_blk_off[f + 1]; b++) ts_block(a, b, f);
+    for (uint32_t v = 0; v < a.n_val; v++) ts_check_value(a, v);
     free(rec_off);
     if (last_ms) *last_ms = 0;
     if (bad) { rc = -1; snprintf(msg, sizeof msg, "cl_seed_types: opcode / modset id outside the tables"); }
