@@ -298,11 +298,18 @@ def typeseed_leg(eng, peak, threads, steps, warmup, with_cpu, n_sass=20_000_000)
     R, V, B, F = corpus.n_insts, len(corpus.val_alive), corpus.n_blocks, corpus.n_funcs
     algo = 64 * R + 7 * R + 8 * V + 16 * B + 4 * (B + 3 * F)
     t = float(np.mean(ms))
+    traffic = None
+    try:                       # DRAM bytes of k_typeseed per launch from the committed ncu capture of this very leg
+        tr = json.loads((ROOT / "profiles" / "r02_traffic.json").read_text())["k_typeseed"]
+        if abs(ns - tr["workload_sass_insts"]) < 0.01 * tr["workload_sass_insts"]:
+            traffic = tr["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
     out = {"config": "typeseed", "workload": f"seed_types over the normalised mixed corpus: {ns} SASS instructions, {R} records, {V} values, {F} kernels",
            "metric": METRIC, "value": ns / (t / 1e3), "unit": UNIT, "ms_per_step": t, "steps": steps, "warmup": warmup,
            "gpu_launches": 4 * steps, "kernel": "k_typeseed (+ k_typeseed_prepare: mask fill, record offsets; k_typeseed_index: function of every run of 32 records; k_typeseed_check: dead values)",
            "roofline": {"bound": "hbm", "achieved": algo / (t / 1e3) / 1e9, "peak": peak, "unit": "GB/s", "frac": algo / (t / 1e3) / 1e9 / peak,
-                        "traffic": None, "algorithmic_bytes_per_launch": int(algo),
+                        "traffic": traffic, "algorithmic_bytes_per_launch": int(algo),
                         "bytes_per_record": "64 read + 7 written per record, 8 per value (fill + result), 16 per block terminator, CSR offsets"},
            "e2e": {"value": ns / float(np.mean(wall)), "unit": UNIT, "ms_per_step": float(np.mean(wall)) * 1e3,
                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(7 * R + 4 * V + F),
