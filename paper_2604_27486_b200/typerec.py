@@ -240,6 +240,62 @@ def seed_corpus(engine, corpus: soa.Corpus, hints: Hints | None = None, upload: 
     return res
 
 
+def _gather_runs(off: np.ndarray, members: np.ndarray) -> np.ndarray:
+    """Indices of the CSR runs ``off[f]:off[f+1]`` of the functions ``members``, run after run."""
+    off = off.astype(np.int64)
+    starts, lens = off[members], (off[1:] - off[:-1])[members]
+    total = int(lens.sum())
+    if total == 0:
+        return np.zeros(0, np.int64)
+    return np.repeat(starts - (np.cumsum(lens) - lens), lens) + np.arange(total, dtype=np.int64)
+
+
+def seed_corpus_sharded(engines, corpus: soa.Corpus, hints: Hints | None = None) -> SeedArrays:
+    """``seed_corpus`` spread over several engines (one per GPU): the corpus is partitioned by kernel
+    (``sharding.shard``: LPT on instruction records; functions are independent, nothing crosses devices) and the
+    arrays come back in the corpus' own order."""
+    import threading
+    from . import sharding
+    engines = list(engines)
+    plan = sharding.shard_plan(corpus, len(engines))
+    parts = sharding.shard(corpus, len(engines), plan)
+    part_hints = [None] * len(engines)
+    if hints is not None:
+        for k, m in enumerate(plan.members):
+            idx = _gather_runs(hints.off, m)
+            lens = np.diff(hints.off.astype(np.int64))[m]
+            part_hints[k] = Hints(np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32), hints.iid[idx], hints.val[idx])
+    outs, errors = [None] * len(engines), []
+
+    def work(k):
+        try:
+            outs[k] = seed_corpus(engines[k], parts[k], part_hints[k])
+        except Exception as e:  # noqa: BLE001 - re-raised on the caller's thread
+            errors.append(e)
+
+    if all(e.backend.startswith("cuda") for e in engines):
+        threads = [threading.Thread(target=work, args=(k,)) for k in range(len(engines))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    else:                                        # the CPU builds: one at a time
+        for k in range(len(engines)):
+            work(k)
+    if errors:
+        raise errors[0]
+    n, nv = corpus.n_insts, len(corpus.val_alive)
+    res = SeedArrays(np.zeros(nv, np.uint32), np.zeros(n, np.uint8), np.zeros(n, np.uint16),
+                     np.zeros(n, np.uint32), np.zeros(corpus.n_funcs, np.uint8))
+    rec_off = corpus.blk_off[corpus.func_blk_off]
+    for m, o in zip(plan.members, outs):
+        rec, val = _gather_runs(rec_off, m), _gather_runs(corpus.val_off, m)
+        res.role[rec], res.link_mask[rec], res.link_def[rec] = o.role, o.link_mask, o.link_def
+        res.val_masks[val] = o.val_masks
+        res.status[m] = o.status
+    return res
+
+
 @dataclass
 class TypeSet:
     """Mirror of ``lattice.TypeSet`` (lattice.py:119-145): candidate set plus the conflicted flag."""
@@ -319,16 +375,19 @@ def states_of(corpus: soa.Corpus, res: SeedArrays) -> list:
     return out
 
 
-def seed_types_batch(functions, engine=None) -> list:
-    """``seed_types`` for many functions in one launch; sets ``fn.meta["type_state"]`` like the reference."""
+def seed_types_batch(functions, engine=None, engines=None) -> list:
+    """``seed_types`` for many functions in one launch; sets ``fn.meta["type_state"]`` like the reference.
+    ``engines=[...]`` (one per GPU) spreads the batch by kernel over several devices."""
     from . import passes
     functions = list(functions)
     for fn in functions:
         phase = sys.modules[type(fn).__module__].Phase          # the Phase enum of the package fn comes from
         fn.require_phase(phase.NORMALIZED, phase.SSA, phase.TYPED)   # typerec.py:290
     corpus = soa.encode(functions)
-    eng = engine or passes.default_engine()
-    res = seed_corpus(eng, corpus, hints_of(functions))
+    if engines is not None:
+        res = seed_corpus_sharded(engines, corpus, hints_of(functions))
+    else:
+        res = seed_corpus(engine or passes.default_engine(), corpus, hints_of(functions))
     states = states_of(corpus, res)
     for k, (fn, st, status) in enumerate(zip(functions, states, res.status.tolist())):
         if status == L.ST_KEY_ERROR:

@@ -206,3 +206,18 @@ def test_hints_survive_the_stage():
     for f in range(len(fns)):
         run = hints.iid[hints.off[f]:hints.off[f + 1]]
         assert (np.diff(run.astype(np.int64)) > 0).all()
+
+
+def test_sharded_over_two_engines_equals_one():
+    """Two engines, the corpus partitioned by kernel: same arrays, same TypeStates (hints sliced per shard)."""
+    fix = helpers.load_fixture("types")
+    fns = copy.deepcopy(fix["functions"])
+    corpus, hints = soa.encode(fns), typerec.hints_of(fns)
+    one = typerec.seed_corpus(helpers.oracle_engine(), corpus, hints)
+    for engines in ([helpers.oracle_engine(), helpers.oracle_engine()], [helpers.oracle_engine()] * 3):
+        two = typerec.seed_corpus_sharded(engines, corpus, hints)
+        for n in ARRAYS:
+            assert np.array_equal(getattr(one, n), getattr(two, n)), n
+    states = typerec.seed_types_batch(fns, engines=[helpers.oracle_engine(), helpers.oracle_engine()])
+    for st, exp in zip(states, fix["expect"]):
+        assert st.seed_mask == exp["seed_mask"] and st.link_exprs == exp["link_exprs"] and st.roles == exp["roles"]
