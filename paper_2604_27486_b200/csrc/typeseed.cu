@@ -289,10 +289,17 @@ template <bool EXT> TS_D void ts_slots(const TsArgs &a, const TsRow *tab, uint32
 #undef TS_PAY
 }
 
-TS_D void ts_record(const TsArgs &a, const TsRow *tab, uint32_t i, uint32_t f) {
+/* the 64 bytes of a record as four 128-bit words (header, tags, payloads) */
+struct TsPlanes { uint4 h, t, p0, p1; };
+TS_D TsPlanes ts_load(const TsArgs &a, uint32_t i) {
+    TsPlanes q;
+    q.h = ((const uint4 *)a.in.hdr)[i]; q.t = ((const uint4 *)a.in.tag)[i];
+    q.p0 = ((const uint4 *)a.in.pay)[2 * (size_t)i]; q.p1 = ((const uint4 *)a.in.pay)[2 * (size_t)i + 1];
+    return q;
+}
+TS_D void ts_record(const TsArgs &a, const TsRow *tab, uint32_t i, uint32_t f, const TsPlanes &q) {
     TsRec r;
-    const uint4 h4 = ((const uint4 *)a.in.hdr)[i];
-    memcpy(&r.h, &h4, 16);
+    memcpy(&r.h, &q.h, 16);
     r.f = f; r.g = (r.h.flags & CL_IF_GUARD) ? 1u : 0u;
     r.xt = nullptr; r.xp = nullptr;
     if (r.h.op >= a.n_ops || r.h.modset >= a.n_mods) { *a.bad = 1; a.role[i] = 0; a.link_mask[i] = 0; a.link_def[i] = CL_NO_VALUE; return; }
@@ -300,9 +307,7 @@ TS_D void ts_record(const TsArgs &a, const TsRow *tab, uint32_t i, uint32_t f) {
         r.xt = a.in.ext_tag + a.in.ext_off[f] + r.h.ext; r.xp = a.in.ext_pay + a.in.ext_off[f] + r.h.ext;
         ts_slots<true>(a, tab, i, f, r);
     } else {
-        const uint4 t4 = ((const uint4 *)a.in.tag)[i];
-        const uint4 p0 = ((const uint4 *)a.in.pay)[2 * (size_t)i], p1 = ((const uint4 *)a.in.pay)[2 * (size_t)i + 1];
-        memcpy(r.tag8, &t4, 16); memcpy(r.pay8, &p0, 16); memcpy(r.pay8 + 4, &p1, 16);
+        memcpy(r.tag8, &q.t, 16); memcpy(r.pay8, &q.p0, 16); memcpy(r.pay8 + 4, &q.p1, 16);
         ts_slots<false>(a, tab, i, f, r);
     }
 }
@@ -337,7 +342,16 @@ TS_D void ts_check_value(const TsArgs &a, uint32_t v) {
 #if TS_CUDA
 __global__ void __launch_bounds__(256) k_typeseed_prepare(TsArgs a, uint32_t *func_rec_off) {
     const size_t n = (size_t)gridDim.x * blockDim.x, t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    for (size_t v = t; v < a.n_val; v += n) a.val_masks[v] = a.in.val_alive[v] ? TS_TOP3 : (TS_DEAD | TS_TOP3);   /* :292-295: TOP */
+    /* :292-295: every value at TOP; four values per thread (the arrays start 256-byte aligned) */
+    const size_t quads = a.n_val / 4;
+    for (size_t q = t; q < quads; q += n) {
+        const uint32_t al = ((const uint32_t *)a.in.val_alive)[q];
+        uint4 m;
+        m.x = (al & 0xFFu) ? TS_TOP3 : (TS_DEAD | TS_TOP3); m.y = (al & 0xFF00u) ? TS_TOP3 : (TS_DEAD | TS_TOP3);
+        m.z = (al & 0xFF0000u) ? TS_TOP3 : (TS_DEAD | TS_TOP3); m.w = (al & 0xFF000000u) ? TS_TOP3 : (TS_DEAD | TS_TOP3);
+        ((uint4 *)a.val_masks)[q] = m;
+    }
+    for (size_t v = quads * 4 + t; v < a.n_val; v += n) a.val_masks[v] = a.in.val_alive[v] ? TS_TOP3 : (TS_DEAD | TS_TOP3);
     for (size_t f = t; f <= a.in.n_funcs; f += n) {
         func_rec_off[f] = a.in.blk_off[a.in.func_blk_off[f]];
         if (f < a.in.n_funcs) a.status[f] = CL_ST_OK;
@@ -350,24 +364,31 @@ __global__ void __launch_bounds__(256) k_typeseed_index(TsArgs a, uint32_t *warp
     for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_runs; w += n) warp_func[w] = ts_func_of(a.func_rec_off, a.in.n_funcs, w * 32);
 }
 #ifndef TS_MINB
-#define TS_MINB 5          /* resident CTAs per SM asked of ptxas: 46 registers, no spill */
+#define TS_MINB 5          /* resident CTAs per SM asked of ptxas: 45 registers, no spill (4 / 5 / 6 / 8 measured alike) */
 #endif
 __global__ void __launch_bounds__(256, TS_MINB) k_typeseed(TsArgs a, const TsRow *g_tab) {
     __shared__ TsRow tab[TS_ROWS];
     for (uint32_t w = threadIdx.x; w < sizeof(tab) / 4; w += blockDim.x) ((uint32_t *)tab)[w] = ((const uint32_t *)g_tab)[w];
     __syncthreads();
     const uint32_t n = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
+    /* (requesting the planes of the thread's next record before working on the current one was measured: no gain,
+     * 0.904 vs 0.903 ms, and 63 registers instead of 45) */
     for (uint32_t i = t; i < a.n_inst; i += n) {
         uint32_t f = a.warp_func[i >> 5];                     /* the 32 records of a warp lie in a few neighbouring functions */
         while (f + 1 < a.in.n_funcs && a.func_rec_off[f + 1] <= i) f++;
-        ts_record(a, tab, i, f);
+        ts_record(a, tab, i, f, ts_load(a, i));
     }
     for (uint32_t f = t; f < a.in.n_funcs; f += n)            /* terminator conditions of the function's blocks */
         for (uint32_t b = a.in.func_blk_off[f]; b < a.in.func_blk_off[f + 1]; b++) ts_block(a, b, f);
 }
 __global__ void __launch_bounds__(256) k_typeseed_check(TsArgs a) {
-    const uint32_t n = gridDim.x * blockDim.x;
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n_val; v += n) ts_check_value(a, v);
+    const uint32_t n = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x, quads = a.n_val / 4;
+    for (uint32_t q = t; q < quads; q += n) {
+        const uint4 m = ((const uint4 *)a.val_masks)[q];
+        if ((m.x | m.y | m.z | m.w) & TS_DEAD)
+            for (uint32_t v = 4 * q; v < 4 * q + 4; v++) ts_check_value(a, v);
+    }
+    for (uint32_t v = quads * 4 + t; v < a.n_val; v += n) ts_check_value(a, v);
 }
 #define TS_OK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { rc = -1; snprintf(msg, sizeof msg, "%s: %s", #x, cudaGetErrorString(e_)); goto done; } } while (0)
 #endif
@@ -446,7 +467,7 @@ done:
     a.val_masks = out->val_masks; a.role = out->role; a.link_mask = out->link_mask; a.link_def = out->link_def; a.status = out->status; a.bad = &bad;
     for (uint32_t v = 0; v < a.n_val; v++) a.val_masks[v] = a.in.val_alive[v] ? TS_TOP3 : (TS_DEAD | TS_TOP3);
     for (uint32_t f = 0; f < F; f++) a.status[f] = CL_ST_OK;
-    for (uint32_t i = 0; i < a.n_inst; i++) ts_record(a, h_tab, i, ts_func_of(rec_off, F, i));
+    for (uint32_t i = 0; i < a.n_inst; i++) ts_record(a, h_tab, i, ts_func_of(rec_off, F, i), ts_load(a, i));
     for (uint32_t f = 0; f < F; f++)
         for (uint32_t b = a.in.func_blk_off[f]; b < a.in.func_blk_off[f + 1]; b++) ts_block(a, b, f);
     for (uint32_t v = 0; v < a.n_val; v++) ts_check_value(a, v);
