@@ -231,16 +231,23 @@ template <bool EXT> TS_D void ts_slots(const TsArgs &a, const TsRow *tab, uint32
 #define TS_TAG(s) (EXT ? (uint32_t)r.xt[s] : (uint32_t)r.tag8[s])
 #define TS_PAY(s) (EXT ? r.xp[s] : r.pay8[s])
 
-    /* operand-dependent parts of the signature, for every record alike (no branch on the opcode): is a use a value,
-     * width of the first ConstMem use (MOV, typerec.py:135-139), widest Reg / UReg def (loads, :176-181)          */
-    bool any_value = false, seen = false; uint32_t cmw = 1, regw = 1;
-    TS_FOR_SLOTS(s) {
-        const uint32_t t = TS_TAG(s), kd = CL_T_KIND(t);
-        const bool is_use = s >= u0 && s < total, is_def = s >= d0 && s < a0;
-        any_value |= is_use && kd == CL_K_VALUE;
-        if (is_use && kd == CL_K_CONSTMEM && !seen) { cmw = CL_T_WIDTH(t); seen = true; }
-        const uint32_t w = TS_PAY(s) >> 16;
-        if (is_def && (kd == CL_K_REG || kd == CL_K_UREG) && w > regw) regw = w;
+    /* operand-dependent parts of the signature: is a use of a MOV a value, width of its first ConstMem use
+     * (typerec.py:135-139); widest Reg / UReg def of a load (:176-181).  Two short loops that only the lanes holding a
+     * MOV / a load run (one loop over all slots for every record cost 17 % of the kernel's instructions).          */
+    bool any_value = false; uint32_t cmw = 1, regw = 1;
+    if (kind == CL_SK_MOV) {
+        bool seen = false;
+        TS_FOR_SLOTS(s) {
+            const uint32_t t = TS_TAG(s), kd = CL_T_KIND(t);
+            const bool is_use = s >= u0 && s < total;
+            any_value |= is_use && kd == CL_K_VALUE;
+            if (is_use && kd == CL_K_CONSTMEM && !seen) { cmw = CL_T_WIDTH(t); seen = true; }
+        }
+    } else if (is_load) {
+        TS_FOR_SLOTS(s) {
+            const uint32_t kd = CL_T_KIND(TS_TAG(s)), w = TS_PAY(s) >> 16;
+            if (s >= d0 && s < a0 && (kd == CL_K_REG || kd == CL_K_UREG) && w > regw) regw = w;
+        }
     }
     const uint32_t loadw = ts_load_mask(is_load ? (CL_TH_DEFW(hint) ? CL_TH_DEFW(hint) : regw) : cmw);
     const uint32_t elem = (is_store && !(ot.flags & CL_OT_RED)) ? ts_load_mask(CL_TH_DATAW(hint) ? CL_TH_DATAW(hint) : 1u) : mt.atom_elem;
@@ -280,7 +287,7 @@ template <bool EXT> TS_D void ts_slots(const TsArgs &a, const TsRow *tab, uint32
             if (ref == CL_NO_VALUE) continue;
         }
         if (c == TS_LINK) {
-            if (is_use) link_mask |= 1u << (k < 15u ? k : 15u); else link_def = p;
+            if (is_use) link_mask |= 1u << (EXT ? (k < 15u ? k : 15u) : k); else link_def = p;
         } else if (c) ts_narrow(a, f, v0, nv, ref, c, !is_use && s >= d0);
     }
     a.role[i] = (uint8_t)sig.role; a.link_mask[i] = (uint16_t)link_mask; a.link_def[i] = link_def;
