@@ -172,7 +172,7 @@ TS_D void ts_narrow(const TsArgs &a, uint32_t f, uint32_t v0, uint32_t nv, uint3
  * TS_LINK, or a sentinel naming a per-record parameter (element type of the modifier tuple, load width ...).   */
 enum { TS_ROW_IMAD_WIDE = CL_SK__COUNT, TS_ROW_LEA_HI, TS_ROW_BITCAST_F2I, TS_ROW_BITCAST_I2F, TS_ROW_MOV_LINK, TS_ROWS };
 enum { TS_P_F16 = 0xE1, TS_P_MMA, TS_P_CONVF, TS_P_CONVI, TS_P_F2FD, TS_P_F2FS, TS_P_ATOM, TS_P_LOADW, TS_P_ELEM, TS_P_ACCW };
-struct TsRow { uint16_t def[2]; uint16_t use[8]; uint16_t role, pad; };      /* def: k = 0, k >= 1; use: k = 0..6, k >= 7 */
+struct TsRow { uint16_t cell[10]; uint16_t role, pad; };      /* cell[0..1]: defs k = 0, k >= 1; cell[2..9]: uses k = 0..6, k >= 7 */
 
 static void ts_build_table(TsRow *tab) {
     cl_modtype mt; mt.f16_elem = TS_P_F16; mt.mma_elem = TS_P_MMA; mt.conv_float = TS_P_CONVF; mt.conv_int = TS_P_CONVI;
@@ -189,8 +189,8 @@ static void ts_build_table(TsRow *tab) {
         case TS_ROW_MOV_LINK: kind = CL_SK_MOV; movlink = TS_LINK; loadw = TS_LINK; break;
         default: break;
         }
-        for (uint32_t k = 0; k < 2; k++) tab[row].def[k] = (uint16_t)ts_def_c(kind, k, m, loadw, TS_P_ACCW);
-        for (uint32_t k = 0; k < 8; k++) tab[row].use[k] = (uint16_t)ts_use_c(kind, k, 255, ot, m, movlink, TS_P_ELEM, TS_P_ACCW, 0);
+        for (uint32_t k = 0; k < 2; k++) tab[row].cell[k] = (uint16_t)ts_def_c(kind, k, m, loadw, TS_P_ACCW);
+        for (uint32_t k = 0; k < 8; k++) tab[row].cell[2 + k] = (uint16_t)ts_use_c(kind, k, 255, ot, m, movlink, TS_P_ELEM, TS_P_ACCW, 0);
         uint32_t role = CL_ROLE_SEED;
         switch (kind) {
         case CL_SK_LOP: case CL_SK_SHF: case CL_SK_SHLR: case CL_SK_SEL: case CL_SK_SELECT: case CL_SK_PHI: case CL_SK_SHUFFLE:
@@ -274,7 +274,7 @@ template <bool EXT> TS_D void ts_slots(const TsArgs &a, const TsRow *tab, uint32
         if (!is_use && is_memref) continue;                               /* defs, aux defs and the guard: values only */
         const uint32_t k = is_use ? s - u0 : s - d0;
         /* the constraint: Bool for the guard (:334) and the aux defs (:323-325), else the table cell */
-        uint32_t c = is_use ? sig.use[k < 7u ? k : 7u] : sig.def[k ? 1u : 0u];
+        uint32_t c = sig.cell[is_use ? 2u + (EXT ? (k < 7u ? k : 7u) : k) : (k ? 1u : 0u)];
         if (is_use && is_tensor) c = k < n_ab ? (uint32_t)TS_P_MMA : k < n_abc ? (uint32_t)TS_P_ACCW : 0u;
         c = ts_cell(c, p0, p1);
         if (is_use && memop && is_memref) c = addr;
