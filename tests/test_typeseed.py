@@ -221,3 +221,17 @@ def test_sharded_over_two_engines_equals_one():
     states = typerec.seed_types_batch(fns, engines=[helpers.oracle_engine(), helpers.oracle_engine()])
     for st, exp in zip(states, fix["expect"]):
         assert st.seed_mask == exp["seed_mask"] and st.link_exprs == exp["link_exprs"] and st.roles == exp["roles"]
+
+
+def test_bench_leg_shape_on_the_oracle_engine(monkeypatch):
+    """bench.py's type-seeding leg end to end on the CPU oracle (small corpus): keys of the object, chained source,
+    equality with the separate oracle pass."""
+    import sys
+    monkeypatch.setattr(sys, "argv", ["bench.py"])
+    sys.path.insert(0, str(ROOT))
+    import bench
+    leg = bench.typeseed_leg(helpers.oracle_engine(), 6538.6, 1, 2, 1, True, n_sass=60_000)
+    assert leg["config"] == "typeseed" and leg["equal_to_oracle"] is True
+    assert leg["roofline"]["bound"] == "hbm" and leg["roofline"]["algorithmic_bytes_per_launch"] > 0
+    assert leg["cpu_baseline"]["kind"] == "port" and leg["e2e"]["d2h_bytes_per_step"] > 0
+    assert leg["narrowed_values"] > 0 and leg["transparent_records"] > 0
