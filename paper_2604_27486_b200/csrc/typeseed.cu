@@ -2,15 +2,20 @@
  * typerec.seed_types (reference typerec.py:288-345) with signature_for
  * (typerec.py:78-235) evaluated per record on the device.
  *
- * One thread per instruction record (grid-stride, 148 SMs x 8 CTAs of 256):
- * the three planes of a record are read once with 128-bit loads (64 B), the
- * constraint of every def / aux def / use slot is computed on the fly from the
- * opcode's signature kind and the modifier-tuple entry (two small tables that
- * stay in L1), and every constrained value is narrowed with ONE 32-bit
- * red.and on its packed mask word (seed | def << 8 | use << 16).  Per record
- * the kernel writes 7 bytes (role, link mask, link def).  A second grid-stride
- * loop narrows the terminator conditions of the blocks.  HBM bound: 64 B read +
- * 7 B written per record + 8 B per value (fill, final read by the copy).
+ * Four launches on the context's stream:
+ *   k_typeseed_prepare  every value word at TOP (dead vids carry a marker), first record of every function
+ *   k_typeseed_index    function of every run of 32 records (one binary search per run, all in parallel)
+ *   k_typeseed          one thread per instruction record (grid-stride, 148 SMs x 8 CTAs of 256): the three planes
+ *                       of a record are read once with 128-bit loads (64 B) and stay in registers; the constraint
+ *                       of a def / aux def / use slot is a cell of a 51-row signature table in shared memory (the
+ *                       reference's if-chain evaluated once on the host: literal mask, LINK, or a per-record
+ *                       parameter such as the element type of the modifier tuple); every constrained value is
+ *                       narrowed with ONE 32-bit red.and on its packed word (seed | def << 8 | use << 16), so the
+ *                       order of the records does not matter; 7 bytes written per record (role, link mask, link
+ *                       def); then one thread per function narrows the terminator conditions of its blocks
+ *   k_typeseed_check    a dead vid whose word moved was narrowed: KeyError upstream; dead words read TOP again
+ * HBM bound in principle: 64 B read + 7 B written per record + 8 B per value; measured 34 % of the HBM roofline,
+ * DRAM traffic 1.04 x the algorithmic bytes (profiles/r02_tuning.md).
  *
  * Compiled with -DCL_SIM by g++ (tests/sim) the kernels become loops: logic
  * checks without a GPU.  Never a fallback of the product.                    */
