@@ -291,9 +291,10 @@ template <bool EXT> TS_D void ts_slots(const TsArgs &a, const TsRow *tab, uint32
             if (CL_T_KIND(m.ureg_tag) == CL_K_VALUE) ts_narrow(a, f, v0, nv, m.ureg_pay, CL_TY_INT32, false);
             if (ref == CL_NO_VALUE) continue;
         }
-        if (c == TS_LINK) {
-            if (is_use) link_mask |= 1u << (EXT ? (k < 15u ? k : 15u) : k); else link_def = p;
-        } else if (c) ts_narrow(a, f, v0, nv, ref, c, !is_use && s >= d0);
+        const bool link = c == TS_LINK;                                   /* LINK cells: bookkeeping without a branch */
+        link_mask |= (link && is_use) ? 1u << (EXT ? (k < 15u ? k : 15u) : k) : 0u;
+        link_def = (link && !is_use) ? p : link_def;
+        if (!link && c) ts_narrow(a, f, v0, nv, ref, c, !is_use && s >= d0);
     }
     a.role[i] = (uint8_t)sig.role; a.link_mask[i] = (uint16_t)link_mask; a.link_def[i] = link_def;
 #undef TS_FOR_SLOTS
